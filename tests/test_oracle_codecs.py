@@ -1,0 +1,187 @@
+"""Pins of the oracle's quantizers: K-means (Alg. 5) and the
+JPEG-style DCT codec, against the JPEG standard's printed table
+(tests/golden), libjpeg's quality scaling (PIL), scipy's real orthonormal DCT,
+brute-force 1-D clustering and the Lloyd fixed-point property."""
+import io
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.fft
+
+import oracle
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ------------------------------------------------------------------ K-means
+def test_kmeans_spec_example():
+    """v = [0,0,1,1,10], K = 2 -> centres {0.5, 10}; decode
+    [0.5,0.5,0.5,0.5,10] (the 1-D optimal 2-partition, reached from quantile init)."""
+    cen, lab = oracle.kmeans_encode([0, 0, 1, 1, 10], 2, 10)
+    assert sorted(cen.tolist()) == [0.5, 10.0]
+    assert oracle.kmeans_decode(cen, lab).tolist() == [0.5, 0.5, 0.5, 0.5, 10.0]
+
+
+def test_kmeans_single_cluster_is_mean():
+    rng = np.random.default_rng(0)
+    v = rng.standard_normal(1001).astype(np.float32)
+    cen, lab = oracle.kmeans_encode(v, 1, 3)
+    assert cen[0] == np.float32(np.mean(v.astype(np.float64)))
+    assert not np.any(lab)
+
+
+def test_kmeans_quantile_init_is_order_statistic():
+    rng = np.random.default_rng(1)
+    v = rng.random(777).astype(np.float32)
+    K = 7
+    cen, _ = oracle.kmeans_encode(v, K, 0)
+    s = np.sort(v)
+    assert np.array_equal(cen, s[[(2 * k + 1) * v.size // (2 * K) for k in range(K)]])
+
+
+def test_kmeans_lloyd_fixed_point():
+    """After Lloyd converges, every centre is the (fp32-rounded) mean of its cell and
+    every element is assigned to a nearest centre."""
+    rng = np.random.default_rng(2)
+    v = np.concatenate([rng.normal(m, 0.05, 400) for m in (0.0, 0.3, 0.9, 1.7)]).astype(np.float32)
+    cen, lab = oracle.kmeans_encode(v, 4, 200)
+    for k in range(4):
+        cell = v[lab == k]
+        assert cell.size > 0
+        assert cen[k] == np.float32(cell.astype(np.float64).mean())
+    dist = np.abs(v[:, None].astype(np.float64) - cen[None, :].astype(np.float64))
+    assert np.all(dist[np.arange(v.size), lab] <= dist.min(axis=1) + 1e-7)
+
+
+def _brute_opt(v, K):
+    s = np.sort(v.astype(np.float64))
+    best = np.inf
+    for cuts in itertools.combinations(range(1, len(s)), K - 1):
+        parts = np.split(s, cuts)
+        best = min(best, sum(((p - p.mean()) ** 2).sum() for p in parts))
+    return best
+
+
+def test_kmeans_vs_bruteforce_optimum():
+    """1-D optimal clusters are contiguous in sorted order: brute force over all cut
+    sets gives the optimum distortion.  Lloyd never beats it, and on well-separated
+    data it reaches it."""
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        v = rng.integers(0, 10, rng.integers(4, 11)).astype(np.float32)
+        for K in (1, 2, 3):
+            cen, lab = oracle.kmeans_encode(v, K, 50)
+            dist = float(((v.astype(np.float64) - cen[lab].astype(np.float64)) ** 2).sum())
+            assert dist >= _brute_opt(v, K) - 1e-9
+    v = np.array([0, 0.1, 0.05, 5, 5.1, 9.9, 10], np.float32)
+    cen, lab = oracle.kmeans_encode(v, 3, 20)
+    dist = float(((v.astype(np.float64) - cen[lab].astype(np.float64)) ** 2).sum())
+    assert abs(dist - _brute_opt(v, 3)) < 1e-6
+
+
+def test_kmeans_exact_when_levels_equal_k():
+    v = np.repeat(np.array([0.25, 1.5, 2.0, 7.0], np.float32), 50)
+    np.random.default_rng(4).shuffle(v)
+    cen, lab = oracle.kmeans_encode(v, 4, 10)
+    assert np.array_equal(oracle.kmeans_decode(cen, lab), v)
+
+
+def test_kmeans_bits_per_element_matches_paper():
+    """K = 16 -> 4 bits, K = 3 -> 2 bits, K = 32 -> 5 bits."""
+    g = json.load(open(os.path.join(GOLD, "paper_values.json")))["kmeans_bits"]
+    for K, bits in g["K_bits"]:
+        assert int(np.ceil(np.log2(K))) == bits
+
+
+# ------------------------------------------------------------------ DCT
+def _annex_k():
+    rows = [l.split() for l in open(os.path.join(GOLD, "jpeg_luminance_annex_k.txt"))
+            if l.strip() and not l.startswith("#")]
+    return np.array(rows, dtype=np.int32)
+
+
+def test_dct_table_q50_is_annex_k():
+    assert np.array_equal(oracle.dct_qtable(50), _annex_k())
+
+
+def test_dct_tables_match_libjpeg_all_qualities():
+    """IJG quality scaling reproduces libjpeg's luminance table for q = 1..100 (PIL)."""
+    from PIL import Image
+    img = Image.fromarray((np.random.default_rng(0).random((16, 16)) * 255).astype(np.uint8))
+    for q in range(1, 101):
+        b = io.BytesIO()
+        img.save(b, "JPEG", quality=q)
+        b.seek(0)
+        ref = np.array(list(Image.open(b).quantization[0]), np.int32).reshape(8, 8)
+        assert np.array_equal(oracle.dct_qtable(q), ref), q
+    assert np.all(oracle.dct_qtable(100) == 1)
+
+
+def _blocks(a):
+    r, c = a.shape
+    return a.reshape(r // 8, 8, c // 8, 8).transpose(0, 2, 1, 3).reshape(-1, 8, 8)
+
+
+def test_integer_dct_close_to_orthonormal_dct():
+    """With Q = 1 (q = 100) the coefficient is round(Y / 2^18) and Y / 2^18 is the
+    integer approximation of the orthonormal 2-D DCT F of the level-shifted block:
+    |coef - F| <= 0.5 + 0.2, and coef == round(F) for >= 99.9% of coefficients."""
+    rng = np.random.default_rng(5)
+    v = rng.random((64, 64)).astype(np.float32)
+    v[0, 0], v[1, 1] = 0.0, 1.0  # min 0, max 1 -> p = rint(255 v)
+    coef, mm = oracle.dct_encode(v, 100)
+    p = np.clip(np.rint((v.astype(np.float64) - mm[0]) * 255.0 / (float(mm[1]) - mm[0])), 0, 255)
+    F = np.stack([scipy.fft.dctn(b - 128.0, norm="ortho") for b in _blocks(p)])
+    cf = coef.reshape(-1, 8, 8).astype(np.float64)
+    assert np.max(np.abs(cf - F)) <= 0.7
+    # the 4 guard bits kept between the passes round each 1-D coefficient to 1/16
+    # (error std ~0.018), so on uniform-noise blocks ~2% of coefficients land across
+    # a rounding boundary; a transposed / mis-scaled matrix would break both bounds
+    assert np.mean(cf == np.round(F)) >= 0.97
+
+
+def test_dct_decode_close_to_real_idct():
+    """Decoded 8-bit samples equal clip(round(IDCT(coef Q)) + 128) for >= 99.5% of
+    pixels and never differ by more than 1."""
+    rng = np.random.default_rng(6)
+    v = (rng.random((32, 48)) + np.linspace(0, 3, 48)[None, :]).astype(np.float32)
+    for q in (25, 50, 75, 95):
+        coef, mm = oracle.dct_encode(v, q)
+        _, smp = oracle.dct_decode(coef, mm, 32, 48, q, return_samples=True)
+        Q = oracle.dct_qtable(q).astype(np.float64)
+        G = coef.reshape(-1, 8, 8) * Q
+        ref = np.clip(np.round(np.stack([scipy.fft.idctn(g, norm="ortho") for g in G]) + 128), 0, 255)
+        got = _blocks(smp.astype(np.float64))
+        assert np.max(np.abs(got - ref)) <= 1
+        assert np.mean(got == ref) >= 0.98
+
+
+def test_dct_constant_vector_exact():
+    v = np.full((16, 24), 3.25, np.float32)
+    coef, mm = oracle.dct_encode(v, 50)
+    assert not np.any(coef) and mm.tolist() == [3.25, 3.25]
+    assert np.array_equal(oracle.dct_decode(coef, mm, 16, 24, 50), v)
+
+
+def test_dct_roundtrip_quality100_ramp():
+    """q = 100 on a smooth ramp -> round-trip RMSE <= 1% of the range."""
+    v = np.add.outer(np.linspace(0, 1, 64), np.linspace(0, 2, 64)).astype(np.float32)
+    coef, mm = oracle.dct_encode(v, 100)
+    out = oracle.dct_decode(coef, mm, 64, 64, 100)
+    assert np.sqrt(np.mean((out - v) ** 2)) <= 0.01 * (v.max() - v.min())
+    # endpoints of the 8-bit map are exact
+    assert out.min() >= mm[0] - 1e-6 and out.max() <= mm[1] + 1e-6
+
+
+def test_dct_error_shrinks_with_quality():
+    rng = np.random.default_rng(7)
+    v = (np.add.outer(np.sin(np.arange(64) / 5), np.cos(np.arange(64) / 7)) +
+         0.05 * rng.standard_normal((64, 64))).astype(np.float32)
+    errs = []
+    for q in (10, 30, 50, 75, 95):
+        coef, mm = oracle.dct_encode(v, q)
+        errs.append(np.sqrt(np.mean((oracle.dct_decode(coef, mm, 64, 64, q) - v) ** 2)))
+    assert all(a > b for a, b in zip(errs, errs[1:]))
