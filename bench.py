@@ -1,0 +1,307 @@
+"""Benchmark of the hot path: decentralized quantized ADMM iterations (Alg. 4
+with K-means quantized exchange) on BASELINE.json config 4 (weak scaling: 8 ADMM
+nodes per GPU, 1024^2 image, 90 angles per GPU, random 4-regular graph, CG5, K=64).
+
+One "step" = one ADMM iteration of every node: E1+1 forward/back projector pairs
+(CG), the K-means encode of every node's iterate, the exchange (NCCL send/recv of
+payloads along cross-GPU edges), decode and the dual/rhs update.
+
+python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ADMM iterations/s and projector Gvoxel-updates/s vs HBM roofline, 1/2/4/8 GPU"
+UNIT = "GVU/s"
+LSU_VU_PER_CLK_SM = 16  # 2 fp32 taps per VU through a 128 B/clk/SM L1/smem path
+
+
+def env_int(k, d):
+    return int(os.environ.get(k, d))
+
+
+def peaks():
+    p = {"hbm_gbs": None, "sm_max_mhz": None, "src": "fallback"}
+    try:
+        m = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        p.update(hbm_gbs=m["hbm_gbs"], sm_max_mhz=m["sm_max_mhz"], src="measured")
+    except Exception:
+        p.update(hbm_gbs=6650.0, sm_max_mhz=1965.0)
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.proc, self.out = device, None, ""
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def vu_per_iter(cfg):
+    """voxel-updates per ADMM iteration over all nodes: (E1+1) A/A^T pairs (CG), each
+    N^2 x (angles of the node) VU; summed over nodes = N^2 x n_angles."""
+    apps = (cfg.e1 + 1) if cfg.inner == 1 else cfg.e1
+    return 2 * apps * cfg.N * cfg.N * cfg.n_angles * cfg.slices
+
+
+def cpu_baseline(cfg_g1, iters=2):
+    """The fp64 oracle as it stands, on the host cores, on a bounded sample: `iters`
+    ADMM iterations of the per-GPU share of the workload (config 4 at G = 1)."""
+    import oracle
+    from paper_2410_06106_b200 import configs as C
+    from tests.cases import oracle_case
+    inp = C.make_inputs(cfg_g1, with_truth=False)
+    threads = min(cfg_g1.nodes, os.cpu_count() or 1)
+    o = oracle_case(cfg_g1, inp, threads=threads)
+    t0 = time.perf_counter()
+    o.run(iters)
+    dt = time.perf_counter() - t0
+    return {"value": vu_per_iter(cfg_g1) * iters / dt / 1e9, "unit": UNIT, "cores": threads,
+            "kind": "oracle", "sample": f"{iters} ADMM iterations of {cfg_g1.name} (8 nodes, 1024^2, "
+                                        f"K-means 64), OpenMP over nodes", "seconds": round(dt, 2)}
+
+
+def run_reference(args):
+    """--impl reference: the oracle, rank 0 only."""
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return
+    from paper_2410_06106_b200 import configs as C
+    from tests.cases import oracle_case
+    cfg = C.C4(1)
+    inp = C.make_inputs(cfg, with_truth=False)
+    threads = min(cfg.nodes, os.cpu_count() or 1)
+    o = oracle_case(cfg, inp, threads=threads)
+    o.run(args.warmup)
+    t0 = time.perf_counter()
+    o.run(args.steps)
+    dt = time.perf_counter() - t0
+    value = vu_per_iter(cfg) * args.steps / dt / 1e9
+    sample = (f"each step = 1 ADMM iteration of {cfg.name} (the per-GPU share of config 4: 8 nodes, "
+              f"1024^2, 90 angles, CG5, K-means 64) on the fp64 CPU oracle")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / max(1, args.steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": cfg.name, "N": cfg.N, "nodes": cfg.nodes,
+                                        "n_angles": cfg.n_angles, "quantizer": "kmeans64"},
+        "admm_iters_per_s": args.steps / dt,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", type=int, default=0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_06106_b200 import configs as C
+    from paper_2410_06106_b200 import tomoq
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    assert args.warmup >= 3, "contract: W >= 3"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = C.C4(world)
+    inp = C.make_inputs(cfg, with_truth=False)
+    nid = None
+    if world > 1:
+        obj = [tomoq.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    ctx = tomoq.Context(cfg.N, cfg.n_angles, cfg.n_det, cfg.nodes, inp.edges, split=cfg.split,
+                        rule=cfg.rule, rank=rank, world=world, nccl_id=nid, precision=args.precision,
+                        device=local)
+    ctx.set_params(cfg.rho, inner=cfg.inner, e1=cfg.e1)
+    ctx.set_quantizer(cfg.quant, k=cfg.k, lloyd=cfg.lloyd)
+    sino_host = torch.from_numpy(inp.sino[0]).pin_memory()
+    ctx.set_sinogram(0, sino_host)
+    stream = torch.cuda.Stream(device=dev)  # a real stream (the legacy default stream has handle 0)
+    torch.cuda.set_stream(stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up (also captures the CUDA graph of one iteration)
+    ctx.run(args.warmup, stream)
+    barrier()
+    # ---- timed region: exactly K steps (ADMM iterations)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ctx.run(args.steps, stream)
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    st = ctx.stats()
+    vu_it = vu_per_iter(cfg)
+    value = vu_it * args.steps / (ms / 1e3) / 1e9
+    iters_per_s = args.steps / (ms / 1e3)
+
+    # ---- end to end through the public API with host buffers: per step, H2D of the
+    # slice sinogram from pinned memory, one iteration, D2H of a node's image
+    img_host = torch.empty(cfg.N * cfg.N, dtype=torch.float32).pin_memory()
+    my_node = rank  # node `rank` lives on this rank (interleaved map)
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e2.record(stream)
+    for _ in range(args.steps):
+        ctx.set_sinogram(0, sino_host)
+        ctx.run(1, stream)
+        ctx.image(0, my_node, host_out=img_host)
+    e3.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(e2.elapsed_time(e3))
+    e2e_wall = max_over_ranks((time.perf_counter() - t0) * 1e3)
+    e2e_value = vu_it * args.steps / (max(e2e_ms, e2e_wall) / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel (timed alone, CUDA events on this stream)
+    pk = peaks()
+    comp_ms, comp_units = {}, {}
+    reps = 20
+    for comp in (0, 1):
+        ctx.launch_component(comp, 3, stream)
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        comp_units[comp] = ctx.launch_component(comp, reps, stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        comp_ms[comp] = a.elapsed_time(b) / reps
+    apps = cfg.e1 + 1
+    share = {c: comp_ms[c] * apps / (ms / args.steps) for c in comp_ms}
+    dom = max(comp_ms, key=lambda c: comp_ms[c])
+    names = {0: "fp_kernel (forward projector A p)", 1: "bp_kernel<CGQ> (A^T s + c p, fused p.q)"}
+    achieved = comp_units[dom] / (comp_ms[dom] / 1e3) / 1e9
+    peak_vu = LSU_VU_PER_CLK_SM * 148 * pk["sm_max_mhz"] * 1e6 / 1e9
+    n_local = st["local_nodes"]
+    compulsory = 4.0 * n_local * cfg.N ** 2 + 8.0 * (comp_units[dom] / cfg.N ** 2) * cfg.n_det
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = prof.get({0: "fp_kernel", 1: "bp_kernel"}[dom])
+    except Exception:
+        pass
+    roofline = {
+        "bound": "alu", "kernel": names[dom], "achieved": achieved, "peak": peak_vu, "unit": "GVU/s",
+        "frac": achieved / peak_vu, "traffic": traffic,
+        "peak_basis": f"LSU/L1 data path: {LSU_VU_PER_CLK_SM} VU/clk/SM x 148 SMs x {pk['sm_max_mhz']} MHz "
+                      f"({pk['src']}); see DESIGN.md",
+        "hbm_compulsory_gbs": compulsory / (comp_ms[dom] / 1e3) / 1e9, "hbm_peak_gbs": pk["hbm_gbs"],
+        "share_of_step": share[dom],
+        "components_ms": {"fp": comp_ms[0], "bp_cgq": comp_ms[1]},
+    }
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(C.C4(1))
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == 0 else "f64",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "N": cfg.N, "nodes": cfg.nodes, "nodes_per_gpu": cfg.nodes // world,
+                       "n_angles": cfg.n_angles, "n_det": cfg.n_det, "graph": "random 4-regular",
+                       "inner": "CG5", "quantizer": "kmeans K=64 (10 Lloyd)", "rule": "graph",
+                       "parallelism": f"nodes interleaved over {world} GPU(s), NCCL send/recv of payloads",
+                       "l2": "no flush: per-GPU working set ~0.2 GB > 126 MB L2"},
+            "admm_iters_per_s": iters_per_s,
+            "vu_per_step": vu_it,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(sino_host.numel() * 4),
+                    "d2h_bytes_per_step": int(cfg.N * cfg.N * 4), "ms_per_step": max(e2e_ms, e2e_wall) / args.steps},
+            "gpu_launches": int(st["kernel_launches"]),
+            "clocks": clk,
+            "payload_bytes_per_step": st["payload_bytes_logical"],
+            "nccl_bytes_per_step_rank0": st["nccl_bytes_sent"],
+        }
+        print(json.dumps(out), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

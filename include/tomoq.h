@@ -1,0 +1,197 @@
+/*
+ * tomoq.h -- C-ABI of libtomoq.so, the B200 (sm_100a) hot path of decentralized
+ * quantized ADMM for parallel-beam tomography (arXiv 2410.06106, "PAPER.md").
+ *
+ * Citations: "P:n" = PAPER.md line n.  "R-k" = a reading of the paper listed in
+ * DESIGN.md ("Readings").  The library never aborts: every call returns a
+ * tq_status; on failure tq_last_error() (per context) / tq_last_error_global()
+ * (for calls without a context) return a one-line message.  Not thread-safe per
+ * context.  The caller owns every pointer it passes; the library copies what it
+ * keeps and owns all device state it allocates until tq_destroy().
+ *
+ * Geometry (R-1..R-3): image N x N, row-major, row 0 on top, pixel centres
+ * x_c = c-(N-1)/2, y_r = (N-1)/2-r; angles theta_a = pi a / n_angles;
+ * bins t_j = j-(n_det-1)/2, unit spacing; n_det >= ceil(N sqrt 2) so every ray
+ * through the grid is measured.  A sinogram is [angle][bin] row-major.
+ * The system matrix P of P:47-77 is Joseph's: P[(a,j),p] = max(0, 1-|t_j-t_p|/m_a)/m_a,
+ * t_p = x_c cos + y_r sin, m_a = max(|cos|,|sin|) with the major axis chosen by
+ * the integer rule 4a in [n_angles, 3 n_angles] -> x-major.
+ *
+ * Precision: 0 = fp32 storage/arithmetic with fp64 dots and epilogues (production);
+ * 1 = fp64 everywhere (verification mode, same kernels instantiated for double).
+ * Quantizers always see the fp32-rounded iterate (the wire format, R-16/R-18).
+ */
+#ifndef TOMOQ_H
+#define TOMOQ_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TQ_OK = 0,
+    TQ_EINVAL = 1,     /* bad argument / geometry / graph */
+    TQ_ENOMEM = 2,     /* device or host allocation failed */
+    TQ_ECUDA = 3,      /* CUDA runtime error (message has the CUDA string) */
+    TQ_ENCCL = 4,      /* NCCL missing or failed */
+    TQ_EDIVERGED = 5,  /* some node's ||x||_2 exceeded 1e12 (SPEC "divergence guard") */
+    TQ_ESTATE = 6      /* call out of order (e.g. tq_run before tq_set_sinogram) */
+} tq_status;
+
+typedef struct tq_ctx tq_ctx;
+
+typedef struct {
+    int32_t image_side;  /* N, multiple of 8, >= 8 */
+    int32_t n_angles;    /* angles evenly spaced in [0, pi) */
+    int32_t n_det;       /* detector bins, >= ceil(N sqrt 2) */
+} tq_geometry;
+
+enum { TQ_SPLIT_ROUND_ROBIN = 0, TQ_SPLIT_CONTIGUOUS = 1 };
+enum { TQ_RULE_GRAPH = 0, TQ_RULE_PAPER = 1 };
+enum { TQ_INNER_GD = 0, TQ_INNER_CG = 1 };
+enum { TQ_Q_NONE = 0, TQ_Q_KMEANS = 1, TQ_Q_DCT = 2, TQ_Q_ALTERNATE = 3 };
+
+/* The communication graph of ONE slice (every slice uses the same graph).
+ * rule TQ_RULE_GRAPH: decentralized consensus ADMM over the edges (R-7, default).
+ * rule TQ_RULE_PAPER: the segment-owner dADMM of P:158-166 (edges unused; every
+ * node needs every segment -- an all-gather). */
+typedef struct {
+    int32_t n_nodes;          /* M ADMM nodes per slice, 1 <= M <= n_angles */
+    int32_t n_edges;
+    const int32_t *edges;     /* 2*n_edges node ids, undirected, no self loops / duplicates */
+    int32_t angle_split;      /* TQ_SPLIT_* (P:319-320 round-robin; R-5 contiguous) */
+    const int32_t *node_rank; /* [n_nodes] rank owning node i (all slices); NULL => i mod world */
+    int32_t rule;             /* TQ_RULE_* */
+} tq_graph;
+
+typedef struct {
+    double rho;            /* penalty rho > 0 */
+    int32_t inner;         /* TQ_INNER_GD (Alg. 2) or TQ_INNER_CG (R-8) */
+    int32_t e1;            /* inner steps E1 >= 0 */
+    const double *eta1;    /* [n_nodes] GD step per node, or NULL => 1/(2 a_i N + c_i) (R-8) */
+    int32_t e2;            /* Alg. 3 steps (paper rule) */
+    double eta2;           /* Alg. 3 step, 0 < eta2 rho < 2 */
+} tq_params;
+
+typedef struct {
+    int32_t kind;         /* TQ_Q_*; ALTERNATE = K-means on even slices, DCT on odd (R-20) */
+    int32_t k;            /* K-means clusters, 1..256 (Alg. 5) */
+    int32_t lloyd_iters;  /* Lloyd iterations after the quantile init (R-16) */
+    int32_t quality;      /* DCT quality 1..100, IJG scaling of the Annex K table (R-18) */
+    int32_t keep_labels;  /* 1: keep the last K-means labels for tq_export_labels (parity) */
+} tq_quant;
+
+typedef struct {
+    int64_t iters;                 /* ADMM iterations run so far */
+    int32_t local_nodes;           /* (slice, node) pairs on this rank */
+    int32_t world;
+    int64_t payload_bytes_logical; /* last iteration: sum over local nodes of bytes each
+                                      node sent (graph: deg x payload; paper: (M-1) x segment) */
+    int64_t nccl_bytes_sent;       /* last iteration, this rank, over NCCL */
+    int64_t nccl_bytes_recv;
+    int64_t kernel_launches;       /* kernels launched by the last tq_run (all iterations) */
+    double ms_last_run;            /* device time of the last tq_run (CUDA events) */
+} tq_stats;
+
+/* ---------------------------------------------------------------- context API */
+tq_status tq_nccl_unique_id(uint8_t id[128]);
+
+/* One context per process/rank, owning every (slice, node) mapped to this rank.
+ * nccl_id: from rank 0's tq_nccl_unique_id (broadcast by the caller), NULL if world == 1.
+ * device: CUDA device ordinal to use. */
+tq_status tq_create(const tq_geometry *geom, const tq_graph *graph, int32_t n_slices,
+                    int32_t rank, int32_t world, const uint8_t *nccl_id, int32_t precision,
+                    int32_t device, tq_ctx **out);
+tq_status tq_set_params(tq_ctx *ctx, const tq_params *p);
+tq_status tq_set_quantizer(tq_ctx *ctx, const tq_quant *q);
+
+/* Sinogram of one slice.  node >= 0: that node's shard ([a_node][n_det], its angles in
+ * increasing order); node == -1: the full slice sinogram [n_angles][n_det] and the
+ * library keeps the rows of its local nodes.  Ignored for nodes not on this rank.
+ * len is in floats; on_device: d is a device pointer. */
+tq_status tq_set_sinogram(tq_ctx *ctx, int32_t slice, int32_t node, const float *d,
+                          int64_t len, int32_t on_device);
+
+/* Enqueue `iters` ADMM iterations (Alg. 4) on `stream` (NULL = the
+ * context's own stream) and wait for them; returns TQ_EDIVERGED if any node's norm
+ * exceeds 1e12 after the last iteration. */
+tq_status tq_run(tq_ctx *ctx, int32_t iters, void *stream);
+
+/* node >= 0: that node's private iterate (graph) / u_m (paper) -- must be local.
+ * node == -1: graph rule: mean over the slice's nodes of x_i (all must be local, R-22);
+ *             paper rule: the consensus x.  out: N*N floats (host or device). */
+tq_status tq_get_image(tq_ctx *ctx, int32_t slice, int32_t node, float *out, int64_t len,
+                       int32_t on_device);
+
+/* State of one local node as 3*N*N doubles: graph rule [x_i | alpha_i | xhat_i];
+ * paper rule [u_m | lambda_m | x].  Import recomputes the next right-hand side. */
+tq_status tq_export_state(tq_ctx *ctx, int32_t slice, int32_t node, double *buf, int64_t len);
+tq_status tq_import_state(tq_ctx *ctx, int32_t slice, int32_t node, const double *buf, int64_t len);
+/* Pre-quantization labels of the last encode of a local node (K-means only), int32 [N*N]. */
+tq_status tq_export_labels(tq_ctx *ctx, int32_t slice, int32_t node, int32_t *buf, int64_t len);
+
+/* Profiling hook: enqueue `reps` launches of one component of the iteration over all
+ * local nodes on `stream` (no synchronisation), with the context's own buffers, so a
+ * caller can time it with events on that stream.  Components: 0 forward projector
+ * S = A P, 1 backprojector with the CG epilogue Q = A^T S + c P, 2 forward residual
+ * S = D - A X, 3 the K-means encode of the quantized slices, 4 the DCT encode,
+ * 5 the consensus/dual kernel without the dual update (b' only).  Overwrites only
+ * scratch (S, Q, payloads, b' is recomputed identically); x and alpha are unchanged.
+ * Returns TQ_EINVAL for a component the context does not have.  *units = algorithmic
+ * work per launch (voxel-updates for 0-2, elements for 3-5). */
+tq_status tq_launch_component(tq_ctx *ctx, int32_t component, int32_t reps, void *stream,
+                              int64_t *units);
+
+tq_status tq_get_stats(const tq_ctx *ctx, tq_stats *out);
+const char *tq_last_error(const tq_ctx *ctx);
+const char *tq_last_error_global(void);
+void tq_destroy(tq_ctx *ctx);
+
+/* ---------------------------------------------------------------- host-side plans
+ * Pure host functions (no GPU needed). */
+/* Angle partition of P:319-320 / R-5: offsets[n_nodes+1], idx[n_angles]. */
+tq_status tq_partition_angles(int32_t n_angles, int32_t n_nodes, int32_t split,
+                              int32_t *offsets, int32_t *idx);
+/* Exchange plan of `rank` for one iteration: sends = (node, peer) pairs this rank
+ * sends node's payload to; recvs = (node, peer) pairs it receives.  Capacity in
+ * pairs; *n_* returns the counts (TQ_EINVAL if capacity is too small). */
+tq_status tq_exchange_plan(const tq_graph *graph, int32_t rank, int32_t world,
+                           int32_t *sends, int32_t cap_sends, int32_t *n_sends,
+                           int32_t *recvs, int32_t cap_recvs, int32_t *n_recvs);
+/* Payload bytes of one encoded vector of n elements (Q kind for the slice). */
+int64_t tq_payload_bytes(int32_t kind, int32_t k, int64_t n, int32_t precision);
+
+/* ---------------------------------------------------------------- stateless kernels
+ * Device pointers, caller-owned; precision selects float (0) / double (1) elements;
+ * stream NULL = default stream; calls are asynchronous. */
+/* sino[k][j] = (A img)[(sel[k], j)]  (Eq. 2). sel: host array of n_sel angle ids. */
+tq_status tq_project(const tq_geometry *g, const int32_t *sel, int32_t n_sel, const void *img,
+                     void *sino, int32_t precision, void *stream);
+/* img = A^T sino over the selected angles (the transpose of Alg. 2 line 3). */
+tq_status tq_backproject(const tq_geometry *g, const int32_t *sel, int32_t n_sel,
+                         const void *sino, void *img, int32_t precision, void *stream);
+/* One node's inner solve of min 1/2||A x - d||^2 + c/2||x||^2 - b'^T x, E1 GD (eta) or
+ * CG steps, warm start x (in/out).  d: [n_sel][n_det]. Synchronous. */
+tq_status tq_local_solve(const tq_geometry *g, const int32_t *sel, int32_t n_sel,
+                         const void *d, const void *bprime, double c, int32_t inner,
+                         int32_t e1, double eta, void *x, int32_t precision, void *stream);
+/* K-means encode (Alg. 5 made exact, R-16) of n fp32 values: centers[k] fp32,
+ * planes[ceil(n/32) * ceil(log2 k)] uint32 bit-planes (group-major), labels (int32,
+ * optional, may be NULL). */
+tq_status tq_kmeans_encode(const float *v, int64_t n, int32_t k, int32_t iters, float *centers,
+                           uint32_t *planes, int32_t *labels, void *stream);
+tq_status tq_kmeans_decode(const float *centers, const uint32_t *planes, int64_t n, int32_t k,
+                           float *out, void *stream);
+/* DCT codec (R-18) of a rows x cols fp32 array (8 | rows, 8 | cols): coef[rows*cols] int16
+ * in [block][u][v] order, minmax[2] fp32. */
+tq_status tq_dct_encode(const float *v, int32_t rows, int32_t cols, int32_t quality,
+                        int16_t *coef, float *minmax, void *stream);
+tq_status tq_dct_decode(const int16_t *coef, const float *minmax, int32_t rows, int32_t cols,
+                        int32_t quality, float *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOMOQ_H */

@@ -1,0 +1,67 @@
+// codecs.cuh -- the two quantizers Q of PAPER.md:268 (eq-compact:conc3), batched over
+// P payloads of nv fp32 values each.  Inputs, payloads and outputs are addressed
+// through device arrays of pointers (one entry per payload), so a batch can mix local
+// iterates, received payloads and segments of the consensus image.
+//
+// K-means (Alg. 5; exact rules DESIGN.md R-16): quantile init by an
+// exact 4-pass radix select (8-bit digits) of the order statistics, E_q Lloyd passes
+// with deterministic fixed-point integer cluster sums, final assignment, labels
+// packed as ceil(log2 K) bit-planes per 32-element group with warp ballots.
+// Payload: [K fp32 centres][ceil(nv/32) * B uint32 planes, group-major].
+//
+// DCT (R-18): per-payload [min,max], fp64 8-bit map, exact integer two-pass
+// 8x8 DCT, IJG-scaled Annex K table, round half away from zero -> int16.
+// Payload: [min, max fp32][nv int16 coefficients in [block][u][v] order].
+#pragma once
+#include "common.cuh"
+
+namespace tq {
+
+int kmeans_bits(int K);
+long long kmeans_payload_bytes(int K, long long nv);
+long long dct_payload_bytes(long long nv);
+
+struct KmeansWork {
+    int P = 0, K = 0, B = 0;        // payloads, clusters, bits per label
+    long long nv = 0;
+    float *cen = nullptr;           // [P][K]
+    float *thr = nullptr;           // [P][K]
+    uint32_t *prefix = nullptr;     // [P][K+2]
+    uint32_t *rank = nullptr;       // [P][K+2]
+    uint32_t *plist = nullptr;      // [P][K+2]
+    int *np = nullptr;              // [P]
+    uint32_t *hist = nullptr;       // [P][K+2][256]
+    int *fexp = nullptr;            // [P] fixed-point exponent F
+    unsigned long long *acc_sum = nullptr;  // [P][K] int64 two's complement
+    unsigned long long *acc_cnt = nullptr;  // [P][K]
+    unsigned *counter = nullptr;    // [P]
+    void alloc(int P, int K, long long nv);
+    void release();
+};
+
+// vin[b]: nv floats; pay[b]: payload bytes; labels: table of int32[nv] or null table
+int kmeans_encode(const float *const *vin, KmeansWork &ws, int lloyd, uint8_t *const *pay,
+                  int32_t *const *labels, cudaStream_t st);
+// out[b]: nv elements of float (prec 0) or double (prec 1)
+int kmeans_decode(const uint8_t *const *pay, int P, long long nv, int K, int prec,
+                  void *const *out, cudaStream_t st);
+
+struct DctWork {
+    int P = 0;
+    float *minmax = nullptr;       // [P][2]
+    unsigned *counter = nullptr;   // [P]
+    float *partial = nullptr;      // [P][part_stride]
+    int part_stride = 0;
+    void alloc(int P, long long nv);
+    void release();
+};
+int dct_encode(const float *const *vin, int P, int rows, int cols, int quality, DctWork &ws,
+               uint8_t *const *pay, cudaStream_t st);
+int dct_decode(const uint8_t *const *pay, int P, int rows, int cols, int quality, int prec,
+               void *const *out, cudaStream_t st);
+
+// host reference tables (independent of the oracle): Annex K table scaled to quality,
+// and the integer DCT matrix round(2^14 alpha(u) cos((2x+1) u pi / 16))
+void dct_host_tables(int quality, int *C64, int *Q64);
+
+}  // namespace tq

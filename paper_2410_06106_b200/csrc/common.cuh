@@ -1,0 +1,117 @@
+// common.cuh -- internal helpers of libtomoq (sm_100a).  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/tomoq.h"
+
+namespace tq {
+
+struct Error {
+    tq_status code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(tq_status code, const std::string &msg);
+
+#define TQ_CHECK_CUDA(call)                                                              \
+    do {                                                                                 \
+        cudaError_t _e = (call);                                                         \
+        if (_e != cudaSuccess)                                                           \
+            ::tq::fail(TQ_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));    \
+    } while (0)
+
+#define TQ_REQUIRE(cond, msg)                                                            \
+    do {                                                                                 \
+        if (!(cond)) ::tq::fail(TQ_EINVAL, msg);                                         \
+    } while (0)
+
+// ---------------------------------------------------------------- geometry (host)
+// DESIGN.md R-1..R-3: theta_a = pi a / n_ang; x-major iff 4a in [n_ang, 3 n_ang];
+// m_a = |sin| (x-major) or |cos| (y-major).
+struct AngleHost {
+    double cs, sn, m;
+    int xmajor;
+};
+std::vector<AngleHost> make_angles(int n_ang);
+void partition_angles(int n_ang, int M, int split, std::vector<int> &off, std::vector<int> &idx);
+void partition_rows(int N, int M, std::vector<int> &row_off);
+
+// Per-angle record used by the projector kernels (one per (local node, angle)).
+struct RayRow {
+    int node;      // local node index
+    int angle;     // global angle id
+    int k;         // index of the angle within the node
+    int pad;
+};
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Fixed-order block sum (deterministic): warp butterflies then warp 0 over the
+// per-warp results.  All threads of the block must call it.  Result valid in
+// every thread.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double *sh /* >= NT/32 + 1 */) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        double t = (l < NT / 32) ? sh[l] : 0.0;
+        t = warp_sum(t);
+        if (l == 0) sh[NT / 32] = t;
+    }
+    __syncthreads();
+    return sh[NT / 32];
+}
+
+// "Last block finalises": every block of a group writes its partial, then the last
+// block to arrive sums all partials in index order (deterministic) and resets the
+// counter.  Returns true in every thread of the last block.
+__device__ __forceinline__ bool last_block_of_group(unsigned *counter, unsigned nblocks,
+                                                    bool *sh_flag) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned prev = atomicAdd(counter, 1u);
+        *sh_flag = (prev == nblocks - 1);
+        if (*sh_flag) *counter = 0u;
+    }
+    __syncthreads();
+    bool last = *sh_flag;
+    if (last) __threadfence();
+    return last;
+}
+
+// floor for 0 <= x < 2^22 without a conversion instruction: the round-down add
+// puts floor(x) in the mantissa of 2^23 + floor(x).
+__device__ __forceinline__ float floor_pos(float x, int &i) {
+    float m = __fadd_rd(x, 8388608.0f);
+    i = __float_as_int(m) - 0x4B000000;
+    return m - 8388608.0f;
+}
+
+template <typename T>
+struct Vec;  // storage helpers
+template <>
+struct Vec<float> {
+    static constexpr int id = 0;
+};
+template <>
+struct Vec<double> {
+    static constexpr int id = 1;
+};
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace tq

@@ -1,0 +1,144 @@
+// consensus.cu -- see consensus.cuh.
+#include "consensus.cuh"
+
+namespace tq {
+
+namespace {
+constexpr int CT = 256;
+
+inline dim3 grid_of(long long n, int L) {
+    return dim3((unsigned)std::max(1LL, std::min<long long>((n + CT * 4 - 1) / (CT * 4), 65535)), L);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(CT) graph_dual(const T *const *xh, const int *own_slot,
+                                                 const int *nbr_off, const int *nbr_slot, T *alpha,
+                                                 T *bprime, long long n, double rho, int update) {
+    const int i = blockIdx.y;
+    const T *own = xh[own_slot[i]];
+    const int k0 = nbr_off[i], k1 = nbr_off[i + 1];
+    const double deg = (double)(k1 - k0);
+    T *al = alpha + (long long)i * n;
+    T *bp = bprime + (long long)i * n;
+    for (long long p = (long long)blockIdx.x * CT + threadIdx.x; p < n; p += (long long)gridDim.x * CT) {
+        const double x = (double)own[p];
+        double s = 0.0;
+        for (int k = k0; k < k1; k++) s += (double)xh[nbr_slot[k]][p];
+        T a = al[p];
+        if (update) {
+            a = (T)((double)a + rho * (deg * x - s));
+            al[p] = a;
+        }
+        bp[p] = (T)(-(double)a + rho * (deg * x + s));
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(CT) paper_alg3(const T *u, const T *lam, T *const *xg,
+                                                 const long long *lo, const long long *lens,
+                                                 float *const *seg, long long n, double rho,
+                                                 double eta2, int e2) {
+    const int i = blockIdx.y;
+    const long long base = lo[i], len = lens[i];
+    T *x = xg[i];
+    float *out = seg ? seg[i] : nullptr;
+    for (long long q = (long long)blockIdx.x * CT + threadIdx.x; q < len; q += (long long)gridDim.x * CT) {
+        const long long p = base + q;
+        double xs = (double)x[p];
+        const double uv = (double)u[(long long)i * n + p], lv = (double)lam[(long long)i * n + p];
+        for (int it = 0; it < e2; it++) {
+            const double delta = rho * (xs - uv - lv / rho);
+            xs = xs - eta2 * delta;
+        }
+        if (out) out[q] = (float)xs;
+        else x[p] = (T)xs;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(CT) paper_dual(const T *u, T *lam, T *bprime, const T *const *xg,
+                                                 long long n, double rho, int update) {
+    const int i = blockIdx.y;
+    const T *x = xg[i];
+    for (long long p = (long long)blockIdx.x * CT + threadIdx.x; p < n; p += (long long)gridDim.x * CT) {
+        const long long g = (long long)i * n + p;
+        const double xv = (double)x[p];
+        T l = lam[g];
+        if (update) {
+            l = (T)((double)l + rho * ((double)u[g] - xv));
+            lam[g] = l;
+        }
+        bprime[g] = (T)(rho * xv - (double)l);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(CT) to_float(const T *const *src, float *const *dst, long long n) {
+    const int i = blockIdx.y;
+    const T *s = src[i];
+    float *d = dst[i];
+    for (long long p = (long long)blockIdx.x * CT + threadIdx.x; p < n; p += (long long)gridDim.x * CT)
+        d[p] = (float)s[p];
+}
+
+}  // namespace
+
+int launch_graph_dual(int prec, const void *const *xh_tab, const int *own_slot, const int *nbr_off,
+                      const int *nbr_slot, void *alpha, void *bprime, long long n, int L, double rho,
+                      int update_alpha, cudaStream_t st) {
+    if (L == 0) return 0;
+    if (prec == 0)
+        graph_dual<float><<<grid_of(n, L), CT, 0, st>>>((const float *const *)xh_tab, own_slot, nbr_off,
+                                                        nbr_slot, (float *)alpha, (float *)bprime, n, rho,
+                                                        update_alpha);
+    else
+        graph_dual<double><<<grid_of(n, L), CT, 0, st>>>((const double *const *)xh_tab, own_slot, nbr_off,
+                                                         nbr_slot, (double *)alpha, (double *)bprime, n,
+                                                         rho, update_alpha);
+    TQ_CHECK_CUDA(cudaGetLastError());
+    return 1;
+}
+
+int launch_paper_alg3(int prec, const void *u, const void *lam, void *const *xg_tab,
+                      const long long *lo, const long long *len, long long max_len,
+                      float *const *seg_tab, long long n, int L, double rho, double eta2, int e2,
+                      cudaStream_t st) {
+    if (L == 0) return 0;
+    if (prec == 0)
+        paper_alg3<float><<<grid_of(max_len, L), CT, 0, st>>>((const float *)u, (const float *)lam,
+                                                              (float *const *)xg_tab, lo, len, seg_tab,
+                                                              n, rho, eta2, e2);
+    else
+        paper_alg3<double><<<grid_of(max_len, L), CT, 0, st>>>((const double *)u, (const double *)lam,
+                                                               (double *const *)xg_tab, lo, len,
+                                                               seg_tab, n, rho, eta2, e2);
+    TQ_CHECK_CUDA(cudaGetLastError());
+    return 1;
+}
+
+int launch_paper_dual(int prec, const void *u, void *lam, void *bprime, const void *const *xg_tab,
+                      long long n, int L, double rho, int update_lam, cudaStream_t st) {
+    if (L == 0) return 0;
+    if (prec == 0)
+        paper_dual<float><<<grid_of(n, L), CT, 0, st>>>((const float *)u, (float *)lam, (float *)bprime,
+                                                        (const float *const *)xg_tab, n, rho, update_lam);
+    else
+        paper_dual<double><<<grid_of(n, L), CT, 0, st>>>((const double *)u, (double *)lam,
+                                                         (double *)bprime, (const double *const *)xg_tab,
+                                                         n, rho, update_lam);
+    TQ_CHECK_CUDA(cudaGetLastError());
+    return 1;
+}
+
+int launch_to_float(int prec, const void *const *src_tab, float *const *dst_tab, long long n, int L,
+                    cudaStream_t st) {
+    if (L == 0) return 0;
+    if (prec == 0)
+        to_float<float><<<grid_of(n, L), CT, 0, st>>>((const float *const *)src_tab, dst_tab, n);
+    else
+        to_float<double><<<grid_of(n, L), CT, 0, st>>>((const double *const *)src_tab, dst_tab, n);
+    TQ_CHECK_CUDA(cudaGetLastError());
+    return 1;
+}
+
+}  // namespace tq

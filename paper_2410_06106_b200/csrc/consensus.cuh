@@ -1,0 +1,32 @@
+// consensus.cuh -- the consensus / dual steps of both ADMM rules (elementwise, HBM
+// streams), fused with the next right-hand side b' of the local problems.
+#pragma once
+#include "common.cuh"
+
+namespace tq {
+
+// rule=graph (R-7): for local node i with public value xh_i = Q(x_i) and
+// neighbour sum S_i = sum_j xh_j:  alpha_i += rho (deg_i xh_i - S_i);
+// b'_i = -alpha_i + rho (deg_i xh_i + S_i).  update_alpha = 0 only recomputes b'.
+int launch_graph_dual(int prec, const void *const *xh_tab, const int *own_slot, const int *nbr_off,
+                      const int *nbr_slot, void *alpha, void *bprime, long long n, int L, double rho,
+                      int update_alpha, cudaStream_t st);
+
+// rule=paper, Alg. 3 on node i's own segment [lo_i, lo_i + len) of its
+// slice's consensus image xg_tab[i]:  E2 times  x <- x - eta2 rho (x - u - lambda/rho).
+// Result to seg_tab[i] (fp32, to be quantized) or, if seg_tab == null, in place in xg.
+int launch_paper_alg3(int prec, const void *u, const void *lam, void *const *xg_tab,
+                      const long long *lo, const long long *len, long long max_len,
+                      float *const *seg_tab, long long n, int L, double rho, double eta2, int e2,
+                      cudaStream_t st);
+
+// rule=paper, eq:solve_lamda and the next b' = rho x - lambda:
+// lambda += rho (u - x) (update_lam = 1), b' = rho x - lambda.
+int launch_paper_dual(int prec, const void *u, void *lam, void *bprime, const void *const *xg_tab,
+                      long long n, int L, double rho, int update_lam, cudaStream_t st);
+
+// dst_tab[i][p] = (float) src_tab[i][p]  (quantizer input = the fp32 wire format)
+int launch_to_float(int prec, const void *const *src_tab, float *const *dst_tab, long long n, int L,
+                    cudaStream_t st);
+
+}  // namespace tq

@@ -1,0 +1,777 @@
+// engine.cu -- see engine.cuh.
+#include <dlfcn.h>
+#include <math.h>
+
+#include <algorithm>
+#include <cstring>
+#include <set>
+
+#include "engine.cuh"
+
+namespace tq {
+
+[[noreturn]] void fail(tq_status code, const std::string &msg) { throw Error{code, msg}; }
+
+// ---------------------------------------------------------------- NCCL (dlopen'd)
+NcclApi &nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!api.h && !tried) {
+        tried = true;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            bool ok = true;
+            auto sym = [&](const char *name) {
+                void *p = dlsym(h, name);
+                if (!p) ok = false;
+                return p;
+            };
+            api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+            api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+            api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+            api.Send = (decltype(api.Send))sym("ncclSend");
+            api.Recv = (decltype(api.Recv))sym("ncclRecv");
+            api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
+            api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
+            api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+            if (ok) api.h = h;
+        }
+    }
+    if (!api.h) fail(TQ_ENCCL, "libnccl.so.2 could not be loaded");
+    return api;
+}
+
+#define TQ_CHECK_NCCL(call)                                                                       \
+    do {                                                                                          \
+        ncclResult_t _r = (call);                                                                 \
+        if (_r != ncclSuccess)                                                                    \
+            ::tq::fail(TQ_ENCCL, std::string(#call) + ": " + ::tq::nccl().GetErrorString(_r));    \
+    } while (0)
+
+// ---------------------------------------------------------------- exchange plan
+// graph rule: a node's payload goes to every rank owning one of its neighbours
+// (deduplicated per (node, peer)); paper rule: every node's segment payload goes
+// to every other rank that owns nodes (the all-gather of P:188).  Sorted by
+// (peer, node) so both ends of every pair post matching send/recv sequences.
+void exchange_plan(int M, const std::vector<int> &edges, const std::vector<int> &node_rank, int rule,
+                   int rank, int world, std::vector<std::pair<int, int>> &sends,
+                   std::vector<std::pair<int, int>> &recvs) {
+    std::set<std::pair<int, int>> S, R;  // (peer, node)
+    if (rule == TQ_RULE_GRAPH) {
+        for (size_t e = 0; e + 1 < edges.size(); e += 2) {
+            const int i = edges[e], j = edges[e + 1];
+            const int ri = node_rank[i], rj = node_rank[j];
+            if (ri == rj) continue;
+            if (ri == rank) { S.insert({rj, i}); R.insert({rj, j}); }
+            if (rj == rank) { S.insert({ri, j}); R.insert({ri, i}); }
+        }
+    } else {
+        std::set<int> owners(node_rank.begin(), node_rank.end());
+        for (int m = 0; m < M; m++) {
+            const int rm = node_rank[m];
+            for (int r : owners) {
+                if (r == rm) continue;
+                if (rm == rank) S.insert({r, m});
+                if (r == rank) R.insert({rm, m});
+            }
+        }
+    }
+    (void)world;
+    sends.clear();
+    recvs.clear();
+    for (auto &p : S) sends.push_back({p.second, p.first});
+    for (auto &p : R) recvs.push_back({p.second, p.first});
+}
+
+// ---------------------------------------------------------------- small kernels
+namespace {
+
+template <typename T>
+__global__ void gather_rows(const float *src, const int *src_row, T *dst, int n_rows, int n_det) {
+    const int r = blockIdx.y;
+    if (r >= n_rows) return;
+    const float *s = src + (long long)src_row[r] * n_det;
+    T *d = dst + (long long)r * n_det;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n_det; j += gridDim.x * blockDim.x) d[j] = (T)s[j];
+}
+
+template <typename T>
+__global__ void mean_rows(const T *base, int rows, long long n, float *out) {
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int r = 0; r < rows; r++) s += (double)base[(long long)r * n + p];
+        out[p] = (float)(s / rows);
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- context
+int Ctx::local(int slice, int node) const {
+    if (slice < 0 || slice >= S || node < 0 || node >= M) return -1;
+    return loc_of[(size_t)slice * M + node];
+}
+
+int Ctx::kind_of_slice(int s) const {
+    if (q.kind == TQ_Q_ALTERNATE) return (s % 2 == 0) ? TQ_Q_KMEANS : TQ_Q_DCT;
+    return q.kind;
+}
+
+void *Ctx::dev_alloc(size_t bytes) {
+    void *p = nullptr;
+    TQ_CHECK_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+    TQ_CHECK_CUDA(cudaMemset(p, 0, std::max<size_t>(bytes, 16)));
+    owned.push_back(p);
+    return p;
+}
+
+void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int rank_, int world_,
+                 const uint8_t *nccl_id, int precision, int device_) {
+    N = g.image_side; n_ang = g.n_angles; n_det = g.n_det;
+    TQ_REQUIRE(N >= 8 && N % 8 == 0, "image_side must be a positive multiple of 8");
+    TQ_REQUIRE(N <= 16384, "image_side too large");
+    TQ_REQUIRE(n_ang >= 1, "n_angles must be >= 1");
+    TQ_REQUIRE((long long)n_det * n_det >= 2LL * N * N, "n_det must be >= ceil(N sqrt 2)");
+    TQ_REQUIRE(precision == 0 || precision == 1, "precision must be 0 (fp32) or 1 (fp64)");
+    TQ_REQUIRE(n_slices >= 1, "n_slices must be >= 1");
+    TQ_REQUIRE(world_ >= 1 && rank_ >= 0 && rank_ < world_, "bad rank/world");
+    M = gr.n_nodes;
+    TQ_REQUIRE(M >= 1 && M <= n_ang, "n_nodes must be in [1, n_angles]");
+    TQ_REQUIRE(gr.rule == TQ_RULE_GRAPH || gr.rule == TQ_RULE_PAPER, "bad rule");
+    TQ_REQUIRE(gr.angle_split == TQ_SPLIT_ROUND_ROBIN || gr.angle_split == TQ_SPLIT_CONTIGUOUS, "bad split");
+    TQ_REQUIRE(gr.n_edges >= 0 && (gr.n_edges == 0 || gr.edges), "edges missing");
+    S = n_slices; rank = rank_; world = world_; prec = precision; device = device_;
+    rule = gr.rule; split = gr.angle_split;
+    n = (long long)N * N;
+    edges.assign(gr.edges, gr.edges + 2 * (size_t)gr.n_edges);
+    adj.assign(M, {});
+    std::set<std::pair<int, int>> seen;
+    for (int e = 0; e < gr.n_edges; e++) {
+        const int i = edges[2 * e], j = edges[2 * e + 1];
+        TQ_REQUIRE(i >= 0 && i < M && j >= 0 && j < M && i != j, "edge endpoints out of range or self loop");
+        TQ_REQUIRE(seen.insert({std::min(i, j), std::max(i, j)}).second, "duplicate edge");
+        adj[i].push_back(j);
+        adj[j].push_back(i);
+    }
+    if (rule == TQ_RULE_GRAPH && M > 1) {  // connected graph (consensus reaches every node)
+        std::vector<int> stack{0}, vis(M, 0);
+        vis[0] = 1;
+        while (!stack.empty()) {
+            const int u = stack.back();
+            stack.pop_back();
+            for (int v : adj[u]) if (!vis[v]) { vis[v] = 1; stack.push_back(v); }
+        }
+        for (int i = 0; i < M; i++) TQ_REQUIRE(vis[i], "graph rule needs a connected graph");
+    }
+    node_rank.resize(M);
+    for (int i = 0; i < M; i++) {
+        node_rank[i] = gr.node_rank ? gr.node_rank[i] : i % world;
+        TQ_REQUIRE(node_rank[i] >= 0 && node_rank[i] < world, "node_rank out of range");
+    }
+    partition_angles(n_ang, M, split, aoff, aidx);
+    partition_rows(N, M, row_off);
+    loc_of.assign((size_t)S * M, -1);
+    std::vector<std::vector<int>> angles;
+    for (int s = 0; s < S; s++)
+        for (int m = 0; m < M; m++)
+            if (node_rank[m] == rank) {
+                loc_of[(size_t)s * M + m] = (int)loc.size();
+                loc.push_back({s, m});
+                angles.push_back(std::vector<int>(aidx.begin() + aoff[m], aidx.begin() + aoff[m + 1]));
+            }
+    L = (int)loc.size();
+    TQ_CHECK_CUDA(cudaSetDevice(device));
+    TQ_CHECK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    TQ_CHECK_CUDA(cudaEventCreate(&ev0));
+    TQ_CHECK_CUDA(cudaEventCreate(&ev1));
+    geo.init(N, n_ang, n_det);
+    in.init(prec, geo, angles);
+    const size_t es = prec ? 8 : 4;
+    TQ_CHECK_CUDA(cudaMalloc(&ALPHA, std::max<size_t>(16, es * n * L)));
+    TQ_CHECK_CUDA(cudaMemset(ALPHA, 0, std::max<size_t>(16, es * n * L)));
+    if (rule == TQ_RULE_PAPER) {
+        TQ_CHECK_CUDA(cudaMalloc(&XG, es * n * S));
+        TQ_CHECK_CUDA(cudaMemset(XG, 0, es * n * S));
+    }
+    if (world > 1) {
+        TQ_REQUIRE(nccl_id != nullptr, "world > 1 needs an NCCL unique id");
+        ncclUniqueId id;
+        memcpy(&id, nccl_id, sizeof(id));
+        TQ_CHECK_NCCL(nccl().CommInitRank(&comm, world, id, rank));
+    }
+    sino_set.assign(L, 0);
+    st.local_nodes = L;
+    st.world = world;
+}
+
+void Ctx::invalidate() {
+    if (gexecA) { cudaGraphExecDestroy(gexecA); gexecA = nullptr; }
+    if (gexecB) { cudaGraphExecDestroy(gexecB); gexecB = nullptr; }
+}
+
+void Ctx::free_exchange() {
+    invalidate();
+    for (void *p : owned) cudaFree(p);
+    owned.clear();
+    kmw.release();
+    dctw.release();
+    pays.clear();
+    pay_of.clear();
+    for (auto &b : enc) b = Batch();
+    for (auto &b : dec) b = Batch();
+    sends.clear(); recvs.clear(); send_buf.clear(); recv_buf.clear(); send_bytes.clear(); recv_bytes.clear();
+    label_row.clear();
+    fstage = nullptr; labels_buf = nullptr; xh_tab = nullptr; own_slot = nbr_off = nbr_slot = nullptr;
+    xg_tab = nullptr; seg_lo = nullptr; seg_len = nullptr; seg_tab = nullptr;
+    xready = false;
+}
+
+void Ctx::destroy() {
+    if (stream) cudaStreamSynchronize(stream);
+    free_exchange();
+    in.release();
+    geo.release();
+    if (ALPHA) cudaFree(ALPHA);
+    if (XG) cudaFree(XG);
+    ALPHA = XG = nullptr;
+    if (sino_stage) cudaFree(sino_stage);
+    if (row_map) cudaFree(row_map);
+    sino_stage = nullptr; row_map = nullptr;
+    if (comm) nccl().CommDestroy(comm);
+    comm = nullptr;
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+    stream = nullptr;
+}
+
+void Ctx::set_params(const tq_params &p) {
+    TQ_REQUIRE(p.rho > 0.0 && std::isfinite(p.rho), "rho must be > 0");
+    TQ_REQUIRE(p.inner == TQ_INNER_GD || p.inner == TQ_INNER_CG, "inner must be GD or CG");
+    TQ_REQUIRE(p.e1 >= 0 && p.e1 <= 100000, "e1 out of range");
+    if (rule == TQ_RULE_PAPER) {
+        TQ_REQUIRE(p.e2 >= 0, "e2 must be >= 0");
+        TQ_REQUIRE(p.eta2 * p.rho > 0.0 && p.eta2 * p.rho < 2.0, "need 0 < eta2 rho < 2 (Alg. 3 contraction)");
+    }
+    prm = p;
+    eta1.clear();
+    if (p.eta1) eta1.assign(p.eta1, p.eta1 + M);
+    prm.eta1 = nullptr;
+    std::vector<double> c(L), eta(L);
+    for (int i = 0; i < L; i++) {
+        const int m = loc[i].second;
+        c[i] = rule == TQ_RULE_GRAPH ? 2.0 * p.rho * (double)adj[m].size() : p.rho;
+        const int a = aoff[m + 1] - aoff[m];
+        eta[i] = eta1.empty() ? 1.0 / (2.0 * a * N + c[i]) : eta1[m];  // R-8
+    }
+    if (L) {
+        TQ_CHECK_CUDA(cudaMemcpy(in.cnode, c.data(), sizeof(double) * L, cudaMemcpyHostToDevice));
+        TQ_CHECK_CUDA(cudaMemcpy(in.eta, eta.data(), sizeof(double) * L, cudaMemcpyHostToDevice));
+    }
+    have_params = true;
+    invalidate();
+}
+
+void Ctx::set_quant(const tq_quant &qq) {
+    TQ_REQUIRE(qq.kind >= TQ_Q_NONE && qq.kind <= TQ_Q_ALTERNATE, "bad quantizer kind");
+    const bool km = qq.kind == TQ_Q_KMEANS || qq.kind == TQ_Q_ALTERNATE;
+    const bool dc = qq.kind == TQ_Q_DCT || qq.kind == TQ_Q_ALTERNATE;
+    if (km) TQ_REQUIRE(qq.k >= 1 && qq.k <= 256 && qq.lloyd_iters >= 0, "kmeans: k in [1,256], lloyd >= 0");
+    if (dc) TQ_REQUIRE(qq.quality >= 1 && qq.quality <= 100, "dct: quality in [1,100]");
+    if (rule == TQ_RULE_PAPER && qq.kind != TQ_Q_NONE) {
+        TQ_REQUIRE(N % M == 0, "paper rule with a quantizer needs equal segments (M | N)");
+        if (dc) TQ_REQUIRE((N / M) % 8 == 0, "paper rule with DCT needs 8 | N/M");
+    }
+    free_exchange();
+    q = qq;
+}
+
+void Ctx::set_sinogram(int slice, int node, const float *d, long long len, bool on_device) {
+    TQ_REQUIRE(slice >= 0 && slice < S, "slice out of range");
+    TQ_REQUIRE(node >= -1 && node < M, "node out of range");
+    TQ_REQUIRE(d != nullptr, "null sinogram");
+    const long long rows = node < 0 ? n_ang : (aoff[node + 1] - aoff[node]);
+    TQ_REQUIRE(len == rows * n_det, "sinogram length mismatch");
+    // staging copy on the device, then a gather of the rows of every local node
+    TQ_CHECK_CUDA(cudaSetDevice(device));
+    if (sino_stage_len < len) {
+        if (sino_stage) cudaFree(sino_stage);
+        sino_stage = nullptr;
+        TQ_CHECK_CUDA(cudaMalloc(&sino_stage, sizeof(float) * len));
+        sino_stage_len = len;
+    }
+    float *stage = sino_stage;
+    TQ_CHECK_CUDA(cudaMemcpyAsync(stage, d, sizeof(float) * len,
+                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream));
+    std::vector<int> src_row, dst_row;
+    for (int i = 0; i < L; i++) {
+        if (loc[i].first != slice) continue;
+        const int m = loc[i].second;
+        if (node >= 0 && m != node) continue;
+        for (int k = 0; k < aoff[m + 1] - aoff[m]; k++) {
+            src_row.push_back(node < 0 ? aidx[aoff[m] + k] : k);
+            dst_row.push_back(in.row0_h[i] + k);
+        }
+        sino_set[i] = 1;
+    }
+    if (!src_row.empty()) {
+        // rows of one node are contiguous in D: gather per node run
+        if (row_map_len < (long long)src_row.size()) {
+            if (row_map) cudaFree(row_map);
+            row_map = nullptr;
+            TQ_CHECK_CUDA(cudaMalloc(&row_map, sizeof(int) * src_row.size()));
+            row_map_len = (long long)src_row.size();
+        }
+        int *srd = row_map;
+        TQ_CHECK_CUDA(cudaMemcpyAsync(srd, src_row.data(), sizeof(int) * src_row.size(),
+                                      cudaMemcpyHostToDevice, stream));
+        size_t k = 0;
+        while (k < src_row.size()) {
+            size_t e = k;
+            while (e + 1 < src_row.size() && dst_row[e + 1] == dst_row[e] + 1) e++;
+            const int cnt = (int)(e - k + 1);
+            dim3 grid(ceil_div(n_det, 256), cnt);
+            if (prec == 0)
+                gather_rows<float><<<grid, 256, 0, stream>>>(stage, srd + k, (float *)in.D + (long long)dst_row[k] * n_det, cnt, n_det);
+            else
+                gather_rows<double><<<grid, 256, 0, stream>>>(stage, srd + k, (double *)in.D + (long long)dst_row[k] * n_det, cnt, n_det);
+            TQ_CHECK_CUDA(cudaGetLastError());
+            k = e + 1;
+        }
+    }
+    TQ_CHECK_CUDA(cudaStreamSynchronize(stream));
+}
+
+long long Ctx::launch_component(int component, int reps, cudaStream_t s) {
+    TQ_REQUIRE(reps >= 0, "reps must be >= 0");
+    if (!have_params) fail(TQ_ESTATE, "tq_set_params must be called first");
+    TQ_CHECK_CUDA(cudaSetDevice(device));
+    if (!xready) setup_exchange();
+    long long vu = 0;
+    for (int i = 0; i < L; i++) vu += (long long)in.nang_h[i] * n;
+    switch (component) {
+        case 0: for (int r = 0; r < reps; r++) in.project(geo, in.P, false, s); return vu;
+        case 1: for (int r = 0; r < reps; r++) in.backproject(geo, EPI_CGQ, in.Q, nullptr, in.P, s); return vu;
+        case 2: for (int r = 0; r < reps; r++) in.project(geo, in.X, true, s); return vu;
+        case 3:
+        case 4: {
+            const int kd = component == 3 ? TQ_Q_KMEANS : TQ_Q_DCT;
+            Batch &E = enc[kd];
+            TQ_REQUIRE(E.P > 0, "no local payloads of that quantizer kind");
+            for (int r = 0; r < reps; r++) {
+                if (E.need_conv) launch_to_float(prec, E.conv_src_d, E.conv_dst_d, n, (int)E.conv_src.size(), s);
+                if (kd == TQ_Q_KMEANS) kmeans_encode(E.vin, kmw, q.lloyd_iters, E.pay, E.labels, s);
+                else dct_encode(E.vin, E.P, rule == TQ_RULE_PAPER ? N / M : N, N, q.quality, dctw, E.pay, s);
+            }
+            return (long long)E.P * payload_len;
+        }
+        case 5: for (int r = 0; r < reps; r++) prepare_rhs(s); return (long long)L * n;
+        default: fail(TQ_EINVAL, "unknown component");
+    }
+}
+
+void Ctx::setup_exchange() {
+    free_exchange();
+    const size_t es = prec ? 8 : 4;
+    const bool paper = rule == TQ_RULE_PAPER;
+    payload_len = paper ? n / M : n;
+    std::vector<std::pair<int, int>> sp, rp;
+    exchange_plan(M, edges, node_rank, rule, rank, world, sp, rp);
+    // ---- payload list
+    auto add_pay = [&](int s, int m, bool local) {
+        if (pay_of.count({s, m})) return;
+        Pay p{s, m, nullptr, local, kind_of_slice(s)};
+        pay_of[{s, m}] = (int)pays.size();
+        pays.push_back(p);
+    };
+    std::vector<int> slices_here;
+    for (int s = 0; s < S; s++) {
+        bool any = false;
+        for (int m = 0; m < M; m++) any |= local(s, m) >= 0;
+        if (any) slices_here.push_back(s);
+    }
+    for (int i = 0; i < L; i++) add_pay(loc[i].first, loc[i].second, true);
+    for (int s : slices_here) {
+        if (paper) {
+            for (int m = 0; m < M; m++) add_pay(s, m, local(s, m) >= 0);
+        } else {
+            for (auto &r : rp) add_pay(s, r.first, false);
+        }
+    }
+    // ---- buffers: payload (wire) and decoded public value
+    std::vector<void *> xh(pays.size(), nullptr), outp(pays.size(), nullptr);
+    std::vector<long long> pbytes(pays.size(), 0);
+    for (size_t k = 0; k < pays.size(); k++) {
+        Pay &p = pays[k];
+        const int li = local(p.slice, p.node);
+        if (p.kind == TQ_Q_NONE) {
+            if (paper) {
+                const long long lo = (long long)row_off[p.node] * N, len = (long long)(row_off[p.node + 1] - row_off[p.node]) * N;
+                p.buf = (uint8_t *)XG + es * ((long long)p.slice * n + lo);
+                pbytes[k] = es * len;
+            } else {
+                p.buf = li >= 0 ? (uint8_t *)in.xrow(in.X, li) : (uint8_t *)dev_alloc(es * n);
+                pbytes[k] = es * n;
+                xh[k] = p.buf;
+            }
+        } else {
+            pbytes[k] = p.kind == TQ_Q_KMEANS ? kmeans_payload_bytes(q.k, payload_len) : dct_payload_bytes(payload_len);
+            p.buf = (uint8_t *)dev_alloc(pbytes[k]);
+            if (paper) {
+                outp[k] = (uint8_t *)XG + es * ((long long)p.slice * n + (long long)row_off[p.node] * N);
+            } else {
+                xh[k] = dev_alloc(es * n);
+                outp[k] = xh[k];
+            }
+        }
+    }
+    auto upload = [&](const void *src, size_t bytes) {
+        void *d = dev_alloc(bytes);
+        TQ_CHECK_CUDA(cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice));
+        return d;
+    };
+    // ---- float staging for quantizer inputs
+    std::vector<int> stage_row(L, -1);
+    int nstage = 0;
+    for (int i = 0; i < L; i++) {
+        const int kd = kind_of_slice(loc[i].first);
+        if (kd == TQ_Q_NONE) continue;
+        if (paper || prec == 1) stage_row[i] = nstage++;
+    }
+    if (nstage) fstage = (float *)dev_alloc(sizeof(float) * payload_len * nstage);
+    label_row.assign(L, -1);
+    int nlab = 0;
+    if (q.keep_labels)
+        for (int i = 0; i < L; i++)
+            if (kind_of_slice(loc[i].first) == TQ_Q_KMEANS) label_row[i] = nlab++;
+    if (nlab) labels_buf = (int32_t *)dev_alloc(sizeof(int32_t) * payload_len * nlab);
+    // ---- encode / decode batches
+    for (int kd = 1; kd <= 2; kd++) {
+        Batch &E = enc[kd], &D = dec[kd];
+        E.kind = D.kind = kd;
+        std::vector<const float *> vin;
+        std::vector<uint8_t *> pe, pd;
+        std::vector<int32_t *> lab;
+        std::vector<const void *> csrc;
+        std::vector<float *> cdst;
+        std::vector<void *> out;
+        for (size_t k = 0; k < pays.size(); k++) {
+            if (pays[k].kind != kd) continue;
+            pd.push_back(pays[k].buf);
+            out.push_back(outp[k]);
+            D.members.push_back((int)k);
+            if (!pays[k].local) continue;
+            const int li = local(pays[k].slice, pays[k].node);
+            E.members.push_back((int)k);
+            pe.push_back(pays[k].buf);
+            const float *v;
+            if (stage_row[li] >= 0) {
+                v = fstage + (long long)stage_row[li] * payload_len;
+                if (!paper) { csrc.push_back(in.xrow(in.X, li)); cdst.push_back((float *)v); }
+            } else {
+                v = (const float *)in.xrow(in.X, li);
+            }
+            vin.push_back(v);
+            lab.push_back(label_row[li] >= 0 ? labels_buf + (long long)label_row[li] * payload_len : nullptr);
+        }
+        E.P = (int)pe.size();
+        D.P = (int)pd.size();
+        if (E.P) {
+            E.vin = (const float **)upload(vin.data(), sizeof(void *) * E.P);
+            E.pay = (uint8_t **)upload(pe.data(), sizeof(void *) * E.P);
+            if (kd == TQ_Q_KMEANS && nlab) E.labels = (int32_t **)upload(lab.data(), sizeof(void *) * E.P);
+            if (!csrc.empty()) {
+                E.need_conv = true;
+                E.conv_src.assign(csrc.begin(), csrc.end());
+                E.conv_src_d = (const void **)upload(csrc.data(), sizeof(void *) * csrc.size());
+                E.conv_dst_d = (float **)upload(cdst.data(), sizeof(void *) * cdst.size());
+            }
+            if (kd == TQ_Q_KMEANS) kmw.alloc(E.P, q.k, payload_len);
+            else dctw.alloc(E.P, payload_len);
+        }
+        if (D.P) {
+            D.pay = (uint8_t **)upload(pd.data(), sizeof(void *) * D.P);
+            D.out = (void **)upload(out.data(), sizeof(void *) * D.P);
+        }
+    }
+    // ---- consensus tables
+    if (!paper) {
+        xh_tab = (const void **)upload(xh.data(), sizeof(void *) * xh.size());
+        std::vector<int> own(L), off(L + 1, 0), nb;
+        for (int i = 0; i < L; i++) {
+            own[i] = pay_of.at(loc[i]);
+            for (int j : adj[loc[i].second]) nb.push_back(pay_of.at({loc[i].first, j}));
+            off[i + 1] = (int)nb.size();
+        }
+        own_slot = (int *)upload(own.data(), sizeof(int) * std::max(1, L));
+        nbr_off = (int *)upload(off.data(), sizeof(int) * (L + 1));
+        if (nb.empty()) nb.push_back(0);
+        nbr_slot = (int *)upload(nb.data(), sizeof(int) * nb.size());
+    } else {
+        std::vector<void *> xg(L);
+        std::vector<long long> lo(L), len(L);
+        std::vector<float *> seg(L, nullptr);
+        for (int i = 0; i < L; i++) {
+            const int s = loc[i].first, m = loc[i].second;
+            xg[i] = (uint8_t *)XG + es * (long long)s * n;
+            lo[i] = (long long)row_off[m] * N;
+            len[i] = (long long)(row_off[m + 1] - row_off[m]) * N;
+            if (stage_row[i] >= 0) seg[i] = fstage + (long long)stage_row[i] * payload_len;
+        }
+        xg_tab = (void **)upload(xg.data(), sizeof(void *) * std::max(1, L));
+        seg_lo = (long long *)upload(lo.data(), sizeof(long long) * std::max(1, L));
+        seg_len = (long long *)upload(len.data(), sizeof(long long) * std::max(1, L));
+        seg_max = 0;
+        for (int m = 0; m < M; m++) seg_max = std::max(seg_max, (long long)(row_off[m + 1] - row_off[m]) * N);
+        seg_tab = (float **)upload(seg.data(), sizeof(void *) * std::max(1, L));
+    }
+    // ---- NCCL transfers (per slice, same plan)
+    for (int s : slices_here) {
+        for (auto &x : sp) {
+            const int k = pay_of.at({s, x.first});
+            sends.push_back({s, x.first, x.second});
+            send_buf.push_back(pays[k].buf);
+            send_bytes.push_back(pbytes[k]);
+        }
+        for (auto &x : rp) {
+            const int k = pay_of.at({s, x.first});
+            recvs.push_back({s, x.first, x.second});
+            recv_buf.push_back(pays[k].buf);
+            recv_bytes.push_back(pbytes[k]);
+        }
+    }
+    // ---- logical bytes (what the method sends, independent of placement)
+    long long logical = 0;
+    for (int i = 0; i < L; i++) {
+        const int kd = kind_of_slice(loc[i].first), m = loc[i].second;
+        const long long len = paper ? (long long)(row_off[m + 1] - row_off[m]) * N : n;
+        const long long pb = kd == TQ_Q_NONE ? (long long)es * len
+                             : kd == TQ_Q_KMEANS ? kmeans_payload_bytes(q.k, payload_len)
+                                                 : dct_payload_bytes(payload_len);
+        logical += pb * (paper ? (M - 1) : (long long)adj[m].size());
+    }
+    st.payload_bytes_logical = logical;
+    st.nccl_bytes_sent = 0;
+    for (auto b : send_bytes) st.nccl_bytes_sent += b;
+    st.nccl_bytes_recv = 0;
+    for (auto b : recv_bytes) st.nccl_bytes_recv += b;
+    xready = true;
+}
+
+int Ctx::phase_a(cudaStream_t s) {
+    int k = prm.inner == TQ_INNER_CG ? in.cg(geo, prm.e1, s) : in.gd(geo, prm.e1, s);
+    if (rule == TQ_RULE_PAPER)
+        k += launch_paper_alg3(prec, in.X, ALPHA, xg_tab, seg_lo, seg_len, seg_max, seg_tab, n, L,
+                               prm.rho, prm.eta2, prm.e2, s);
+    for (int kd = 1; kd <= 2; kd++) {
+        Batch &E = enc[kd];
+        if (!E.P) continue;
+        if (E.need_conv) k += launch_to_float(prec, E.conv_src_d, E.conv_dst_d, n, (int)E.conv_src.size(), s);
+        if (kd == TQ_Q_KMEANS) k += kmeans_encode(E.vin, kmw, q.lloyd_iters, E.pay, E.labels, s);
+        else {
+            const int rows = rule == TQ_RULE_PAPER ? N / M : N;
+            k += dct_encode(E.vin, E.P, rows, N, q.quality, dctw, E.pay, s);
+        }
+    }
+    return k;
+}
+
+void Ctx::exchange(cudaStream_t s) {
+    if (world == 1 || (sends.empty() && recvs.empty())) return;
+    NcclApi &api = nccl();
+    TQ_CHECK_NCCL(api.GroupStart());
+    for (size_t i = 0; i < sends.size(); i++)
+        TQ_CHECK_NCCL(api.Send(send_buf[i], (size_t)send_bytes[i], ncclUint8, sends[i].peer, comm, s));
+    for (size_t i = 0; i < recvs.size(); i++)
+        TQ_CHECK_NCCL(api.Recv(recv_buf[i], (size_t)recv_bytes[i], ncclUint8, recvs[i].peer, comm, s));
+    TQ_CHECK_NCCL(api.GroupEnd());
+}
+
+int Ctx::phase_b(cudaStream_t s) {
+    int k = 0;
+    for (int kd = 1; kd <= 2; kd++) {
+        Batch &D = dec[kd];
+        if (!D.P) continue;
+        if (kd == TQ_Q_KMEANS) k += kmeans_decode(D.pay, D.P, payload_len, q.k, prec, D.out, s);
+        else {
+            const int rows = rule == TQ_RULE_PAPER ? N / M : N;
+            k += dct_decode(D.pay, D.P, rows, N, q.quality, prec, D.out, s);
+        }
+    }
+    if (rule == TQ_RULE_GRAPH)
+        k += launch_graph_dual(prec, xh_tab, own_slot, nbr_off, nbr_slot, ALPHA, in.BP, n, L, prm.rho, 1, s);
+    else
+        k += launch_paper_dual(prec, in.X, ALPHA, in.BP, (const void *const *)xg_tab, n, L, prm.rho, 1, s);
+    return k;
+}
+
+int Ctx::prepare_rhs(cudaStream_t s) {
+    if (rule == TQ_RULE_GRAPH)
+        return launch_graph_dual(prec, xh_tab, own_slot, nbr_off, nbr_slot, ALPHA, in.BP, n, L, prm.rho, 0, s);
+    return launch_paper_dual(prec, in.X, ALPHA, in.BP, (const void *const *)xg_tab, n, L, prm.rho, 0, s);
+}
+
+void Ctx::run(int iters, cudaStream_t user) {
+    TQ_REQUIRE(iters >= 0, "iters must be >= 0");
+    if (!have_params) fail(TQ_ESTATE, "tq_set_params must be called before tq_run");
+    for (int i = 0; i < L; i++)
+        if (!sino_set[i]) fail(TQ_ESTATE, "sinogram of a local node was never set");
+    TQ_CHECK_CUDA(cudaSetDevice(device));
+    if (!xready) setup_exchange();
+    cudaStream_t s = user ? user : stream;
+    if (need_rhs) {
+        prepare_rhs(s);
+        need_rhs = false;
+    }
+    auto capture = [&](cudaGraphExec_t &ge, int &cnt, bool a_part, bool b_part) {
+        cudaGraph_t g;
+        TQ_CHECK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        int c = 0;
+        try {
+            if (a_part) c += phase_a(s);
+            if (b_part) c += phase_b(s);
+        } catch (...) {
+            cudaStreamEndCapture(s, &g);
+            throw;
+        }
+        TQ_CHECK_CUDA(cudaStreamEndCapture(s, &g));
+        TQ_CHECK_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        cudaGraphDestroy(g);
+        cnt = c;
+    };
+    const bool split_phases = world > 1 && !(sends.empty() && recvs.empty());
+    if (!gexecA) {
+        if (split_phases) {
+            capture(gexecA, launchesA, true, false);
+            capture(gexecB, launchesB, false, true);
+        } else {
+            capture(gexecA, launchesA, true, true);
+            launchesB = 0;
+        }
+    }
+    TQ_CHECK_CUDA(cudaEventRecord(ev0, s));
+    for (int it = 0; it < iters; it++) {
+        TQ_CHECK_CUDA(cudaGraphLaunch(gexecA, s));
+        if (split_phases) {
+            exchange(s);
+            TQ_CHECK_CUDA(cudaGraphLaunch(gexecB, s));
+        }
+    }
+    TQ_CHECK_CUDA(cudaEventRecord(ev1, s));
+    in.norm2(s);
+    std::vector<double> sc((size_t)S_NSLOT * std::max(1, L));
+    TQ_CHECK_CUDA(cudaMemcpyAsync(sc.data(), in.scal, sizeof(double) * S_NSLOT * L, cudaMemcpyDeviceToHost, s));
+    TQ_CHECK_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    TQ_CHECK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    st.ms_last_run = ms;
+    st.iters += iters;
+    st.kernel_launches = (long long)iters * (launchesA + launchesB);
+    for (int i = 0; i < L; i++) {
+        const double nrm = sqrt(sc[(size_t)i * S_NSLOT + S_NORM]);
+        if (!(nrm <= 1e12)) fail(TQ_EDIVERGED, "node iterate norm exceeded 1e12 (diverged)");
+    }
+}
+
+void Ctx::get_image(int slice, int node, float *out, long long len, bool on_device) {
+    TQ_REQUIRE(len == n, "image length must be N*N");
+    TQ_CHECK_CUDA(cudaSetDevice(device));
+    float *d = nullptr;
+    TQ_CHECK_CUDA(cudaMalloc(&d, sizeof(float) * n));
+    const int blocks = (int)std::min<long long>(2048, (n + 255) / 256);
+    if (node >= 0) {
+        const int i = local(slice, node);
+        if (i < 0) { cudaFree(d); fail(TQ_EINVAL, "node is not local to this rank"); }
+        launch_convert(prec, in.xrow(in.X, i), 0, d, n, stream);
+    } else if (rule == TQ_RULE_PAPER) {
+        TQ_REQUIRE(slice >= 0 && slice < S, "slice out of range");
+        launch_convert(prec, (uint8_t *)XG + (prec ? 8 : 4) * (long long)slice * n, 0, d, n, stream);
+    } else {
+        const int i0 = local(slice, 0);
+        bool all = i0 >= 0;
+        for (int m = 0; m < M && all; m++) all = local(slice, m) == i0 + m;
+        if (!all) { cudaFree(d); fail(TQ_EINVAL, "node=-1 (mean image) needs every node of the slice on this rank"); }
+        if (prec == 0) mean_rows<float><<<blocks, 256, 0, stream>>>((const float *)in.xrow(in.X, i0), M, n, d);
+        else mean_rows<double><<<blocks, 256, 0, stream>>>((const double *)in.xrow(in.X, i0), M, n, d);
+        TQ_CHECK_CUDA(cudaGetLastError());
+    }
+    TQ_CHECK_CUDA(cudaMemcpyAsync(out, d, sizeof(float) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream));
+    TQ_CHECK_CUDA(cudaStreamSynchronize(stream));
+    cudaFree(d);
+}
+
+static void to_host_double(int prec, const void *src, double *dst, long long n, cudaStream_t s) {
+    double *d = nullptr;
+    TQ_CHECK_CUDA(cudaMalloc(&d, sizeof(double) * n));
+    launch_convert(prec, src, 1, d, n, s);
+    TQ_CHECK_CUDA(cudaMemcpyAsync(dst, d, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    TQ_CHECK_CUDA(cudaStreamSynchronize(s));
+    cudaFree(d);
+}
+
+static void from_host_double(int prec, const double *src, void *dst, long long n, cudaStream_t s) {
+    double *d = nullptr;
+    TQ_CHECK_CUDA(cudaMalloc(&d, sizeof(double) * n));
+    TQ_CHECK_CUDA(cudaMemcpyAsync(d, src, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    launch_convert(1, d, prec, dst, n, s);
+    TQ_CHECK_CUDA(cudaStreamSynchronize(s));
+    cudaFree(d);
+}
+
+void Ctx::export_state(int slice, int node, double *buf, long long len) {
+    TQ_REQUIRE(len == 3 * n, "state length must be 3*N*N");
+    const int i = local(slice, node);
+    TQ_REQUIRE(i >= 0, "node is not local to this rank");
+    TQ_CHECK_CUDA(cudaSetDevice(device));
+    if (!xready) setup_exchange();
+    const size_t es = prec ? 8 : 4;
+    to_host_double(prec, in.xrow(in.X, i), buf, n, stream);
+    to_host_double(prec, (uint8_t *)ALPHA + es * n * i, buf + n, n, stream);
+    if (rule == TQ_RULE_PAPER) {
+        to_host_double(prec, (uint8_t *)XG + es * n * slice, buf + 2 * n, n, stream);
+    } else {
+        const int k = pay_of.at({slice, node});
+        const void *xh = pays[k].kind == TQ_Q_NONE ? pays[k].buf : nullptr;
+        if (!xh) {  // decoded buffer of the own payload
+            std::vector<const void *> tab((size_t)pays.size());
+            TQ_CHECK_CUDA(cudaMemcpy(tab.data(), xh_tab, sizeof(void *) * pays.size(), cudaMemcpyDeviceToHost));
+            xh = tab[k];
+        }
+        to_host_double(prec, xh, buf + 2 * n, n, stream);
+    }
+}
+
+void Ctx::import_state(int slice, int node, const double *buf, long long len) {
+    TQ_REQUIRE(len == 3 * n, "state length must be 3*N*N");
+    const int i = local(slice, node);
+    TQ_REQUIRE(i >= 0, "node is not local to this rank");
+    TQ_CHECK_CUDA(cudaSetDevice(device));
+    if (!xready) setup_exchange();
+    const size_t es = prec ? 8 : 4;
+    from_host_double(prec, buf, in.xrow(in.X, i), n, stream);
+    from_host_double(prec, buf + n, (uint8_t *)ALPHA + es * n * i, n, stream);
+    if (rule == TQ_RULE_PAPER) {
+        from_host_double(prec, buf + 2 * n, (uint8_t *)XG + es * n * slice, n, stream);
+    } else {
+        const int k = pay_of.at({slice, node});
+        if (pays[k].kind != TQ_Q_NONE) {
+            std::vector<void *> tab((size_t)pays.size());
+            TQ_CHECK_CUDA(cudaMemcpy(tab.data(), xh_tab, sizeof(void *) * pays.size(), cudaMemcpyDeviceToHost));
+            from_host_double(prec, buf + 2 * n, tab[k], n, stream);
+        }
+    }
+    need_rhs = true;
+}
+
+void Ctx::export_labels(int slice, int node, int32_t *buf, long long len) {
+    const int i = local(slice, node);
+    TQ_REQUIRE(i >= 0, "node is not local to this rank");
+    TQ_REQUIRE(xready && (int)label_row.size() == L && label_row[i] >= 0,
+               "labels not kept (set keep_labels and a K-means quantizer, then run)");
+    TQ_REQUIRE(len == payload_len, "labels length must equal the payload length");
+    TQ_CHECK_CUDA(cudaMemcpy(buf, labels_buf + (long long)label_row[i] * payload_len, sizeof(int32_t) * len,
+                             cudaMemcpyDeviceToHost));
+}
+
+}  // namespace tq

@@ -1,0 +1,136 @@
+// engine.cuh -- the ADMM context behind the C-ABI: per-rank device state for every
+// (slice, node) mapped to this rank, the outer loop of Alg. 4
+// for both consensus rules, the quantized exchange (NCCL send/recv between ranks,
+// pointers within a rank) and CUDA-graph replay of whole iterations.
+#pragma once
+#include <nccl.h>
+
+#include <map>
+
+#include "codecs.cuh"
+#include "consensus.cuh"
+#include "solver.cuh"
+
+namespace tq {
+
+struct NcclApi {
+    void *h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi &nccl();  // loads libnccl.so.2 on first use (fails with TQ_ENCCL if absent)
+
+struct XferItem {  // one payload crossing ranks in an iteration
+    int slice, node, peer;
+};
+// exchange plan of one rank for one slice-independent graph
+void exchange_plan(int M, const std::vector<int> &edges, const std::vector<int> &node_rank, int rule,
+                   int rank, int world, std::vector<std::pair<int, int>> &sends,
+                   std::vector<std::pair<int, int>> &recvs);
+
+struct Ctx {
+    // ---- problem
+    int N = 0, n_ang = 0, n_det = 0, S = 1, M = 1, rank = 0, world = 1, prec = 0, device = 0;
+    int rule = 0, split = 0;
+    long long n = 0;
+    std::vector<int> edges, node_rank, aoff, aidx, row_off;
+    std::vector<std::vector<int>> adj;
+    // ---- local (slice, node) pairs, slice-major
+    std::vector<std::pair<int, int>> loc;
+    std::vector<int> loc_of;  // [S*M] -> local index or -1
+    int L = 0;
+    DevGeom geo;
+    Inner in;
+    void *ALPHA = nullptr;      // [L][n] alpha_i (graph) / lambda_m (paper)
+    void *XG = nullptr;         // paper: [S][n] consensus x
+    // ---- settings
+    tq_params prm{};
+    std::vector<double> eta1;
+    bool have_params = false;
+    tq_quant q{TQ_Q_NONE, 16, 10, 50};
+    std::vector<char> sino_set;
+    bool need_rhs = false;      // recompute b' from the state before the next iteration
+    // ---- quantizer / exchange state (rebuilt by setup_exchange)
+    bool xready = false;
+    int kind_of_slice(int s) const;
+    long long payload_len = 0;                // elements per payload (n or segment)
+    struct Pay { int slice, node; uint8_t *buf; bool local; int kind; };
+    std::vector<Pay> pays;                    // every payload this rank touches
+    std::map<std::pair<int, int>, int> pay_of;
+    std::vector<void *> owned;                // device allocations of the exchange state
+    // encode batches (local payloads) and decode batches (all payloads) per kind
+    struct Batch {
+        int kind = 0, P = 0;
+        const float **vin = nullptr;          // device tables
+        uint8_t **pay = nullptr;
+        int32_t **labels = nullptr;
+        void **out = nullptr;
+        std::vector<int> members;             // pays index
+        std::vector<const void *> conv_src;   // to_float sources
+        const void **conv_src_d = nullptr;
+        float **conv_dst_d = nullptr;
+        bool need_conv = false;
+    };
+    Batch enc[3], dec[3];
+    KmeansWork kmw;
+    DctWork dctw;
+    float *fstage = nullptr;                  // float staging for quantizer inputs
+    int32_t *labels_buf = nullptr;            // [L][payload_len] when keep_labels
+    std::vector<int> label_row;               // local idx -> row in labels_buf or -1
+    // graph rule dual tables
+    const void **xh_tab = nullptr;
+    int *own_slot = nullptr, *nbr_off = nullptr, *nbr_slot = nullptr;
+    // paper rule tables
+    void **xg_tab = nullptr;
+    long long *seg_lo = nullptr, *seg_len = nullptr;
+    long long seg_max = 0;
+    float **seg_tab = nullptr;
+    // NCCL
+    ncclComm_t comm = nullptr;
+    std::vector<XferItem> sends, recvs;
+    std::vector<uint8_t *> send_buf, recv_buf;
+    std::vector<long long> send_bytes, recv_bytes;
+    // ---- execution
+    cudaStream_t stream = nullptr;
+    cudaGraphExec_t gexecA = nullptr, gexecB = nullptr;
+    int launchesA = 0, launchesB = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    tq_stats st{};
+    std::string err;
+
+    void create(const tq_geometry &g, const tq_graph &gr, int n_slices, int rank, int world,
+                const uint8_t *nccl_id, int precision, int device);
+    void destroy();
+    void set_params(const tq_params &p);
+    void set_quant(const tq_quant &qq);
+    void set_sinogram(int slice, int node, const float *d, long long len, bool on_device);
+    void run(int iters, cudaStream_t user);
+    void get_image(int slice, int node, float *out, long long len, bool on_device);
+    void export_state(int slice, int node, double *buf, long long len);
+    void import_state(int slice, int node, const double *buf, long long len);
+    void export_labels(int slice, int node, int32_t *buf, long long len);
+    long long launch_component(int component, int reps, cudaStream_t s);
+    float *sino_stage = nullptr;   // persistent device staging for tq_set_sinogram
+    long long sino_stage_len = 0;
+    int *row_map = nullptr;        // persistent gather indices
+    long long row_map_len = 0;
+
+   private:
+    void invalidate();
+    void setup_exchange();
+    void free_exchange();
+    int phase_a(cudaStream_t s);  // inner solves + (Alg. 3) + encode
+    void exchange(cudaStream_t s);
+    int phase_b(cudaStream_t s);  // decode + dual / next b'
+    int prepare_rhs(cudaStream_t s);
+    void *dev_alloc(size_t bytes);
+    int local(int slice, int node) const;
+};
+
+}  // namespace tq

@@ -1,0 +1,170 @@
+// solver.cu -- see solver.cuh.
+#include <math.h>
+
+#include "solver.cuh"
+
+namespace tq {
+
+void DevGeom::init(int N_, int n_ang_, int n_det_) {
+    N = N_; n_ang = n_ang_; n_det = n_det_;
+    n = (long long)N * N;
+    std::vector<AngleHost> a = make_angles(n_ang);
+    std::vector<double2> t(n_ang);
+    std::vector<int> xm(n_ang);
+    for (int i = 0; i < n_ang; i++) {
+        t[i] = make_double2(a[i].cs, a[i].sn);
+        xm[i] = a[i].xmajor;
+    }
+    TQ_CHECK_CUDA(cudaMalloc(&trig, sizeof(double2) * n_ang));
+    TQ_CHECK_CUDA(cudaMalloc(&xmaj, sizeof(int) * n_ang));
+    TQ_CHECK_CUDA(cudaMemcpy(trig, t.data(), sizeof(double2) * n_ang, cudaMemcpyHostToDevice));
+    TQ_CHECK_CUDA(cudaMemcpy(xmaj, xm.data(), sizeof(int) * n_ang, cudaMemcpyHostToDevice));
+}
+
+void DevGeom::release() {
+    if (trig) cudaFree(trig);
+    if (xmaj) cudaFree(xmaj);
+    trig = nullptr; xmaj = nullptr;
+}
+
+void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>> &angles) {
+    prec = prec_;
+    L = (int)angles.size();
+    n = g.n;
+    rows_h.clear(); row0_h.clear(); nang_h.clear();
+    for (int i = 0; i < L; i++) {
+        row0_h.push_back((int)rows_h.size());
+        nang_h.push_back((int)angles[i].size());
+        for (size_t k = 0; k < angles[i].size(); k++) rows_h.push_back(RayRow{i, angles[i][k], (int)k, 0});
+    }
+    n_rows = (int)rows_h.size();
+    sp = g.n_det + 2;
+    part_stride = std::max(bp_tiles(g.N), vec_blocks(n));
+    const size_t es = esize();
+    auto A = [&](void **p, size_t bytes) {
+        TQ_CHECK_CUDA(cudaMalloc(p, std::max<size_t>(bytes, 16)));
+        TQ_CHECK_CUDA(cudaMemset(*p, 0, std::max<size_t>(bytes, 16)));
+    };
+    A((void **)&rows, sizeof(RayRow) * n_rows);
+    A((void **)&row0, sizeof(int) * L);
+    A((void **)&nang, sizeof(int) * L);
+    TQ_CHECK_CUDA(cudaMemcpy(rows, rows_h.data(), sizeof(RayRow) * n_rows, cudaMemcpyHostToDevice));
+    TQ_CHECK_CUDA(cudaMemcpy(row0, row0_h.data(), sizeof(int) * L, cudaMemcpyHostToDevice));
+    TQ_CHECK_CUDA(cudaMemcpy(nang, nang_h.data(), sizeof(int) * L, cudaMemcpyHostToDevice));
+    for (void **v : {&X, &R, &P, &Q, &BP}) A(v, es * n * L);
+    A(&D, es * (size_t)n_rows * g.n_det);
+    A(&S, es * (size_t)n_rows * sp);
+    A((void **)&cnode, sizeof(double) * L);
+    A((void **)&eta, sizeof(double) * L);
+    A((void **)&scal, sizeof(double) * S_NSLOT * L);
+    A((void **)&partial, sizeof(double) * (size_t)part_stride * L);
+    A((void **)&counter, sizeof(unsigned) * L);
+}
+
+void Inner::release() {
+    for (void *p : {(void *)rows, (void *)row0, (void *)nang, X, R, P, Q, BP, D, S, (void *)cnode,
+                    (void *)eta, (void *)scal, (void *)partial, (void *)counter})
+        if (p) cudaFree(p);
+    rows = nullptr; row0 = nang = nullptr;
+    X = R = P = Q = BP = D = S = nullptr;
+    cnode = eta = scal = partial = nullptr;
+    counter = nullptr;
+}
+
+int Inner::project(const DevGeom &g, const void *img, bool resid, cudaStream_t st) {
+    if (prec == 0) {
+        FpArgs<float> a{(const float *)img, (const float *)D, (float *)S, rows, g.trig, g.xmaj,
+                        g.N, g.n_det, sp, 1, n};
+        launch_fp(0, resid, &a, n_rows, g.n_det, st);
+    } else {
+        FpArgs<double> a{(const double *)img, (const double *)D, (double *)S, rows, g.trig, g.xmaj,
+                         g.N, g.n_det, sp, 1, n};
+        launch_fp(1, resid, &a, n_rows, g.n_det, st);
+    }
+    return 1;
+}
+
+int Inner::backproject(const DevGeom &g, int epi, void *out, void *out2, const void *vin, cudaStream_t st) {
+    if (prec == 0) {
+        BpArgs<float> a{(const float *)S, sp, 1, row0, nang, rows, g.trig, g.xmaj, g.N, g.n_det, n,
+                        (float *)out, (float *)out2, (const float *)vin, (const float *)BP, cnode, eta,
+                        partial, counter, scal, part_stride};
+        launch_bp(0, epi, &a, L, g.N, st);
+    } else {
+        BpArgs<double> a{(const double *)S, sp, 1, row0, nang, rows, g.trig, g.xmaj, g.N, g.n_det, n,
+                         (double *)out, (double *)out2, (const double *)vin, (const double *)BP, cnode,
+                         eta, partial, counter, scal, part_stride};
+        launch_bp(1, epi, &a, L, g.N, st);
+    }
+    return 1;
+}
+
+// CG on (A^T A + c I) x = A^T d + b' from the warm start X (R-8):
+// r0 = A^T(d - A x) + b' - c x (sinogram-space residual), then E1 steps.
+int Inner::cg(const DevGeom &g, int e1, cudaStream_t st) {
+    int k = 0;
+    k += project(g, X, true, st);
+    k += backproject(g, EPI_RESID, R, P, X, st);
+    for (int it = 0; it < e1; it++) {
+        k += project(g, P, false, st);
+        k += backproject(g, EPI_CGQ, Q, nullptr, P, st);
+        launch_cg_update_xr(prec, X, R, P, Q, n, L, scal, partial, part_stride, counter, st);
+        k++;
+        if (it + 1 < e1) {  // the last search direction is never used
+            launch_cg_update_p(prec, P, R, n, L, scal, st);
+            k++;
+        }
+    }
+    return k;
+}
+
+// Alg. 2: x <- x - eta (A^T(A x - d) + c x - b'), E1 times
+int Inner::gd(const DevGeom &g, int e1, cudaStream_t st) {
+    int k = 0;
+    for (int it = 0; it < e1; it++) {
+        k += project(g, X, true, st);
+        k += backproject(g, EPI_GD, X, nullptr, X, st);
+    }
+    return k;
+}
+
+int Inner::norm2(cudaStream_t st) {
+    launch_norm2(prec, X, n, L, scal, partial, part_stride, counter, st);
+    return 1;
+}
+
+// ---------------------------------------------------------------- host geometry
+std::vector<AngleHost> make_angles(int n_ang) {
+    std::vector<AngleHost> a(n_ang);
+    for (int i = 0; i < n_ang; i++) {
+        const double th = M_PI * (double)i / (double)n_ang;
+        a[i].cs = cos(th);
+        a[i].sn = sin(th);
+        a[i].xmajor = (4 * i >= n_ang && 4 * i <= 3 * n_ang) ? 1 : 0;
+        a[i].m = a[i].xmajor ? fabs(a[i].sn) : fabs(a[i].cs);
+    }
+    return a;
+}
+
+void partition_angles(int n_ang, int M, int split, std::vector<int> &off, std::vector<int> &idx) {
+    off.assign(M + 1, 0);
+    idx.clear();
+    for (int m = 0; m < M; m++) {
+        if (split == TQ_SPLIT_CONTIGUOUS) {
+            const int base = n_ang / M, rem = n_ang % M;
+            const int start = m * base + std::min(m, rem), cnt = base + (m < rem ? 1 : 0);
+            for (int k = 0; k < cnt; k++) idx.push_back(start + k);
+        } else {
+            for (int a = m; a < n_ang; a += M) idx.push_back(a);
+        }
+        off[m + 1] = (int)idx.size();
+    }
+}
+
+void partition_rows(int N, int M, std::vector<int> &row_off) {
+    row_off.assign(M + 1, 0);
+    const int base = N / M, rem = N % M;
+    for (int m = 0; m < M; m++) row_off[m + 1] = row_off[m] + base + (m < rem ? 1 : 0);
+}
+
+}  // namespace tq

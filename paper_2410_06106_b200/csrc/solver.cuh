@@ -1,0 +1,50 @@
+// solver.cuh -- device geometry tables and the batched inner solver: every local node
+// i solves min 1/2||A_i x - d_i||^2 + c_i/2 ||x||^2 - b_i'^T x (PAPER.md:158
+// eq:solve_u; R-7) by E1 steps of GD (Alg. 2) or CG (R-8), all
+// nodes of the rank in the same launches.
+#pragma once
+#include "common.cuh"
+#include "projector.cuh"
+#include "vec.cuh"
+
+namespace tq {
+
+// device geometry shared by all nodes of a context
+struct DevGeom {
+    int N = 0, n_ang = 0, n_det = 0;
+    long long n = 0;
+    double2 *trig = nullptr;  // [n_ang]
+    int *xmaj = nullptr;      // [n_ang]
+    void init(int N, int n_ang, int n_det);
+    void release();
+};
+
+struct Inner {
+    int prec = 0, L = 0, n_rows = 0, sp = 0, part_stride = 0;
+    long long n = 0;
+    RayRow *rows = nullptr;    // [n_rows]
+    int *row0 = nullptr;       // [L]
+    int *nang = nullptr;       // [L]
+    void *X = nullptr, *R = nullptr, *P = nullptr, *Q = nullptr, *BP = nullptr;  // [L][n]
+    void *D = nullptr;         // [n_rows][n_det]
+    void *S = nullptr;         // [n_rows][sp], guard column at 0 and n_det+1
+    double *cnode = nullptr, *eta = nullptr;  // [L]
+    double *scal = nullptr;    // [L][S_NSLOT]
+    double *partial = nullptr; // [L][part_stride]
+    unsigned *counter = nullptr;
+    std::vector<RayRow> rows_h;
+    std::vector<int> row0_h, nang_h;
+    // angle lists per local node (global angle ids, increasing)
+    void init(int prec, const DevGeom &g, const std::vector<std::vector<int>> &angles);
+    void release();
+    size_t esize() const { return prec ? 8 : 4; }
+    void *xrow(void *base, int i) const { return (char *)base + esize() * n * i; }
+    // launches; return the number of kernels launched
+    int cg(const DevGeom &g, int e1, cudaStream_t st);
+    int gd(const DevGeom &g, int e1, cudaStream_t st);
+    int norm2(cudaStream_t st);
+    int project(const DevGeom &g, const void *img, bool resid, cudaStream_t st);   // S = (D -) A img
+    int backproject(const DevGeom &g, int epi, void *out, void *out2, const void *vin, cudaStream_t st);
+};
+
+}  // namespace tq

@@ -1,0 +1,160 @@
+"""GPU parity of the single kernels, through the C-ABI, against the fp64 oracle on
+identical seeded inputs: projector / backprojector (relative L2 <= 1e-5 in fp32,
+north_star), one node's inner solve, and the two codecs (DCT bit-exact, K-means
+labels >= 99.99% with dequantized values within 1e-4)."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2410_06106_b200 import synth, tomoq
+from tests.cases import rel
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+TOL = {0: 1e-5, 1: 1e-12}
+DT = {0: torch.float32, 1: torch.float64}
+
+
+def phantom(N, seed, n_e=8, noise=0.05):
+    e = synth.random_ellipses(n_e, N, seed)
+    img = synth.rasterize(e, N, supersample=2)
+    img += noise * np.random.default_rng(seed).standard_normal((N, N))
+    return img
+
+
+def as_input(a, prec):
+    """the exact values both sides see: fp32-rounded for the fp32 path"""
+    return a.astype(np.float32).astype(np.float64) if prec == 0 else a
+
+
+PROJ_CASES = [
+    (64, 90, 91, None),                       # C1 geometry, all angles
+    (64, 90, 91, list(range(0, 23))),         # C1 node 0 (contiguous)
+    (40, 33, 57, [0, 5, 8, 16, 17, 24, 32]),  # ragged tile tails, odd angle count
+    (37, 20, 53, None),                       # N not a multiple of 8 (stateless API allows it)
+    (256, 180, 363, list(range(3, 180, 8))),  # C2 node 3 (round-robin)
+    (8, 4, 13, None),                         # tiny, includes the 45 degree tie
+]
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("N,n_ang,n_det,sel", PROJ_CASES)
+def test_project_backproject_parity(N, n_ang, n_det, sel, prec):
+    img = as_input(phantom(N, N + n_ang), prec)
+    sel_a = np.arange(n_ang) if sel is None else np.asarray(sel)
+    ref = oracle.project(img, n_ang, n_det, sel_a)
+    got = tomoq.project(torch.tensor(img, dtype=DT[prec], device=DEV), n_ang, n_det, sel_a)
+    assert rel(got.cpu().numpy(), ref) <= TOL[prec]
+    y = as_input(np.random.default_rng(N).standard_normal((len(sel_a), n_det)), prec)
+    refb = oracle.backproject(y, N, n_ang, sel_a)
+    gotb = tomoq.backproject(torch.tensor(y, dtype=DT[prec], device=DEV), N, n_ang, sel_a)
+    assert rel(gotb.cpu().numpy(), refb) <= TOL[prec]
+
+
+def test_adjoint_identity_fp32_and_fp64():
+    N, n_ang, n_det = 128, 60, 183
+    rng = np.random.default_rng(9)
+    for prec, tol in ((0, 1e-5), (1, 1e-12)):
+        x = torch.tensor(rng.standard_normal((N, N)), dtype=DT[prec], device=DEV)
+        y = torch.tensor(rng.standard_normal((n_ang, n_det)), dtype=DT[prec], device=DEV)
+        lhs = float((tomoq.project(x, n_ang, n_det) * y).double().sum())
+        rhs = float((x * tomoq.backproject(y, N, n_ang)).double().sum())
+        assert abs(lhs - rhs) <= tol * abs(lhs)
+
+
+@pytest.mark.parametrize("N,n_ang,n_det,sel", [
+    (1024, 90, 1449, [0, 8, 40, 88]),           # C4 (G=1) node 0 sample of its angles
+    (2048, 1500, 2897, [0, 376, 752, 1128]),    # C5 node 0 sample
+])
+def test_projector_full_size_sampled(N, n_ang, n_det, sel):
+    """BASELINE sizes: the oracle computes a sample of the angles in full."""
+    img = as_input(phantom(N, 5, n_e=30), 0)
+    ref = oracle.project(img, n_ang, n_det, sel)
+    timg = torch.tensor(img, dtype=torch.float32, device=DEV)
+    got = tomoq.project(timg, n_ang, n_det, sel)
+    assert rel(got.cpu().numpy(), ref) <= 1e-5
+    y = as_input(ref / ref.max(), 0)
+    refb = oracle.backproject(y, N, n_ang, sel)
+    gotb = tomoq.backproject(torch.tensor(y, dtype=torch.float32, device=DEV), N, n_ang, sel)
+    assert rel(gotb.cpu().numpy(), refb) <= 1e-5
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("inner,e1", [(tomoq.INNER_CG, 5), (tomoq.INNER_GD, 10), (tomoq.INNER_CG, 0)])
+def test_local_solve_parity(prec, inner, e1):
+    N, n_ang, n_det = 128, 90, 183
+    sel = list(range(2, 90, 8))
+    rng = np.random.default_rng(4)
+    truth = phantom(N, 11)
+    d = as_input(oracle.project(truth, n_ang, n_det, sel) + 0.1 * rng.standard_normal((len(sel), n_det)), prec)
+    bp = as_input(rng.standard_normal(N * N) * 0.5, prec)
+    x0 = as_input(truth + 0.1 * rng.standard_normal((N, N)), prec)
+    c, eta = 2.0, 1.0 / (2 * len(sel) * N + 2.0)
+    if inner == tomoq.INNER_CG:
+        ref = oracle.cg(d, bp, c, e1, x0, n_ang, sel)
+    else:
+        ref = oracle.gd(d, bp, c, eta, e1, x0, n_ang, sel)
+    T = lambda a: torch.tensor(a, dtype=DT[prec], device=DEV)
+    got = tomoq.local_solve(T(d), T(bp.reshape(N, N)), c, e1, T(x0), n_ang, sel, inner=inner, eta=eta)
+    assert rel(got.cpu().numpy(), ref) <= (1e-5 if prec == 0 else 1e-11)
+
+
+# ---------------------------------------------------------------- codecs
+def kmeans_input(n, seed):
+    rng = np.random.default_rng(seed)
+    N = int(np.ceil(np.sqrt(n)))
+    img = phantom(max(N, 8), seed, noise=0.02).ravel()[:n]
+    return (img + 1e-3 * rng.standard_normal(n)).astype(np.float32)
+
+
+@pytest.mark.parametrize("n,K,iters", [(5, 2, 10), (1000, 1, 3), (1000, 16, 10), (65536, 16, 10),
+                                       (65537, 64, 10), (4099, 3, 0), (1 << 20, 64, 10),
+                                       (20000, 100, 5), (3000, 256, 4)])
+def test_kmeans_parity(n, K, iters):
+    v = kmeans_input(n, n + K)
+    cen_r, lab_r = oracle.kmeans_encode(v, K, iters)
+    cen, planes, lab = tomoq.kmeans_encode(torch.tensor(v, device=DEV), K, iters)
+    lab = lab.cpu().numpy()
+    assert np.mean(lab == lab_r) >= 0.9999
+    assert np.max(np.abs(cen.cpu().numpy() - cen_r)) <= 1e-4 * max(1.0, np.abs(v).max())
+    dec = tomoq.kmeans_decode(cen, planes, n, K).cpu().numpy()
+    assert np.array_equal(dec, cen.cpu().numpy()[lab])  # bit-planes carry exactly the labels
+    assert np.max(np.abs(dec - oracle.kmeans_decode(cen_r, lab_r))[lab == lab_r]) <= 1e-4
+
+
+def test_kmeans_spec_example_and_edges():
+    cen, planes, lab = tomoq.kmeans_encode(torch.tensor([0, 0, 1, 1, 10], dtype=torch.float32, device=DEV), 2, 10)
+    assert sorted(cen.cpu().tolist()) == [0.5, 10.0]
+    assert tomoq.kmeans_decode(cen, planes, 5, 2).cpu().tolist() == [0.5, 0.5, 0.5, 0.5, 10.0]
+    const = torch.full((777,), 2.5, device=DEV)
+    cen, planes, lab = tomoq.kmeans_encode(const, 8, 10)
+    assert np.all(tomoq.kmeans_decode(cen, planes, 777, 8).cpu().numpy() == 2.5)
+    neg = torch.tensor(-np.abs(kmeans_input(3333, 1)) - 5, device=DEV)
+    cr, lr = oracle.kmeans_encode(neg.cpu().numpy(), 7, 6)
+    c, p, l = tomoq.kmeans_encode(neg, 7, 6)
+    assert np.mean(l.cpu().numpy() == lr) >= 0.9999
+
+
+@pytest.mark.parametrize("rows,cols", [(8, 8), (64, 64), (16, 512), (512, 512), (256, 64)])
+@pytest.mark.parametrize("q", [1, 25, 50, 75, 100])
+def test_dct_bit_exact(rows, cols, q):
+    v = (phantom(max(rows, cols), rows + q, noise=0.03)[:rows, :cols] * 3 - 1).astype(np.float32)
+    coef_r, mm_r = oracle.dct_encode(v, q)
+    coef, mm = tomoq.dct_encode(torch.tensor(v, device=DEV), q)
+    assert np.array_equal(mm.cpu().numpy(), mm_r)
+    assert np.array_equal(coef.cpu().numpy(), coef_r)
+    dec_r = oracle.dct_decode(coef_r, mm_r, rows, cols, q)
+    dec = tomoq.dct_decode(coef, mm, rows, cols, q).cpu().numpy()
+    assert np.array_equal(dec, dec_r)
+
+
+def test_dct_constant_and_extremes():
+    v = np.full((16, 16), -3.5, np.float32)
+    coef, mm = tomoq.dct_encode(torch.tensor(v, device=DEV), 50)
+    assert not torch.any(coef) and np.all(tomoq.dct_decode(coef, mm, 16, 16, 50).cpu().numpy() == -3.5)
+    v = np.zeros((8, 16), np.float32)
+    v[0, 0], v[7, 15] = -1e30, 1e30
+    coef_r, mm_r = oracle.dct_encode(v, 75)
+    coef, mm = tomoq.dct_encode(torch.tensor(v, device=DEV), 75)
+    assert np.array_equal(coef.cpu().numpy(), coef_r)
