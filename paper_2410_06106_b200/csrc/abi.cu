@@ -235,21 +235,12 @@ tq_status tq_project(const tq_geometry *g, const int32_t *sel, int32_t n_sel, co
         std::vector<int> s = check_sel(g, sel, n_sel);
         DevGeom geo;
         geo.init(g->image_side, g->n_angles, g->n_det);
-        DevTmp t;
-        std::vector<RayRow> rows;
-        for (int k = 0; k < n_sel; k++) rows.push_back(RayRow{0, s[k], k, 0});
-        RayRow *rd = t.up(rows.data(), rows.size());
+        Inner in;
+        in.init(precision, geo, {s});
         cudaStream_t st = (cudaStream_t)stream;
-        if (precision == 0) {
-            FpArgs<float> a{(const float *)img, nullptr, (float *)sino, rd, geo.trig, geo.xmaj,
-                            g->image_side, g->n_det, g->n_det, 0, geo.n};
-            launch_fp(0, false, &a, n_sel, g->n_det, st);
-        } else {
-            FpArgs<double> a{(const double *)img, nullptr, (double *)sino, rd, geo.trig, geo.xmaj,
-                             g->image_side, g->n_det, g->n_det, 0, geo.n};
-            launch_fp(1, false, &a, n_sel, g->n_det, st);
-        }
+        in.project(geo, img, false, st, sino, g->n_det, 0);
         TQ_CHECK_CUDA(cudaStreamSynchronize(st));
+        in.release();
         geo.release();
     });
 }
@@ -273,13 +264,13 @@ tq_status tq_backproject(const tq_geometry *g, const int32_t *sel, int32_t n_sel
             BpArgs<float> a{};
             a.s = (const float *)sino; a.s_stride = g->n_det; a.s_off = 0;
             a.node_row0 = row0; a.node_nang = nang; a.rows = rd; a.trig = geo.trig; a.xmaj = geo.xmaj;
-            a.N = g->image_side; a.n_det = g->n_det; a.n = geo.n; a.out = (float *)img;
+            a.N = g->image_side; a.n_det = g->n_det; a.n = geo.n; a.out = (float *)img; a.magic = kMagicBits4;
             launch_bp(0, EPI_PLAIN, &a, 1, g->image_side, st);
         } else {
             BpArgs<double> a{};
             a.s = (const double *)sino; a.s_stride = g->n_det; a.s_off = 0;
             a.node_row0 = row0; a.node_nang = nang; a.rows = rd; a.trig = geo.trig; a.xmaj = geo.xmaj;
-            a.N = g->image_side; a.n_det = g->n_det; a.n = geo.n; a.out = (double *)img;
+            a.N = g->image_side; a.n_det = g->n_det; a.n = geo.n; a.out = (double *)img; a.magic = kMagicBits4;
             launch_bp(1, EPI_PLAIN, &a, 1, g->image_side, st);
         }
         TQ_CHECK_CUDA(cudaStreamSynchronize(st));

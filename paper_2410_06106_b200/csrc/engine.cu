@@ -632,7 +632,8 @@ void Ctx::run(int iters, cudaStream_t user) {
             if (a_part) c += phase_a(s);
             if (b_part) c += phase_b(s);
         } catch (...) {
-            cudaStreamEndCapture(s, &g);
+            if (cudaStreamEndCapture(s, &g) == cudaSuccess && g) cudaGraphDestroy(g);
+            (void)cudaGetLastError();  // do not leave the capture failure as the sticky last error
             throw;
         }
         TQ_CHECK_CUDA(cudaStreamEndCapture(s, &g));

@@ -5,10 +5,16 @@ namespace tq {
 
 namespace {
 
-constexpr int FP_THREADS = 128;   // consecutive bins of one (node, angle)
-constexpr int BP_TX = 32, BP_TY = 8, BP_PX = 2;  // tile = (32*PX) x 8 pixels
-constexpr int BP_THREADS = BP_TX * BP_TY;
-constexpr int BP_MAXA = 128;      // angles staged per smem chunk
+// ------------------------------------------------------------------ shared helpers
+constexpr int FP_HALO_A = (FP_HALO + 3) / 4 * 4;          // 16-byte aligned halo (40)
+constexpr int FP_PITCH_Y = FP_TW + 2 * FP_HALO_A;        // 208: rows of the wide tile, float4 stores
+constexpr int FP_PITCH_X = FP_TW + 2 * FP_HALO_A + 1;    // 209: odd, conflict-free transposed stores
+static_assert(FP_PITCH_Y % 4 == 0, "row pitch must keep 16-byte alignment");
+
+constexpr int BP_TS = 64;       // backprojector pixel tile side
+constexpr int BP_THREADS = 256;
+constexpr int BP_WB = 96;       // staged bins per angle: >= 63(|cos|+|sin|) + 4
+constexpr int BP_MAXA = 64;     // angles per staged batch
 
 template <typename T>
 __device__ __forceinline__ T floor_split(T x, int &i);
@@ -16,178 +22,364 @@ template <>
 __device__ __forceinline__ float floor_split<float>(float x, int &i) { return floor_pos(x, i); }
 template <>
 __device__ __forceinline__ double floor_split<double>(double x, int &i) {
-    double f = floor(x);
+    const double f = floor(x);
     i = (int)f;
     return f;
 }
 
-// Range of lines l in [0, N) where the ray's fractional index f0 + l df lies in
-// (-1, N) (outside it both taps are off the grid).  Conservative by one line.
-__device__ __forceinline__ void line_range(double f0, double df, int N, int &lo, int &hi) {
-    if (fabs(df) < 1e-12) {
-        if (f0 > -1.0 && f0 < (double)N) { lo = 0; hi = N; } else { lo = 0; hi = 0; }
-        return;
+template <typename T>
+__device__ __forceinline__ T sat(T x);
+template <>
+__device__ __forceinline__ float sat<float>(float x) { return __saturatef(x); }
+template <>
+__device__ __forceinline__ double sat<double>(double x) { return fmin(fmax(x, 0.0), 1.0); }
+
+// Ray geometry along the major axis (R-1/R-2, the ray-driven form of the
+// oracle's or_project): on major-axis line l (row for y-major, column for x-major)
+// the ray (theta, t) sits at fractional cross index  a0 + t*at + l*B.
+struct LineGeo {
+    double a0, at, B, inv_m;
+};
+__device__ __forceinline__ LineGeo line_geo(double cs, double sn, int xmajor, int N) {
+    const double h = 0.5 * (double)(N - 1);
+    LineGeo g;
+    if (!xmajor) {  // column on row r: (t - y_r sin)/cos + h, y_r = h - r
+        g.at = 1.0 / cs; g.a0 = h - h * sn / cs; g.B = sn / cs; g.inv_m = 1.0 / fabs(cs);
+    } else {        // row on column c: h - (t - x_c cos)/sin, x_c = c - h
+        g.at = -1.0 / sn; g.a0 = h - h * cs / sn; g.B = cs / sn; g.inv_m = 1.0 / fabs(sn);
     }
-    double a = (-1.0 - f0) / df, b = ((double)N - f0) / df;
-    double l0 = fmin(a, b), l1 = fmax(a, b);
-    lo = (int)fmax(0.0, floor(l0) - 1.0);
-    hi = (int)fmin((double)N, ceil(l1) + 2.0);
-    if (hi < lo) hi = lo;
+    return g;
 }
 
-template <typename T, bool RESID>
-__global__ void __launch_bounds__(FP_THREADS) fp_kernel(const FpArgs<T> a) {
-    const RayRow rr = a.rows[blockIdx.y];
-    const int j = blockIdx.x * FP_THREADS + threadIdx.x;
-    if (j >= a.n_det) return;
-    const int N = a.N;
-    const T *__restrict__ img = a.img + (long long)rr.node * a.n;
-    const double2 cs_sn = a.trig[rr.angle];
-    const double cs = cs_sn.x, sn = cs_sn.y;
-    const bool xm = a.xmaj[rr.angle] != 0;
-    const double half = 0.5 * (double)(N - 1);
-    const double t = (double)j - 0.5 * (double)(a.n_det - 1);
-    // fractional index of the ray on line l: y-major -> column on row l,
-    // x-major -> row on column l (R-1 ray-driven form)
-    double f0, df, inv_m;
-    if (!xm) { f0 = (t - half * sn) / cs + half; df = sn / cs; inv_m = 1.0 / fabs(cs); }
-    else     { f0 = half - (t + half * cs) / sn; df = cs / sn; inv_m = 1.0 / fabs(sn); }
-    int lo, hi;
-    line_range(f0, df, N, lo, hi);
-    const T dfT = (T)df;
-    T acc0 = 0, acc1 = 0;
-    for (int L0 = lo; L0 < hi; L0 += 32) {
-        const double b = f0 + (double)L0 * df;
-        const int bi = (int)floor(b) - 64;
-        const T bf = (T)(b - (double)bi);          // in [64, 65)
-        const int cnt = min(32, hi - L0);
-        if (!xm) {
-            const T *rowp = img + (long long)L0 * N;
-#pragma unroll 4
-            for (int l = 0; l < cnt; l++, rowp += N) {
-                int i0;
-                const T cl = bf + (T)l * dfT;
-                const T fl = floor_split<T>(cl, i0);
-                i0 += bi;
-                const T f = cl - fl;
-                const T v0 = ((unsigned)i0 < (unsigned)N) ? __ldg(rowp + i0) : (T)0;
-                const T v1 = ((unsigned)(i0 + 1) < (unsigned)N) ? __ldg(rowp + i0 + 1) : (T)0;
-                if (l & 1) acc1 += v0 + f * (v1 - v0); else acc0 += v0 + f * (v1 - v0);
-            }
-        } else {
-            const T *colp = img + L0;
-#pragma unroll 4
-            for (int l = 0; l < cnt; l++, colp++) {
-                int i0;
-                const T cl = bf + (T)l * dfT;
-                const T fl = floor_split<T>(cl, i0);
-                i0 += bi;
-                const T f = cl - fl;
-                const T v0 = ((unsigned)i0 < (unsigned)N) ? __ldg(colp + (long long)i0 * N) : (T)0;
-                const T v1 = ((unsigned)(i0 + 1) < (unsigned)N) ? __ldg(colp + (long long)(i0 + 1) * N) : (T)0;
-                if (l & 1) acc1 += v0 + f * (v1 - v0); else acc0 += v0 + f * (v1 - v0);
-            }
-        }
-    }
-    T v = (acc0 + acc1) * (T)inv_m;
-    const long long o = (long long)blockIdx.y * a.out_stride + a.out_off + j;
-    if (RESID) v = a.d[(long long)blockIdx.y * a.n_det + j] - v;
-    a.out[o] = v;
+// Shared-memory load at a 32-bit shared address + immediate byte offset.  The
+// fp32 fast paths below index with the float bits of (x + 2^23) directly:
+// addr = (bits << 2) + base - (0x4B000000 << 2), so one LEA forms the address of
+// floor(x) and both taps use immediate offsets.
+template <int OFF>
+__device__ __forceinline__ float lds(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(OFF));
+    return v;
+}
+constexpr uint32_t MAGIC_BITS4 = 0x4B000000u << 2;  // wraps mod 2^32 (intended)
+// shared base minus MAGIC_BITS4.  `magic` is MAGIC_BITS4 passed as a kernel argument,
+// so ptxas cannot split the constant back out of the base register and re-add it
+// before every load (it does that when it can see the constant).
+__device__ __forceinline__ uint32_t magic_base(const void *smem_ptr, uint32_t magic) {
+    return (uint32_t)__cvta_generic_to_shared(smem_ptr) - magic;
 }
 
 template <typename T>
-struct AngleRec {
-    T base_f, cs, sn, inv_m, inv_m2, w1c;  // w1c = inv_m - inv_m2
-    int base_i, row;
+struct V16;  // 16-byte vector of T
+template <>
+struct V16<float> {
+    using type = float4;
+    static constexpr int n = 4;
+};
+template <>
+struct V16<double> {
+    using type = double2;
+    static constexpr int n = 2;
 };
 
+// ------------------------------------------------------------------ forward: tile pass
+template <typename T, int O>  // O = 0: y-major angles (lines = rows), 1: x-major (lines = columns)
+__global__ void __launch_bounds__(FP_THREADS) fp_tile_kernel(const FpArgs<T> a) {
+    constexpr int PITCH = O == 0 ? FP_PITCH_Y : FP_PITCH_X;
+    constexpr int H = FP_HALO_A;
+    extern __shared__ __align__(16) unsigned char fp_smem[];
+    T *tile = reinterpret_cast<T *>(fp_smem);  // [FP_TH][PITCH]
+    __shared__ double s_kap[FP_MAXA], s_at[FP_MAXA];
+    __shared__ T s_B[FP_MAXA];
+    __shared__ int s_row[FP_MAXA], s_W[FP_MAXA], s_cofs[FP_MAXA + 1];
+
+    const int node = blockIdx.y;
+    const int grp = 2 * node + O;
+    const int a_begin = a.oofs[grp], a_end = a.oofs[grp + 1];
+    if (a_begin == a_end) return;  // uniform over the block
+    const int N = a.N;
+    const int tile_id = blockIdx.x;
+    const int ntiles = a.nt_line * a.nt_cross;
+    const int lt = tile_id / a.nt_cross, ct = tile_id % a.nt_cross;
+    const int L0 = lt * FP_TH, X0 = ct * FP_TW;
+    const T *img = a.img + (long long)node * a.n;
+
+    // ---- stage the tile: tile[l][k] = image at (line L0+l, cross X0-H+k); zero outside
+    for (int i = threadIdx.x; i < FP_TH * (PITCH - FP_TW); i += FP_THREADS) {
+        const int l = i / (PITCH - FP_TW), k = i % (PITCH - FP_TW);
+        tile[l * PITCH + (k < H ? k : k + FP_TW)] = (T)0;
+    }
+    using VT = typename V16<T>::type;
+    constexpr int VN = V16<T>::n;
+    if (N % VN != 0) {  // rows not 16-byte aligned (odd N, stateless calls only): scalar staging
+        for (int i = threadIdx.x; i < FP_TH * FP_TW; i += FP_THREADS) {
+            const int l = i / FP_TW, x = i % FP_TW;
+            const int r = O == 0 ? L0 + l : X0 + x, c = O == 0 ? X0 + x : L0 + l;
+            tile[l * PITCH + H + x] = (r < N && c < N && L0 + l < N && X0 + x < N) ? img[(long long)r * N + c] : (T)0;
+        }
+    } else if (O == 0) {  // rows of the image: 16-byte loads along the row, 16-byte stores
+        constexpr int VPL = FP_TW / VN;
+        for (int i = threadIdx.x; i < FP_TH * VPL; i += FP_THREADS) {
+            const int l = i / VPL, q = i % VPL;
+            const int r = L0 + l, c = X0 + q * VN;
+            VT v;
+            if (r < N && c < N) v = __ldg(reinterpret_cast<const VT *>(img + (long long)r * N + c));
+            else memset(&v, 0, sizeof(v));
+            *reinterpret_cast<VT *>(tile + l * PITCH + H + q * VN) = v;
+        }
+    } else {  // columns of the image: a warp reads 16-byte pieces of consecutive rows
+        constexpr int VPR = FP_TH / VN;
+        for (int i = threadIdx.x; i < FP_TW * VPR; i += FP_THREADS) {
+            const int y = i / VPR, q = i % VPR;
+            const int r = X0 + y, c = L0 + q * VN;
+            VT v;
+            if (r < N && c < N) v = __ldg(reinterpret_cast<const VT *>(img + (long long)r * N + c));
+            else memset(&v, 0, sizeof(v));
+            const T *e = reinterpret_cast<const T *>(&v);
+#pragma unroll
+            for (int u = 0; u < VN; u++) tile[(q * VN + u) * PITCH + H + y] = e[u];
+        }
+    }
+
+    const double c0 = 0.5 * (double)(a.n_det - 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int b0 = a_begin; b0 < a_end; b0 += FP_MAXA) {
+        const int nb = min(FP_MAXA, a_end - b0);
+        __syncthreads();  // tile staged / previous batch consumed
+        // ---- rays of each angle that cross the tile: window [jlo, jlo + W)
+        for (int k = threadIdx.x; k < nb; k += FP_THREADS) {
+            const int row = a.olist[b0 + k];
+            const double2 t2 = a.trig[a.rows[row].angle];
+            const LineGeo G = line_geo(t2.x, t2.y, O, N);
+            const double l1 = (double)(min(L0 + FP_TH, N) - 1);
+            const double bA = (double)L0 * G.B, bB = l1 * G.B;
+            // cross over the tile's lines must meet (X0 - 1, X0 + TW): t*at in (lo, hi)
+            const double lo = (double)(X0 - 1) - fmax(bA, bB) - G.a0;
+            const double hi = (double)(X0 + FP_TW) - fmin(bA, bB) - G.a0;
+            double tl = lo / G.at, th = hi / G.at;
+            if (tl > th) { const double x = tl; tl = th; th = x; }
+            const int jlo = max(0, (int)floor(tl + c0) - 1);
+            const int jhi = min(a.n_det, (int)ceil(th + c0) + 2);
+            const int W = max(0, jhi - jlo);
+            s_row[k] = row;
+            s_W[k] = W;
+            s_at[k] = G.at;
+            s_B[k] = (T)G.B;
+            // smem cross coordinate of ray jlo on the tile's first line
+            s_kap[k] = G.a0 + ((double)jlo - c0) * G.at + (double)L0 * G.B - (double)(X0 - H);
+            a.win[(long long)row * ntiles + tile_id] = make_int2(jlo, W);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int acc = 0;
+            for (int k = 0; k < nb; k++) {
+                s_cofs[k] = acc;
+                acc += (s_W[k] + 31) >> 5;
+            }
+            s_cofs[nb] = acc;
+        }
+        __syncthreads();
+        const int nitems = s_cofs[nb];
+        // ---- one warp item = 32 consecutive rays of one angle over the tile's TH lines
+        for (int it = warp; it < nitems; it += FP_THREADS / 32) {
+            int lo = 0, hi = nb - 1;  // largest k with s_cofs[k] <= it
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_cofs[mid] <= it) lo = mid; else hi = mid - 1;
+            }
+            const int k = lo;
+            const int W = s_W[k];
+            const int w = (it - s_cofs[k]) * 32 + lane;
+            const int wc = min(w, W - 1);
+            const T kap = (T)(s_kap[k] + (double)wc * s_at[k]);
+            const T B = s_B[k];
+            T acc0 = 0, acc1 = 0;
+            if constexpr (sizeof(T) == 4) {
+                const uint32_t sb = magic_base(tile, a.magic);
+#pragma unroll
+                for (int l = 0; l < FP_TH; l++) {
+                    const float kf = fmaf((float)l, B, kap);
+                    const float m = __fadd_rd(kf, 8388608.0f);     // 2^23 + floor(kf)
+                    const uint32_t ad = (__float_as_uint(m) << 2) + sb;
+                    const float v0 = lds<0>(ad + l * PITCH * 4), v1 = lds<4>(ad + l * PITCH * 4);
+                    const float f = kf - (m - 8388608.0f);
+                    acc0 += v0;
+                    acc1 = fmaf(f, v1 - v0, acc1);
+                }
+            } else {
+#pragma unroll
+                for (int l = 0; l < FP_TH; l++) {
+                    const T kf = fma((T)l, B, kap);
+                    int i0;
+                    const T fl = floor_split<T>(kf, i0);
+                    const T f = kf - fl;
+                    const T *p = tile + l * PITCH + i0;
+                    const T v0 = p[0], v1 = p[1];
+                    acc0 += v0;
+                    acc1 = fma(f, v1 - v0, acc1);
+                }
+            }
+            if (w < W) a.partial[((long long)s_row[k] * ntiles + tile_id) * FP_WMAX + w] = acc0 + acc1;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ forward: reduction
+// s[row][j] = (1/m) * sum over the tiles the ray crosses (line bands in order, then
+// cross tiles in order) of the tile partials; RESID: s = d - A x.
+template <typename T, bool RESID>
+__global__ void __launch_bounds__(128) fp_reduce_kernel(const FpRedArgs<T> a) {
+    const int row = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= a.n_det) return;
+    const RayRow rr = a.rows[row];
+    const double2 t2 = a.trig[rr.angle];
+    const LineGeo G = line_geo(t2.x, t2.y, a.xmaj[rr.angle], a.N);
+    const double base = G.a0 + ((double)j - 0.5 * (double)(a.n_det - 1)) * G.at;
+    const int ntiles = a.nt_line * a.nt_cross;
+    const long long rbase = (long long)row * ntiles;
+    double acc = 0.0;
+    for (int lt = 0; lt < a.nt_line; lt++) {
+        const int L0 = lt * FP_TH, L1 = min(L0 + FP_TH, a.N) - 1;
+        const double cA = base + (double)L0 * G.B, cB = base + (double)L1 * G.B;
+        const double cmin = fmin(cA, cB) - 3.0, cmax = fmax(cA, cB) + 3.0;
+        if (cmax < 0.0 || cmin > (double)a.N) continue;
+        const int ct0 = max(0, (int)floor(cmin / FP_TW));
+        const int ct1 = min(a.nt_cross - 1, (int)floor(cmax / FP_TW));
+        for (int ct = ct0; ct <= ct1; ct++) {
+            const int tile = lt * a.nt_cross + ct;
+            const int2 w = a.win[rbase + tile];
+            const int jj = j - w.x;
+            if (jj >= 0 && jj < w.y) acc += (double)a.partial[(rbase + tile) * FP_WMAX + jj];
+        }
+    }
+    T v = (T)(acc * G.inv_m);
+    if (RESID) v = a.d[(long long)row * a.n_det + j] - v;
+    a.out[(long long)row * a.out_stride + a.out_off + j] = v;
+}
+
+// ------------------------------------------------------------------ backprojector
 template <typename T, int EPI>
-__global__ void __launch_bounds__(BP_THREADS) bp_kernel(const BpArgs<T> a) {
-    __shared__ AngleRec<T> tab[BP_MAXA];
+__global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char bp_smem[];
+    T *win = reinterpret_cast<T *>(bp_smem);  // [BP_MAXA][BP_WB], bins pre-scaled by 1/m
+    __shared__ double s_tau[BP_MAXA], s_csd[BP_MAXA], s_snd[BP_MAXA];
+    __shared__ T s_cs[BP_MAXA], s_sn[BP_MAXA], s_im[BP_MAXA];
+    __shared__ int s_jlo[BP_MAXA];
     __shared__ double red[BP_THREADS / 32 + 1];
     __shared__ bool last_flag;
     const int node = blockIdx.y;
     const int N = a.N;
-    const int tiles_x = (N + BP_TX * BP_PX - 1) / (BP_TX * BP_PX);
-    const int tile_r = blockIdx.x / tiles_x, tile_c = blockIdx.x % tiles_x;
-    const int r0 = tile_r * BP_TY, c0 = tile_c * BP_TX * BP_PX;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const int r = r0 + ty;
-    const double half = 0.5 * (double)(N - 1);
-    // tile reference point (centre of the tile) for the tile-relative t (precision)
-    const double cref = (double)c0 + 0.5 * (BP_TX * BP_PX) , rref = (double)r0;
+    const int tpr = (N + BP_TS - 1) / BP_TS;
+    const int r0 = (blockIdx.x / tpr) * BP_TS, c0 = (blockIdx.x % tpr) * BP_TS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lx = lane & 7, prow = 8 * warp + (lane >> 3);  // pixel (prow + 4 ky, 8 kx + lx)
+    const double h = 0.5 * (double)(N - 1), t0 = -0.5 * (double)(a.n_det - 1);
     const int nang = a.node_nang[node], row0 = a.node_row0[node];
-    T acc[BP_PX];
+    T acc[2][8];
 #pragma unroll
-    for (int i = 0; i < BP_PX; i++) acc[i] = 0;
-    const T dr = (T)(r - r0);
+    for (int ky = 0; ky < 2; ky++)
+#pragma unroll
+        for (int kx = 0; kx < 8; kx++) acc[ky][kx] = 0;
+
     for (int k0 = 0; k0 < nang; k0 += BP_MAXA) {
         const int kc = min(BP_MAXA, nang - k0);
         __syncthreads();
         for (int k = threadIdx.x; k < kc; k += BP_THREADS) {
-            const int row = row0 + k0 + k;
-            const int ang = a.rows[row].angle;
+            const int ang = a.rows[row0 + k0 + k].angle;
             const double2 t2 = a.trig[ang];
-            const double m = a.xmaj[ang] ? fabs(t2.y) : fabs(t2.x);
-            const double base = (cref - half) * t2.x + (half - rref) * t2.y + 0.5 * (double)(a.n_det - 1);
-            const int bi = (int)floor(base) - 48;
-            AngleRec<T> rec;
-            rec.base_f = (T)(base - (double)bi);
-            rec.cs = (T)t2.x;
-            rec.sn = (T)t2.y;
-            rec.inv_m = (T)(1.0 / m);
-            rec.inv_m2 = (T)(1.0 / (m * m));
-            rec.w1c = (T)(1.0 / m - 1.0 / (m * m));
-            rec.base_i = bi;
-            rec.row = row;
-            tab[k] = rec;
+            const double cs = t2.x, sn = t2.y;
+            const double m = a.xmaj[ang] ? fabs(sn) : fabs(cs);
+            const double tp0 = ((double)c0 - h) * cs + (h - (double)r0) * sn;  // t_p of pixel (r0, c0)
+            const double ext = (double)(BP_TS - 1);
+            const double tmin = tp0 + fmin(0.0, ext * cs) + fmin(0.0, -ext * sn);
+            const int jlo = (int)floor(tmin - t0) - 1;  // one bin of margin below
+            s_jlo[k] = jlo;
+            s_tau[k] = tp0 - t0 - (double)jlo;  // tile-relative bin coordinate of pixel (r0, c0)
+            s_csd[k] = cs;
+            s_snd[k] = sn;
+            s_cs[k] = (T)cs;
+            s_sn[k] = (T)sn;
+            s_im[k] = (T)(1.0 / m);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kc * BP_WB; i += BP_THREADS) {
+            const int k = i / BP_WB, w = i - k * BP_WB;
+            const int j = s_jlo[k] + w;
+            T v = 0;
+            if (j >= 0 && j < a.n_det) v = a.s[(long long)(row0 + k0 + k) * a.s_stride + a.s_off + j] * s_im[k];
+            win[i] = v;
         }
         __syncthreads();
         for (int k = 0; k < kc; k++) {
-            const AngleRec<T> rec = tab[k];
-            const T *__restrict__ srow = a.s + (long long)rec.row * a.s_stride + a.s_off;
-            // t of this thread's first pixel relative to the tile reference
-            const T tl0 = rec.base_f + ((T)tx - (T)(0.5 * (BP_TX * BP_PX))) * rec.cs - dr * rec.sn;
+            const T cs = s_cs[k], sn = s_sn[k], im = s_im[k], omi = (T)1 - im;
+            const T tau_t = (T)(s_tau[k] + (double)lx * s_csd[k] - (double)prow * s_snd[k]);
+            if constexpr (sizeof(T) == 4) {
+                const uint32_t wb = magic_base(win + k * BP_WB, a.magic);
 #pragma unroll
-            for (int i = 0; i < BP_PX; i++) {
-                const T tl = tl0 + (T)(BP_TX * i) * rec.cs;
-                int ji;
-                const T fl = floor_split<T>(tl, ji);
-                const T u = tl - fl;
-                const int j = rec.base_i + ji;
-                const T w0 = max((T)0, rec.inv_m - u * rec.inv_m2);
-                const T w1 = max((T)0, rec.w1c + u * rec.inv_m2);
-                acc[i] += w0 * __ldg(srow + j) + w1 * __ldg(srow + j + 1);
+                for (int ky = 0; ky < 2; ky++) {
+                    const float tau_r = fmaf((float)(-4 * ky), sn, tau_t);
+#pragma unroll
+                    for (int kx = 0; kx < 8; kx++) {
+                        const float tau = fmaf((float)(8 * kx), cs, tau_r);
+                        const float m = __fadd_rd(tau, 8388608.0f);   // 2^23 + floor(tau)
+                        const uint32_t ad = (__float_as_uint(m) << 2) + wb;
+                        const float u = tau - (m - 8388608.0f);
+                        const float w0 = __saturatef(fmaf(-u, im, 1.0f));
+                        const float w1 = __saturatef(fmaf(u, im, omi));
+                        acc[ky][kx] = fmaf(w0, lds<0>(ad), acc[ky][kx]);
+                        acc[ky][kx] = fmaf(w1, lds<4>(ad), acc[ky][kx]);
+                    }
+                }
+            } else {
+                const T *wk = win + k * BP_WB;
+#pragma unroll
+                for (int ky = 0; ky < 2; ky++) {
+                    const T tau_r = fma((T)(-4 * ky), sn, tau_t);
+#pragma unroll
+                    for (int kx = 0; kx < 8; kx++) {
+                        const T tau = fma((T)(8 * kx), cs, tau_r);
+                        int i0;
+                        const T fl = floor_split<T>(tau, i0);
+                        const T u = tau - fl;
+                        const T w0 = sat<T>(fma(-u, im, (T)1));
+                        const T w1 = sat<T>(fma(u, im, omi));
+                        acc[ky][kx] = fma(w0, wk[i0], acc[ky][kx]);
+                        acc[ky][kx] = fma(w1, wk[i0 + 1], acc[ky][kx]);
+                    }
+                }
             }
         }
     }
-    // ---------------- epilogue
+    // ---------------- epilogue (fp64 in registers)
     const double c = (EPI == EPI_CGQ || EPI == EPI_RESID || EPI == EPI_GD) ? a.cnode[node] : 0.0;
     double dot = 0.0;
     const long long nb = (long long)node * a.n;
 #pragma unroll
-    for (int i = 0; i < BP_PX; i++) {
-        const int col = c0 + tx + BP_TX * i;
-        if (r >= N || col >= N) continue;
-        const long long p = nb + (long long)r * N + col;
-        const double g = (double)acc[i];
-        if (EPI == EPI_PLAIN) {
-            a.out[p] = acc[i];
-        } else if (EPI == EPI_CGQ) {
-            const double pv = (double)a.vin[p];
-            const T q = (T)(g + c * pv);
-            a.out[p] = q;
-            dot += pv * (double)q;
-        } else if (EPI == EPI_RESID) {
-            const T rv = (T)(g + (double)a.bprime[p] - c * (double)a.vin[p]);
-            a.out[p] = rv;
-            a.out2[p] = rv;
-            dot += (double)rv * (double)rv;
-        } else {  // EPI_GD: x <- x - eta (c x - b' - A^T(d - A x))
-            const double xv = (double)a.vin[p];
-            a.out[p] = (T)(xv - a.eta[node] * (c * xv - (double)a.bprime[p] - g));
+    for (int ky = 0; ky < 2; ky++)
+#pragma unroll
+        for (int kx = 0; kx < 8; kx++) {
+            const int r = r0 + prow + 4 * ky, col = c0 + 8 * kx + lx;
+            if (r >= N || col >= N) continue;
+            const long long p = nb + (long long)r * N + col;
+            const double g = (double)acc[ky][kx];
+            if (EPI == EPI_PLAIN) {
+                a.out[p] = acc[ky][kx];
+            } else if (EPI == EPI_CGQ) {
+                const double pv = (double)a.vin[p];
+                const T q = (T)(g + c * pv);
+                a.out[p] = q;
+                dot += pv * (double)q;
+            } else if (EPI == EPI_RESID) {
+                const T rv = (T)(g + (double)a.bprime[p] - c * (double)a.vin[p]);
+                a.out[p] = rv;
+                a.out2[p] = rv;
+                dot += (double)rv * (double)rv;
+            } else {  // EPI_GD: x <- x - eta (c x - b' - A^T(d - A x))
+                const double xv = (double)a.vin[p];
+                a.out[p] = (T)(xv - a.eta[node] * (c * xv - (double)a.bprime[p] - g));
+            }
         }
-    }
     if (EPI == EPI_CGQ || EPI == EPI_RESID) {
         const double bs = block_sum<BP_THREADS>(dot, red);
         double *part = a.partial + (long long)node * a.part_stride;
@@ -209,42 +401,85 @@ __global__ void __launch_bounds__(BP_THREADS) bp_kernel(const BpArgs<T> a) {
     }
 }
 
-}  // namespace
-
-int bp_tiles(int N) {
-    const int tx = (N + BP_TX * BP_PX - 1) / (BP_TX * BP_PX);
-    const int ty = (N + BP_TY - 1) / BP_TY;
-    return tx * ty;
+template <typename K>
+void set_smem(K kernel, size_t dyn) {
+    TQ_CHECK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
 }
 
-void launch_fp(int prec, bool resid, const void *args, int n_rows, int n_det, cudaStream_t st) {
-    dim3 grid(ceil_div(n_det, FP_THREADS), n_rows);
+template <typename T>
+size_t fp_smem(int o) { return sizeof(T) * FP_TH * (o == 0 ? FP_PITCH_Y : FP_PITCH_X); }
+template <typename T>
+size_t bp_smem() { return sizeof(T) * BP_MAXA * BP_WB; }
+
+template <typename T>
+void set_all_smem() {
+    set_smem(fp_tile_kernel<T, 0>, fp_smem<T>(0));
+    set_smem(fp_tile_kernel<T, 1>, fp_smem<T>(1));
+    set_smem(bp_tile_kernel<T, EPI_PLAIN>, bp_smem<T>());
+    set_smem(bp_tile_kernel<T, EPI_CGQ>, bp_smem<T>());
+    set_smem(bp_tile_kernel<T, EPI_RESID>, bp_smem<T>());
+    set_smem(bp_tile_kernel<T, EPI_GD>, bp_smem<T>());
+}
+
+template <typename T>
+void fp_dispatch(const FpArgs<T> &A, int L, cudaStream_t st) {
+    const dim3 grid(A.nt_line * A.nt_cross, L);
+    fp_tile_kernel<T, 0><<<grid, FP_THREADS, fp_smem<T>(0), st>>>(A);
+    fp_tile_kernel<T, 1><<<grid, FP_THREADS, fp_smem<T>(1), st>>>(A);
+}
+
+template <typename T>
+void bp_dispatch(int epi, const BpArgs<T> &A, dim3 grid, cudaStream_t st) {
+    const size_t sm = bp_smem<T>();
+    switch (epi) {
+        case EPI_PLAIN: bp_tile_kernel<T, EPI_PLAIN><<<grid, BP_THREADS, sm, st>>>(A); break;
+        case EPI_CGQ: bp_tile_kernel<T, EPI_CGQ><<<grid, BP_THREADS, sm, st>>>(A); break;
+        case EPI_RESID: bp_tile_kernel<T, EPI_RESID><<<grid, BP_THREADS, sm, st>>>(A); break;
+        default: bp_tile_kernel<T, EPI_GD><<<grid, BP_THREADS, sm, st>>>(A); break;
+    }
+}
+
+}  // namespace
+
+// Dynamic shared-memory limits of the projector kernels on the current device; called
+// outside stream capture (Inner::init) because cudaFuncSetAttribute is not capturable.
+void projector_setup() {
+    set_all_smem<float>();
+    set_all_smem<double>();
+}
+
+int fp_ntiles(int N) { return ceil_div(N, FP_TH) * ceil_div(N, FP_TW); }
+
+int bp_tiles(int N) {
+    const int t = ceil_div(N, BP_TS);
+    return t * t;
+}
+
+void launch_fp(int prec, const void *args, int L, cudaStream_t st) {
+    if (L == 0) return;
+    if (prec == 0) fp_dispatch<float>(*static_cast<const FpArgs<float> *>(args), L, st);
+    else fp_dispatch<double>(*static_cast<const FpArgs<double> *>(args), L, st);
+    TQ_CHECK_CUDA(cudaGetLastError());
+}
+
+void launch_fp_reduce(int prec, bool resid, const void *args, int n_rows, int n_det, cudaStream_t st) {
     if (n_rows == 0) return;
+    const dim3 grid(ceil_div(n_det, 128), n_rows);
     if (prec == 0) {
-        const auto &A = *static_cast<const FpArgs<float> *>(args);
-        if (resid) fp_kernel<float, true><<<grid, FP_THREADS, 0, st>>>(A);
-        else fp_kernel<float, false><<<grid, FP_THREADS, 0, st>>>(A);
+        const auto &A = *static_cast<const FpRedArgs<float> *>(args);
+        if (resid) fp_reduce_kernel<float, true><<<grid, 128, 0, st>>>(A);
+        else fp_reduce_kernel<float, false><<<grid, 128, 0, st>>>(A);
     } else {
-        const auto &A = *static_cast<const FpArgs<double> *>(args);
-        if (resid) fp_kernel<double, true><<<grid, FP_THREADS, 0, st>>>(A);
-        else fp_kernel<double, false><<<grid, FP_THREADS, 0, st>>>(A);
+        const auto &A = *static_cast<const FpRedArgs<double> *>(args);
+        if (resid) fp_reduce_kernel<double, true><<<grid, 128, 0, st>>>(A);
+        else fp_reduce_kernel<double, false><<<grid, 128, 0, st>>>(A);
     }
     TQ_CHECK_CUDA(cudaGetLastError());
 }
 
-template <typename T>
-static void bp_dispatch(int epi, const BpArgs<T> &A, dim3 grid, cudaStream_t st) {
-    switch (epi) {
-        case EPI_PLAIN: bp_kernel<T, EPI_PLAIN><<<grid, BP_THREADS, 0, st>>>(A); break;
-        case EPI_CGQ: bp_kernel<T, EPI_CGQ><<<grid, BP_THREADS, 0, st>>>(A); break;
-        case EPI_RESID: bp_kernel<T, EPI_RESID><<<grid, BP_THREADS, 0, st>>>(A); break;
-        default: bp_kernel<T, EPI_GD><<<grid, BP_THREADS, 0, st>>>(A); break;
-    }
-}
-
 void launch_bp(int prec, int epi, const void *args, int L, int N, cudaStream_t st) {
     if (L == 0) return;
-    dim3 grid(bp_tiles(N), L);
+    const dim3 grid(bp_tiles(N), L);
     if (prec == 0) bp_dispatch<float>(epi, *static_cast<const BpArgs<float> *>(args), grid, st);
     else bp_dispatch<double>(epi, *static_cast<const BpArgs<double> *>(args), grid, st);
     TQ_CHECK_CUDA(cudaGetLastError());

@@ -1,12 +1,23 @@
-// projector.cuh -- Joseph forward projector A (ray-driven) and matched backprojector
-// A^T (pixel-driven) for sm_100a, with the inner-solver epilogues fused into A^T.
+// projector.cuh -- Joseph forward projector A and matched backprojector A^T for sm_100a,
+// with the inner-solver epilogues fused into A^T.
 //
 // Operator (R-1): P[(a,j),p] = max(0, 1-|t_j-t_p|/m_a)/m_a.
-// Forward: each thread owns one ray (a, j) and walks the N lines of the ray's major
-// axis, interpolating linearly between the two pixels it passes between (2 taps per
-// voxel-update, "VU").  Backward: each thread owns PX pixels and, per angle of its
-// node, gathers the <= 2 bins whose triangle covers the pixel.  No atomics: every
-// output is summed by one thread in a fixed order, so results are deterministic.
+//
+// Forward (A), "image-tile stationary": one CTA stages a TH x TW tile of one node's
+// image in shared memory (zero halo on both sides of the cross axis) and walks, for
+// EVERY angle of that node whose major axis matches the tile orientation, all rays
+// that cross the tile: per line of the tile one bilinear sample (2 taps) from shared
+// memory.  Each ray's partial sum over the tile goes to a scratch buffer; fp_reduce
+// adds the partials of the tiles a ray crosses in a fixed order (deterministic, no
+// atomics) and applies 1/m_a and the residual.  y-major angles walk rows of a wide
+// tile, x-major angles walk columns of a tall tile (the transposed staging), so the
+// rays a tile touches are mostly full-length segments.  Each image pixel is read from
+// HBM/L2 once per orientation per application, for all angles of its node.
+//
+// Backward (A^T), pixel-driven: one CTA owns a 64 x 64 pixel tile, stages for every
+// angle of its node the window of <= 96 sinogram bins the tile projects onto
+// (pre-scaled by 1/m_a), and each thread gathers the <= 2 bins under each of its 16
+// pixels per angle (2 shared-memory taps + 2 saturating FMAs for the weights).
 #pragma once
 #include "common.cuh"
 
@@ -15,16 +26,40 @@ namespace tq {
 enum BpEpi { EPI_PLAIN = 0, EPI_CGQ = 1, EPI_RESID = 2, EPI_GD = 3 };
 enum ScalSlot { S_RR = 0, S_PQ = 1, S_ALPHA = 2, S_RRNEW = 3, S_BETA = 4, S_NORM = 5, S_NSLOT = 8 };
 
+// forward tile geometry
+constexpr int FP_TH = 32;                 // lines (major-axis steps) per tile
+constexpr int FP_TW = 128;                // cross-axis extent of a tile
+constexpr int FP_HALO = FP_TH + 6;        // zero columns each side: covers a ray's drift over TH lines
+constexpr int FP_WMAX = FP_TW + FP_TH + 8;  // max rays crossing one tile for one angle
+constexpr int FP_THREADS = 256;
+constexpr int FP_MAXA = 64;               // angles per shared-memory batch
+
 template <typename T>
 struct FpArgs {
-    const T *img;          // [L][n], image of local node r.node
-    const T *d;            // RESID: data rows [n_rows][n_det]
-    T *out;                // [n_rows][out_stride] + out_off
-    const RayRow *rows;    // [n_rows]
-    const double2 *trig;   // [n_angles] (cos, sin)
-    const int *xmaj;       // [n_angles]
-    int N, n_det, out_stride, out_off;
+    const T *img;          // [L][n] node-major images
     long long n;
+    int N, n_det;
+    const int *olist;      // ray rows grouped by (node, orientation)
+    const int *oofs;       // [2L+1] offsets into olist; group g = 2*node + orientation
+    const RayRow *rows;    // [n_rows] (node, angle)
+    const double2 *trig;   // [n_angles] (cos, sin)
+    T *partial;            // [n_rows][ntiles][FP_WMAX]
+    int2 *win;             // [n_rows][ntiles] (first ray, number of rays) per (row, tile)
+    int nt_line, nt_cross; // tiles along the major / cross axis (same for both orientations)
+    uint32_t magic;        // = 0x4B000000 << 2 (mod 2^32), see projector.cu magic_base
+};
+
+template <typename T>
+struct FpRedArgs {
+    const T *partial;
+    const int2 *win;
+    const RayRow *rows;
+    const double2 *trig;
+    const int *xmaj;
+    const T *d;            // RESID: data [n_rows][n_det]
+    T *out;                // [n_rows][out_stride] + out_off
+    int out_stride, out_off;
+    int N, n_det, nt_line, nt_cross;
 };
 
 template <typename T>
@@ -49,10 +84,16 @@ struct BpArgs {
     unsigned *counter;       // [L]
     double *scal;            // [L][S_NSLOT]
     int part_stride;
+    uint32_t magic;          // = 0x4B000000 << 2 (mod 2^32)
 };
 
-void launch_fp(int prec, bool resid, const void *args, int n_rows, int n_det, cudaStream_t st);
-void launch_bp(int prec, int epi, const void *args, int L, int N, cudaStream_t st);
+constexpr uint32_t kMagicBits4 = 0x2C000000u;  // (0x4B000000 << 2) mod 2^32
+void projector_setup();                   // per-device kernel attributes (not capturable)
+int fp_ntiles(int N);                     // tiles per orientation
 int bp_tiles(int N);
+// forward: tile pass over L nodes then the fixed-order reduction over n_rows rows
+void launch_fp(int prec, const void *args, int L, cudaStream_t st);
+void launch_fp_reduce(int prec, bool resid, const void *args, int n_rows, int n_det, cudaStream_t st);
+void launch_bp(int prec, int epi, const void *args, int L, int N, cudaStream_t st);
 
 }  // namespace tq

@@ -6,6 +6,7 @@
 namespace tq {
 
 void DevGeom::init(int N_, int n_ang_, int n_det_) {
+    projector_setup();
     N = N_; n_ang = n_ang_; n_det = n_det_;
     n = (long long)N * N;
     std::vector<AngleHost> a = make_angles(n_ang);
@@ -19,6 +20,7 @@ void DevGeom::init(int N_, int n_ang_, int n_det_) {
     TQ_CHECK_CUDA(cudaMalloc(&xmaj, sizeof(int) * n_ang));
     TQ_CHECK_CUDA(cudaMemcpy(trig, t.data(), sizeof(double2) * n_ang, cudaMemcpyHostToDevice));
     TQ_CHECK_CUDA(cudaMemcpy(xmaj, xm.data(), sizeof(int) * n_ang, cudaMemcpyHostToDevice));
+    xmaj_h = xm;
 }
 
 void DevGeom::release() {
@@ -38,6 +40,15 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
         for (size_t k = 0; k < angles[i].size(); k++) rows_h.push_back(RayRow{i, angles[i][k], (int)k, 0});
     }
     n_rows = (int)rows_h.size();
+    std::vector<int> ol, of(1, 0);
+    for (int i = 0; i < L; i++)
+        for (int o = 0; o < 2; o++) {
+            for (int r = row0_h[i]; r < row0_h[i] + nang_h[i]; r++)
+                if (g.xmaj_h[rows_h[r].angle] == o) ol.push_back(r);
+            of.push_back((int)ol.size());
+        }
+    nt_line = ceil_div(g.N, FP_TH);
+    nt_cross = ceil_div(g.N, FP_TW);
     sp = g.n_det + 2;
     part_stride = std::max(bp_tiles(g.N), vec_blocks(n));
     const size_t es = esize();
@@ -51,6 +62,13 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
     TQ_CHECK_CUDA(cudaMemcpy(rows, rows_h.data(), sizeof(RayRow) * n_rows, cudaMemcpyHostToDevice));
     TQ_CHECK_CUDA(cudaMemcpy(row0, row0_h.data(), sizeof(int) * L, cudaMemcpyHostToDevice));
     TQ_CHECK_CUDA(cudaMemcpy(nang, nang_h.data(), sizeof(int) * L, cudaMemcpyHostToDevice));
+    A((void **)&olist, sizeof(int) * ol.size());
+    A((void **)&oofs, sizeof(int) * of.size());
+    if (!ol.empty()) TQ_CHECK_CUDA(cudaMemcpy(olist, ol.data(), sizeof(int) * ol.size(), cudaMemcpyHostToDevice));
+    TQ_CHECK_CUDA(cudaMemcpy(oofs, of.data(), sizeof(int) * of.size(), cudaMemcpyHostToDevice));
+    const size_t nwin = (size_t)n_rows * nt_line * nt_cross;
+    A(&fpart, es * nwin * FP_WMAX);
+    A((void **)&fwin, sizeof(int2) * nwin);
     for (void **v : {&X, &R, &P, &Q, &BP}) A(v, es * n * L);
     A(&D, es * (size_t)n_rows * g.n_det);
     A(&S, es * (size_t)n_rows * sp);
@@ -63,37 +81,47 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
 
 void Inner::release() {
     for (void *p : {(void *)rows, (void *)row0, (void *)nang, X, R, P, Q, BP, D, S, (void *)cnode,
-                    (void *)eta, (void *)scal, (void *)partial, (void *)counter})
+                    (void *)eta, (void *)scal, (void *)partial, (void *)counter, (void *)olist,
+                    (void *)oofs, fpart, (void *)fwin})
         if (p) cudaFree(p);
-    rows = nullptr; row0 = nang = nullptr;
+    rows = nullptr; row0 = nang = olist = oofs = nullptr;
+    fpart = nullptr; fwin = nullptr;
     X = R = P = Q = BP = D = S = nullptr;
     cnode = eta = scal = partial = nullptr;
     counter = nullptr;
 }
 
-int Inner::project(const DevGeom &g, const void *img, bool resid, cudaStream_t st) {
+int Inner::project(const DevGeom &g, const void *img, bool resid, cudaStream_t st, void *out,
+                   int out_stride, int out_off) {
+    if (!out) { out = S; out_stride = sp; out_off = 1; }
     if (prec == 0) {
-        FpArgs<float> a{(const float *)img, (const float *)D, (float *)S, rows, g.trig, g.xmaj,
-                        g.N, g.n_det, sp, 1, n};
-        launch_fp(0, resid, &a, n_rows, g.n_det, st);
+        FpArgs<float> a{(const float *)img, n, g.N, g.n_det, olist, oofs, rows, g.trig, (float *)fpart,
+                        fwin, nt_line, nt_cross, kMagicBits4};
+        launch_fp(0, &a, L, st);
+        FpRedArgs<float> r{(const float *)fpart, fwin, rows, g.trig, g.xmaj, (const float *)D, (float *)out,
+                           out_stride, out_off, g.N, g.n_det, nt_line, nt_cross};
+        launch_fp_reduce(0, resid, &r, n_rows, g.n_det, st);
     } else {
-        FpArgs<double> a{(const double *)img, (const double *)D, (double *)S, rows, g.trig, g.xmaj,
-                         g.N, g.n_det, sp, 1, n};
-        launch_fp(1, resid, &a, n_rows, g.n_det, st);
+        FpArgs<double> a{(const double *)img, n, g.N, g.n_det, olist, oofs, rows, g.trig, (double *)fpart,
+                         fwin, nt_line, nt_cross, kMagicBits4};
+        launch_fp(1, &a, L, st);
+        FpRedArgs<double> r{(const double *)fpart, fwin, rows, g.trig, g.xmaj, (const double *)D,
+                            (double *)out, out_stride, out_off, g.N, g.n_det, nt_line, nt_cross};
+        launch_fp_reduce(1, resid, &r, n_rows, g.n_det, st);
     }
-    return 1;
+    return 3;
 }
 
 int Inner::backproject(const DevGeom &g, int epi, void *out, void *out2, const void *vin, cudaStream_t st) {
     if (prec == 0) {
         BpArgs<float> a{(const float *)S, sp, 1, row0, nang, rows, g.trig, g.xmaj, g.N, g.n_det, n,
                         (float *)out, (float *)out2, (const float *)vin, (const float *)BP, cnode, eta,
-                        partial, counter, scal, part_stride};
+                        partial, counter, scal, part_stride, kMagicBits4};
         launch_bp(0, epi, &a, L, g.N, st);
     } else {
         BpArgs<double> a{(const double *)S, sp, 1, row0, nang, rows, g.trig, g.xmaj, g.N, g.n_det, n,
                          (double *)out, (double *)out2, (const double *)vin, (const double *)BP, cnode,
-                         eta, partial, counter, scal, part_stride};
+                         eta, partial, counter, scal, part_stride, kMagicBits4};
         launch_bp(1, epi, &a, L, g.N, st);
     }
     return 1;

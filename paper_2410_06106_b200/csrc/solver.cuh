@@ -15,6 +15,7 @@ struct DevGeom {
     long long n = 0;
     double2 *trig = nullptr;  // [n_ang]
     int *xmaj = nullptr;      // [n_ang]
+    std::vector<int> xmaj_h;
     void init(int N, int n_ang, int n_det);
     void release();
 };
@@ -25,6 +26,11 @@ struct Inner {
     RayRow *rows = nullptr;    // [n_rows]
     int *row0 = nullptr;       // [L]
     int *nang = nullptr;       // [L]
+    int *olist = nullptr;      // ray rows grouped by (node, major axis) for the forward tiles
+    int *oofs = nullptr;       // [2L+1]
+    void *fpart = nullptr;     // forward partial sums [n_rows][fp_ntiles][FP_WMAX]
+    int2 *fwin = nullptr;      // [n_rows][fp_ntiles]
+    int nt_line = 0, nt_cross = 0;
     void *X = nullptr, *R = nullptr, *P = nullptr, *Q = nullptr, *BP = nullptr;  // [L][n]
     void *D = nullptr;         // [n_rows][n_det]
     void *S = nullptr;         // [n_rows][sp], guard column at 0 and n_det+1
@@ -43,7 +49,9 @@ struct Inner {
     int cg(const DevGeom &g, int e1, cudaStream_t st);
     int gd(const DevGeom &g, int e1, cudaStream_t st);
     int norm2(cudaStream_t st);
-    int project(const DevGeom &g, const void *img, bool resid, cudaStream_t st);   // S = (D -) A img
+    // S = (D -) A img (2 tile launches + 1 reduction); out/out_stride/out_off override S
+    int project(const DevGeom &g, const void *img, bool resid, cudaStream_t st, void *out = nullptr,
+                int out_stride = 0, int out_off = 0);
     int backproject(const DevGeom &g, int epi, void *out, void *out2, const void *vin, cudaStream_t st);
 };
 
