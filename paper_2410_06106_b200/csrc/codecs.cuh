@@ -3,10 +3,10 @@
 // through device arrays of pointers (one entry per payload), so a batch can mix local
 // iterates, received payloads and segments of the consensus image.
 //
-// K-means (Alg. 5; exact rules DESIGN.md R-16): quantile init by an
-// exact 4-pass radix select (8-bit digits) of the order statistics, E_q Lloyd passes
-// with deterministic fixed-point integer cluster sums, final assignment, labels
-// packed as ceil(log2 K) bit-planes per 32-element group with warp ballots.
+// K-means (Alg. 5; exact rules DESIGN.md R-16): LSD radix sort of the
+// payload keys, quantile init as exact order statistics, E_q Lloyd steps as upper
+// bounds + fixed-point prefix sums on the sorted keys (exact, deterministic), final
+// assignment, labels packed as ceil(log2 K) bit-planes per 32-element group.
 // Payload: [K fp32 centres][ceil(nv/32) * B uint32 planes, group-major].
 //
 // DCT (R-18): per-payload [min,max], fp64 8-bit map, exact integer two-pass
@@ -22,19 +22,16 @@ long long kmeans_payload_bytes(int K, long long nv);
 long long dct_payload_bytes(long long nv);
 
 struct KmeansWork {
-    int P = 0, K = 0, B = 0;        // payloads, clusters, bits per label
+    int P = 0, K = 0, B = 0, T = 0;  // payloads, clusters, bits per label, 2048-key tiles per payload
     long long nv = 0;
+    uint32_t *keysA = nullptr;      // [P][T*2048] order-preserving keys (sorted in place)
+    uint32_t *keysB = nullptr;      // radix-sort ping-pong buffer
+    uint32_t *hist = nullptr;       // [P][T][256] per-tile digit counts -> offsets
+    uint32_t *base = nullptr;       // [P][256] digit bases
+    long long *tsum = nullptr;      // [P][T] fixed-point sums of the sorted tiles
     float *cen = nullptr;           // [P][K]
     float *thr = nullptr;           // [P][K]
-    uint32_t *prefix = nullptr;     // [P][K+2]
-    uint32_t *rank = nullptr;       // [P][K+2]
-    uint32_t *plist = nullptr;      // [P][K+2]
-    int *np = nullptr;              // [P]
-    uint32_t *hist = nullptr;       // [P][K+2][256]
     int *fexp = nullptr;            // [P] fixed-point exponent F
-    unsigned long long *acc_sum = nullptr;  // [P][K] int64 two's complement
-    unsigned long long *acc_cnt = nullptr;  // [P][K]
-    unsigned *counter = nullptr;    // [P]
     void alloc(int P, int K, long long nv);
     void release();
 };

@@ -1,14 +1,39 @@
 // kmeans.cu -- K-means quantizer (Alg. 5), exact rules DESIGN.md R-16.
+//
+// Sort-based exact Lloyd.  Each payload's values are mapped to order-preserving
+// 32-bit keys and sorted by an LSD radix sort (4 passes of 8-bit digits: per-tile
+// digit histograms, per-payload offset scan, stable tile sort + scatter).  On the
+// sorted keys:
+//   * the quantile init c_k = v_(floor((2k+1) n / 2K)) is a direct read (exact order
+//     statistic);
+//   * a Lloyd step needs, for each threshold b_k, C_k = #{v <= b_k} and
+//     S_k = sum_{v <= b_k} fix(v): C_k is an upper bound in the sorted keys (binary
+//     search over the tile heads in shared memory, then one warp counts inside one
+//     2048-key tile), S_k = (exclusive prefix of the tile sums) + the in-tile part.
+//     Cluster k = (b_{k-1}, b_k], i.e. label(v) = #{k : v > b_k}, ties to the lower
+//     cluster -- the same decision the oracle takes per element.
+// fix(v) = round(v 2^F) as int64 with F chosen from max|v| and n so no sum overflows:
+// cluster sums are exact integers, hence independent of summation order.
+// All Lloyd iterations of a payload run in one CTA; the cost of an iteration no
+// longer depends on n.  The final assignment packs labels into bit-planes.
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
 #include "codecs.cuh"
 
 namespace tq {
 
 namespace {
 
-constexpr int KT = 256;
-constexpr int SMEM_HIST_MAX_ROWS = 64;  // np*256 u32 histogram rows kept in shared memory
+constexpr int KT = 256;               // threads of the per-tile kernels
+constexpr int KI = 8;                 // keys per thread
+constexpr int KTILE = KT * KI;        // keys per tile
+constexpr int LT = 1024;              // threads of the Lloyd kernel
+constexpr int MAX_TILES = 8192;       // per payload (n <= 16.7 M)
 
 __device__ __forceinline__ uint32_t f2key(float f) {
+    if (f == 0.0f) f = 0.0f;  // -0 and +0 are the same value for every comparison
     const uint32_t u = __float_as_uint(f);
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
@@ -27,191 +52,243 @@ __device__ __forceinline__ int kmeans_label(float v, const float *thr, int K) {
 }
 
 struct KmPtr {
+    uint32_t *keysA, *keysB, *hist, *base;
+    long long *tsum;
     float *cen, *thr;
-    uint32_t *prefix, *rank, *plist, *hist;
-    int *np, *fexp;
-    unsigned long long *acc_sum, *acc_cnt;
-    unsigned *counter;
-    int K, NT;
+    int *fexp;
+    int K, T;
     long long nv;
 };
 
 KmPtr ptrs(const KmeansWork &w) {
-    return KmPtr{w.cen, w.thr, w.prefix, w.rank, w.plist, w.hist, w.np, w.fexp, w.acc_sum,
-                 w.acc_cnt, w.counter, w.K, w.K + 2, w.nv};
+    return KmPtr{w.keysA, w.keysB, w.hist, w.base, w.tsum, w.cen, w.thr, w.fexp, w.K, w.T, w.nv};
 }
 
-// targets: t = 0 -> rank 0 (min), t = 1..K -> floor((2k+1) nv / 2K), t = K+1 -> nv-1 (max)
-__global__ void km_init(KmPtr w) {
-    const int b = blockIdx.x;
-    const int NT = w.NT;
-    for (int t = threadIdx.x; t < NT; t += blockDim.x) {
-        unsigned long long r;
-        if (t == 0) r = 0;
-        else if (t == NT - 1) r = (unsigned long long)(w.nv - 1);
-        else r = ((unsigned long long)(2 * (t - 1) + 1) * (unsigned long long)w.nv) /
-                 (unsigned long long)(2 * w.K);
-        w.rank[(long long)b * NT + t] = (uint32_t)r;
-        w.prefix[(long long)b * NT + t] = 0u;
+__device__ __forceinline__ void load_tile(const uint32_t *keys, long long off, uint32_t (&k)[KI]) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(keys + off + threadIdx.x * KI);
+    const uint4 a = p[0], b = p[1];
+    k[0] = a.x; k[1] = a.y; k[2] = a.z; k[3] = a.w;
+    k[4] = b.x; k[5] = b.y; k[6] = b.z; k[7] = b.w;
+}
+
+// warp-aggregated shared histogram of one digit of the thread's keys
+__device__ __forceinline__ void tile_hist(const uint32_t (&k)[KI], int shift, uint32_t *sh) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int r = 0; r < KI; r++) {
+        const uint32_t d = (k[r] >> shift) & 255u;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (lane == __ffs(peers) - 1) atomicAdd(&sh[d], (uint32_t)__popc(peers));
     }
+}
+
+__device__ __forceinline__ void flush_hist(uint32_t *sh, uint32_t *g) {
+    __syncthreads();
+    g[threadIdx.x] = sh[threadIdx.x];  // KT == 256 digits
+}
+
+// keys of the raw payload (padding keys sort last) + digit-0 histogram
+__global__ void __launch_bounds__(KT) km_keys(const float *const *vin, KmPtr w) {
+    __shared__ uint32_t sh[256];
+    const int b = blockIdx.y, t = blockIdx.x;
+    sh[threadIdx.x] = 0u;
+    __syncthreads();
+    const float *v = vin[b];
+    const long long i0 = (long long)t * KTILE + threadIdx.x * KI;
+    uint32_t k[KI];
+#pragma unroll
+    for (int r = 0; r < KI; r++) k[r] = (i0 + r < w.nv) ? f2key(v[i0 + r]) : 0xffffffffu;
+    uint4 *o = reinterpret_cast<uint4 *>(w.keysA + (long long)b * w.T * KTILE + i0);
+    o[0] = make_uint4(k[0], k[1], k[2], k[3]);
+    o[1] = make_uint4(k[4], k[5], k[6], k[7]);
+    tile_hist(k, 0, sh);
+    flush_hist(sh, w.hist + ((long long)b * w.T + t) * 256);
+}
+
+__global__ void __launch_bounds__(KT) km_hist(const uint32_t *keys, KmPtr w, int shift) {
+    __shared__ uint32_t sh[256];
+    const int b = blockIdx.y, t = blockIdx.x;
+    sh[threadIdx.x] = 0u;
+    __syncthreads();
+    uint32_t k[KI];
+    load_tile(keys, ((long long)b * w.T + t) * KTILE, k);
+    tile_hist(k, shift, sh);
+    flush_hist(sh, w.hist + ((long long)b * w.T + t) * 256);
+}
+
+// per payload: hist[t][d] <- sum_{t' < t} hist[t'][d]; base[d] <- sum_{d' < d} total[d']
+__global__ void __launch_bounds__(256) km_scan(KmPtr w) {
+    using Scan = cub::BlockScan<uint32_t, 256>;
+    __shared__ typename Scan::TempStorage tmp;
+    const int b = blockIdx.x, d = threadIdx.x;
+    uint32_t *h = w.hist + (long long)b * w.T * 256 + d;
+    uint32_t run = 0;
+    int t = 0;
+    for (; t + 4 <= w.T; t += 4) {
+        const uint32_t c0 = h[(t + 0) * 256], c1 = h[(t + 1) * 256], c2 = h[(t + 2) * 256], c3 = h[(t + 3) * 256];
+        h[(t + 0) * 256] = run; run += c0;
+        h[(t + 1) * 256] = run; run += c1;
+        h[(t + 2) * 256] = run; run += c2;
+        h[(t + 3) * 256] = run; run += c3;
+    }
+    for (; t < w.T; t++) {
+        const uint32_t c = h[t * 256];
+        h[t * 256] = run;
+        run += c;
+    }
+    uint32_t excl;
+    Scan(tmp).ExclusiveSum(run, excl);
+    w.base[(long long)b * 256 + d] = excl;
+}
+
+// stable sort of the tile by the digit, then scatter to base[d] + tile offset + rank
+__global__ void __launch_bounds__(KT) km_scatter(const uint32_t *kin, uint32_t *kout, KmPtr w, int shift) {
+    using Sort = cub::BlockRadixSort<uint32_t, KT, KI>;
+    __shared__ typename Sort::TempStorage tmp;
+    __shared__ uint32_t dstart[256], goff[256], lastd[KT];
+    const int b = blockIdx.y, t = blockIdx.x;
+    const long long pb = (long long)b * w.T * KTILE;
+    uint32_t k[KI];
+    load_tile(kin, pb + (long long)t * KTILE, k);
+    goff[threadIdx.x] = w.base[(long long)b * 256 + threadIdx.x] +
+                        w.hist[((long long)b * w.T + t) * 256 + threadIdx.x];
+    Sort(tmp).Sort(k, shift, shift + 8);  // blocked arrangement, stable
+    lastd[threadIdx.x] = (k[KI - 1] >> shift) & 255u;
+    __syncthreads();
+    uint32_t prev = threadIdx.x ? lastd[threadIdx.x - 1] : 0xffffffffu;
+#pragma unroll
+    for (int r = 0; r < KI; r++) {
+        const uint32_t d = (k[r] >> shift) & 255u;
+        if (d != prev) dstart[d] = threadIdx.x * KI + r;
+        prev = d;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < KI; r++) {
+        const uint32_t d = (k[r] >> shift) & 255u;
+        kout[pb + goff[d] + (threadIdx.x * KI + r - dstart[d])] = k[r];
+    }
+}
+
+// fixed-point exponent F: |sum of nv values * 2^F| < 2^62
+__device__ __forceinline__ int fixed_exp(const uint32_t *sorted, long long nv) {
+    const double mx = fmax(fabs((double)key2f(sorted[0])), fabs((double)key2f(sorted[nv - 1])));
+    if (!(mx > 0.0)) return 0;
+    const int E = ilogb(mx) + 1;
+    int lg = 0;
+    while ((1LL << lg) < nv) lg++;
+    return 62 - E - lg;
+}
+
+// per-tile sums of fix(v) over the sorted keys
+__global__ void __launch_bounds__(KT) km_tsum(KmPtr w) {
+    using Red = cub::BlockReduce<long long, KT>;
+    __shared__ typename Red::TempStorage tmp;
+    const int b = blockIdx.y, t = blockIdx.x;
+    const uint32_t *sorted = w.keysA + (long long)b * w.T * KTILE;
+    const int F = fixed_exp(sorted, w.nv);
+    const double scale = ldexp(1.0, F);
+    uint32_t k[KI];
+    load_tile(sorted, (long long)t * KTILE, k);
+    long long s = 0;
+    const long long i0 = (long long)t * KTILE + threadIdx.x * KI;
+#pragma unroll
+    for (int r = 0; r < KI; r++)
+        if (i0 + r < w.nv) s += __double2ll_rn((double)key2f(k[r]) * scale);
+    const long long tot = Red(tmp).Sum(s);
     if (threadIdx.x == 0) {
-        w.np[b] = 1;
-        w.plist[(long long)b * NT] = 0u;
+        w.tsum[(long long)b * w.T + t] = tot;
+        if (t == 0) w.fexp[b] = F;
     }
 }
 
-template <bool SMEM>
-__global__ void __launch_bounds__(KT) km_hist(const float *const *vin, KmPtr w, int shift) {
-    extern __shared__ uint32_t sh[];
-    const int b = blockIdx.y;
-    const int np = w.np[b];
-    const uint32_t *plist = w.plist + (long long)b * w.NT;
-    uint32_t *gh = w.hist + (long long)b * w.NT * 256;
-    if (SMEM) {
-        for (int i = threadIdx.x; i < np * 256; i += KT) sh[i] = 0u;
+// one CTA per payload: quantile init, then `iters` exact Lloyd steps on the sorted keys
+__global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters) {
+    using Scan = cub::BlockScan<long long, LT>;
+    __shared__ typename Scan::TempStorage tmp;
+    extern __shared__ __align__(16) unsigned char lsm[];
+    long long *tpre = reinterpret_cast<long long *>(lsm);         // [T + 1]
+    uint32_t *thead = reinterpret_cast<uint32_t *>(tpre + w.T + 1);  // [T]
+    __shared__ float cen[256], thr[256];
+    __shared__ long long Cs[256], Ss[256];
+    const int b = blockIdx.x, K = w.K, T = w.T;
+    const long long nv = w.nv;
+    const uint32_t *sorted = w.keysA + (long long)b * T * KTILE;
+    const long long *ts = w.tsum + (long long)b * T;
+    const int F = w.fexp[b];
+    const double scale = ldexp(1.0, F);
+    // exclusive prefix of the tile sums (chunked block scan) and the tile head keys
+    long long carry = 0;
+    for (int c0 = 0; c0 < T; c0 += LT) {
+        const int t = c0 + threadIdx.x;
+        const long long x = t < T ? ts[t] : 0;
+        long long ex, agg;
+        Scan(tmp).ExclusiveSum(x, ex, agg);
+        if (t < T) {
+            tpre[t] = carry + ex;
+            thead[t] = sorted[(long long)t * KTILE];
+        }
+        carry += agg;
         __syncthreads();
     }
-    const float *vb = vin[b];
-    for (long long i = (long long)blockIdx.x * KT + threadIdx.x; i < w.nv; i += (long long)gridDim.x * KT) {
-        const uint32_t k = f2key(vb[i]);
-        const uint32_t pf = (uint32_t)((unsigned long long)k >> (shift + 8));
-        int lo = 0, hi = np;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (plist[mid] < pf) lo = mid + 1; else hi = mid;
-        }
-        if (lo < np && plist[lo] == pf) {
-            const int d = (k >> shift) & 255;
-            if (SMEM) atomicAdd(&sh[lo * 256 + d], 1u);
-            else atomicAdd(&gh[lo * 256 + d], 1u);
-        }
+    if (threadIdx.x == 0) tpre[T] = carry;
+    // quantile init: c_k = v_(floor((2k+1) nv / 2K))
+    for (int k = threadIdx.x; k < K; k += LT) {
+        const long long idx = ((long long)(2 * k + 1) * nv) / (2LL * K);
+        cen[k] = key2f(sorted[idx]);
     }
-    if (SMEM) {
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int it = 0; it < iters; it++) {
+        for (int k = threadIdx.x; k + 1 < K; k += LT) thr[k] = (float)(((double)cen[k] + (double)cen[k + 1]) * 0.5);
         __syncthreads();
-        for (int i = threadIdx.x; i < np * 256; i += KT)
-            if (sh[i]) atomicAdd(&gh[i], sh[i]);
-    }
-}
-
-__global__ void __launch_bounds__(KT) km_select(KmPtr w, int shift) {
-    const int b = blockIdx.x;
-    const int NT = w.NT;
-    __shared__ int np_s;
-    if (threadIdx.x == 0) np_s = w.np[b];
-    __syncthreads();
-    const int np = np_s;
-    uint32_t *plist = w.plist + (long long)b * NT;
-    uint32_t *prefix = w.prefix + (long long)b * NT;
-    uint32_t *rank = w.rank + (long long)b * NT;
-    uint32_t *hist = w.hist + (long long)b * NT * 256;
-    for (int t = threadIdx.x; t < NT; t += KT) {
-        const uint32_t pf = prefix[t];
-        int lo = 0, hi = np;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (plist[mid] < pf) lo = mid + 1; else hi = mid;
-        }
-        const uint32_t *H = hist + (long long)lo * 256;
-        uint32_t r = rank[t], cum = 0;
-        int d = 255;
-        for (int q = 0; q < 256; q++) {
-            const uint32_t c = H[q];
-            if (r < cum + c) { d = q; break; }
-            cum += c;
-        }
-        rank[t] = r - cum;
-        prefix[t] = (shift == 24) ? (uint32_t)d : ((pf << 8) | (uint32_t)d);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < np * 256; i += KT) hist[i] = 0u;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int m = 0;
-        for (int t = 0; t < NT; t++)
-            if (t == 0 || prefix[t] != prefix[t - 1]) plist[m++] = prefix[t];
-        w.np[b] = m;
-        if (shift == 0) {
-            // order statistics found: centres, and the fixed-point exponent F such that
-            // |sum of nv values * 2^F| < 2^62 (deterministic integer cluster sums)
-            const int K = w.K;
-            float *cen = w.cen + (long long)b * K;
-            for (int k = 0; k < K; k++) cen[k] = key2f(prefix[1 + k]);
-            const double mx = fmax(fabs((double)key2f(prefix[0])), fabs((double)key2f(prefix[NT - 1])));
-            int F = 0;
-            if (mx > 0.0) {
-                const int E = ilogb(mx) + 1;
-                int lg = 0;
-                while ((1LL << lg) < w.nv) lg++;
-                F = 62 - E - lg;
+        for (int k = warp; k + 1 < K; k += LT / 32) {
+            const uint32_t kb = f2key(thr[k]);
+            int lo = 0, hi = T - 1, tt = -1;  // last tile whose head key <= kb
+            while (lo <= hi) {
+                const int mid = (lo + hi) >> 1;
+                if (thead[mid] <= kb) { tt = mid; lo = mid + 1; } else hi = mid - 1;
             }
-            w.fexp[b] = F;
-            float *thr = w.thr + (long long)b * K;
-            for (int k = 0; k + 1 < K; k++) thr[k] = (float)(((double)cen[k] + (double)cen[k + 1]) * 0.5);
-        }
-    }
-}
-
-__global__ void __launch_bounds__(KT) km_lloyd(const float *const *vin, KmPtr w) {
-    extern __shared__ unsigned long long shl[];  // sum[K] then cnt[K]
-    __shared__ float thr_s[256];
-    __shared__ bool last;
-    const int b = blockIdx.y;
-    const int K = w.K;
-    unsigned long long *s_sum = shl, *s_cnt = shl + K;
-    for (int k = threadIdx.x; k < K; k += KT) {
-        s_sum[k] = 0ull;
-        s_cnt[k] = 0ull;
-        if (k + 1 < K) thr_s[k] = w.thr[(long long)b * K + k];
-    }
-    __syncthreads();
-    const double scale = ldexp(1.0, w.fexp[b]);
-    const float *vb = vin[b];
-    for (long long i0 = ((long long)blockIdx.x * KT + threadIdx.x) * 4; i0 < w.nv;
-         i0 += (long long)gridDim.x * KT * 4) {
-        int cur = -1;
-        long long csum = 0;
-        unsigned long long ccnt = 0;
-        for (int e = 0; e < 4; e++) {
-            const long long i = i0 + e;
-            if (i >= w.nv) break;
-            const float x = vb[i];
-            const int l = kmeans_label(x, thr_s, K);
-            const long long fx = __double2ll_rn((double)x * scale);
-            if (l != cur) {
-                if (cur >= 0) {
-                    atomicAdd(&s_sum[cur], (unsigned long long)csum);
-                    atomicAdd(&s_cnt[cur], ccnt);
+            long long C = 0, S = 0;
+            if (tt >= 0) {
+                const long long off = (long long)tt * KTILE;
+                int cnt = 0;
+                long long s = 0;
+                const uint4 *p = reinterpret_cast<const uint4 *>(sorted + off);
+#pragma unroll 4
+                for (int q = lane; q < KTILE / 4; q += 32) {
+                    const uint4 v4 = p[q];
+                    const uint32_t e[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const long long i = off + 4 * q + u;
+                        if (e[u] <= kb && i < nv) {
+                            cnt++;
+                            s += __double2ll_rn((double)key2f(e[u]) * scale);
+                        }
+                    }
                 }
-                cur = l; csum = 0; ccnt = 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+                    s += __shfl_xor_sync(0xffffffffu, s, o);
+                }
+                C = off + cnt;
+                S = tpre[tt] + s;
             }
-            csum += fx;
-            ccnt += 1;
-        }
-        if (cur >= 0) {
-            atomicAdd(&s_sum[cur], (unsigned long long)csum);
-            atomicAdd(&s_cnt[cur], ccnt);
-        }
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < K; k += KT) {
-        if (s_cnt[k]) {
-            atomicAdd(&w.acc_sum[(long long)b * K + k], s_sum[k]);
-            atomicAdd(&w.acc_cnt[(long long)b * K + k], s_cnt[k]);
-        }
-    }
-    if (last_block_of_group(w.counter + b, gridDim.x, &last)) {
-        float *cen = w.cen + (long long)b * K;
-        for (int k = threadIdx.x; k < K; k += KT) {
-            const unsigned long long c = w.acc_cnt[(long long)b * K + k];
-            const long long s = (long long)w.acc_sum[(long long)b * K + k];
-            if (c) cen[k] = (float)(((double)s / scale) / (double)c);
-            w.acc_cnt[(long long)b * K + k] = 0ull;
-            w.acc_sum[(long long)b * K + k] = 0ull;
+            if (lane == 0) { Cs[k] = C; Ss[k] = S; }
         }
         __syncthreads();
-        float *thr = w.thr + (long long)b * K;
-        for (int k = threadIdx.x; k + 1 < K; k += KT)
-            thr[k] = (float)(((double)cen[k] + (double)cen[k + 1]) * 0.5);
+        for (int k = threadIdx.x; k < K; k += LT) {
+            const long long c1 = k + 1 < K ? Cs[k] : nv, c0 = k ? Cs[k - 1] : 0;
+            const long long s1 = k + 1 < K ? Ss[k] : tpre[T], s0 = k ? Ss[k - 1] : 0;
+            if (c1 > c0) cen[k] = (float)(((double)(s1 - s0) / scale) / (double)(c1 - c0));
+        }
+        __syncthreads();
+    }
+    for (int k = threadIdx.x; k < K; k += LT) {
+        w.cen[(long long)b * K + k] = cen[k];
+        if (k + 1 < K) w.thr[(long long)b * K + k] = (float)(((double)cen[k] + (double)cen[k + 1]) * 0.5);
     }
 }
 
@@ -262,12 +339,7 @@ __global__ void km_decode(const uint8_t *const *pay, long long nv, int K, int B,
     }
 }
 
-int grid_for(long long nv, int P) {
-    // enough blocks to fill 148 SMs a few times over all payloads
-    long long want = std::max(1LL, (148LL * 8 + P - 1) / P);
-    long long need = (nv + KT * 4 - 1) / (KT * 4);
-    return (int)std::max(1LL, std::min(want, need));
-}
+size_t lloyd_smem(int T) { return sizeof(long long) * (T + 1) + sizeof(uint32_t) * T; }
 
 }  // namespace
 
@@ -283,30 +355,24 @@ long long kmeans_payload_bytes(int K, long long nv) {
 
 void KmeansWork::alloc(int P_, int K_, long long nv_) {
     P = P_; K = K_; nv = nv_; B = kmeans_bits(K_);
-    const int NT = K + 2;
     TQ_REQUIRE(K >= 1 && K <= 256, "kmeans: k must be in [1, 256]");
-    TQ_CHECK_CUDA(cudaFuncSetAttribute(km_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       SMEM_HIST_MAX_ROWS * 256 * 4));
+    TQ_REQUIRE(nv >= 1 && nv <= (long long)MAX_TILES * KTILE, "kmeans: payload length must be in [1, 16777216]");
+    T = (int)((nv + KTILE - 1) / KTILE);
+    const size_t nk = (size_t)P * T * KTILE;
+    TQ_CHECK_CUDA(cudaMalloc(&keysA, sizeof(uint32_t) * nk));
+    TQ_CHECK_CUDA(cudaMalloc(&keysB, sizeof(uint32_t) * nk));
+    TQ_CHECK_CUDA(cudaMalloc(&hist, sizeof(uint32_t) * (size_t)P * T * 256));
+    TQ_CHECK_CUDA(cudaMalloc(&base, sizeof(uint32_t) * (size_t)P * 256));
+    TQ_CHECK_CUDA(cudaMalloc(&tsum, sizeof(long long) * (size_t)P * T));
     TQ_CHECK_CUDA(cudaMalloc(&cen, sizeof(float) * P * K));
     TQ_CHECK_CUDA(cudaMalloc(&thr, sizeof(float) * P * K));
-    TQ_CHECK_CUDA(cudaMalloc(&prefix, sizeof(uint32_t) * P * NT));
-    TQ_CHECK_CUDA(cudaMalloc(&rank, sizeof(uint32_t) * P * NT));
-    TQ_CHECK_CUDA(cudaMalloc(&plist, sizeof(uint32_t) * P * NT));
-    TQ_CHECK_CUDA(cudaMalloc(&np, sizeof(int) * P));
-    TQ_CHECK_CUDA(cudaMalloc(&hist, sizeof(uint32_t) * P * NT * 256));
-    TQ_CHECK_CUDA(cudaMemset(hist, 0, sizeof(uint32_t) * P * NT * 256));
     TQ_CHECK_CUDA(cudaMalloc(&fexp, sizeof(int) * P));
-    TQ_CHECK_CUDA(cudaMalloc(&acc_sum, sizeof(unsigned long long) * P * K));
-    TQ_CHECK_CUDA(cudaMalloc(&acc_cnt, sizeof(unsigned long long) * P * K));
-    TQ_CHECK_CUDA(cudaMemset(acc_sum, 0, sizeof(unsigned long long) * P * K));
-    TQ_CHECK_CUDA(cudaMemset(acc_cnt, 0, sizeof(unsigned long long) * P * K));
-    TQ_CHECK_CUDA(cudaMalloc(&counter, sizeof(unsigned) * P));
-    TQ_CHECK_CUDA(cudaMemset(counter, 0, sizeof(unsigned) * P));
+    TQ_CHECK_CUDA(cudaFuncSetAttribute(km_lloyd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lloyd_smem(T)));
 }
 
 void KmeansWork::release() {
-    for (void *p : {(void *)cen, (void *)thr, (void *)prefix, (void *)rank, (void *)plist, (void *)np,
-                    (void *)hist, (void *)fexp, (void *)acc_sum, (void *)acc_cnt, (void *)counter})
+    for (void *p : {(void *)keysA, (void *)keysB, (void *)hist, (void *)base, (void *)tsum, (void *)cen,
+                    (void *)thr, (void *)fexp})
         if (p) cudaFree(p);
     *this = KmeansWork();
 }
@@ -316,21 +382,26 @@ int kmeans_encode(const float *const *v, KmeansWork &ws, int lloyd, uint8_t *con
     const KmPtr w = ptrs(ws);
     const int P = ws.P;
     if (P == 0) return 0;
-    TQ_REQUIRE(ws.nv >= 1 && ws.nv < (1LL << 31), "kmeans: payload length must be in [1, 2^31)");
-    km_init<<<P, 64, 0, st>>>(w);
-    const dim3 grid(grid_for(ws.nv, P), P);
-    const bool smem = w.NT <= SMEM_HIST_MAX_ROWS;
-    const size_t hsm = smem ? (size_t)w.NT * 256 * 4 : 0;  // opt-in set in KmeansWork::alloc
-    for (int shift = 24; shift >= 0; shift -= 8) {
-        if (smem) km_hist<true><<<grid, KT, hsm, st>>>(v, w, shift);
-        else km_hist<false><<<grid, KT, 0, st>>>(v, w, shift);
-        km_select<<<P, KT, 0, st>>>(w, shift);
+    const dim3 tiles(ws.T, P);
+    km_keys<<<tiles, KT, 0, st>>>(v, w);
+    int k = 1;
+    uint32_t *src = ws.keysA, *dst = ws.keysB;
+    for (int pass = 0; pass < 4; pass++) {
+        if (pass) { km_hist<<<tiles, KT, 0, st>>>(src, w, 8 * pass); k++; }
+        km_scan<<<P, 256, 0, st>>>(w);
+        km_scatter<<<tiles, KT, 0, st>>>(src, dst, w, 8 * pass);
+        k += 2;
+        std::swap(src, dst);
     }
-    const size_t lsm = sizeof(unsigned long long) * 2 * ws.K;
-    for (int it = 0; it < lloyd; it++) km_lloyd<<<grid, KT, lsm, st>>>(v, w);
+    // four passes: A -> B -> A -> B -> A, sorted keys in keysA
+    km_tsum<<<tiles, KT, 0, st>>>(w);
+    km_lloyd<<<P, LT, lloyd_smem(ws.T), st>>>(w, lloyd);
+    long long want = std::max(1LL, (148LL * 8 + P - 1) / P);
+    long long need = (ws.nv + KT * 4 - 1) / (KT * 4);
+    const dim3 grid((unsigned)std::max(1LL, std::min(want, need)), P);
     km_final<<<grid, KT, 0, st>>>(v, w, ws.B, pay, labels);
     TQ_CHECK_CUDA(cudaGetLastError());
-    return 1 + 8 + lloyd + 1;
+    return k + 3;
 }
 
 int kmeans_decode(const uint8_t *const *pay, int P, long long nv, int K, int prec,
