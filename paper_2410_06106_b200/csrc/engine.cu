@@ -237,7 +237,8 @@ void Ctx::destroy() {
     ALPHA = XG = nullptr;
     if (sino_stage) cudaFree(sino_stage);
     if (row_map) cudaFree(row_map);
-    sino_stage = nullptr; row_map = nullptr;
+    if (img_stage) cudaFree(img_stage);
+    sino_stage = nullptr; row_map = nullptr; img_stage = nullptr;
     if (comm) nccl().CommDestroy(comm);
     comm = nullptr;
     if (ev0) cudaEventDestroy(ev0);
@@ -678,12 +679,12 @@ void Ctx::run(int iters, cudaStream_t user) {
 void Ctx::get_image(int slice, int node, float *out, long long len, bool on_device) {
     TQ_REQUIRE(len == n, "image length must be N*N");
     TQ_CHECK_CUDA(cudaSetDevice(device));
-    float *d = nullptr;
-    TQ_CHECK_CUDA(cudaMalloc(&d, sizeof(float) * n));
+    if (!img_stage) TQ_CHECK_CUDA(cudaMalloc(&img_stage, sizeof(float) * n));
+    float *d = img_stage;
     const int blocks = (int)std::min<long long>(2048, (n + 255) / 256);
     if (node >= 0) {
         const int i = local(slice, node);
-        if (i < 0) { cudaFree(d); fail(TQ_EINVAL, "node is not local to this rank"); }
+        if (i < 0) fail(TQ_EINVAL, "node is not local to this rank");
         launch_convert(prec, in.xrow(in.X, i), 0, d, n, stream);
     } else if (rule == TQ_RULE_PAPER) {
         TQ_REQUIRE(slice >= 0 && slice < S, "slice out of range");
@@ -692,14 +693,13 @@ void Ctx::get_image(int slice, int node, float *out, long long len, bool on_devi
         const int i0 = local(slice, 0);
         bool all = i0 >= 0;
         for (int m = 0; m < M && all; m++) all = local(slice, m) == i0 + m;
-        if (!all) { cudaFree(d); fail(TQ_EINVAL, "node=-1 (mean image) needs every node of the slice on this rank"); }
+        if (!all) fail(TQ_EINVAL, "node=-1 (mean image) needs every node of the slice on this rank");
         if (prec == 0) mean_rows<float><<<blocks, 256, 0, stream>>>((const float *)in.xrow(in.X, i0), M, n, d);
         else mean_rows<double><<<blocks, 256, 0, stream>>>((const double *)in.xrow(in.X, i0), M, n, d);
         TQ_CHECK_CUDA(cudaGetLastError());
     }
     TQ_CHECK_CUDA(cudaMemcpyAsync(out, d, sizeof(float) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream));
     TQ_CHECK_CUDA(cudaStreamSynchronize(stream));
-    cudaFree(d);
 }
 
 static void to_host_double(int prec, const void *src, double *dst, long long n, cudaStream_t s) {

@@ -119,6 +119,7 @@ struct Ctx {
     float *sino_stage = nullptr;   // persistent device staging for tq_set_sinogram
     long long sino_stage_len = 0;
     int *row_map = nullptr;        // persistent gather indices
+    float *img_stage = nullptr;    // persistent staging of tq_get_image
     long long row_map_len = 0;
 
    private:

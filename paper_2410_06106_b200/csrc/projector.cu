@@ -91,7 +91,8 @@ __global__ void __launch_bounds__(FP_THREADS) fp_tile_kernel(const FpArgs<T> a) 
     T *tile = reinterpret_cast<T *>(fp_smem);  // [FP_TH][PITCH]
     __shared__ double s_kap[FP_MAXA], s_at[FP_MAXA];
     __shared__ T s_B[FP_MAXA];
-    __shared__ int s_row[FP_MAXA], s_W[FP_MAXA], s_cofs[FP_MAXA + 1];
+    __shared__ int s_row[FP_MAXA], s_W[FP_MAXA], s_jlo[FP_MAXA], s_cofs[FP_MAXA + 1], s_wsum[2];
+    static_assert(FP_MAXA == 64, "the chunk prefix below uses two warps");
 
     const int node = blockIdx.y;
     const int grp = 2 * node + O;
@@ -141,48 +142,44 @@ __global__ void __launch_bounds__(FP_THREADS) fp_tile_kernel(const FpArgs<T> a) 
         }
     }
 
-    const double c0 = 0.5 * (double)(a.n_det - 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int b0 = a_begin; b0 < a_end; b0 += FP_MAXA) {
         const int nb = min(FP_MAXA, a_end - b0);
         __syncthreads();  // tile staged / previous batch consumed
-        // ---- rays of each angle that cross the tile: window [jlo, jlo + W)
-        for (int k = threadIdx.x; k < nb; k += FP_THREADS) {
-            const int row = a.olist[b0 + k];
-            const double2 t2 = a.trig[a.rows[row].angle];
-            const LineGeo G = line_geo(t2.x, t2.y, O, N);
-            const double l1 = (double)(min(L0 + FP_TH, N) - 1);
-            const double bA = (double)L0 * G.B, bB = l1 * G.B;
-            // cross over the tile's lines must meet (X0 - 1, X0 + TW): t*at in (lo, hi)
-            const double lo = (double)(X0 - 1) - fmax(bA, bB) - G.a0;
-            const double hi = (double)(X0 + FP_TW) - fmin(bA, bB) - G.a0;
-            double tl = lo / G.at, th = hi / G.at;
-            if (tl > th) { const double x = tl; tl = th; th = x; }
-            const int jlo = max(0, (int)floor(tl + c0) - 1);
-            const int jhi = min(a.n_det, (int)ceil(th + c0) + 2);
-            const int W = max(0, jhi - jlo);
-            s_row[k] = row;
-            s_W[k] = W;
-            s_at[k] = G.at;
-            s_B[k] = (T)G.B;
-            // smem cross coordinate of ray jlo on the tile's first line
-            s_kap[k] = G.a0 + ((double)jlo - c0) * G.at + (double)L0 * G.B - (double)(X0 - H);
-            a.win[(long long)row * ntiles + tile_id] = make_int2(jlo, W);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int acc = 0;
-            for (int k = 0; k < nb; k++) {
-                s_cofs[k] = acc;
-                acc += (s_W[k] + 31) >> 5;
+        // ---- static window of each angle (fp_setup): rays [jlo, jlo + W) cross the tile
+        if (threadIdx.x < FP_MAXA) {
+            const int k = threadIdx.x;
+            int nch = 0;
+            if (k < nb) {
+                const int row = a.olist[b0 + k];
+                const FpWin wv = a.wins[(long long)row * ntiles + tile_id];
+                const FpRowGeo rg = a.rgeo[row];
+                s_row[k] = row;
+                s_jlo[k] = wv.jlo;
+                s_W[k] = wv.W;
+                s_kap[k] = wv.kap;
+                s_at[k] = rg.at;
+                s_B[k] = (T)rg.B;
+                nch = (wv.W + 31) >> 5;
             }
-            s_cofs[nb] = acc;
+            // exclusive prefix of the chunk counts over the (<= 64) angles: two warps
+            int inc = nch;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (lane == 31) s_wsum[warp] = inc;
+            s_cofs[k] = inc - nch;
         }
         __syncthreads();
-        const int nitems = s_cofs[nb];
+        if (threadIdx.x >= 32 && threadIdx.x < FP_MAXA) s_cofs[threadIdx.x] += s_wsum[0];
+        if (threadIdx.x == 0) s_cofs[FP_MAXA] = s_wsum[0] + s_wsum[1];
+        __syncthreads();
+        const int nitems = s_cofs[FP_MAXA];
         // ---- one warp item = 32 consecutive rays of one angle over the tile's TH lines
         for (int it = warp; it < nitems; it += FP_THREADS / 32) {
-            int lo = 0, hi = nb - 1;  // largest k with s_cofs[k] <= it
+            int lo = 0, hi = FP_MAXA - 1;  // largest k with s_cofs[k] <= it (empty angles repeat offsets)
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
                 if (s_cofs[mid] <= it) lo = mid; else hi = mid - 1;
@@ -219,41 +216,66 @@ __global__ void __launch_bounds__(FP_THREADS) fp_tile_kernel(const FpArgs<T> a) 
                     acc1 = fma(f, v1 - v0, acc1);
                 }
             }
-            if (w < W) a.partial[((long long)s_row[k] * ntiles + tile_id) * FP_WMAX + w] = acc0 + acc1;
+            if (w < W) a.partial[((long long)s_row[k] * a.nt_line + lt) * 2 * a.n_det + (ct & 1) * a.n_det + s_jlo[k] + w] = acc0 + acc1;
         }
     }
 }
 
+// ------------------------------------------------------------------ forward: static windows
+// For every (ray row, tile): the rays whose cross coordinate over the tile's real lines
+// meets (X0 - 1, X0 + TW), padded by one ray below and two above, and the shared-memory
+// cross coordinate of the first of them on the tile's first line.
+__global__ void fp_setup_kernel(const RayRow *rows, const int *xmaj, const double2 *trig, int n_rows, int N,
+                                int n_det, FpWin *wins, FpRowGeo *rgeo) {
+    const int nt_line = (N + FP_TH - 1) / FP_TH, nt_cross = (N + FP_TW - 1) / FP_TW;
+    const int ntiles = nt_line * nt_cross;
+    const int row = blockIdx.y;
+    const int ang = rows[row].angle;
+    const int O = xmaj[ang];
+    const double2 t2 = trig[ang];
+    const LineGeo G = line_geo(t2.x, t2.y, O, N);
+    const double c0 = 0.5 * (double)(n_det - 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0) rgeo[row] = FpRowGeo{G.at, G.B};
+    for (int tile = blockIdx.x * blockDim.x + threadIdx.x; tile < ntiles; tile += gridDim.x * blockDim.x) {
+        const int lt = tile / nt_cross, ct = tile % nt_cross;
+        const int L0 = lt * FP_TH, X0 = ct * FP_TW;
+        const double l1 = (double)(min(L0 + FP_TH, N) - 1);
+        const double bA = (double)L0 * G.B, bB = l1 * G.B;
+        const double lo = (double)(X0 - 1) - fmax(bA, bB) - G.a0;   // t*at in (lo, hi)
+        const double hi = (double)(X0 + FP_TW) - fmin(bA, bB) - G.a0;
+        double tl = lo / G.at, th = hi / G.at;
+        if (tl > th) { const double x = tl; tl = th; th = x; }
+        const int jlo = max(0, (int)floor(tl + c0) - 1);
+        const int jhi = min(n_det, (int)ceil(th + c0) + 2);
+        FpWin w;
+        w.jlo = jlo;
+        w.W = max(0, jhi - jlo);
+        w.kap = G.a0 + ((double)jlo - c0) * G.at + (double)L0 * G.B - (double)(X0 - FP_HALO_A);
+        wins[(long long)row * ntiles + tile] = w;
+    }
+}
+
 // ------------------------------------------------------------------ forward: reduction
-// s[row][j] = (1/m) * sum over the tiles the ray crosses (line bands in order, then
-// cross tiles in order) of the tile partials; RESID: s = d - A x.
+// s[row][j] = (1/m) * sum over line bands (in order) of the two parity slots; RESID: d - A x.
 template <typename T, bool RESID>
 __global__ void __launch_bounds__(128) fp_reduce_kernel(const FpRedArgs<T> a) {
     const int row = blockIdx.y;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= a.n_det) return;
-    const RayRow rr = a.rows[row];
-    const double2 t2 = a.trig[rr.angle];
-    const LineGeo G = line_geo(t2.x, t2.y, a.xmaj[rr.angle], a.N);
-    const double base = G.a0 + ((double)j - 0.5 * (double)(a.n_det - 1)) * G.at;
-    const int ntiles = a.nt_line * a.nt_cross;
-    const long long rbase = (long long)row * ntiles;
-    double acc = 0.0;
-    for (int lt = 0; lt < a.nt_line; lt++) {
-        const int L0 = lt * FP_TH, L1 = min(L0 + FP_TH, a.N) - 1;
-        const double cA = base + (double)L0 * G.B, cB = base + (double)L1 * G.B;
-        const double cmin = fmin(cA, cB) - 3.0, cmax = fmax(cA, cB) + 3.0;
-        if (cmax < 0.0 || cmin > (double)a.N) continue;
-        const int ct0 = max(0, (int)floor(cmin / FP_TW));
-        const int ct1 = min(a.nt_cross - 1, (int)floor(cmax / FP_TW));
-        for (int ct = ct0; ct <= ct1; ct++) {
-            const int tile = lt * a.nt_cross + ct;
-            const int2 w = a.win[rbase + tile];
-            const int jj = j - w.x;
-            if (jj >= 0 && jj < w.y) acc += (double)a.partial[(rbase + tile) * FP_WMAX + jj];
-        }
+    const int ang = a.rows[row].angle;
+    const double2 t2 = a.trig[ang];
+    const double inv_m = a.xmaj[ang] ? 1.0 / fabs(t2.y) : 1.0 / fabs(t2.x);
+    const T *p = a.partial + (long long)row * a.nt_line * 2 * a.n_det + j;
+    T acc0 = 0, acc1 = 0;
+    int lt = 0;
+    for (; lt + 2 <= a.nt_line; lt += 2) {
+        const T x0 = p[0], x1 = p[a.n_det], x2 = p[2 * a.n_det], x3 = p[3 * a.n_det];
+        acc0 += x0 + x1;
+        acc1 += x2 + x3;
+        p += 4 * a.n_det;
     }
-    T v = (T)(acc * G.inv_m);
+    if (lt < a.nt_line) acc0 += p[0] + p[a.n_det];
+    T v = (T)((double)(acc0 + acc1) * inv_m);
     if (RESID) v = a.d[(long long)row * a.n_det + j] - v;
     a.out[(long long)row * a.out_stride + a.out_off + j] = v;
 }
@@ -459,6 +481,14 @@ void launch_fp(int prec, const void *args, int L, cudaStream_t st) {
     if (L == 0) return;
     if (prec == 0) fp_dispatch<float>(*static_cast<const FpArgs<float> *>(args), L, st);
     else fp_dispatch<double>(*static_cast<const FpArgs<double> *>(args), L, st);
+    TQ_CHECK_CUDA(cudaGetLastError());
+}
+
+void launch_fp_setup(const RayRow *rows, const int *xmaj, const double2 *trig, int n_rows, int N, int n_det,
+                     FpWin *wins, FpRowGeo *rgeo, cudaStream_t st) {
+    if (n_rows == 0) return;
+    const int ntiles = fp_ntiles(N);
+    fp_setup_kernel<<<dim3(ceil_div(ntiles, 128), n_rows), 128, 0, st>>>(rows, xmaj, trig, n_rows, N, n_det, wins, rgeo);
     TQ_CHECK_CUDA(cudaGetLastError());
 }
 

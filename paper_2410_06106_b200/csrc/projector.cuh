@@ -7,9 +7,11 @@
 // image in shared memory (zero halo on both sides of the cross axis) and walks, for
 // EVERY angle of that node whose major axis matches the tile orientation, all rays
 // that cross the tile: per line of the tile one bilinear sample (2 taps) from shared
-// memory.  Each ray's partial sum over the tile goes to a scratch buffer; fp_reduce
-// adds the partials of the tiles a ray crosses in a fixed order (deterministic, no
-// atomics) and applies 1/m_a and the residual.  y-major angles walk rows of a wide
+// memory.  Each ray's partial sum over the tile goes to a dense scratch slot indexed by
+// (ray row, line band, parity of the cross tile, bin): a ray meets at most two cross
+// tiles per band, and they differ in parity, so no slot has two writers.  fp_reduce
+// adds a ray's slots in band order (deterministic, no atomics) and applies 1/m_a and
+// the residual.  y-major angles walk rows of a wide
 // tile, x-major angles walk columns of a tall tile (the transposed staging), so the
 // rays a tile touches are mostly full-length segments.  Each image pixel is read from
 // HBM/L2 once per orientation per application, for all angles of its node.
@@ -34,6 +36,17 @@ constexpr int FP_WMAX = FP_TW + FP_TH + 8;  // max rays crossing one tile for on
 constexpr int FP_THREADS = 256;
 constexpr int FP_MAXA = 64;               // angles per shared-memory batch
 
+// Static per-(ray row, tile) geometry of the forward tiles, computed once (fp_setup):
+// the window of rays [jlo, jlo + W) that cross the tile and the shared-memory cross
+// coordinate kap of ray jlo on the tile's first line (ray jlo + w sits at kap + w*at).
+struct FpWin {
+    double kap;
+    int jlo, W;
+};
+struct FpRowGeo {   // per ray row: cross step per bin and per line
+    double at, B;
+};
+
 template <typename T>
 struct FpArgs {
     const T *img;          // [L][n] node-major images
@@ -41,25 +54,23 @@ struct FpArgs {
     int N, n_det;
     const int *olist;      // ray rows grouped by (node, orientation)
     const int *oofs;       // [2L+1] offsets into olist; group g = 2*node + orientation
-    const RayRow *rows;    // [n_rows] (node, angle)
-    const double2 *trig;   // [n_angles] (cos, sin)
-    T *partial;            // [n_rows][ntiles][FP_WMAX]
-    int2 *win;             // [n_rows][ntiles] (first ray, number of rays) per (row, tile)
+    const FpWin *wins;     // [n_rows][ntiles]
+    const FpRowGeo *rgeo;  // [n_rows]
+    T *partial;            // [n_rows][nt_line][2][n_det]: band lt, cross-tile parity ct & 1
     int nt_line, nt_cross; // tiles along the major / cross axis (same for both orientations)
     uint32_t magic;        // = 0x4B000000 << 2 (mod 2^32), see projector.cu magic_base
 };
 
 template <typename T>
 struct FpRedArgs {
-    const T *partial;
-    const int2 *win;
+    const T *partial;      // as FpArgs::partial; slots no tile writes stay zero
     const RayRow *rows;
     const double2 *trig;
     const int *xmaj;
     const T *d;            // RESID: data [n_rows][n_det]
     T *out;                // [n_rows][out_stride] + out_off
     int out_stride, out_off;
-    int N, n_det, nt_line, nt_cross;
+    int N, n_det, nt_line;
 };
 
 template <typename T>
@@ -93,6 +104,9 @@ int fp_ntiles(int N);                     // tiles per orientation
 int bp_tiles(int N);
 // forward: tile pass over L nodes then the fixed-order reduction over n_rows rows
 void launch_fp(int prec, const void *args, int L, cudaStream_t st);
+// static forward geometry of n_rows rows (once per context)
+void launch_fp_setup(const RayRow *rows, const int *xmaj, const double2 *trig, int n_rows, int N, int n_det,
+                     FpWin *wins, FpRowGeo *rgeo, cudaStream_t st);
 void launch_fp_reduce(int prec, bool resid, const void *args, int n_rows, int n_det, cudaStream_t st);
 void launch_bp(int prec, int epi, const void *args, int L, int N, cudaStream_t st);
 

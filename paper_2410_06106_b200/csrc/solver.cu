@@ -67,8 +67,11 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
     if (!ol.empty()) TQ_CHECK_CUDA(cudaMemcpy(olist, ol.data(), sizeof(int) * ol.size(), cudaMemcpyHostToDevice));
     TQ_CHECK_CUDA(cudaMemcpy(oofs, of.data(), sizeof(int) * of.size(), cudaMemcpyHostToDevice));
     const size_t nwin = (size_t)n_rows * nt_line * nt_cross;
-    A(&fpart, es * nwin * FP_WMAX);
-    A((void **)&fwin, sizeof(int2) * nwin);
+    A(&fpart, es * (size_t)n_rows * nt_line * 2 * g.n_det);
+    A((void **)&fwin, sizeof(FpWin) * nwin);
+    A((void **)&frg, sizeof(FpRowGeo) * n_rows);
+    launch_fp_setup(rows, g.xmaj, g.trig, n_rows, g.N, g.n_det, fwin, frg, 0);
+    TQ_CHECK_CUDA(cudaDeviceSynchronize());
     for (void **v : {&X, &R, &P, &Q, &BP}) A(v, es * n * L);
     A(&D, es * (size_t)n_rows * g.n_det);
     A(&S, es * (size_t)n_rows * sp);
@@ -82,10 +85,10 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
 void Inner::release() {
     for (void *p : {(void *)rows, (void *)row0, (void *)nang, X, R, P, Q, BP, D, S, (void *)cnode,
                     (void *)eta, (void *)scal, (void *)partial, (void *)counter, (void *)olist,
-                    (void *)oofs, fpart, (void *)fwin})
+                    (void *)oofs, fpart, (void *)fwin, (void *)frg})
         if (p) cudaFree(p);
     rows = nullptr; row0 = nang = olist = oofs = nullptr;
-    fpart = nullptr; fwin = nullptr;
+    fpart = nullptr; fwin = nullptr; frg = nullptr;
     X = R = P = Q = BP = D = S = nullptr;
     cnode = eta = scal = partial = nullptr;
     counter = nullptr;
@@ -95,18 +98,18 @@ int Inner::project(const DevGeom &g, const void *img, bool resid, cudaStream_t s
                    int out_stride, int out_off) {
     if (!out) { out = S; out_stride = sp; out_off = 1; }
     if (prec == 0) {
-        FpArgs<float> a{(const float *)img, n, g.N, g.n_det, olist, oofs, rows, g.trig, (float *)fpart,
-                        fwin, nt_line, nt_cross, kMagicBits4};
+        FpArgs<float> a{(const float *)img, n, g.N, g.n_det, olist, oofs, fwin, frg, (float *)fpart,
+                        nt_line, nt_cross, kMagicBits4};
         launch_fp(0, &a, L, st);
-        FpRedArgs<float> r{(const float *)fpart, fwin, rows, g.trig, g.xmaj, (const float *)D, (float *)out,
-                           out_stride, out_off, g.N, g.n_det, nt_line, nt_cross};
+        FpRedArgs<float> r{(const float *)fpart, rows, g.trig, g.xmaj, (const float *)D, (float *)out,
+                           out_stride, out_off, g.N, g.n_det, nt_line};
         launch_fp_reduce(0, resid, &r, n_rows, g.n_det, st);
     } else {
-        FpArgs<double> a{(const double *)img, n, g.N, g.n_det, olist, oofs, rows, g.trig, (double *)fpart,
-                         fwin, nt_line, nt_cross, kMagicBits4};
+        FpArgs<double> a{(const double *)img, n, g.N, g.n_det, olist, oofs, fwin, frg, (double *)fpart,
+                         nt_line, nt_cross, kMagicBits4};
         launch_fp(1, &a, L, st);
-        FpRedArgs<double> r{(const double *)fpart, fwin, rows, g.trig, g.xmaj, (const double *)D,
-                            (double *)out, out_stride, out_off, g.N, g.n_det, nt_line, nt_cross};
+        FpRedArgs<double> r{(const double *)fpart, rows, g.trig, g.xmaj, (const double *)D,
+                            (double *)out, out_stride, out_off, g.N, g.n_det, nt_line};
         launch_fp_reduce(1, resid, &r, n_rows, g.n_det, st);
     }
     return 3;

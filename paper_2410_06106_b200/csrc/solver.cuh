@@ -28,8 +28,9 @@ struct Inner {
     int *nang = nullptr;       // [L]
     int *olist = nullptr;      // ray rows grouped by (node, major axis) for the forward tiles
     int *oofs = nullptr;       // [2L+1]
-    void *fpart = nullptr;     // forward partial sums [n_rows][fp_ntiles][FP_WMAX]
-    int2 *fwin = nullptr;      // [n_rows][fp_ntiles]
+    void *fpart = nullptr;     // forward partial sums [n_rows][nt_line][2][n_det] (zeroed once)
+    FpWin *fwin = nullptr;     // [n_rows][fp_ntiles] static ray windows of the forward tiles
+    FpRowGeo *frg = nullptr;   // [n_rows]
     int nt_line = 0, nt_cross = 0;
     void *X = nullptr, *R = nullptr, *P = nullptr, *Q = nullptr, *BP = nullptr;  // [L][n]
     void *D = nullptr;         // [n_rows][n_det]
