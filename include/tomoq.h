@@ -60,7 +60,8 @@ enum { TQ_Q_NONE = 0, TQ_Q_KMEANS = 1, TQ_Q_DCT = 2, TQ_Q_ALTERNATE = 3 };
 typedef struct {
     int32_t n_nodes;          /* M ADMM nodes per slice, 1 <= M <= n_angles */
     int32_t n_edges;
-    const int32_t *edges;     /* 2*n_edges node ids, undirected, no self loops / duplicates */
+    const int32_t *edges;     /* 2*n_edges node ids, undirected, no self loops / duplicates;
+                                 every node degree <= 64 (TQ_EINVAL otherwise) */
     int32_t angle_split;      /* TQ_SPLIT_* (P:319-320 round-robin; R-5 contiguous) */
     const int32_t *node_rank; /* [n_nodes] rank owning node i (all slices); NULL => i mod world */
     int32_t rule;             /* TQ_RULE_* */

@@ -101,6 +101,27 @@ __device__ __forceinline__ float floor_pos(float x, int &i) {
     return m - 8388608.0f;
 }
 
+// 4 consecutive elements through 16-byte accesses (p must be 4-element aligned)
+template <typename T>
+struct Q4 {
+    T v[4];
+};
+__device__ __forceinline__ Q4<float> ld4(const float *__restrict__ p) {
+    const float4 a = *reinterpret_cast<const float4 *>(p);
+    return Q4<float>{{a.x, a.y, a.z, a.w}};
+}
+__device__ __forceinline__ Q4<double> ld4(const double *__restrict__ p) {
+    const double2 a = reinterpret_cast<const double2 *>(p)[0], b = reinterpret_cast<const double2 *>(p)[1];
+    return Q4<double>{{a.x, a.y, b.x, b.y}};
+}
+__device__ __forceinline__ void st4(float *__restrict__ p, const Q4<float> &q) {
+    *reinterpret_cast<float4 *>(p) = make_float4(q.v[0], q.v[1], q.v[2], q.v[3]);
+}
+__device__ __forceinline__ void st4(double *__restrict__ p, const Q4<double> &q) {
+    reinterpret_cast<double2 *>(p)[0] = make_double2(q.v[0], q.v[1]);
+    reinterpret_cast<double2 *>(p)[1] = make_double2(q.v[2], q.v[3]);
+}
+
 template <typename T>
 struct Vec;  // storage helpers
 template <>
@@ -111,6 +132,8 @@ template <>
 struct Vec<double> {
     static constexpr int id = 1;
 };
+
+constexpr int TQ_MAX_DEGREE = 64;  // graph rule: neighbours per node (tq_create validates)
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 

@@ -9,27 +9,62 @@ constexpr int CT = 256;
 inline dim3 grid_of(long long n, int L) {
     return dim3((unsigned)std::max(1LL, std::min<long long>((n + CT * 4 - 1) / (CT * 4), 65535)), L);
 }
+// the graph-rule kernel covers 8 elements per thread (2 quads)
+inline dim3 grid_dual(long long n, int L) {
+    return dim3((unsigned)std::max(1LL, std::min<long long>((n + CT * 8 - 1) / (CT * 8), 65535)), L);
+}
 
+constexpr int MAXNB = TQ_MAX_DEGREE;  // neighbour pointers cached in shared memory (host-validated)
+
+template <typename T>
+__device__ __forceinline__ void graph_dual_elem(const T *const *nb, int deg, const T *own, T *al, T *bp,
+                                                long long p, double rho, int update) {
+    const double x = (double)own[p];
+    double s = 0.0;
+    for (int k = 0; k < deg; k++) s += (double)nb[k][p];
+    T a = al[p];
+    if (update) {
+        a = (T)((double)a + rho * ((double)deg * x - s));
+        al[p] = a;
+    }
+    bp[p] = (T)(-(double)a + rho * ((double)deg * x + s));
+}
+
+// one node per blockIdx.y; 4 elements per thread per step through 16-byte accesses
 template <typename T>
 __global__ void __launch_bounds__(CT) graph_dual(const T *const *xh, const int *own_slot,
                                                  const int *nbr_off, const int *nbr_slot, T *alpha,
                                                  T *bprime, long long n, double rho, int update) {
+    __shared__ const T *nb[MAXNB];
     const int i = blockIdx.y;
     const T *own = xh[own_slot[i]];
-    const int k0 = nbr_off[i], k1 = nbr_off[i + 1];
-    const double deg = (double)(k1 - k0);
+    const int k0 = nbr_off[i], deg = nbr_off[i + 1] - k0;
+    for (int k = threadIdx.x; k < deg; k += CT) nb[k] = xh[nbr_slot[k0 + k]];
+    __syncthreads();
     T *al = alpha + (long long)i * n;
     T *bp = bprime + (long long)i * n;
-    for (long long p = (long long)blockIdx.x * CT + threadIdx.x; p < n; p += (long long)gridDim.x * CT) {
-        const double x = (double)own[p];
-        double s = 0.0;
-        for (int k = k0; k < k1; k++) s += (double)xh[nbr_slot[k]][p];
-        T a = al[p];
-        if (update) {
-            a = (T)((double)a + rho * (deg * x - s));
-            al[p] = a;
+    if ((n & 3) == 0) {
+        for (long long p = 4 * ((long long)blockIdx.x * CT + threadIdx.x); p < n; p += 4LL * gridDim.x * CT) {
+            const Q4<T> xv = ld4(own + p);
+            Q4<T> av = ld4(al + p), bv;
+            double s[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int k = 0; k < deg; k++) {
+                const Q4<T> y = ld4(nb[k] + p);
+#pragma unroll
+                for (int u = 0; u < 4; u++) s[u] += (double)y.v[u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const double x = (double)xv.v[u];
+                if (update) av.v[u] = (T)((double)av.v[u] + rho * ((double)deg * x - s[u]));
+                bv.v[u] = (T)(-(double)av.v[u] + rho * ((double)deg * x + s[u]));
+            }
+            if (update) st4(al + p, av);
+            st4(bp + p, bv);
         }
-        bp[p] = (T)(-(double)a + rho * (deg * x + s));
+    } else {
+        for (long long p = (long long)blockIdx.x * CT + threadIdx.x; p < n; p += (long long)gridDim.x * CT)
+            graph_dual_elem(nb, deg, own, al, bp, p, rho, update);
     }
 }
 
@@ -88,11 +123,11 @@ int launch_graph_dual(int prec, const void *const *xh_tab, const int *own_slot, 
                       int update_alpha, cudaStream_t st) {
     if (L == 0) return 0;
     if (prec == 0)
-        graph_dual<float><<<grid_of(n, L), CT, 0, st>>>((const float *const *)xh_tab, own_slot, nbr_off,
+        graph_dual<float><<<grid_dual(n, L), CT, 0, st>>>((const float *const *)xh_tab, own_slot, nbr_off,
                                                         nbr_slot, (float *)alpha, (float *)bprime, n, rho,
                                                         update_alpha);
     else
-        graph_dual<double><<<grid_of(n, L), CT, 0, st>>>((const double *const *)xh_tab, own_slot, nbr_off,
+        graph_dual<double><<<grid_dual(n, L), CT, 0, st>>>((const double *const *)xh_tab, own_slot, nbr_off,
                                                          nbr_slot, (double *)alpha, (double *)bprime, n,
                                                          rho, update_alpha);
     TQ_CHECK_CUDA(cudaGetLastError());

@@ -154,6 +154,8 @@ void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int ran
         adj[i].push_back(j);
         adj[j].push_back(i);
     }
+    for (int i = 0; i < M; i++)
+        TQ_REQUIRE((int)adj[i].size() <= TQ_MAX_DEGREE, "graph rule: node degree must be <= 64");
     if (rule == TQ_RULE_GRAPH && M > 1) {  // connected graph (consensus reaches every node)
         std::vector<int> stack{0}, vis(M, 0);
         vis[0] = 1;

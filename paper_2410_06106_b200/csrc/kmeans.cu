@@ -2,21 +2,23 @@
 //
 // Sort-based exact Lloyd.  Each payload's values are mapped to order-preserving
 // 32-bit keys and sorted by an LSD radix sort (4 passes of 8-bit digits: per-tile
-// digit histograms, per-payload offset scan, stable tile sort + scatter).  On the
-// sorted keys:
+// digit histograms stored digit-major, one exclusive scan per payload over
+// (digit, tile) = the global output offsets, stable match-based tile ranking +
+// scatter).  On the sorted keys:
 //   * the quantile init c_k = v_(floor((2k+1) n / 2K)) is a direct read (exact order
 //     statistic);
 //   * a Lloyd step needs, for each threshold b_k, C_k = #{v <= b_k} and
 //     S_k = sum_{v <= b_k} fix(v): C_k is an upper bound in the sorted keys (binary
-//     search over the tile heads in shared memory, then one warp counts inside one
-//     2048-key tile), S_k = (exclusive prefix of the tile sums) + the in-tile part.
+//     search over the tile heads in shared memory, a warp ballot over the 32 chunk
+//     heads of that tile, then one warp counts inside one 64-key chunk),
+//     S_k = (exclusive prefix of the chunk sums) + the in-chunk part.
 //     Cluster k = (b_{k-1}, b_k], i.e. label(v) = #{k : v > b_k}, ties to the lower
 //     cluster -- the same decision the oracle takes per element.
 // fix(v) = round(v 2^F) as int64 with F chosen from max|v| and n so no sum overflows:
 // cluster sums are exact integers, hence independent of summation order.
 // All Lloyd iterations of a payload run in one CTA; the cost of an iteration no
 // longer depends on n.  The final assignment packs labels into bit-planes.
-#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_radix_rank.cuh>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
@@ -31,6 +33,9 @@ constexpr int KI = 8;                 // keys per thread
 constexpr int KTILE = KT * KI;        // keys per tile
 constexpr int LT = 1024;              // threads of the Lloyd kernel
 constexpr int MAX_TILES = 8192;       // per payload (n <= 16.7 M)
+constexpr int KCH = 64;               // keys per prefix-sum chunk
+constexpr int CPT = KTILE / KCH;      // chunks per tile (32)
+static_assert(CPT == 32, "one warp lane per chunk head");
 
 __device__ __forceinline__ uint32_t f2key(float f) {
     if (f == 0.0f) f = 0.0f;  // -0 and +0 are the same value for every comparison
@@ -52,8 +57,8 @@ __device__ __forceinline__ int kmeans_label(float v, const float *thr, int K) {
 }
 
 struct KmPtr {
-    uint32_t *keysA, *keysB, *hist, *base;
-    long long *tsum;
+    uint32_t *keysA, *keysB, *hist, *dtot;
+    long long *csum, *cpre;
     float *cen, *thr;
     int *fexp;
     int K, T;
@@ -61,7 +66,7 @@ struct KmPtr {
 };
 
 KmPtr ptrs(const KmeansWork &w) {
-    return KmPtr{w.keysA, w.keysB, w.hist, w.base, w.tsum, w.cen, w.thr, w.fexp, w.K, w.T, w.nv};
+    return KmPtr{w.keysA, w.keysB, w.hist, w.dtot, w.csum, w.cpre, w.cen, w.thr, w.fexp, w.K, w.T, w.nv};
 }
 
 __device__ __forceinline__ void load_tile(const uint32_t *keys, long long off, uint32_t (&k)[KI]) {
@@ -82,9 +87,11 @@ __device__ __forceinline__ void tile_hist(const uint32_t (&k)[KI], int shift, ui
     }
 }
 
-__device__ __forceinline__ void flush_hist(uint32_t *sh, uint32_t *g) {
+// digit-major [P][256][T]: the exclusive scan of a payload's row-major counts is the
+// global output offset of (digit, tile)
+__device__ __forceinline__ void flush_hist(const uint32_t *sh, uint32_t *hp, int T, int t) {
     __syncthreads();
-    g[threadIdx.x] = sh[threadIdx.x];  // KT == 256 digits
+    hp[(long long)threadIdx.x * T + t] = sh[threadIdx.x];  // KT == 256 digits
 }
 
 // keys of the raw payload (padding keys sort last) + digit-0 histogram
@@ -102,7 +109,7 @@ __global__ void __launch_bounds__(KT) km_keys(const float *const *vin, KmPtr w) 
     o[0] = make_uint4(k[0], k[1], k[2], k[3]);
     o[1] = make_uint4(k[4], k[5], k[6], k[7]);
     tile_hist(k, 0, sh);
-    flush_hist(sh, w.hist + ((long long)b * w.T + t) * 256);
+    flush_hist(sh, w.hist + (long long)b * 256 * w.T, w.T, t);
 }
 
 __global__ void __launch_bounds__(KT) km_hist(const uint32_t *keys, KmPtr w, int shift) {
@@ -113,60 +120,72 @@ __global__ void __launch_bounds__(KT) km_hist(const uint32_t *keys, KmPtr w, int
     uint32_t k[KI];
     load_tile(keys, ((long long)b * w.T + t) * KTILE, k);
     tile_hist(k, shift, sh);
-    flush_hist(sh, w.hist + ((long long)b * w.T + t) * 256);
+    flush_hist(sh, w.hist + (long long)b * 256 * w.T, w.T, t);
 }
 
-// per payload: hist[t][d] <- sum_{t' < t} hist[t'][d]; base[d] <- sum_{d' < d} total[d']
-__global__ void __launch_bounds__(256) km_scan(KmPtr w) {
-    using Scan = cub::BlockScan<uint32_t, 256>;
-    __shared__ typename Scan::TempStorage tmp;
-    const int b = blockIdx.x, d = threadIdx.x;
-    uint32_t *h = w.hist + (long long)b * w.T * 256 + d;
-    uint32_t run = 0;
-    int t = 0;
-    for (; t + 4 <= w.T; t += 4) {
-        const uint32_t c0 = h[(t + 0) * 256], c1 = h[(t + 1) * 256], c2 = h[(t + 2) * 256], c3 = h[(t + 3) * 256];
-        h[(t + 0) * 256] = run; run += c0;
-        h[(t + 1) * 256] = run; run += c1;
-        h[(t + 2) * 256] = run; run += c2;
-        h[(t + 3) * 256] = run; run += c3;
+// exclusive scan along the tiles of each (payload, digit) row of the digit-major
+// counts, in place; the row total goes to dtot[payload][digit].  One warp per row,
+// lanes strided over the tiles (coalesced), rounds chained by a carry.
+constexpr int SCW = 8;  // rows (warps) per CTA
+__global__ void __launch_bounds__(SCW * 32) km_scan(KmPtr w) {
+    const int b = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int d = blockIdx.x * SCW + warp;
+    uint32_t *h = w.hist + ((long long)b * 256 + d) * w.T;
+    uint32_t carry = 0;
+    for (int t0 = 0; t0 < w.T; t0 += 128) {
+        uint32_t c[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int t = t0 + 32 * u + lane;
+            c[u] = t < w.T ? h[t] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            uint32_t inc = c[u];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            const int t = t0 + 32 * u + lane;
+            if (t < w.T) h[t] = carry + inc - c[u];
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
     }
-    for (; t < w.T; t++) {
-        const uint32_t c = h[t * 256];
-        h[t * 256] = run;
-        run += c;
-    }
-    uint32_t excl;
-    Scan(tmp).ExclusiveSum(run, excl);
-    w.base[(long long)b * 256 + d] = excl;
+    if (lane == 0) w.dtot[(long long)b * 256 + d] = carry;
 }
 
-// stable sort of the tile by the digit, then scatter to base[d] + tile offset + rank
+struct DigitOf {
+    uint32_t shift;
+    __device__ __forceinline__ uint32_t Digit(uint32_t k) const { return (k >> shift) & 255u; }
+};
+
+// stable rank of the tile's keys by the digit (match-based, warp-striped input), then
+// scatter to offset(digit, tile) + (rank - first rank of the digit in the tile)
 __global__ void __launch_bounds__(KT) km_scatter(const uint32_t *kin, uint32_t *kout, KmPtr w, int shift) {
-    using Sort = cub::BlockRadixSort<uint32_t, KT, KI>;
-    __shared__ typename Sort::TempStorage tmp;
-    __shared__ uint32_t dstart[256], goff[256], lastd[KT];
+    using Rank = cub::BlockRadixRankMatch<KT, 8, false>;
+    using Scan = cub::BlockScan<uint32_t, KT>;
+    __shared__ typename Rank::TempStorage tmp;
+    __shared__ typename Scan::TempStorage stmp;
+    __shared__ uint32_t dstart[256], goff[256];
     const int b = blockIdx.y, t = blockIdx.x;
     const long long pb = (long long)b * w.T * KTILE;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t *src = kin + pb + (long long)t * KTILE + warp * 32 * KI + lane;
     uint32_t k[KI];
-    load_tile(kin, pb + (long long)t * KTILE, k);
-    goff[threadIdx.x] = w.base[(long long)b * 256 + threadIdx.x] +
-                        w.hist[((long long)b * w.T + t) * 256 + threadIdx.x];
-    Sort(tmp).Sort(k, shift, shift + 8);  // blocked arrangement, stable
-    lastd[threadIdx.x] = (k[KI - 1] >> shift) & 255u;
-    __syncthreads();
-    uint32_t prev = threadIdx.x ? lastd[threadIdx.x - 1] : 0xffffffffu;
 #pragma unroll
-    for (int r = 0; r < KI; r++) {
-        const uint32_t d = (k[r] >> shift) & 255u;
-        if (d != prev) dstart[d] = threadIdx.x * KI + r;
-        prev = d;
-    }
+    for (int r = 0; r < KI; r++) k[r] = src[r * 32];  // warp-striped
+    uint32_t base;
+    Scan(stmp).ExclusiveSum(w.dtot[(long long)b * 256 + threadIdx.x], base);
+    goff[threadIdx.x] = base + w.hist[((long long)b * 256 + threadIdx.x) * w.T + t];
+    int rank[KI], pre[1];
+    Rank(tmp).RankKeys(k, rank, DigitOf{(uint32_t)shift}, pre);
+    dstart[threadIdx.x] = (uint32_t)pre[0];
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < KI; r++) {
         const uint32_t d = (k[r] >> shift) & 255u;
-        kout[pb + goff[d] + (threadIdx.x * KI + r - dstart[d])] = k[r];
+        kout[pb + goff[d] + ((uint32_t)rank[r] - dstart[d])] = k[r];
     }
 }
 
@@ -180,10 +199,8 @@ __device__ __forceinline__ int fixed_exp(const uint32_t *sorted, long long nv) {
     return 62 - E - lg;
 }
 
-// per-tile sums of fix(v) over the sorted keys
-__global__ void __launch_bounds__(KT) km_tsum(KmPtr w) {
-    using Red = cub::BlockReduce<long long, KT>;
-    __shared__ typename Red::TempStorage tmp;
+// per-chunk (64 keys) sums of fix(v) over the sorted keys
+__global__ void __launch_bounds__(KT) km_csum(KmPtr w) {
     const int b = blockIdx.y, t = blockIdx.x;
     const uint32_t *sorted = w.keysA + (long long)b * w.T * KTILE;
     const int F = fixed_exp(sorted, w.nv);
@@ -195,11 +212,10 @@ __global__ void __launch_bounds__(KT) km_tsum(KmPtr w) {
 #pragma unroll
     for (int r = 0; r < KI; r++)
         if (i0 + r < w.nv) s += __double2ll_rn((double)key2f(k[r]) * scale);
-    const long long tot = Red(tmp).Sum(s);
-    if (threadIdx.x == 0) {
-        w.tsum[(long long)b * w.T + t] = tot;
-        if (t == 0) w.fexp[b] = F;
-    }
+#pragma unroll
+    for (int o = 1; o < KCH / KI; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);  // 8 lanes per chunk
+    if ((threadIdx.x & (KCH / KI - 1)) == 0) w.csum[(long long)b * w.T * CPT + (long long)t * CPT + threadIdx.x / (KCH / KI)] = s;
+    if (t == 0 && threadIdx.x == 0) w.fexp[b] = F;
 }
 
 // one CTA per payload: quantile init, then `iters` exact Lloyd steps on the sorted keys
@@ -207,37 +223,31 @@ __global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters) {
     using Scan = cub::BlockScan<long long, LT>;
     __shared__ typename Scan::TempStorage tmp;
     extern __shared__ __align__(16) unsigned char lsm[];
-    long long *tpre = reinterpret_cast<long long *>(lsm);         // [T + 1]
-    uint32_t *thead = reinterpret_cast<uint32_t *>(tpre + w.T + 1);  // [T]
+    uint32_t *thead = reinterpret_cast<uint32_t *>(lsm);  // [T] first key of each tile
     __shared__ float cen[256], thr[256];
-    __shared__ long long Cs[256], Ss[256];
+    __shared__ long long Cs[256], Ss[256], total_s;
     const int b = blockIdx.x, K = w.K, T = w.T;
-    const long long nv = w.nv;
+    const long long nv = w.nv, nch = (long long)T * CPT;
     const uint32_t *sorted = w.keysA + (long long)b * T * KTILE;
-    const long long *ts = w.tsum + (long long)b * T;
-    const int F = w.fexp[b];
-    const double scale = ldexp(1.0, F);
-    // exclusive prefix of the tile sums (chunked block scan) and the tile head keys
+    const long long *cs = w.csum + (long long)b * nch;
+    long long *cp = w.cpre + (long long)b * nch;
+    const double scale = ldexp(1.0, w.fexp[b]);
+    // exclusive prefix of the chunk sums (global) and the tile head keys (shared)
     long long carry = 0;
-    for (int c0 = 0; c0 < T; c0 += LT) {
-        const int t = c0 + threadIdx.x;
-        const long long x = t < T ? ts[t] : 0;
+    for (long long c0 = 0; c0 < nch; c0 += LT) {
+        const long long c = c0 + threadIdx.x;
+        const long long x = c < nch ? cs[c] : 0;
         long long ex, agg;
         Scan(tmp).ExclusiveSum(x, ex, agg);
-        if (t < T) {
-            tpre[t] = carry + ex;
-            thead[t] = sorted[(long long)t * KTILE];
-        }
+        if (c < nch) cp[c] = carry + ex;
         carry += agg;
         __syncthreads();
     }
-    if (threadIdx.x == 0) tpre[T] = carry;
+    for (int t = threadIdx.x; t < T; t += LT) thead[t] = sorted[(long long)t * KTILE];
+    if (threadIdx.x == 0) total_s = carry;
     // quantile init: c_k = v_(floor((2k+1) nv / 2K))
-    for (int k = threadIdx.x; k < K; k += LT) {
-        const long long idx = ((long long)(2 * k + 1) * nv) / (2LL * K);
-        cen[k] = key2f(sorted[idx]);
-    }
-    __syncthreads();
+    for (int k = threadIdx.x; k < K; k += LT) cen[k] = key2f(sorted[((long long)(2 * k + 1) * nv) / (2LL * K)]);
+    __syncthreads();  // also orders the cpre stores before the loads below (same CTA)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int it = 0; it < iters; it++) {
         for (int k = threadIdx.x; k + 1 < K; k += LT) thr[k] = (float)(((double)cen[k] + (double)cen[k + 1]) * 0.5);
@@ -251,37 +261,31 @@ __global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters) {
             }
             long long C = 0, S = 0;
             if (tt >= 0) {
-                const long long off = (long long)tt * KTILE;
+                const long long tb = (long long)tt * KTILE;
+                // last chunk of the tile whose head key <= kb (chunk 0 qualifies)
+                const unsigned m = __ballot_sync(0xffffffffu, sorted[tb + lane * KCH] <= kb);
+                const int cc = 31 - __clz(m);
+                const long long cb = tb + (long long)cc * KCH;
+                const uint32_t e0 = sorted[cb + lane], e1 = sorted[cb + 32 + lane];
+                const long long pre = cp[(long long)tt * CPT + cc];
                 int cnt = 0;
                 long long s = 0;
-                const uint4 *p = reinterpret_cast<const uint4 *>(sorted + off);
-#pragma unroll 4
-                for (int q = lane; q < KTILE / 4; q += 32) {
-                    const uint4 v4 = p[q];
-                    const uint32_t e[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const long long i = off + 4 * q + u;
-                        if (e[u] <= kb && i < nv) {
-                            cnt++;
-                            s += __double2ll_rn((double)key2f(e[u]) * scale);
-                        }
-                    }
-                }
+                if (e0 <= kb && cb + lane < nv) { cnt++; s += __double2ll_rn((double)key2f(e0) * scale); }
+                if (e1 <= kb && cb + 32 + lane < nv) { cnt++; s += __double2ll_rn((double)key2f(e1) * scale); }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
                     cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
                     s += __shfl_xor_sync(0xffffffffu, s, o);
                 }
-                C = off + cnt;
-                S = tpre[tt] + s;
+                C = cb + cnt;
+                S = pre + s;
             }
             if (lane == 0) { Cs[k] = C; Ss[k] = S; }
         }
         __syncthreads();
         for (int k = threadIdx.x; k < K; k += LT) {
             const long long c1 = k + 1 < K ? Cs[k] : nv, c0 = k ? Cs[k - 1] : 0;
-            const long long s1 = k + 1 < K ? Ss[k] : tpre[T], s0 = k ? Ss[k - 1] : 0;
+            const long long s1 = k + 1 < K ? Ss[k] : total_s, s0 = k ? Ss[k - 1] : 0;
             if (c1 > c0) cen[k] = (float)(((double)(s1 - s0) / scale) / (double)(c1 - c0));
         }
         __syncthreads();
@@ -292,12 +296,16 @@ __global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters) {
     }
 }
 
-__global__ void __launch_bounds__(KT) km_final(const float *const *vin, KmPtr w, int B,
-                                               uint8_t *const *pay, int32_t *const *labels_tab) {
+// final assignment: label(v) = #{k : v > thr[k]} by a branchless search over the
+// thresholds padded with +inf to 2^B - 1 entries; lane `bit` stores bit-plane `bit`
+// of its warp's 32-element group.  U groups per warp per step (loads in flight).
+template <int B>
+__global__ void __launch_bounds__(KT) km_final(const float *const *vin, KmPtr w, uint8_t *const *pay,
+                                               int32_t *const *labels_tab) {
     __shared__ float thr_s[256];
     const int b = blockIdx.y;
     const int K = w.K;
-    for (int k = threadIdx.x; k + 1 < K; k += KT) thr_s[k] = w.thr[(long long)b * K + k];
+    for (int k = threadIdx.x; k < 256; k += KT) thr_s[k] = (k + 1 < K) ? w.thr[(long long)b * K + k] : INFINITY;
     float *cen_out = reinterpret_cast<float *>(pay[b]);
     uint32_t *planes = reinterpret_cast<uint32_t *>(pay[b] + 4 * (long long)K);
     int32_t *labels = labels_tab ? labels_tab[b] : nullptr;
@@ -305,41 +313,81 @@ __global__ void __launch_bounds__(KT) km_final(const float *const *vin, KmPtr w,
         for (int k = threadIdx.x; k < K; k += KT) cen_out[k] = w.cen[(long long)b * K + k];
     __syncthreads();
     const float *vb = vin[b];
-    const long long G = (w.nv + 31) / 32;
+    const long long nv = w.nv;
+    const long long G = (nv + 31) / 32;
     const int lane = threadIdx.x & 31;
     const long long warp0 = ((long long)blockIdx.x * KT + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * KT) >> 5;
-    for (long long g = warp0; g < G; g += nwarps) {
-        const long long i = g * 32 + lane;
-        int l = 0;
-        if (i < w.nv) {
-            l = kmeans_label(vb[i], thr_s, K);
-            if (labels) labels[i] = l;
+    constexpr int U = 4;
+    for (long long g0 = warp0 * U; g0 < G; g0 += nwarps * U) {  // warp-uniform
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const long long i = (g0 + u) * 32 + lane;
+            v[u] = i < nv ? __ldg(vb + i) : 0.0f;
         }
-        for (int bit = 0; bit < B; bit++) {
-            const unsigned word = __ballot_sync(0xffffffffu, (l >> bit) & 1);
-            if (lane == 0) planes[g * B + bit] = word;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            int l = 0;
+#pragma unroll
+            for (int step = (1 << B) >> 1; step > 0; step >>= 1) l += (v[u] > thr_s[l + step - 1]) ? step : 0;
+            const long long i = (g0 + u) * 32 + lane;
+            if (labels && i < nv) labels[i] = l;
+            uint32_t mine = 0;
+#pragma unroll
+            for (int bit = 0; bit < B; bit++) {
+                const uint32_t word = __ballot_sync(0xffffffffu, (l >> bit) & 1);
+                mine = lane == bit ? word : mine;
+            }
+            if (lane < B && g0 + u < G) planes[(g0 + u) * B + lane] = mine;
         }
     }
 }
 
-template <typename T>
-__global__ void km_decode(const uint8_t *const *pay, long long nv, int K, int B, T *const *outp) {
+template <int B, typename T>
+__global__ void __launch_bounds__(256) km_decode(const uint8_t *const *pay, long long nv, int K, T *const *outp) {
+    __shared__ float c[256];
     const int b = blockIdx.y;
-    const float *c = reinterpret_cast<const float *>(pay[b]);
+    for (int k = threadIdx.x; k < K; k += 256) c[k] = reinterpret_cast<const float *>(pay[b])[k];
+    __syncthreads();
     const uint32_t *pl = reinterpret_cast<const uint32_t *>(pay[b] + 4 * (long long)K);
     T *out = outp[b];
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long g = i >> 5;
-        const int lane = (int)(i & 31);
-        int l = 0;
-        for (int bit = 0; bit < B; bit++) l |= (int)((__ldg(pl + g * B + bit) >> lane) & 1u) << bit;
-        out[i] = (T)c[l];
+    const int lane = threadIdx.x & 31;
+    const long long G = (nv + 31) / 32;
+    const long long warp0 = ((long long)blockIdx.x * 256 + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * 256) >> 5;
+    constexpr int U = 4;  // groups per warp per step, plane loads in flight
+    for (long long g0 = warp0 * U; g0 < G; g0 += nwarps * U) {
+        uint32_t word[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) word[u] = (lane < B && g0 + u < G) ? __ldg(pl + (g0 + u) * B + lane) : 0u;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            int l = 0;
+#pragma unroll
+            for (int bit = 0; bit < B; bit++) l |= (int)((__shfl_sync(0xffffffffu, word[u], bit) >> lane) & 1u) << bit;
+            const long long i = (g0 + u) * 32 + lane;
+            if (i < nv) out[i] = (T)c[l];
+        }
     }
 }
 
-size_t lloyd_smem(int T) { return sizeof(long long) * (T + 1) + sizeof(uint32_t) * T; }
+template <typename F>
+void with_bits(int B, F &&f) {
+    switch (B) {
+        case 0: f(std::integral_constant<int, 0>()); break;
+        case 1: f(std::integral_constant<int, 1>()); break;
+        case 2: f(std::integral_constant<int, 2>()); break;
+        case 3: f(std::integral_constant<int, 3>()); break;
+        case 4: f(std::integral_constant<int, 4>()); break;
+        case 5: f(std::integral_constant<int, 5>()); break;
+        case 6: f(std::integral_constant<int, 6>()); break;
+        case 7: f(std::integral_constant<int, 7>()); break;
+        default: f(std::integral_constant<int, 8>()); break;
+    }
+}
+
+size_t lloyd_smem(int T) { return sizeof(uint32_t) * T; }
 
 }  // namespace
 
@@ -362,8 +410,9 @@ void KmeansWork::alloc(int P_, int K_, long long nv_) {
     TQ_CHECK_CUDA(cudaMalloc(&keysA, sizeof(uint32_t) * nk));
     TQ_CHECK_CUDA(cudaMalloc(&keysB, sizeof(uint32_t) * nk));
     TQ_CHECK_CUDA(cudaMalloc(&hist, sizeof(uint32_t) * (size_t)P * T * 256));
-    TQ_CHECK_CUDA(cudaMalloc(&base, sizeof(uint32_t) * (size_t)P * 256));
-    TQ_CHECK_CUDA(cudaMalloc(&tsum, sizeof(long long) * (size_t)P * T));
+    TQ_CHECK_CUDA(cudaMalloc(&dtot, sizeof(uint32_t) * (size_t)P * 256));
+    TQ_CHECK_CUDA(cudaMalloc(&csum, sizeof(long long) * (size_t)P * T * CPT));
+    TQ_CHECK_CUDA(cudaMalloc(&cpre, sizeof(long long) * (size_t)P * T * CPT));
     TQ_CHECK_CUDA(cudaMalloc(&cen, sizeof(float) * P * K));
     TQ_CHECK_CUDA(cudaMalloc(&thr, sizeof(float) * P * K));
     TQ_CHECK_CUDA(cudaMalloc(&fexp, sizeof(int) * P));
@@ -371,7 +420,7 @@ void KmeansWork::alloc(int P_, int K_, long long nv_) {
 }
 
 void KmeansWork::release() {
-    for (void *p : {(void *)keysA, (void *)keysB, (void *)hist, (void *)base, (void *)tsum, (void *)cen,
+    for (void *p : {(void *)keysA, (void *)keysB, (void *)hist, (void *)dtot, (void *)csum, (void *)cpre, (void *)cen,
                     (void *)thr, (void *)fexp})
         if (p) cudaFree(p);
     *this = KmeansWork();
@@ -388,18 +437,18 @@ int kmeans_encode(const float *const *v, KmeansWork &ws, int lloyd, uint8_t *con
     uint32_t *src = ws.keysA, *dst = ws.keysB;
     for (int pass = 0; pass < 4; pass++) {
         if (pass) { km_hist<<<tiles, KT, 0, st>>>(src, w, 8 * pass); k++; }
-        km_scan<<<P, 256, 0, st>>>(w);
+        km_scan<<<dim3(256 / SCW, P), SCW * 32, 0, st>>>(w);
         km_scatter<<<tiles, KT, 0, st>>>(src, dst, w, 8 * pass);
         k += 2;
         std::swap(src, dst);
     }
     // four passes: A -> B -> A -> B -> A, sorted keys in keysA
-    km_tsum<<<tiles, KT, 0, st>>>(w);
+    km_csum<<<tiles, KT, 0, st>>>(w);
     km_lloyd<<<P, LT, lloyd_smem(ws.T), st>>>(w, lloyd);
     long long want = std::max(1LL, (148LL * 8 + P - 1) / P);
-    long long need = (ws.nv + KT * 4 - 1) / (KT * 4);
+    long long need = (ws.nv + KT * 16 - 1) / (KT * 16);
     const dim3 grid((unsigned)std::max(1LL, std::min(want, need)), P);
-    km_final<<<grid, KT, 0, st>>>(v, w, ws.B, pay, labels);
+    with_bits(ws.B, [&](auto Bc) { km_final<decltype(Bc)::value><<<grid, KT, 0, st>>>(v, w, pay, labels); });
     TQ_CHECK_CUDA(cudaGetLastError());
     return k + 3;
 }
@@ -408,11 +457,12 @@ int kmeans_decode(const uint8_t *const *pay, int P, long long nv, int K, int pre
                   void *const *out, cudaStream_t st) {
     if (P == 0) return 0;
     const int B = kmeans_bits(K);
-    const dim3 grid((unsigned)std::min<long long>(1024, (nv + 255) / 256), P);
-    if (prec == 0)
-        km_decode<float><<<grid, 256, 0, st>>>(pay, nv, K, B, (float *const *)out);
-    else
-        km_decode<double><<<grid, 256, 0, st>>>(pay, nv, K, B, (double *const *)out);
+    const dim3 grid((unsigned)std::max(1LL, std::min<long long>(1184 / P + 1, (nv + 255) / 256)), P);
+    with_bits(B, [&](auto Bc) {
+        constexpr int BB = decltype(Bc)::value;
+        if (prec == 0) km_decode<BB, float><<<grid, 256, 0, st>>>(pay, nv, K, (float *const *)out);
+        else km_decode<BB, double><<<grid, 256, 0, st>>>(pay, nv, K, (double *const *)out);
+    });
     TQ_CHECK_CUDA(cudaGetLastError());
     return 1;
 }

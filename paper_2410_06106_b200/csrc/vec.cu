@@ -5,33 +5,61 @@ namespace tq {
 
 namespace {
 constexpr int VT = 256;  // threads
-constexpr int VE = 4;    // elements per thread
+constexpr int VE = 8;    // elements per thread: two 16-byte quads of every operand in flight
 }
 
 int vec_blocks(long long n) { return ceil_div(n, (long long)VT * VE); }
 
+// Element e of thread t in block b: quads at b*VT*VE + {0, VT*4} + 4t (coalesced 16-byte
+// accesses).  n % 4 != 0 (odd-size stateless calls) takes the scalar path.
+template <typename F4, typename F1>
+__device__ __forceinline__ void vec_loop(long long n, F4 &&body4, F1 &&body1) {
+    if ((n & 3) == 0) {
+#pragma unroll
+        for (int h = 0; h < VE / 4; h++) {
+            const long long i = (long long)blockIdx.x * VT * VE + h * VT * 4 + 4 * threadIdx.x;
+            if (i < n) body4(i);
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < VE; e++) {
+            const long long i = (long long)blockIdx.x * VT * VE + e * VT + threadIdx.x;
+            if (i < n) body1(i);
+        }
+    }
+}
+
 template <typename T>
-__global__ void __launch_bounds__(VT) cg_update_xr(T *x, T *r, const T *p, const T *q, long long n,
-                                                   double *scal, double *partial, int part_stride,
-                                                   unsigned *counter) {
+__global__ void __launch_bounds__(VT) cg_update_xr(T *__restrict__ x, T *__restrict__ r, const T *__restrict__ p,
+                                                   const T *__restrict__ q, long long n, double *scal,
+                                                   double *partial, int part_stride, unsigned *counter) {
     __shared__ double red[VT / 32 + 1];
     __shared__ bool last;
     const int node = blockIdx.y;
     const long long base = (long long)node * n;
     double *sc = scal + (long long)node * S_NSLOT;
     const double alpha = sc[S_ALPHA];
+    x += base; r += base; p += base; q += base;
     double dot = 0.0;
+    vec_loop(n,
+        [&](long long i) {
+            Q4<T> xv = ld4(x + i), rv = ld4(r + i);
+            const Q4<T> pv = ld4(p + i), qv = ld4(q + i);
 #pragma unroll
-    for (int e = 0; e < VE; e++) {
-        const long long i = (long long)blockIdx.x * VT * VE + e * VT + threadIdx.x;
-        if (i < n) {
-            const long long g = base + i;
-            x[g] = (T)((double)x[g] + alpha * (double)p[g]);
-            const T rv = (T)((double)r[g] - alpha * (double)q[g]);
-            r[g] = rv;
+            for (int u = 0; u < 4; u++) {
+                xv.v[u] = (T)((double)xv.v[u] + alpha * (double)pv.v[u]);
+                rv.v[u] = (T)((double)rv.v[u] - alpha * (double)qv.v[u]);
+                dot += (double)rv.v[u] * (double)rv.v[u];
+            }
+            st4(x + i, xv);
+            st4(r + i, rv);
+        },
+        [&](long long i) {
+            x[i] = (T)((double)x[i] + alpha * (double)p[i]);
+            const T rv = (T)((double)r[i] - alpha * (double)q[i]);
+            r[i] = rv;
             dot += (double)rv * (double)rv;
-        }
-    }
+        });
     const double bs = block_sum<VT>(dot, red);
     double *part = partial + (long long)node * part_stride;
     if (threadIdx.x == 0) part[blockIdx.x] = bs;
@@ -49,36 +77,38 @@ __global__ void __launch_bounds__(VT) cg_update_xr(T *x, T *r, const T *p, const
 }
 
 template <typename T>
-__global__ void __launch_bounds__(VT) cg_update_p(T *p, const T *r, long long n, const double *scal) {
+__global__ void __launch_bounds__(VT) cg_update_p(T *__restrict__ p, const T *__restrict__ r, long long n,
+                                                  const double *scal) {
     const int node = blockIdx.y;
     const long long base = (long long)node * n;
     const double beta = scal[(long long)node * S_NSLOT + S_BETA];
+    p += base; r += base;
+    vec_loop(n,
+        [&](long long i) {
+            Q4<T> pv = ld4(p + i);
+            const Q4<T> rv = ld4(r + i);
 #pragma unroll
-    for (int e = 0; e < VE; e++) {
-        const long long i = (long long)blockIdx.x * VT * VE + e * VT + threadIdx.x;
-        if (i < n) {
-            const long long g = base + i;
-            p[g] = (T)((double)r[g] + beta * (double)p[g]);
-        }
-    }
+            for (int u = 0; u < 4; u++) pv.v[u] = (T)((double)rv.v[u] + beta * (double)pv.v[u]);
+            st4(p + i, pv);
+        },
+        [&](long long i) { p[i] = (T)((double)r[i] + beta * (double)p[i]); });
 }
 
 template <typename T>
-__global__ void __launch_bounds__(VT) norm2_kernel(const T *x, long long n, double *scal, double *partial,
-                                                   int part_stride, unsigned *counter) {
+__global__ void __launch_bounds__(VT) norm2_kernel(const T *__restrict__ x, long long n, double *scal,
+                                                   double *partial, int part_stride, unsigned *counter) {
     __shared__ double red[VT / 32 + 1];
     __shared__ bool last;
     const int node = blockIdx.y;
-    const long long base = (long long)node * n;
+    x += (long long)node * n;
     double dot = 0.0;
+    vec_loop(n,
+        [&](long long i) {
+            const Q4<T> xv = ld4(x + i);
 #pragma unroll
-    for (int e = 0; e < VE; e++) {
-        const long long i = (long long)blockIdx.x * VT * VE + e * VT + threadIdx.x;
-        if (i < n) {
-            const double v = (double)x[base + i];
-            dot += v * v;
-        }
-    }
+            for (int u = 0; u < 4; u++) dot += (double)xv.v[u] * (double)xv.v[u];
+        },
+        [&](long long i) { dot += (double)x[i] * (double)x[i]; });
     const double bs = block_sum<VT>(dot, red);
     double *part = partial + (long long)node * part_stride;
     if (threadIdx.x == 0) part[blockIdx.x] = bs;
