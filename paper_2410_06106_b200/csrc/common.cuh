@@ -75,22 +75,25 @@ __device__ __forceinline__ double block_sum(double v, double *sh /* >= NT/32 + 1
     return sh[NT / 32];
 }
 
-// "Last block finalises": every block of a group writes its partial, then the last
-// block to arrive sums all partials in index order (deterministic) and resets the
-// counter.  Returns true in every thread of the last block.
+// "Last block finalises": every block of a group has thread 0 write its partial, then
+// the last block to arrive sums all partials in index order (deterministic) and resets
+// the counter.  Only thread 0 fences (release before the arrival count, acquire after
+// it); readers of the partials use __ldcg.  Returns true in every thread of the last block.
 __device__ __forceinline__ bool last_block_of_group(unsigned *counter, unsigned nblocks,
                                                     bool *sh_flag) {
-    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned prev = atomicAdd(counter, 1u);
-        *sh_flag = (prev == nblocks - 1);
-        if (*sh_flag) *counter = 0u;
+        __threadfence();
+        const unsigned prev = atomicAdd(counter, 1u);
+        const bool last = (prev == nblocks - 1);
+        if (last) {
+            *counter = 0u;
+            __threadfence();
+        }
+        *sh_flag = last;
     }
     __syncthreads();
-    bool last = *sh_flag;
-    if (last) __threadfence();
-    return last;
+    return *sh_flag;
 }
 
 // floor for 0 <= x < 2^22 without a conversion instruction: the round-down add

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(DT) dct_minmax(const float *const *vin, long l
     if (last_block_of_group(counter + b, gridDim.x, &last)) {
         if (threadIdx.x == 0) {
             float a = INFINITY, c = -INFINITY;
-            for (unsigned k = 0; k < gridDim.x; k++) { a = fminf(a, part[2 * k]); c = fmaxf(c, part[2 * k + 1]); }
+            for (unsigned k = 0; k < gridDim.x; k++) { a = fminf(a, __ldcg(part + 2 * k)); c = fmaxf(c, __ldcg(part + 2 * k + 1)); }
             mm_work[2 * b] = a;
             mm_work[2 * b + 1] = c;
             float *hdr = reinterpret_cast<float *>(pay[b]);

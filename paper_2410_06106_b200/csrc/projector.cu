@@ -14,7 +14,7 @@ static_assert(FP_PITCH_Y % 4 == 0, "row pitch must keep 16-byte alignment");
 constexpr int BP_TS = 64;       // backprojector pixel tile side
 constexpr int BP_THREADS = 256;
 constexpr int BP_WB = 96;       // staged bins per angle: >= 63(|cos|+|sin|) + 4
-constexpr int BP_MAXA = 64;     // angles per staged batch
+constexpr int BP_MAXA = 32;     // angles per staged batch
 
 template <typename T>
 __device__ __forceinline__ T floor_split(T x, int &i);
@@ -221,6 +221,364 @@ __global__ void __launch_bounds__(FP_THREADS) fp_tile_kernel(const FpArgs<T> a) 
     }
 }
 
+// ------------------------------------------------------------------ forward: fp32 tile pass
+// The fp32 production kernel.  Shared memory holds, for every cross index i of every
+// tile line, the pair (e_i, d_i) with d_i = x_{i+1} - x_i and e_i = x_i - (i - ORG) d_i,
+// so a bilinear sample at cross coordinate kf' = kf - ORG is  e_i + kf' d_i  with
+// i = floor(kf):  x_i + (kf - i)(x_{i+1} - x_i).  Per sample: FFMA (position), FADD.RM
+// (floor into the mantissa of 2^23 + ORG + kf'), LEA, LDS.64, FFMA + FADD (sample and
+// accumulate) -- six instructions.  ORG = the middle of the padded row keeps |i - ORG|
+// <= 104, so e_i loses no more than the plain lerp does.
+// Rays of consecutive angles are packed into full 32-lane items.
+constexpr int FP2_PITCH = FP_TW + 2 * FP_HALO_A;  // 208 pairs per line
+constexpr int FP2_ORG = FP2_PITCH / 2;            // 104
+constexpr float FP2_MAGIC = 8388608.0f + (float)FP2_ORG;
+
+__device__ __forceinline__ float2 lds64(uint32_t addr) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
+
+template <int O>
+__global__ void __launch_bounds__(FP_THREADS, 4) fp_tile_f32(const FpArgs<float> a) {
+    constexpr int H = FP_HALO_A;
+    extern __shared__ __align__(16) unsigned char fp_smem[];
+    float2 *pt = reinterpret_cast<float2 *>(fp_smem);  // [FP_TH][FP2_PITCH] (e, d)
+    __shared__ double s_kap[FP_MAXA], s_at[FP_MAXA];
+    __shared__ float s_B[FP_MAXA];
+    __shared__ int s_row[FP_MAXA], s_jlo[FP_MAXA], s_pre[FP_MAXA + 1];
+
+    const int node = blockIdx.y;
+    const int grp = 2 * node + O;
+    const int a_begin = a.oofs[grp], a_end = a.oofs[grp + 1];
+    if (a_begin == a_end) return;  // uniform over the block
+    const int N = a.N;
+    const int tile_id = blockIdx.x;
+    const int ntiles = a.nt_line * a.nt_cross;
+    const int lt = tile_id / a.nt_cross, ct = tile_id % a.nt_cross;
+    const int L0 = lt * FP_TH, X0 = ct * FP_TW;
+    const float *img = a.img + (long long)node * a.n;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // ---- stage the (e, d) pairs; x = 0 outside the image and outside [H, H + TW)
+    for (int i = threadIdx.x; i < FP_TH * (FP2_PITCH - FP_TW - 1); i += FP_THREADS) {
+        const int l = i / (FP2_PITCH - FP_TW - 1), k = i % (FP2_PITCH - FP_TW - 1);
+        pt[l * FP2_PITCH + (k < H - 1 ? k : k + FP_TW + 1)] = make_float2(0.f, 0.f);
+    }
+    auto pair = [](float x, float xn, int i) {
+        const float d = xn - x;
+        return make_float2(fmaf(-(float)(i - FP2_ORG), d, x), d);
+    };
+    if ((N & 3) != 0) {  // odd N (stateless calls only): scalar loads
+        for (int i = threadIdx.x; i < FP_TH * (FP_TW + 1); i += FP_THREADS) {
+            const int l = i / (FP_TW + 1), k = i % (FP_TW + 1) - 1;  // k = -1 .. TW-1
+            auto at = [&](int kk) -> float {
+                if (kk < 0 || kk >= FP_TW) return 0.f;
+                const int r = O == 0 ? L0 + l : X0 + kk, c = O == 0 ? X0 + kk : L0 + l;
+                return (r < N && c < N) ? img[(long long)r * N + c] : 0.f;
+            };
+            pt[l * FP2_PITCH + H + k] = pair(at(k), at(k + 1), H + k);
+        }
+    } else if (O == 0) {  // a warp stages one row segment of 128: float4 per lane, neighbour by shuffle
+        for (int l = warp; l < FP_TH; l += FP_THREADS / 32) {
+            const int r = L0 + l, c = X0 + 4 * lane;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (r < N && c < N) v = __ldg(reinterpret_cast<const float4 *>(img + (long long)r * N + c));
+            float nx = __shfl_down_sync(0xffffffffu, v.x, 1);
+            if (lane == 31) nx = 0.f;
+            const int i0 = H + 4 * lane;
+            float4 *dst = reinterpret_cast<float4 *>(pt + l * FP2_PITCH + i0);
+            const float2 p0 = pair(v.x, v.y, i0), p1 = pair(v.y, v.z, i0 + 1), p2 = pair(v.z, v.w, i0 + 2),
+                         p3 = pair(v.w, nx, i0 + 3);
+            dst[0] = make_float4(p0.x, p0.y, p1.x, p1.y);
+            dst[1] = make_float4(p2.x, p2.y, p3.x, p3.y);
+            if (lane == 0) pt[l * FP2_PITCH + H - 1] = pair(0.f, v.x, H - 1);
+        }
+    } else {  // lines are image columns: lanes along rows (cross), float4 = 4 lines, neighbour by shuffle
+        for (int job = warp; job < (FP_TW / 32) * (FP_TH / 4); job += FP_THREADS / 32) {
+            const int yg = job % (FP_TW / 32), q = job / (FP_TW / 32);
+            const int y = 32 * yg + lane, r = X0 + y, c = L0 + 4 * q;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (r < N && c < N) v = __ldg(reinterpret_cast<const float4 *>(img + (long long)r * N + c));
+            float4 nv;
+            nv.x = __shfl_down_sync(0xffffffffu, v.x, 1);
+            nv.y = __shfl_down_sync(0xffffffffu, v.y, 1);
+            nv.z = __shfl_down_sync(0xffffffffu, v.z, 1);
+            nv.w = __shfl_down_sync(0xffffffffu, v.w, 1);
+            if (lane == 31) {
+                nv = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (y + 1 < FP_TW && r + 1 < N && c < N)
+                    nv = __ldg(reinterpret_cast<const float4 *>(img + (long long)(r + 1) * N + c));
+            }
+            const int i = H + y;
+            pt[(4 * q + 0) * FP2_PITCH + i] = pair(v.x, nv.x, i);
+            pt[(4 * q + 1) * FP2_PITCH + i] = pair(v.y, nv.y, i);
+            pt[(4 * q + 2) * FP2_PITCH + i] = pair(v.z, nv.z, i);
+            pt[(4 * q + 3) * FP2_PITCH + i] = pair(v.w, nv.w, i);
+            if (yg == 0 && lane == 0) {
+                pt[(4 * q + 0) * FP2_PITCH + H - 1] = pair(0.f, v.x, H - 1);
+                pt[(4 * q + 1) * FP2_PITCH + H - 1] = pair(0.f, v.y, H - 1);
+                pt[(4 * q + 2) * FP2_PITCH + H - 1] = pair(0.f, v.z, H - 1);
+                pt[(4 * q + 3) * FP2_PITCH + H - 1] = pair(0.f, v.w, H - 1);
+            }
+        }
+    }
+
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(pt) - a.magic;  // a.magic = 0x4B000000 << 3
+    for (int b0 = a_begin; b0 < a_end; b0 += FP_MAXA) {
+        const int nb = min(FP_MAXA, a_end - b0);
+        __syncthreads();  // tile staged / previous batch consumed
+        if (threadIdx.x < FP_MAXA) {
+            const int k = threadIdx.x;
+            int W = 0;
+            if (k < nb) {
+                const int row = a.olist[b0 + k];
+                const FpWin wv = a.wins[(long long)row * ntiles + tile_id];
+                const FpRowGeo rg = a.rgeo[row];
+                s_row[k] = row;
+                s_jlo[k] = wv.jlo;
+                s_kap[k] = wv.kap - (double)FP2_ORG;
+                s_at[k] = rg.at;
+                s_B[k] = (float)rg.B;
+                W = wv.W;
+            }
+            int inc = W;  // exclusive prefix of the window sizes over the (<= 64) angles
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            s_pre[k + 1] = inc;  // provisional (warp 1 adds warp 0's total below)
+            if (k == 0) s_pre[0] = 0;
+        }
+        __syncthreads();
+        if (threadIdx.x >= 32 && threadIdx.x < FP_MAXA) s_pre[threadIdx.x + 1] += s_pre[32];
+        __syncthreads();
+        const int R = s_pre[nb];
+        // ---- one warp item = 32 consecutive rays of the batch (angles packed back to back)
+        for (int g0 = warp * 32; g0 < R; g0 += FP_THREADS) {
+            const int g = min(g0 + lane, R - 1);
+            int lo = 0, hi = nb - 1;  // angle of the first lane, then step forward per lane
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_pre[mid] <= g0) lo = mid; else hi = mid - 1;
+            }
+            int k = lo;
+            while (s_pre[k + 1] <= g) k++;
+            const int w = g - s_pre[k];
+            const float kap = (float)(s_kap[k] + (double)w * s_at[k]);
+            const float B = s_B[k];
+            float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+            for (int l = 0; l < FP_TH; l += 2) {
+                const float kf0 = fmaf((float)l, B, kap), kf1 = fmaf((float)(l + 1), B, kap);
+                const float m0 = __fadd_rd(kf0, FP2_MAGIC), m1 = __fadd_rd(kf1, FP2_MAGIC);
+                const float2 q0 = lds64((__float_as_uint(m0) << 3) + sb + l * FP2_PITCH * 8);
+                const float2 q1 = lds64((__float_as_uint(m1) << 3) + sb + (l + 1) * FP2_PITCH * 8);
+                acc0 += fmaf(kf0, q0.y, q0.x);
+                acc1 += fmaf(kf1, q1.y, q1.x);
+            }
+            if (g0 + lane < R)
+                a.partial[((long long)s_row[k] * a.nt_line + lt) * 2 * a.n_det + (ct & 1) * a.n_det + s_jlo[k] + w] =
+                    acc0 + acc1;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ forward: persistent fp32
+// Persistent, software-pipelined version of fp_tile_f32: each CTA walks the work units
+// u = (orientation, node, tile) round-robin; while it computes unit u from the pair
+// tile P, cp.async (LDGSTS) brings the raw pixels of its next unit into R and that
+// unit's window records into a second table buffer, so the global-memory latency of
+// staging is hidden behind the previous unit's ray walks.
+constexpr int FPP_RAW = FP_TH * FP_TW;  // raw floats per unit (both orientations)
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+struct FpUnit {
+    int O, node, tile, a_begin, a_end;
+};
+__device__ __forceinline__ FpUnit fp_unit(const FpArgs<float> &a, int u, int ntiles) {
+    FpUnit U;
+    const int per = a.L * ntiles;
+    U.O = u / per;
+    const int rem = u - U.O * per;
+    U.node = rem / ntiles;
+    U.tile = rem - U.node * ntiles;
+    const int grp = 2 * U.node + U.O;
+    U.a_begin = a.oofs[grp];
+    U.a_end = a.oofs[grp + 1];
+    return U;
+}
+
+__global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<float> a, int nunits) {
+    constexpr int H = FP_HALO_A;
+    extern __shared__ __align__(16) unsigned char fp_smem[];
+    float2 *pt = reinterpret_cast<float2 *>(fp_smem);                       // [TH][PITCH] (e, d)
+    float *raw = reinterpret_cast<float *>(pt + FP_TH * FP2_PITCH);           // [FPP_RAW]
+    FpRec *rec = reinterpret_cast<FpRec *>(raw + FPP_RAW);                    // [2][FP_MAXA]
+    __shared__ int s_pre[FP_MAXA + 1];
+    const int N = a.N;
+    const int ntiles = a.nt_line * a.nt_cross;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t raw_s = (uint32_t)__cvta_generic_to_shared(raw);
+    const uint32_t rec_s = (uint32_t)__cvta_generic_to_shared(rec);
+
+    // halo pairs are (0, 0) for every unit
+    for (int i = threadIdx.x; i < FP_TH * (FP2_PITCH - FP_TW - 1); i += FP_THREADS) {
+        const int l = i / (FP2_PITCH - FP_TW - 1), k = i % (FP2_PITCH - FP_TW - 1);
+        pt[l * FP2_PITCH + (k < H - 1 ? k : k + FP_TW + 1)] = make_float2(0.f, 0.f);
+    }
+    // prefetch of unit u into raw (+ its first window records into rec buffer rb)
+    auto issue = [&](int u, int rb) {
+        if (u >= nunits) return;
+        const FpUnit U = fp_unit(a, u, ntiles);
+        if (U.a_begin == U.a_end) return;
+        const int lt = U.tile / a.nt_cross, ct = U.tile % a.nt_cross;
+        const int L0 = lt * FP_TH, X0 = ct * FP_TW;
+        const float *img = a.img + (long long)U.node * a.n;
+        for (int c = threadIdx.x; c < FPP_RAW / 4; c += FP_THREADS) {
+            int r, col;
+            uint32_t dst;
+            if (U.O == 0) {  // raw[l][x]
+                const int l = c >> 5, q = c & 31;
+                r = L0 + l; col = X0 + 4 * q;
+                dst = raw_s + 16u * c;
+            } else {  // raw[y][line], 16-byte chunks XOR-swizzled by (y & 7): conflict-free column reads
+                const int y = c >> 3, q = c & 7;
+                r = X0 + y; col = L0 + 4 * q;
+                dst = raw_s + 16u * (8 * y + (q ^ (y & 7)));
+            }
+            const bool ok = r < N && col < N;
+            cp_async16(dst, ok ? (const void *)(img + (long long)r * N + col) : (const void *)img, ok);
+        }
+        const int nb = min(FP_MAXA, U.a_end - U.a_begin);
+        const FpRec *src = a.recs + (long long)U.tile * a.n_olist + U.a_begin;
+        for (int c = threadIdx.x; c < nb * 2; c += FP_THREADS)
+            cp_async16(rec_s + (uint32_t)(rb * FP_MAXA * 32 + 16 * c), reinterpret_cast<const char *>(src) + 16 * c, true);
+    };
+    auto pair = [](float x, float xn, int i) {
+        const float d = xn - x;
+        return make_float2(fmaf(-(float)(i - FP2_ORG), d, x), d);
+    };
+
+    int rb = 0;
+    issue(blockIdx.x, rb);
+    cp_async_commit();
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x, rb ^= 1) {
+        const FpUnit U = fp_unit(a, u, ntiles);
+        cp_async_wait_all();
+        __syncthreads();  // raw + rec[rb] of unit u landed; previous unit's P reads done
+        const bool active = U.a_begin != U.a_end;
+        const int lt = U.tile / a.nt_cross, ct = U.tile % a.nt_cross;
+        if (active) {  // ---- raw -> (e, d) pairs
+            if (U.O == 0) {
+                for (int l = warp; l < FP_TH; l += FP_THREADS / 32) {
+                    const float4 v = *reinterpret_cast<const float4 *>(raw + l * FP_TW + 4 * lane);
+                    float nx = __shfl_down_sync(0xffffffffu, v.x, 1);
+                    if (lane == 31) nx = 0.f;
+                    const int i0 = H + 4 * lane;
+                    float4 *dst = reinterpret_cast<float4 *>(pt + l * FP2_PITCH + i0);
+                    const float2 p0 = pair(v.x, v.y, i0), p1 = pair(v.y, v.z, i0 + 1),
+                                 p2 = pair(v.z, v.w, i0 + 2), p3 = pair(v.w, nx, i0 + 3);
+                    dst[0] = make_float4(p0.x, p0.y, p1.x, p1.y);
+                    dst[1] = make_float4(p2.x, p2.y, p3.x, p3.y);
+                    if (lane == 0) pt[l * FP2_PITCH + H - 1] = pair(0.f, v.x, H - 1);
+                }
+            } else {
+                for (int job = warp; job < (FP_TW / 32) * (FP_TH / 4); job += FP_THREADS / 32) {
+                    const int yg = job % (FP_TW / 32), q = job / (FP_TW / 32);
+                    const int y = 32 * yg + lane;
+                    const float4 v = *reinterpret_cast<const float4 *>(raw + 4 * (8 * y + (q ^ (y & 7))));
+                    float4 nv;
+                    nv.x = __shfl_down_sync(0xffffffffu, v.x, 1);
+                    nv.y = __shfl_down_sync(0xffffffffu, v.y, 1);
+                    nv.z = __shfl_down_sync(0xffffffffu, v.z, 1);
+                    nv.w = __shfl_down_sync(0xffffffffu, v.w, 1);
+                    if (lane == 31) {
+                        const int y1 = y + 1;
+                        nv = y1 < FP_TW ? *reinterpret_cast<const float4 *>(raw + 4 * (8 * y1 + (q ^ (y1 & 7))))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                    const int i = H + y;
+                    pt[(4 * q + 0) * FP2_PITCH + i] = pair(v.x, nv.x, i);
+                    pt[(4 * q + 1) * FP2_PITCH + i] = pair(v.y, nv.y, i);
+                    pt[(4 * q + 2) * FP2_PITCH + i] = pair(v.z, nv.z, i);
+                    pt[(4 * q + 3) * FP2_PITCH + i] = pair(v.w, nv.w, i);
+                    if (yg == 0 && lane == 0) {
+                        pt[(4 * q + 0) * FP2_PITCH + H - 1] = pair(0.f, v.x, H - 1);
+                        pt[(4 * q + 1) * FP2_PITCH + H - 1] = pair(0.f, v.y, H - 1);
+                        pt[(4 * q + 2) * FP2_PITCH + H - 1] = pair(0.f, v.z, H - 1);
+                        pt[(4 * q + 3) * FP2_PITCH + H - 1] = pair(0.f, v.w, H - 1);
+                    }
+                }
+            }
+        }
+        __syncthreads();  // P ready; raw free
+        issue(u + gridDim.x, rb ^ 1);
+        cp_async_commit();
+        if (!active) continue;
+        const uint32_t sb = (uint32_t)__cvta_generic_to_shared(pt) - a.magic;
+        for (int b0 = U.a_begin; b0 < U.a_end; b0 += FP_MAXA) {
+            const int nb = min(FP_MAXA, U.a_end - b0);
+            FpRec *R = rec + rb * FP_MAXA;
+            if (b0 != U.a_begin) {  // later batches (> 64 angles per orientation): plain loads
+                __syncthreads();
+                for (int k = threadIdx.x; k < nb; k += FP_THREADS) R[k] = a.recs[(long long)U.tile * a.n_olist + b0 + k];
+                __syncthreads();
+            }
+            if (threadIdx.x < FP_MAXA) {
+                const int k = threadIdx.x;
+                int inc = k < nb ? R[k].W : 0;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += y;
+                }
+                s_pre[k + 1] = inc;
+                if (k == 0) s_pre[0] = 0;
+            }
+            __syncthreads();
+            if (threadIdx.x >= 32 && threadIdx.x < FP_MAXA) s_pre[threadIdx.x + 1] += s_pre[32];
+            __syncthreads();
+            const int Rn = s_pre[nb];
+            for (int g0 = warp * 32; g0 < Rn; g0 += FP_THREADS) {
+                const int g = min(g0 + lane, Rn - 1);
+                int lo = 0, hi = nb - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s_pre[mid] <= g0) lo = mid; else hi = mid - 1;
+                }
+                int k = lo;
+                while (s_pre[k + 1] <= g) k++;
+                const int w = g - s_pre[k];
+                const float kap = (float)(R[k].kap + (double)w * R[k].at);
+                const float B = R[k].B;
+                float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+                for (int l = 0; l < FP_TH; l += 2) {
+                    const float kf0 = fmaf((float)l, B, kap), kf1 = fmaf((float)(l + 1), B, kap);
+                    const float m0 = __fadd_rd(kf0, FP2_MAGIC), m1 = __fadd_rd(kf1, FP2_MAGIC);
+                    const float2 q0 = lds64((__float_as_uint(m0) << 3) + sb + l * FP2_PITCH * 8);
+                    const float2 q1 = lds64((__float_as_uint(m1) << 3) + sb + (l + 1) * FP2_PITCH * 8);
+                    acc0 += fmaf(kf0, q0.y, q0.x);
+                    acc1 += fmaf(kf1, q1.y, q1.x);
+                }
+                if (g0 + lane < Rn)
+                    a.partial[((long long)R[k].row * a.nt_line + lt) * 2 * a.n_det + (ct & 1) * a.n_det + R[k].jlo + w] =
+                        acc0 + acc1;
+            }
+            __syncthreads();  // s_pre / R reuse
+        }
+    }
+    cp_async_wait_all();
+}
+
 // ------------------------------------------------------------------ forward: static windows
 // For every (ray row, tile): the rays whose cross coordinate over the tile's real lines
 // meets (X0 - 1, X0 + TW), padded by one ray below and two above, and the shared-memory
@@ -255,6 +613,23 @@ __global__ void fp_setup_kernel(const RayRow *rows, const int *xmaj, const doubl
     }
 }
 
+__global__ void fp_rec_kernel(const int *olist, int n_olist, int ntiles, const FpWin *wins,
+                              const FpRowGeo *rgeo, FpRec *recs) {
+    const int pos = blockIdx.y;
+    const int row = olist[pos];
+    for (int tile = blockIdx.x * blockDim.x + threadIdx.x; tile < ntiles; tile += gridDim.x * blockDim.x) {
+        const FpWin w = wins[(long long)row * ntiles + tile];
+        FpRec r;
+        r.kap = w.kap - (double)FP2_ORG;
+        r.at = rgeo[row].at;
+        r.B = (float)rgeo[row].B;
+        r.jlo = w.jlo;
+        r.W = w.W;
+        r.row = row;
+        recs[(long long)tile * n_olist + pos] = r;
+    }
+}
+
 // ------------------------------------------------------------------ forward: reduction
 // s[row][j] = (1/m) * sum over line bands (in order) of the two parity slots; RESID: d - A x.
 template <typename T, bool RESID>
@@ -285,6 +660,9 @@ template <typename T, int EPI>
 __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) {
     extern __shared__ __align__(16) unsigned char bp_smem[];
     T *win = reinterpret_cast<T *>(bp_smem);  // [BP_MAXA][BP_WB], bins pre-scaled by 1/m
+    // fp32: the epilogue operands of the tile, prefetched with cp.async at entry so their
+    // latency overlaps the angle loop: ep[0] = vin (p or x), ep[1] = b' (RESID, GD)
+    float *ep = reinterpret_cast<float *>(win + BP_MAXA * BP_WB);  // [2][BP_TS * BP_TS]
     __shared__ double s_tau[BP_MAXA], s_csd[BP_MAXA], s_snd[BP_MAXA];
     __shared__ T s_cs[BP_MAXA], s_sn[BP_MAXA], s_im[BP_MAXA];
     __shared__ int s_jlo[BP_MAXA];
@@ -298,6 +676,21 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
     const int lx = lane & 7, prow = 8 * warp + (lane >> 3);  // pixel (prow + 4 ky, 8 kx + lx)
     const double h = 0.5 * (double)(N - 1), t0 = -0.5 * (double)(a.n_det - 1);
     const int nang = a.node_nang[node], row0 = a.node_row0[node];
+    constexpr int NEP = (EPI == EPI_CGQ) ? 1 : ((EPI == EPI_RESID || EPI == EPI_GD) ? 2 : 0);
+    const bool pre = sizeof(T) == 4 && NEP > 0 && (N & 3) == 0;
+    if (pre) {
+        const long long nb0 = (long long)node * a.n;
+        const uint32_t eps = (uint32_t)__cvta_generic_to_shared(ep);
+        for (int c = threadIdx.x; c < NEP * BP_TS * BP_TS / 4; c += BP_THREADS) {
+            const int o = c / (BP_TS * BP_TS / 4), cc = c % (BP_TS * BP_TS / 4);
+            const int r = r0 + cc / (BP_TS / 4), col = c0 + 4 * (cc % (BP_TS / 4));
+            const float *src = reinterpret_cast<const float *>(o == 0 ? (const void *)a.vin : (const void *)a.bprime) + nb0;
+            const bool ok = r < N && col < N;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(eps + 16u * c),
+                         "l"(ok ? src + (long long)r * N + col : src), "r"(ok ? 16 : 0));
+        }
+        asm volatile("cp.async.commit_group;");
+    }
     T acc[2][8];
 #pragma unroll
     for (int ky = 0; ky < 2; ky++)
@@ -374,6 +767,10 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
         }
     }
     // ---------------- epilogue (fp64 in registers)
+    if (pre) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+    }
     const double c = (EPI == EPI_CGQ || EPI == EPI_RESID || EPI == EPI_GD) ? a.cnode[node] : 0.0;
     double dot = 0.0;
     const long long nb = (long long)node * a.n;
@@ -384,22 +781,26 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
             const int r = r0 + prow + 4 * ky, col = c0 + 8 * kx + lx;
             if (r >= N || col >= N) continue;
             const long long p = nb + (long long)r * N + col;
+            const int sp = (prow + 4 * ky) * BP_TS + 8 * kx + lx;
             const double g = (double)acc[ky][kx];
             if (EPI == EPI_PLAIN) {
                 a.out[p] = acc[ky][kx];
             } else if (EPI == EPI_CGQ) {
-                const double pv = (double)a.vin[p];
+                const double pv = pre ? (double)ep[sp] : (double)a.vin[p];
                 const T q = (T)(g + c * pv);
                 a.out[p] = q;
                 dot += pv * (double)q;
             } else if (EPI == EPI_RESID) {
-                const T rv = (T)(g + (double)a.bprime[p] - c * (double)a.vin[p]);
+                const double xv = pre ? (double)ep[sp] : (double)a.vin[p];
+                const double bv = pre ? (double)ep[BP_TS * BP_TS + sp] : (double)a.bprime[p];
+                const T rv = (T)(g + bv - c * xv);
                 a.out[p] = rv;
                 a.out2[p] = rv;
                 dot += (double)rv * (double)rv;
             } else {  // EPI_GD: x <- x - eta (c x - b' - A^T(d - A x))
-                const double xv = (double)a.vin[p];
-                a.out[p] = (T)(xv - a.eta[node] * (c * xv - (double)a.bprime[p] - g));
+                const double xv = pre ? (double)ep[sp] : (double)a.vin[p];
+                const double bv = pre ? (double)ep[BP_TS * BP_TS + sp] : (double)a.bprime[p];
+                a.out[p] = (T)(xv - a.eta[node] * (c * xv - bv - g));
             }
         }
     if (EPI == EPI_CGQ || EPI == EPI_RESID) {
@@ -408,7 +809,7 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
         if (threadIdx.x == 0) part[blockIdx.x] = bs;
         if (last_block_of_group(a.counter + node, gridDim.x, &last_flag)) {
             double s = 0.0;
-            for (int b = threadIdx.x; b < (int)gridDim.x; b += BP_THREADS) s += part[b];
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += BP_THREADS) s += __ldcg(part + b);
             s = block_sum<BP_THREADS>(s, red);
             if (threadIdx.x == 0) {
                 double *sc = a.scal + (long long)node * S_NSLOT;
@@ -430,13 +831,26 @@ void set_smem(K kernel, size_t dyn) {
 
 template <typename T>
 size_t fp_smem(int o) { return sizeof(T) * FP_TH * (o == 0 ? FP_PITCH_Y : FP_PITCH_X); }
+size_t fp2_smem() { return sizeof(float2) * FP_TH * FP2_PITCH; }
+size_t fpp_smem() { return sizeof(float2) * FP_TH * FP2_PITCH + sizeof(float) * FPP_RAW + sizeof(FpRec) * 2 * FP_MAXA; }
+int g_fpp_grid = 0;  // persistent grid: SMs x resident CTAs (projector_setup)
 template <typename T>
-size_t bp_smem() { return sizeof(T) * BP_MAXA * BP_WB; }
+size_t bp_smem() { return sizeof(T) * BP_MAXA * BP_WB + (sizeof(T) == 4 ? 2 * sizeof(float) * BP_TS * BP_TS : 0); }
 
 template <typename T>
 void set_all_smem() {
     set_smem(fp_tile_kernel<T, 0>, fp_smem<T>(0));
     set_smem(fp_tile_kernel<T, 1>, fp_smem<T>(1));
+    if (sizeof(T) == 4) {
+        set_smem(fp_tile_f32<0>, fp2_smem());
+        set_smem(fp_tile_f32<1>, fp2_smem());
+        set_smem(fp_persist_f32, fpp_smem());
+        int dev = 0, sms = 0, per = 0;
+        TQ_CHECK_CUDA(cudaGetDevice(&dev));
+        TQ_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        TQ_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fp_persist_f32, FP_THREADS, fpp_smem()));
+        g_fpp_grid = sms * std::max(1, per);
+    }
     set_smem(bp_tile_kernel<T, EPI_PLAIN>, bp_smem<T>());
     set_smem(bp_tile_kernel<T, EPI_CGQ>, bp_smem<T>());
     set_smem(bp_tile_kernel<T, EPI_RESID>, bp_smem<T>());
@@ -446,8 +860,20 @@ void set_all_smem() {
 template <typename T>
 void fp_dispatch(const FpArgs<T> &A, int L, cudaStream_t st) {
     const dim3 grid(A.nt_line * A.nt_cross, L);
-    fp_tile_kernel<T, 0><<<grid, FP_THREADS, fp_smem<T>(0), st>>>(A);
-    fp_tile_kernel<T, 1><<<grid, FP_THREADS, fp_smem<T>(1), st>>>(A);
+    if constexpr (sizeof(T) == 4) {
+        FpArgs<float> B = A;
+        B.magic = 0x4B000000u << 3;  // 8-byte pairs (wraps mod 2^32)
+        if (A.N % 4 == 0 && A.recs) {
+            const int nunits = 2 * L * A.nt_line * A.nt_cross;
+            fp_persist_f32<<<std::min(nunits, g_fpp_grid), FP_THREADS, fpp_smem(), st>>>(B, nunits);
+        } else {
+            fp_tile_f32<0><<<grid, FP_THREADS, fp2_smem(), st>>>(B);
+            fp_tile_f32<1><<<grid, FP_THREADS, fp2_smem(), st>>>(B);
+        }
+    } else {
+        fp_tile_kernel<T, 0><<<grid, FP_THREADS, fp_smem<T>(0), st>>>(A);
+        fp_tile_kernel<T, 1><<<grid, FP_THREADS, fp_smem<T>(1), st>>>(A);
+    }
 }
 
 template <typename T>
@@ -485,11 +911,15 @@ void launch_fp(int prec, const void *args, int L, cudaStream_t st) {
 }
 
 void launch_fp_setup(const RayRow *rows, const int *xmaj, const double2 *trig, int n_rows, int N, int n_det,
-                     FpWin *wins, FpRowGeo *rgeo, cudaStream_t st) {
+                     FpWin *wins, FpRowGeo *rgeo, const int *olist, int n_olist, FpRec *recs, cudaStream_t st) {
     if (n_rows == 0) return;
     const int ntiles = fp_ntiles(N);
     fp_setup_kernel<<<dim3(ceil_div(ntiles, 128), n_rows), 128, 0, st>>>(rows, xmaj, trig, n_rows, N, n_det, wins, rgeo);
     TQ_CHECK_CUDA(cudaGetLastError());
+    if (n_olist) {
+        fp_rec_kernel<<<dim3(ceil_div(ntiles, 128), n_olist), 128, 0, st>>>(olist, n_olist, ntiles, wins, rgeo, recs);
+        TQ_CHECK_CUDA(cudaGetLastError());
+    }
 }
 
 void launch_fp_reduce(int prec, bool resid, const void *args, int n_rows, int n_det, cudaStream_t st) {

@@ -47,6 +47,16 @@ struct FpRowGeo {   // per ray row: cross step per bin and per line
     double at, B;
 };
 
+// The same, per (tile, position in the orientation-grouped row list `olist`), laid out
+// so that one forward work unit (node, orientation, tile) reads its records as one
+// contiguous run (prefetched with cp.async by the persistent fp32 kernel).
+struct FpRec {
+    double kap;  // shared-memory cross coordinate of ray jlo on the tile's first line, minus FP2 origin
+    double at;   // cross step per bin
+    float B;     // cross step per line
+    int jlo, W, row;
+};
+
 template <typename T>
 struct FpArgs {
     const T *img;          // [L][n] node-major images
@@ -59,6 +69,8 @@ struct FpArgs {
     T *partial;            // [n_rows][nt_line][2][n_det]: band lt, cross-tile parity ct & 1
     int nt_line, nt_cross; // tiles along the major / cross axis (same for both orientations)
     uint32_t magic;        // = 0x4B000000 << 2 (mod 2^32), see projector.cu magic_base
+    const FpRec *recs;     // [ntiles][n_olist] (fp32 persistent kernel)
+    int n_olist, L;
 };
 
 template <typename T>
@@ -106,7 +118,7 @@ int bp_tiles(int N);
 void launch_fp(int prec, const void *args, int L, cudaStream_t st);
 // static forward geometry of n_rows rows (once per context)
 void launch_fp_setup(const RayRow *rows, const int *xmaj, const double2 *trig, int n_rows, int N, int n_det,
-                     FpWin *wins, FpRowGeo *rgeo, cudaStream_t st);
+                     FpWin *wins, FpRowGeo *rgeo, const int *olist, int n_olist, FpRec *recs, cudaStream_t st);
 void launch_fp_reduce(int prec, bool resid, const void *args, int n_rows, int n_det, cudaStream_t st);
 void launch_bp(int prec, int epi, const void *args, int L, int N, cudaStream_t st);
 

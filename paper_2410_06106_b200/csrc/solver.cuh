@@ -31,6 +31,8 @@ struct Inner {
     void *fpart = nullptr;     // forward partial sums [n_rows][nt_line][2][n_det] (zeroed once)
     FpWin *fwin = nullptr;     // [n_rows][fp_ntiles] static ray windows of the forward tiles
     FpRowGeo *frg = nullptr;   // [n_rows]
+    FpRec *frec = nullptr;     // [fp_ntiles][n_olist] (persistent fp32 forward kernel)
+    int n_olist = 0;
     int nt_line = 0, nt_cross = 0;
     void *X = nullptr, *R = nullptr, *P = nullptr, *Q = nullptr, *BP = nullptr;  // [L][n]
     void *D = nullptr;         // [n_rows][n_det]

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(VT) cg_update_xr(T *__restrict__ x, T *__restr
     if (threadIdx.x == 0) part[blockIdx.x] = bs;
     if (last_block_of_group(counter + node, gridDim.x, &last)) {
         double s = 0.0;
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += VT) s += part[b];
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += VT) s += __ldcg(part + b);
         s = block_sum<VT>(s, red);
         if (threadIdx.x == 0) {
             const double rr = sc[S_RR];
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(VT) norm2_kernel(const T *__restrict__ x, long
     if (threadIdx.x == 0) part[blockIdx.x] = bs;
     if (last_block_of_group(counter + node, gridDim.x, &last)) {
         double s = 0.0;
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += VT) s += part[b];
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += VT) s += __ldcg(part + b);
         s = block_sum<VT>(s, red);
         if (threadIdx.x == 0) scal[(long long)node * S_NSLOT + S_NORM] = s;
     }
