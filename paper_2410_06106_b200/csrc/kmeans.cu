@@ -18,7 +18,6 @@
 // cluster sums are exact integers, hence independent of summation order.
 // All Lloyd iterations of a payload run in one CTA; the cost of an iteration no
 // longer depends on n.  The final assignment packs labels into bit-planes.
-#include <cub/block/block_radix_rank.cuh>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
@@ -76,15 +75,46 @@ __device__ __forceinline__ void load_tile(const uint32_t *keys, long long off, u
     k[4] = b.x; k[5] = b.y; k[6] = b.z; k[7] = b.w;
 }
 
-// warp-aggregated shared histogram of one digit of the thread's keys
-__device__ __forceinline__ void tile_hist(const uint32_t (&k)[KI], int shift, uint32_t *sh) {
-    const int lane = threadIdx.x & 31;
+// Warp multisplit by ballots: peers = lanes of the warp whose digit equals mine
+// (8 ballots, no match/atomics).  Keys of a tile are warp-striped: warp w, round r,
+// lane l holds key w*256 + r*32 + l, so (w, r, l) is the tile's index order.
+__device__ __forceinline__ unsigned digit_peers(uint32_t d) {
+    unsigned peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        const bool bit = (d >> b) & 1u;
+        const unsigned bal = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bal : ~bal;
+    }
+    return peers;
+}
+
+__device__ __forceinline__ void load_striped(const uint32_t *keys, long long off, uint32_t (&k)[KI]) {
+    const uint32_t *p = keys + off + (threadIdx.x >> 5) * 32 * KI + (threadIdx.x & 31);
+#pragma unroll
+    for (int r = 0; r < KI; r++) k[r] = p[r * 32];
+}
+
+// per-warp private digit counts (no atomics: the leader of each peer group owns its
+// digit within the warp), then the tile histogram into sh[256]
+__device__ __forceinline__ void tile_hist(const uint32_t (&k)[KI], int shift, uint32_t *wc /* [8][256] */,
+                                          uint32_t *sh) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t *c = wc + warp * 256;
+    for (int i = lane; i < 256; i += 32) c[i] = 0u;
+    __syncwarp();
 #pragma unroll
     for (int r = 0; r < KI; r++) {
         const uint32_t d = (k[r] >> shift) & 255u;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        if (lane == __ffs(peers) - 1) atomicAdd(&sh[d], (uint32_t)__popc(peers));
+        const unsigned peers = digit_peers(d);
+        if (lane == __ffs(peers) - 1) c[d] += (uint32_t)__popc(peers);
+        __syncwarp();
     }
+    __syncthreads();
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < KT / 32; w++) tot += wc[w * 256 + threadIdx.x];
+    sh[threadIdx.x] = tot;
 }
 
 // digit-major [P][256][T]: the exclusive scan of a payload's row-major counts is the
@@ -96,30 +126,26 @@ __device__ __forceinline__ void flush_hist(const uint32_t *sh, uint32_t *hp, int
 
 // keys of the raw payload (padding keys sort last) + digit-0 histogram
 __global__ void __launch_bounds__(KT) km_keys(const float *const *vin, KmPtr w) {
-    __shared__ uint32_t sh[256];
+    __shared__ uint32_t sh[256], wc[KT / 32 * 256];
     const int b = blockIdx.y, t = blockIdx.x;
-    sh[threadIdx.x] = 0u;
-    __syncthreads();
     const float *v = vin[b];
-    const long long i0 = (long long)t * KTILE + threadIdx.x * KI;
+    const long long i0 = (long long)t * KTILE + (threadIdx.x >> 5) * 32 * KI + (threadIdx.x & 31);
     uint32_t k[KI];
 #pragma unroll
-    for (int r = 0; r < KI; r++) k[r] = (i0 + r < w.nv) ? f2key(v[i0 + r]) : 0xffffffffu;
-    uint4 *o = reinterpret_cast<uint4 *>(w.keysA + (long long)b * w.T * KTILE + i0);
-    o[0] = make_uint4(k[0], k[1], k[2], k[3]);
-    o[1] = make_uint4(k[4], k[5], k[6], k[7]);
-    tile_hist(k, 0, sh);
+    for (int r = 0; r < KI; r++) k[r] = (i0 + r * 32 < w.nv) ? f2key(v[i0 + r * 32]) : 0xffffffffu;
+    uint32_t *o = w.keysA + (long long)b * w.T * KTILE + i0;
+#pragma unroll
+    for (int r = 0; r < KI; r++) o[r * 32] = k[r];
+    tile_hist(k, 0, wc, sh);
     flush_hist(sh, w.hist + (long long)b * 256 * w.T, w.T, t);
 }
 
 __global__ void __launch_bounds__(KT) km_hist(const uint32_t *keys, KmPtr w, int shift) {
-    __shared__ uint32_t sh[256];
+    __shared__ uint32_t sh[256], wc[KT / 32 * 256];
     const int b = blockIdx.y, t = blockIdx.x;
-    sh[threadIdx.x] = 0u;
-    __syncthreads();
     uint32_t k[KI];
-    load_tile(keys, ((long long)b * w.T + t) * KTILE, k);
-    tile_hist(k, shift, sh);
+    load_striped(keys, ((long long)b * w.T + t) * KTILE, k);
+    tile_hist(k, shift, wc, sh);
     flush_hist(sh, w.hist + (long long)b * 256 * w.T, w.T, t);
 }
 
@@ -155,37 +181,50 @@ __global__ void __launch_bounds__(SCW * 32) km_scan(KmPtr w) {
     if (lane == 0) w.dtot[(long long)b * 256 + d] = carry;
 }
 
-struct DigitOf {
-    uint32_t shift;
-    __device__ __forceinline__ uint32_t Digit(uint32_t k) const { return (k >> shift) & 255u; }
-};
-
-// stable rank of the tile's keys by the digit (match-based, warp-striped input), then
-// scatter to offset(digit, tile) + (rank - first rank of the digit in the tile)
+// stable scatter of one tile by the digit: rank = (keys of the digit in earlier warps)
+// + (in earlier rounds of my warp) + (in lower lanes of my round); destination =
+// offset(digit, tile) + rank.
 __global__ void __launch_bounds__(KT) km_scatter(const uint32_t *kin, uint32_t *kout, KmPtr w, int shift) {
-    using Rank = cub::BlockRadixRankMatch<KT, 8, false>;
     using Scan = cub::BlockScan<uint32_t, KT>;
-    __shared__ typename Rank::TempStorage tmp;
     __shared__ typename Scan::TempStorage stmp;
-    __shared__ uint32_t dstart[256], goff[256];
+    __shared__ uint32_t wc[KT / 32 * 256], goff[256];
     const int b = blockIdx.y, t = blockIdx.x;
-    const long long pb = (long long)b * w.T * KTILE;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t *src = kin + pb + (long long)t * KTILE + warp * 32 * KI + lane;
-    uint32_t k[KI];
-#pragma unroll
-    for (int r = 0; r < KI; r++) k[r] = src[r * 32];  // warp-striped
+    const long long pb = (long long)b * w.T * KTILE;
+    uint32_t k[KI], rank[KI];
+    load_striped(kin, pb + (long long)t * KTILE, k);
     uint32_t base;
     Scan(stmp).ExclusiveSum(w.dtot[(long long)b * 256 + threadIdx.x], base);
     goff[threadIdx.x] = base + w.hist[((long long)b * 256 + threadIdx.x) * w.T + t];
-    int rank[KI], pre[1];
-    Rank(tmp).RankKeys(k, rank, DigitOf{(uint32_t)shift}, pre);
-    dstart[threadIdx.x] = (uint32_t)pre[0];
+    uint32_t *c = wc + warp * 256;
+    for (int i = lane; i < 256; i += 32) c[i] = 0u;
+    __syncwarp();
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int r = 0; r < KI; r++) {
+        const uint32_t d = (k[r] >> shift) & 255u;
+        const unsigned peers = digit_peers(d);
+        const uint32_t before = c[d];
+        rank[r] = before + (uint32_t)__popc(peers & lt);
+        __syncwarp();
+        if (lane == __ffs(peers) - 1) c[d] = before + (uint32_t)__popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {  // exclusive prefix over warps, per digit (thread = digit), in place
+        uint32_t run = 0;
+#pragma unroll
+        for (int q = 0; q < KT / 32; q++) {
+            const uint32_t x = wc[q * 256 + threadIdx.x];
+            wc[q * 256 + threadIdx.x] = run;
+            run += x;
+        }
+    }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < KI; r++) {
         const uint32_t d = (k[r] >> shift) & 255u;
-        kout[pb + goff[d] + ((uint32_t)rank[r] - dstart[d])] = k[r];
+        kout[pb + goff[d] + c[d] + rank[r]] = k[r];
     }
 }
 
