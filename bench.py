@@ -250,7 +250,8 @@ def main():
     apps = cfg.e1 + 1
     share = {c: comp_ms[c] * apps / (ms / args.steps) for c in comp_ms}
     dom = max(comp_ms, key=lambda c: comp_ms[c])
-    names = {0: "fp_kernel (forward projector A p)", 1: "bp_kernel<CGQ> (A^T s + c p, fused p.q)"}
+    names = {0: "forward projector A p (fp_persist_f32 tile pass + fp_reduce)",
+             1: "backprojector A^T s + c p with fused p.q (bp_tile_kernel<float,CGQ>)"}
     achieved = comp_units[dom] / (comp_ms[dom] / 1e3) / 1e9
     peak_vu = LSU_VU_PER_CLK_SM * 148 * pk["sm_max_mhz"] * 1e6 / 1e9
     n_local = st["local_nodes"]
@@ -258,14 +259,14 @@ def main():
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = prof.get({0: "fp_kernel", 1: "bp_kernel"}[dom])
+        traffic = prof.get({0: "fp", 1: "bp"}[dom])
     except Exception:
         pass
     roofline = {
         "bound": "alu", "kernel": names[dom], "achieved": achieved, "peak": peak_vu, "unit": "GVU/s",
         "frac": achieved / peak_vu, "traffic": traffic,
-        "peak_basis": f"LSU/L1 data path: {LSU_VU_PER_CLK_SM} VU/clk/SM x 148 SMs x {pk['sm_max_mhz']} MHz "
-                      f"({pk['src']}); see DESIGN.md",
+        "peak_basis": f"shared-memory data path: 2 x 4-byte taps per VU at 128 B/clk/SM = {LSU_VU_PER_CLK_SM} "
+                      f"VU/clk/SM x 148 SMs x {pk['sm_max_mhz']} MHz (sm_max_mhz {pk['src']}); DESIGN.md section 6",
         "hbm_compulsory_gbs": compulsory / (comp_ms[dom] / 1e3) / 1e9, "hbm_peak_gbs": pk["hbm_gbs"],
         "share_of_step": share[dom],
         "components_ms": {"fp": comp_ms[0], "bp_cgq": comp_ms[1]},
