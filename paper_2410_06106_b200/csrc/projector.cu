@@ -1,4 +1,6 @@
 // projector.cu -- see projector.cuh.
+#include <cuda.h>
+
 #include "projector.cuh"
 
 namespace tq {
@@ -416,51 +418,82 @@ __device__ __forceinline__ FpUnit fp_unit(const FpArgs<float> &a, int u, int nti
     return U;
 }
 
-__global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<float> a, int nunits) {
+// mbarrier / TMA helpers (sm_90+ PTX; sm_100a SASS: SYNCS / UTMALDG / UBLKCP)
+__device__ __forceinline__ void mbar_init(uint32_t bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, unsigned phase) {
+    unsigned ok = 0;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, uint32_t bar) {
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                 ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, unsigned bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
+// Persistent, TMA-pipelined forward tile pass.  Each CTA walks the work units
+// u = (orientation, node, tile) round-robin; while it computes unit u from the pair
+// tile P, one thread has already issued the TMA tensor load of unit u+grid's raw tile
+// (y-major: a 32 x 128 box of the [L][N][N] images; x-major: a 128 x 32 box stored with
+// the 128-byte swizzle, i.e. conflict-free column reads) and a bulk copy of its window
+// records, both completing on one mbarrier.  Out-of-image pixels are zero-filled by TMA.
+__global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<float> a, int nunits,
+                                                                const __grid_constant__ CUtensorMap tm_rows,
+                                                                const __grid_constant__ CUtensorMap tm_cols) {
     constexpr int H = FP_HALO_A;
-    extern __shared__ __align__(16) unsigned char fp_smem[];
-    float2 *pt = reinterpret_cast<float2 *>(fp_smem);                       // [TH][PITCH] (e, d)
-    float *raw = reinterpret_cast<float *>(pt + FP_TH * FP2_PITCH);           // [FPP_RAW]
-    FpRec *rec = reinterpret_cast<FpRec *>(raw + FPP_RAW);                    // [2][FP_MAXA]
+    extern __shared__ __align__(16) unsigned char fp_smem_raw[];
+    // raw first, 1024-byte aligned (TMA 128-byte swizzle)
+    unsigned char *fp_smem = fp_smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(fp_smem_raw) & 1023u)) & 1023u);
+    float *raw = reinterpret_cast<float *>(fp_smem);                          // [FPP_RAW]
+    float2 *pt = reinterpret_cast<float2 *>(raw + FPP_RAW);                    // [TH][PITCH] (e, d)
+    FpRec *rec = reinterpret_cast<FpRec *>(pt + FP_TH * FP2_PITCH);            // [2][FP_MAXA]
     __shared__ int s_pre[FP_MAXA + 1];
-    const int N = a.N;
+    __shared__ unsigned char s_item_k[256];
+    __shared__ __align__(8) unsigned long long bar;
     const int ntiles = a.nt_line * a.nt_cross;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t raw_s = (uint32_t)__cvta_generic_to_shared(raw);
     const uint32_t rec_s = (uint32_t)__cvta_generic_to_shared(rec);
+    const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&bar);
 
     // halo pairs are (0, 0) for every unit
     for (int i = threadIdx.x; i < FP_TH * (FP2_PITCH - FP_TW - 1); i += FP_THREADS) {
         const int l = i / (FP2_PITCH - FP_TW - 1), k = i % (FP2_PITCH - FP_TW - 1);
         pt[l * FP2_PITCH + (k < H - 1 ? k : k + FP_TW + 1)] = make_float2(0.f, 0.f);
     }
-    // prefetch of unit u into raw (+ its first window records into rec buffer rb)
-    auto issue = [&](int u, int rb) {
-        if (u >= nunits) return;
+    if (threadIdx.x == 0) {
+        mbar_init(bar_s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // thread 0: TMA of unit u's raw tile + bulk copy of its first window records; returns
+    // whether anything was issued (units without angles of that orientation are skipped)
+    auto issue = [&](int u, int rb) -> bool {
+        if (u >= nunits) return false;
         const FpUnit U = fp_unit(a, u, ntiles);
-        if (U.a_begin == U.a_end) return;
-        const int lt = U.tile / a.nt_cross, ct = U.tile % a.nt_cross;
-        const int L0 = lt * FP_TH, X0 = ct * FP_TW;
-        const float *img = a.img + (long long)U.node * a.n;
-        for (int c = threadIdx.x; c < FPP_RAW / 4; c += FP_THREADS) {
-            int r, col;
-            uint32_t dst;
-            if (U.O == 0) {  // raw[l][x]
-                const int l = c >> 5, q = c & 31;
-                r = L0 + l; col = X0 + 4 * q;
-                dst = raw_s + 16u * c;
-            } else {  // raw[y][line], 16-byte chunks XOR-swizzled by (y & 7): conflict-free column reads
-                const int y = c >> 3, q = c & 7;
-                r = X0 + y; col = L0 + 4 * q;
-                dst = raw_s + 16u * (8 * y + (q ^ (y & 7)));
-            }
-            const bool ok = r < N && col < N;
-            cp_async16(dst, ok ? (const void *)(img + (long long)r * N + col) : (const void *)img, ok);
+        if (U.a_begin == U.a_end) return false;
+        if (threadIdx.x == 0) {
+            const int lt = U.tile / a.nt_cross, ct = U.tile % a.nt_cross;
+            const int L0 = lt * FP_TH, X0 = ct * FP_TW;
+            const int nb = min(FP_MAXA, U.a_end - U.a_begin);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of raw before the async write
+            mbar_expect_tx(bar_s, FPP_RAW * 4 + nb * (unsigned)sizeof(FpRec));
+            if (U.O == 0) tma_load_3d(raw_s, &tm_rows, X0, L0, U.node, bar_s);
+            else tma_load_3d(raw_s, &tm_cols, L0, X0, U.node, bar_s);
+            bulk_load(rec_s + (uint32_t)(rb * FP_MAXA * sizeof(FpRec)), a.recs + (long long)U.tile * a.n_olist + U.a_begin,
+                      nb * (unsigned)sizeof(FpRec), bar_s);
         }
-        const int nb = min(FP_MAXA, U.a_end - U.a_begin);
-        const FpRec *src = a.recs + (long long)U.tile * a.n_olist + U.a_begin;
-        for (int c = threadIdx.x; c < nb * 2; c += FP_THREADS)
-            cp_async16(rec_s + (uint32_t)(rb * FP_MAXA * 32 + 16 * c), reinterpret_cast<const char *>(src) + 16 * c, true);
+        return true;
     };
     auto pair = [](float x, float xn, int i) {
         const float d = xn - x;
@@ -468,11 +501,14 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
     };
 
     int rb = 0;
-    issue(blockIdx.x, rb);
-    cp_async_commit();
+    unsigned phase = 0;
+    bool pending = issue(blockIdx.x, rb);
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, rb ^= 1) {
         const FpUnit U = fp_unit(a, u, ntiles);
-        cp_async_wait_all();
+        if (pending) {
+            mbar_wait(bar_s, phase);
+            phase ^= 1;
+        }
         __syncthreads();  // raw + rec[rb] of unit u landed; previous unit's P reads done
         const bool active = U.a_begin != U.a_end;
         const int lt = U.tile / a.nt_cross, ct = U.tile % a.nt_cross;
@@ -520,8 +556,7 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
             }
         }
         __syncthreads();  // P ready; raw free
-        issue(u + gridDim.x, rb ^ 1);
-        cp_async_commit();
+        pending = issue(u + gridDim.x, rb ^ 1);
         if (!active) continue;
         const uint32_t sb = (uint32_t)__cvta_generic_to_shared(pt) - a.magic;
         for (int b0 = U.a_begin; b0 < U.a_end; b0 += FP_MAXA) {
@@ -547,14 +582,21 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
             if (threadIdx.x >= 32 && threadIdx.x < FP_MAXA) s_pre[threadIdx.x + 1] += s_pre[32];
             __syncthreads();
             const int Rn = s_pre[nb];
+            // item table: the angle of each item's first ray (<= 256 items per batch)
+            for (int k = threadIdx.x; k < nb; k += FP_THREADS)
+                for (int it = (s_pre[k] + 31) >> 5; (it << 5) < s_pre[k + 1] && it < 256; it++) s_item_k[it] = (unsigned char)k;
+            __syncthreads();
             for (int g0 = warp * 32; g0 < Rn; g0 += FP_THREADS) {
                 const int g = min(g0 + lane, Rn - 1);
-                int lo = 0, hi = nb - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (s_pre[mid] <= g0) lo = mid; else hi = mid - 1;
+                int k = (g0 >> 5) < 256 ? s_item_k[g0 >> 5] : 0;
+                if ((g0 >> 5) >= 256) {  // very many rays in one batch: search
+                    int lo = 0, hi = nb - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (s_pre[mid] <= g0) lo = mid; else hi = mid - 1;
+                    }
+                    k = lo;
                 }
-                int k = lo;
                 while (s_pre[k + 1] <= g) k++;
                 const int w = g - s_pre[k];
                 const float kap = (float)(R[k].kap + (double)w * R[k].at);
@@ -573,10 +615,10 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
                     a.partial[((long long)R[k].row * a.nt_line + lt) * 2 * a.n_det + (ct & 1) * a.n_det + R[k].jlo + w] =
                         acc0 + acc1;
             }
-            __syncthreads();  // s_pre / R reuse
+            __syncthreads();  // s_pre / R / item table reuse
         }
     }
-    cp_async_wait_all();
+    if (pending) mbar_wait(bar_s, phase);
 }
 
 // ------------------------------------------------------------------ forward: static windows
@@ -832,7 +874,7 @@ void set_smem(K kernel, size_t dyn) {
 template <typename T>
 size_t fp_smem(int o) { return sizeof(T) * FP_TH * (o == 0 ? FP_PITCH_Y : FP_PITCH_X); }
 size_t fp2_smem() { return sizeof(float2) * FP_TH * FP2_PITCH; }
-size_t fpp_smem() { return sizeof(float2) * FP_TH * FP2_PITCH + sizeof(float) * FPP_RAW + sizeof(FpRec) * 2 * FP_MAXA; }
+size_t fpp_smem() { return 1024 + sizeof(float2) * FP_TH * FP2_PITCH + sizeof(float) * FPP_RAW + sizeof(FpRec) * 2 * FP_MAXA; }
 int g_fpp_grid = 0;  // persistent grid: SMs x resident CTAs (projector_setup)
 template <typename T>
 size_t bp_smem() { return sizeof(T) * BP_MAXA * BP_WB + (sizeof(T) == 4 ? 2 * sizeof(float) * BP_TS * BP_TS : 0); }
@@ -857,15 +899,48 @@ void set_all_smem() {
     set_smem(bp_tile_kernel<T, EPI_GD>, bp_smem<T>());
 }
 
+// TMA descriptors of the [L][N][N] fp32 images: a 128 x 32 (cols x rows) box for the
+// y-major tiles and a 32 x 128 box with the 128-byte swizzle for the x-major tiles.
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        TQ_CHECK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) fail(TQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+void make_image_maps(const float *img, int N, int L, CUtensorMap *rows, CUtensorMap *cols) {
+    const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)L};
+    const cuuint64_t strides[2] = {(cuuint64_t)N * 4, (cuuint64_t)N * N * 4};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const cuuint32_t box_r[3] = {FP_TW, FP_TH, 1}, box_c[3] = {FP_TH, FP_TW, 1};
+    auto enc = encode_tiled();
+    CUresult r1 = enc(rows, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)img, dims, strides, box_r, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r2 = enc(cols, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)img, dims, strides, box_c, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) fail(TQ_ECUDA, "cuTensorMapEncodeTiled failed");
+}
+
 template <typename T>
 void fp_dispatch(const FpArgs<T> &A, int L, cudaStream_t st) {
     const dim3 grid(A.nt_line * A.nt_cross, L);
     if constexpr (sizeof(T) == 4) {
         FpArgs<float> B = A;
         B.magic = 0x4B000000u << 3;  // 8-byte pairs (wraps mod 2^32)
-        if (A.N % 4 == 0 && A.recs) {
+        if (A.N % 4 == 0 && A.recs && ((uintptr_t)A.img & 15) == 0) {
             const int nunits = 2 * L * A.nt_line * A.nt_cross;
-            fp_persist_f32<<<std::min(nunits, g_fpp_grid), FP_THREADS, fpp_smem(), st>>>(B, nunits);
+            CUtensorMap tr, tc;
+            make_image_maps(A.img, A.N, L, &tr, &tc);
+            fp_persist_f32<<<std::min(nunits, g_fpp_grid), FP_THREADS, fpp_smem(), st>>>(B, nunits, tr, tc);
         } else {
             fp_tile_f32<0><<<grid, FP_THREADS, fp2_smem(), st>>>(B);
             fp_tile_f32<1><<<grid, FP_THREADS, fp2_smem(), st>>>(B);
