@@ -683,15 +683,22 @@ __global__ void __launch_bounds__(128) fp_reduce_kernel(const FpRedArgs<T> a) {
     const double2 t2 = a.trig[ang];
     const double inv_m = a.xmaj[ang] ? 1.0 / fabs(t2.y) : 1.0 / fabs(t2.x);
     const T *p = a.partial + (long long)row * a.nt_line * 2 * a.n_det + j;
-    T acc0 = 0, acc1 = 0;
+    // 16 independent loads in flight per step; fixed summation order (deterministic)
+    T acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int lt = 0;
-    for (; lt + 2 <= a.nt_line; lt += 2) {
-        const T x0 = p[0], x1 = p[a.n_det], x2 = p[2 * a.n_det], x3 = p[3 * a.n_det];
-        acc0 += x0 + x1;
-        acc1 += x2 + x3;
-        p += 4 * a.n_det;
+    for (; lt + 8 <= a.nt_line; lt += 8) {
+        T x[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) x[u] = p[(long long)u * a.n_det];
+#pragma unroll
+        for (int u = 0; u < 8; u++) acc[u] += x[2 * u] + x[2 * u + 1];
+        p += 16LL * a.n_det;
     }
-    if (lt < a.nt_line) acc0 += p[0] + p[a.n_det];
+    for (; lt < a.nt_line; lt++) {
+        acc[lt & 7] += p[0] + p[a.n_det];
+        p += 2LL * a.n_det;
+    }
+    const T acc0 = (acc[0] + acc[1]) + (acc[2] + acc[3]), acc1 = (acc[4] + acc[5]) + (acc[6] + acc[7]);
     T v = (T)((double)(acc0 + acc1) * inv_m);
     if (RESID) v = a.d[(long long)row * a.n_det + j] - v;
     a.out[(long long)row * a.out_stride + a.out_off + j] = v;
@@ -701,10 +708,11 @@ __global__ void __launch_bounds__(128) fp_reduce_kernel(const FpRedArgs<T> a) {
 template <typename T, int EPI>
 __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) {
     extern __shared__ __align__(16) unsigned char bp_smem[];
-    T *win = reinterpret_cast<T *>(bp_smem);  // [BP_MAXA][BP_WB], bins pre-scaled by 1/m
+    T *win = reinterpret_cast<T *>(bp_smem);  // [BP_MAXA][BP_WB], bins pre-scaled by 1/m (fp64)
+    float2 *win2 = reinterpret_cast<float2 *>(bp_smem);  // fp32: [BP_MAXA][BP_WB] pairs (s'_j, s'_{j+1})
     // fp32: the epilogue operands of the tile, prefetched with cp.async at entry so their
     // latency overlaps the angle loop: ep[0] = vin (p or x), ep[1] = b' (RESID, GD)
-    float *ep = reinterpret_cast<float *>(win + BP_MAXA * BP_WB);  // [2][BP_TS * BP_TS]
+    float *ep = reinterpret_cast<float *>(bp_smem + (sizeof(T) == 4 ? sizeof(float2) : sizeof(T)) * BP_MAXA * BP_WB);
     __shared__ double s_tau[BP_MAXA], s_csd[BP_MAXA], s_snd[BP_MAXA];
     __shared__ T s_cs[BP_MAXA], s_sn[BP_MAXA], s_im[BP_MAXA];
     __shared__ int s_jlo[BP_MAXA];
@@ -763,16 +771,21 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
         for (int i = threadIdx.x; i < kc * BP_WB; i += BP_THREADS) {
             const int k = i / BP_WB, w = i - k * BP_WB;
             const int j = s_jlo[k] + w;
-            T v = 0;
-            if (j >= 0 && j < a.n_det) v = a.s[(long long)(row0 + k0 + k) * a.s_stride + a.s_off + j] * s_im[k];
-            win[i] = v;
+            const T *srow = a.s + (long long)(row0 + k0 + k) * a.s_stride + a.s_off;
+            const T v = (j >= 0 && j < a.n_det) ? srow[j] * s_im[k] : (T)0;
+            if constexpr (sizeof(T) == 4) {
+                const T v1 = (j + 1 >= 0 && j + 1 < a.n_det) ? srow[j + 1] * s_im[k] : (T)0;
+                win2[i] = make_float2(v, v1);
+            } else {
+                win[i] = v;
+            }
         }
         __syncthreads();
         for (int k = 0; k < kc; k++) {
             const T cs = s_cs[k], sn = s_sn[k], im = s_im[k], omi = (T)1 - im;
             const T tau_t = (T)(s_tau[k] + (double)lx * s_csd[k] - (double)prow * s_snd[k]);
             if constexpr (sizeof(T) == 4) {
-                const uint32_t wb = magic_base(win + k * BP_WB, a.magic);
+                const uint32_t wb = magic_base(win2 + k * BP_WB, a.magic);  // magic = 0x4B000000 << 3
 #pragma unroll
                 for (int ky = 0; ky < 2; ky++) {
                     const float tau_r = fmaf((float)(-4 * ky), sn, tau_t);
@@ -780,12 +793,12 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
                     for (int kx = 0; kx < 8; kx++) {
                         const float tau = fmaf((float)(8 * kx), cs, tau_r);
                         const float m = __fadd_rd(tau, 8388608.0f);   // 2^23 + floor(tau)
-                        const uint32_t ad = (__float_as_uint(m) << 2) + wb;
+                        const float2 sv = lds64((__float_as_uint(m) << 3) + wb);
                         const float u = tau - (m - 8388608.0f);
                         const float w0 = __saturatef(fmaf(-u, im, 1.0f));
                         const float w1 = __saturatef(fmaf(u, im, omi));
-                        acc[ky][kx] = fmaf(w0, lds<0>(ad), acc[ky][kx]);
-                        acc[ky][kx] = fmaf(w1, lds<4>(ad), acc[ky][kx]);
+                        acc[ky][kx] = fmaf(w0, sv.x, acc[ky][kx]);
+                        acc[ky][kx] = fmaf(w1, sv.y, acc[ky][kx]);
                     }
                 }
             } else {
@@ -876,8 +889,12 @@ size_t fp_smem(int o) { return sizeof(T) * FP_TH * (o == 0 ? FP_PITCH_Y : FP_PIT
 size_t fp2_smem() { return sizeof(float2) * FP_TH * FP2_PITCH; }
 size_t fpp_smem() { return 1024 + sizeof(float2) * FP_TH * FP2_PITCH + sizeof(float) * FPP_RAW + sizeof(FpRec) * 2 * FP_MAXA; }
 int g_fpp_grid = 0;  // persistent grid: SMs x resident CTAs (projector_setup)
-template <typename T>
-size_t bp_smem() { return sizeof(T) * BP_MAXA * BP_WB + (sizeof(T) == 4 ? 2 * sizeof(float) * BP_TS * BP_TS : 0); }
+template <typename T, int EPI>
+size_t bp_smem() {
+    constexpr int NEP = (EPI == EPI_CGQ) ? 1 : ((EPI == EPI_RESID || EPI == EPI_GD) ? 2 : 0);
+    return sizeof(T) == 4 ? sizeof(float2) * BP_MAXA * BP_WB + NEP * sizeof(float) * BP_TS * BP_TS
+                          : sizeof(T) * BP_MAXA * BP_WB;
+}
 
 template <typename T>
 void set_all_smem() {
@@ -893,10 +910,10 @@ void set_all_smem() {
         TQ_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fp_persist_f32, FP_THREADS, fpp_smem()));
         g_fpp_grid = sms * std::max(1, per);
     }
-    set_smem(bp_tile_kernel<T, EPI_PLAIN>, bp_smem<T>());
-    set_smem(bp_tile_kernel<T, EPI_CGQ>, bp_smem<T>());
-    set_smem(bp_tile_kernel<T, EPI_RESID>, bp_smem<T>());
-    set_smem(bp_tile_kernel<T, EPI_GD>, bp_smem<T>());
+    set_smem(bp_tile_kernel<T, EPI_PLAIN>, bp_smem<T, EPI_PLAIN>());
+    set_smem(bp_tile_kernel<T, EPI_CGQ>, bp_smem<T, EPI_CGQ>());
+    set_smem(bp_tile_kernel<T, EPI_RESID>, bp_smem<T, EPI_RESID>());
+    set_smem(bp_tile_kernel<T, EPI_GD>, bp_smem<T, EPI_GD>());
 }
 
 // TMA descriptors of the [L][N][N] fp32 images: a 128 x 32 (cols x rows) box for the
@@ -952,13 +969,14 @@ void fp_dispatch(const FpArgs<T> &A, int L, cudaStream_t st) {
 }
 
 template <typename T>
-void bp_dispatch(int epi, const BpArgs<T> &A, dim3 grid, cudaStream_t st) {
-    const size_t sm = bp_smem<T>();
+void bp_dispatch(int epi, const BpArgs<T> &A0, dim3 grid, cudaStream_t st) {
+    BpArgs<T> A = A0;
+    A.magic = 0x4B000000u << 3;  // fp32 pair windows (wraps mod 2^32)
     switch (epi) {
-        case EPI_PLAIN: bp_tile_kernel<T, EPI_PLAIN><<<grid, BP_THREADS, sm, st>>>(A); break;
-        case EPI_CGQ: bp_tile_kernel<T, EPI_CGQ><<<grid, BP_THREADS, sm, st>>>(A); break;
-        case EPI_RESID: bp_tile_kernel<T, EPI_RESID><<<grid, BP_THREADS, sm, st>>>(A); break;
-        default: bp_tile_kernel<T, EPI_GD><<<grid, BP_THREADS, sm, st>>>(A); break;
+        case EPI_PLAIN: bp_tile_kernel<T, EPI_PLAIN><<<grid, BP_THREADS, bp_smem<T, EPI_PLAIN>(), st>>>(A); break;
+        case EPI_CGQ: bp_tile_kernel<T, EPI_CGQ><<<grid, BP_THREADS, bp_smem<T, EPI_CGQ>(), st>>>(A); break;
+        case EPI_RESID: bp_tile_kernel<T, EPI_RESID><<<grid, BP_THREADS, bp_smem<T, EPI_RESID>(), st>>>(A); break;
+        default: bp_tile_kernel<T, EPI_GD><<<grid, BP_THREADS, bp_smem<T, EPI_GD>(), st>>>(A); break;
     }
 }
 
