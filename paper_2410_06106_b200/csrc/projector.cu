@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(FP_THREADS) fp_tile_kernel(const FpArgs<T> a) 
     }
     using VT = typename V16<T>::type;
     constexpr int VN = V16<T>::n;
-    if (N % VN != 0) {  // rows not 16-byte aligned (odd N, stateless calls only): scalar staging
+    if (N % VN != 0 || ((uintptr_t)img & 15) != 0) {  // rows not 16-byte aligned (stateless calls only): scalar staging
         for (int i = threadIdx.x; i < FP_TH * FP_TW; i += FP_THREADS) {
             const int l = i / FP_TW, x = i % FP_TW;
             const int r = O == 0 ? L0 + l : X0 + x, c = O == 0 ? X0 + x : L0 + l;
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(FP_THREADS, 4) fp_tile_f32(const FpArgs<float>
         const float d = xn - x;
         return make_float2(fmaf(-(float)(i - FP2_ORG), d, x), d);
     };
-    if ((N & 3) != 0) {  // odd N (stateless calls only): scalar loads
+    if ((N & 3) != 0 || ((uintptr_t)img & 15) != 0) {  // unaligned rows (stateless calls only): scalar loads
         for (int i = threadIdx.x; i < FP_TH * (FP_TW + 1); i += FP_THREADS) {
             const int l = i / (FP_TW + 1), k = i % (FP_TW + 1) - 1;  // k = -1 .. TW-1
             auto at = [&](int kk) -> float {

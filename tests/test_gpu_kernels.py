@@ -35,6 +35,8 @@ PROJ_CASES = [
     (37, 20, 53, None),                       # N not a multiple of 8 (stateless API allows it)
     (256, 180, 363, list(range(3, 180, 8))),  # C2 node 3 (round-robin)
     (8, 4, 13, None),                         # tiny, includes the 45 degree tie
+    (64, 180, 91, None),                      # > 64 angles per orientation: several forward and backward batches
+    (200, 100, 283, None),                    # N not a multiple of the 128 x 32 / 64 x 64 tiles (TMA zero fill)
 ]
 
 
@@ -50,6 +52,19 @@ def test_project_backproject_parity(N, n_ang, n_det, sel, prec):
     refb = oracle.backproject(y, N, n_ang, sel_a)
     gotb = tomoq.backproject(torch.tensor(y, dtype=DT[prec], device=DEV), N, n_ang, sel_a)
     assert rel(gotb.cpu().numpy(), refb) <= TOL[prec]
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_project_unaligned_input(prec):
+    """A caller's image that is not 16-byte aligned takes the scalar staging path."""
+    N, n_ang, n_det = 64, 30, 91
+    img = as_input(phantom(N, 77), prec)
+    buf = torch.zeros(N * N + 1, dtype=DT[prec], device=DEV)
+    buf[1:] = torch.tensor(img.ravel(), dtype=DT[prec], device=DEV)
+    view = buf[1:].view(N, N)
+    assert view.data_ptr() % 16 != 0
+    got = tomoq.project(view, n_ang, n_det)
+    assert rel(got.cpu().numpy(), oracle.project(img, n_ang, n_det)) <= TOL[prec]
 
 
 def test_adjoint_identity_fp32_and_fp64():
