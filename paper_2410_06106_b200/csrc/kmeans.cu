@@ -271,16 +271,29 @@ __global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters) {
     const long long *cs = w.csum + (long long)b * nch;
     long long *cp = w.cpre + (long long)b * nch;
     const double scale = ldexp(1.0, w.fexp[b]);
-    // exclusive prefix of the chunk sums (global) and the tile head keys (shared)
-    long long carry = 0;
-    for (long long c0 = 0; c0 < nch; c0 += LT) {
-        const long long c = c0 + threadIdx.x;
-        const long long x = c < nch ? cs[c] : 0;
-        long long ex, agg;
-        Scan(tmp).ExclusiveSum(x, ex, agg);
-        if (c < nch) cp[c] = carry + ex;
-        carry += agg;
-        __syncthreads();
+    // exclusive prefix of the chunk sums (global): each thread scans a run of consecutive
+    // chunks, one block scan joins the runs
+    const long long per = (nch + LT - 1) / LT;
+    const long long c_lo = min(nch, threadIdx.x * per), c_hi = min(nch, c_lo + per);
+    long long run = 0;
+    for (long long c = c_lo; c < c_hi; c += 8) {  // 8 independent loads in flight
+        long long x[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) x[u] = c + u < c_hi ? __ldcg(cs + c + u) : 0;
+#pragma unroll
+        for (int u = 0; u < 8; u++) run += x[u];
+    }
+    long long ex, carry;
+    Scan(tmp).ExclusiveSum(run, ex, carry);
+    for (long long c = c_lo; c < c_hi; c += 8) {
+        long long x[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) x[u] = c + u < c_hi ? __ldcg(cs + c + u) : 0;
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            if (c + u < c_hi) cp[c + u] = ex;
+            ex += x[u];
+        }
     }
     for (int t = threadIdx.x; t < T; t += LT) thead[t] = sorted[(long long)t * KTILE];
     if (threadIdx.x == 0) total_s = carry;
@@ -291,35 +304,54 @@ __global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters) {
     for (int it = 0; it < iters; it++) {
         for (int k = threadIdx.x; k + 1 < K; k += LT) thr[k] = (float)(((double)cen[k] + (double)cen[k + 1]) * 0.5);
         __syncthreads();
-        for (int k = warp; k + 1 < K; k += LT / 32) {
-            const uint32_t kb = f2key(thr[k]);
-            int lo = 0, hi = T - 1, tt = -1;  // last tile whose head key <= kb
-            while (lo <= hi) {
-                const int mid = (lo + hi) >> 1;
-                if (thead[mid] <= kb) { tt = mid; lo = mid + 1; } else hi = mid - 1;
+        // two thresholds per warp at a time: their dependent global loads overlap
+        for (int k0 = warp; k0 + 1 < K; k0 += 2 * (LT / 32)) {
+            int kk[2], tt[2], cc[2];
+            uint32_t kb[2], h[2], e0[2], e1[2];
+            long long pre[2];
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
+                kk[q] = k0 + q * (LT / 32);
+                kb[q] = kk[q] + 1 < K ? f2key(thr[kk[q]]) : 0u;
+                int lo = 0, hi = T - 1, t = -1;  // last tile whose head key <= kb
+                while (lo <= hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (thead[mid] <= kb[q]) { t = mid; lo = mid + 1; } else hi = mid - 1;
+                }
+                tt[q] = kk[q] + 1 < K ? t : -1;
             }
-            long long C = 0, S = 0;
-            if (tt >= 0) {
-                const long long tb = (long long)tt * KTILE;
+#pragma unroll
+            for (int q = 0; q < 2; q++) h[q] = tt[q] >= 0 ? sorted[(long long)tt[q] * KTILE + lane * KCH] : 0xffffffffu;
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
                 // last chunk of the tile whose head key <= kb (chunk 0 qualifies)
-                const unsigned m = __ballot_sync(0xffffffffu, sorted[tb + lane * KCH] <= kb);
-                const int cc = 31 - __clz(m);
-                const long long cb = tb + (long long)cc * KCH;
-                const uint32_t e0 = sorted[cb + lane], e1 = sorted[cb + 32 + lane];
-                const long long pre = cp[(long long)tt * CPT + cc];
+                const unsigned m = __ballot_sync(0xffffffffu, h[q] <= kb[q]);
+                cc[q] = m ? 31 - __clz(m) : 0;
+                const long long cb = (long long)max(tt[q], 0) * KTILE + (long long)cc[q] * KCH;
+                e0[q] = tt[q] >= 0 ? sorted[cb + lane] : 0xffffffffu;
+                e1[q] = tt[q] >= 0 ? sorted[cb + 32 + lane] : 0xffffffffu;
+                pre[q] = tt[q] >= 0 ? cp[(long long)tt[q] * CPT + cc[q]] : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
+                if (kk[q] + 1 >= K) continue;
+                const long long cb = (long long)max(tt[q], 0) * KTILE + (long long)cc[q] * KCH;
                 int cnt = 0;
-                long long s = 0;
-                if (e0 <= kb && cb + lane < nv) { cnt++; s += __double2ll_rn((double)key2f(e0) * scale); }
-                if (e1 <= kb && cb + 32 + lane < nv) { cnt++; s += __double2ll_rn((double)key2f(e1) * scale); }
+                long long sm = 0;
+                if (tt[q] >= 0) {
+                    if (e0[q] <= kb[q] && cb + lane < nv) { cnt++; sm += __double2ll_rn((double)key2f(e0[q]) * scale); }
+                    if (e1[q] <= kb[q] && cb + 32 + lane < nv) { cnt++; sm += __double2ll_rn((double)key2f(e1[q]) * scale); }
+                }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
                     cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-                    s += __shfl_xor_sync(0xffffffffu, s, o);
+                    sm += __shfl_xor_sync(0xffffffffu, sm, o);
                 }
-                C = cb + cnt;
-                S = pre + s;
+                if (lane == 0) {
+                    Cs[kk[q]] = tt[q] >= 0 ? cb + cnt : 0;
+                    Ss[kk[q]] = tt[q] >= 0 ? pre[q] + sm : 0;
+                }
             }
-            if (lane == 0) { Cs[k] = C; Ss[k] = S; }
         }
         __syncthreads();
         for (int k = threadIdx.x; k < K; k += LT) {
