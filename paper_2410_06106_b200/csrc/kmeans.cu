@@ -28,11 +28,11 @@ namespace tq {
 namespace {
 
 constexpr int KT = 256;               // threads of the per-tile kernels
-constexpr int KI = 8;                 // keys per thread
+constexpr int KI = 16;                // keys per thread
 constexpr int KTILE = KT * KI;        // keys per tile
 constexpr int LT = 1024;              // threads of the Lloyd kernel
-constexpr int MAX_TILES = 8192;       // per payload (n <= 16.7 M)
-constexpr int KCH = 64;               // keys per prefix-sum chunk
+constexpr int MAX_TILES = 4096;       // per payload (n <= 16.7 M)
+constexpr int KCH = 128;              // keys per prefix-sum chunk
 constexpr int CPT = KTILE / KCH;      // chunks per tile (32)
 static_assert(CPT == 32, "one warp lane per chunk head");
 
@@ -70,9 +70,11 @@ KmPtr ptrs(const KmeansWork &w) {
 
 __device__ __forceinline__ void load_tile(const uint32_t *keys, long long off, uint32_t (&k)[KI]) {
     const uint4 *p = reinterpret_cast<const uint4 *>(keys + off + threadIdx.x * KI);
-    const uint4 a = p[0], b = p[1];
-    k[0] = a.x; k[1] = a.y; k[2] = a.z; k[3] = a.w;
-    k[4] = b.x; k[5] = b.y; k[6] = b.z; k[7] = b.w;
+#pragma unroll
+    for (int q = 0; q < KI / 4; q++) {
+        const uint4 a = p[q];
+        k[4 * q] = a.x; k[4 * q + 1] = a.y; k[4 * q + 2] = a.z; k[4 * q + 3] = a.w;
+    }
 }
 
 // Warp multisplit by ballots: peers = lanes of the warp whose digit equals mine
@@ -184,7 +186,7 @@ __global__ void __launch_bounds__(SCW * 32) km_scan(KmPtr w) {
 // stable scatter of one tile by the digit: rank = (keys of the digit in earlier warps)
 // + (in earlier rounds of my warp) + (in lower lanes of my round); destination =
 // offset(digit, tile) + rank.
-__global__ void __launch_bounds__(KT) km_scatter(const uint32_t *kin, uint32_t *kout, KmPtr w, int shift) {
+__global__ void __launch_bounds__(KT, 3) km_scatter(const uint32_t *kin, uint32_t *kout, KmPtr w, int shift) {
     using Scan = cub::BlockScan<uint32_t, KT>;
     __shared__ typename Scan::TempStorage stmp;
     __shared__ uint32_t wc[KT / 32 * 256], goff[256];
@@ -252,7 +254,7 @@ __global__ void __launch_bounds__(KT) km_csum(KmPtr w) {
     for (int r = 0; r < KI; r++)
         if (i0 + r < w.nv) s += __double2ll_rn((double)key2f(k[r]) * scale);
 #pragma unroll
-    for (int o = 1; o < KCH / KI; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);  // 8 lanes per chunk
+    for (int o = 1; o < KCH / KI; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);  // KCH/KI lanes per chunk
     if ((threadIdx.x & (KCH / KI - 1)) == 0) w.csum[(long long)b * w.T * CPT + (long long)t * CPT + threadIdx.x / (KCH / KI)] = s;
     if (t == 0 && threadIdx.x == 0) w.fexp[b] = F;
 }
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters) {
         // two thresholds per warp at a time: their dependent global loads overlap
         for (int k0 = warp; k0 + 1 < K; k0 += 2 * (LT / 32)) {
             int kk[2], tt[2], cc[2];
-            uint32_t kb[2], h[2], e0[2], e1[2];
+            uint32_t kb[2], h[2], e[2][KCH / 32];
             long long pre[2];
 #pragma unroll
             for (int q = 0; q < 2; q++) {
@@ -328,8 +330,8 @@ __global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters) {
                 const unsigned m = __ballot_sync(0xffffffffu, h[q] <= kb[q]);
                 cc[q] = m ? 31 - __clz(m) : 0;
                 const long long cb = (long long)max(tt[q], 0) * KTILE + (long long)cc[q] * KCH;
-                e0[q] = tt[q] >= 0 ? sorted[cb + lane] : 0xffffffffu;
-                e1[q] = tt[q] >= 0 ? sorted[cb + 32 + lane] : 0xffffffffu;
+#pragma unroll
+                for (int u = 0; u < KCH / 32; u++) e[q][u] = tt[q] >= 0 ? sorted[cb + 32 * u + lane] : 0xffffffffu;
                 pre[q] = tt[q] >= 0 ? cp[(long long)tt[q] * CPT + cc[q]] : 0;
             }
 #pragma unroll
@@ -339,8 +341,12 @@ __global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters) {
                 int cnt = 0;
                 long long sm = 0;
                 if (tt[q] >= 0) {
-                    if (e0[q] <= kb[q] && cb + lane < nv) { cnt++; sm += __double2ll_rn((double)key2f(e0[q]) * scale); }
-                    if (e1[q] <= kb[q] && cb + 32 + lane < nv) { cnt++; sm += __double2ll_rn((double)key2f(e1[q]) * scale); }
+#pragma unroll
+                    for (int u = 0; u < KCH / 32; u++)
+                        if (e[q][u] <= kb[q] && cb + 32 * u + lane < nv) {
+                            cnt++;
+                            sm += __double2ll_rn((double)key2f(e[q][u]) * scale);
+                        }
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
