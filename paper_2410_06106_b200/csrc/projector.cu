@@ -827,7 +827,9 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
         __syncthreads();
     }
     const double c = (EPI == EPI_CGQ || EPI == EPI_RESID || EPI == EPI_GD) ? a.cnode[node] : 0.0;
+    const float cf = (float)c;
     double dot = 0.0;
+    float dotf = 0.f;
     const long long nb = (long long)node * a.n;
 #pragma unroll
     for (int ky = 0; ky < 2; ky++)
@@ -841,10 +843,17 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
             if (EPI == EPI_PLAIN) {
                 a.out[p] = acc[ky][kx];
             } else if (EPI == EPI_CGQ) {
-                const double pv = pre ? (double)ep[sp] : (double)a.vin[p];
-                const T q = (T)(g + c * pv);
-                a.out[p] = q;
-                dot += pv * (double)q;
+                if constexpr (sizeof(T) == 4) {  // fp32: one rounding (fmaf), per-thread fp32 partial of 16 products
+                    const float pv = pre ? ep[sp] : (float)a.vin[p];
+                    const float q = fmaf(cf, pv, acc[ky][kx]);
+                    a.out[p] = q;
+                    dotf = fmaf(pv, q, dotf);
+                } else {
+                    const double pv = (double)a.vin[p];
+                    const T q = (T)(g + c * pv);
+                    a.out[p] = q;
+                    dot += pv * (double)q;
+                }
             } else if (EPI == EPI_RESID) {
                 const double xv = pre ? (double)ep[sp] : (double)a.vin[p];
                 const double bv = pre ? (double)ep[BP_TS * BP_TS + sp] : (double)a.bprime[p];
@@ -859,7 +868,7 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
             }
         }
     if (EPI == EPI_CGQ || EPI == EPI_RESID) {
-        const double bs = block_sum<BP_THREADS>(dot, red);
+        const double bs = block_sum<BP_THREADS>(dot + (double)dotf, red);
         double *part = a.partial + (long long)node * a.part_stride;
         if (threadIdx.x == 0) part[blockIdx.x] = bs;
         if (last_block_of_group(a.counter + node, gridDim.x, &last_flag)) {
