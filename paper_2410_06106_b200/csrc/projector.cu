@@ -456,8 +456,9 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
     unsigned char *fp_smem = fp_smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(fp_smem_raw) & 1023u)) & 1023u);
     float *raw = reinterpret_cast<float *>(fp_smem);                          // [FPP_RAW]
     float2 *pt = reinterpret_cast<float2 *>(raw + FPP_RAW);                    // [TH][PITCH] (e, d)
-    FpRec *rec = reinterpret_cast<FpRec *>(pt + FP_TH * FP2_PITCH);            // [2][FP_MAXA]
-    __shared__ int s_pre[FP_MAXA + 1];
+    FpRec *rec = reinterpret_cast<FpRec *>(pt + FP_TH * FP2_PITCH);            // [2][FPP_MAXA]
+    FpUnitTab *utb = reinterpret_cast<FpUnitTab *>(rec + 2 * FPP_MAXA);          // [2]
+    __shared__ int s_pre[FPP_MAXA + 1];
     __shared__ unsigned char s_item_k[256];
     __shared__ __align__(8) unsigned long long bar;
     const int ntiles = a.nt_line * a.nt_cross;
@@ -485,13 +486,14 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
         if (threadIdx.x == 0) {
             const int lt = U.tile / a.nt_cross, ct = U.tile % a.nt_cross;
             const int L0 = lt * FP_TH, X0 = ct * FP_TW;
-            const int nb = min(FP_MAXA, U.a_end - U.a_begin);
+            const int nb = min(FPP_MAXA, U.a_end - U.a_begin);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of raw before the async write
-            mbar_expect_tx(bar_s, FPP_RAW * 4 + nb * (unsigned)sizeof(FpRec));
+            mbar_expect_tx(bar_s, FPP_RAW * 4 + nb * (unsigned)sizeof(FpRec) + (unsigned)sizeof(FpUnitTab));
             if (U.O == 0) tma_load_3d(raw_s, &tm_rows, X0, L0, U.node, bar_s);
             else tma_load_3d(raw_s, &tm_cols, L0, X0, U.node, bar_s);
-            bulk_load(rec_s + (uint32_t)(rb * FP_MAXA * sizeof(FpRec)), a.recs + (long long)U.tile * a.n_olist + U.a_begin,
+            bulk_load(rec_s + (uint32_t)(rb * FPP_MAXA * sizeof(FpRec)), a.recs + (long long)U.tile * a.n_olist + U.a_begin,
                       nb * (unsigned)sizeof(FpRec), bar_s);
+            bulk_load((uint32_t)__cvta_generic_to_shared(utb + rb), a.utab + u, (unsigned)sizeof(FpUnitTab), bar_s);
         }
         return true;
     };
@@ -559,46 +561,49 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
         pending = issue(u + gridDim.x, rb ^ 1);
         if (!active) continue;
         const uint32_t sb = (uint32_t)__cvta_generic_to_shared(pt) - a.magic;
-        for (int b0 = U.a_begin; b0 < U.a_end; b0 += FP_MAXA) {
-            const int nb = min(FP_MAXA, U.a_end - b0);
-            FpRec *R = rec + rb * FP_MAXA;
+        for (int b0 = U.a_begin; b0 < U.a_end; b0 += FPP_MAXA) {
+            const int nb = min(FPP_MAXA, U.a_end - b0);
+            FpRec *R = rec + rb * FPP_MAXA;
             if (b0 != U.a_begin) {  // later batches (> 64 angles per orientation): plain loads
                 __syncthreads();
                 for (int k = threadIdx.x; k < nb; k += FP_THREADS) R[k] = a.recs[(long long)U.tile * a.n_olist + b0 + k];
                 __syncthreads();
             }
-            if (threadIdx.x < FP_MAXA) {
-                const int k = threadIdx.x;
-                int inc = k < nb ? R[k].W : 0;
+            const int *pre = utb[rb].pre;
+            const unsigned char *itk = utb[rb].item;
+            if (b0 != U.a_begin) {  // later batches: plan computed here
+                if (threadIdx.x < FPP_MAXA) {
+                    const int k = threadIdx.x;
+                    int inc = k < nb ? R[k].W : 0;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane >= o) inc += y;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                        if (lane >= o) inc += y;
+                    }
+                    s_pre[k + 1] = inc;
+                    if (k == 0) s_pre[0] = 0;
                 }
-                s_pre[k + 1] = inc;
-                if (k == 0) s_pre[0] = 0;
+                __syncthreads();
+                for (int k = threadIdx.x; k < nb; k += FP_THREADS)
+                    for (int it = (s_pre[k] + 31) >> 5; (it << 5) < s_pre[k + 1] && it < 256; it++) s_item_k[it] = (unsigned char)k;
+                __syncthreads();
+                pre = s_pre;
+                itk = s_item_k;
             }
-            __syncthreads();
-            if (threadIdx.x >= 32 && threadIdx.x < FP_MAXA) s_pre[threadIdx.x + 1] += s_pre[32];
-            __syncthreads();
-            const int Rn = s_pre[nb];
-            // item table: the angle of each item's first ray (<= 256 items per batch)
-            for (int k = threadIdx.x; k < nb; k += FP_THREADS)
-                for (int it = (s_pre[k] + 31) >> 5; (it << 5) < s_pre[k + 1] && it < 256; it++) s_item_k[it] = (unsigned char)k;
-            __syncthreads();
+            const int Rn = pre[nb];
             for (int g0 = warp * 32; g0 < Rn; g0 += FP_THREADS) {
                 const int g = min(g0 + lane, Rn - 1);
-                int k = (g0 >> 5) < 256 ? s_item_k[g0 >> 5] : 0;
+                int k = (g0 >> 5) < 256 ? itk[g0 >> 5] : 0;
                 if ((g0 >> 5) >= 256) {  // very many rays in one batch: search
                     int lo = 0, hi = nb - 1;
                     while (lo < hi) {
                         const int mid = (lo + hi + 1) >> 1;
-                        if (s_pre[mid] <= g0) lo = mid; else hi = mid - 1;
+                        if (pre[mid] <= g0) lo = mid; else hi = mid - 1;
                     }
                     k = lo;
                 }
-                while (s_pre[k + 1] <= g) k++;
-                const int w = g - s_pre[k];
+                while (pre[k + 1] <= g) k++;
+                const int w = g - pre[k];
                 const float kap = (float)(R[k].kap + (double)w * R[k].at);
                 const float B = R[k].B;
                 float acc0 = 0.f, acc1 = 0.f;
@@ -615,7 +620,7 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
                     a.partial[((long long)R[k].row * a.nt_line + lt) * 2 * a.n_det + (ct & 1) * a.n_det + R[k].jlo + w] =
                         acc0 + acc1;
             }
-            __syncthreads();  // s_pre / R / item table reuse
+            if (b0 + FPP_MAXA < U.a_end) __syncthreads();  // R / plan reuse by the next batch
         }
     }
     if (pending) mbar_wait(bar_s, phase);
@@ -669,6 +674,33 @@ __global__ void fp_rec_kernel(const int *olist, int n_olist, int ntiles, const F
         r.W = w.W;
         r.row = row;
         recs[(long long)tile * n_olist + pos] = r;
+    }
+}
+
+__global__ void fp_unit_kernel(const int *oofs, const FpRec *recs, int n_olist, int ntiles, int L, FpUnitTab *utab) {
+    __shared__ int pre[FPP_MAXA + 1];
+    const int u = blockIdx.x, per = L * ntiles;
+    const int O = u / per, rem = u - O * per, node = rem / ntiles, tile = rem - node * ntiles;
+    const int a0 = oofs[2 * node + O], a1 = oofs[2 * node + O + 1];
+    const int nb = min(FPP_MAXA, a1 - a0);
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int k = 0; k < nb; k++) {
+            pre[k] = acc;
+            acc += recs[(long long)tile * n_olist + a0 + k].W;
+        }
+        for (int k = nb; k <= FPP_MAXA; k++) pre[k] = acc;
+    }
+    __syncthreads();
+    FpUnitTab *t = utab + u;
+    for (int k = threadIdx.x; k <= FPP_MAXA; k += blockDim.x) t->pre[k] = pre[k];
+    for (int it = threadIdx.x; it < 256; it += blockDim.x) {
+        int lo = 0, hi = max(nb - 1, 0);  // angle of ray 32*it: largest k with pre[k] <= 32 it
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pre[mid] <= 32 * it) lo = mid; else hi = mid - 1;
+        }
+        t->item[it] = (unsigned char)lo;
     }
 }
 
@@ -896,7 +928,7 @@ void set_smem(K kernel, size_t dyn) {
 template <typename T>
 size_t fp_smem(int o) { return sizeof(T) * FP_TH * (o == 0 ? FP_PITCH_Y : FP_PITCH_X); }
 size_t fp2_smem() { return sizeof(float2) * FP_TH * FP2_PITCH; }
-size_t fpp_smem() { return 1024 + sizeof(float2) * FP_TH * FP2_PITCH + sizeof(float) * FPP_RAW + sizeof(FpRec) * 2 * FP_MAXA; }
+size_t fpp_smem() { return 1024 + sizeof(float2) * FP_TH * FP2_PITCH + sizeof(float) * FPP_RAW + sizeof(FpRec) * 2 * FPP_MAXA + 2 * sizeof(FpUnitTab); }
 int g_fpp_grid = 0;  // persistent grid: SMs x resident CTAs (projector_setup)
 template <typename T, int EPI>
 size_t bp_smem() {
@@ -1013,13 +1045,16 @@ void launch_fp(int prec, const void *args, int L, cudaStream_t st) {
 }
 
 void launch_fp_setup(const RayRow *rows, const int *xmaj, const double2 *trig, int n_rows, int N, int n_det,
-                     FpWin *wins, FpRowGeo *rgeo, const int *olist, int n_olist, FpRec *recs, cudaStream_t st) {
+                     FpWin *wins, FpRowGeo *rgeo, const int *olist, int n_olist, FpRec *recs, const int *oofs, int L,
+                     FpUnitTab *utab, cudaStream_t st) {
     if (n_rows == 0) return;
     const int ntiles = fp_ntiles(N);
     fp_setup_kernel<<<dim3(ceil_div(ntiles, 128), n_rows), 128, 0, st>>>(rows, xmaj, trig, n_rows, N, n_det, wins, rgeo);
     TQ_CHECK_CUDA(cudaGetLastError());
     if (n_olist) {
         fp_rec_kernel<<<dim3(ceil_div(ntiles, 128), n_olist), 128, 0, st>>>(olist, n_olist, ntiles, wins, rgeo, recs);
+        TQ_CHECK_CUDA(cudaGetLastError());
+        fp_unit_kernel<<<2 * L * ntiles, 64, 0, st>>>(oofs, recs, n_olist, ntiles, L, utab);
         TQ_CHECK_CUDA(cudaGetLastError());
     }
 }

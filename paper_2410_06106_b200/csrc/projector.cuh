@@ -35,6 +35,7 @@ constexpr int FP_HALO = FP_TH + 6;        // zero columns each side: covers a ra
 constexpr int FP_WMAX = FP_TW + FP_TH + 8;  // max rays crossing one tile for one angle
 constexpr int FP_THREADS = 256;
 constexpr int FP_MAXA = 64;               // angles per shared-memory batch
+constexpr int FPP_MAXA = 32;              // angles per batch of the persistent fp32 forward kernel
 
 // Static per-(ray row, tile) geometry of the forward tiles, computed once (fp_setup):
 // the window of rays [jlo, jlo + W) that cross the tile and the shared-memory cross
@@ -57,6 +58,16 @@ struct FpRec {
     int jlo, W, row;
 };
 
+// Static per-unit item plan of the persistent fp32 forward kernel (first batch of <= 64
+// angles of a unit): exclusive prefix of the window sizes, and the angle of each 32-ray
+// item's first ray.  Bulk-copied with the unit's records.
+struct FpUnitTab {
+    int pre[FPP_MAXA + 1];
+    unsigned char item[256];
+    int pad[3];
+};
+static_assert(sizeof(FpUnitTab) % 16 == 0, "bulk-copy granularity");
+
 template <typename T>
 struct FpArgs {
     const T *img;          // [L][n] node-major images
@@ -71,6 +82,7 @@ struct FpArgs {
     uint32_t magic;        // = 0x4B000000 << 2 (mod 2^32), see projector.cu magic_base
     const FpRec *recs;     // [ntiles][n_olist] (fp32 persistent kernel)
     int n_olist, L;
+    const FpUnitTab *utab; // [2 * L * ntiles] (fp32 persistent kernel)
 };
 
 template <typename T>
@@ -118,7 +130,8 @@ int bp_tiles(int N);
 void launch_fp(int prec, const void *args, int L, cudaStream_t st);
 // static forward geometry of n_rows rows (once per context)
 void launch_fp_setup(const RayRow *rows, const int *xmaj, const double2 *trig, int n_rows, int N, int n_det,
-                     FpWin *wins, FpRowGeo *rgeo, const int *olist, int n_olist, FpRec *recs, cudaStream_t st);
+                     FpWin *wins, FpRowGeo *rgeo, const int *olist, int n_olist, FpRec *recs, const int *oofs, int L,
+                     FpUnitTab *utab, cudaStream_t st);
 void launch_fp_reduce(int prec, bool resid, const void *args, int n_rows, int n_det, cudaStream_t st);
 void launch_bp(int prec, int epi, const void *args, int L, int N, cudaStream_t st);
 

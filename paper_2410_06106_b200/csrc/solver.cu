@@ -72,7 +72,8 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
     A((void **)&frg, sizeof(FpRowGeo) * n_rows);
     n_olist = (int)ol.size();
     A((void **)&frec, sizeof(FpRec) * (size_t)nt_line * nt_cross * std::max(1, n_olist));
-    launch_fp_setup(rows, g.xmaj, g.trig, n_rows, g.N, g.n_det, fwin, frg, olist, n_olist, frec, 0);
+    A((void **)&futab, sizeof(FpUnitTab) * 2 * (size_t)std::max(1, L) * nt_line * nt_cross);
+    launch_fp_setup(rows, g.xmaj, g.trig, n_rows, g.N, g.n_det, fwin, frg, olist, n_olist, frec, oofs, L, futab, 0);
     TQ_CHECK_CUDA(cudaDeviceSynchronize());
     for (void **v : {&X, &R, &P, &Q, &BP}) A(v, es * n * L);
     A(&D, es * (size_t)n_rows * g.n_det);
@@ -87,10 +88,10 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
 void Inner::release() {
     for (void *p : {(void *)rows, (void *)row0, (void *)nang, X, R, P, Q, BP, D, S, (void *)cnode,
                     (void *)eta, (void *)scal, (void *)partial, (void *)counter, (void *)olist,
-                    (void *)oofs, fpart, (void *)fwin, (void *)frg, (void *)frec})
+                    (void *)oofs, fpart, (void *)fwin, (void *)frg, (void *)frec, (void *)futab})
         if (p) cudaFree(p);
     rows = nullptr; row0 = nang = olist = oofs = nullptr;
-    fpart = nullptr; fwin = nullptr; frg = nullptr; frec = nullptr;
+    fpart = nullptr; fwin = nullptr; frg = nullptr; frec = nullptr; futab = nullptr;
     X = R = P = Q = BP = D = S = nullptr;
     cnode = eta = scal = partial = nullptr;
     counter = nullptr;
@@ -101,14 +102,14 @@ int Inner::project(const DevGeom &g, const void *img, bool resid, cudaStream_t s
     if (!out) { out = S; out_stride = sp; out_off = 1; }
     if (prec == 0) {
         FpArgs<float> a{(const float *)img, n, g.N, g.n_det, olist, oofs, fwin, frg, (float *)fpart,
-                        nt_line, nt_cross, kMagicBits4, frec, n_olist, L};
+                        nt_line, nt_cross, kMagicBits4, frec, n_olist, L, futab};
         launch_fp(0, &a, L, st);
         FpRedArgs<float> r{(const float *)fpart, rows, g.trig, g.xmaj, (const float *)D, (float *)out,
                            out_stride, out_off, g.N, g.n_det, nt_line};
         launch_fp_reduce(0, resid, &r, n_rows, g.n_det, st);
     } else {
         FpArgs<double> a{(const double *)img, n, g.N, g.n_det, olist, oofs, fwin, frg, (double *)fpart,
-                         nt_line, nt_cross, kMagicBits4, frec, n_olist, L};
+                         nt_line, nt_cross, kMagicBits4, frec, n_olist, L, futab};
         launch_fp(1, &a, L, st);
         FpRedArgs<double> r{(const double *)fpart, rows, g.trig, g.xmaj, (const double *)D,
                             (double *)out, out_stride, out_off, g.N, g.n_det, nt_line};

@@ -32,6 +32,7 @@ struct Inner {
     FpWin *fwin = nullptr;     // [n_rows][fp_ntiles] static ray windows of the forward tiles
     FpRowGeo *frg = nullptr;   // [n_rows]
     FpRec *frec = nullptr;     // [fp_ntiles][n_olist] (persistent fp32 forward kernel)
+    FpUnitTab *futab = nullptr; // [2 L fp_ntiles]
     int n_olist = 0;
     int nt_line = 0, nt_cross = 0;
     void *X = nullptr, *R = nullptr, *P = nullptr, *Q = nullptr, *BP = nullptr;  // [L][n]
