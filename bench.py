@@ -112,14 +112,23 @@ def cpu_baseline(cfg_g1, iters=2):
                                         f"K-means 64), OpenMP over nodes", "seconds": round(dt, 2)}
 
 
+def bench_config(cfg, world):
+    """The `config` object of the JSON line (identical for both arms)."""
+    return {"workload": cfg.name, "N": cfg.N, "nodes": cfg.nodes, "nodes_per_gpu": cfg.nodes // world,
+            "n_angles": cfg.n_angles, "n_det": cfg.n_det, "graph": "random 4-regular",
+            "inner": "CG5", "quantizer": "kmeans K=64 (10 Lloyd)", "rule": "graph",
+            "parallelism": f"nodes interleaved over {world} GPU(s), NCCL send/recv of payloads",
+            "l2": "no flush: per-GPU working set ~0.25 GB > 126 MB L2"}
+
+
 def run_reference(args):
     """--impl reference: the oracle, rank 0 only."""
-    rank = env_int("RANK", 0)
+    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
     if rank != 0:
         return
     from paper_2410_06106_b200 import configs as C
     from tests.cases import oracle_case
-    cfg = C.C4(1)
+    cfg = C.C4(1)  # bounded sample: the per-GPU share of C4_G<world> (8 nodes, 90 angles)
     inp = C.make_inputs(cfg, with_truth=False)
     threads = min(cfg.nodes, os.cpu_count() or 1)
     o = oracle_case(cfg, inp, threads=threads)
@@ -128,14 +137,13 @@ def run_reference(args):
     o.run(args.steps)
     dt = time.perf_counter() - t0
     value = vu_per_iter(cfg) * args.steps / dt / 1e9
-    sample = (f"each step = 1 ADMM iteration of {cfg.name} (the per-GPU share of config 4: 8 nodes, "
-              f"1024^2, 90 angles, CG5, K-means 64) on the fp64 CPU oracle")
+    sample = (f"each step = 1 ADMM iteration of {cfg.name} (the per-GPU share of C4_G{world}: 8 nodes, "
+              f"1024^2, 90 angles, CG5, K-means 64) on the fp64 CPU oracle, OpenMP over nodes")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / max(1, args.steps),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": cfg.name, "N": cfg.N, "nodes": cfg.nodes,
-                                        "n_angles": cfg.n_angles, "quantizer": "kmeans64"},
+        "data": "synthetic", "config": bench_config(C.C4(world), world),
         "admm_iters_per_s": args.steps / dt,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -145,7 +153,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -282,11 +290,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == 0 else "f64",
             "data": "synthetic",
-            "config": {"workload": cfg.name, "N": cfg.N, "nodes": cfg.nodes, "nodes_per_gpu": cfg.nodes // world,
-                       "n_angles": cfg.n_angles, "n_det": cfg.n_det, "graph": "random 4-regular",
-                       "inner": "CG5", "quantizer": "kmeans K=64 (10 Lloyd)", "rule": "graph",
-                       "parallelism": f"nodes interleaved over {world} GPU(s), NCCL send/recv of payloads",
-                       "l2": "no flush: per-GPU working set ~0.2 GB > 126 MB L2"},
+            "config": bench_config(cfg, world),
             "admm_iters_per_s": iters_per_s,
             "vu_per_step": vu_it,
             "roofline": roofline,
