@@ -127,6 +127,15 @@ def test_lockstep_full_size_bench_config():
     assert lockstep(cfg, inp, steps=1, warm=1, label_nodes=[0, 5]) <= 1e-3
 
 
+@pytest.mark.parametrize("make", [C.C2, C.C3])
+def test_lockstep_full_size_configs(make):
+    """Configs 2 (256^2, ring of 8, K-means 16) and 3 (512^2, 4x4 torus, DCT q50) at their
+    stated sizes: one lockstep iteration of every node after one free iteration."""
+    cfg = make()
+    inp = C.make_inputs(cfg, with_truth=False)
+    assert lockstep(cfg, inp, steps=1, warm=1) <= 1e-3
+
+
 def test_graph_rule_dual_sum_invariant_full_size():
     cfg = C.C4(1)
     inp = C.make_inputs(cfg, with_truth=False)

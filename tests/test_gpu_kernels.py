@@ -125,7 +125,8 @@ def kmeans_input(n, seed):
 
 @pytest.mark.parametrize("n,K,iters", [(5, 2, 10), (1000, 1, 3), (1000, 16, 10), (65536, 16, 10),
                                        (65537, 64, 10), (4099, 3, 0), (1 << 20, 64, 10),
-                                       (20000, 100, 5), (3000, 256, 4)])
+                                       (20000, 100, 5), (3000, 256, 4),
+                                       (2048 * 2048, 32, 10)])  # config 5 payload (a 2048^2 slice)
 def test_kmeans_parity(n, K, iters):
     v = kmeans_input(n, n + K)
     cen_r, lab_r = oracle.kmeans_encode(v, K, iters)
@@ -149,6 +150,11 @@ def test_kmeans_spec_example_and_edges():
     cr, lr = oracle.kmeans_encode(neg.cpu().numpy(), 7, 6)
     c, p, l = tomoq.kmeans_encode(neg, 7, 6)
     assert np.mean(l.cpu().numpy() == lr) >= 0.9999
+
+
+@pytest.mark.parametrize("rows,cols,q", [(2048, 2048, 75), (1024, 1024, 50)])  # configs 5 and 4 sizes
+def test_dct_bit_exact_full_size(rows, cols, q):
+    test_dct_bit_exact(rows, cols, q)
 
 
 @pytest.mark.parametrize("rows,cols", [(8, 8), (64, 64), (16, 512), (512, 512), (256, 64)])
