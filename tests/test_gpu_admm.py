@@ -145,6 +145,33 @@ def test_graph_rule_dual_sum_invariant_full_size():
     assert np.linalg.norm(L.sum(axis=0)) <= 1e-5 * np.linalg.norm(L)
 
 
+def test_config5_full_size_two_slices():
+    """Config 5 at its stated size (2048^2, 1500 angles, 2897 bins, 8 nodes per slice on a
+    complete graph), two slices -- slice 0 K-means K=32, slice 1 DCT q75 (reading R-20) --
+    two ADMM iterations: finite iterates, the graph-rule dual invariant sum_i alpha_i = 0 per
+    slice, and a sampled forward projection of node 0's angles against the oracle."""
+    cfg = C.C5(slices=2)
+    inp = C.make_inputs(cfg, with_truth=False)
+    ctx = gpu_context(cfg, inp)
+    ctx.run(2)
+    n = cfg.N * cfg.N
+    for s in range(2):
+        asum, anorm = np.zeros(n), 0.0
+        for m in range(cfg.nodes):
+            st = ctx.export_state(s, m)
+            assert np.all(np.isfinite(st))
+            asum += st[1]
+            anorm = max(anorm, float(np.linalg.norm(st[1])))
+        assert anorm > 0 and np.linalg.norm(asum) <= 1e-5 * anorm
+    x0 = ctx.image(0, 0)
+    sel = [0, 752]  # two of node 0's angles (round-robin: a = 0 mod 8)
+    ref = oracle.project(x0.astype(np.float64), cfg.n_angles, cfg.n_det, sel)
+    import torch
+    got = tomoq.project(torch.tensor(x0, device="cuda:0"), cfg.n_angles, cfg.n_det, sel)
+    assert rel(got.cpu().numpy(), ref) <= 1e-5
+    ctx.close()
+
+
 def test_deterministic_bitwise():
     cfg = c2s()
     cfg.iters = 5
