@@ -3,7 +3,7 @@
 # Usage: bash tools/gpu_profile.sh TAG regex1 [regex2 ...]
 mkdir -p gpurun_out
 TAG=$1; shift
-CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"
+CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-c5-geometry"
 timeout 600 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -c 3000 --csv \
     --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1
