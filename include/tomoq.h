@@ -139,7 +139,8 @@ tq_status tq_export_labels(tq_ctx *ctx, int32_t slice, int32_t node, int32_t *bu
  * S = A P, 1 backprojector with the CG epilogue Q = A^T S + c P, 2 forward residual
  * S = D - A X, 3 the K-means encode of the quantized slices, 4 the DCT encode,
  * 5 the consensus/dual kernel without the dual update (b' only).  Overwrites only
- * scratch (S, Q, payloads, b' is recomputed identically); x and alpha are unchanged.
+ * scratch (S, Q, payloads and the decoded public values of local K-means payloads,
+ * b' is recomputed identically); x and alpha are unchanged.
  * Returns TQ_EINVAL for a component the context does not have.  *units = algorithmic
  * work per launch (voxel-updates for 0-2, elements for 3-5). */
 tq_status tq_launch_component(tq_ctx *ctx, int32_t component, int32_t reps, void *stream,

@@ -38,8 +38,10 @@ struct KmeansWork {
 };
 
 // vin[b]: nv floats; pay[b]: payload bytes; labels: table of int32[nv] or null table
+// dec_out (optional): per payload, the decoded values c[label] written by the final pass
+// (elements of float for prec 0, double for prec 1) -- the decode of a local payload fused
 int kmeans_encode(const float *const *vin, KmeansWork &ws, int lloyd, uint8_t *const *pay,
-                  int32_t *const *labels, cudaStream_t st);
+                  int32_t *const *labels, cudaStream_t st, void *const *dec_out = nullptr, int prec = 0);
 // out[b]: nv elements of float (prec 0) or double (prec 1)
 int kmeans_decode(const uint8_t *const *pay, int P, long long nv, int K, int prec,
                   void *const *out, cudaStream_t st);

@@ -364,7 +364,7 @@ long long Ctx::launch_component(int component, int reps, cudaStream_t s) {
             TQ_REQUIRE(E.P > 0, "no local payloads of that quantizer kind");
             for (int r = 0; r < reps; r++) {
                 if (E.need_conv) launch_to_float(prec, E.conv_src_d, E.conv_dst_d, n, (int)E.conv_src.size(), s);
-                if (kd == TQ_Q_KMEANS) kmeans_encode(E.vin, kmw, q.lloyd_iters, E.pay, E.labels, s);
+                if (kd == TQ_Q_KMEANS) kmeans_encode(E.vin, kmw, q.lloyd_iters, E.pay, E.labels, s, E.dec_out, prec);
                 else dct_encode(E.vin, E.P, rule == TQ_RULE_PAPER ? N / M : N, N, q.quality, dctw, E.pay, s);
             }
             return (long long)E.P * payload_len;
@@ -458,13 +458,17 @@ void Ctx::setup_exchange() {
         std::vector<int32_t *> lab;
         std::vector<const void *> csrc;
         std::vector<float *> cdst;
-        std::vector<void *> out;
+        std::vector<void *> out, eout;
         for (size_t k = 0; k < pays.size(); k++) {
             if (pays[k].kind != kd) continue;
-            pd.push_back(pays[k].buf);
-            out.push_back(outp[k]);
-            D.members.push_back((int)k);
+            // K-means payloads produced here are decoded by the encoder's final pass
+            if (!(kd == TQ_Q_KMEANS && pays[k].local)) {
+                pd.push_back(pays[k].buf);
+                out.push_back(outp[k]);
+                D.members.push_back((int)k);
+            }
             if (!pays[k].local) continue;
+            eout.push_back(outp[k]);
             const int li = local(pays[k].slice, pays[k].node);
             E.members.push_back((int)k);
             pe.push_back(pays[k].buf);
@@ -484,6 +488,7 @@ void Ctx::setup_exchange() {
             E.vin = (const float **)upload(vin.data(), sizeof(void *) * E.P);
             E.pay = (uint8_t **)upload(pe.data(), sizeof(void *) * E.P);
             if (kd == TQ_Q_KMEANS && nlab) E.labels = (int32_t **)upload(lab.data(), sizeof(void *) * E.P);
+            if (kd == TQ_Q_KMEANS) E.dec_out = (void **)upload(eout.data(), sizeof(void *) * E.P);
             if (!csrc.empty()) {
                 E.need_conv = true;
                 E.conv_src.assign(csrc.begin(), csrc.end());
@@ -571,7 +576,7 @@ int Ctx::phase_a(cudaStream_t s) {
         Batch &E = enc[kd];
         if (!E.P) continue;
         if (E.need_conv) k += launch_to_float(prec, E.conv_src_d, E.conv_dst_d, n, (int)E.conv_src.size(), s);
-        if (kd == TQ_Q_KMEANS) k += kmeans_encode(E.vin, kmw, q.lloyd_iters, E.pay, E.labels, s);
+        if (kd == TQ_Q_KMEANS) k += kmeans_encode(E.vin, kmw, q.lloyd_iters, E.pay, E.labels, s, E.dec_out, prec);
         else {
             const int rows = rule == TQ_RULE_PAPER ? N / M : N;
             k += dct_encode(E.vin, E.P, rows, N, q.quality, dctw, E.pay, s);

@@ -71,6 +71,7 @@ struct Ctx {
         uint8_t **pay = nullptr;
         int32_t **labels = nullptr;
         void **out = nullptr;
+        void **dec_out = nullptr;             // K-means: fused decode outputs of the local payloads
         std::vector<int> members;             // pays index
         std::vector<const void *> conv_src;   // to_float sources
         const void **conv_src_d = nullptr;

@@ -386,9 +386,9 @@ __global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters) {
 // final assignment: label(v) = #{k : v > thr[k]} by a branchless search over the
 // thresholds padded with +inf to 2^B - 1 entries; lane `bit` stores bit-plane `bit`
 // of its warp's 32-element group.  U groups per warp per step (loads in flight).
-template <int B>
+template <int B, typename TO>
 __global__ void __launch_bounds__(KT) km_final(const float *const *vin, KmPtr w, uint8_t *const *pay,
-                                               int32_t *const *labels_tab) {
+                                               int32_t *const *labels_tab, TO *const *dec_out) {
     __shared__ float thr_s[256];
     const int b = blockIdx.y;
     const int K = w.K;
@@ -396,8 +396,12 @@ __global__ void __launch_bounds__(KT) km_final(const float *const *vin, KmPtr w,
     float *cen_out = reinterpret_cast<float *>(pay[b]);
     uint32_t *planes = reinterpret_cast<uint32_t *>(pay[b] + 4 * (long long)K);
     int32_t *labels = labels_tab ? labels_tab[b] : nullptr;
-    if (blockIdx.x == 0)
-        for (int k = threadIdx.x; k < K; k += KT) cen_out[k] = w.cen[(long long)b * K + k];
+    TO *dec = dec_out ? dec_out[b] : nullptr;  // fused decode of this (local) payload
+    __shared__ float cen_s[256];
+    for (int k = threadIdx.x; k < K; k += KT) {
+        cen_s[k] = w.cen[(long long)b * K + k];
+        if (blockIdx.x == 0) cen_out[k] = cen_s[k];
+    }
     __syncthreads();
     const float *vb = vin[b];
     const long long nv = w.nv;
@@ -420,6 +424,7 @@ __global__ void __launch_bounds__(KT) km_final(const float *const *vin, KmPtr w,
             for (int step = (1 << B) >> 1; step > 0; step >>= 1) l += (v[u] > thr_s[l + step - 1]) ? step : 0;
             const long long i = (g0 + u) * 32 + lane;
             if (labels && i < nv) labels[i] = l;
+            if (dec && i < nv) dec[i] = (TO)cen_s[l];
             uint32_t mine = 0;
 #pragma unroll
             for (int bit = 0; bit < B; bit++) {
@@ -514,7 +519,7 @@ void KmeansWork::release() {
 }
 
 int kmeans_encode(const float *const *v, KmeansWork &ws, int lloyd, uint8_t *const *pay,
-                  int32_t *const *labels, cudaStream_t st) {
+                  int32_t *const *labels, cudaStream_t st, void *const *dec_out, int prec) {
     const KmPtr w = ptrs(ws);
     const int P = ws.P;
     if (P == 0) return 0;
@@ -535,7 +540,11 @@ int kmeans_encode(const float *const *v, KmeansWork &ws, int lloyd, uint8_t *con
     long long want = std::max(1LL, (148LL * 8 + P - 1) / P);
     long long need = (ws.nv + KT * 16 - 1) / (KT * 16);
     const dim3 grid((unsigned)std::max(1LL, std::min(want, need)), P);
-    with_bits(ws.B, [&](auto Bc) { km_final<decltype(Bc)::value><<<grid, KT, 0, st>>>(v, w, pay, labels); });
+    with_bits(ws.B, [&](auto Bc) {
+        constexpr int BB = decltype(Bc)::value;
+        if (prec == 1) km_final<BB, double><<<grid, KT, 0, st>>>(v, w, pay, labels, (double *const *)dec_out);
+        else km_final<BB, float><<<grid, KT, 0, st>>>(v, w, pay, labels, (float *const *)dec_out);
+    });
     TQ_CHECK_CUDA(cudaGetLastError());
     return k + 3;
 }
