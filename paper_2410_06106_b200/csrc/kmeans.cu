@@ -250,8 +250,10 @@ __device__ __forceinline__ int fixed_exp(const uint32_t *sorted, long long nv) {
     return 62 - E - lg;
 }
 
-// per-chunk (64 keys) sums of fix(v) over the sorted keys
+// chunk (128 keys) sums of fix(v) over the sorted keys: csum[chunk] = exclusive prefix of
+// the chunk sums within its tile, cpre[tile] = the tile's total
 __global__ void __launch_bounds__(KT) km_csum(KmPtr w) {
+    __shared__ long long ch[CPT];
     const int b = blockIdx.y, t = blockIdx.x;
     const uint32_t *sorted = w.keysA + (long long)b * w.T * KTILE;
     const int F = fixed_exp(sorted, w.nv);
@@ -265,53 +267,58 @@ __global__ void __launch_bounds__(KT) km_csum(KmPtr w) {
         if (i0 + r < w.nv) s += __double2ll_rn((double)key2f(k[r]) * scale);
 #pragma unroll
     for (int o = 1; o < KCH / KI; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);  // KCH/KI lanes per chunk
-    if ((threadIdx.x & (KCH / KI - 1)) == 0) w.csum[(long long)b * w.T * CPT + (long long)t * CPT + threadIdx.x / (KCH / KI)] = s;
+    if ((threadIdx.x & (KCH / KI - 1)) == 0) ch[threadIdx.x / (KCH / KI)] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const long long x = ch[threadIdx.x];
+        long long inc = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (threadIdx.x >= o) inc += y;
+        }
+        w.csum[(long long)b * w.T * CPT + (long long)t * CPT + threadIdx.x] = inc - x;
+        if (threadIdx.x == 31) w.cpre[(long long)b * w.T + t] = inc;
+    }
     if (t == 0 && threadIdx.x == 0) w.fexp[b] = F;
 }
 
-// one CTA per payload: quantile init, then `iters` exact Lloyd steps on the sorted keys
 __global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters) {
     using Scan = cub::BlockScan<long long, LT>;
     __shared__ typename Scan::TempStorage tmp;
     extern __shared__ __align__(16) unsigned char lsm[];
-    uint32_t *thead = reinterpret_cast<uint32_t *>(lsm);  // [T] first key of each tile
+    long long *tpre = reinterpret_cast<long long *>(lsm);           // [T + 1] tile prefix of fix sums
+    uint32_t *thead = reinterpret_cast<uint32_t *>(tpre + w.T + 1);  // [T] first key of each tile
     __shared__ float cen[256], thr[256];
     __shared__ long long Cs[256], Ss[256], total_s;
     const int b = blockIdx.x, K = w.K, T = w.T;
     const long long nv = w.nv, nch = (long long)T * CPT;
     const uint32_t *sorted = w.keysA + (long long)b * T * KTILE;
-    const long long *cs = w.csum + (long long)b * nch;
-    long long *cp = w.cpre + (long long)b * nch;
+    const long long *cp = w.csum + (long long)b * nch;  // in-tile exclusive chunk prefix
+    const long long *ts = w.cpre + (long long)b * T;    // tile totals
     const double scale = ldexp(1.0, w.fexp[b]);
-    // exclusive prefix of the chunk sums (global): each thread scans a run of consecutive
-    // chunks, one block scan joins the runs
-    const long long per = (nch + LT - 1) / LT;
-    const long long c_lo = min(nch, threadIdx.x * per), c_hi = min(nch, c_lo + per);
-    long long run = 0;
-    for (long long c = c_lo; c < c_hi; c += 8) {  // 8 independent loads in flight
-        long long x[8];
+    {  // exclusive prefix over the (<= 4096) tile totals: 4 per thread
+        long long x[4], run = 0;
 #pragma unroll
-        for (int u = 0; u < 8; u++) x[u] = c + u < c_hi ? __ldcg(cs + c + u) : 0;
+        for (int u = 0; u < 4; u++) {
+            const int t = 4 * threadIdx.x + u;
+            x[u] = t < T ? ts[t] : 0;
+            run += x[u];
+        }
+        long long ex, carry;
+        Scan(tmp).ExclusiveSum(run, ex, carry);
 #pragma unroll
-        for (int u = 0; u < 8; u++) run += x[u];
-    }
-    long long ex, carry;
-    Scan(tmp).ExclusiveSum(run, ex, carry);
-    for (long long c = c_lo; c < c_hi; c += 8) {
-        long long x[8];
-#pragma unroll
-        for (int u = 0; u < 8; u++) x[u] = c + u < c_hi ? __ldcg(cs + c + u) : 0;
-#pragma unroll
-        for (int u = 0; u < 8; u++) {
-            if (c + u < c_hi) cp[c + u] = ex;
+        for (int u = 0; u < 4; u++) {
+            const int t = 4 * threadIdx.x + u;
+            if (t < T) tpre[t] = ex;
             ex += x[u];
         }
+        if (threadIdx.x == 0) total_s = carry;
     }
     for (int t = threadIdx.x; t < T; t += LT) thead[t] = sorted[(long long)t * KTILE];
-    if (threadIdx.x == 0) total_s = carry;
     // quantile init: c_k = v_(floor((2k+1) nv / 2K))
     for (int k = threadIdx.x; k < K; k += LT) cen[k] = key2f(sorted[((long long)(2 * k + 1) * nv) / (2LL * K)]);
-    __syncthreads();  // also orders the cpre stores before the loads below (same CTA)
+    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int it = 0; it < iters; it++) {
         for (int k = threadIdx.x; k + 1 < K; k += LT) thr[k] = (float)(((double)cen[k] + (double)cen[k + 1]) * 0.5);
@@ -342,7 +349,7 @@ __global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters) {
                 const long long cb = (long long)max(tt[q], 0) * KTILE + (long long)cc[q] * KCH;
 #pragma unroll
                 for (int u = 0; u < KCH / 32; u++) e[q][u] = tt[q] >= 0 ? sorted[cb + 32 * u + lane] : 0xffffffffu;
-                pre[q] = tt[q] >= 0 ? cp[(long long)tt[q] * CPT + cc[q]] : 0;
+                pre[q] = tt[q] >= 0 ? tpre[tt[q]] + cp[(long long)tt[q] * CPT + cc[q]] : 0;
             }
 #pragma unroll
             for (int q = 0; q < 2; q++) {
@@ -479,7 +486,7 @@ void with_bits(int B, F &&f) {
     }
 }
 
-size_t lloyd_smem(int T) { return sizeof(uint32_t) * T; }
+size_t lloyd_smem(int T) { return sizeof(long long) * (T + 1) + sizeof(uint32_t) * T; }
 
 }  // namespace
 
