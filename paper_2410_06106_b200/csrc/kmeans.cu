@@ -45,16 +45,6 @@ __device__ __forceinline__ float key2f(uint32_t k) {
     return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
-// label(v) = #{k < K-1 : v > thr[k]} for non-decreasing thr (ties go to the lower cluster)
-__device__ __forceinline__ int kmeans_label(float v, const float *thr, int K) {
-    int lo = 0, hi = K - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (v > thr[mid]) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-
 struct KmPtr {
     uint32_t *keysA, *keysB, *hist, *dtot;
     long long *csum, *cpre;

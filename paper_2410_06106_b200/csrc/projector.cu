@@ -21,8 +21,6 @@ constexpr int BP_MAXA = 32;     // angles per staged batch
 template <typename T>
 __device__ __forceinline__ T floor_split(T x, int &i);
 template <>
-__device__ __forceinline__ float floor_split<float>(float x, int &i) { return floor_pos(x, i); }
-template <>
 __device__ __forceinline__ double floor_split<double>(double x, int &i) {
     const double f = floor(x);
     i = (int)f;
@@ -31,8 +29,6 @@ __device__ __forceinline__ double floor_split<double>(double x, int &i) {
 
 template <typename T>
 __device__ __forceinline__ T sat(T x);
-template <>
-__device__ __forceinline__ float sat<float>(float x) { return __saturatef(x); }
 template <>
 __device__ __forceinline__ double sat<double>(double x) { return fmin(fmax(x, 0.0), 1.0); }
 
@@ -63,8 +59,7 @@ __device__ __forceinline__ float lds(uint32_t addr) {
     asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(OFF));
     return v;
 }
-constexpr uint32_t MAGIC_BITS4 = 0x4B000000u << 2;  // wraps mod 2^32 (intended)
-// shared base minus MAGIC_BITS4.  `magic` is MAGIC_BITS4 passed as a kernel argument,
+// shared base minus the magic bits (0x4B000000 << log2(entry bytes), mod 2^32), passed as a kernel argument,
 // so ptxas cannot split the constant back out of the base register and re-add it
 // before every load (it does that when it can see the constant).
 __device__ __forceinline__ uint32_t magic_base(const void *smem_ptr, uint32_t magic) {
@@ -395,12 +390,6 @@ __global__ void __launch_bounds__(FP_THREADS, 4) fp_tile_f32(const FpArgs<float>
 // unit's window records into a second table buffer, so the global-memory latency of
 // staging is hidden behind the previous unit's ray walks.
 constexpr int FPP_RAW = FP_TH * FP_TW;  // raw floats per unit (both orientations)
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, bool valid) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 struct FpUnit {
     int O, node, tile, a_begin, a_end;
