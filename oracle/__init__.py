@@ -208,17 +208,19 @@ def comm_model(M: int, X: float) -> float:
 # ----------------------------------------------------------------- ADMM
 class OracleADMM:
     """The ADMM outer loop (Alg. 4 PAPER.md:207-229 / DESIGN.md R-7) on one slice.
+    rule 0 graph (R-7), 1 paper (eq:solve_u..eq:solve_lamda), 2 consensus (P:121-131,
+    segment-sharded with Q per segment).
 
     State: X (private x_i / u_m), L (alpha_i / lambda_m), XH (graph: xhat_i per node;
-    paper: the consensus x in XH[0])."""
+    paper / consensus: x in XH[0])."""
 
     def __init__(self, N, n_det, n_ang, M, edges, sino_full, split_contig, rule=0, inner=1,
                  e1=5, rho=1.0, eta1=None, e2=10, eta2=0.2, qkind=0, K=16, lloyd=10,
                  quality=50, threads=1):
         self.N, self.n_det, self.n_ang, self.M = N, n_det, n_ang, M
         if qkind == 2:  # the DCT codec works on whole 8x8 blocks (DESIGN.md R-18)
-            rows = N // M if rule == 1 else N
-            if N % 8 or rows % 8 or (rule == 1 and N % M):
+            rows = N // M if rule in (1, 2) else N
+            if N % 8 or rows % 8 or (rule in (1, 2) and N % M):
                 raise ValueError("DCT quantizer needs 8 | N and 8 | segment rows")
         self.off, self.idx = partition_angles(n_ang, M, split_contig)
         sino_full = np.asarray(sino_full, np.float64).reshape(n_ang, n_det)
@@ -235,7 +237,7 @@ class OracleADMM:
         n = N * N
         self.X = np.zeros((M, n))
         self.L = np.zeros((M, n))
-        self.XH = np.zeros((M if rule == 0 else 1, n))
+        self.XH = np.zeros((M if rule == 0 else 1, n))  # rule 1 (paper) and 2 (consensus): x
         self.iters = 0
         self.bytes_per_iter = 0
 

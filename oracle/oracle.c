@@ -461,6 +461,12 @@ static long quantize(int kind, int K, int iters, int quality, const double *x, i
  *            started from the current x[m]
  *   x     <- conc(Q(x[1]), ..., Q(x[M]))
  *   lambda_m <- lambda_m + rho (u_m - x)
+ * rule 2 "consensus" (the standard consensus ADMM of P:121-131, eq-compact:solve_u /
+ *   eq-compact:solve_x / eq-compact:solve_lambda, with x sharded in the paper's segments
+ *   and Q applied to each segment as in P:268):  state X = u_m, L = lambda_m,
+ *   XG = x.  u_m <- inner solve with c = rho, b' = rho x - lambda_m (as rule 1);
+ *   x[m] <- (1/M) sum_n (u_n + lambda_n/rho)[m]  (the argmin of eq-compact:solve_x);
+ *   x <- conc(Q(x[1]), ..., Q(x[M]));  lambda_m <- lambda_m + rho (u_m - x).
  * rule 0 "graph" (decentralized consensus ADMM over the graph, R-7):
  *   state X = x_i (private), L = alpha_i, XH = xhat_i = Q(x_i) (public).
  *   b'_i = -alpha_i + rho (deg_i xhat_i + S_i), c_i = 2 rho deg_i, S_i = sum_{j in N(i)} xhat_j
@@ -582,8 +588,13 @@ long or_admm_run(int N, int n_det, int n_ang, int M, const int32_t *off, const i
                 size_t lo = (size_t)roff[m] * N, hi = (size_t)roff[m + 1] * N;
                 double *seg = malloc((hi - lo) * sizeof(double));
                 for (size_t p = lo; p < hi; p++) {
-                    seg[p - lo] = or_alg3(XH[p], X[(size_t)m * n + p], L[(size_t)m * n + p],
-                                          rho, eta2, e2);
+                    if (rule == 1) {
+                        seg[p - lo] = or_alg3(XH[p], X[(size_t)m * n + p], L[(size_t)m * n + p], rho, eta2, e2);
+                    } else {  /* consensus: the mean over all nodes, summed in node order */
+                        double acc = 0.0;
+                        for (int q = 0; q < M; q++) acc += X[(size_t)q * n + p] + L[(size_t)q * n + p] / rho;
+                        seg[p - lo] = acc / (double)M;
+                    }
                 }
                 long b = quantize(qkind, K, lloyd, quality, seg, roff[m + 1] - roff[m], N, XN + lo, NULL);
                 bytes += b * (M - 1);

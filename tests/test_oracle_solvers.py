@@ -165,9 +165,54 @@ def test_paper_rule_steps_match_dense_and_own_segment_dual_vanishes():
         assert np.max(np.abs(seg)) <= 1e-12 * max(1.0, np.max(np.abs(o2.L)))
 
 
+def dense_consensus_rule(A_blocks, d_blocks, M, N, rho, iters):
+    """The standard consensus ADMM of PAPER.md:121-131 (eq-compact:solve_u / solve_x /
+    solve_lambda): u exact by a dense solve, x = mean over nodes of u + lambda/rho."""
+    n = N * N
+    u = np.zeros((M, n)); lam = np.zeros((M, n)); x = np.zeros(n)
+    for _ in range(iters):
+        for m in range(M):
+            Am = A_blocks[m]
+            u[m] = np.linalg.solve(Am.T @ Am + rho * np.eye(n), Am.T @ d_blocks[m] + rho * x - lam[m])
+        x = (u + lam / rho).mean(axis=0)
+        lam += rho * (u - x[None, :])
+    return u, lam, x
+
+
+def test_consensus_rule_steps_match_dense():
+    """rule 2 (sharded consensus) step by step against the dense
+    transcription of eq-compact:solve_u / solve_x / solve_lambda; Q = identity, so the
+    sharding into segments does not change x."""
+    N, n_ang, n_det, M = 16, 24, 23, 4
+    d = small_problem(N, n_ang, n_det)
+    off, idx = oracle.partition_angles(n_ang, M, False)
+    Ab = [dense_joseph(N, n_ang, n_det, idx[off[m]:off[m + 1]]) for m in range(M)]
+    db = [d[idx[off[m]:off[m + 1]]].ravel() for m in range(M)]
+    rho = 0.5
+    u, lam, x = dense_consensus_rule(Ab, db, M, N, rho, 3)
+    o = oracle.OracleADMM(N, n_det, n_ang, M, [], d, False, rule=2, inner=1, e1=600, rho=rho)
+    o.run(3)
+    assert rel(o.X, u) <= 1e-9 and rel(o.XH[0], x) <= 1e-9 and rel(o.L, lam) <= 1e-9
+
+
+def test_consensus_rule_converges_to_dense_least_squares(ls16):
+    """Standard consensus ADMM (PAPER.md:121-131) converges to the centralized LS solution;
+    with Q = identity sum_m lambda_m = 0 after every iteration (x is their mean)."""
+    N, n_ang, n_det, d, A, x_ls = ls16
+    o = oracle.OracleADMM(N, n_det, n_ang, 4, [], d, False, rule=2, inner=1, e1=20, rho=0.3, threads=4)
+    o.run(4000)
+    assert rel(o.image(), x_ls) <= 1e-5
+    assert np.linalg.norm(o.L.sum(axis=0)) <= 1e-12 * max(1.0, np.linalg.norm(o.L))
+    # M = 1: lambda stays 0 and x = u (a proximal point method, fixed point = LS)
+    o1 = oracle.OracleADMM(N, n_det, n_ang, 1, [], d, False, rule=2, inner=1, e1=20, rho=0.1)
+    o1.run(300)
+    assert np.max(np.abs(o1.L)) == 0.0 and np.array_equal(o1.X[0], o1.XH[0])
+    assert rel(o1.image(), x_ls) <= 1e-8
+
+
 def test_admm_zero_data_stays_zero():
     N, n_ang, n_det = 16, 12, 23
-    for rule in (0, 1):
+    for rule in (0, 1, 2):
         for q in (0, 1, 2):
             o = oracle.OracleADMM(N, n_det, n_ang, 2, synth.ring(2), np.zeros((n_ang, n_det)), True,
                                   rule=rule, inner=1, e1=3, rho=1.0, qkind=q, K=4)
