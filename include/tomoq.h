@@ -49,14 +49,17 @@ typedef struct {
 } tq_geometry;
 
 enum { TQ_SPLIT_ROUND_ROBIN = 0, TQ_SPLIT_CONTIGUOUS = 1 };
-enum { TQ_RULE_GRAPH = 0, TQ_RULE_PAPER = 1 };
+enum { TQ_RULE_GRAPH = 0, TQ_RULE_PAPER = 1, TQ_RULE_CONSENSUS = 2 };
 enum { TQ_INNER_GD = 0, TQ_INNER_CG = 1 };
 enum { TQ_Q_NONE = 0, TQ_Q_KMEANS = 1, TQ_Q_DCT = 2, TQ_Q_ALTERNATE = 3 };
 
 /* The communication graph of ONE slice (every slice uses the same graph).
  * rule TQ_RULE_GRAPH: decentralized consensus ADMM over the edges (R-7, default).
  * rule TQ_RULE_PAPER: the segment-owner dADMM of P:158-166 (edges unused; every
- * node needs every segment -- an all-gather). */
+ * node needs every segment -- an all-gather).
+ * rule TQ_RULE_CONSENSUS: the standard consensus ADMM of P:121-131 with x sharded in
+ * the same segments: x[m] = mean over all nodes of (u + lambda/rho)[m] (an all-reduce
+ * of per-rank partial sums across ranks), Q per segment, all-gather. */
 typedef struct {
     int32_t n_nodes;          /* M ADMM nodes per slice, 1 <= M <= n_angles */
     int32_t n_edges;

@@ -12,7 +12,7 @@ import numpy as np
 
 from . import synth
 
-RULE_GRAPH, RULE_PAPER = 0, 1
+RULE_GRAPH, RULE_PAPER, RULE_CONSENSUS = 0, 1, 2
 INNER_GD, INNER_CG = 0, 1
 SPLIT_RR, SPLIT_CONTIG = 0, 1
 Q_NONE, Q_KMEANS, Q_DCT, Q_ALT = 0, 1, 2, 3

@@ -151,7 +151,7 @@ tq_status tq_import_state(tq_ctx *ctx, int32_t slice, int32_t node, const double
     if (!ctx) return TQ_EINVAL;
     return guard(ctx, [&] {
         TQ_REQUIRE(buf != nullptr, "null buffer");
-        TQ_REQUIRE(ctx->c.world == 1 || ctx->c.rule == TQ_RULE_PAPER,
+        TQ_REQUIRE(ctx->c.world == 1 || ctx->c.rule != TQ_RULE_GRAPH,
                    "import_state with the graph rule needs world == 1 (neighbour values)");
         ctx->c.import_state(slice, node, buf, len);
     });

@@ -108,6 +108,38 @@ __global__ void __launch_bounds__(CT) paper_dual(const T *u, T *lam, T *bprime, 
 }
 
 template <typename T>
+__global__ void __launch_bounds__(CT) consensus_partial(const T *u, const T *lam, double *csum, const int *slice_of,
+                                                        const int *first, const int *cnt, long long n, double rho) {
+    const int js = blockIdx.y;
+    const int i0 = first[js], c = cnt[js];
+    double *out = csum + (long long)slice_of[js] * n;
+    for (long long p = (long long)blockIdx.x * CT + threadIdx.x; p < n; p += (long long)gridDim.x * CT) {
+        double acc = 0.0;
+        for (int q = 0; q < c; q++) {
+            const long long g = (long long)(i0 + q) * n + p;
+            acc += (double)u[g] + (double)lam[g] / rho;
+        }
+        out[p] = acc;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(CT) consensus_segment(const double *csum, const int *node_slice, T *const *xg,
+                                                        const long long *lo, const long long *lens,
+                                                        float *const *seg, long long n, int M) {
+    const int i = blockIdx.y;
+    const long long base = lo[i], len = lens[i];
+    const double *cs = csum + (long long)node_slice[i] * n;
+    T *x = xg[i];
+    float *out = seg ? seg[i] : nullptr;
+    for (long long q = (long long)blockIdx.x * CT + threadIdx.x; q < len; q += (long long)gridDim.x * CT) {
+        const double v = cs[base + q] / (double)M;
+        if (out) out[q] = (float)v;
+        else x[base + q] = (T)v;
+    }
+}
+
+template <typename T>
 __global__ void __launch_bounds__(CT) to_float(const T *const *src, float *const *dst, long long n) {
     const int i = blockIdx.y;
     const T *s = src[i];
@@ -161,6 +193,34 @@ int launch_paper_dual(int prec, const void *u, void *lam, void *bprime, const vo
         paper_dual<double><<<grid_of(n, L), CT, 0, st>>>((const double *)u, (double *)lam,
                                                          (double *)bprime, (const double *const *)xg_tab,
                                                          n, rho, update_lam);
+    TQ_CHECK_CUDA(cudaGetLastError());
+    return 1;
+}
+
+int launch_consensus_partial(int prec, const void *u, const void *lam, double *csum, const int *slice_of,
+                             const int *first, const int *cnt, int n_local_slices, long long n, double rho,
+                             cudaStream_t st) {
+    if (n_local_slices == 0) return 0;
+    if (prec == 0)
+        consensus_partial<float><<<grid_of(n, n_local_slices), CT, 0, st>>>((const float *)u, (const float *)lam, csum,
+                                                                            slice_of, first, cnt, n, rho);
+    else
+        consensus_partial<double><<<grid_of(n, n_local_slices), CT, 0, st>>>((const double *)u, (const double *)lam,
+                                                                             csum, slice_of, first, cnt, n, rho);
+    TQ_CHECK_CUDA(cudaGetLastError());
+    return 1;
+}
+
+int launch_consensus_segment(int prec, const double *csum, const int *node_slice, void *const *xg_tab,
+                             const long long *lo, const long long *len, long long max_len, float *const *seg_tab,
+                             long long n, int L, int M, cudaStream_t st) {
+    if (L == 0) return 0;
+    if (prec == 0)
+        consensus_segment<float><<<grid_of(max_len, L), CT, 0, st>>>(csum, node_slice, (float *const *)xg_tab, lo,
+                                                                     len, seg_tab, n, M);
+    else
+        consensus_segment<double><<<grid_of(max_len, L), CT, 0, st>>>(csum, node_slice, (double *const *)xg_tab, lo,
+                                                                      len, seg_tab, n, M);
     TQ_CHECK_CUDA(cudaGetLastError());
     return 1;
 }

@@ -32,6 +32,7 @@ NcclApi &nccl() {
             api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
             api.Send = (decltype(api.Send))sym("ncclSend");
             api.Recv = (decltype(api.Recv))sym("ncclRecv");
+            api.Reduce = (decltype(api.Reduce))sym("ncclReduce");
             api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
             api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
             api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
@@ -51,8 +52,8 @@ NcclApi &nccl() {
 
 // ---------------------------------------------------------------- exchange plan
 // graph rule: a node's payload goes to every rank owning one of its neighbours
-// (deduplicated per (node, peer)); paper rule: every node's segment payload goes
-// to every other rank that owns nodes (the all-gather of P:188).  Sorted by
+// (deduplicated per (node, peer)); paper / consensus rule: every node's segment
+// payload goes to every other rank that owns nodes (the all-gather of P:188).  Sorted by
 // (peer, node) so both ends of every pair post matching send/recv sequences.
 void exchange_plan(int M, const std::vector<int> &edges, const std::vector<int> &node_rank, int rule,
                    int rank, int world, std::vector<std::pair<int, int>> &sends,
@@ -138,7 +139,7 @@ void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int ran
     TQ_REQUIRE(world_ >= 1 && rank_ >= 0 && rank_ < world_, "bad rank/world");
     M = gr.n_nodes;
     TQ_REQUIRE(M >= 1 && M <= n_ang, "n_nodes must be in [1, n_angles]");
-    TQ_REQUIRE(gr.rule == TQ_RULE_GRAPH || gr.rule == TQ_RULE_PAPER, "bad rule");
+    TQ_REQUIRE(gr.rule == TQ_RULE_GRAPH || gr.rule == TQ_RULE_PAPER || gr.rule == TQ_RULE_CONSENSUS, "bad rule");
     TQ_REQUIRE(gr.angle_split == TQ_SPLIT_ROUND_ROBIN || gr.angle_split == TQ_SPLIT_CONTIGUOUS, "bad split");
     TQ_REQUIRE(gr.n_edges >= 0 && (gr.n_edges == 0 || gr.edges), "edges missing");
     S = n_slices; rank = rank_; world = world_; prec = precision; device = device_;
@@ -192,9 +193,13 @@ void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int ran
     const size_t es = prec ? 8 : 4;
     TQ_CHECK_CUDA(cudaMalloc(&ALPHA, std::max<size_t>(16, es * n * L)));
     TQ_CHECK_CUDA(cudaMemset(ALPHA, 0, std::max<size_t>(16, es * n * L)));
-    if (rule == TQ_RULE_PAPER) {
+    if (segmented()) {
         TQ_CHECK_CUDA(cudaMalloc(&XG, es * n * S));
         TQ_CHECK_CUDA(cudaMemset(XG, 0, es * n * S));
+    }
+    if (rule == TQ_RULE_CONSENSUS) {  // every rank joins the segment reductions, even without nodes
+        TQ_CHECK_CUDA(cudaMalloc(&CSUM, sizeof(double) * n * S));
+        TQ_CHECK_CUDA(cudaMemset(CSUM, 0, sizeof(double) * n * S));
     }
     if (world > 1) {
         TQ_REQUIRE(nccl_id != nullptr, "world > 1 needs an NCCL unique id");
@@ -208,8 +213,8 @@ void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int ran
 }
 
 void Ctx::invalidate() {
-    if (gexecA) { cudaGraphExecDestroy(gexecA); gexecA = nullptr; }
-    if (gexecB) { cudaGraphExecDestroy(gexecB); gexecB = nullptr; }
+    for (auto &g : segs) cudaGraphExecDestroy(g.exec);
+    segs.clear();
 }
 
 void Ctx::free_exchange() {
@@ -226,6 +231,7 @@ void Ctx::free_exchange() {
     label_row.clear();
     fstage = nullptr; labels_buf = nullptr; xh_tab = nullptr; own_slot = nbr_off = nbr_slot = nullptr;
     xg_tab = nullptr; seg_lo = nullptr; seg_len = nullptr; seg_tab = nullptr;
+    cs_slice = cs_first = cs_cnt = node_slice = nullptr;
     xready = false;
 }
 
@@ -236,7 +242,9 @@ void Ctx::destroy() {
     geo.release();
     if (ALPHA) cudaFree(ALPHA);
     if (XG) cudaFree(XG);
+    if (CSUM) cudaFree(CSUM);
     ALPHA = XG = nullptr;
+    CSUM = nullptr;
     if (sino_stage) cudaFree(sino_stage);
     if (row_map) cudaFree(row_map);
     if (img_stage) cudaFree(img_stage);
@@ -282,9 +290,9 @@ void Ctx::set_quant(const tq_quant &qq) {
     const bool dc = qq.kind == TQ_Q_DCT || qq.kind == TQ_Q_ALTERNATE;
     if (km) TQ_REQUIRE(qq.k >= 1 && qq.k <= 256 && qq.lloyd_iters >= 0, "kmeans: k in [1,256], lloyd >= 0");
     if (dc) TQ_REQUIRE(qq.quality >= 1 && qq.quality <= 100, "dct: quality in [1,100]");
-    if (rule == TQ_RULE_PAPER && qq.kind != TQ_Q_NONE) {
-        TQ_REQUIRE(N % M == 0, "paper rule with a quantizer needs equal segments (M | N)");
-        if (dc) TQ_REQUIRE((N / M) % 8 == 0, "paper rule with DCT needs 8 | N/M");
+    if (segmented() && qq.kind != TQ_Q_NONE) {
+        TQ_REQUIRE(N % M == 0, "paper/consensus rule with a quantizer needs equal segments (M | N)");
+        if (dc) TQ_REQUIRE((N / M) % 8 == 0, "paper/consensus rule with DCT needs 8 | N/M");
     }
     free_exchange();
     q = qq;
@@ -365,7 +373,7 @@ long long Ctx::launch_component(int component, int reps, cudaStream_t s) {
             for (int r = 0; r < reps; r++) {
                 if (E.need_conv) launch_to_float(prec, E.conv_src_d, E.conv_dst_d, n, (int)E.conv_src.size(), s);
                 if (kd == TQ_Q_KMEANS) kmeans_encode(E.vin, kmw, q.lloyd_iters, E.pay, E.labels, s, E.dec_out, prec);
-                else dct_encode(E.vin, E.P, rule == TQ_RULE_PAPER ? N / M : N, N, q.quality, dctw, E.pay, s);
+                else dct_encode(E.vin, E.P, segmented() ? N / M : N, N, q.quality, dctw, E.pay, s);
             }
             return (long long)E.P * payload_len;
         }
@@ -377,7 +385,7 @@ long long Ctx::launch_component(int component, int reps, cudaStream_t s) {
 void Ctx::setup_exchange() {
     free_exchange();
     const size_t es = prec ? 8 : 4;
-    const bool paper = rule == TQ_RULE_PAPER;
+    const bool paper = segmented();  // segment payloads + all-gather (paper and consensus rules)
     payload_len = paper ? n / M : n;
     std::vector<std::pair<int, int>> sp, rp;
     exchange_plan(M, edges, node_rank, rule, rank, world, sp, rp);
@@ -533,6 +541,18 @@ void Ctx::setup_exchange() {
         seg_max = 0;
         for (int m = 0; m < M; m++) seg_max = std::max(seg_max, (long long)(row_off[m + 1] - row_off[m]) * N);
         seg_tab = (float **)upload(seg.data(), sizeof(void *) * std::max(1, L));
+        if (rule == TQ_RULE_CONSENSUS) {
+            // partial-sum tables over ALL slices (slices without local nodes write zeros, so
+            // the reduction never re-adds a stale sum); local nodes of a slice are contiguous
+            std::vector<int> sl(S), fi(S, 0), cn(S, 0), ns(L);
+            for (int t = 0; t < S; t++) sl[t] = t;
+            for (int i = L - 1; i >= 0; i--) { fi[loc[i].first] = i; cn[loc[i].first]++; }
+            for (int i = 0; i < L; i++) ns[i] = loc[i].first;
+            cs_slice = (int *)upload(sl.data(), sizeof(int) * S);
+            cs_first = (int *)upload(fi.data(), sizeof(int) * S);
+            cs_cnt = (int *)upload(cn.data(), sizeof(int) * S);
+            node_slice = (int *)upload(ns.data(), sizeof(int) * std::max(1, L));
+        }
     }
     // ---- NCCL transfers (per slice, same plan)
     for (int s : slices_here) {
@@ -558,6 +578,7 @@ void Ctx::setup_exchange() {
                              : kd == TQ_Q_KMEANS ? kmeans_payload_bytes(q.k, payload_len)
                                                  : dct_payload_bytes(payload_len);
         logical += pb * (paper ? (M - 1) : (long long)adj[m].size());
+        if (rule == TQ_RULE_CONSENSUS) logical += 8LL * (n - len);  // fp64 sums of the other segments
     }
     st.payload_bytes_logical = logical;
     st.nccl_bytes_sent = 0;
@@ -567,22 +588,46 @@ void Ctx::setup_exchange() {
     xready = true;
 }
 
-int Ctx::phase_a(cudaStream_t s) {
-    int k = prm.inner == TQ_INNER_CG ? in.cg(geo, prm.e1, s) : in.gd(geo, prm.e1, s);
-    if (rule == TQ_RULE_PAPER)
-        k += launch_paper_alg3(prec, in.X, ALPHA, xg_tab, seg_lo, seg_len, seg_max, seg_tab, n, L,
-                               prm.rho, prm.eta2, prm.e2, s);
+int Ctx::stage(int id, cudaStream_t s) {
+    if (id == 2) return phase_b(s);
+    int k = 0;
+    if (id == 0) {
+        k += prm.inner == TQ_INNER_CG ? in.cg(geo, prm.e1, s) : in.gd(geo, prm.e1, s);
+        if (rule == TQ_RULE_PAPER)
+            k += launch_paper_alg3(prec, in.X, ALPHA, xg_tab, seg_lo, seg_len, seg_max, seg_tab, n, L,
+                                   prm.rho, prm.eta2, prm.e2, s);
+        if (rule == TQ_RULE_CONSENSUS)
+            k += launch_consensus_partial(prec, in.X, ALPHA, CSUM, cs_slice, cs_first, cs_cnt, S, n, prm.rho, s);
+        return k;
+    }
+    if (rule == TQ_RULE_CONSENSUS)
+        k += launch_consensus_segment(prec, CSUM, node_slice, xg_tab, seg_lo, seg_len, seg_max, seg_tab, n, L, M, s);
     for (int kd = 1; kd <= 2; kd++) {
         Batch &E = enc[kd];
         if (!E.P) continue;
         if (E.need_conv) k += launch_to_float(prec, E.conv_src_d, E.conv_dst_d, n, (int)E.conv_src.size(), s);
         if (kd == TQ_Q_KMEANS) k += kmeans_encode(E.vin, kmw, q.lloyd_iters, E.pay, E.labels, s, E.dec_out, prec);
         else {
-            const int rows = rule == TQ_RULE_PAPER ? N / M : N;
+            const int rows = segmented() ? N / M : N;
             k += dct_encode(E.vin, E.P, rows, N, q.quality, dctw, E.pay, s);
         }
     }
     return k;
+}
+
+// consensus rule, world > 1: segment m of every slice's partial sum is summed onto the
+// rank owning node m (one grouped ncclReduce per (slice, segment) -- a reduce-scatter in
+// the paper's segment layout), which then forms x[m] locally.
+void Ctx::reduce_sums(cudaStream_t s) {
+    NcclApi &api = nccl();
+    TQ_CHECK_NCCL(api.GroupStart());
+    for (int t = 0; t < S; t++)
+        for (int m = 0; m < M; m++) {
+            double *p = CSUM + (long long)t * n + (long long)row_off[m] * N;
+            const size_t cnt = (size_t)(row_off[m + 1] - row_off[m]) * N;
+            TQ_CHECK_NCCL(api.Reduce(p, p, cnt, ncclFloat64, ncclSum, node_rank[m], comm, s));
+        }
+    TQ_CHECK_NCCL(api.GroupEnd());
 }
 
 void Ctx::exchange(cudaStream_t s) {
@@ -603,7 +648,7 @@ int Ctx::phase_b(cudaStream_t s) {
         if (!D.P) continue;
         if (kd == TQ_Q_KMEANS) k += kmeans_decode(D.pay, D.P, payload_len, q.k, prec, D.out, s);
         else {
-            const int rows = rule == TQ_RULE_PAPER ? N / M : N;
+            const int rows = segmented() ? N / M : N;
             k += dct_decode(D.pay, D.P, rows, N, q.quality, prec, D.out, s);
         }
     }
@@ -632,41 +677,44 @@ void Ctx::run(int iters, cudaStream_t user) {
         prepare_rhs(s);
         need_rhs = false;
     }
-    auto capture = [&](cudaGraphExec_t &ge, int &cnt, bool a_part, bool b_part) {
+    auto capture = [&](const std::vector<int> &ids, int comm_after) {
         cudaGraph_t g;
         TQ_CHECK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         int c = 0;
         try {
-            if (a_part) c += phase_a(s);
-            if (b_part) c += phase_b(s);
+            for (int id : ids) c += stage(id, s);
         } catch (...) {
             if (cudaStreamEndCapture(s, &g) == cudaSuccess && g) cudaGraphDestroy(g);
             (void)cudaGetLastError();  // do not leave the capture failure as the sticky last error
             throw;
         }
         TQ_CHECK_CUDA(cudaStreamEndCapture(s, &g));
-        TQ_CHECK_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        Seg sg{nullptr, c, comm_after};
+        const cudaError_t e = cudaGraphInstantiate(&sg.exec, g, 0);
         cudaGraphDestroy(g);
-        cnt = c;
+        TQ_CHECK_CUDA(e);
+        segs.push_back(sg);
     };
-    const bool split_phases = world > 1 && !(sends.empty() && recvs.empty());
-    if (!gexecA) {
-        if (split_phases) {
-            capture(gexecA, launchesA, true, false);
-            capture(gexecB, launchesB, false, true);
-        } else {
-            capture(gexecA, launchesA, true, true);
-            launchesB = 0;
-        }
+    if (segs.empty()) {
+        // stages 0 | reduce | 1 | exchange | 2, merged where no communication separates them
+        const bool red = rule == TQ_RULE_CONSENSUS && world > 1;
+        const bool exch = world > 1 && !(sends.empty() && recvs.empty());
+        std::vector<int> cur{0};
+        if (red) { capture(cur, COMM_REDUCE); cur.clear(); }
+        cur.push_back(1);
+        if (exch) { capture(cur, COMM_EXCHANGE); cur.clear(); }
+        cur.push_back(2);
+        capture(cur, COMM_NONE);
     }
+    int per_iter = 0;
+    for (auto &g : segs) per_iter += g.launches;
     TQ_CHECK_CUDA(cudaEventRecord(ev0, s));
-    for (int it = 0; it < iters; it++) {
-        TQ_CHECK_CUDA(cudaGraphLaunch(gexecA, s));
-        if (split_phases) {
-            exchange(s);
-            TQ_CHECK_CUDA(cudaGraphLaunch(gexecB, s));
+    for (int it = 0; it < iters; it++)
+        for (auto &g : segs) {
+            TQ_CHECK_CUDA(cudaGraphLaunch(g.exec, s));
+            if (g.comm == COMM_REDUCE) reduce_sums(s);
+            else if (g.comm == COMM_EXCHANGE) exchange(s);
         }
-    }
     TQ_CHECK_CUDA(cudaEventRecord(ev1, s));
     in.norm2(s);
     std::vector<double> sc((size_t)S_NSLOT * std::max(1, L));
@@ -676,7 +724,7 @@ void Ctx::run(int iters, cudaStream_t user) {
     TQ_CHECK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
     st.ms_last_run = ms;
     st.iters += iters;
-    st.kernel_launches = (long long)iters * (launchesA + launchesB);
+    st.kernel_launches = (long long)iters * per_iter;
     for (int i = 0; i < L; i++) {
         const double nrm = sqrt(sc[(size_t)i * S_NSLOT + S_NORM]);
         if (!(nrm <= 1e12)) fail(TQ_EDIVERGED, "node iterate norm exceeded 1e12 (diverged)");
@@ -693,7 +741,7 @@ void Ctx::get_image(int slice, int node, float *out, long long len, bool on_devi
         const int i = local(slice, node);
         if (i < 0) fail(TQ_EINVAL, "node is not local to this rank");
         launch_convert(prec, in.xrow(in.X, i), 0, d, n, stream);
-    } else if (rule == TQ_RULE_PAPER) {
+    } else if (segmented()) {
         TQ_REQUIRE(slice >= 0 && slice < S, "slice out of range");
         launch_convert(prec, (uint8_t *)XG + (prec ? 8 : 4) * (long long)slice * n, 0, d, n, stream);
     } else {
@@ -736,7 +784,7 @@ void Ctx::export_state(int slice, int node, double *buf, long long len) {
     const size_t es = prec ? 8 : 4;
     to_host_double(prec, in.xrow(in.X, i), buf, n, stream);
     to_host_double(prec, (uint8_t *)ALPHA + es * n * i, buf + n, n, stream);
-    if (rule == TQ_RULE_PAPER) {
+    if (segmented()) {
         to_host_double(prec, (uint8_t *)XG + es * n * slice, buf + 2 * n, n, stream);
     } else {
         const int k = pay_of.at({slice, node});
@@ -759,7 +807,7 @@ void Ctx::import_state(int slice, int node, const double *buf, long long len) {
     const size_t es = prec ? 8 : 4;
     from_host_double(prec, buf, in.xrow(in.X, i), n, stream);
     from_host_double(prec, buf + n, (uint8_t *)ALPHA + es * n * i, n, stream);
-    if (rule == TQ_RULE_PAPER) {
+    if (segmented()) {
         from_host_double(prec, buf + 2 * n, (uint8_t *)XG + es * n * slice, n, stream);
     } else {
         const int k = pay_of.at({slice, node});

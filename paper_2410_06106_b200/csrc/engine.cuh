@@ -1,6 +1,6 @@
 // engine.cuh -- the ADMM context behind the C-ABI: per-rank device state for every
 // (slice, node) mapped to this rank, the outer loop of Alg. 4
-// for both consensus rules, the quantized exchange (NCCL send/recv between ranks,
+// for the three consensus rules, the quantized exchange (NCCL send/recv between ranks,
 // pointers within a rank) and CUDA-graph replay of whole iterations.
 #pragma once
 #include <nccl.h>
@@ -20,6 +20,8 @@ struct NcclApi {
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Reduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                           cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
@@ -48,7 +50,8 @@ struct Ctx {
     DevGeom geo;
     Inner in;
     void *ALPHA = nullptr;      // [L][n] alpha_i (graph) / lambda_m (paper)
-    void *XG = nullptr;         // paper: [S][n] consensus x
+    void *XG = nullptr;         // paper / consensus: [S][n] consensus x
+    double *CSUM = nullptr;     // consensus: [S][n] sum of u + lambda/rho over nodes (fp64)
     // ---- settings
     tq_params prm{};
     std::vector<double> eta1;
@@ -87,7 +90,8 @@ struct Ctx {
     // graph rule dual tables
     const void **xh_tab = nullptr;
     int *own_slot = nullptr, *nbr_off = nullptr, *nbr_slot = nullptr;
-    // paper rule tables
+    // paper / consensus rule tables
+    int *cs_slice = nullptr, *cs_first = nullptr, *cs_cnt = nullptr, *node_slice = nullptr;
     void **xg_tab = nullptr;
     long long *seg_lo = nullptr, *seg_len = nullptr;
     long long seg_max = 0;
@@ -99,8 +103,10 @@ struct Ctx {
     std::vector<long long> send_bytes, recv_bytes;
     // ---- execution
     cudaStream_t stream = nullptr;
-    cudaGraphExec_t gexecA = nullptr, gexecB = nullptr;
-    int launchesA = 0, launchesB = 0;
+    // an iteration = graph segments separated by communication steps (none when world == 1)
+    enum Comm { COMM_NONE = 0, COMM_REDUCE = 1, COMM_EXCHANGE = 2 };
+    struct Seg { cudaGraphExec_t exec; int launches, comm; };
+    std::vector<Seg> segs;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     tq_stats st{};
     std::string err;
@@ -127,7 +133,10 @@ struct Ctx {
     void invalidate();
     void setup_exchange();
     void free_exchange();
-    int phase_a(cudaStream_t s);  // inner solves + (Alg. 3) + encode
+    bool segmented() const { return rule != TQ_RULE_GRAPH; }
+    int stage(int id, cudaStream_t s);  // 0: inner solves (+ Alg. 3 / partial sums), 1: x + encode,
+                                        // 2: decode + dual (phase_b)
+    void reduce_sums(cudaStream_t s);   // consensus, world > 1: segment sums to their owners
     void exchange(cudaStream_t s);
     int phase_b(cudaStream_t s);  // decode + dual / next b'
     int prepare_rhs(cudaStream_t s);

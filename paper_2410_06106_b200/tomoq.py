@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(HERE, "libtomoq.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "tomoq.h")
 
 SPLIT_RR, SPLIT_CONTIG = 0, 1
-RULE_GRAPH, RULE_PAPER = 0, 1
+RULE_GRAPH, RULE_PAPER, RULE_CONSENSUS = 0, 1, 2
 INNER_GD, INNER_CG = 0, 1
 Q_NONE, Q_KMEANS, Q_DCT, Q_ALT = 0, 1, 2, 3
 STATUS = {0: "TQ_OK", 1: "TQ_EINVAL", 2: "TQ_ENOMEM", 3: "TQ_ECUDA", 4: "TQ_ENCCL",

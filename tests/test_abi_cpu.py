@@ -53,7 +53,7 @@ def test_payload_bytes():
 
 @pytest.mark.parametrize("kind,M,world", [("ring", 8, 2), ("ring", 8, 4), ("torus", 16, 8),
                                           ("regular4", 16, 8), ("complete", 8, 8), ("ring", 2, 2)])
-@pytest.mark.parametrize("rule", [tomoq.RULE_GRAPH, tomoq.RULE_PAPER])
+@pytest.mark.parametrize("rule", [tomoq.RULE_GRAPH, tomoq.RULE_PAPER, tomoq.RULE_CONSENSUS])
 def test_exchange_plans_pair_up(kind, M, world, rule):
     edges = synth.make_graph(kind, M, 4003)
     plans = [tomoq.exchange_plan(M, edges, rule, r, world) for r in range(world)]

@@ -83,6 +83,60 @@ def test_paper_rule_quantized_fp64():
         assert rel(ctx.image(), o.image()) <= 1e-6
 
 
+@pytest.mark.parametrize("prec,tol", [(0, 1e-3), (1, 1e-6)])
+def test_consensus_rule_c1(prec, tol):
+    """Rule 2 (standard consensus ADMM of P:121-131, x sharded in segments)."""
+    cfg = C.C1()
+    cfg.rule = C.RULE_CONSENSUS
+    cfg.iters = 20
+    inp = C.make_inputs(cfg)
+    ctx = gpu_context(cfg, inp, precision=prec)
+    ctx.run(cfg.iters)
+    o = oracle_case(cfg, inp).run(cfg.iters)
+    assert rel(ctx.image(), o.image()) <= tol
+    for m in range(cfg.nodes):
+        assert rel(ctx.image(0, m), o.X[m]) <= tol
+
+
+@pytest.mark.parametrize("q", [C.Q_KMEANS, C.Q_DCT])
+def test_consensus_rule_quantized_fp64(q):
+    cfg = C.C1()
+    cfg.rule, cfg.quant, cfg.iters, cfg.k = C.RULE_CONSENSUS, q, 5, 8
+    cfg.nodes, cfg.graph = 2, "ring"
+    inp = C.make_inputs(cfg)
+    ctx = gpu_context(cfg, inp, precision=1)
+    ctx.run(cfg.iters)
+    o = oracle_case(cfg, inp).run(cfg.iters)
+    assert rel(ctx.image(), o.image()) <= 1e-6
+
+
+def test_consensus_rule_lockstep_full_size():
+    """Rule 2 on the bench geometry (C4 at G = 1: 1024^2, 8 nodes, K-means 64 per 128-row
+    segment), fp32: the oracle advances one iteration from the exported GPU state; the
+    next u_m (pre-quantization) and the consensus x must match, and the dual sum over
+    nodes is rho * sum_m (u_m - x) (eq-compact:solve_lambda)."""
+    cfg = C.C4(1)
+    cfg.rule = C.RULE_CONSENSUS
+    inp = C.make_inputs(cfg, with_truth=False)
+    ctx = gpu_context(cfg, inp, precision=0)
+    ctx.run(1)
+    X, L, XH = export_all(ctx, cfg)
+    o = oracle_case(cfg, inp)
+    o.X, o.L, o.XH = X.copy(), L.copy(), XH.copy()
+    o.run(1)
+    ctx.run(1)
+    Xg, Lg, XHg = export_all(ctx, cfg)
+    for m in range(cfg.nodes):
+        assert rel(Xg[m], o.X[m]) <= 1e-3
+    # x is K-means-quantized per segment: compare on the segments where both decode the
+    # same centroids (>= 99.9% of pixels; a near-tie label flip moves one pixel)
+    close = np.abs(XHg[0] - o.XH[0]) <= 1e-3 * np.abs(o.XH[0]).max()
+    assert close.mean() >= 0.999
+    dl = (Lg - L).sum(axis=0)
+    want = cfg.rho * (Xg - XHg[0]).sum(axis=0)
+    assert rel(dl, want) <= 1e-3
+
+
 def lockstep(cfg, inp, prec=0, steps=3, warm=2, label_nodes=None):
     """GPU runs `warm` iterations, then for each step: the oracle advances one
     iteration from the exported GPU state; compare the pre-quantization iterates."""

@@ -111,3 +111,77 @@ def test_gloo_world2_matches_single_process(tmp_path):
         for k, i in enumerate(nodes):
             np.testing.assert_allclose(got[k], ref.X[i], rtol=0, atol=1e-12 * np.abs(ref.X[i]).max())
     assert np.abs(ref.X).max() > 0
+
+
+def _distributed_consensus(rank, world, port, iters, out):
+    """Rule 2 (P:121-131 with x sharded in segments) split over the ranks as libtomoq
+    places it: per-rank partial sums of u + lambda/rho, one reduce per segment onto the
+    rank owning that segment (Ctx::reduce_sums), x[m] formed there, then the all-gather
+    of the segments in tq_exchange_plan order."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg, inp = _case()
+        M, N = cfg.nodes, cfg.N
+        n = N * N
+        off, idx = oracle.partition_angles(cfg.n_angles, M, cfg.split == C.SPLIT_CONTIG)
+        rows = [m * N // M for m in range(M + 1)]  # the oracle's row partition (M | N here)
+        sino = inp.sino[0].astype(np.float64)
+        sends, recvs = tomoq.exchange_plan(M, inp.edges, tomoq.RULE_CONSENSUS, rank, world)
+        mine = [i for i in range(M) if i % world == rank]
+        X = {i: np.zeros(n) for i in mine}
+        A = {i: np.zeros(n) for i in mine}
+        x = np.zeros(n)
+        rho = cfg.rho
+        for _ in range(iters):
+            for i in mine:
+                sel = idx[off[i]:off[i + 1]]
+                X[i] = oracle.cg(sino[sel], (rho * x - A[i]).reshape(N, N), rho, cfg.e1,
+                                 X[i].reshape(N, N), cfg.n_angles, sel).ravel()
+            psum = np.zeros(n)
+            for i in mine:
+                psum = psum + (X[i] + A[i] / rho)
+            t = torch.from_numpy(psum)
+            for m in range(M):
+                seg = t[rows[m] * N:rows[m + 1] * N].clone()
+                dist.reduce(seg, dst=m % world)
+                if m % world == rank:
+                    x[rows[m] * N:rows[m + 1] * N] = seg.numpy() / M
+            reqs, bufs = [], []
+            for node, peer in sends:
+                reqs.append(dist.isend(torch.from_numpy(x[rows[node] * N:rows[node + 1] * N].copy()), dst=peer))
+            for node, peer in recvs:
+                b = torch.empty((rows[node + 1] - rows[node]) * N, dtype=torch.float64)
+                reqs.append(dist.irecv(b, src=peer))
+                bufs.append((node, b))
+            for r in reqs:
+                r.wait()
+            for node, b in bufs:
+                x[rows[node] * N:rows[node + 1] * N] = b.numpy()
+            for i in mine:
+                A[i] = A[i] + rho * (X[i] - x)
+        np.save(os.path.join(out, f"x_rank{rank}.npy"), x)
+        np.save(os.path.join(out, f"u_rank{rank}.npy"), np.stack([X[i] for i in mine]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world2_consensus_rule_matches_single_process(tmp_path):
+    iters = 3
+    world = 2
+    port = _free_port()
+    mp.start_processes(_distributed_consensus, args=(world, port, iters, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    cfg, inp = _case()
+    ref = oracle.OracleADMM(cfg.N, cfg.n_det, cfg.n_angles, cfg.nodes, inp.edges,
+                            inp.sino[0].astype(np.float64), cfg.split == C.SPLIT_CONTIG, rule=2,
+                            inner=1, e1=cfg.e1, rho=cfg.rho, qkind=0, threads=1).run(iters)
+    # the cross-rank sum order differs from the oracle's node order: equal to rounding
+    for r in range(world):
+        x = np.load(os.path.join(tmp_path, f"x_rank{r}.npy"))
+        np.testing.assert_allclose(x, ref.XH[0], rtol=0, atol=1e-11 * np.abs(ref.XH[0]).max())
+        got = np.load(os.path.join(tmp_path, f"u_rank{r}.npy"))
+        for k, i in enumerate(i for i in range(cfg.nodes) if i % world == r):
+            np.testing.assert_allclose(got[k], ref.X[i], rtol=0, atol=1e-11 * np.abs(ref.X[i]).max())
+    assert np.abs(ref.XH[0]).max() > 0
