@@ -87,8 +87,9 @@ __device__ __forceinline__ void load_striped(const uint32_t *keys, long long off
     for (int r = 0; r < KI; r++) k[r] = p[r * 32];
 }
 
-// per-warp private digit counts (no atomics: the leader of each peer group owns its
-// digit within the warp), then the tile histogram into sh[256]
+// tile histogram: per-warp private digit counters updated with shared-memory atomics
+// (integer counts: the result does not depend on the order of the updates), then the
+// column sums into sh[256]
 __device__ __forceinline__ void tile_hist(const uint32_t (&k)[KI], int shift, uint32_t *wc /* [8][256] */,
                                           uint32_t *sh) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -96,12 +97,7 @@ __device__ __forceinline__ void tile_hist(const uint32_t (&k)[KI], int shift, ui
     for (int i = lane; i < 256; i += 32) c[i] = 0u;
     __syncwarp();
 #pragma unroll
-    for (int r = 0; r < KI; r++) {
-        const uint32_t d = (k[r] >> shift) & 255u;
-        const unsigned peers = digit_peers(d);
-        if (lane == __ffs(peers) - 1) c[d] += (uint32_t)__popc(peers);
-        __syncwarp();
-    }
+    for (int r = 0; r < KI; r++) atomicAdd(&c[(k[r] >> shift) & 255u], 1u);
     __syncthreads();
     uint32_t tot = 0;
 #pragma unroll
@@ -136,7 +132,7 @@ __global__ void __launch_bounds__(KT) km_hist(const uint32_t *keys, KmPtr w, int
     __shared__ uint32_t sh[256], wc[KT / 32 * 256];
     const int b = blockIdx.y, t = blockIdx.x;
     uint32_t k[KI];
-    load_striped(keys, ((long long)b * w.T + t) * KTILE, k);
+    load_tile(keys, ((long long)b * w.T + t) * KTILE, k);  // order does not matter for counting
     tile_hist(k, shift, wc, sh);
     flush_hist(sh, w.hist + (long long)b * 256 * w.T, w.T, t);
 }
