@@ -430,6 +430,12 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, unsigne
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 
+// rays per half-warp item: 16 lanes on one line span <= 16 consecutive pair slots
+__device__ __forceinline__ int fp_half_rays(double at) {
+    const int h = (int)(15.0 / fabs(at)) + 1;
+    return h < 1 ? 1 : (h > 16 ? 16 : h);
+}
+
 // Persistent, TMA-pipelined forward tile pass.  Each CTA walks the work units
 // u = (orientation, node, tile) round-robin; while it computes unit u from the pair
 // tile P, one thread has already issued the TMA tensor load of unit u+grid's raw tile
@@ -447,8 +453,6 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
     float2 *pt = reinterpret_cast<float2 *>(raw + FPP_RAW);                    // [TH][PITCH] (e, d)
     FpRec *rec = reinterpret_cast<FpRec *>(pt + FP_TH * FP2_PITCH);            // [2][FPP_MAXA]
     FpUnitTab *utb = reinterpret_cast<FpUnitTab *>(rec + 2 * FPP_MAXA);          // [2]
-    __shared__ int s_pre[FPP_MAXA + 1];
-    __shared__ unsigned char s_item_k[256];
     __shared__ __align__(8) unsigned long long bar;
     const int ntiles = a.nt_line * a.nt_cross;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -558,41 +562,40 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
                 for (int k = threadIdx.x; k < nb; k += FP_THREADS) R[k] = a.recs[(long long)U.tile * a.n_olist + b0 + k];
                 __syncthreads();
             }
-            const int *pre = utb[rb].pre;
-            const unsigned char *itk = utb[rb].item;
-            if (b0 != U.a_begin) {  // later batches: plan computed here
+            FpUnitTab &ut = utb[rb];
+            if (b0 != U.a_begin) {  // later batches: plan computed here, over the unit's table
                 if (threadIdx.x < FPP_MAXA) {
                     const int k = threadIdx.x;
-                    int inc = k < nb ? R[k].W : 0;
+                    const int nh = k < nb ? fp_half_rays(R[k].at) : 1;
+                    int inc = k < nb ? (R[k].W + nh - 1) / nh : 0;
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
                         const int y = __shfl_up_sync(0xffffffffu, inc, o);
                         if (lane >= o) inc += y;
                     }
-                    s_pre[k + 1] = inc;
-                    if (k == 0) s_pre[0] = 0;
+                    ut.hpre[k + 1] = inc;
+                    ut.nh[k] = (unsigned char)nh;
+                    if (k == 0) ut.hpre[0] = 0;
                 }
                 __syncthreads();
                 for (int k = threadIdx.x; k < nb; k += FP_THREADS)
-                    for (int it = (s_pre[k] + 31) >> 5; (it << 5) < s_pre[k + 1] && it < 256; it++) s_item_k[it] = (unsigned char)k;
+                    for (int it = ut.hpre[k]; it < ut.hpre[k + 1]; it++) ut.hk[it] = (unsigned char)k;
                 __syncthreads();
-                pre = s_pre;
-                itk = s_item_k;
             }
-            const int Rn = pre[nb];
-            for (int g0 = warp * 32; g0 < Rn; g0 += FP_THREADS) {
-                const int g = min(g0 + lane, Rn - 1);
-                int k = (g0 >> 5) < 256 ? itk[g0 >> 5] : 0;
-                if ((g0 >> 5) >= 256) {  // very many rays in one batch: search
-                    int lo = 0, hi = nb - 1;
-                    while (lo < hi) {
-                        const int mid = (lo + hi + 1) >> 1;
-                        if (pre[mid] <= g0) lo = mid; else hi = mid - 1;
-                    }
-                    k = lo;
-                }
-                while (pre[k + 1] <= g) k++;
-                const int w = g - pre[k];
+            const int *hpre = ut.hpre;
+            const unsigned char *nhv = ut.nh;
+            const unsigned char *hk = ut.hk;
+            const int Hn = hpre[nb];
+            const int hl = lane & 15;
+            // one warp item = two half-warp items (each nh_k <= 16 rays of one angle)
+            for (int h0 = 2 * warp; h0 < Hn; h0 += 2 * (FP_THREADS / 32)) {
+                const int hraw = h0 + (lane >> 4);
+                const int hi = min(hraw, Hn - 1);
+                const int k = hk[hi];
+                const int nh = nhv[k], W = R[k].W;
+                const int w0 = (hi - hpre[k]) * nh + hl;
+                const bool ok = hraw < Hn && hl < nh && w0 < W;
+                const int w = min(min(w0, (hi - hpre[k]) * nh + nh - 1), W - 1);  // idle lanes repeat a ray
                 const float kap = (float)(R[k].kap + (double)w * R[k].at);
                 const float B = R[k].B;
                 float acc0 = 0.f, acc1 = 0.f;
@@ -605,7 +608,7 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
                     acc0 += fmaf(kf0, q0.y, q0.x);
                     acc1 += fmaf(kf1, q1.y, q1.x);
                 }
-                if (g0 + lane < Rn)
+                if (ok)
                     a.partial[((long long)R[k].row * a.nt_line + lt) * 2 * a.n_det + (ct & 1) * a.n_det + R[k].jlo + w] =
                         acc0 + acc1;
             }
@@ -668,28 +671,36 @@ __global__ void fp_rec_kernel(const int *olist, int n_olist, int ntiles, const F
 
 __global__ void fp_unit_kernel(const int *oofs, const FpRec *recs, int n_olist, int ntiles, int L, FpUnitTab *utab) {
     __shared__ int pre[FPP_MAXA + 1];
+    __shared__ unsigned char nhs[FPP_MAXA];
     const int u = blockIdx.x, per = L * ntiles;
     const int O = u / per, rem = u - O * per, node = rem / ntiles, tile = rem - node * ntiles;
     const int a0 = oofs[2 * node + O], a1 = oofs[2 * node + O + 1];
     const int nb = min(FPP_MAXA, a1 - a0);
     if (threadIdx.x == 0) {
         int acc = 0;
-        for (int k = 0; k < nb; k++) {
+        for (int k = 0; k < FPP_MAXA; k++) {
             pre[k] = acc;
-            acc += recs[(long long)tile * n_olist + a0 + k].W;
+            int nh = 1;
+            if (k < nb) {
+                const FpRec r = recs[(long long)tile * n_olist + a0 + k];
+                nh = fp_half_rays(r.at);
+                acc += (r.W + nh - 1) / nh;
+            }
+            nhs[k] = (unsigned char)nh;
         }
-        for (int k = nb; k <= FPP_MAXA; k++) pre[k] = acc;
+        pre[FPP_MAXA] = acc;
     }
     __syncthreads();
     FpUnitTab *t = utab + u;
-    for (int k = threadIdx.x; k <= FPP_MAXA; k += blockDim.x) t->pre[k] = pre[k];
-    for (int it = threadIdx.x; it < 256; it += blockDim.x) {
-        int lo = 0, hi = max(nb - 1, 0);  // angle of ray 32*it: largest k with pre[k] <= 32 it
+    for (int k = threadIdx.x; k <= FPP_MAXA; k += blockDim.x) t->hpre[k] = pre[k];
+    for (int k = threadIdx.x; k < FPP_MAXA; k += blockDim.x) t->nh[k] = nhs[k];
+    for (int it = threadIdx.x; it < FPP_HMAX; it += blockDim.x) {
+        int lo = 0, hi = max(nb - 1, 0);  // angle of half-item it: largest k with pre[k] <= it
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
-            if (pre[mid] <= 32 * it) lo = mid; else hi = mid - 1;
+            if (pre[mid] <= it) lo = mid; else hi = mid - 1;
         }
-        t->item[it] = (unsigned char)lo;
+        t->hk[it] = (unsigned char)lo;
     }
 }
 

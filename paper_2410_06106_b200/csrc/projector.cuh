@@ -58,15 +58,22 @@ struct FpRec {
     int jlo, W, row;
 };
 
-// Static per-unit item plan of the persistent fp32 forward kernel (first batch of <= 64
-// angles of a unit): exclusive prefix of the window sizes, and the angle of each 32-ray
-// item's first ray.  Bulk-copied with the unit's records.
+// Static per-unit item plan of the persistent fp32 forward kernel (first batch of <= 32
+// angles of a unit).  Work is split into half-warp items of nh_k consecutive rays of one
+// angle k, nh_k = min(16, floor(15 / at_k) + 1), so the 16 lanes of a half-warp read one
+// line's (e, d) pairs within a window of 16 consecutive 8-byte slots: every LDS.64 of the
+// ray walk is conflict-free (2 wavefronts per warp).  hpre = exclusive prefix of the
+// half-item counts ceil(W_k / nh_k); hk = angle of each half-item.  Bulk-copied with the
+// unit's records.
+constexpr int FPP_HMAX = 512;  // >= FPP_MAXA * ceil(FP_WMAX / 11) half-items per batch
 struct FpUnitTab {
-    int pre[FPP_MAXA + 1];
-    unsigned char item[256];
+    int hpre[FPP_MAXA + 1];
+    unsigned char nh[FPP_MAXA];
+    unsigned char hk[FPP_HMAX];
     int pad[3];
 };
 static_assert(sizeof(FpUnitTab) % 16 == 0, "bulk-copy granularity");
+static_assert(FPP_MAXA * ((FP_WMAX + 10) / 11) <= FPP_HMAX, "half-item table too small");
 
 template <typename T>
 struct FpArgs {
