@@ -454,6 +454,7 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
     FpRec *rec = reinterpret_cast<FpRec *>(pt + FP_TH * FP2_PITCH);            // [2][FPP_MAXA]
     FpUnitTab *utb = reinterpret_cast<FpUnitTab *>(rec + 2 * FPP_MAXA);          // [2]
     __shared__ __align__(8) unsigned long long bar;
+    __shared__ int s_hdr[2][8];  // per unit buffer: O, tile, a_begin, a_end, lt, ct (written by thread 0)
     const int ntiles = a.nt_line * a.nt_cross;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t raw_s = (uint32_t)__cvta_generic_to_shared(raw);
@@ -470,23 +471,28 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    // thread 0: TMA of unit u's raw tile + bulk copy of its first window records; returns
-    // whether anything was issued (units without angles of that orientation are skipped)
+    // thread 0: decodes unit u into s_hdr[rb] and issues the TMA of its raw tile + bulk
+    // copies of its first window records and item plan (units without angles of their
+    // orientation load only the tile and are skipped); every thread learns whether a load
+    // is pending from u alone, so the integer divisions of the decode run in one thread
     auto issue = [&](int u, int rb) -> bool {
         if (u >= nunits) return false;
-        const FpUnit U = fp_unit(a, u, ntiles);
-        if (U.a_begin == U.a_end) return false;
         if (threadIdx.x == 0) {
+            const FpUnit U = fp_unit(a, u, ntiles);
             const int lt = U.tile / a.nt_cross, ct = U.tile % a.nt_cross;
+            s_hdr[rb][0] = U.O; s_hdr[rb][1] = U.tile; s_hdr[rb][2] = U.a_begin; s_hdr[rb][3] = U.a_end;
+            s_hdr[rb][4] = lt; s_hdr[rb][5] = ct;
             const int L0 = lt * FP_TH, X0 = ct * FP_TW;
             const int nb = min(FPP_MAXA, U.a_end - U.a_begin);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of raw before the async write
-            mbar_expect_tx(bar_s, FPP_RAW * 4 + nb * (unsigned)sizeof(FpRec) + (unsigned)sizeof(FpUnitTab));
+            mbar_expect_tx(bar_s, FPP_RAW * 4 + (nb > 0 ? nb * (unsigned)sizeof(FpRec) + (unsigned)sizeof(FpUnitTab) : 0u));
             if (U.O == 0) tma_load_3d(raw_s, &tm_rows, X0, L0, U.node, bar_s);
             else tma_load_3d(raw_s, &tm_cols, L0, X0, U.node, bar_s);
-            bulk_load(rec_s + (uint32_t)(rb * FPP_MAXA * sizeof(FpRec)), a.recs + (long long)U.tile * a.n_olist + U.a_begin,
-                      nb * (unsigned)sizeof(FpRec), bar_s);
-            bulk_load((uint32_t)__cvta_generic_to_shared(utb + rb), a.utab + u, (unsigned)sizeof(FpUnitTab), bar_s);
+            if (nb > 0) {
+                bulk_load(rec_s + (uint32_t)(rb * FPP_MAXA * sizeof(FpRec)), a.recs + (long long)U.tile * a.n_olist + U.a_begin,
+                          nb * (unsigned)sizeof(FpRec), bar_s);
+                bulk_load((uint32_t)__cvta_generic_to_shared(utb + rb), a.utab + u, (unsigned)sizeof(FpUnitTab), bar_s);
+            }
         }
         return true;
     };
@@ -499,14 +505,15 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
     unsigned phase = 0;
     bool pending = issue(blockIdx.x, rb);
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, rb ^= 1) {
-        const FpUnit U = fp_unit(a, u, ntiles);
         if (pending) {
             mbar_wait(bar_s, phase);
             phase ^= 1;
         }
-        __syncthreads();  // raw + rec[rb] of unit u landed; previous unit's P reads done
+        __syncthreads();  // raw + rec[rb] of unit u landed; previous unit's P reads done; s_hdr[rb] set
+        FpUnit U;
+        U.O = s_hdr[rb][0]; U.tile = s_hdr[rb][1]; U.a_begin = s_hdr[rb][2]; U.a_end = s_hdr[rb][3];
         const bool active = U.a_begin != U.a_end;
-        const int lt = U.tile / a.nt_cross, ct = U.tile % a.nt_cross;
+        const int lt = s_hdr[rb][4], ct = s_hdr[rb][5];
         if (active) {  // ---- raw -> (e, d) pairs
             if (U.O == 0) {
                 for (int l = warp; l < FP_TH; l += FP_THREADS / 32) {
