@@ -142,12 +142,11 @@ int Inner::cg(const DevGeom &g, int e1, cudaStream_t st) {
     for (int it = 0; it < e1; it++) {
         k += project(g, P, false, st);
         k += backproject(g, EPI_CGQ, Q, nullptr, P, st);
-        launch_cg_update_xr(prec, X, R, P, Q, n, L, scal, partial, part_stride, counter, st);
-        k++;
-        if (it + 1 < e1) {  // the last search direction is never used
-            launch_cg_update_p(prec, P, R, n, L, scal, st);
-            k++;
-        }
+        launch_cg_update_r(prec, R, Q, n, L, scal, partial, part_stride, counter, st);
+        // x += alpha p (deferred from the r update: this pass reads p anyway), then the next
+        // search direction p = r + beta p (the last one is never used)
+        launch_cg_update_px(prec, X, P, R, n, L, scal, it + 1 < e1, st);
+        k += 2;
     }
     return k;
 }

@@ -30,32 +30,28 @@ __device__ __forceinline__ void vec_loop(long long n, F4 &&body4, F1 &&body1) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(VT) cg_update_xr(T *__restrict__ x, T *__restrict__ r, const T *__restrict__ p,
-                                                   const T *__restrict__ q, long long n, double *scal,
-                                                   double *partial, int part_stride, unsigned *counter) {
+__global__ void __launch_bounds__(VT) cg_update_r(T *__restrict__ r, const T *__restrict__ q, long long n,
+                                                  double *scal, double *partial, int part_stride, unsigned *counter) {
     __shared__ double red[VT / 32 + 1];
     __shared__ bool last;
     const int node = blockIdx.y;
     const long long base = (long long)node * n;
     double *sc = scal + (long long)node * S_NSLOT;
     const double alpha = sc[S_ALPHA];
-    x += base; r += base; p += base; q += base;
+    r += base; q += base;
     double dot = 0.0;
     vec_loop(n,
         [&](long long i) {
-            Q4<T> xv = ld4(x + i), rv = ld4(r + i);
-            const Q4<T> pv = ld4(p + i), qv = ld4(q + i);
+            Q4<T> rv = ld4(r + i);
+            const Q4<T> qv = ld4(q + i);
 #pragma unroll
             for (int u = 0; u < 4; u++) {
-                xv.v[u] = (T)((double)xv.v[u] + alpha * (double)pv.v[u]);
                 rv.v[u] = (T)((double)rv.v[u] - alpha * (double)qv.v[u]);
                 dot += (double)rv.v[u] * (double)rv.v[u];
             }
-            st4(x + i, xv);
             st4(r + i, rv);
         },
         [&](long long i) {
-            x[i] = (T)((double)x[i] + alpha * (double)p[i]);
             const T rv = (T)((double)r[i] - alpha * (double)q[i]);
             r[i] = rv;
             dot += (double)rv * (double)rv;
@@ -76,22 +72,32 @@ __global__ void __launch_bounds__(VT) cg_update_xr(T *__restrict__ x, T *__restr
     }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(VT) cg_update_p(T *__restrict__ p, const T *__restrict__ r, long long n,
-                                                  const double *scal) {
+template <typename T, bool WITH_P>
+__global__ void __launch_bounds__(VT) cg_update_px(T *__restrict__ x, T *__restrict__ p, const T *__restrict__ r,
+                                                   long long n, const double *scal) {
     const int node = blockIdx.y;
     const long long base = (long long)node * n;
+    const double alpha = scal[(long long)node * S_NSLOT + S_ALPHA];
     const double beta = scal[(long long)node * S_NSLOT + S_BETA];
-    p += base; r += base;
+    x += base; p += base; r += base;
     vec_loop(n,
         [&](long long i) {
-            Q4<T> pv = ld4(p + i);
-            const Q4<T> rv = ld4(r + i);
+            Q4<T> xv = ld4(x + i), pv = ld4(p + i);
+            Q4<T> rv;
+            if (WITH_P) rv = ld4(r + i);
 #pragma unroll
-            for (int u = 0; u < 4; u++) pv.v[u] = (T)((double)rv.v[u] + beta * (double)pv.v[u]);
-            st4(p + i, pv);
+            for (int u = 0; u < 4; u++) {
+                xv.v[u] = (T)((double)xv.v[u] + alpha * (double)pv.v[u]);
+                if (WITH_P) pv.v[u] = (T)((double)rv.v[u] + beta * (double)pv.v[u]);
+            }
+            st4(x + i, xv);
+            if (WITH_P) st4(p + i, pv);
         },
-        [&](long long i) { p[i] = (T)((double)r[i] + beta * (double)p[i]); });
+        [&](long long i) {
+            const T pv = p[i];
+            x[i] = (T)((double)x[i] + alpha * (double)pv);
+            if (WITH_P) p[i] = (T)((double)r[i] + beta * (double)pv);
+        });
 }
 
 template <typename T>
@@ -127,24 +133,26 @@ __global__ void convert_kernel(const A *src, B *dst, long long n) {
         dst[i] = (B)src[i];
 }
 
-void launch_cg_update_xr(int prec, void *x, void *r, const void *p, const void *q, long long n,
-                         int L, double *scal, double *partial, int part_stride, unsigned *counter,
-                         cudaStream_t st) {
+void launch_cg_update_r(int prec, void *r, const void *q, long long n, int L, double *scal, double *partial,
+                        int part_stride, unsigned *counter, cudaStream_t st) {
     dim3 grid(vec_blocks(n), L);
     if (prec == 0)
-        cg_update_xr<float><<<grid, VT, 0, st>>>((float *)x, (float *)r, (const float *)p,
-                                                 (const float *)q, n, scal, partial, part_stride, counter);
+        cg_update_r<float><<<grid, VT, 0, st>>>((float *)r, (const float *)q, n, scal, partial, part_stride, counter);
     else
-        cg_update_xr<double><<<grid, VT, 0, st>>>((double *)x, (double *)r, (const double *)p,
-                                                  (const double *)q, n, scal, partial, part_stride, counter);
+        cg_update_r<double><<<grid, VT, 0, st>>>((double *)r, (const double *)q, n, scal, partial, part_stride, counter);
     TQ_CHECK_CUDA(cudaGetLastError());
 }
 
-void launch_cg_update_p(int prec, void *p, const void *r, long long n, int L, const double *scal,
-                        cudaStream_t st) {
+void launch_cg_update_px(int prec, void *x, void *p, const void *r, long long n, int L, const double *scal,
+                         bool with_p, cudaStream_t st) {
     dim3 grid(vec_blocks(n), L);
-    if (prec == 0) cg_update_p<float><<<grid, VT, 0, st>>>((float *)p, (const float *)r, n, scal);
-    else cg_update_p<double><<<grid, VT, 0, st>>>((double *)p, (const double *)r, n, scal);
+    if (prec == 0) {
+        if (with_p) cg_update_px<float, true><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal);
+        else cg_update_px<float, false><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal);
+    } else {
+        if (with_p) cg_update_px<double, true><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal);
+        else cg_update_px<double, false><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal);
+    }
     TQ_CHECK_CUDA(cudaGetLastError());
 }
 

@@ -6,14 +6,14 @@
 
 namespace tq {
 
-// x += alpha p; r -= alpha q; rr_new = r.r (per node, deterministic); last block:
-// beta = rr_new / rr, rr = rr_new.
-void launch_cg_update_xr(int prec, void *x, void *r, const void *p, const void *q, long long n,
-                         int L, double *scal, double *partial, int part_stride, unsigned *counter,
-                         cudaStream_t st);
-// p = r + beta p
-void launch_cg_update_p(int prec, void *p, const void *r, long long n, int L, const double *scal,
-                        cudaStream_t st);
+// r -= alpha q; rr_new = r.r (per node, deterministic); last block: beta = rr_new / rr,
+// rr = rr_new.  (The matching x += alpha p is deferred to launch_cg_update_px, which reads
+// p anyway: one pass over x, p fewer per CG step, identical arithmetic.)
+void launch_cg_update_r(int prec, void *r, const void *q, long long n, int L, double *scal, double *partial,
+                        int part_stride, unsigned *counter, cudaStream_t st);
+// x += alpha p, then (with_p) p = r + beta p
+void launch_cg_update_px(int prec, void *x, void *p, const void *r, long long n, int L, const double *scal,
+                         bool with_p, cudaStream_t st);
 // scal[node][S_NORM] = ||x_node||^2
 void launch_norm2(int prec, const void *x, long long n, int L, double *scal, double *partial,
                   int part_stride, unsigned *counter, cudaStream_t st);
