@@ -58,6 +58,12 @@ def lib():
         L.or_dct_cmatrix.argtypes = [_ip]
         L.or_dct_encode.argtypes = [_fp, C.c_int, C.c_int, C.c_int, _sp, _fp]
         L.or_dct_decode.argtypes = [_sp, _fp, C.c_int, C.c_int, C.c_int, _fp, C.c_void_p]
+        L.or_jpeg_tables.argtypes = [_up, _up, _up, _up]
+        L.or_jpeg_zigzag.argtypes = [_ip]
+        L.or_jpeg_encode.argtypes = [_sp, C.c_long, C.c_int, _up, C.c_long]
+        L.or_jpeg_encode.restype = C.c_long
+        L.or_jpeg_decode.argtypes = [_up, C.c_long, C.c_long, C.c_int, _sp]
+        L.or_jpeg_decode.restype = C.c_int
         L.or_partition_angles.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip]
         L.or_partition_rows.argtypes = [C.c_int, C.c_int, _ip]
         L.or_admm_run.restype = C.c_long
@@ -176,6 +182,41 @@ def dct_decode(coef, mm, rows: int, cols: int, quality: int, return_samples: boo
     lib().or_dct_decode(np.ascontiguousarray(coef, dtype=np.int16), _f32(mm), rows, cols,
                         quality, out, smp.ctypes.data if return_samples else None)
     return (out, smp) if return_samples else out
+
+
+# ----------------------------------------------------------------- JPEG entropy coding (NEXT-2)
+def jpeg_tables():
+    """(dc_bits, dc_val, ac_bits, ac_val) as the oracle stores them (T.81 Tables K.3, K.5)."""
+    t = [np.zeros(16, np.uint8), np.zeros(12, np.uint8), np.zeros(16, np.uint8), np.zeros(162, np.uint8)]
+    lib().or_jpeg_tables(*t)
+    return tuple(t)
+
+
+def jpeg_zigzag():
+    z = np.zeros(64, np.int32)
+    lib().or_jpeg_zigzag(z)
+    return z
+
+
+def jpeg_encode(coef, restart: int = 0) -> bytes:
+    """Baseline JPEG Huffman entropy coding (T.81 F.1.2) of int16 blocks [nblocks*64]
+    (natural order, raster block order) with a restart marker every `restart` blocks."""
+    c = np.ascontiguousarray(coef, dtype=np.int16).ravel()
+    nb = c.size // 64
+    cap = 16 + nb * 512 + 4 * (nb // max(1, restart) + 1)
+    out = np.zeros(cap, np.uint8)
+    n = lib().or_jpeg_encode(c, nb, restart, out, cap)
+    if n < 0:
+        raise ValueError("jpeg_encode: value outside the baseline categories")
+    return out[:n].tobytes()
+
+
+def jpeg_decode(stream: bytes, nblocks: int, restart: int = 0):
+    buf = np.frombuffer(bytes(stream), np.uint8).copy() if len(stream) else np.zeros(1, np.uint8)
+    coef = np.zeros(nblocks * 64, np.int16)
+    if lib().or_jpeg_decode(buf, len(stream), nblocks, restart, coef) != 0:
+        raise ValueError("jpeg_decode: malformed stream")
+    return coef
 
 
 # ----------------------------------------------------------------- partitions / models

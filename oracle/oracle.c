@@ -380,6 +380,236 @@ void or_dct_decode(const int16_t *coef, const float *minmax, int rows, int cols,
         }
 }
 
+/* ------------------------------------------------------------------ JPEG entropy coding
+ * the lossless stage of "standard JPEG" after the DCT
+ * quantizer -- baseline sequential Huffman coding of ITU-T T.81, written out from the
+ * standard: Annex K.3 Tables K.3 / K.5 (luminance DC / AC BITS and HUFFVAL), Annex C
+ * (code generation: HUFFSIZE, HUFFCODE, EHUFCO/EHUFSI), Figure A.6 (zig-zag order),
+ * F.1.2.1 / F.1.2.2 (DC difference and AC run-length coding, Figures F.1-F.3, ZRL /
+ * EOB), F.1.2.3 (byte stuffing: 0x00 after every 0xFF), B.2.1 / E.1.4 / F.1.2.3 (fill
+ * bits are 1s; RSTm markers every R blocks with m = 0..7 cycling and the DC
+ * predictor reset, F.1.4.4; R-25), F.2.2.1-F.2.2.4 (decode: DECODE with
+ * MINCODE/MAXCODE/VALPTR, RECEIVE, EXTEND).  Blocks are the DCT quantizer's 8x8 blocks
+ * in raster order, coefficients in natural order (row = vertical frequency) as
+ * or_dct_encode writes them.  Returns the stream length, or -1 if the output capacity
+ * is exceeded or a value is outside the baseline categories (DC difference > 11 bits,
+ * AC > 10 bits). */
+static const uint8_t JPEG_DC_BITS[16] = {0, 1, 5, 1, 1, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0};
+static const uint8_t JPEG_DC_VAL[12] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11};
+static const uint8_t JPEG_AC_BITS[16] = {0, 2, 1, 3, 3, 2, 4, 3, 5, 5, 4, 4, 0, 0, 1, 0x7d};
+static const uint8_t JPEG_AC_VAL[162] = {
+    0x01, 0x02, 0x03, 0x00, 0x04, 0x11, 0x05, 0x12, 0x21, 0x31, 0x41, 0x06, 0x13, 0x51, 0x61, 0x07,
+    0x22, 0x71, 0x14, 0x32, 0x81, 0x91, 0xa1, 0x08, 0x23, 0x42, 0xb1, 0xc1, 0x15, 0x52, 0xd1, 0xf0,
+    0x24, 0x33, 0x62, 0x72, 0x82, 0x09, 0x0a, 0x16, 0x17, 0x18, 0x19, 0x1a, 0x25, 0x26, 0x27, 0x28,
+    0x29, 0x2a, 0x34, 0x35, 0x36, 0x37, 0x38, 0x39, 0x3a, 0x43, 0x44, 0x45, 0x46, 0x47, 0x48, 0x49,
+    0x4a, 0x53, 0x54, 0x55, 0x56, 0x57, 0x58, 0x59, 0x5a, 0x63, 0x64, 0x65, 0x66, 0x67, 0x68, 0x69,
+    0x6a, 0x73, 0x74, 0x75, 0x76, 0x77, 0x78, 0x79, 0x7a, 0x83, 0x84, 0x85, 0x86, 0x87, 0x88, 0x89,
+    0x8a, 0x92, 0x93, 0x94, 0x95, 0x96, 0x97, 0x98, 0x99, 0x9a, 0xa2, 0xa3, 0xa4, 0xa5, 0xa6, 0xa7,
+    0xa8, 0xa9, 0xaa, 0xb2, 0xb3, 0xb4, 0xb5, 0xb6, 0xb7, 0xb8, 0xb9, 0xba, 0xc2, 0xc3, 0xc4, 0xc5,
+    0xc6, 0xc7, 0xc8, 0xc9, 0xca, 0xd2, 0xd3, 0xd4, 0xd5, 0xd6, 0xd7, 0xd8, 0xd9, 0xda, 0xe1, 0xe2,
+    0xe3, 0xe4, 0xe5, 0xe6, 0xe7, 0xe8, 0xe9, 0xea, 0xf1, 0xf2, 0xf3, 0xf4, 0xf5, 0xf6, 0xf7, 0xf8,
+    0xf9, 0xfa};
+
+/* the tables as stored (for the pin against libjpeg's DHT segments) */
+void or_jpeg_tables(uint8_t *dc_bits, uint8_t *dc_val, uint8_t *ac_bits, uint8_t *ac_val)
+{
+    memcpy(dc_bits, JPEG_DC_BITS, 16); memcpy(dc_val, JPEG_DC_VAL, 12);
+    memcpy(ac_bits, JPEG_AC_BITS, 16); memcpy(ac_val, JPEG_AC_VAL, 162);
+}
+
+/* Annex C: HUFFSIZE (Figure C.1), HUFFCODE (Figure C.2), then EHUFCO/EHUFSI indexed by
+ * symbol (Figure C.3).  Also the decoder tables of F.2.2.3 (Figure F.15): per code length
+ * l = 1..16, MINCODE, MAXCODE (-1 if no codes), VALPTR. */
+typedef struct {
+    uint16_t ehufco[256]; uint8_t ehufsi[256];
+    int32_t mincode[17], maxcode[17], valptr[17];
+    const uint8_t *huffval;
+} or_huff;
+
+static void huff_build(const uint8_t *bits, const uint8_t *val, or_huff *h)
+{
+    int huffsize[257], huffcode[257], k = 0;
+    for (int l = 1; l <= 16; l++)
+        for (int i = 1; i <= bits[l - 1]; i++) huffsize[k++] = l;
+    huffsize[k] = 0;
+    int lastk = k, code = 0, si = huffsize[0];
+    k = 0;
+    while (huffsize[k]) {
+        while (huffsize[k] == si) { huffcode[k] = code; code++; k++; }
+        code <<= 1; si++;
+    }
+    memset(h->ehufsi, 0, sizeof h->ehufsi);
+    for (k = 0; k < lastk; k++) { h->ehufco[val[k]] = (uint16_t)huffcode[k]; h->ehufsi[val[k]] = (uint8_t)huffsize[k]; }
+    int j = 0;
+    for (int l = 1; l <= 16; l++) {
+        if (bits[l - 1] == 0) { h->maxcode[l] = -1; h->mincode[l] = 0; h->valptr[l] = 0; continue; }
+        h->valptr[l] = j; h->mincode[l] = huffcode[j];
+        j += bits[l - 1];
+        h->maxcode[l] = huffcode[j - 1];
+    }
+    h->huffval = val;
+}
+
+/* Figure A.6: zig-zag sequence, zz[k] = natural index (row * 8 + col) of the k-th
+ * coefficient, by walking the anti-diagonals, alternating direction. */
+static void zigzag(int *zz)
+{
+    int k = 0;
+    for (int s = 0; s <= 14; s++) {
+        if (s % 2 == 0) { /* up-right: row decreasing */
+            for (int r = (s < 8 ? s : 7); r >= 0 && s - r <= 7; r--) zz[k++] = r * 8 + (s - r);
+        } else {          /* down-left: row increasing */
+            for (int r = (s < 8 ? 0 : s - 7); r <= s && r <= 7; r++) zz[k++] = r * 8 + (s - r);
+        }
+    }
+}
+void or_jpeg_zigzag(int32_t *zz) { int z[64]; zigzag(z); for (int i = 0; i < 64; i++) zz[i] = z[i]; }
+
+typedef struct { uint8_t *out; long cap, n; uint32_t acc; int nbits; int over; } or_bitw;
+
+static void emit_byte(or_bitw *w, uint8_t b)
+{
+    if (w->n < w->cap) w->out[w->n] = b; else w->over = 1;
+    w->n++;
+}
+/* append `size` bits of `code`, MSB first; 0x00 stuffed after each 0xFF data byte (F.1.2.3) */
+static void put_bits(or_bitw *w, uint32_t code, int size)
+{
+    for (int i = size - 1; i >= 0; i--) {
+        w->acc = (w->acc << 1) | ((code >> i) & 1u);
+        if (++w->nbits == 8) {
+            emit_byte(w, (uint8_t)w->acc);
+            if ((uint8_t)w->acc == 0xFF) emit_byte(w, 0x00);
+            w->acc = 0; w->nbits = 0;
+        }
+    }
+}
+static void pad_ones(or_bitw *w) { while (w->nbits) put_bits(w, 1, 1); }
+
+static int category(int v) { int a = v < 0 ? -v : v, s = 0; while (a) { s++; a >>= 1; } return s; }
+
+long or_jpeg_encode(const int16_t *coef, long nblocks, int restart, uint8_t *out, long cap)
+{
+    or_huff dc, ac;
+    huff_build(JPEG_DC_BITS, JPEG_DC_VAL, &dc);
+    huff_build(JPEG_AC_BITS, JPEG_AC_VAL, &ac);
+    int zz[64];
+    zigzag(zz);
+    or_bitw w = {out, cap, 0, 0, 0, 0};
+    int pred = 0;
+    for (long b = 0; b < nblocks; b++) {
+        if (restart > 0 && b > 0 && b % restart == 0) { /* RSTm, m = interval index mod 8 */
+            pad_ones(&w);
+            emit_byte(&w, 0xFF);
+            emit_byte(&w, (uint8_t)(0xD0 + ((b / restart - 1) % 8)));
+            pred = 0;
+        }
+        const int16_t *c = coef + b * 64;
+        int diff = c[0] - pred; /* F.1.2.1 */
+        pred = c[0];
+        int s = category(diff);
+        if (s > 11) return -1;
+        put_bits(&w, dc.ehufco[s], dc.ehufsi[s]);
+        if (s) put_bits(&w, (uint32_t)(diff < 0 ? diff - 1 : diff) & ((1u << s) - 1u), s);
+        int r = 0; /* F.1.2.2, Figure F.2 */
+        for (int k = 1; k < 64; k++) {
+            int v = c[zz[k]];
+            if (v == 0) {
+                if (k == 63) put_bits(&w, ac.ehufco[0x00], ac.ehufsi[0x00]); /* EOB */
+                else r++;
+                continue;
+            }
+            while (r > 15) { put_bits(&w, ac.ehufco[0xF0], ac.ehufsi[0xF0]); r -= 16; } /* ZRL */
+            int sz = category(v);
+            if (sz > 10) return -1;
+            int rs = (r << 4) | sz;
+            put_bits(&w, ac.ehufco[rs], ac.ehufsi[rs]);
+            put_bits(&w, (uint32_t)(v < 0 ? v - 1 : v) & ((1u << sz) - 1u), sz);
+            r = 0;
+        }
+    }
+    pad_ones(&w);
+    return w.over ? -1 : w.n;
+}
+
+typedef struct { const uint8_t *in; long n, pos; uint32_t byte; int cnt; int marker; } or_bitr;
+
+/* NEXTBIT (Figure F.18): a 0xFF data byte is followed by a stuffed 0x00; a marker
+ * (0xFF, non-zero) stops the bit supply -- the decoder then reads zeros and flags it. */
+static int next_bit(or_bitr *r)
+{
+    if (r->cnt == 0) {
+        if (r->pos >= r->n || r->marker) { r->marker = 1; r->byte = 0; r->cnt = 8; }
+        else {
+            r->byte = r->in[r->pos++];
+            if (r->byte == 0xFF) {
+                if (r->pos < r->n && r->in[r->pos] == 0x00) r->pos++;
+                else { r->pos--; r->marker = 1; r->byte = 0; }
+            }
+            r->cnt = 8;
+        }
+    }
+    r->cnt--;
+    return (r->byte >> r->cnt) & 1;
+}
+static int decode_sym(or_bitr *r, const or_huff *h) /* DECODE, Figure F.16 */
+{
+    int code = next_bit(r), l = 1;
+    while (code > h->maxcode[l]) {
+        if (++l > 16) return -1;
+        code = (code << 1) | next_bit(r);
+    }
+    return h->huffval[h->valptr[l] + code - h->mincode[l]];
+}
+static int receive_extend(or_bitr *r, int s) /* RECEIVE (F.17) and EXTEND (F.12) */
+{
+    int v = 0;
+    for (int i = 0; i < s; i++) v = (v << 1) | next_bit(r);
+    if (s && v < (1 << (s - 1))) v = v - (1 << s) + 1;
+    return v;
+}
+
+/* returns 0, or -1 for a malformed stream (bad code, missing / wrong RSTm, bits left over) */
+int or_jpeg_decode(const uint8_t *in, long nbytes, long nblocks, int restart, int16_t *coef)
+{
+    or_huff dc, ac;
+    huff_build(JPEG_DC_BITS, JPEG_DC_VAL, &dc);
+    huff_build(JPEG_AC_BITS, JPEG_AC_VAL, &ac);
+    int zz[64];
+    zigzag(zz);
+    or_bitr r = {in, nbytes, 0, 0, 0, 0};
+    int pred = 0;
+    for (long b = 0; b < nblocks; b++) {
+        if (restart > 0 && b > 0 && b % restart == 0) {
+            r.cnt = 0; /* discard the fill bits of the current byte */
+            if (r.pos + 1 >= r.n || in[r.pos] != 0xFF || in[r.pos + 1] != 0xD0 + ((b / restart - 1) % 8)) return -1;
+            r.pos += 2; r.marker = 0; pred = 0;
+        }
+        int16_t *c = coef + b * 64;
+        for (int i = 0; i < 64; i++) c[i] = 0;
+        int s = decode_sym(&r, &dc);
+        if (s < 0 || s > 11) return -1;
+        pred += receive_extend(&r, s);
+        c[0] = (int16_t)pred;
+        for (int k = 1; k < 64; k++) { /* Figure F.13 */
+            int rs = decode_sym(&r, &ac);
+            if (rs < 0) return -1;
+            int run = rs >> 4, sz = rs & 15;
+            if (sz == 0) {
+                if (run == 15) { k += 15; continue; } /* ZRL */
+                break;                                 /* EOB */
+            }
+            k += run;
+            if (k > 63) return -1;
+            c[zz[k]] = (int16_t)receive_extend(&r, sz);
+        }
+        if (r.marker && r.pos >= r.n) return -1; /* ran past the data */
+    }
+    /* everything consumed: the remaining bits of the last byte are fill 1s */
+    if (r.cnt && ((r.byte & ((1u << r.cnt) - 1u)) != ((1u << r.cnt) - 1u))) return -1;
+    return r.pos == nbytes ? 0 : -1;
+}
+
 /* ------------------------------------------------------------------ partitions
  * Angle partition: round-robin -- node m holds angles a = m (mod M);
  * contiguous (config 1) -- consecutive blocks, the first n_ang mod M nodes one

@@ -9,9 +9,9 @@
 //     statistic);
 //   * a Lloyd step needs, for each threshold b_k, C_k = #{v <= b_k} and
 //     S_k = sum_{v <= b_k} fix(v): C_k is an upper bound in the sorted keys (binary
-//     search over the tile heads in shared memory, a warp ballot over the 32 chunk
-//     heads of that tile, then one warp counts inside one 64-key chunk),
-//     S_k = (exclusive prefix of the chunk sums) + the in-chunk part.
+//     search over the super-chunk heads held in shared memory, then one warp counts
+//     inside one super-chunk read from global memory),
+//     S_k = (exclusive prefix at the super-chunk start) + the in-chunk part.
 //     Cluster k = (b_{k-1}, b_k], i.e. label(v) = #{k : v > b_k}, ties to the lower
 //     cluster -- the same decision the oracle takes per element.
 // fix(v) = round(v 2^F) as int64 with F chosen from max|v| and n so no sum overflows:
@@ -34,6 +34,7 @@ constexpr int LT = 1024;              // threads of the Lloyd kernel
 constexpr int MAX_TILES = 4096;       // per payload (n <= 16.7 M)
 constexpr int KCH = 128;              // keys per prefix-sum chunk
 constexpr int CPT = KTILE / KCH;      // chunks per tile (32)
+constexpr int LSC_MAX = 8192;         // super-chunks resident in the Lloyd kernel's shared memory (32 * 32 * 8)
 static_assert(CPT == 32, "one warp lane per chunk head");
 
 __device__ __forceinline__ uint32_t f2key(float f) {
@@ -269,15 +270,24 @@ __global__ void __launch_bounds__(KT) km_csum(KmPtr w) {
     if (t == 0 && threadIdx.x == 0) w.fexp[b] = F;
 }
 
-__global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters) {
+// All Lloyd iterations of one payload in one CTA.  The sorted keys are split into
+// super-chunks of S = KCH << sh keys (sh chosen so at most LSC_MAX of them); their first
+// keys and the exclusive prefix of fix(v) at their starts live in shared memory, so a
+// threshold query is a shared-memory binary search plus ONE global read of one
+// super-chunk (S / 32 keys per lane), counted and summed by a warp.
+__global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters, int sh) {
     using Scan = cub::BlockScan<long long, LT>;
     __shared__ typename Scan::TempStorage tmp;
     extern __shared__ __align__(16) unsigned char lsm[];
-    long long *tpre = reinterpret_cast<long long *>(lsm);           // [T + 1] tile prefix of fix sums
-    uint32_t *thead = reinterpret_cast<uint32_t *>(tpre + w.T + 1);  // [T] first key of each tile
+    const int T = w.T;
+    const int S = KCH << sh;
+    const int NS = (int)(((long long)T * KTILE) >> (7 + sh));       // super-chunks (KCH == 2^7)
+    long long *tpre = reinterpret_cast<long long *>(lsm);            // [T + 1] tile prefix of fix sums
+    long long *spre = tpre + T + 1;                                   // [NS] prefix at super-chunk starts
+    uint32_t *shead = reinterpret_cast<uint32_t *>(spre + NS);        // [NS] first key of each super-chunk
     __shared__ float cen[256], thr[256];
     __shared__ long long Cs[256], Ss[256], total_s;
-    const int b = blockIdx.x, K = w.K, T = w.T;
+    const int b = blockIdx.x, K = w.K;
     const long long nv = w.nv, nch = (long long)T * CPT;
     const uint32_t *sorted = w.keysA + (long long)b * T * KTILE;
     const long long *cp = w.csum + (long long)b * nch;  // in-tile exclusive chunk prefix
@@ -301,64 +311,89 @@ __global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters) {
         }
         if (threadIdx.x == 0) total_s = carry;
     }
-    for (int t = threadIdx.x; t < T; t += LT) thead[t] = sorted[(long long)t * KTILE];
+    __syncthreads();
+    // super-chunk heads and prefixes: all global loads of a thread issued before any use
+    constexpr int SPT = LSC_MAX / LT;  // <= 8 super-chunks per thread
+    {
+        uint32_t hv[SPT];
+        long long pv[SPT];
+#pragma unroll
+        for (int u = 0; u < SPT; u++) {
+            const int c = threadIdx.x + u * LT;
+            const long long k0 = (long long)c * S;
+            const long long ci = k0 / KCH;  // chunk index = t * CPT + in-tile chunk
+            hv[u] = c < NS ? sorted[k0] : 0u;
+            pv[u] = c < NS ? cp[ci] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < SPT; u++) {
+            const int c = threadIdx.x + u * LT;
+            if (c < NS) {
+                shead[c] = hv[u];
+                spre[c] = tpre[(int)(((long long)c * S) / KTILE)] + pv[u];
+            }
+        }
+    }
     // quantile init: c_k = v_(floor((2k+1) nv / 2K))
     for (int k = threadIdx.x; k < K; k += LT) cen[k] = key2f(sorted[((long long)(2 * k + 1) * nv) / (2LL * K)]);
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int per_lane = S / 32;
     for (int it = 0; it < iters; it++) {
         for (int k = threadIdx.x; k + 1 < K; k += LT) thr[k] = (float)(((double)cen[k] + (double)cen[k + 1]) * 0.5);
         __syncthreads();
         // two thresholds per warp at a time: their dependent global loads overlap
         for (int k0 = warp; k0 + 1 < K; k0 += 2 * (LT / 32)) {
-            int kk[2], tt[2], cc[2];
-            uint32_t kb[2], h[2], e[2][KCH / 32];
-            long long pre[2];
+            int kk[2], cc[2];
+            uint32_t kb[2];
 #pragma unroll
             for (int q = 0; q < 2; q++) {
                 kk[q] = k0 + q * (LT / 32);
                 kb[q] = kk[q] + 1 < K ? f2key(thr[kk[q]]) : 0u;
-                int lo = 0, hi = T - 1, t = -1;  // last tile whose head key <= kb
-                while (lo <= hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (thead[mid] <= kb[q]) { t = mid; lo = mid + 1; } else hi = mid - 1;
+                // last super-chunk whose head key <= kb: warp-parallel search over strides
+                // 256, 8, 1 (heads are sorted; NS <= 8192 = 32 * 32 * 8)
+                int c = -1;
+                const int i1 = lane * 256;
+                const unsigned m1 = __ballot_sync(0xffffffffu, i1 < NS && shead[i1] <= kb[q]);
+                if (m1) {
+                    const int b1 = (31 - __clz(m1)) * 256;
+                    const int i2 = b1 + lane * 8;
+                    const unsigned m2 = __ballot_sync(0xffffffffu, i2 < NS && shead[i2] <= kb[q]);
+                    const int b2 = b1 + (31 - __clz(m2)) * 8;
+                    const int i3 = b2 + lane;
+                    const unsigned m3 = __ballot_sync(0xffffffffu, lane < 8 && i3 < NS && shead[i3] <= kb[q]);
+                    c = b2 + (31 - __clz(m3));
                 }
-                tt[q] = kk[q] + 1 < K ? t : -1;
+                cc[q] = kk[q] + 1 < K ? c : -1;
             }
+            int cnt[2] = {0, 0};
+            long long sm[2] = {0, 0};
+            for (int u0 = 0; u0 < per_lane; u0 += 4) {
+                uint32_t e[2][4];
 #pragma unroll
-            for (int q = 0; q < 2; q++) h[q] = tt[q] >= 0 ? sorted[(long long)tt[q] * KTILE + lane * KCH] : 0xffffffffu;
+                for (int q = 0; q < 2; q++)
 #pragma unroll
-            for (int q = 0; q < 2; q++) {
-                // last chunk of the tile whose head key <= kb (chunk 0 qualifies)
-                const unsigned m = __ballot_sync(0xffffffffu, h[q] <= kb[q]);
-                cc[q] = m ? 31 - __clz(m) : 0;
-                const long long cb = (long long)max(tt[q], 0) * KTILE + (long long)cc[q] * KCH;
+                    for (int u = 0; u < 4; u++)
+                        e[q][u] = cc[q] >= 0 ? sorted[(long long)cc[q] * S + 32 * (u0 + u) + lane] : 0xffffffffu;
 #pragma unroll
-                for (int u = 0; u < KCH / 32; u++) e[q][u] = tt[q] >= 0 ? sorted[cb + 32 * u + lane] : 0xffffffffu;
-                pre[q] = tt[q] >= 0 ? tpre[tt[q]] + cp[(long long)tt[q] * CPT + cc[q]] : 0;
-            }
+                for (int q = 0; q < 2; q++)
 #pragma unroll
-            for (int q = 0; q < 2; q++) {
-                if (kk[q] + 1 >= K) continue;
-                const long long cb = (long long)max(tt[q], 0) * KTILE + (long long)cc[q] * KCH;
-                int cnt = 0;
-                long long sm = 0;
-                if (tt[q] >= 0) {
-#pragma unroll
-                    for (int u = 0; u < KCH / 32; u++)
-                        if (e[q][u] <= kb[q] && cb + 32 * u + lane < nv) {
-                            cnt++;
-                            sm += __double2ll_rn((double)key2f(e[q][u]) * scale);
+                    for (int u = 0; u < 4; u++)
+                        if (cc[q] >= 0 && e[q][u] <= kb[q] && (long long)cc[q] * S + 32 * (u0 + u) + lane < nv) {
+                            cnt[q]++;
+                            sm[q] += __double2ll_rn((double)key2f(e[q][u]) * scale);
                         }
-                }
+            }
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
-                    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-                    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+                    cnt[q] += __shfl_xor_sync(0xffffffffu, cnt[q], o);
+                    sm[q] += __shfl_xor_sync(0xffffffffu, sm[q], o);
                 }
-                if (lane == 0) {
-                    Cs[kk[q]] = tt[q] >= 0 ? cb + cnt : 0;
-                    Ss[kk[q]] = tt[q] >= 0 ? pre[q] + sm : 0;
+                if (lane == 0 && kk[q] + 1 < K) {
+                    Cs[kk[q]] = cc[q] >= 0 ? (long long)cc[q] * S + cnt[q] : 0;
+                    Ss[kk[q]] = cc[q] >= 0 ? spre[cc[q]] + sm[q] : 0;
                 }
             }
         }
@@ -472,7 +507,15 @@ void with_bits(int B, F &&f) {
     }
 }
 
-size_t lloyd_smem(int T) { return sizeof(long long) * (T + 1) + sizeof(uint32_t) * T; }
+int lloyd_shift(int T) {
+    int sh = 0;
+    while ((((long long)T * KTILE) >> (7 + sh)) > LSC_MAX) sh++;
+    return sh;
+}
+size_t lloyd_smem(int T) {
+    const long long ns = ((long long)T * KTILE) >> (7 + lloyd_shift(T));
+    return sizeof(long long) * (T + 1 + ns) + sizeof(uint32_t) * ns;
+}
 
 }  // namespace
 
@@ -529,7 +572,7 @@ int kmeans_encode(const float *const *v, KmeansWork &ws, int lloyd, uint8_t *con
     }
     // four passes: A -> B -> A -> B -> A, sorted keys in keysA
     km_csum<<<tiles, KT, 0, st>>>(w);
-    km_lloyd<<<P, LT, lloyd_smem(ws.T), st>>>(w, lloyd);
+    km_lloyd<<<P, LT, lloyd_smem(ws.T), st>>>(w, lloyd, lloyd_shift(ws.T));
     long long want = std::max(1LL, (148LL * 8 + P - 1) / P);
     long long need = (ws.nv + KT * 16 - 1) / (KT * 16);
     const dim3 grid((unsigned)std::max(1LL, std::min(want, need)), P);

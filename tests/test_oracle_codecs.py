@@ -185,3 +185,141 @@ def test_dct_error_shrinks_with_quality():
         coef, mm = oracle.dct_encode(v, q)
         errs.append(np.sqrt(np.mean((oracle.dct_decode(coef, mm, 64, 64, q) - v) ** 2)))
     assert all(a > b for a, b in zip(errs, errs[1:]))
+
+
+# ----------------------------------------------------------------- JPEG entropy coding (NEXT-2)
+def _pil_jpeg(img, quality):
+    from PIL import Image
+    b = io.BytesIO()
+    Image.fromarray(np.asarray(img, np.uint8), "L").save(b, "JPEG", quality=quality)
+    return b.getvalue()
+
+
+def _jpeg_parts(data):
+    """Marker segments of a baseline JPEG file: DHT tables {(class, id): (bits, vals)} and
+    the entropy-coded segment after SOS (up to the EOI marker)."""
+    i, dht, ent = 2, {}, None
+    while i < len(data):
+        assert data[i] == 0xFF
+        m = data[i + 1]
+        if m == 0xD9:
+            break
+        L = data[i + 2] * 256 + data[i + 3]
+        body = data[i + 4:i + 2 + L]
+        if m == 0xC4:
+            j = 0
+            while j < len(body):
+                tc, th = body[j] >> 4, body[j] & 15
+                bits = np.frombuffer(body[j + 1:j + 17], np.uint8)
+                nv = int(bits.sum())
+                dht[(tc, th)] = (bits.copy(), np.frombuffer(body[j + 17:j + 17 + nv], np.uint8).copy())
+                j += 17 + nv
+        if m == 0xDA:
+            s = i + 2 + L
+            e = s
+            while not (data[e] == 0xFF and data[e + 1] not in (0x00,) and not 0xD0 <= data[e + 1] <= 0xD7):
+                e += 1
+            ent = data[s:e]
+            i = e
+            continue
+        i += 2 + L
+    return dht, ent
+
+
+def test_jpeg_huffman_tables_match_libjpeg():
+    """The oracle's Annex K tables equal the DHT segments libjpeg (via PIL) writes."""
+    dht, _ = _jpeg_parts(_pil_jpeg(np.zeros((8, 8)), 75))
+    dc_bits, dc_val, ac_bits, ac_val = oracle.jpeg_tables()
+    assert np.array_equal(dht[(0, 0)][0], dc_bits) and np.array_equal(dht[(0, 0)][1], dc_val)
+    assert np.array_equal(dht[(1, 0)][0], ac_bits) and np.array_equal(dht[(1, 0)][1], ac_val)
+
+
+def test_jpeg_hand_coded_blocks():
+    """T.81 by hand: an all-zero block = DC category 0 ('00') + EOB ('1010') + two fill
+    1s = 0x2B; DC +1 = '010' '1' + EOB = 0x5A; DC -1 = '010' '0' + EOB = 0x4A."""
+    z = np.zeros(64, np.int16)
+    assert oracle.jpeg_encode(z) == b"\x2b"
+    z[0] = 1
+    assert oracle.jpeg_encode(z) == b"\x5a"
+    z[0] = -1
+    assert oracle.jpeg_encode(z) == b"\x4a"
+
+
+@pytest.mark.parametrize("quality,shape,seed", [(50, (16, 24), 1), (75, (32, 32), 2), (95, (8, 64), 3),
+                                                (100, (24, 16), 4), (10, (40, 40), 5)])
+def test_jpeg_reencodes_libjpeg_entropy_segment(quality, shape, seed):
+    """libjpeg's entropy-coded segment decodes with the oracle and re-encodes to the same
+    bytes (Huffman codes, category bits, ZRL/EOB, byte stuffing, fill bits)."""
+    rng = np.random.default_rng(seed)
+    img = rng.integers(0, 256, size=shape)
+    img[: shape[0] // 2] = np.clip(img[: shape[0] // 2] // 8 + 100, 0, 255)  # smooth + noisy halves
+    _, ent = _jpeg_parts(_pil_jpeg(img, quality))
+    nb = shape[0] * shape[1] // 64
+    coef = oracle.jpeg_decode(ent, nb, 0)
+    assert oracle.jpeg_encode(coef, 0) == ent
+    if quality >= 95:  # long noisy streams: byte stuffing is exercised
+        assert b"\xff\x00" in ent
+
+
+def test_jpeg_zigzag_pinned_by_libjpeg_basis_images():
+    """Figure A.6 and the natural layout: libjpeg (quality 100, all-ones table) codes the
+    DCT basis image of vertical frequency a, horizontal frequency b with its dominant
+    coefficient at natural index 8a + b of the oracle's decode."""
+    x = np.arange(8)
+    for a in range(8):
+        for b in range(8):
+            if a == b == 0:
+                continue
+            basis = np.outer(np.cos((2 * x + 1) * a * np.pi / 16), np.cos((2 * x + 1) * b * np.pi / 16))
+            img = np.clip(np.rint(128 + 100 * basis), 0, 255)
+            _, ent = _jpeg_parts(_pil_jpeg(img, 100))
+            c = oracle.jpeg_decode(ent, 1, 0).astype(np.int64)
+            ac = c.copy()
+            ac[0] = 0
+            assert int(np.argmax(np.abs(ac))) == 8 * a + b, (a, b)
+    z = oracle.jpeg_zigzag()
+    assert sorted(z.tolist()) == list(range(64)) and z[1] == 1 and z[2] == 8 and z[63] == 63
+
+
+@pytest.mark.parametrize("restart", [0, 1, 3, 8])
+def test_jpeg_restart_roundtrip_and_markers(restart):
+    rng = np.random.default_rng(10 + restart)
+    nb = 45
+    c = (rng.integers(-40, 41, size=nb * 64) * (rng.random(nb * 64) < 0.2)).astype(np.int16)
+    c[::64] = rng.integers(-1024, 1017, size=nb)  # DC differences up to 11 bits
+    s = oracle.jpeg_encode(c, restart)
+    assert np.array_equal(oracle.jpeg_decode(s, nb, restart), c)
+    # RSTm markers: one per interval boundary, m cycling 0..7 (F.1.4.4 / B.2.1)
+    marks = [s[i + 1] for i in range(len(s) - 1) if s[i] == 0xFF and 0xD0 <= s[i + 1] <= 0xD7]
+    n_int = 0 if restart == 0 else (nb + restart - 1) // restart - 1
+    assert marks == [0xD0 + (k % 8) for k in range(n_int)]
+    # every 0xFF data byte is stuffed
+    for i in range(len(s) - 1):
+        if s[i] == 0xFF:
+            assert s[i + 1] == 0x00 or 0xD0 <= s[i + 1] <= 0xD7
+    # a restart resets the DC predictor: interval k's first block codes its DC absolutely,
+    # so each interval decodes alone
+    if restart:
+        parts = s.split(b"\xff\xd0")[0] if n_int else s
+        first = oracle.jpeg_decode(parts, min(restart, nb), restart)
+        assert np.array_equal(first, c[:64 * min(restart, nb)])
+
+
+def test_jpeg_extreme_values_and_runs():
+    """AC +-1023 (category 10), DC jumps of 2040 (category 11), runs of 15, 16, 17 and 62
+    zeros (ZRL), a non-zero last coefficient (no EOB), an all-zero block."""
+    zz = oracle.jpeg_zigzag()
+    blocks = []
+    b = np.zeros(64, np.int16); b[0] = -1024; b[zz[1]] = 1023; b[zz[17]] = -1023; blocks.append(b)
+    b = np.zeros(64, np.int16); b[0] = 1016; b[zz[63]] = 5; blocks.append(b)
+    b = np.zeros(64, np.int16); b[zz[16]] = 1; b[zz[33]] = -2; b[zz[51]] = 3; blocks.append(b)
+    blocks.append(np.zeros(64, np.int16))
+    b = np.zeros(64, np.int16); b[zz[63]] = -1; blocks.append(b)
+    c = np.concatenate(blocks)
+    for r in (0, 2):
+        assert np.array_equal(oracle.jpeg_decode(oracle.jpeg_encode(c, r), len(blocks), r), c)
+    bad = np.zeros(64, np.int16); bad[1] = 1024  # outside the baseline AC categories
+    with pytest.raises(ValueError):
+        oracle.jpeg_encode(bad)
+    with pytest.raises(ValueError):
+        oracle.jpeg_decode(b"\x2b\x00", 1, 0)  # trailing garbage
