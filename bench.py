@@ -123,6 +123,38 @@ def projector_c5_geometry(tomoq, torch, stream, reps=5):
     return out
 
 
+def dct_entropy_c3(tomoq, torch, stream, reps=10, restart=4):
+    """NEXT-2 measurement on config 3 as stated (16 nodes x 512^2, 4x4 torus, DCT q50):
+    the DCT-J encode stage (tq_launch_component 4: min/max, integer DCT, quantisation and,
+    with JPEG entropy coding, Huffman coding of every local payload) timed with events,
+    and the payload bytes per ADMM iteration with and without entropy coding (after 3
+    iterations from zero, synthetic phantom data)."""
+    from paper_2410_06106_b200 import configs as C
+    cfg = C.C3()
+    inp = C.make_inputs(cfg, with_truth=False)
+    out = {"workload": "C3: 16 nodes x 512^2, DCT q50, restart interval %d blocks" % restart}
+    for R in (0, restart):
+        ctx = tomoq.Context(cfg.N, cfg.n_angles, cfg.n_det, cfg.nodes, inp.edges, split=cfg.split, rule=cfg.rule)
+        ctx.set_params(cfg.rho, inner=cfg.inner, e1=cfg.e1)
+        ctx.set_quantizer(cfg.quant, quality=cfg.quality, jpeg_restart=R)
+        ctx.set_sinogram(0, torch.tensor(inp.sino[0], device="cuda"))
+        ctx.run(3)
+        ctx.launch_component(4, 2, stream)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        units = ctx.launch_component(4, reps, stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = a.elapsed_time(b) / reps
+        key = "entropy" if R else "plain"
+        out[key] = {"encode_us": t * 1e3, "pixels_per_s": units / (t / 1e3),
+                    "payload_bytes_per_iter": ctx.stats()["payload_bytes_logical"]}
+        ctx.close()
+    out["compression_vs_plain"] = out["plain"]["payload_bytes_per_iter"] / out["entropy"]["payload_bytes_per_iter"]
+    return out
+
+
 def cpu_baseline(cfg_g1, iters=2):
     """The fp64 oracle as it stands, on the host cores, on a bounded sample: `iters`
     ADMM iterations of the per-GPU share of the workload (config 4 at G = 1)."""
@@ -317,6 +349,13 @@ def main():
             c5_geom = projector_c5_geometry(tomoq, torch, stream, reps=5)
         except Exception as exc:  # report, never fail the bench line
             c5_geom = {"error": str(exc)[:200]}
+    # ---- NEXT-2: JPEG entropy coding of the DCT payloads on config 3 (context, not the headline)
+    jpeg_c3 = None
+    if rank == 0 and not args.no_c5_geometry:
+        try:
+            jpeg_c3 = dct_entropy_c3(tomoq, torch, stream)
+        except Exception as exc:
+            jpeg_c3 = {"error": str(exc)[:200]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -333,6 +372,7 @@ def main():
             "vu_per_step": vu_it,
             "roofline": roofline,
             "projector_c5_geometry": c5_geom,
+            "dct_entropy_c3": jpeg_c3,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(sino_host.numel() * 4),
                     "d2h_bytes_per_step": int(cfg.N * cfg.N * 4), "ms_per_step": max(e2e_ms, e2e_wall) / args.steps},

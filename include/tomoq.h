@@ -85,6 +85,10 @@ typedef struct {
     int32_t lloyd_iters;  /* Lloyd iterations after the quantile init (R-16) */
     int32_t quality;      /* DCT quality 1..100, IJG scaling of the Annex K table (R-18) */
     int32_t keep_labels;  /* 1: keep the last K-means labels for tq_export_labels (parity) */
+    int32_t jpeg_restart; /* DCT payloads: 0 = plain int16 coefficients; R >= 1 = baseline JPEG
+                             Huffman entropy coding (T.81 Annex F, Annex K luminance tables)
+                             with an RSTm marker every R 8x8 blocks;
+                             lossless, so iterates are unchanged; payload bytes shrink */
 } tq_quant;
 
 typedef struct {
@@ -195,6 +199,22 @@ tq_status tq_dct_encode(const float *v, int32_t rows, int32_t cols, int32_t qual
                         int16_t *coef, float *minmax, void *stream);
 tq_status tq_dct_decode(const int16_t *coef, const float *minmax, int32_t rows, int32_t cols,
                         int32_t quality, float *out, void *stream);
+/* Baseline JPEG Huffman entropy coding (ITU-T T.81 Annex C code
+ * generation, F.1.2 DC-difference / AC run-length coding with ZRL and EOB, F.1.2.3 byte
+ * stuffing and 1-fill, F.1.4.4 RSTm markers every `restart` >= 1 blocks with the DC
+ * predictor reset; Annex K Tables K.3 / K.5 luminance Huffman tables; R-25) of
+ * n_blocks 8x8 blocks of coefficients in the order tq_dct_encode writes them (raster
+ * blocks, natural order inside a block).  Device pointers, caller-owned.
+ * Encode writes the entropy-coded segment (no JPEG headers) to out[cap] and its length to
+ * *nbytes (host pointer); TQ_EINVAL if a value lies outside the baseline categories (DC
+ * difference > 11 bits, AC > 10 bits), or if the stream would exceed 2 bytes per
+ * coefficient or cap.  Decode reads nbytes of such a segment and writes the
+ * coefficients; TQ_EINVAL on a malformed stream (bad code, missing or misnumbered RSTm,
+ * truncated data).  Both synchronise the stream. */
+tq_status tq_jpeg_encode(const int16_t *coef, int64_t n_blocks, int32_t restart, uint8_t *out,
+                         int64_t cap, int64_t *nbytes, void *stream);
+tq_status tq_jpeg_decode(const uint8_t *in, int64_t nbytes, int64_t n_blocks, int32_t restart,
+                         int16_t *coef, void *stream);
 
 #ifdef __cplusplus
 }

@@ -389,4 +389,57 @@ tq_status tq_dct_decode(const int16_t *coef, const float *minmax, int32_t rows, 
     });
 }
 
+tq_status tq_jpeg_encode(const int16_t *coef, int64_t n_blocks, int32_t restart, uint8_t *out, int64_t cap,
+                         int64_t *nbytes, void *stream) {
+    return guard(nullptr, [&] {
+        TQ_REQUIRE(coef && out && nbytes && n_blocks >= 1 && restart >= 1 && cap >= 0, "bad jpeg arguments");
+        cudaStream_t st = (cudaStream_t)stream;
+        DevTmp t;
+        const long long nv = 64LL * n_blocks;
+        uint8_t *pay = (uint8_t *)t.get(jpeg_payload_bytes(nv));
+        TQ_CHECK_CUDA(cudaMemsetAsync(pay, 0, 8, st));
+        uint8_t **pt = t.up(&pay, 1);
+        JpegWork w;
+        w.alloc(1, nv, restart);
+        TQ_CHECK_CUDA(cudaMemcpyAsync(w.coef, coef, 2 * nv, cudaMemcpyDeviceToDevice, st));
+        jpeg_encode(pt, w, st);
+        unsigned stat[2];
+        TQ_CHECK_CUDA(cudaMemcpyAsync(stat, w.status, sizeof stat, cudaMemcpyDeviceToHost, st));
+        TQ_CHECK_CUDA(cudaStreamSynchronize(st));
+        w.release();
+        TQ_REQUIRE(stat[1] == 0, "jpeg: a coefficient lies outside the baseline categories");
+        TQ_REQUIRE(!(stat[0] & 0x80000000u), "jpeg: stream would exceed 2 bytes per coefficient");
+        const long long n = stat[0];
+        TQ_REQUIRE(n <= cap, "jpeg: output capacity too small");
+        *nbytes = n;
+        TQ_CHECK_CUDA(cudaMemcpyAsync(out, pay + 16, n, cudaMemcpyDeviceToDevice, st));
+        TQ_CHECK_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+tq_status tq_jpeg_decode(const uint8_t *in, int64_t nbytes, int64_t n_blocks, int32_t restart, int16_t *coef,
+                         void *stream) {
+    return guard(nullptr, [&] {
+        TQ_REQUIRE(in && coef && n_blocks >= 1 && restart >= 1 && nbytes >= 0 && nbytes < (1LL << 31),
+                   "bad jpeg arguments");
+        cudaStream_t st = (cudaStream_t)stream;
+        DevTmp t;
+        const long long nv = 64LL * n_blocks;
+        uint8_t *pay = (uint8_t *)t.get(16 + std::max<long long>(nbytes, 2 * nv));
+        const uint32_t hdr[4] = {0u, 0u, (uint32_t)nbytes, (uint32_t)n_blocks};
+        TQ_CHECK_CUDA(cudaMemcpyAsync(pay, hdr, sizeof hdr, cudaMemcpyHostToDevice, st));
+        TQ_CHECK_CUDA(cudaMemcpyAsync(pay + 16, in, nbytes, cudaMemcpyDeviceToDevice, st));
+        uint8_t **pt = t.up(&pay, 1);
+        JpegWork w;
+        w.alloc(1, nv, restart);
+        jpeg_decode(pt, w, st);
+        unsigned stat[2];
+        TQ_CHECK_CUDA(cudaMemcpyAsync(stat, w.status, sizeof stat, cudaMemcpyDeviceToHost, st));
+        TQ_CHECK_CUDA(cudaMemcpyAsync(coef, w.coef, 2 * nv, cudaMemcpyDeviceToDevice, st));
+        TQ_CHECK_CUDA(cudaStreamSynchronize(st));
+        w.release();
+        TQ_REQUIRE(stat[1] == 0, "jpeg: malformed entropy-coded stream");
+    });
+}
+
 }  // extern "C"

@@ -55,10 +55,36 @@ struct DctWork {
     void alloc(int P, long long nv);
     void release();
 };
+
+// Baseline JPEG Huffman entropy coding of the DCT coefficients (SURVEY NEXT-2, T.81
+// Annex F with the Annex K luminance tables, an RSTm marker every R blocks; R-25).
+// Entropy payload: [mn f32][mx f32][u32 nbytes | raw flag bit 31][u32 blocks] then the
+// entropy-coded segment -- or, when it would exceed the 2 nv bytes of the plain
+// coefficients (raw flag), the int16 coefficients.  Capacity 16 + 2 nv bytes.
+struct JpegWork {
+    int P = 0, R = 0, nint = 0;
+    long long nv = 0;
+    int16_t *coef = nullptr;        // [P][nv] coefficients (encode input / decode output)
+    long long *len = nullptr;       // [P][nint] interval bytes (encode)
+    long long *off = nullptr;       // [P][nint] interval offsets (encode) / starts (decode)
+    unsigned *status = nullptr;     // [P][2]: header word, error bits (1 category, 2 markers, 4 code, 8 overrun)
+    long long *enc_bytes = nullptr; // [P] payload bytes of the last encode (header included)
+    void alloc(int P, long long nv, int R);
+    void release();
+};
+long long jpeg_payload_bytes(long long nv);
+int jpeg_intervals(long long nv, int R);
+// pay[b]: payload with mn/mx in bytes 0..7 already; coefficients in w.coef
+int jpeg_encode(uint8_t *const *pay, JpegWork &w, cudaStream_t st);
+// coefficients of the payloads into w.coef (status bits set on a malformed stream)
+int jpeg_decode(uint8_t *const *pay, JpegWork &w, cudaStream_t st);
+
+// jw == nullptr: plain payload [mn][mx][int16 coefficients]; otherwise the entropy
+// payload above, the coefficients passing through jw->coef
 int dct_encode(const float *const *vin, int P, int rows, int cols, int quality, DctWork &ws,
-               uint8_t *const *pay, cudaStream_t st);
+               uint8_t *const *pay, cudaStream_t st, JpegWork *jw = nullptr);
 int dct_decode(const uint8_t *const *pay, int P, int rows, int cols, int quality, int prec,
-               void *const *out, cudaStream_t st);
+               void *const *out, cudaStream_t st, JpegWork *jw = nullptr);
 
 // host reference tables (independent of the oracle): Annex K table scaled to quality,
 // and the integer DCT matrix round(2^14 alpha(u) cos((2x+1) u pi / 16))

@@ -71,7 +71,8 @@ __global__ void __launch_bounds__(DT) dct_minmax(const float *const *vin, long l
 }
 
 __global__ void __launch_bounds__(DT) dct_enc(const float *const *vin, int rows, int cols,
-                                              const float *mm, DctTables tab, uint8_t *const *pay) {
+                                              const float *mm, DctTables tab, uint8_t *const *pay,
+                                              int16_t *coef_base) {
     __shared__ int Ts[BLK_PER_CTA][8][9];
     __shared__ int Cs[64], Qs[64];
     if (threadIdx.x < 64) { Cs[threadIdx.x] = tab.C[threadIdx.x]; Qs[threadIdx.x] = tab.Q[threadIdx.x]; }
@@ -106,7 +107,8 @@ __global__ void __launch_bounds__(DT) dct_enc(const float *const *vin, int rows,
     }
     __syncwarp();
     if (!active) return;
-    int16_t *out = reinterpret_cast<int16_t *>(pay[b] + 8) + blk * 64;
+    int16_t *out = (coef_base ? coef_base + (long long)b * rows * cols : reinterpret_cast<int16_t *>(pay[b] + 8)) +
+                   blk * 64;
     const int w = lane8;  // column pass: lane = column w
 #pragma unroll
     for (int u = 0; u < 8; u++) {
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(DT) dct_enc(const float *const *vin, int rows,
 
 template <typename T>
 __global__ void __launch_bounds__(DT) dct_dec(const uint8_t *const *pay, int rows, int cols,
-                                              DctTables tab, T *const *outp) {
+                                              DctTables tab, T *const *outp, const int16_t *coef_base) {
     __shared__ long long Ts[BLK_PER_CTA][8][9];
     __shared__ int Cs[64], Qs[64];
     if (threadIdx.x < 64) { Cs[threadIdx.x] = tab.C[threadIdx.x]; Qs[threadIdx.x] = tab.Q[threadIdx.x]; }
@@ -140,7 +142,9 @@ __global__ void __launch_bounds__(DT) dct_dec(const uint8_t *const *pay, int row
     const float *hdr = reinterpret_cast<const float *>(pay[b]);
     const float mn = hdr[0], mx = hdr[1];
     if (active) {
-        const int16_t *in = reinterpret_cast<const int16_t *>(pay[b] + 8) + blk * 64;
+        const int16_t *in = (coef_base ? coef_base + (long long)b * rows * cols
+                                       : reinterpret_cast<const int16_t *>(pay[b] + 8)) +
+                            blk * 64;
         const int w = lane8;  // pass 1, lane = column w: T'[x][w] = rs(sum_u C[u][x] G[u][w], 10)
         long long G[8];
 #pragma unroll
@@ -203,7 +207,7 @@ void DctWork::release() {
 }
 
 int dct_encode(const float *const *vin, int P, int rows, int cols, int quality, DctWork &ws,
-               uint8_t *const *pay, cudaStream_t st) {
+               uint8_t *const *pay, cudaStream_t st, JpegWork *jw) {
     if (P == 0) return 0;
     TQ_REQUIRE(rows % 8 == 0 && cols % 8 == 0 && rows > 0, "dct: rows and cols must be multiples of 8");
     const long long nv = (long long)rows * cols;
@@ -212,24 +216,27 @@ int dct_encode(const float *const *vin, int P, int rows, int cols, int quality, 
                                                  ws.minmax);
     const DctTables tab = make_tables(quality);
     const long long nblk = nv / 64;
-    dct_enc<<<dim3(ceil_div(nblk, BLK_PER_CTA), P), DT, 0, st>>>(vin, rows, cols, ws.minmax, tab, pay);
+    dct_enc<<<dim3(ceil_div(nblk, BLK_PER_CTA), P), DT, 0, st>>>(vin, rows, cols, ws.minmax, tab, pay,
+                                                                  jw ? jw->coef : nullptr);
     TQ_CHECK_CUDA(cudaGetLastError());
-    return 2;
+    return 2 + (jw ? jpeg_encode(pay, *jw, st) : 0);
 }
 
 int dct_decode(const uint8_t *const *pay, int P, int rows, int cols, int quality, int prec,
-               void *const *out, cudaStream_t st) {
+               void *const *out, cudaStream_t st, JpegWork *jw) {
     if (P == 0) return 0;
+    const int kj = jw ? jpeg_decode(const_cast<uint8_t *const *>(pay), *jw, st) : 0;
     TQ_REQUIRE(rows % 8 == 0 && cols % 8 == 0 && rows > 0, "dct: rows and cols must be multiples of 8");
     const DctTables tab = make_tables(quality);
     const long long nblk = (long long)rows * cols / 64;
     const dim3 grid(ceil_div(nblk, BLK_PER_CTA), P);
+    const int16_t *cb = jw ? jw->coef : nullptr;
     if (prec == 0)
-        dct_dec<float><<<grid, DT, 0, st>>>(pay, rows, cols, tab, (float *const *)out);
+        dct_dec<float><<<grid, DT, 0, st>>>(pay, rows, cols, tab, (float *const *)out, cb);
     else
-        dct_dec<double><<<grid, DT, 0, st>>>(pay, rows, cols, tab, (double *const *)out);
+        dct_dec<double><<<grid, DT, 0, st>>>(pay, rows, cols, tab, (double *const *)out, cb);
     TQ_CHECK_CUDA(cudaGetLastError());
-    return 1;
+    return 1 + kj;
 }
 
 }  // namespace tq

@@ -114,6 +114,10 @@ int Ctx::local(int slice, int node) const {
     return loc_of[(size_t)slice * M + node];
 }
 
+long long Ctx::dct_bytes(long long nv) const {
+    return q.jpeg_restart > 0 ? jpeg_payload_bytes(nv) : dct_payload_bytes(nv);
+}
+
 int Ctx::kind_of_slice(int s) const {
     if (q.kind == TQ_Q_ALTERNATE) return (s % 2 == 0) ? TQ_Q_KMEANS : TQ_Q_DCT;
     return q.kind;
@@ -223,6 +227,10 @@ void Ctx::free_exchange() {
     owned.clear();
     kmw.release();
     dctw.release();
+    jenc.release();
+    jdec.release();
+    jmult.clear();
+    logical_fixed = 0;
     pays.clear();
     pay_of.clear();
     for (auto &b : enc) b = Batch();
@@ -290,6 +298,7 @@ void Ctx::set_quant(const tq_quant &qq) {
     const bool dc = qq.kind == TQ_Q_DCT || qq.kind == TQ_Q_ALTERNATE;
     if (km) TQ_REQUIRE(qq.k >= 1 && qq.k <= 256 && qq.lloyd_iters >= 0, "kmeans: k in [1,256], lloyd >= 0");
     if (dc) TQ_REQUIRE(qq.quality >= 1 && qq.quality <= 100, "dct: quality in [1,100]");
+    TQ_REQUIRE(qq.jpeg_restart >= 0 && qq.jpeg_restart <= (1 << 20), "jpeg_restart must be in [0, 2^20]");
     if (segmented() && qq.kind != TQ_Q_NONE) {
         TQ_REQUIRE(N % M == 0, "paper/consensus rule with a quantizer needs equal segments (M | N)");
         if (dc) TQ_REQUIRE((N / M) % 8 == 0, "paper/consensus rule with DCT needs 8 | N/M");
@@ -373,7 +382,7 @@ long long Ctx::launch_component(int component, int reps, cudaStream_t s) {
             for (int r = 0; r < reps; r++) {
                 if (E.need_conv) launch_to_float(prec, E.conv_src_d, E.conv_dst_d, n, (int)E.conv_src.size(), s);
                 if (kd == TQ_Q_KMEANS) kmeans_encode(E.vin, kmw, q.lloyd_iters, E.pay, E.labels, s, E.dec_out, prec);
-                else dct_encode(E.vin, E.P, segmented() ? N / M : N, N, q.quality, dctw, E.pay, s);
+                else dct_encode(E.vin, E.P, segmented() ? N / M : N, N, q.quality, dctw, E.pay, s, jw_enc());
             }
             return (long long)E.P * payload_len;
         }
@@ -427,7 +436,7 @@ void Ctx::setup_exchange() {
                 xh[k] = p.buf;
             }
         } else {
-            pbytes[k] = p.kind == TQ_Q_KMEANS ? kmeans_payload_bytes(q.k, payload_len) : dct_payload_bytes(payload_len);
+            pbytes[k] = p.kind == TQ_Q_KMEANS ? kmeans_payload_bytes(q.k, payload_len) : dct_bytes(payload_len);
             p.buf = (uint8_t *)dev_alloc(pbytes[k]);
             if (paper) {
                 outp[k] = (uint8_t *)XG + es * ((long long)p.slice * n + (long long)row_off[p.node] * N);
@@ -504,8 +513,12 @@ void Ctx::setup_exchange() {
                 E.conv_dst_d = (float **)upload(cdst.data(), sizeof(void *) * cdst.size());
             }
             if (kd == TQ_Q_KMEANS) kmw.alloc(E.P, q.k, payload_len);
-            else dctw.alloc(E.P, payload_len);
+            else {
+                dctw.alloc(E.P, payload_len);
+                if (q.jpeg_restart > 0) jenc.alloc(E.P, payload_len, q.jpeg_restart);
+            }
         }
+        if (kd == TQ_Q_DCT && D.P && q.jpeg_restart > 0) jdec.alloc(D.P, payload_len, q.jpeg_restart);
         if (D.P) {
             D.pay = (uint8_t **)upload(pd.data(), sizeof(void *) * D.P);
             D.out = (void **)upload(out.data(), sizeof(void *) * D.P);
@@ -570,15 +583,26 @@ void Ctx::setup_exchange() {
         }
     }
     // ---- logical bytes (what the method sends, independent of placement)
+    // (entropy-coded DCT payloads: capacity until a run reports their actual sizes)
     long long logical = 0;
     for (int i = 0; i < L; i++) {
         const int kd = kind_of_slice(loc[i].first), m = loc[i].second;
         const long long len = paper ? (long long)(row_off[m + 1] - row_off[m]) * N : n;
         const long long pb = kd == TQ_Q_NONE ? (long long)es * len
                              : kd == TQ_Q_KMEANS ? kmeans_payload_bytes(q.k, payload_len)
-                                                 : dct_payload_bytes(payload_len);
-        logical += pb * (paper ? (M - 1) : (long long)adj[m].size());
+                                                 : dct_bytes(payload_len);
+        const long long mult = paper ? (M - 1) : (long long)adj[m].size();
+        logical += pb * mult;
         if (rule == TQ_RULE_CONSENSUS) logical += 8LL * (n - len);  // fp64 sums of the other segments
+        if (kd == TQ_Q_DCT && q.jpeg_restart > 0) logical_fixed -= pb * mult;
+    }
+    logical_fixed += logical;
+    if (jenc.P) {
+        Batch &E = enc[TQ_Q_DCT];
+        for (int k : E.members) {
+            const int m = pays[k].node;
+            jmult.push_back(paper ? (M - 1) : (long long)adj[m].size());
+        }
     }
     st.payload_bytes_logical = logical;
     st.nccl_bytes_sent = 0;
@@ -609,7 +633,7 @@ int Ctx::stage(int id, cudaStream_t s) {
         if (kd == TQ_Q_KMEANS) k += kmeans_encode(E.vin, kmw, q.lloyd_iters, E.pay, E.labels, s, E.dec_out, prec);
         else {
             const int rows = segmented() ? N / M : N;
-            k += dct_encode(E.vin, E.P, rows, N, q.quality, dctw, E.pay, s);
+            k += dct_encode(E.vin, E.P, rows, N, q.quality, dctw, E.pay, s, jw_enc());
         }
     }
     return k;
@@ -649,7 +673,7 @@ int Ctx::phase_b(cudaStream_t s) {
         if (kd == TQ_Q_KMEANS) k += kmeans_decode(D.pay, D.P, payload_len, q.k, prec, D.out, s);
         else {
             const int rows = segmented() ? N / M : N;
-            k += dct_decode(D.pay, D.P, rows, N, q.quality, prec, D.out, s);
+            k += dct_decode(D.pay, D.P, rows, N, q.quality, prec, D.out, s, jdec.P ? &jdec : nullptr);
         }
     }
     if (rule == TQ_RULE_GRAPH)
@@ -728,6 +752,17 @@ void Ctx::run(int iters, cudaStream_t user) {
     for (int i = 0; i < L; i++) {
         const double nrm = sqrt(sc[(size_t)i * S_NSLOT + S_NORM]);
         if (!(nrm <= 1e12)) fail(TQ_EDIVERGED, "node iterate norm exceeded 1e12 (diverged)");
+    }
+    if (iters > 0 && (jenc.P || jdec.P)) {  // entropy-coded DCT payloads: actual sizes, stream checks
+        std::vector<long long> eb(std::max(1, jenc.P));
+        std::vector<unsigned> sd(2 * std::max(1, jdec.P), 0u);
+        if (jenc.P) TQ_CHECK_CUDA(cudaMemcpy(eb.data(), jenc.enc_bytes, sizeof(long long) * jenc.P, cudaMemcpyDeviceToHost));
+        if (jdec.P) TQ_CHECK_CUDA(cudaMemcpy(sd.data(), jdec.status, sizeof(unsigned) * 2 * jdec.P, cudaMemcpyDeviceToHost));
+        long long logical = logical_fixed;
+        for (int b = 0; b < jenc.P; b++) logical += eb[b] * jmult[b];
+        st.payload_bytes_logical = logical;
+        for (int b = 0; b < jdec.P; b++)
+            if (sd[2 * b + 1]) fail(TQ_ECUDA, "malformed JPEG entropy stream in a received DCT payload");
     }
 }
 

@@ -56,12 +56,14 @@ struct Ctx {
     tq_params prm{};
     std::vector<double> eta1;
     bool have_params = false;
-    tq_quant q{TQ_Q_NONE, 16, 10, 50};
+    tq_quant q{TQ_Q_NONE, 16, 10, 50, 0, 0};
     std::vector<char> sino_set;
     bool need_rhs = false;      // recompute b' from the state before the next iteration
     // ---- quantizer / exchange state (rebuilt by setup_exchange)
     bool xready = false;
     int kind_of_slice(int s) const;
+    long long dct_bytes(long long nv) const;   // payload capacity of a DCT payload
+    JpegWork *jw_enc() { return jenc.P ? &jenc : nullptr; }
     long long payload_len = 0;                // elements per payload (n or segment)
     struct Pay { int slice, node; uint8_t *buf; bool local; int kind; };
     std::vector<Pay> pays;                    // every payload this rank touches
@@ -84,6 +86,9 @@ struct Ctx {
     Batch enc[3], dec[3];
     KmeansWork kmw;
     DctWork dctw;
+    JpegWork jenc, jdec;                      // DCT entropy coding (q.jpeg_restart > 0)
+    long long logical_fixed = 0;              // logical bytes of the fixed-size payloads
+    std::vector<long long> jmult;             // per jenc payload: times it is sent per iteration
     float *fstage = nullptr;                  // float staging for quantizer inputs
     int32_t *labels_buf = nullptr;            // [L][payload_len] when keep_labels
     std::vector<int> label_row;               // local idx -> row in labels_buf or -1

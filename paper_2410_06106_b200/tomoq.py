@@ -45,7 +45,7 @@ class Params(C.Structure):
 
 class Quant(C.Structure):
     _fields_ = [("kind", C.c_int32), ("k", C.c_int32), ("lloyd_iters", C.c_int32),
-                ("quality", C.c_int32), ("keep_labels", C.c_int32)]
+                ("quality", C.c_int32), ("keep_labels", C.c_int32), ("jpeg_restart", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -79,6 +79,8 @@ _SIGS = {
     "tq_kmeans_decode": [_vp, _vp, _i64, _i32, _vp, _vp],
     "tq_dct_encode": [_vp, _i32, _i32, _i32, _vp, _vp, _vp],
     "tq_dct_decode": [_vp, _vp, _i32, _i32, _i32, _vp, _vp],
+    "tq_jpeg_encode": [_vp, _i64, _i32, _vp, _i64, C.POINTER(C.c_int64), _vp],
+    "tq_jpeg_decode": [_vp, _i64, _i64, _i32, _vp, _vp],
 }
 
 
@@ -190,8 +192,8 @@ class Context:
                    e2, eta2)
         self._c(lib().tq_set_params(self.h, C.byref(p)))
 
-    def set_quantizer(self, kind, k=16, lloyd=10, quality=50, keep_labels=False):
-        q = Quant(kind, k, lloyd, quality, int(bool(keep_labels)))
+    def set_quantizer(self, kind, k=16, lloyd=10, quality=50, keep_labels=False, jpeg_restart=0):
+        q = Quant(kind, k, lloyd, quality, int(bool(keep_labels)), int(jpeg_restart))
         self._c(lib().tq_set_quantizer(self.h, C.byref(q)))
 
     def set_sinogram(self, slice_, sino, node=-1):
@@ -334,6 +336,27 @@ def dct_encode(v, quality, stream=None):
     _check(lib().tq_dct_encode(v.contiguous().data_ptr(), rows, cols, quality, coef.data_ptr(),
                                mm.data_ptr(), _stream(stream)))
     return coef, mm
+
+
+def jpeg_encode(coef, restart, stream=None):
+    """Baseline JPEG Huffman entropy coding of int16 coefficient blocks (device tensor,
+    tq_dct_encode order) with an RSTm marker every `restart` blocks -> uint8 device tensor."""
+    import torch
+    coef = coef.contiguous().view(-1)
+    nb = coef.numel() // 64
+    cap = 2 * coef.numel()
+    out = torch.empty(max(1, cap), dtype=torch.uint8, device=coef.device)
+    n = C.c_int64()
+    _check(lib().tq_jpeg_encode(coef.data_ptr(), nb, restart, out.data_ptr(), cap, C.byref(n), _stream(stream)))
+    return out[:n.value]
+
+
+def jpeg_decode(stream_bytes, n_blocks, restart, stream=None):
+    import torch
+    coef = torch.empty(64 * n_blocks, dtype=torch.int16, device=stream_bytes.device)
+    _check(lib().tq_jpeg_decode(stream_bytes.contiguous().data_ptr(), stream_bytes.numel(), n_blocks, restart,
+                                coef.data_ptr(), _stream(stream)))
+    return coef
 
 
 def dct_decode(coef, mm, rows, cols, quality, stream=None):

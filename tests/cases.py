@@ -19,7 +19,8 @@ def gpu_context(cfg, inp, precision=0, keep_labels=False, eta1=None):
     ctx = tomoq.Context(cfg.N, cfg.n_angles, cfg.n_det, cfg.nodes, inp.edges, split=cfg.split,
                         rule=cfg.rule, n_slices=len(inp.sino), precision=precision)
     ctx.set_params(cfg.rho, inner=cfg.inner, e1=cfg.e1, eta1=eta1, e2=cfg.e2, eta2=cfg.eta2)
-    ctx.set_quantizer(cfg.quant, k=cfg.k, lloyd=cfg.lloyd, quality=cfg.quality, keep_labels=keep_labels)
+    ctx.set_quantizer(cfg.quant, k=cfg.k, lloyd=cfg.lloyd, quality=cfg.quality, keep_labels=keep_labels,
+                      jpeg_restart=cfg.jpeg_restart)
     for s, d in enumerate(inp.sino):
         ctx.set_sinogram(s, d)
     return ctx

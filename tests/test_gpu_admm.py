@@ -268,3 +268,37 @@ def test_stats_bytes_match_model():
     deg = 2  # ring
     assert st["payload_bytes_logical"] == cfg.nodes * deg * tomoq.payload_bytes(C.Q_KMEANS, cfg.k, cfg.N ** 2)
     assert st["kernel_launches"] > 0 and st["ms_last_run"] > 0
+
+
+@pytest.mark.parametrize("rule", [C.RULE_GRAPH, C.RULE_CONSENSUS])
+def test_dct_entropy_coded_payloads(rule):
+    """NEXT-2: JPEG entropy coding of the DCT payloads is lossless -- the run equals the
+    plain-coefficient run bit for bit and the oracle (fp64, 1e-6).  Graph rule: the
+    reported per-iteration bytes equal deg_i x (16 + the oracle's entropy-coded length of
+    the same coefficients) summed over nodes, and are below the plain payloads."""
+    cfg = c3s() if rule == C.RULE_GRAPH else C.C1()
+    if rule == C.RULE_CONSENSUS:
+        cfg.rule, cfg.quant, cfg.quality, cfg.nodes, cfg.graph = rule, C.Q_DCT, 50, 2, "ring"
+    cfg.iters = 4
+    inp = C.make_inputs(cfg)
+    plain = gpu_context(cfg, inp, precision=1)
+    plain.run(cfg.iters)
+    cfg.jpeg_restart = 4
+    ent = gpu_context(cfg, inp, precision=1)
+    ent.run(cfg.iters)
+    assert np.array_equal(ent.image(), plain.image())
+    o = oracle_case(cfg, inp).run(cfg.iters)
+    assert rel(ent.image(), o.image()) <= 1e-6
+    if rule != C.RULE_GRAPH:
+        return
+    Xg, _, _ = export_all(ent, cfg)  # x_i of the last iteration = the quantizer inputs
+    deg = np.zeros(cfg.nodes, int)
+    for i, j in inp.edges:
+        deg[i] += 1
+        deg[j] += 1
+    total = 0
+    for m in range(cfg.nodes):
+        coef, _ = oracle.dct_encode(Xg[m].astype(np.float32).reshape(cfg.N, cfg.N), cfg.quality)
+        total += (16 + len(oracle.jpeg_encode(coef, 4))) * int(deg[m])
+    assert ent.stats()["payload_bytes_logical"] == total
+    assert total < int(deg.sum()) * (8 + 2 * cfg.N * cfg.N)

@@ -179,3 +179,48 @@ def test_dct_constant_and_extremes():
     coef_r, mm_r = oracle.dct_encode(v, 75)
     coef, mm = tomoq.dct_encode(torch.tensor(v, device=DEV), 75)
     assert np.array_equal(coef.cpu().numpy(), coef_r)
+
+
+# ----------------------------------------------------------------- JPEG entropy coding (NEXT-2)
+@pytest.mark.parametrize("rows,cols,q", [(64, 64, 50), (512, 512, 50), (256, 512, 75), (2048, 2048, 75),
+                                         (8, 8, 100), (40, 24, 10)])
+@pytest.mark.parametrize("restart", [1, 4, 16])
+def test_jpeg_entropy_bit_exact(rows, cols, q, restart):
+    """GPU entropy-coded segment == the oracle's byte for byte (coefficients of the DCT
+    quantizer on the phantom recipe, several sizes, qualities and restart intervals);
+    the GPU decoder returns the coefficients of both streams."""
+    v = (phantom(max(rows, cols), rows + q, noise=0.03)[:rows, :cols] * 3 - 1).astype(np.float32)
+    coef_r, _ = oracle.dct_encode(v, q)
+    nb = rows * cols // 64
+    ref = oracle.jpeg_encode(coef_r, restart)
+    got = tomoq.jpeg_encode(torch.tensor(coef_r, device=DEV), restart).cpu().numpy().tobytes()
+    assert got == ref
+    dec = tomoq.jpeg_decode(torch.tensor(np.frombuffer(ref, np.uint8).copy(), device=DEV), nb, restart)
+    assert np.array_equal(dec.cpu().numpy(), coef_r)
+
+
+def test_jpeg_entropy_extremes_and_errors():
+    zz = oracle.jpeg_zigzag()
+    rng = np.random.default_rng(7)
+    c = np.zeros((33, 64), np.int16)
+    c[:, 0] = rng.integers(-1024, 1017, size=33)          # DC differences up to 11 bits
+    c[0, zz[1]], c[1, zz[17]], c[2, zz[63]] = 1023, -1023, 7  # AC category 10, no EOB
+    c[3, zz[16]], c[3, zz[33]], c[4, zz[62]] = 1, -2, 3     # ZRL runs
+    c[5:] *= 1
+    flat = c.ravel()
+    for r in (1, 2, 7, 64):
+        ref = oracle.jpeg_encode(flat, r)
+        got = tomoq.jpeg_encode(torch.tensor(flat, device=DEV), r).cpu().numpy().tobytes()
+        assert got == ref
+        back = tomoq.jpeg_decode(torch.tensor(np.frombuffer(ref, np.uint8).copy(), device=DEV), 33, r)
+        assert np.array_equal(back.cpu().numpy(), flat)
+    bad = np.zeros(64, np.int16)
+    bad[1] = 1024
+    with pytest.raises(tomoq.TomoQError):
+        tomoq.jpeg_encode(torch.tensor(bad, device=DEV), 1)
+    s = oracle.jpeg_encode(flat, 4)
+    broken = np.frombuffer(s, np.uint8).copy()
+    k = bytes(broken).index(b"\xff\xd1")
+    broken[k + 1] = 0xD3  # misnumbered RSTm
+    with pytest.raises(tomoq.TomoQError):
+        tomoq.jpeg_decode(torch.tensor(broken, device=DEV), 33, 4)
