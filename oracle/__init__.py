@@ -58,6 +58,8 @@ def lib():
         L.or_dct_cmatrix.argtypes = [_ip]
         L.or_dct_encode.argtypes = [_fp, C.c_int, C.c_int, C.c_int, _sp, _fp]
         L.or_dct_decode.argtypes = [_sp, _fp, C.c_int, C.c_int, C.c_int, _fp, C.c_void_p]
+        L.or_project_siddon.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _dp, _dp]
+        L.or_backproject_siddon.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _dp, _dp]
         L.or_jpeg_tables.argtypes = [_up, _up, _up, _up]
         L.or_jpeg_zigzag.argtypes = [_ip]
         L.or_jpeg_encode.argtypes = [_sp, C.c_long, C.c_int, _up, C.c_long]
@@ -70,7 +72,7 @@ def lib():
         L.or_admm_run.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip, C.c_int, _ip,
                                   C.c_int, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int,
                                   C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, _dp, C.c_int,
-                                  _dp, _dp, _dp, C.c_int]
+                                  _dp, _dp, _dp, C.c_int, C.c_int]
         L.or_alg3.restype = C.c_double
         L.or_alg3.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int]
         L.or_memory_model.restype = C.c_double
@@ -108,6 +110,26 @@ def project(img, n_ang: int, n_det: int, sel=None):
     sel = _i32(np.arange(n_ang) if sel is None else sel)
     out = np.zeros((len(sel), n_det))
     lib().or_project(N, n_det, n_ang, len(sel), sel, img, out)
+    return out
+
+
+def project_siddon(img, n_ang: int, n_det: int, sel=None):
+    """A img with P_ji = length of ray j inside pixel i (Siddon's
+    algorithm, R-26)."""
+    img = _f64(img)
+    N = img.shape[0]
+    sel = _i32(np.arange(n_ang) if sel is None else sel)
+    out = np.zeros((len(sel), n_det))
+    lib().or_project_siddon(N, n_det, n_ang, len(sel), sel, img, out)
+    return out
+
+
+def backproject_siddon(sino, N: int, n_ang: int, sel=None):
+    sino = _f64(sino)
+    sel = _i32(np.arange(n_ang) if sel is None else sel)
+    n_det = sino.shape[-1]
+    out = np.zeros((N, N))
+    lib().or_backproject_siddon(N, n_det, n_ang, len(sel), sel, sino.reshape(len(sel), n_det), out)
     return out
 
 
@@ -257,8 +279,9 @@ class OracleADMM:
 
     def __init__(self, N, n_det, n_ang, M, edges, sino_full, split_contig, rule=0, inner=1,
                  e1=5, rho=1.0, eta1=None, e2=10, eta2=0.2, qkind=0, K=16, lloyd=10,
-                 quality=50, threads=1):
+                 quality=50, threads=1, projector=0):
         self.N, self.n_det, self.n_ang, self.M = N, n_det, n_ang, M
+        self.projector = projector  # 0 Joseph (R-1), 1 Siddon (R-26, NEXT-3)
         if qkind == 2:  # the DCT codec works on whole 8x8 blocks (R-18)
             rows = N // M if rule in (1, 2) else N
             if N % 8 or rows % 8 or (rule in (1, 2) and N % M):
@@ -288,7 +311,7 @@ class OracleADMM:
             self.rule, self.inner, self.e1, self.rho,
             None if self.eta1 is None else self.eta1.ctypes.data, self.e2, self.eta2,
             self.qkind, self.K, self.lloyd, self.quality, self.d, iters, self.X, self.L, self.XH,
-            self.threads)
+            self.threads, self.projector)
         self.iters += iters
         return self
 

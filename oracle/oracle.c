@@ -131,6 +131,126 @@ void or_backproject(int N, int n_det, int n_ang, int n_sel, const int *sel,
     }
 }
 
+/* ------------------------------------------------------------------ Siddon
+ * The paper's literal system matrix: P_ji = length of the intersection of
+ * ray j with pixel i.  Siddon's algorithm (parametric ray, the sorted crossings with the
+ * N+1 vertical and N+1 horizontal grid lines, one segment per pair of consecutive
+ * crossings, the segment's midpoint names its pixel, its length is the weight).
+ * DESIGN.md R-26: pixel (r, c) is the closed unit square x in [c - N/2, c + 1 - N/2],
+ * y in [N/2 - r - 1, N/2 - r]; trig at theta = 0 and theta = pi/2 (2a = n_ang) is exact
+ * (1, 0) / (0, 1); a ray lying exactly on a grid line (axis-parallel, on a pixel edge)
+ * gives half of each segment's length to each of the two pixels sharing that edge (the
+ * mean of the two one-sided limits; pixels outside the grid are absent).
+ * Ray (theta, t): P(alpha) = t (cos, sin) + alpha (-sin, cos), unit speed.
+ */
+static void siddon_trig(int a, int n_ang, double *cs, double *sn)
+{
+    if (a == 0) { *cs = 1.0; *sn = 0.0; return; }
+    if (2 * a == n_ang) { *cs = 0.0; *sn = 1.0; return; }
+    double th = M_PI * (double)a / (double)n_ang;
+    *cs = cos(th); *sn = sin(th);
+}
+
+static int cmp_double(const void *a, const void *b)
+{
+    double x = *(const double *)a, y = *(const double *)b;
+    return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* the (pixel, length) list of one ray; returns the count (<= 4N + 4 entries) */
+static int siddon_ray(int N, double cs, double sn, double t, int *pix, double *len, double *alist)
+{
+    double h = 0.5 * (double)N;
+    double x0 = t * cs, y0 = t * sn, dx = -sn, dy = cs;
+    double amin = -INFINITY, amax = INFINITY;
+    if (dx != 0.0) {
+        double a1 = (-h - x0) / dx, a2 = (h - x0) / dx;
+        amin = fmax(amin, fmin(a1, a2)); amax = fmin(amax, fmax(a1, a2));
+    } else if (x0 < -h || x0 > h) return 0;
+    if (dy != 0.0) {
+        double a1 = (-h - y0) / dy, a2 = (h - y0) / dy;
+        amin = fmax(amin, fmin(a1, a2)); amax = fmin(amax, fmax(a1, a2));
+    } else if (y0 < -h || y0 > h) return 0;
+    if (!(amax > amin)) return 0;
+    int na = 0;
+    alist[na++] = amin;
+    alist[na++] = amax;
+    for (int k = 0; k <= N; k++) {
+        double g = (double)k - h; /* grid line coordinate */
+        if (dx != 0.0) { double a = (g - x0) / dx; if (a > amin && a < amax) alist[na++] = a; }
+        if (dy != 0.0) { double a = (g - y0) / dy; if (a > amin && a < amax) alist[na++] = a; }
+    }
+    qsort(alist, (size_t)na, sizeof(double), cmp_double);
+    /* on a grid line: x0 (dx == 0) or y0 (dy == 0) exactly on one */
+    int on_x = dx == 0.0 && floor(x0 + h) == x0 + h;
+    int on_y = dy == 0.0 && floor(h - y0) == h - y0;
+    int cnt = 0;
+    for (int i = 0; i + 1 < na; i++) {
+        double l = alist[i + 1] - alist[i];
+        if (!(l > 0.0)) continue;
+        double am = 0.5 * (alist[i] + alist[i + 1]);
+        double xm = x0 + am * dx, ym = y0 + am * dy;
+        int c = (int)floor(xm + h), r = (int)floor(h - ym);
+        if (on_x) { /* columns c-1 and c share the line x = x0 */
+            if (c - 1 >= 0 && c - 1 < N && r >= 0 && r < N) { pix[cnt] = r * N + c - 1; len[cnt++] = 0.5 * l; }
+            if (c >= 0 && c < N && r >= 0 && r < N) { pix[cnt] = r * N + c; len[cnt++] = 0.5 * l; }
+        } else if (on_y) { /* rows r-1 and r share the line y = y0 */
+            if (r - 1 >= 0 && r - 1 < N && c >= 0 && c < N) { pix[cnt] = (r - 1) * N + c; len[cnt++] = 0.5 * l; }
+            if (r >= 0 && r < N && c >= 0 && c < N) { pix[cnt] = r * N + c; len[cnt++] = 0.5 * l; }
+        } else if (r >= 0 && r < N && c >= 0 && c < N) {
+            pix[cnt] = r * N + c; len[cnt++] = l;
+        }
+    }
+    return cnt;
+}
+
+void or_project_siddon(int N, int n_det, int n_ang, int n_sel, const int *sel, const double *img, double *sino)
+{
+    int *pix = malloc(sizeof(int) * (size_t)(4 * N + 8));
+    double *len = malloc(sizeof(double) * (size_t)(4 * N + 8)), *al = malloc(sizeof(double) * (size_t)(2 * N + 8));
+    for (int k = 0; k < n_sel; k++) {
+        double cs, sn;
+        siddon_trig(sel[k], n_ang, &cs, &sn);
+        for (int j = 0; j < n_det; j++) {
+            double t = (double)j - 0.5 * (double)(n_det - 1);
+            int cnt = siddon_ray(N, cs, sn, t, pix, len, al);
+            double acc = 0.0;
+            for (int i = 0; i < cnt; i++) acc += len[i] * img[pix[i]];
+            sino[(size_t)k * n_det + j] = acc;
+        }
+    }
+    free(pix); free(len); free(al);
+}
+
+void or_backproject_siddon(int N, int n_det, int n_ang, int n_sel, const int *sel, const double *sino, double *img)
+{
+    int *pix = malloc(sizeof(int) * (size_t)(4 * N + 8));
+    double *len = malloc(sizeof(double) * (size_t)(4 * N + 8)), *al = malloc(sizeof(double) * (size_t)(2 * N + 8));
+    for (size_t p = 0; p < (size_t)N * N; p++) img[p] = 0.0;
+    for (int k = 0; k < n_sel; k++) {
+        double cs, sn;
+        siddon_trig(sel[k], n_ang, &cs, &sn);
+        for (int j = 0; j < n_det; j++) {
+            double t = (double)j - 0.5 * (double)(n_det - 1);
+            int cnt = siddon_ray(N, cs, sn, t, pix, len, al);
+            for (int i = 0; i < cnt; i++) img[pix[i]] += len[i] * sino[(size_t)k * n_det + j];
+        }
+    }
+    free(pix); free(len); free(al);
+}
+
+/* the projector of a run: 0 Joseph (R-1), 1 Siddon (R-26) */
+static void fwd(int proj, int N, int n_det, int n_ang, int n_sel, const int *sel, const double *img, double *sino)
+{
+    if (proj == 1) or_project_siddon(N, n_det, n_ang, n_sel, sel, img, sino);
+    else or_project(N, n_det, n_ang, n_sel, sel, img, sino);
+}
+static void bwd(int proj, int N, int n_det, int n_ang, int n_sel, const int *sel, const double *sino, double *img)
+{
+    if (proj == 1) or_backproject_siddon(N, n_det, n_ang, n_sel, sel, sino, img);
+    else or_backproject(N, n_det, n_ang, n_sel, sel, sino, img);
+}
+
 /* ------------------------------------------------------------------ vectors */
 static double dot(size_t n, const double *a, const double *b)
 {
@@ -148,15 +268,15 @@ static double dot(size_t n, const double *a, const double *b)
 
 /* Alg. 2: E1 gradient steps  Delta = A^T(A u - d) + c u - b', u -= eta Delta,
  * warm-started from the input u (R-9). */
-void or_gd(int N, int n_det, int n_ang, int n_sel, const int *sel, const double *d,
-           const double *bprime, double c, double eta, int e1, double *u)
+void or_gd_p(int proj, int N, int n_det, int n_ang, int n_sel, const int *sel, const double *d,
+             const double *bprime, double c, double eta, int e1, double *u)
 {
     size_t n = (size_t)N * N, l = (size_t)n_sel * n_det;
     double *s = malloc(l * sizeof(double)), *g = malloc(n * sizeof(double));
     for (int it = 0; it < e1; it++) {
-        or_project(N, n_det, n_ang, n_sel, sel, u, s);
+        fwd(proj, N, n_det, n_ang, n_sel, sel, u, s);
         for (size_t i = 0; i < l; i++) s[i] = s[i] - d[i];
-        or_backproject(N, n_det, n_ang, n_sel, sel, s, g);
+        bwd(proj, N, n_det, n_ang, n_sel, sel, s, g);
         for (size_t i = 0; i < n; i++) {
             double delta = g[i] + c * u[i] - bprime[i];
             u[i] = u[i] - eta * delta;
@@ -171,21 +291,21 @@ void or_gd(int N, int n_det, int n_ang, int n_sel, const int *sel, const double 
  *   repeat E1: q = A^T(A p) + c p; alpha = rr/(p.q); x += alpha p; r -= alpha q;
  *              beta = rr'/rr; p = r + beta p.
  * Guards (R-8): alpha = 0 if p.q <= 0; beta = 0 if rr == 0. */
-void or_cg(int N, int n_det, int n_ang, int n_sel, const int *sel, const double *d,
-           const double *bprime, double c, int e1, double *x)
+void or_cg_p(int proj, int N, int n_det, int n_ang, int n_sel, const int *sel, const double *d,
+             const double *bprime, double c, int e1, double *x)
 {
     size_t n = (size_t)N * N, l = (size_t)n_sel * n_det;
     double *s = malloc(l * sizeof(double));
     double *r = malloc(n * sizeof(double)), *p = malloc(n * sizeof(double));
     double *q = malloc(n * sizeof(double));
-    or_project(N, n_det, n_ang, n_sel, sel, x, s);
+    fwd(proj, N, n_det, n_ang, n_sel, sel, x, s);
     for (size_t i = 0; i < l; i++) s[i] = d[i] - s[i];
-    or_backproject(N, n_det, n_ang, n_sel, sel, s, r);
+    bwd(proj, N, n_det, n_ang, n_sel, sel, s, r);
     for (size_t i = 0; i < n; i++) { r[i] = r[i] + bprime[i] - c * x[i]; p[i] = r[i]; }
     double rr = dot(n, r, r);
     for (int it = 0; it < e1; it++) {
-        or_project(N, n_det, n_ang, n_sel, sel, p, s);
-        or_backproject(N, n_det, n_ang, n_sel, sel, s, q);
+        fwd(proj, N, n_det, n_ang, n_sel, sel, p, s);
+        bwd(proj, N, n_det, n_ang, n_sel, sel, s, q);
         for (size_t i = 0; i < n; i++) q[i] = q[i] + c * p[i];
         double pq = dot(n, p, q);
         double alpha = pq > 0.0 ? rr / pq : 0.0;
@@ -196,6 +316,17 @@ void or_cg(int N, int n_det, int n_ang, int n_sel, const int *sel, const double 
         rr = rr2;
     }
     free(s); free(r); free(p); free(q);
+}
+
+void or_gd(int N, int n_det, int n_ang, int n_sel, const int *sel, const double *d,
+           const double *bprime, double c, double eta, int e1, double *u)
+{
+    or_gd_p(0, N, n_det, n_ang, n_sel, sel, d, bprime, c, eta, e1, u);
+}
+void or_cg(int N, int n_det, int n_ang, int n_sel, const int *sel, const double *d,
+           const double *bprime, double c, int e1, double *x)
+{
+    or_cg_p(0, N, n_det, n_ang, n_sel, sel, d, bprime, c, e1, x);
 }
 
 /* ------------------------------------------------------------------ K-means (Alg. 5)
@@ -715,6 +846,7 @@ typedef struct {
     double rho; const double *eta1;
     int e2; double eta2;
     int qkind, K, lloyd, quality;
+    int proj;                        /* 0 Joseph (R-1), 1 Siddon (R-26) */
 } or_problem;
 
 /* Alg. 3 for one element of the owned segment x[m]:
@@ -743,20 +875,20 @@ static void local_solve(const or_problem *P, int m, const double *dm, const doub
 {
     int na = P->off[m + 1] - P->off[m];
     const int *sel = P->idx + P->off[m];
-    if (P->inner == 1) or_cg(P->N, P->n_det, P->n_ang, na, sel, dm, bp, c, P->e1, x);
+    if (P->inner == 1) or_cg_p(P->proj, P->N, P->n_det, P->n_ang, na, sel, dm, bp, c, P->e1, x);
     else {
         double eta = P->eta1 ? P->eta1[m] : 1.0 / (2.0 * na * P->N + c);
-        or_gd(P->N, P->n_det, P->n_ang, na, sel, dm, bp, c, eta, P->e1, x);
+        or_gd_p(P->proj, P->N, P->n_det, P->n_ang, na, sel, dm, bp, c, eta, P->e1, x);
     }
 }
 
 long or_admm_run(int N, int n_det, int n_ang, int M, const int32_t *off, const int32_t *idx,
                  int n_edges, const int32_t *edges, int rule, int inner, int e1, double rho,
                  const double *eta1, int e2, double eta2, int qkind, int K, int lloyd, int quality,
-                 const double *d, int iters, double *X, double *L, double *XH, int threads)
+                 const double *d, int iters, double *X, double *L, double *XH, int threads, int proj)
 {
     or_problem P = {N, n_det, n_ang, M, off, idx, n_edges, edges, rule, inner, e1, rho, eta1,
-                    e2, eta2, qkind, K, lloyd, quality};
+                    e2, eta2, qkind, K, lloyd, quality, proj};
     size_t n = (size_t)N * N;
     int *deg = calloc((size_t)M, sizeof(int)), *nb = calloc((size_t)M * M, sizeof(int));
     adjacency(&P, deg, nb);

@@ -167,3 +167,98 @@ def test_linearity_nonnegativity():
 def test_zero_inputs():
     assert not np.any(oracle.project(np.zeros((16, 16)), 8, 23))
     assert not np.any(oracle.backproject(np.zeros((8, 23)), 16, 8))
+
+
+# ----------------------------------------------------------------- Siddon (NEXT-3, R-26)
+from tests.helpers import clip_length, dense_siddon  # noqa: E402
+
+
+@pytest.mark.parametrize("N,n_ang,n_det", [(6, 8, 9), (8, 12, 12), (7, 10, 11), (8, 4, 13)])
+def test_siddon_equals_bruteforce_clipping(N, n_ang, n_det):
+    """P_ji = length of ray j inside pixel i: the oracle's Siddon crossing
+    lists vs clipping each ray against each pixel square; odd and even N and n_det put
+    rays on pixel edges (theta = 0, pi/2), through corners (pi/4) and in general position."""
+    A = dense_siddon(N, n_ang, n_det)
+    rng = np.random.default_rng(N * 100 + n_ang)
+    img = rng.random((N, N))
+    got = oracle.project_siddon(img, n_ang, n_det)
+    np.testing.assert_allclose(got.ravel(), A @ img.ravel(), rtol=0, atol=1e-12)
+    sino = rng.random((n_ang, n_det))
+    np.testing.assert_allclose(oracle.backproject_siddon(sino, N, n_ang).ravel(), A.T @ sino.ravel(),
+                               rtol=0, atol=1e-12)
+
+
+def test_siddon_chord_sums():
+    """Sum over pixels of P_ji = length of ray j inside the image square,
+    for 2000 random rays: the projection of the all-ones image."""
+    N, n_ang, n_det = 32, 250, 47
+    ones = np.ones((N, N))
+    got = oracle.project_siddon(ones, n_ang, n_det)
+    h = N / 2
+    for a in range(n_ang):
+        cs, sn = (1.0, 0.0) if a == 0 else ((0.0, 1.0) if 2 * a == n_ang else
+                                            (math.cos(math.pi * a / n_ang), math.sin(math.pi * a / n_ang)))
+        for j in range(0, n_det, 6):
+            t = j - 0.5 * (n_det - 1)
+            want = clip_length(-h, h, -h, h, t * cs, t * sn, -sn, cs)
+            # a ray on the outer boundary line keeps half (its outer neighbour is absent)
+            if (sn == 0 and abs(t * cs) == h) or (cs == 0 and abs(t * sn) == h):
+                want *= 0.5
+            assert abs(got[a, j] - want) <= 1e-12 * max(1.0, want), (a, j)
+
+
+def test_siddon_axis_rays_are_half_column_sums():
+    """theta = 0 with even N and odd n_det: every ray lies on a column boundary, so its
+    value is the mean of the two adjacent column sums (R-26)."""
+    N, n_ang, n_det = 16, 6, 23
+    img = np.random.default_rng(3).random((N, N))
+    s = oracle.project_siddon(img, n_ang, n_det)
+    cols = np.concatenate([[0.0], img.sum(axis=0), [0.0]])
+    for j in range(n_det):
+        t = j - (n_det - 1) // 2
+        k = int(t + N // 2)  # boundary index 0..N
+        want = 0.5 * (cols[k] + cols[k + 1]) if 0 <= k <= N else 0.0
+        assert abs(s[0, j] - want) <= 1e-12
+    rows = np.concatenate([[0.0], img.sum(axis=1)[::-1], [0.0]])  # bottom row first (y up)
+    for j in range(n_det):  # theta = pi/2: rays y = t on row boundaries
+        t = j - (n_det - 1) // 2
+        k = int(t + N // 2)
+        want = 0.5 * (rows[k] + rows[k + 1]) if 0 <= k <= N else 0.0
+        assert abs(s[3, j] - want) <= 1e-12
+
+
+@pytest.mark.parametrize("shape", ["disk", "ellipse"])
+def test_siddon_analytic_chord_lengths(shape):
+    """As for Joseph: a supersampled disk / rotated ellipse vs the closed-form line
+    integral (RMSE <= 0.5% of the peak)."""
+    N, n_ang, n_det = 256, 180, 363
+    if shape == "disk":
+        e = synth.Ellipses(np.array([10.3]), np.array([-7.9]), np.array([60.0]),
+                           np.array([60.0]), np.array([0.0]), np.array([1.0]))
+    else:
+        e = synth.Ellipses(np.array([-12.5]), np.array([20.25]), np.array([70.0]),
+                           np.array([35.0]), np.array([0.6]), np.array([0.8]))
+    img = synth.rasterize(e, N)
+    ref = synth.ellipse_sinogram(e, synth.default_angles(n_ang), n_det)
+    got = oracle.project_siddon(img, n_ang, n_det)
+    assert np.sqrt(np.mean((got - ref) ** 2)) <= 0.005 * ref.max()
+
+
+def test_siddon_adjoint_and_admm_runs():
+    N, n_ang, n_det = 24, 30, 35
+    rng = np.random.default_rng(9)
+    x, y = rng.random((N, N)), rng.random((n_ang, n_det))
+    lhs = np.sum(oracle.project_siddon(x, n_ang, n_det) * y)
+    rhs = np.sum(x * oracle.backproject_siddon(y, N, n_ang))
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+    # the ADMM loop with the Siddon projector: graph rule converges towards the Siddon
+    # least-squares solution on a tiny problem
+    N, n_ang, n_det = 8, 16, 13
+    A = dense_siddon(N, n_ang, n_det)
+    xt = rng.random(N * N)
+    sino = (A @ xt).reshape(n_ang, n_det)
+    edges = [(0, 1), (1, 2), (2, 3), (3, 0)]
+    o = oracle.OracleADMM(N, n_det, n_ang, 4, edges, sino, False, rule=0, inner=1, e1=5, rho=0.1,
+                          projector=1).run(3000)
+    ls = np.linalg.lstsq(A, sino.ravel(), rcond=None)[0]
+    assert np.linalg.norm(o.image().ravel() - ls) <= 1e-4 * np.linalg.norm(ls)
