@@ -123,6 +123,40 @@ def projector_c5_geometry(tomoq, torch, stream, reps=5):
     return out
 
 
+def projector_siddon_c4(tomoq, torch, stream, reps=10):
+    """NEXT-3 measurement: the Siddon projector (exact intersection lengths, R-26) on the
+    bench workload's geometry (C4_G1: 1024^2, 90 angles, 8 nodes), forward and CG
+    backprojector timed like the roofline components, next to Joseph."""
+    from paper_2410_06106_b200 import configs as C
+    cfg = C.C4(1)
+    inp = C.make_inputs(cfg, with_truth=False)
+    out = {"workload": "C4_G1 geometry with the Siddon projector"}
+    peak = LSU_VU_PER_CLK_SM * 148 * peaks()["sm_max_mhz"] * 1e6 / 1e9
+    for proj, name in ((tomoq.PROJ_SIDDON, "siddon"), (tomoq.PROJ_JOSEPH, "joseph")):
+        ctx = tomoq.Context(cfg.N, cfg.n_angles, cfg.n_det, cfg.nodes, inp.edges, split=cfg.split, rule=cfg.rule,
+                            projector=proj)
+        ctx.set_params(cfg.rho, inner=cfg.inner, e1=cfg.e1)
+        ctx.set_quantizer(tomoq.Q_NONE)
+        ctx.set_sinogram(0, torch.tensor(inp.sino[0], device="cuda"))
+        ctx.run(1)
+        res = {}
+        for comp, cname in ((0, "fp"), (1, "bp_cgq")):
+            ctx.launch_component(comp, 2, stream)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            units = ctx.launch_component(comp, reps, stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            t = a.elapsed_time(b) / reps
+            res[cname] = {"us": t * 1e3, "gvu_s": units / (t / 1e3) / 1e9, "frac": units / (t / 1e3) / 1e9 / peak}
+        ctx.run(5)
+        res["admm_iter_ms"] = ctx.stats()["ms_last_run"] / 5
+        out[name] = res
+        ctx.close()
+    return out
+
+
 def dct_entropy_c3(tomoq, torch, stream, reps=10, restart=4):
     """NEXT-2 measurement on config 3 as stated (16 nodes x 512^2, 4x4 torus, DCT q50):
     the DCT-J encode stage (tq_launch_component 4: min/max, integer DCT, quantisation and,
@@ -349,6 +383,13 @@ def main():
             c5_geom = projector_c5_geometry(tomoq, torch, stream, reps=5)
         except Exception as exc:  # report, never fail the bench line
             c5_geom = {"error": str(exc)[:200]}
+    # ---- NEXT-3: the Siddon projector on the bench geometry (context, not the headline)
+    siddon_c4 = None
+    if rank == 0 and not args.no_c5_geometry:
+        try:
+            siddon_c4 = projector_siddon_c4(tomoq, torch, stream)
+        except Exception as exc:
+            siddon_c4 = {"error": str(exc)[:200]}
     # ---- NEXT-2: JPEG entropy coding of the DCT payloads on config 3 (context, not the headline)
     jpeg_c3 = None
     if rank == 0 and not args.no_c5_geometry:
@@ -373,6 +414,7 @@ def main():
             "roofline": roofline,
             "projector_c5_geometry": c5_geom,
             "dct_entropy_c3": jpeg_c3,
+            "projector_siddon_c4": siddon_c4,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(sino_host.numel() * 4),
                     "d2h_bytes_per_step": int(cfg.N * cfg.N * 4), "ms_per_step": max(e2e_ms, e2e_wall) / args.steps},

@@ -46,7 +46,13 @@ typedef struct {
     int32_t image_side;  /* N, multiple of 8, >= 8 */
     int32_t n_angles;    /* angles evenly spaced in [0, pi) */
     int32_t n_det;       /* detector bins, >= ceil(N sqrt 2) */
+    int32_t projector;   /* TQ_PROJ_JOSEPH (R-1, default) or TQ_PROJ_SIDDON: exact intersection
+                            lengths P_ji = |ray j inside pixel i| (SURVEY NEXT-3,
+                            R-26: trig exact at 0 and pi/2, a ray on a pixel edge counts half
+                            in each of the two pixels) */
 } tq_geometry;
+
+enum { TQ_PROJ_JOSEPH = 0, TQ_PROJ_SIDDON = 1 };
 
 enum { TQ_SPLIT_ROUND_ROBIN = 0, TQ_SPLIT_CONTIGUOUS = 1 };
 enum { TQ_RULE_GRAPH = 0, TQ_RULE_PAPER = 1, TQ_RULE_CONSENSUS = 2 };

@@ -37,6 +37,7 @@ class Config:
     k: int = 16
     lloyd: int = 10
     quality: int = 50
+    projector: int = 0     # 0 Joseph (R-1), 1 Siddon (R-26, NEXT-3)
     jpeg_restart: int = 0  # DCT payloads: 0 plain int16 coefficients, R > 0 JPEG entropy coding (NEXT-2)
     texture: float = 0.0
     slices: int = 1

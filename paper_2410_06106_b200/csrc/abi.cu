@@ -37,6 +37,7 @@ tq_status guard(tq_ctx *ctx, F &&f) {
 void check_geom(const tq_geometry *g) {
     TQ_REQUIRE(g != nullptr, "null geometry");
     TQ_REQUIRE(g->image_side >= 1 && g->n_angles >= 1, "bad geometry");
+    TQ_REQUIRE(g->projector == TQ_PROJ_JOSEPH || g->projector == TQ_PROJ_SIDDON, "bad projector");
     TQ_REQUIRE((long long)g->n_det * g->n_det >= 2LL * g->image_side * g->image_side,
                "n_det must be >= ceil(N sqrt 2)");
 }
@@ -234,7 +235,7 @@ tq_status tq_project(const tq_geometry *g, const int32_t *sel, int32_t n_sel, co
         TQ_REQUIRE(img && sino && (precision == 0 || precision == 1), "bad arguments");
         std::vector<int> s = check_sel(g, sel, n_sel);
         DevGeom geo;
-        geo.init(g->image_side, g->n_angles, g->n_det);
+        geo.init(g->image_side, g->n_angles, g->n_det, g->projector);
         Inner in;
         in.init(precision, geo, {s});
         cudaStream_t st = (cudaStream_t)stream;
@@ -252,7 +253,7 @@ tq_status tq_backproject(const tq_geometry *g, const int32_t *sel, int32_t n_sel
         TQ_REQUIRE(img && sino && (precision == 0 || precision == 1), "bad arguments");
         std::vector<int> s = check_sel(g, sel, n_sel);
         DevGeom geo;
-        geo.init(g->image_side, g->n_angles, g->n_det);
+        geo.init(g->image_side, g->n_angles, g->n_det, g->projector);
         DevTmp t;
         std::vector<RayRow> rows;
         for (int k = 0; k < n_sel; k++) rows.push_back(RayRow{0, s[k], k, 0});
@@ -265,12 +266,14 @@ tq_status tq_backproject(const tq_geometry *g, const int32_t *sel, int32_t n_sel
             a.s = (const float *)sino; a.s_stride = g->n_det; a.s_off = 0;
             a.node_row0 = row0; a.node_nang = nang; a.rows = rd; a.trig = geo.trig; a.xmaj = geo.xmaj;
             a.N = g->image_side; a.n_det = g->n_det; a.n = geo.n; a.out = (float *)img; a.magic = kMagicBits4;
+            a.siddon = geo.proj;
             launch_bp(0, EPI_PLAIN, &a, 1, g->image_side, st);
         } else {
             BpArgs<double> a{};
             a.s = (const double *)sino; a.s_stride = g->n_det; a.s_off = 0;
             a.node_row0 = row0; a.node_nang = nang; a.rows = rd; a.trig = geo.trig; a.xmaj = geo.xmaj;
             a.N = g->image_side; a.n_det = g->n_det; a.n = geo.n; a.out = (double *)img; a.magic = kMagicBits4;
+            a.siddon = geo.proj;
             launch_bp(1, EPI_PLAIN, &a, 1, g->image_side, st);
         }
         TQ_CHECK_CUDA(cudaStreamSynchronize(st));
@@ -288,7 +291,7 @@ tq_status tq_local_solve(const tq_geometry *g, const int32_t *sel, int32_t n_sel
         TQ_REQUIRE(e1 >= 0 && c >= 0.0, "bad e1 / c");
         std::vector<int> s = check_sel(g, sel, n_sel);
         DevGeom geo;
-        geo.init(g->image_side, g->n_angles, g->n_det);
+        geo.init(g->image_side, g->n_angles, g->n_det, g->projector);
         Inner in;
         in.init(precision, geo, {s});
         cudaStream_t st = (cudaStream_t)stream;

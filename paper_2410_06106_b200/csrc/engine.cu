@@ -192,7 +192,8 @@ void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int ran
     TQ_CHECK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     TQ_CHECK_CUDA(cudaEventCreate(&ev0));
     TQ_CHECK_CUDA(cudaEventCreate(&ev1));
-    geo.init(N, n_ang, n_det);
+    TQ_REQUIRE(g.projector == TQ_PROJ_JOSEPH || g.projector == TQ_PROJ_SIDDON, "bad projector");
+    geo.init(N, n_ang, n_det, g.projector);
     in.init(prec, geo, angles);
     const size_t es = prec ? 8 : 4;
     TQ_CHECK_CUDA(cudaMalloc(&ALPHA, std::max<size_t>(16, es * n * L)));

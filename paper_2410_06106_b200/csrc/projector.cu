@@ -80,7 +80,14 @@ struct V16<double> {
 };
 
 // ------------------------------------------------------------------ forward: tile pass
-template <typename T, int O>  // O = 0: y-major angles (lines = rows), 1: x-major (lines = columns)
+// slope 1/w of the Siddon band fraction (w = |cross drift per line|); 2^22 for axis rays
+template <typename T>
+__device__ __forceinline__ T siddon_iw(T B) {
+    const T w = B < (T)0 ? -B : B;
+    return w > (T)1e-9 ? (T)1 / w : (T)4194304;
+}
+
+template <typename T, int O, bool SID = false>  // O = 0: y-major angles (lines = rows), 1: x-major (lines = columns)
 __global__ void __launch_bounds__(FP_THREADS) fp_tile_kernel(const FpArgs<T> a) {
     constexpr int PITCH = O == 0 ? FP_PITCH_Y : FP_PITCH_X;
     constexpr int H = FP_HALO_A;
@@ -187,6 +194,7 @@ __global__ void __launch_bounds__(FP_THREADS) fp_tile_kernel(const FpArgs<T> a) 
             const int wc = min(w, W - 1);
             const T kap = (T)(s_kap[k] + (double)wc * s_at[k]);
             const T B = s_B[k];
+            const T iw = SID ? siddon_iw(B) : (T)1, hw = SID ? (T)0.5 - (T)0.5 * iw : (T)0;
             T acc0 = 0, acc1 = 0;
             if constexpr (sizeof(T) == 4) {
                 const uint32_t sb = magic_base(tile, a.magic);
@@ -196,7 +204,8 @@ __global__ void __launch_bounds__(FP_THREADS) fp_tile_kernel(const FpArgs<T> a) 
                     const float m = __fadd_rd(kf, 8388608.0f);     // 2^23 + floor(kf)
                     const uint32_t ad = (__float_as_uint(m) << 2) + sb;
                     const float v0 = lds<0>(ad + l * PITCH * 4), v1 = lds<4>(ad + l * PITCH * 4);
-                    const float f = kf - (m - 8388608.0f);
+                    float f = kf - (m - 8388608.0f);
+                    if (SID) f = __saturatef(fmaf(f, iw, hw));
                     acc0 += v0;
                     acc1 = fmaf(f, v1 - v0, acc1);
                 }
@@ -206,7 +215,8 @@ __global__ void __launch_bounds__(FP_THREADS) fp_tile_kernel(const FpArgs<T> a) 
                     const T kf = fma((T)l, B, kap);
                     int i0;
                     const T fl = floor_split<T>(kf, i0);
-                    const T f = kf - fl;
+                    T f = kf - fl;
+                    if (SID) f = sat<T>(fma(f, iw, hw));
                     const T *p = tile + l * PITCH + i0;
                     const T v0 = p[0], v1 = p[1];
                     acc0 += v0;
@@ -442,6 +452,7 @@ __device__ __forceinline__ int fp_half_rays(double at) {
 // (y-major: a 32 x 128 box of the [L][N][N] images; x-major: a 128 x 32 box stored with
 // the 128-byte swizzle, i.e. conflict-free column reads) and a bulk copy of its window
 // records, both completing on one mbarrier.  Out-of-image pixels are zero-filled by TMA.
+template <bool SID>  // SID: Siddon weights (R-26) over natural pairs (x_i, d_i)
 __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<float> a, int nunits,
                                                                 const __grid_constant__ CUtensorMap tm_rows,
                                                                 const __grid_constant__ CUtensorMap tm_cols) {
@@ -498,7 +509,7 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
     };
     auto pair = [](float x, float xn, int i) {
         const float d = xn - x;
-        return make_float2(fmaf(-(float)(i - FP2_ORG), d, x), d);
+        return SID ? make_float2(x, d) : make_float2(fmaf(-(float)(i - FP2_ORG), d, x), d);
     };
 
     int rb = 0;
@@ -606,14 +617,29 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
                 const float kap = (float)(R[k].kap + (double)w * R[k].at);
                 const float B = R[k].B;
                 float acc0 = 0.f, acc1 = 0.f;
+                if (!SID) {
 #pragma unroll
-                for (int l = 0; l < FP_TH; l += 2) {
-                    const float kf0 = fmaf((float)l, B, kap), kf1 = fmaf((float)(l + 1), B, kap);
-                    const float m0 = __fadd_rd(kf0, FP2_MAGIC), m1 = __fadd_rd(kf1, FP2_MAGIC);
-                    const float2 q0 = lds64((__float_as_uint(m0) << 3) + sb + l * FP2_PITCH * 8);
-                    const float2 q1 = lds64((__float_as_uint(m1) << 3) + sb + (l + 1) * FP2_PITCH * 8);
-                    acc0 += fmaf(kf0, q0.y, q0.x);
-                    acc1 += fmaf(kf1, q1.y, q1.x);
+                    for (int l = 0; l < FP_TH; l += 2) {
+                        const float kf0 = fmaf((float)l, B, kap), kf1 = fmaf((float)(l + 1), B, kap);
+                        const float m0 = __fadd_rd(kf0, FP2_MAGIC), m1 = __fadd_rd(kf1, FP2_MAGIC);
+                        const float2 q0 = lds64((__float_as_uint(m0) << 3) + sb + l * FP2_PITCH * 8);
+                        const float2 q1 = lds64((__float_as_uint(m1) << 3) + sb + (l + 1) * FP2_PITCH * 8);
+                        acc0 += fmaf(kf0, q0.y, q0.x);
+                        acc1 += fmaf(kf1, q1.y, q1.x);
+                    }
+                } else {  // pixel a + 1 gets g = sat((u - 1/2) / w + 1/2) of the band's length
+                    const float iw = siddon_iw(B), hw = 0.5f - 0.5f * iw;
+#pragma unroll
+                    for (int l = 0; l < FP_TH; l += 2) {
+                        const float kf0 = fmaf((float)l, B, kap), kf1 = fmaf((float)(l + 1), B, kap);
+                        const float m0 = __fadd_rd(kf0, FP2_MAGIC), m1 = __fadd_rd(kf1, FP2_MAGIC);
+                        const float2 q0 = lds64((__float_as_uint(m0) << 3) + sb + l * FP2_PITCH * 8);
+                        const float2 q1 = lds64((__float_as_uint(m1) << 3) + sb + (l + 1) * FP2_PITCH * 8);
+                        const float g0 = __saturatef(fmaf(kf0 - (m0 - FP2_MAGIC), iw, hw));
+                        const float g1 = __saturatef(fmaf(kf1 - (m1 - FP2_MAGIC), iw, hw));
+                        acc0 += fmaf(g0, q0.y, q0.x);
+                        acc1 += fmaf(g1, q1.y, q1.x);
+                    }
                 }
                 if (ok)
                     a.partial[((long long)R[k].row * a.nt_line + lt) * 2 * a.n_det + (ct & 1) * a.n_det + R[k].jlo + w] =
@@ -753,7 +779,7 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
     // latency overlaps the angle loop: ep[0] = vin (p or x), ep[1] = b' (RESID, GD)
     float *ep = reinterpret_cast<float *>(bp_smem + (sizeof(T) == 4 ? sizeof(float2) : sizeof(T)) * BP_MAXA * BP_WB);
     __shared__ double s_tau[BP_MAXA], s_csd[BP_MAXA], s_snd[BP_MAXA];
-    __shared__ T s_cs[BP_MAXA], s_sn[BP_MAXA], s_im[BP_MAXA];
+    __shared__ T s_cs[BP_MAXA], s_sn[BP_MAXA], s_im[BP_MAXA], s_a1[BP_MAXA], s_a0[BP_MAXA];
     __shared__ int s_jlo[BP_MAXA];
     __shared__ double red[BP_THREADS / 32 + 1];
     __shared__ bool last_flag;
@@ -805,6 +831,17 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
             s_cs[k] = (T)cs;
             s_sn[k] = (T)sn;
             s_im[k] = (T)(1.0 / m);
+            // tap weight sat(a0 - s a1) at bin distance s (times the 1/m pre-scale): Joseph
+            // a1 = 1/m, a0 = 1; Siddon (R-26) a1 = 1/(m w), a0 = (1 + 1/w)/2, w = drift per line
+            if (a.siddon) {
+                const double w = a.xmaj[ang] ? fabs(cs / sn) : fabs(sn / cs);
+                const double iw = w > 1e-9 ? 1.0 / w : 4194304.0;
+                s_a1[k] = (T)(iw / m);
+                s_a0[k] = (T)(0.5 + 0.5 * iw);
+            } else {
+                s_a1[k] = (T)(1.0 / m);
+                s_a0[k] = (T)1;
+            }
         }
         __syncthreads();
         for (int i = threadIdx.x; i < kc * BP_WB; i += BP_THREADS) {
@@ -821,7 +858,7 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
         }
         __syncthreads();
         for (int k = 0; k < kc; k++) {
-            const T cs = s_cs[k], sn = s_sn[k], im = s_im[k], omi = (T)1 - im;
+            const T cs = s_cs[k], sn = s_sn[k], a1 = s_a1[k], a0 = s_a0[k], a0m = a0 - a1;
             const T tau_t = (T)(s_tau[k] + (double)lx * s_csd[k] - (double)prow * s_snd[k]);
             if constexpr (sizeof(T) == 4) {
                 const uint32_t wb = magic_base(win2 + k * BP_WB, a.magic);  // magic = 0x4B000000 << 3
@@ -834,8 +871,8 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
                         const float m = __fadd_rd(tau, 8388608.0f);   // 2^23 + floor(tau)
                         const float2 sv = lds64((__float_as_uint(m) << 3) + wb);
                         const float u = tau - (m - 8388608.0f);
-                        const float w0 = __saturatef(fmaf(-u, im, 1.0f));
-                        const float w1 = __saturatef(fmaf(u, im, omi));
+                        const float w0 = __saturatef(fmaf(-u, a1, a0));
+                        const float w1 = __saturatef(fmaf(u, a1, a0m));
                         acc[ky][kx] = fmaf(w0, sv.x, acc[ky][kx]);
                         acc[ky][kx] = fmaf(w1, sv.y, acc[ky][kx]);
                     }
@@ -851,8 +888,8 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
                         int i0;
                         const T fl = floor_split<T>(tau, i0);
                         const T u = tau - fl;
-                        const T w0 = sat<T>(fma(-u, im, (T)1));
-                        const T w1 = sat<T>(fma(u, im, omi));
+                        const T w0 = sat<T>(fma(-u, a1, a0));
+                        const T w1 = sat<T>(fma(u, a1, a0m));
                         acc[ky][kx] = fma(w0, wk[i0], acc[ky][kx]);
                         acc[ky][kx] = fma(w1, wk[i0 + 1], acc[ky][kx]);
                     }
@@ -948,14 +985,17 @@ template <typename T>
 void set_all_smem() {
     set_smem(fp_tile_kernel<T, 0>, fp_smem<T>(0));
     set_smem(fp_tile_kernel<T, 1>, fp_smem<T>(1));
+    set_smem(fp_tile_kernel<T, 0, true>, fp_smem<T>(0));
+    set_smem(fp_tile_kernel<T, 1, true>, fp_smem<T>(1));
     if (sizeof(T) == 4) {
         set_smem(fp_tile_f32<0>, fp2_smem());
         set_smem(fp_tile_f32<1>, fp2_smem());
-        set_smem(fp_persist_f32, fpp_smem());
+        set_smem(fp_persist_f32<false>, fpp_smem());
+        set_smem(fp_persist_f32<true>, fpp_smem());
         int dev = 0, sms = 0, per = 0;
         TQ_CHECK_CUDA(cudaGetDevice(&dev));
         TQ_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        TQ_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fp_persist_f32, FP_THREADS, fpp_smem()));
+        TQ_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fp_persist_f32<false>, FP_THREADS, fpp_smem()));
         g_fpp_grid = sms * std::max(1, per);
     }
     set_smem(bp_tile_kernel<T, EPI_PLAIN>, bp_smem<T, EPI_PLAIN>());
@@ -998,6 +1038,14 @@ void make_image_maps(const float *img, int N, int L, CUtensorMap *rows, CUtensor
 template <typename T>
 void fp_dispatch(const FpArgs<T> &A, int L, cudaStream_t st) {
     const dim3 grid(A.nt_line * A.nt_cross, L);
+    const bool persist = sizeof(T) == 4 && A.N % 4 == 0 && A.recs && ((uintptr_t)A.img & 15) == 0;
+    if (A.siddon && !persist) {  // Siddon (NEXT-3) outside the persistent fp32 kernel: the generic tile kernel
+        FpArgs<T> S = A;
+        S.magic = 0x4B000000u << 2;  // 4-byte entries
+        fp_tile_kernel<T, 0, true><<<grid, FP_THREADS, fp_smem<T>(0), st>>>(S);
+        fp_tile_kernel<T, 1, true><<<grid, FP_THREADS, fp_smem<T>(1), st>>>(S);
+        return;
+    }
     if constexpr (sizeof(T) == 4) {
         FpArgs<float> B = A;
         B.magic = 0x4B000000u << 3;  // 8-byte pairs (wraps mod 2^32)
@@ -1005,7 +1053,8 @@ void fp_dispatch(const FpArgs<T> &A, int L, cudaStream_t st) {
             const int nunits = 2 * L * A.nt_line * A.nt_cross;
             CUtensorMap tr, tc;
             make_image_maps(A.img, A.N, L, &tr, &tc);
-            fp_persist_f32<<<std::min(nunits, g_fpp_grid), FP_THREADS, fpp_smem(), st>>>(B, nunits, tr, tc);
+            if (A.siddon) fp_persist_f32<true><<<std::min(nunits, g_fpp_grid), FP_THREADS, fpp_smem(), st>>>(B, nunits, tr, tc);
+            else fp_persist_f32<false><<<std::min(nunits, g_fpp_grid), FP_THREADS, fpp_smem(), st>>>(B, nunits, tr, tc);
         } else {
             fp_tile_f32<0><<<grid, FP_THREADS, fp2_smem(), st>>>(B);
             fp_tile_f32<1><<<grid, FP_THREADS, fp2_smem(), st>>>(B);

@@ -3,6 +3,15 @@
 //
 // Operator (R-1): P[(a,j),p] = max(0, 1-|t_j-t_p|/m_a)/m_a.
 //
+// Siddon (R-26): on each major-axis line (a band one pixel thick) the
+// ray covers the cross interval [c - w/2, c + w/2], w = |B| <= 1 the cross drift per
+// line, with length 1/m_a; it meets pixels a = floor(c) and a + 1 only, and pixel a + 1
+// receives the fraction g = sat((u - 1/2) / w + 1/2), u = c - a (g = u is Joseph).  The
+// same tiles, windows and reduction serve both; w = 0 (axis rays, exact trig) uses the
+// slope 2^22 so that u = 1/2 (a ray on a pixel edge) gives exactly 1/2.  The transpose
+// weight of bin distance s is sat(a0 - s a1), a1 = 1/(m w), a0 = (1 + 1/w)/2 (Joseph:
+// a1 = 1/m, a0 = 1), times the 1/m pre-scale of the staged bins.
+//
 // Forward (A), "image-tile stationary": one CTA stages a TH x TW tile of one node's
 // image in shared memory (zero halo on both sides of the cross axis) and walks, for
 // EVERY angle of that node whose major axis matches the tile orientation, all rays
@@ -90,6 +99,7 @@ struct FpArgs {
     const FpRec *recs;     // [ntiles][n_olist] (fp32 persistent kernel)
     int n_olist, L;
     const FpUnitTab *utab; // [2 * L * ntiles] (fp32 persistent kernel)
+    int siddon;            // 1: Siddon weights (R-26) -- generic tile kernel
 };
 
 template <typename T>
@@ -127,6 +137,7 @@ struct BpArgs {
     double *scal;            // [L][S_NSLOT]
     int part_stride;
     uint32_t magic;          // = 0x4B000000 << 2 (mod 2^32)
+    int siddon;              // 1: Siddon weights (R-26)
 };
 
 constexpr uint32_t kMagicBits4 = 0x2C000000u;  // (0x4B000000 << 2) mod 2^32

@@ -5,15 +5,16 @@
 
 namespace tq {
 
-void DevGeom::init(int N_, int n_ang_, int n_det_) {
+void DevGeom::init(int N_, int n_ang_, int n_det_, int proj_) {
     projector_setup();
-    N = N_; n_ang = n_ang_; n_det = n_det_;
+    N = N_; n_ang = n_ang_; n_det = n_det_; proj = proj_;
     n = (long long)N * N;
     std::vector<AngleHost> a = make_angles(n_ang);
     std::vector<double2> t(n_ang);
     std::vector<int> xm(n_ang);
     for (int i = 0; i < n_ang; i++) {
         t[i] = make_double2(a[i].cs, a[i].sn);
+        if (proj == 1 && 2 * i == n_ang) t[i] = make_double2(0.0, 1.0);  // R-26: exact trig at pi/2
         xm[i] = a[i].xmajor;
     }
     TQ_CHECK_CUDA(cudaMalloc(&trig, sizeof(double2) * n_ang));
@@ -102,14 +103,14 @@ int Inner::project(const DevGeom &g, const void *img, bool resid, cudaStream_t s
     if (!out) { out = S; out_stride = sp; out_off = 1; }
     if (prec == 0) {
         FpArgs<float> a{(const float *)img, n, g.N, g.n_det, olist, oofs, fwin, frg, (float *)fpart,
-                        nt_line, nt_cross, kMagicBits4, frec, n_olist, L, futab};
+                        nt_line, nt_cross, kMagicBits4, frec, n_olist, L, futab, g.proj};
         launch_fp(0, &a, L, st);
         FpRedArgs<float> r{(const float *)fpart, rows, g.trig, g.xmaj, (const float *)D, (float *)out,
                            out_stride, out_off, g.N, g.n_det, nt_line};
         launch_fp_reduce(0, resid, &r, n_rows, g.n_det, st);
     } else {
         FpArgs<double> a{(const double *)img, n, g.N, g.n_det, olist, oofs, fwin, frg, (double *)fpart,
-                         nt_line, nt_cross, kMagicBits4, frec, n_olist, L, futab};
+                         nt_line, nt_cross, kMagicBits4, frec, n_olist, L, futab, g.proj};
         launch_fp(1, &a, L, st);
         FpRedArgs<double> r{(const double *)fpart, rows, g.trig, g.xmaj, (const double *)D,
                             (double *)out, out_stride, out_off, g.N, g.n_det, nt_line};
@@ -122,12 +123,12 @@ int Inner::backproject(const DevGeom &g, int epi, void *out, void *out2, const v
     if (prec == 0) {
         BpArgs<float> a{(const float *)S, sp, 1, row0, nang, rows, g.trig, g.xmaj, g.N, g.n_det, n,
                         (float *)out, (float *)out2, (const float *)vin, (const float *)BP, cnode, eta,
-                        partial, counter, scal, part_stride, kMagicBits4};
+                        partial, counter, scal, part_stride, kMagicBits4, g.proj};
         launch_bp(0, epi, &a, L, g.N, st);
     } else {
         BpArgs<double> a{(const double *)S, sp, 1, row0, nang, rows, g.trig, g.xmaj, g.N, g.n_det, n,
                          (double *)out, (double *)out2, (const double *)vin, (const double *)BP, cnode,
-                         eta, partial, counter, scal, part_stride, kMagicBits4};
+                         eta, partial, counter, scal, part_stride, kMagicBits4, g.proj};
         launch_bp(1, epi, &a, L, g.N, st);
     }
     return 1;

@@ -11,12 +11,12 @@ namespace tq {
 
 // device geometry shared by all nodes of a context
 struct DevGeom {
-    int N = 0, n_ang = 0, n_det = 0;
+    int N = 0, n_ang = 0, n_det = 0, proj = 0;  // proj: 0 Joseph, 1 Siddon
     long long n = 0;
     double2 *trig = nullptr;  // [n_ang]
     int *xmaj = nullptr;      // [n_ang]
     std::vector<int> xmaj_h;
-    void init(int N, int n_ang, int n_det);
+    void init(int N, int n_ang, int n_det, int proj = 0);
     void release();
 };
 

@@ -17,6 +17,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "tomoq.h")
 
 SPLIT_RR, SPLIT_CONTIG = 0, 1
 RULE_GRAPH, RULE_PAPER, RULE_CONSENSUS = 0, 1, 2
+PROJ_JOSEPH, PROJ_SIDDON = 0, 1
 INNER_GD, INNER_CG = 0, 1
 Q_NONE, Q_KMEANS, Q_DCT, Q_ALT = 0, 1, 2, 3
 STATUS = {0: "TQ_OK", 1: "TQ_EINVAL", 2: "TQ_ENOMEM", 3: "TQ_ECUDA", 4: "TQ_ENCCL",
@@ -30,7 +31,8 @@ class TomoQError(RuntimeError):
 
 
 class Geometry(C.Structure):
-    _fields_ = [("image_side", C.c_int32), ("n_angles", C.c_int32), ("n_det", C.c_int32)]
+    _fields_ = [("image_side", C.c_int32), ("n_angles", C.c_int32), ("n_det", C.c_int32),
+                ("projector", C.c_int32)]
 
 
 class Graph(C.Structure):
@@ -171,10 +173,10 @@ class Context:
 
     def __init__(self, N, n_angles, n_det, n_nodes, edges, split=SPLIT_RR, rule=RULE_GRAPH,
                  n_slices=1, rank=0, world=1, nccl_id: bytes | None = None, precision=0,
-                 device=0, node_rank=None):
+                 device=0, node_rank=None, projector=PROJ_JOSEPH):
         self.N, self.n = N, N * N
         self.precision = precision
-        geom = Geometry(N, n_angles, n_det)
+        geom = Geometry(N, n_angles, n_det, projector)
         g, self._keep = _graph(n_nodes, edges, split, rule, node_rank)
         h = C.c_void_p()
         idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id else None
@@ -275,33 +277,34 @@ def _prec(t):
     raise TypeError("float32 or float64 tensors only")
 
 
-def project(img, n_angles, n_det, sel=None, stream=None):
+def project(img, n_angles, n_det, sel=None, stream=None, projector=PROJ_JOSEPH):
     """A img for the selected angles; img: CUDA tensor N x N (fp32/fp64)."""
     import torch
     N = img.shape[-1]
     sel = _i32arr(np.arange(n_angles) if sel is None else sel)
     out = torch.empty((len(sel), n_det), dtype=img.dtype, device=img.device)
-    g = Geometry(N, n_angles, n_det)
+    g = Geometry(N, n_angles, n_det, projector)
     _check(lib().tq_project(C.byref(g), sel.ctypes.data, len(sel), img.contiguous().data_ptr(),
                             out.data_ptr(), _prec(img), _stream(stream)))
     return out
 
 
-def backproject(sino, N, n_angles, sel=None, stream=None):
+def backproject(sino, N, n_angles, sel=None, stream=None, projector=PROJ_JOSEPH):
     import torch
     sel = _i32arr(np.arange(n_angles) if sel is None else sel)
     out = torch.empty((N, N), dtype=sino.dtype, device=sino.device)
-    g = Geometry(N, n_angles, sino.shape[-1])
+    g = Geometry(N, n_angles, sino.shape[-1], projector)
     _check(lib().tq_backproject(C.byref(g), sel.ctypes.data, len(sel), sino.contiguous().data_ptr(),
                                 out.data_ptr(), _prec(sino), _stream(stream)))
     return out
 
 
-def local_solve(d, bprime, c, e1, x0, n_angles, sel, inner=INNER_CG, eta=0.0, stream=None):
+def local_solve(d, bprime, c, e1, x0, n_angles, sel, inner=INNER_CG, eta=0.0, stream=None,
+                projector=PROJ_JOSEPH):
     x = x0.clone().contiguous()
     N = x.shape[-1]
     sel = _i32arr(sel)
-    g = Geometry(N, n_angles, d.shape[-1])
+    g = Geometry(N, n_angles, d.shape[-1], projector)
     _check(lib().tq_local_solve(C.byref(g), sel.ctypes.data, len(sel), d.contiguous().data_ptr(),
                                 bprime.contiguous().data_ptr(), float(c), inner, e1, float(eta),
                                 x.data_ptr(), _prec(x), _stream(stream)))

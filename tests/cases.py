@@ -17,7 +17,7 @@ def slice_kind(cfg, s):
 
 def gpu_context(cfg, inp, precision=0, keep_labels=False, eta1=None):
     ctx = tomoq.Context(cfg.N, cfg.n_angles, cfg.n_det, cfg.nodes, inp.edges, split=cfg.split,
-                        rule=cfg.rule, n_slices=len(inp.sino), precision=precision)
+                        rule=cfg.rule, n_slices=len(inp.sino), precision=precision, projector=cfg.projector)
     ctx.set_params(cfg.rho, inner=cfg.inner, e1=cfg.e1, eta1=eta1, e2=cfg.e2, eta2=cfg.eta2)
     ctx.set_quantizer(cfg.quant, k=cfg.k, lloyd=cfg.lloyd, quality=cfg.quality, keep_labels=keep_labels,
                       jpeg_restart=cfg.jpeg_restart)
@@ -31,7 +31,7 @@ def oracle_case(cfg, inp, s=0, threads=8, eta1=None):
                              inp.sino[s].astype(np.float64), cfg.split == C.SPLIT_CONTIG,
                              rule=cfg.rule, inner=cfg.inner, e1=cfg.e1, rho=cfg.rho, eta1=eta1,
                              e2=cfg.e2, eta2=cfg.eta2, qkind=QKIND[slice_kind(cfg, s)], K=cfg.k,
-                             lloyd=cfg.lloyd, quality=cfg.quality, threads=threads)
+                             lloyd=cfg.lloyd, quality=cfg.quality, threads=threads, projector=cfg.projector)
 
 
 def export_all(ctx, cfg, s=0):

@@ -302,3 +302,17 @@ def test_dct_entropy_coded_payloads(rule):
         total += (16 + len(oracle.jpeg_encode(coef, 4))) * int(deg[m])
     assert ent.stats()["payload_bytes_logical"] == total
     assert total < int(deg.sum()) * (8 + 2 * cfg.N * cfg.N)
+
+
+@pytest.mark.parametrize("prec,tol", [(0, 1e-3), (1, 1e-6)])
+def test_siddon_projector_admm_c1(prec, tol):
+    """NEXT-3: the whole ADMM iteration with the Siddon projector (C1, graph rule, CG5)
+    against the oracle run with the same projector."""
+    cfg = C.C1()
+    cfg.projector, cfg.iters = 1, 10
+    inp = C.make_inputs(cfg)
+    ctx = gpu_context(cfg, inp, precision=prec)
+    ctx.run(cfg.iters)
+    o = oracle_case(cfg, inp).run(cfg.iters)
+    assert rel(ctx.image(), o.image()) <= tol
+    assert rel(ctx.image(), oracle_case(C.C1(), inp).run(cfg.iters).image()) > 10 * tol  # not Joseph

@@ -224,3 +224,44 @@ def test_jpeg_entropy_extremes_and_errors():
     broken[k + 1] = 0xD3  # misnumbered RSTm
     with pytest.raises(tomoq.TomoQError):
         tomoq.jpeg_decode(torch.tensor(broken, device=DEV), 33, 4)
+
+
+# ----------------------------------------------------------------- Siddon (NEXT-3, R-26)
+SIDDON_CASES = [
+    (64, 90, 91, None),                       # C1 geometry: theta = 0 / pi/2 rays on pixel edges
+    (64, 90, 92, list(range(0, 90, 4))),      # even n_det: axis rays through pixel centres
+    (40, 33, 57, [0, 5, 8, 16, 17, 24, 32]),  # ragged tiles
+    (37, 20, 53, None),                       # odd N
+    (8, 4, 13, None),                         # 45 degree rays through corners
+    (256, 180, 363, list(range(3, 180, 8))),  # C2 node 3
+    (200, 100, 283, None),
+]
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("N,n_ang,n_det,sel", SIDDON_CASES)
+def test_siddon_project_backproject_parity(N, n_ang, n_det, sel, prec):
+    img = as_input(phantom(N, N + n_ang + 1), prec)
+    sel_a = np.arange(n_ang) if sel is None else np.asarray(sel)
+    ref = oracle.project_siddon(img, n_ang, n_det, sel_a)
+    got = tomoq.project(torch.tensor(img, dtype=DT[prec], device=DEV), n_ang, n_det, sel_a,
+                        projector=tomoq.PROJ_SIDDON)
+    assert rel(got.cpu().numpy(), ref) <= TOL[prec]
+    y = as_input(np.random.default_rng(N + 1).standard_normal((len(sel_a), n_det)), prec)
+    refb = oracle.backproject_siddon(y, N, n_ang, sel_a)
+    gotb = tomoq.backproject(torch.tensor(y, dtype=DT[prec], device=DEV), N, n_ang, sel_a,
+                             projector=tomoq.PROJ_SIDDON)
+    assert rel(gotb.cpu().numpy(), refb) <= TOL[prec]
+
+
+def test_siddon_axis_rays_exact_half_split():
+    """theta = 0 and pi/2 with even N, odd n_det: every ray on a pixel edge takes half of
+    each neighbouring column / row (R-26) -- exactly, in fp32 and fp64."""
+    N, n_ang, n_det = 32, 8, 47
+    img = phantom(N, 5)
+    for prec in (0, 1):
+        x = as_input(img, prec)
+        got = tomoq.project(torch.tensor(x, dtype=DT[prec], device=DEV), n_ang, n_det, [0, 4],
+                            projector=tomoq.PROJ_SIDDON).cpu().numpy()
+        ref = oracle.project_siddon(x, n_ang, n_det, [0, 4])
+        assert np.max(np.abs(got - ref)) <= (2e-5 if prec == 0 else 1e-12) * np.abs(ref).max()
