@@ -33,6 +33,9 @@ struct KmeansWork {
     float *cen = nullptr;           // [P][K]
     float *thr = nullptr;           // [P][K]
     int *fexp = nullptr;            // [P] fixed-point exponent F
+    int *lut = nullptr;             // [P][1025] final-assignment bucket table (km_lloyd)
+    uint32_t *heads = nullptr;      // [P][<= 8192] first key of each Lloyd super-chunk (km_csum)
+    float *lutmap = nullptr;        // [P][2] bucket map: lo, scale
     void alloc(int P, int K, long long nv);
     void release();
 };

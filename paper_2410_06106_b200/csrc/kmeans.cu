@@ -18,6 +18,7 @@
 // cluster sums are exact integers, hence independent of summation order.
 // All Lloyd iterations of a payload run in one CTA; the cost of an iteration no
 // longer depends on n.  The final assignment packs labels into bit-planes.
+#include <cooperative_groups.h>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
@@ -53,10 +54,22 @@ struct KmPtr {
     int *fexp;
     int K, T;
     long long nv;
+    int *lut;
+    float *lutmap;
+    uint32_t *heads;
 };
 
 KmPtr ptrs(const KmeansWork &w) {
-    return KmPtr{w.keysA, w.keysB, w.hist, w.dtot, w.csum, w.cpre, w.cen, w.thr, w.fexp, w.K, w.T, w.nv};
+    return KmPtr{w.keysA, w.keysB, w.hist, w.dtot, w.csum, w.cpre, w.cen, w.thr, w.fexp, w.K, w.T, w.nv,
+                 w.lut, w.lutmap, w.heads};
+}
+
+// final-assignment bucket map (see km_final): 1024 buckets over [min, max] of the payload
+constexpr int LUT_NB = 1024;
+__device__ __forceinline__ int km_bucket(float v, float lo, float scale) {
+    float t = __fmul_rn(__fsub_rn(v, lo), scale);
+    t = fminf(fmaxf(t, 0.0f), (float)(LUT_NB - 1));
+    return (int)t;
 }
 
 __device__ __forceinline__ void load_tile(const uint32_t *keys, long long off, uint32_t (&k)[KI]) {
@@ -239,7 +252,7 @@ __device__ __forceinline__ int fixed_exp(const uint32_t *sorted, long long nv) {
 
 // chunk (128 keys) sums of fix(v) over the sorted keys: csum[chunk] = exclusive prefix of
 // the chunk sums within its tile, cpre[tile] = the tile's total
-__global__ void __launch_bounds__(KT) km_csum(KmPtr w) {
+__global__ void __launch_bounds__(KT) km_csum(KmPtr w, int sh) {
     __shared__ long long ch[CPT];
     const int b = blockIdx.y, t = blockIdx.x;
     const uint32_t *sorted = w.keysA + (long long)b * w.T * KTILE;
@@ -254,7 +267,12 @@ __global__ void __launch_bounds__(KT) km_csum(KmPtr w) {
         if (i0 + r < w.nv) s += __double2ll_rn((double)key2f(k[r]) * scale);
 #pragma unroll
     for (int o = 1; o < KCH / KI; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);  // KCH/KI lanes per chunk
-    if ((threadIdx.x & (KCH / KI - 1)) == 0) ch[threadIdx.x / (KCH / KI)] = s;
+    if ((threadIdx.x & (KCH / KI - 1)) == 0) {
+        ch[threadIdx.x / (KCH / KI)] = s;
+        // first key of every Lloyd super-chunk (2^sh chunks), contiguous for km_lloyd
+        const long long chunk = (long long)t * CPT + threadIdx.x / (KCH / KI);
+        if ((chunk & ((1LL << sh) - 1)) == 0) w.heads[(long long)b * LSC_MAX + (chunk >> sh)] = k[0];
+    }
     __syncthreads();
     if (threadIdx.x < 32) {
         const long long x = ch[threadIdx.x];
@@ -270,13 +288,21 @@ __global__ void __launch_bounds__(KT) km_csum(KmPtr w) {
     if (t == 0 && threadIdx.x == 0) w.fexp[b] = F;
 }
 
-// All Lloyd iterations of one payload in one CTA.  The sorted keys are split into
-// super-chunks of S = KCH << sh keys (sh chosen so at most LSC_MAX of them); their first
-// keys and the exclusive prefix of fix(v) at their starts live in shared memory, so a
-// threshold query is a shared-memory binary search plus ONE global read of one
-// super-chunk (S / 32 keys per lane), counted and summed by a warp.
-__global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters, int sh) {
-    using Scan = cub::BlockScan<long long, LT>;
+// All Lloyd iterations of one payload in one thread-block cluster of LCL CTAs (one per
+// SM).  Every CTA holds the super-chunk heads of the sorted keys (S = KCH << sh keys
+// each, sh chosen so at most LSC_MAX of them) and the exclusive prefix of fix(v) at their
+// starts in shared memory; CTA r answers the thresholds k = r (mod LCL), one warp each: a
+// warp-parallel search over the heads plus ONE global read of one super-chunk (S / 32
+// keys per lane), counted and summed by the warp.  Each (C_k, S_k) is stored into every
+// CTA's shared memory (DSMEM, double-buffered by iteration parity), one cluster barrier
+// per iteration, and every CTA recomputes the centres from the same integers (identical
+// results).  Rank 0 writes the centres, thresholds and the final-assignment table.
+constexpr int LCL = 8;    // CTAs per payload (portable cluster size)
+constexpr int LCT = 256;  // threads per CTA: LCL * 8 warps >= 64 thresholds
+__global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPtr w, int iters, int sh) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    using Scan = cub::BlockScan<long long, LCT>;
     __shared__ typename Scan::TempStorage tmp;
     extern __shared__ __align__(16) unsigned char lsm[];
     const int T = w.T;
@@ -286,48 +312,49 @@ __global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters, int sh) {
     long long *spre = tpre + T + 1;                                   // [NS] prefix at super-chunk starts
     uint32_t *shead = reinterpret_cast<uint32_t *>(spre + NS);        // [NS] first key of each super-chunk
     __shared__ float cen[256], thr[256];
-    __shared__ long long Cs[256], Ss[256], total_s;
-    const int b = blockIdx.x, K = w.K;
+    __shared__ long long Cs[2][256], Ss[2][256], total_s;
+    const int rank = (int)cluster.block_rank();
+    const int b = blockIdx.x / LCL, K = w.K;
     const long long nv = w.nv, nch = (long long)T * CPT;
     const uint32_t *sorted = w.keysA + (long long)b * T * KTILE;
     const long long *cp = w.csum + (long long)b * nch;  // in-tile exclusive chunk prefix
     const long long *ts = w.cpre + (long long)b * T;    // tile totals
     const double scale = ldexp(1.0, w.fexp[b]);
-    {  // exclusive prefix over the (<= 4096) tile totals: 4 per thread
-        long long x[4], run = 0;
+    {  // exclusive prefix over the (<= 4096) tile totals: 16 per thread
+        constexpr int TPT = MAX_TILES / LCT;
+        long long x[TPT], run = 0;
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const int t = 4 * threadIdx.x + u;
+        for (int u = 0; u < TPT; u++) {
+            const int t = TPT * threadIdx.x + u;
             x[u] = t < T ? ts[t] : 0;
             run += x[u];
         }
         long long ex, carry;
         Scan(tmp).ExclusiveSum(run, ex, carry);
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const int t = 4 * threadIdx.x + u;
+        for (int u = 0; u < TPT; u++) {
+            const int t = TPT * threadIdx.x + u;
             if (t < T) tpre[t] = ex;
             ex += x[u];
         }
         if (threadIdx.x == 0) total_s = carry;
     }
     __syncthreads();
-    // super-chunk heads and prefixes: all global loads of a thread issued before any use
-    constexpr int SPT = LSC_MAX / LT;  // <= 8 super-chunks per thread
-    {
+    // super-chunk heads and prefixes: 8 global loads of a thread in flight per round
+    constexpr int SPT = 8;
+    for (int c0 = 0; c0 < NS; c0 += SPT * LCT) {
         uint32_t hv[SPT];
         long long pv[SPT];
 #pragma unroll
         for (int u = 0; u < SPT; u++) {
-            const int c = threadIdx.x + u * LT;
+            const int c = c0 + threadIdx.x + u * LCT;
             const long long k0 = (long long)c * S;
-            const long long ci = k0 / KCH;  // chunk index = t * CPT + in-tile chunk
-            hv[u] = c < NS ? sorted[k0] : 0u;
-            pv[u] = c < NS ? cp[ci] : 0;
+            hv[u] = c < NS ? w.heads[(long long)b * LSC_MAX + c] : 0u;
+            pv[u] = c < NS ? cp[k0 / KCH] : 0;
         }
 #pragma unroll
         for (int u = 0; u < SPT; u++) {
-            const int c = threadIdx.x + u * LT;
+            const int c = c0 + threadIdx.x + u * LCT;
             if (c < NS) {
                 shead[c] = hv[u];
                 spre[c] = tpre[(int)(((long long)c * S) / KTILE)] + pv[u];
@@ -335,97 +362,115 @@ __global__ void __launch_bounds__(LT) km_lloyd(KmPtr w, int iters, int sh) {
         }
     }
     // quantile init: c_k = v_(floor((2k+1) nv / 2K))
-    for (int k = threadIdx.x; k < K; k += LT) cen[k] = key2f(sorted[((long long)(2 * k + 1) * nv) / (2LL * K)]);
-    __syncthreads();
+    for (int k = threadIdx.x; k < K; k += LCT) cen[k] = key2f(sorted[((long long)(2 * k + 1) * nv) / (2LL * K)]);
+    cluster.sync();  // every CTA of the cluster started (DSMEM targets exist) and staged
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int per_lane = S / 32;
     for (int it = 0; it < iters; it++) {
-        for (int k = threadIdx.x; k + 1 < K; k += LT) thr[k] = (float)(((double)cen[k] + (double)cen[k + 1]) * 0.5);
+        const int buf = it & 1;
+        for (int k = threadIdx.x; k + 1 < K; k += LCT) thr[k] = (float)(((double)cen[k] + (double)cen[k + 1]) * 0.5);
         __syncthreads();
-        // two thresholds per warp at a time: their dependent global loads overlap
-        for (int k0 = warp; k0 + 1 < K; k0 += 2 * (LT / 32)) {
-            int kk[2], cc[2];
-            uint32_t kb[2];
-#pragma unroll
-            for (int q = 0; q < 2; q++) {
-                kk[q] = k0 + q * (LT / 32);
-                kb[q] = kk[q] + 1 < K ? f2key(thr[kk[q]]) : 0u;
-                // last super-chunk whose head key <= kb: warp-parallel search over strides
-                // 256, 8, 1 (heads are sorted; NS <= 8192 = 32 * 32 * 8)
-                int c = -1;
-                const int i1 = lane * 256;
-                const unsigned m1 = __ballot_sync(0xffffffffu, i1 < NS && shead[i1] <= kb[q]);
-                if (m1) {
-                    const int b1 = (31 - __clz(m1)) * 256;
-                    const int i2 = b1 + lane * 8;
-                    const unsigned m2 = __ballot_sync(0xffffffffu, i2 < NS && shead[i2] <= kb[q]);
-                    const int b2 = b1 + (31 - __clz(m2)) * 8;
-                    const int i3 = b2 + lane;
-                    const unsigned m3 = __ballot_sync(0xffffffffu, lane < 8 && i3 < NS && shead[i3] <= kb[q]);
-                    c = b2 + (31 - __clz(m3));
-                }
-                cc[q] = kk[q] + 1 < K ? c : -1;
+        const int kk = rank + LCL * warp;  // this warp's threshold (at most one: K <= 256 < LCL * 8 * 4)
+        for (int k0 = kk; k0 + 1 < K; k0 += LCL * (LCT / 32)) {
+            const uint32_t kb = f2key(thr[k0]);
+            // last super-chunk whose head key <= kb: warp-parallel search over strides 256, 8, 1
+            int c = -1;
+            const int i1 = lane * 256;
+            const unsigned m1 = __ballot_sync(0xffffffffu, i1 < NS && shead[i1] <= kb);
+            if (m1) {
+                const int b1 = (31 - __clz(m1)) * 256;
+                const int i2 = b1 + lane * 8;
+                const unsigned m2 = __ballot_sync(0xffffffffu, i2 < NS && shead[i2] <= kb);
+                const int b2 = b1 + (31 - __clz(m2)) * 8;
+                const int i3 = b2 + lane;
+                const unsigned m3 = __ballot_sync(0xffffffffu, lane < 8 && i3 < NS && shead[i3] <= kb);
+                c = b2 + (31 - __clz(m3));
             }
-            int cnt[2] = {0, 0};
-            long long sm[2] = {0, 0};
-            for (int u0 = 0; u0 < per_lane; u0 += 4) {
-                uint32_t e[2][4];
+            int cnt = 0;
+            long long sm = 0;
+            if (c >= 0) {
+                for (int u0 = 0; u0 < per_lane; u0 += 4) {
+                    uint32_t e[4];
 #pragma unroll
-                for (int q = 0; q < 2; q++)
-#pragma unroll
-                    for (int u = 0; u < 4; u++)
-                        e[q][u] = cc[q] >= 0 ? sorted[(long long)cc[q] * S + 32 * (u0 + u) + lane] : 0xffffffffu;
-#pragma unroll
-                for (int q = 0; q < 2; q++)
+                    for (int u = 0; u < 4; u++) e[u] = sorted[(long long)c * S + 32 * (u0 + u) + lane];
 #pragma unroll
                     for (int u = 0; u < 4; u++)
-                        if (cc[q] >= 0 && e[q][u] <= kb[q] && (long long)cc[q] * S + 32 * (u0 + u) + lane < nv) {
-                            cnt[q]++;
-                            sm[q] += __double2ll_rn((double)key2f(e[q][u]) * scale);
+                        if (e[u] <= kb && (long long)c * S + 32 * (u0 + u) + lane < nv) {
+                            cnt++;
+                            sm += __double2ll_rn((double)key2f(e[u]) * scale);
                         }
+                }
             }
 #pragma unroll
-            for (int q = 0; q < 2; q++) {
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    cnt[q] += __shfl_xor_sync(0xffffffffu, cnt[q], o);
-                    sm[q] += __shfl_xor_sync(0xffffffffu, sm[q], o);
-                }
-                if (lane == 0 && kk[q] + 1 < K) {
-                    Cs[kk[q]] = cc[q] >= 0 ? (long long)cc[q] * S + cnt[q] : 0;
-                    Ss[kk[q]] = cc[q] >= 0 ? spre[cc[q]] + sm[q] : 0;
-                }
+            for (int o = 16; o > 0; o >>= 1) {
+                cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+                sm += __shfl_xor_sync(0xffffffffu, sm, o);
+            }
+            const long long cv = c >= 0 ? (long long)c * S + cnt : 0;
+            const long long sv = c >= 0 ? spre[c] + sm : 0;
+            if (lane < LCL) {  // lane r stores into CTA r's shared memory
+                *cluster.map_shared_rank(&Cs[buf][k0], lane) = cv;
+                *cluster.map_shared_rank(&Ss[buf][k0], lane) = sv;
             }
         }
-        __syncthreads();
-        for (int k = threadIdx.x; k < K; k += LT) {
-            const long long c1 = k + 1 < K ? Cs[k] : nv, c0 = k ? Cs[k - 1] : 0;
-            const long long s1 = k + 1 < K ? Ss[k] : total_s, s0 = k ? Ss[k - 1] : 0;
+        cluster.sync();  // all (C_k, S_k) of this iteration delivered everywhere
+        for (int k = threadIdx.x; k < K; k += LCT) {
+            const long long c1 = k + 1 < K ? Cs[buf][k] : nv, c0 = k ? Cs[buf][k - 1] : 0;
+            const long long s1 = k + 1 < K ? Ss[buf][k] : total_s, s0 = k ? Ss[buf][k - 1] : 0;
             if (c1 > c0) cen[k] = (float)(((double)(s1 - s0) / scale) / (double)(c1 - c0));
         }
         __syncthreads();
     }
-    for (int k = threadIdx.x; k < K; k += LT) {
-        w.cen[(long long)b * K + k] = cen[k];
-        if (k + 1 < K) w.thr[(long long)b * K + k] = (float)(((double)cen[k] + (double)cen[k + 1]) * 0.5);
+    if (rank != 0) {
+        cluster.sync();  // keep this CTA's shared memory alive until every remote store landed
+        return;
     }
+    // final thresholds and the final assignment's bucket table: cnt[q] = #{k : bucket(thr_k) < q}
+    const float lo = key2f(sorted[0]), span = __fsub_rn(key2f(sorted[nv - 1]), lo);
+    const float bscale = (span > 0.0f && span < INFINITY) ? (float)LUT_NB / span : 0.0f;
+    __shared__ int bk[256];
+    for (int k = threadIdx.x; k < K; k += LCT) {
+        w.cen[(long long)b * K + k] = cen[k];
+        if (k + 1 < K) {
+            const float t = (float)(((double)cen[k] + (double)cen[k + 1]) * 0.5);
+            w.thr[(long long)b * K + k] = t;
+            bk[k] = km_bucket(t, lo, bscale);
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q <= LUT_NB; q += LCT) {
+        int l0 = 0, h0 = K - 1;
+        while (l0 < h0) {
+            const int mid = (l0 + h0) >> 1;
+            if (bk[mid] < q) l0 = mid + 1; else h0 = mid;
+        }
+        w.lut[(long long)b * (LUT_NB + 1) + q] = l0;
+    }
+    if (threadIdx.x == 0) { w.lutmap[2 * b] = lo; w.lutmap[2 * b + 1] = bscale; }
+    cluster.sync();
 }
 
-// final assignment: label(v) = #{k : v > thr[k]} by a branchless search over the
-// thresholds padded with +inf to 2^B - 1 entries; lane `bit` stores bit-plane `bit`
-// of its warp's 32-element group.  U groups per warp per step (loads in flight).
+// final assignment: label(v) = #{k : v > thr[k]}.  A 1024-bucket table over the payload's
+// [min, max] (the first and last sorted keys) maps v to the thresholds that share its
+// bucket: with bucket() monotone (one rounded subtraction and one rounded product), every
+// threshold in an earlier bucket is < v and every one in a later bucket is > v, so
+// label = cnt[b] + #{k in bucket b : v > thr_k} -- exact, usually zero or one comparison.
+// Lane `bit` stores bit-plane `bit` of its warp's 32-element group; U groups per warp
+// per step (loads in flight).
 template <int B, typename TO>
 __global__ void __launch_bounds__(KT) km_final(const float *const *vin, KmPtr w, uint8_t *const *pay,
                                                int32_t *const *labels_tab, TO *const *dec_out) {
-    __shared__ float thr_s[256];
+    __shared__ float thr_s[256], cen_s[256];
+    __shared__ int cnt_s[LUT_NB + 1];
     const int b = blockIdx.y;
     const int K = w.K;
+    const float lo = w.lutmap[2 * b], scale = w.lutmap[2 * b + 1];
     for (int k = threadIdx.x; k < 256; k += KT) thr_s[k] = (k + 1 < K) ? w.thr[(long long)b * K + k] : INFINITY;
+    for (int q = threadIdx.x; q <= LUT_NB; q += KT) cnt_s[q] = w.lut[(long long)b * (LUT_NB + 1) + q];
     float *cen_out = reinterpret_cast<float *>(pay[b]);
     uint32_t *planes = reinterpret_cast<uint32_t *>(pay[b] + 4 * (long long)K);
     int32_t *labels = labels_tab ? labels_tab[b] : nullptr;
     TO *dec = dec_out ? dec_out[b] : nullptr;  // fused decode of this (local) payload
-    __shared__ float cen_s[256];
     for (int k = threadIdx.x; k < K; k += KT) {
         cen_s[k] = w.cen[(long long)b * K + k];
         if (blockIdx.x == 0) cen_out[k] = cen_s[k];
@@ -447,19 +492,21 @@ __global__ void __launch_bounds__(KT) km_final(const float *const *vin, KmPtr w,
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            int l = 0;
-#pragma unroll
-            for (int step = (1 << B) >> 1; step > 0; step >>= 1) l += (v[u] > thr_s[l + step - 1]) ? step : 0;
+            const int q = km_bucket(v[u], lo, scale);
+            int l = cnt_s[q];
+            const int e = cnt_s[q + 1];
+            for (int k = l; k < e; k++) l += v[u] > thr_s[k] ? 1 : 0;
             const long long i = (g0 + u) * 32 + lane;
             if (labels && i < nv) labels[i] = l;
             if (dec && i < nv) dec[i] = (TO)cen_s[l];
-            uint32_t mine = 0;
+            // the B ballot words are warp-uniform: lane 0 stores them (no per-lane select)
+            uint32_t word[B > 0 ? B : 1];
 #pragma unroll
-            for (int bit = 0; bit < B; bit++) {
-                const uint32_t word = __ballot_sync(0xffffffffu, (l >> bit) & 1);
-                mine = lane == bit ? word : mine;
+            for (int bit = 0; bit < B; bit++) word[bit] = __ballot_sync(0xffffffffu, l & (1 << bit));
+            if (lane == 0 && g0 + u < G) {
+#pragma unroll
+                for (int bit = 0; bit < B; bit++) planes[(g0 + u) * B + bit] = word[bit];
             }
-            if (lane < B && g0 + u < G) planes[(g0 + u) * B + lane] = mine;
         }
     }
 }
@@ -544,12 +591,15 @@ void KmeansWork::alloc(int P_, int K_, long long nv_) {
     TQ_CHECK_CUDA(cudaMalloc(&cen, sizeof(float) * P * K));
     TQ_CHECK_CUDA(cudaMalloc(&thr, sizeof(float) * P * K));
     TQ_CHECK_CUDA(cudaMalloc(&fexp, sizeof(int) * P));
+    TQ_CHECK_CUDA(cudaMalloc(&lut, sizeof(int) * P * (LUT_NB + 1)));
+    TQ_CHECK_CUDA(cudaMalloc(&lutmap, sizeof(float) * 2 * P));
+    TQ_CHECK_CUDA(cudaMalloc(&heads, sizeof(uint32_t) * P * LSC_MAX));
     TQ_CHECK_CUDA(cudaFuncSetAttribute(km_lloyd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lloyd_smem(T)));
 }
 
 void KmeansWork::release() {
     for (void *p : {(void *)keysA, (void *)keysB, (void *)hist, (void *)dtot, (void *)csum, (void *)cpre, (void *)cen,
-                    (void *)thr, (void *)fexp})
+                    (void *)thr, (void *)fexp, (void *)lut, (void *)lutmap, (void *)heads})
         if (p) cudaFree(p);
     *this = KmeansWork();
 }
@@ -571,8 +621,8 @@ int kmeans_encode(const float *const *v, KmeansWork &ws, int lloyd, uint8_t *con
         std::swap(src, dst);
     }
     // four passes: A -> B -> A -> B -> A, sorted keys in keysA
-    km_csum<<<tiles, KT, 0, st>>>(w);
-    km_lloyd<<<P, LT, lloyd_smem(ws.T), st>>>(w, lloyd, lloyd_shift(ws.T));
+    km_csum<<<tiles, KT, 0, st>>>(w, lloyd_shift(ws.T));
+    km_lloyd<<<LCL * P, LCT, lloyd_smem(ws.T), st>>>(w, lloyd, lloyd_shift(ws.T));
     long long want = std::max(1LL, (148LL * 8 + P - 1) / P);
     long long need = (ws.nv + KT * 16 - 1) / (KT * 16);
     const dim3 grid((unsigned)std::max(1LL, std::min(want, need)), P);

@@ -57,6 +57,31 @@ def random_ellipses(n_ellipses: int, N: int, seed: int) -> Ellipses:
     return Ellipses(rad * np.cos(ang), rad * np.sin(ang), a, b, phi, rho)
 
 
+def three_level_phantom(N: int, seed: int) -> Ellipses:
+    """Paper-shaped stand-in for the ToMoBAR Phantom ("three
+    distinct gray levels"): a body ellipse of level 0.5 (semi-axes 0.80R x 0.68R, tilted
+    0.1 rad) holding 5..8 disjoint inner ellipses that add 0.5 (level 1.0) -- background 0,
+    body 0.5, features 1.0.  Inner semi-axes ~ U[0.06R, 0.22R], centres drawn until the
+    inner ellipses' bounding circles are disjoint and inside 0.85 of the body."""
+    g = _rng(seed)
+    R = N / 2.0
+    x0, y0, a, b, phi, rho = [0.0], [0.0], [0.80 * R], [0.68 * R], [0.1], [0.5]
+    n_in = int(g.integers(5, 9))
+    circles = []
+    tries = 0
+    while len(circles) < n_in and tries < 10000:
+        tries += 1
+        ai, bi = g.uniform(0.06 * R, 0.22 * R), g.uniform(0.06 * R, 0.22 * R)
+        r = max(ai, bi)
+        ang, rad = g.uniform(0, 2 * np.pi), np.sqrt(g.uniform()) * 0.85 * (0.68 * R - r)
+        cx, cy = rad * np.cos(ang), rad * np.sin(ang)
+        if all(math.hypot(cx - x, cy - y) > r + q + 1.0 for x, y, q in circles):
+            circles.append((cx, cy, r))
+            x0.append(cx); y0.append(cy); a.append(ai); b.append(bi)
+            phi.append(g.uniform(0, np.pi)); rho.append(0.5)
+    return Ellipses(np.array(x0), np.array(y0), np.array(a), np.array(b), np.array(phi), np.array(rho))
+
+
 def pixel_centres(N: int):
     """x_c = c - (N-1)/2 (c = column), y_r = (N-1)/2 - r (r = row, row 0 on top)."""
     c = np.arange(N, dtype=np.float64)
