@@ -261,16 +261,24 @@ tq_status tq_backproject(const tq_geometry *g, const int32_t *sel, int32_t n_sel
         const int zero = 0;
         int *row0 = t.up(&zero, 1), *nang = t.up(&n_sel, 1);
         cudaStream_t st = (cudaStream_t)stream;
+        // guarded copy: zero bins at 0 and n_det + 1 of every row, SPAD zeros around (BpArgs::s)
+        const size_t es = precision ? 8 : 4;
+        const long long sp = g->n_det + 2;
+        uint8_t *gs = (uint8_t *)t.get(es * ((size_t)n_sel * sp + 2 * SPAD));
+        TQ_CHECK_CUDA(cudaMemsetAsync(gs, 0, es * ((size_t)n_sel * sp + 2 * SPAD), st));
+        TQ_CHECK_CUDA(cudaMemcpy2DAsync(gs + es * (SPAD + 1), es * sp, sino, es * g->n_det, es * g->n_det, n_sel,
+                                        cudaMemcpyDeviceToDevice, st));
+        const void *sg = gs + es * SPAD;
         if (precision == 0) {
             BpArgs<float> a{};
-            a.s = (const float *)sino; a.s_stride = g->n_det; a.s_off = 0;
+            a.s = (const float *)sg; a.s_stride = (int)sp; a.s_off = 1;
             a.node_row0 = row0; a.node_nang = nang; a.rows = rd; a.trig = geo.trig; a.xmaj = geo.xmaj;
             a.N = g->image_side; a.n_det = g->n_det; a.n = geo.n; a.out = (float *)img; a.magic = kMagicBits4;
             a.siddon = geo.proj;
             launch_bp(0, EPI_PLAIN, &a, 1, g->image_side, st);
         } else {
             BpArgs<double> a{};
-            a.s = (const double *)sino; a.s_stride = g->n_det; a.s_off = 0;
+            a.s = (const double *)sg; a.s_stride = (int)sp; a.s_off = 1;
             a.node_row0 = row0; a.node_nang = nang; a.rows = rd; a.trig = geo.trig; a.xmaj = geo.xmaj;
             a.N = g->image_side; a.n_det = g->n_det; a.n = geo.n; a.out = (double *)img; a.magic = kMagicBits4;
             a.siddon = geo.proj;

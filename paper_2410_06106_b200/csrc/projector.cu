@@ -781,6 +781,7 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
     __shared__ double s_tau[BP_MAXA], s_csd[BP_MAXA], s_snd[BP_MAXA];
     __shared__ T s_cs[BP_MAXA], s_sn[BP_MAXA], s_im[BP_MAXA], s_a1[BP_MAXA], s_a0[BP_MAXA];
     __shared__ int s_jlo[BP_MAXA];
+    __shared__ const T *s_src[BP_MAXA];
     __shared__ double red[BP_THREADS / 32 + 1];
     __shared__ bool last_flag;
     const int node = blockIdx.y;
@@ -796,13 +797,21 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
     if (pre) {
         const long long nb0 = (long long)node * a.n;
         const uint32_t eps = (uint32_t)__cvta_generic_to_shared(ep);
-        for (int c = threadIdx.x; c < NEP * BP_TS * BP_TS / 4; c += BP_THREADS) {
-            const int o = c / (BP_TS * BP_TS / 4), cc = c % (BP_TS * BP_TS / 4);
-            const int r = r0 + cc / (BP_TS / 4), col = c0 + 4 * (cc % (BP_TS / 4));
+        // thread t copies the 16-byte pieces (row t/16 + 16 i, columns 4 (t%16) .. +3) of each operand
+        constexpr int RPI = BP_THREADS / (BP_TS / 4);  // rows per pass (16)
+        const int tr = threadIdx.x / (BP_TS / 4), tc = 4 * (threadIdx.x % (BP_TS / 4));
+        const bool col_ok = c0 + tc < N;
+#pragma unroll
+        for (int o = 0; o < NEP; o++) {
             const float *src = reinterpret_cast<const float *>(o == 0 ? (const void *)a.vin : (const void *)a.bprime) + nb0;
-            const bool ok = r < N && col < N;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(eps + 16u * c),
-                         "l"(ok ? src + (long long)r * N + col : src), "r"(ok ? 16 : 0));
+            const float *p0 = src + (long long)(r0 + tr) * N + c0 + tc;
+            const uint32_t d0 = eps + 4u * (o * BP_TS * BP_TS + tr * BP_TS + tc);
+#pragma unroll
+            for (int i = 0; i < BP_TS / RPI; i++) {
+                const bool ok = col_ok && r0 + tr + RPI * i < N;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d0 + 4u * RPI * BP_TS * i),
+                             "l"(ok ? p0 + (long long)RPI * i * N : src), "r"(ok ? 16 : 0));
+            }
         }
         asm volatile("cp.async.commit_group;");
     }
@@ -825,6 +834,7 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
             const double tmin = tp0 + fmin(0.0, ext * cs) + fmin(0.0, -ext * sn);
             const int jlo = (int)floor(tmin - t0) - 1;  // one bin of margin below
             s_jlo[k] = jlo;
+            s_src[k] = a.s + (long long)(row0 + k0 + k) * a.s_stride + a.s_off + jlo;
             s_tau[k] = tp0 - t0 - (double)jlo;  // tile-relative bin coordinate of pixel (r0, c0)
             s_csd[k] = cs;
             s_snd[k] = sn;
@@ -844,17 +854,13 @@ __global__ void __launch_bounds__(BP_THREADS) bp_tile_kernel(const BpArgs<T> a) 
             }
         }
         __syncthreads();
+        // bins of the window: zero guards / pads stand in for j < 0 and j >= n_det (SPAD)
         for (int i = threadIdx.x; i < kc * BP_WB; i += BP_THREADS) {
             const int k = i / BP_WB, w = i - k * BP_WB;
-            const int j = s_jlo[k] + w;
-            const T *srow = a.s + (long long)(row0 + k0 + k) * a.s_stride + a.s_off;
-            const T v = (j >= 0 && j < a.n_det) ? srow[j] * s_im[k] : (T)0;
-            if constexpr (sizeof(T) == 4) {
-                const T v1 = (j + 1 >= 0 && j + 1 < a.n_det) ? srow[j + 1] * s_im[k] : (T)0;
-                win2[i] = make_float2(v, v1);
-            } else {
-                win[i] = v;
-            }
+            const T *p = s_src[k] + w;
+            const T im = s_im[k];
+            if constexpr (sizeof(T) == 4) win2[i] = make_float2(__ldg(p) * im, __ldg(p + 1) * im);
+            else win[i] = __ldg(p) * im;
         }
         __syncthreads();
         for (int k = 0; k < kc; k++) {

@@ -35,6 +35,10 @@
 namespace tq {
 
 enum BpEpi { EPI_PLAIN = 0, EPI_CGQ = 1, EPI_RESID = 2, EPI_GD = 3 };
+// zero elements before and after a backprojector input (rows with zero guard bins at 0 and
+// n_det + 1): the 96-bin windows are staged without bounds checks; slots outside
+// [-1, n_det] only feed pixels outside the image
+constexpr int SPAD = 256;
 enum ScalSlot { S_RR = 0, S_PQ = 1, S_ALPHA = 2, S_RRNEW = 3, S_BETA = 4, S_NORM = 5, S_NSLOT = 8 };
 
 // forward tile geometry
@@ -116,7 +120,8 @@ struct FpRedArgs {
 
 template <typename T>
 struct BpArgs {
-    const T *s;              // [n_rows][s_stride] + s_off
+    const T *s;              // [n_rows][s_stride] + s_off; s_off >= 1 zero guard bins each side,
+                             // SPAD zero elements before row 0 and after the last row
     int s_stride, s_off;
     const int *node_row0;    // [L] first ray row of each node
     const int *node_nang;    // [L]

@@ -78,7 +78,10 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
     TQ_CHECK_CUDA(cudaDeviceSynchronize());
     for (void **v : {&X, &R, &P, &Q, &BP}) A(v, es * n * L);
     A(&D, es * (size_t)n_rows * g.n_det);
-    A(&S, es * (size_t)n_rows * sp);
+    // S rows carry a zero guard bin at 0 and n_det + 1; SPAD zero elements before and after the
+    // whole array let the backprojector stage its fixed 96-bin windows without bounds checks
+    A(&S_base, es * ((size_t)n_rows * sp + 2 * SPAD));
+    S = (uint8_t *)S_base + es * SPAD;
     A((void **)&cnode, sizeof(double) * L);
     A((void **)&eta, sizeof(double) * L);
     A((void **)&scal, sizeof(double) * S_NSLOT * L);
@@ -87,13 +90,13 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
 }
 
 void Inner::release() {
-    for (void *p : {(void *)rows, (void *)row0, (void *)nang, X, R, P, Q, BP, D, S, (void *)cnode,
+    for (void *p : {(void *)rows, (void *)row0, (void *)nang, X, R, P, Q, BP, D, S_base, (void *)cnode,
                     (void *)eta, (void *)scal, (void *)partial, (void *)counter, (void *)olist,
                     (void *)oofs, fpart, (void *)fwin, (void *)frg, (void *)frec, (void *)futab})
         if (p) cudaFree(p);
     rows = nullptr; row0 = nang = olist = oofs = nullptr;
     fpart = nullptr; fwin = nullptr; frg = nullptr; frec = nullptr; futab = nullptr;
-    X = R = P = Q = BP = D = S = nullptr;
+    X = R = P = Q = BP = D = S = S_base = nullptr;
     cnode = eta = scal = partial = nullptr;
     counter = nullptr;
 }

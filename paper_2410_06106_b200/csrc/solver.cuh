@@ -37,7 +37,8 @@ struct Inner {
     int nt_line = 0, nt_cross = 0;
     void *X = nullptr, *R = nullptr, *P = nullptr, *Q = nullptr, *BP = nullptr;  // [L][n]
     void *D = nullptr;         // [n_rows][n_det]
-    void *S = nullptr;         // [n_rows][sp], guard column at 0 and n_det+1
+    void *S = nullptr;         // [n_rows][sp], guard column at 0 and n_det+1 (inside S_base)
+    void *S_base = nullptr;    // S with SPAD zero elements before and after
     double *cnode = nullptr, *eta = nullptr;  // [L]
     double *scal = nullptr;    // [L][S_NSLOT]
     double *partial = nullptr; // [L][part_stride]
