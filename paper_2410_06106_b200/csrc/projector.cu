@@ -738,33 +738,45 @@ __global__ void fp_unit_kernel(const int *oofs, const FpRec *recs, int n_olist, 
 }
 
 // ------------------------------------------------------------------ forward: reduction
-// s[row][j] = (1/m) * sum over line bands (in order) of the two parity slots; RESID: d - A x.
+// s[row][j] = (1/m) * sum over line bands of the two parity slots; RESID: d - A x.
+// RG groups of threads split the bands of 32 bins (one round of <= 16 independent loads
+// per thread for nt_line <= 8 RG), then the group partials are added in a fixed order in
+// shared memory (deterministic, no atomics).
+constexpr int RJ = 32, RG = 4;  // bins per CTA, band groups
 template <typename T, bool RESID>
-__global__ void __launch_bounds__(128) fp_reduce_kernel(const FpRedArgs<T> a) {
+__global__ void __launch_bounds__(RJ * RG) fp_reduce_kernel(const FpRedArgs<T> a) {
+    __shared__ T part[RG][RJ];
     const int row = blockIdx.y;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= a.n_det) return;
+    const int jj = threadIdx.x % RJ, g = threadIdx.x / RJ;
+    const int j = blockIdx.x * RJ + jj;
+    const int nb = a.nt_line;
+    const int per = (nb + RG - 1) / RG;
+    const int l0 = g * per, l1 = min(nb, l0 + per);
+    T acc = 0;
+    if (j < a.n_det) {
+        const T *p = a.partial + (long long)row * nb * 2 * a.n_det + j;
+        int lt = l0;
+        for (; lt + 8 <= l1; lt += 8) {  // 16 loads in flight
+            T x[16];
+#pragma unroll
+            for (int u = 0; u < 16; u++) x[u] = p[(long long)(2 * lt + u) * a.n_det];
+            T s8[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) s8[u] = x[2 * u] + x[2 * u + 1];
+            acc += ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+        }
+        for (; lt < l1; lt++) acc += p[(long long)(2 * lt) * a.n_det] + p[(long long)(2 * lt + 1) * a.n_det];
+    }
+    part[g][jj] = acc;
+    __syncthreads();
+    if (g != 0 || j >= a.n_det) return;
+    T tot = part[0][jj];
+#pragma unroll
+    for (int q = 1; q < RG; q++) tot += part[q][jj];
     const int ang = a.rows[row].angle;
     const double2 t2 = a.trig[ang];
     const double inv_m = a.xmaj[ang] ? 1.0 / fabs(t2.y) : 1.0 / fabs(t2.x);
-    const T *p = a.partial + (long long)row * a.nt_line * 2 * a.n_det + j;
-    // 16 independent loads in flight per step; fixed summation order (deterministic)
-    T acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int lt = 0;
-    for (; lt + 8 <= a.nt_line; lt += 8) {
-        T x[16];
-#pragma unroll
-        for (int u = 0; u < 16; u++) x[u] = p[(long long)u * a.n_det];
-#pragma unroll
-        for (int u = 0; u < 8; u++) acc[u] += x[2 * u] + x[2 * u + 1];
-        p += 16LL * a.n_det;
-    }
-    for (; lt < a.nt_line; lt++) {
-        acc[lt & 7] += p[0] + p[a.n_det];
-        p += 2LL * a.n_det;
-    }
-    const T acc0 = (acc[0] + acc[1]) + (acc[2] + acc[3]), acc1 = (acc[4] + acc[5]) + (acc[6] + acc[7]);
-    T v = (T)((double)(acc0 + acc1) * inv_m);
+    T v = (T)((double)tot * inv_m);
     if (RESID) v = a.d[(long long)row * a.n_det + j] - v;
     a.out[(long long)row * a.out_stride + a.out_off + j] = v;
 }
@@ -1123,15 +1135,15 @@ void launch_fp_setup(const RayRow *rows, const int *xmaj, const double2 *trig, i
 
 void launch_fp_reduce(int prec, bool resid, const void *args, int n_rows, int n_det, cudaStream_t st) {
     if (n_rows == 0) return;
-    const dim3 grid(ceil_div(n_det, 128), n_rows);
+    const dim3 grid(ceil_div(n_det, RJ), n_rows);
     if (prec == 0) {
         const auto &A = *static_cast<const FpRedArgs<float> *>(args);
-        if (resid) fp_reduce_kernel<float, true><<<grid, 128, 0, st>>>(A);
-        else fp_reduce_kernel<float, false><<<grid, 128, 0, st>>>(A);
+        if (resid) fp_reduce_kernel<float, true><<<grid, RJ * RG, 0, st>>>(A);
+        else fp_reduce_kernel<float, false><<<grid, RJ * RG, 0, st>>>(A);
     } else {
         const auto &A = *static_cast<const FpRedArgs<double> *>(args);
-        if (resid) fp_reduce_kernel<double, true><<<grid, 128, 0, st>>>(A);
-        else fp_reduce_kernel<double, false><<<grid, 128, 0, st>>>(A);
+        if (resid) fp_reduce_kernel<double, true><<<grid, RJ * RG, 0, st>>>(A);
+        else fp_reduce_kernel<double, false><<<grid, RJ * RG, 0, st>>>(A);
     }
     TQ_CHECK_CUDA(cudaGetLastError());
 }
