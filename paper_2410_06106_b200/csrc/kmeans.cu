@@ -16,8 +16,9 @@
 //     cluster -- the same decision the oracle takes per element.
 // fix(v) = round(v 2^F) as int64 with F chosen from max|v| and n so no sum overflows:
 // cluster sums are exact integers, hence independent of summation order.
-// All Lloyd iterations of a payload run in one CTA; the cost of an iteration no
-// longer depends on n.  The final assignment packs labels into bit-planes.
+// All Lloyd iterations of a payload run in one thread-block cluster (8 CTAs exchanging
+// (C_k, S_k) through distributed shared memory); the cost of an iteration does not
+// depend on n.  The final assignment (bucket table) packs labels into bit-planes.
 #include <cooperative_groups.h>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
@@ -31,7 +32,6 @@ namespace {
 constexpr int KT = 256;               // threads of the per-tile kernels
 constexpr int KI = 16;                // keys per thread
 constexpr int KTILE = KT * KI;        // keys per tile
-constexpr int LT = 1024;              // threads of the Lloyd kernel
 constexpr int MAX_TILES = 4096;       // per payload (n <= 16.7 M)
 constexpr int KCH = 128;              // keys per prefix-sum chunk
 constexpr int CPT = KTILE / KCH;      // chunks per tile (32)
