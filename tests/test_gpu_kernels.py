@@ -265,3 +265,30 @@ def test_siddon_axis_rays_exact_half_split():
                             projector=tomoq.PROJ_SIDDON).cpu().numpy()
         ref = oracle.project_siddon(x, n_ang, n_det, [0, 4])
         assert np.max(np.abs(got - ref)) <= (2e-5 if prec == 0 else 1e-12) * np.abs(ref).max()
+
+
+def test_kmeans_ties_and_extreme_ranges():
+    """Values equal to a threshold go to the lower cluster on both sides (R-16); the final
+    assignment's bucket map stays exact when the payload range overflows fp32 (max - min =
+    inf) or is a handful of discrete levels.  (Cluster sums are fixed-point integers with
+    resolution 2^(E + ceil(log2 n) - 62), E = exponent of max|v| -- DESIGN.md R-16: exact
+    for the iterates' dynamic range; a payload mixing +-3e38 with O(1) values is outside it,
+    so that case checks only the assignment against the GPU's own centres.)"""
+    rng = np.random.default_rng(3)
+    for v, K in ((rng.integers(0, 3, 5000).astype(np.float32), 2),           # {0, 1, 2}: thresholds hit values
+                 (np.repeat(np.arange(10, dtype=np.float32), 300), 4),       # ten levels
+                 ((rng.standard_normal(6000) * 1e-20).astype(np.float32), 16)):  # tiny values
+        cen_r, lab_r = oracle.kmeans_encode(v, K, 10)
+        cen, planes, lab = tomoq.kmeans_encode(torch.tensor(v, device=DEV), K, 10)
+        assert np.array_equal(lab.cpu().numpy(), lab_r)
+        assert np.array_equal(cen.cpu().numpy(), cen_r.astype(np.float32))
+    wide = np.concatenate([rng.standard_normal(4000) * 1e6, rng.standard_normal(4000)]).astype(np.float32)
+    cen_r, lab_r = oracle.kmeans_encode(wide, 8, 10)
+    cen, planes, lab = tomoq.kmeans_encode(torch.tensor(wide, device=DEV), 8, 10)
+    assert np.mean(lab.cpu().numpy() == lab_r) >= 0.999
+    huge = np.concatenate([rng.standard_normal(4000), [3.0e38, -3.0e38]]).astype(np.float32)
+    cen, planes, lab = tomoq.kmeans_encode(torch.tensor(huge, device=DEV), 8, 10)
+    c = cen.cpu().numpy().astype(np.float64)
+    thr = np.sort(((c[:-1] + c[1:]) * 0.5).astype(np.float32))
+    want = np.searchsorted(thr, huge, side="left")  # label = #{k : v > thr_k}
+    assert np.array_equal(lab.cpu().numpy(), want)
