@@ -418,7 +418,7 @@ tq_status tq_jpeg_encode(const int16_t *coef, int64_t n_blocks, int32_t restart,
         TQ_CHECK_CUDA(cudaMemcpyAsync(stat, w.status, sizeof stat, cudaMemcpyDeviceToHost, st));
         TQ_CHECK_CUDA(cudaStreamSynchronize(st));
         w.release();
-        TQ_REQUIRE(stat[1] == 0, "jpeg: a coefficient lies outside the baseline categories");
+        TQ_REQUIRE(!(stat[1] & 1u), "jpeg: a coefficient lies outside the baseline categories");
         TQ_REQUIRE(!(stat[0] & 0x80000000u), "jpeg: stream would exceed 2 bytes per coefficient");
         const long long n = stat[0];
         TQ_REQUIRE(n <= cap, "jpeg: output capacity too small");

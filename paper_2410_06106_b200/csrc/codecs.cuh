@@ -70,8 +70,10 @@ struct JpegWork {
     int16_t *coef = nullptr;        // [P][nv] coefficients (encode input / decode output)
     long long *len = nullptr;       // [P][nint] interval bytes (encode)
     long long *off = nullptr;       // [P][nint] interval offsets (encode) / starts (decode)
-    unsigned *status = nullptr;     // [P][2]: header word, error bits (1 category, 2 markers, 4 code, 8 overrun)
+    unsigned *status = nullptr;     // [P][2]: header word, flags (1 category, 16 slot overflow -> raw;
+                                    // decode: 2 markers, 4 code, 8 overrun)
     long long *enc_bytes = nullptr; // [P] payload bytes of the last encode (header included)
+    uint8_t *scratch = nullptr;     // [P][nint][128 R + 16] per-interval coder output (encode)
     void alloc(int P, long long nv, int R);
     void release();
 };

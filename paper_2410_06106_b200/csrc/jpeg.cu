@@ -42,6 +42,7 @@ struct JpegTabs {
     int32_t dc_max[18], dc_min[17], dc_ptr[17];  // canonical decode per code length
     int32_t ac_max[18], ac_min[17], ac_ptr[17];
     uint8_t dc_val[16], ac_val[176];
+    uint16_t dc_lut[512], ac_lut[512];  // first 9 bits -> (length << 8) | symbol, 0: longer code
 };
 
 // Annex C for one table: code lengths in order of BITS, canonical code values
@@ -76,6 +77,17 @@ const JpegTabs &tabs() {
         build_table(kAcBits, kAcVal, t.ac_co, t.ac_si, t.ac_max, t.ac_min, t.ac_ptr);
         memcpy(t.dc_val, kDcVal, 12);
         memcpy(t.ac_val, kAcVal, 162);
+        // decode lookahead: every code of <= 9 bits fills the entries it prefixes
+        auto fill = [](const uint16_t *co, const uint8_t *si, int nsym, uint16_t *lut) {
+            for (int sym = 0; sym < nsym; sym++) {
+                const int L = si[sym];
+                if (L == 0 || L > 9) continue;
+                const int base = co[sym] << (9 - L);
+                for (int x = 0; x < (1 << (9 - L)); x++) lut[base + x] = (uint16_t)((L << 8) | sym);
+            }
+        };
+        fill(t.dc_co, t.dc_si, 16, t.dc_lut);
+        fill(t.ac_co, t.ac_si, 256, t.ac_lut);
         // zig-zag (T.81 Figure A.6): anti-diagonals d = row + col, even d walked with the
         // row decreasing, odd d with the row increasing
         int k = 0;
@@ -96,12 +108,12 @@ constexpr int BLKP = 66; // int16 pitch of a thread's staged block: 33 words, co
 
 // stream writer of one thread: bits MSB first, 0x00 stuffed after 0xFF, fill bits 1
 struct BitW {
-    uint8_t *out;  // null: count only
-    long long pos;
+    uint8_t *out;  // bytes beyond cap are counted, not stored
+    long long pos, cap;
     unsigned long long acc;
     int nb;
     __device__ void byte(unsigned b) {
-        if (out) out[pos] = (uint8_t)b;
+        if (pos < cap) out[pos] = (uint8_t)b;
         pos++;
     }
     __device__ void put(unsigned code, int size) {
@@ -170,11 +182,12 @@ __device__ __forceinline__ const int16_t *coef_of(uint8_t *const *pay, const int
     return coef_base ? coef_base + (long long)b * nv : reinterpret_cast<const int16_t *>(pay[b] + 8);
 }
 
-// pass 1 (out == false) / pass 2: interval k of payload blockIdx.y
-template <bool WRITE>
+// interval k of payload blockIdx.y coded into its scratch slot (SLOT(R) bytes: the raw
+// size of its blocks; a longer interval makes the payload fall back to raw coefficients)
+__device__ __forceinline__ long long jpeg_slot(int R) { return 128LL * R + 16; }
 __global__ void __launch_bounds__(JT) jpeg_code(const __grid_constant__ JpegTabs tab, const int16_t *coef_base,
                                                 uint8_t *const *pay, long long nv, int R, int nint, long long *len,
-                                                const long long *off, unsigned *status) {
+                                                uint8_t *scratch, unsigned *status) {
     __shared__ JpegTabs T;
     __shared__ __align__(16) int16_t blk[JT][BLKP];
     for (int i = threadIdx.x; i < (int)(sizeof(JpegTabs) / 4); i += JT)
@@ -187,16 +200,25 @@ __global__ void __launch_bounds__(JT) jpeg_code(const __grid_constant__ JpegTabs
     const long long b0 = (long long)k * R, b1 = min(nblk, b0 + R);
     const int16_t *coef = coef_of(pay, coef_base, b, nv);
     unsigned *st = status + 2 * b;
-    if (WRITE) {
-        if (st[0] & 0x80000000u) return;  // raw fallback: the coefficients are copied instead
-        BitW w{pay[b] + 16 + off[(long long)b * nint + k], 0, 0, 0};
-        code_interval(T, coef, b0, b1, w, blk[threadIdx.x], st + 1);
-        if (k + 1 < nint) { w.byte(0xFF); w.byte(0xD0 + (k & 7)); }
-    } else {
-        BitW w{nullptr, 0, 0, 0};
-        code_interval(T, coef, b0, b1, w, blk[threadIdx.x], st + 1);
-        len[(long long)b * nint + k] = w.pos + (k + 1 < nint ? 2 : 0);
-    }
+    const long long slot = jpeg_slot(R);
+    BitW w{scratch + ((long long)b * nint + k) * slot, 0, slot, 0, 0};
+    code_interval(T, coef, b0, b1, w, blk[threadIdx.x], st + 1);
+    if (k + 1 < nint) { w.byte(0xFF); w.byte(0xD0 + (k & 7)); }
+    if (w.pos > slot) atomicOr(st + 1, 16u);  // slot overflow: raw fallback (not an error)
+    len[(long long)b * nint + k] = w.pos;
+}
+
+// one warp per interval: the scratch bytes to their scanned offset in the payload
+__global__ void jpeg_copy(uint8_t *const *pay, const uint8_t *scratch, const long long *len, const long long *off,
+                          int nint, int R, const unsigned *status) {
+    const int b = blockIdx.y;
+    if (status[2 * b] & 0x80000000u) return;
+    const int k = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (k >= nint) return;
+    const long long slot = jpeg_slot(R), n = len[(long long)b * nint + k];
+    const uint8_t *src = scratch + ((long long)b * nint + k) * slot;
+    uint8_t *dst = pay[b] + 16 + off[(long long)b * nint + k];
+    for (long long i = lane; i < n; i += 32) dst[i] = src[i];
 }
 
 // exclusive scan of the interval lengths of payload blockIdx.x; header word 2 =
@@ -219,7 +241,7 @@ __global__ void __launch_bounds__(ST) jpeg_scan(const long long *len, long long 
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        const bool bad = status[2 * b + 1] != 0;
+        const bool bad = status[2 * b + 1] != 0;  // category overflow (1) or slot overflow (16)
         const bool raw = bad || carry > 2 * nv;
         uint32_t *hdr = reinterpret_cast<uint32_t *>(pay[b]);
         hdr[2] = raw ? 0x80000000u : (uint32_t)carry;
@@ -271,39 +293,56 @@ __global__ void __launch_bounds__(ST) jpeg_markers(uint8_t *const *pay, int nint
         }
 }
 
+// stream reader of one thread: a 64-bit buffer refilled bytewise (stuffed 0x00 after
+// 0xFF skipped); bits beyond the interval read as zeros and are counted as an overrun
 struct BitR {
     const uint8_t *in;
     long long pos, end;
-    unsigned cur;
-    int cnt;
-    bool past;  // ran out of interval data
-    __device__ unsigned bit() {
-        if (cnt == 0) {
-            if (pos >= end) { past = true; cur = 0; }
-            else {
-                cur = in[pos++];
-                if (cur == 0xFFu) pos++;  // stuffed 0x00
+    unsigned long long buf;
+    int nb;
+    long long real_bits, used;
+    __device__ void refill() {
+        while (nb <= 48) {
+            unsigned byte = 0;
+            if (pos < end) {
+                byte = in[pos];
+                pos += byte == 0xFFu ? 2 : 1;
+                real_bits += 8;
             }
-            cnt = 8;
+            buf |= (unsigned long long)byte << (56 - nb);
+            nb += 8;
         }
-        cnt--;
-        return (cur >> cnt) & 1u;
     }
+    __device__ unsigned peek(int n) const { return (unsigned)(buf >> (64 - n)); }
+    __device__ void skip(int n) { buf <<= n; nb -= n; used += n; }
     __device__ int bits(int s) {
-        int v = 0;
-        for (int i = 0; i < s; i++) v = (v << 1) | (int)bit();
+        if (s == 0) return 0;
+        refill();
+        const int v = (int)peek(s);
+        skip(s);
         return v;
     }
 };
 
-__device__ __forceinline__ int decode_symbol(BitR &r, const int32_t *mx, const int32_t *mn, const int32_t *ptr,
-                                             const uint8_t *val) {
-    int code = (int)r.bit(), l = 1;
-    while (code > mx[l]) {
-        if (++l > 16) return -1;
-        code = (code << 1) | (int)r.bit();
+// DECODE (T.81 F.2.2.3): 9-bit lookahead table, then the canonical MAXCODE search for
+// longer codes
+__device__ __forceinline__ int decode_symbol(BitR &r, const uint16_t *lut, const int32_t *mx, const int32_t *mn,
+                                             const int32_t *ptr, const uint8_t *val) {
+    r.refill();
+    const unsigned p = r.peek(16);
+    const unsigned e = lut[p >> 7];
+    if (e) {
+        r.skip((int)(e >> 8));
+        return (int)(e & 0xffu);
     }
-    return val[ptr[l] + code - mn[l]];
+    for (int l = 10; l <= 16; l++) {
+        const int code = (int)(p >> (16 - l));
+        if (code <= mx[l]) {
+            r.skip(l);
+            return val[ptr[l] + code - mn[l]];
+        }
+    }
+    return -1;
 }
 
 __global__ void __launch_bounds__(JT) jpeg_decode_k(const __grid_constant__ JpegTabs tab, uint8_t *const *pay,
@@ -320,7 +359,7 @@ __global__ void __launch_bounds__(JT) jpeg_decode_k(const __grid_constant__ Jpeg
     if ((w2 & 0x80000000u) || status[2 * b + 1]) return;
     const long long n = w2;
     const long long *sb = starts + (long long)b * nint;
-    BitR r{pay[b] + 16, sb[k], k + 1 < nint ? sb[k + 1] - 2 : n, 0, 0, false};
+    BitR r{pay[b] + 16, sb[k], k + 1 < nint ? sb[k + 1] - 2 : n, 0ull, 0, 0, 0};
     const long long nblk = nv / 64;
     const long long b0 = (long long)k * R, b1 = min(nblk, b0 + R);
     int16_t *out = coef_base + (long long)b * nv;
@@ -330,14 +369,14 @@ __global__ void __launch_bounds__(JT) jpeg_decode_k(const __grid_constant__ Jpeg
         int16_t v[64];
 #pragma unroll
         for (int i = 0; i < 64; i++) v[i] = 0;
-        const int s = decode_symbol(r, T.dc_max, T.dc_min, T.dc_ptr, T.dc_val);
+        const int s = decode_symbol(r, T.dc_lut, T.dc_max, T.dc_min, T.dc_ptr, T.dc_val);
         if (s < 0 || s > 11) { atomicOr(status + 2 * b + 1, 4u); return; }
         int d = r.bits(s);
         if (s && d < (1 << (s - 1))) d += 1 - (1 << s);  // EXTEND
         pred += d;
         v[0] = (int16_t)pred;
         for (int kk = 1; kk < 64; kk++) {
-            const int rs = decode_symbol(r, T.ac_max, T.ac_min, T.ac_ptr, T.ac_val);
+            const int rs = decode_symbol(r, T.ac_lut, T.ac_max, T.ac_min, T.ac_ptr, T.ac_val);
             if (rs < 0) { atomicOr(status + 2 * b + 1, 4u); return; }
             const int run = rs >> 4, sz = rs & 15;
             if (sz == 0) {
@@ -355,7 +394,7 @@ __global__ void __launch_bounds__(JT) jpeg_decode_k(const __grid_constant__ Jpeg
 #pragma unroll
         for (int q = 0; q < 8; q++) dst[q] = src[q];
     }
-    if (r.past) atomicOr(status + 2 * b + 1, 8u);
+    if (r.used > r.real_bits) atomicOr(status + 2 * b + 1, 8u);
 }
 
 // raw payloads: coefficients straight from the payload
@@ -384,11 +423,12 @@ void JpegWork::alloc(int P_, long long nv_, int R_) {
     TQ_CHECK_CUDA(cudaMalloc(&off, sizeof(long long) * nint * np));
     TQ_CHECK_CUDA(cudaMalloc(&status, sizeof(unsigned) * 2 * np));
     TQ_CHECK_CUDA(cudaMalloc(&enc_bytes, sizeof(long long) * np));
+    TQ_CHECK_CUDA(cudaMalloc(&scratch, (size_t)(128LL * R + 16) * nint * np));
     TQ_CHECK_CUDA(cudaMemset(enc_bytes, 0, sizeof(long long) * np));
 }
 
 void JpegWork::release() {
-    for (void *p : {(void *)coef, (void *)len, (void *)off, (void *)status, (void *)enc_bytes})
+    for (void *p : {(void *)coef, (void *)len, (void *)off, (void *)status, (void *)enc_bytes, (void *)scratch})
         if (p) cudaFree(p);
     *this = JpegWork();
 }
@@ -398,9 +438,9 @@ int jpeg_encode(uint8_t *const *pay, JpegWork &w, cudaStream_t st) {
     const JpegTabs &t = tabs();
     TQ_CHECK_CUDA(cudaMemsetAsync(w.status, 0, sizeof(unsigned) * 2 * w.P, st));
     const dim3 grid(ceil_div(w.nint, JT), w.P);
-    jpeg_code<false><<<grid, JT, 0, st>>>(t, w.coef, pay, w.nv, w.R, w.nint, w.len, nullptr, w.status);
+    jpeg_code<<<grid, JT, 0, st>>>(t, w.coef, pay, w.nv, w.R, w.nint, w.len, w.scratch, w.status);
     jpeg_scan<<<w.P, ST, 0, st>>>(w.len, w.off, w.nint, w.nv, pay, w.status, w.enc_bytes);
-    jpeg_code<true><<<grid, JT, 0, st>>>(t, w.coef, pay, w.nv, w.R, w.nint, nullptr, w.off, w.status);
+    jpeg_copy<<<dim3(ceil_div(w.nint, 8), w.P), 256, 0, st>>>(pay, w.scratch, w.len, w.off, w.nint, w.R, w.status);
     jpeg_raw_copy<<<dim3(std::max(1, std::min(1184, (int)ceil_div(w.nv / 8, 256))), w.P), 256, 0, st>>>(
         w.coef, pay, w.nv, w.status);
     TQ_CHECK_CUDA(cudaGetLastError());
