@@ -88,12 +88,12 @@ void exchange_plan(int M, const std::vector<int> &edges, const std::vector<int> 
 // ---------------------------------------------------------------- small kernels
 namespace {
 
+// row pairs[2 r] of src -> row pairs[2 r + 1] of dst
 template <typename T>
-__global__ void gather_rows(const float *src, const int *src_row, T *dst, int n_rows, int n_det) {
+__global__ void gather_rows(const float *src, const int *pairs, T *dst, int n_det) {
     const int r = blockIdx.y;
-    if (r >= n_rows) return;
-    const float *s = src + (long long)src_row[r] * n_det;
-    T *d = dst + (long long)r * n_det;
+    const float *s = src + (long long)pairs[2 * r] * n_det;
+    T *d = dst + (long long)pairs[2 * r + 1] * n_det;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n_det; j += gridDim.x * blockDim.x) d[j] = (T)s[j];
 }
 
@@ -255,9 +255,11 @@ void Ctx::destroy() {
     ALPHA = XG = nullptr;
     CSUM = nullptr;
     if (sino_stage) cudaFree(sino_stage);
-    if (row_map) cudaFree(row_map);
+    for (auto &g : gather_maps)
+        if (g.second.pairs) cudaFree(g.second.pairs);
+    gather_maps.clear();
     if (img_stage) cudaFree(img_stage);
-    sino_stage = nullptr; row_map = nullptr; img_stage = nullptr;
+    sino_stage = nullptr; img_stage = nullptr;
     if (comm) nccl().CommDestroy(comm);
     comm = nullptr;
     if (ev0) cudaEventDestroy(ev0);
@@ -325,41 +327,33 @@ void Ctx::set_sinogram(int slice, int node, const float *d, long long len, bool 
     float *stage = sino_stage;
     TQ_CHECK_CUDA(cudaMemcpyAsync(stage, d, sizeof(float) * len,
                                   on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream));
-    std::vector<int> src_row, dst_row;
-    for (int i = 0; i < L; i++) {
-        if (loc[i].first != slice) continue;
-        const int m = loc[i].second;
-        if (node >= 0 && m != node) continue;
-        for (int k = 0; k < aoff[m + 1] - aoff[m]; k++) {
-            src_row.push_back(node < 0 ? aidx[aoff[m] + k] : k);
-            dst_row.push_back(in.row0_h[i] + k);
+    // (source row, destination row) pairs of the local nodes, built once per (slice, node)
+    auto it = gather_maps.find({slice, node});
+    if (it == gather_maps.end()) {
+        std::vector<int> pr;
+        for (int i = 0; i < L; i++) {
+            if (loc[i].first != slice) continue;
+            const int m = loc[i].second;
+            if (node >= 0 && m != node) continue;
+            for (int k = 0; k < aoff[m + 1] - aoff[m]; k++) {
+                pr.push_back(node < 0 ? aidx[aoff[m] + k] : k);
+                pr.push_back(in.row0_h[i] + k);
+            }
         }
-        sino_set[i] = 1;
+        GatherMap gm{nullptr, (int)pr.size() / 2};
+        if (gm.count) {
+            TQ_CHECK_CUDA(cudaMalloc(&gm.pairs, sizeof(int) * pr.size()));
+            TQ_CHECK_CUDA(cudaMemcpy(gm.pairs, pr.data(), sizeof(int) * pr.size(), cudaMemcpyHostToDevice));
+        }
+        it = gather_maps.emplace(std::make_pair(slice, node), gm).first;
     }
-    if (!src_row.empty()) {
-        // rows of one node are contiguous in D: gather per node run
-        if (row_map_len < (long long)src_row.size()) {
-            if (row_map) cudaFree(row_map);
-            row_map = nullptr;
-            TQ_CHECK_CUDA(cudaMalloc(&row_map, sizeof(int) * src_row.size()));
-            row_map_len = (long long)src_row.size();
-        }
-        int *srd = row_map;
-        TQ_CHECK_CUDA(cudaMemcpyAsync(srd, src_row.data(), sizeof(int) * src_row.size(),
-                                      cudaMemcpyHostToDevice, stream));
-        size_t k = 0;
-        while (k < src_row.size()) {
-            size_t e = k;
-            while (e + 1 < src_row.size() && dst_row[e + 1] == dst_row[e] + 1) e++;
-            const int cnt = (int)(e - k + 1);
-            dim3 grid(ceil_div(n_det, 256), cnt);
-            if (prec == 0)
-                gather_rows<float><<<grid, 256, 0, stream>>>(stage, srd + k, (float *)in.D + (long long)dst_row[k] * n_det, cnt, n_det);
-            else
-                gather_rows<double><<<grid, 256, 0, stream>>>(stage, srd + k, (double *)in.D + (long long)dst_row[k] * n_det, cnt, n_det);
-            TQ_CHECK_CUDA(cudaGetLastError());
-            k = e + 1;
-        }
+    for (int i = 0; i < L; i++)
+        if (loc[i].first == slice && (node < 0 || loc[i].second == node)) sino_set[i] = 1;
+    if (it->second.count) {
+        const dim3 grid(ceil_div(n_det, 256), it->second.count);
+        if (prec == 0) gather_rows<float><<<grid, 256, 0, stream>>>(stage, it->second.pairs, (float *)in.D, n_det);
+        else gather_rows<double><<<grid, 256, 0, stream>>>(stage, it->second.pairs, (double *)in.D, n_det);
+        TQ_CHECK_CUDA(cudaGetLastError());
     }
     TQ_CHECK_CUDA(cudaStreamSynchronize(stream));
 }
@@ -741,7 +735,8 @@ void Ctx::run(int iters, cudaStream_t user) {
             else if (g.comm == COMM_EXCHANGE) exchange(s);
         }
     TQ_CHECK_CUDA(cudaEventRecord(ev1, s));
-    in.norm2(s);
+    // CG with E1 >= 1 leaves ||x||^2 in the scalar table (its last step); otherwise compute it
+    if (!(iters > 0 && prm.inner == TQ_INNER_CG && prm.e1 >= 1)) in.norm2(s);
     std::vector<double> sc((size_t)S_NSLOT * std::max(1, L));
     TQ_CHECK_CUDA(cudaMemcpyAsync(sc.data(), in.scal, sizeof(double) * S_NSLOT * L, cudaMemcpyDeviceToHost, s));
     TQ_CHECK_CUDA(cudaStreamSynchronize(s));
@@ -776,10 +771,13 @@ void Ctx::get_image(int slice, int node, float *out, long long len, bool on_devi
     if (node >= 0) {
         const int i = local(slice, node);
         if (i < 0) fail(TQ_EINVAL, "node is not local to this rank");
-        launch_convert(prec, in.xrow(in.X, i), 0, d, n, stream);
+        if (prec == 0) d = (float *)in.xrow(in.X, i);  // fp32 state: copied out directly
+        else launch_convert(prec, in.xrow(in.X, i), 0, d, n, stream);
     } else if (segmented()) {
         TQ_REQUIRE(slice >= 0 && slice < S, "slice out of range");
-        launch_convert(prec, (uint8_t *)XG + (prec ? 8 : 4) * (long long)slice * n, 0, d, n, stream);
+        const void *xg = (uint8_t *)XG + (prec ? 8 : 4) * (long long)slice * n;
+        if (prec == 0) d = (float *)xg;
+        else launch_convert(prec, xg, 0, d, n, stream);
     } else {
         const int i0 = local(slice, 0);
         bool all = i0 >= 0;

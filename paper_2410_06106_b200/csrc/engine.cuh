@@ -130,9 +130,9 @@ struct Ctx {
     long long launch_component(int component, int reps, cudaStream_t s);
     float *sino_stage = nullptr;   // persistent device staging for tq_set_sinogram
     long long sino_stage_len = 0;
-    int *row_map = nullptr;        // persistent gather indices
+    struct GatherMap { int *pairs; int count; };
+    std::map<std::pair<int, int>, GatherMap> gather_maps;  // (slice, node) -> sinogram row pairs
     float *img_stage = nullptr;    // persistent staging of tq_get_image
-    long long row_map_len = 0;
 
    private:
     void invalidate();

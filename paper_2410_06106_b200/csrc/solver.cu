@@ -149,7 +149,7 @@ int Inner::cg(const DevGeom &g, int e1, cudaStream_t st) {
         launch_cg_update_r(prec, R, Q, n, L, scal, partial, part_stride, counter, st);
         // x += alpha p (deferred from the r update: this pass reads p anyway), then the next
         // search direction p = r + beta p (the last one is never used)
-        launch_cg_update_px(prec, X, P, R, n, L, scal, it + 1 < e1, st);
+        launch_cg_update_px(prec, X, P, R, n, L, scal, partial, part_stride, counter, it + 1 < e1, st);
         k += 2;
     }
     return k;

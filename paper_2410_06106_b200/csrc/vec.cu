@@ -72,14 +72,20 @@ __global__ void __launch_bounds__(VT) cg_update_r(T *__restrict__ r, const T *__
     }
 }
 
+// WITH_P = false (the last CG step of an inner solve): no new direction; instead the
+// final ||x||^2 per node goes to scal[S_NORM] (the divergence check of tq_run).
 template <typename T, bool WITH_P>
 __global__ void __launch_bounds__(VT) cg_update_px(T *__restrict__ x, T *__restrict__ p, const T *__restrict__ r,
-                                                   long long n, const double *scal) {
+                                                   long long n, double *scal, double *partial, int part_stride,
+                                                   unsigned *counter) {
+    __shared__ double red[VT / 32 + 1];
+    __shared__ bool last;
     const int node = blockIdx.y;
     const long long base = (long long)node * n;
     const double alpha = scal[(long long)node * S_NSLOT + S_ALPHA];
     const double beta = scal[(long long)node * S_NSLOT + S_BETA];
     x += base; p += base; r += base;
+    double nrm = 0.0;
     vec_loop(n,
         [&](long long i) {
             Q4<T> xv = ld4(x + i), pv = ld4(p + i);
@@ -89,15 +95,28 @@ __global__ void __launch_bounds__(VT) cg_update_px(T *__restrict__ x, T *__restr
             for (int u = 0; u < 4; u++) {
                 xv.v[u] = (T)((double)xv.v[u] + alpha * (double)pv.v[u]);
                 if (WITH_P) pv.v[u] = (T)((double)rv.v[u] + beta * (double)pv.v[u]);
+                else nrm += (double)xv.v[u] * (double)xv.v[u];
             }
             st4(x + i, xv);
             if (WITH_P) st4(p + i, pv);
         },
         [&](long long i) {
             const T pv = p[i];
-            x[i] = (T)((double)x[i] + alpha * (double)pv);
+            const T xv = (T)((double)x[i] + alpha * (double)pv);
+            x[i] = xv;
             if (WITH_P) p[i] = (T)((double)r[i] + beta * (double)pv);
+            else nrm += (double)xv * (double)xv;
         });
+    if (WITH_P) return;
+    const double bs = block_sum<VT>(nrm, red);
+    double *part = partial + (long long)node * part_stride;
+    if (threadIdx.x == 0) part[blockIdx.x] = bs;
+    if (last_block_of_group(counter + node, gridDim.x, &last)) {
+        double s = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += VT) s += __ldcg(part + b);
+        s = block_sum<VT>(s, red);
+        if (threadIdx.x == 0) scal[(long long)node * S_NSLOT + S_NORM] = s;
+    }
 }
 
 template <typename T>
@@ -143,15 +162,15 @@ void launch_cg_update_r(int prec, void *r, const void *q, long long n, int L, do
     TQ_CHECK_CUDA(cudaGetLastError());
 }
 
-void launch_cg_update_px(int prec, void *x, void *p, const void *r, long long n, int L, const double *scal,
-                         bool with_p, cudaStream_t st) {
+void launch_cg_update_px(int prec, void *x, void *p, const void *r, long long n, int L, double *scal,
+                         double *partial, int part_stride, unsigned *counter, bool with_p, cudaStream_t st) {
     dim3 grid(vec_blocks(n), L);
     if (prec == 0) {
-        if (with_p) cg_update_px<float, true><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal);
-        else cg_update_px<float, false><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal);
+        if (with_p) cg_update_px<float, true><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal, partial, part_stride, counter);
+        else cg_update_px<float, false><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal, partial, part_stride, counter);
     } else {
-        if (with_p) cg_update_px<double, true><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal);
-        else cg_update_px<double, false><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal);
+        if (with_p) cg_update_px<double, true><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal, partial, part_stride, counter);
+        else cg_update_px<double, false><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal, partial, part_stride, counter);
     }
     TQ_CHECK_CUDA(cudaGetLastError());
 }

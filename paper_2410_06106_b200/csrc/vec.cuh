@@ -11,9 +11,9 @@ namespace tq {
 // p anyway: one pass over x, p fewer per CG step, identical arithmetic.)
 void launch_cg_update_r(int prec, void *r, const void *q, long long n, int L, double *scal, double *partial,
                         int part_stride, unsigned *counter, cudaStream_t st);
-// x += alpha p, then (with_p) p = r + beta p
-void launch_cg_update_px(int prec, void *x, void *p, const void *r, long long n, int L, const double *scal,
-                         bool with_p, cudaStream_t st);
+// x += alpha p, then (with_p) p = r + beta p, else scal[node][S_NORM] = ||x||^2 (last CG step)
+void launch_cg_update_px(int prec, void *x, void *p, const void *r, long long n, int L, double *scal,
+                         double *partial, int part_stride, unsigned *counter, bool with_p, cudaStream_t st);
 // scal[node][S_NORM] = ||x_node||^2
 void launch_norm2(int prec, const void *x, long long n, int L, double *scal, double *partial,
                   int part_stride, unsigned *counter, cudaStream_t st);
