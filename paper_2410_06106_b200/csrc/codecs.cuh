@@ -26,7 +26,7 @@ struct KmeansWork {
     long long nv = 0;
     uint32_t *keysA = nullptr;      // [P][T*2048] order-preserving keys (sorted in place)
     uint32_t *keysB = nullptr;      // radix-sort ping-pong buffer
-    uint32_t *hist = nullptr;       // [P][256][T] per-tile digit counts -> offsets within the digit
+    uint32_t *hist = nullptr;       // [P][T][256] per-tile digit counts -> offsets within the digit
     uint32_t *dtot = nullptr;       // [P][256] digit totals
     long long *csum = nullptr;      // [P][T*32] fixed-point sums of 64-key chunks of the sorted keys
     long long *cpre = nullptr;      // [P][T*32] their exclusive prefix

@@ -2,7 +2,7 @@
 //
 // Sort-based exact Lloyd.  Each payload's values are mapped to order-preserving
 // 32-bit keys and sorted by an LSD radix sort (4 passes of 8-bit digits: per-tile
-// digit histograms stored digit-major, one exclusive scan per payload over
+// digit histograms stored tile-major, one exclusive scan per payload over
 // (digit, tile) = the global output offsets, stable match-based tile ranking +
 // scatter).  On the sorted keys:
 //   * the quantile init c_k = v_(floor((2k+1) n / 2K)) is a direct read (exact order
@@ -119,11 +119,11 @@ __device__ __forceinline__ void tile_hist(const uint32_t (&k)[KI], int shift, ui
     sh[threadIdx.x] = tot;
 }
 
-// digit-major [P][256][T]: the exclusive scan of a payload's row-major counts is the
-// global output offset of (digit, tile)
+// tile-major [P][T][256] (coalesced rows); km_scan turns each digit column into the
+// global output offsets of (digit, tile)
 __device__ __forceinline__ void flush_hist(const uint32_t *sh, uint32_t *hp, int T, int t) {
     __syncthreads();
-    hp[(long long)threadIdx.x * T + t] = sh[threadIdx.x];  // KT == 256 digits
+    hp[(long long)t * 256 + threadIdx.x] = sh[threadIdx.x];  // KT == 256 digits
 }
 
 // keys of the raw payload (padding keys sort last) + digit-0 histogram
@@ -151,36 +151,34 @@ __global__ void __launch_bounds__(KT) km_hist(const uint32_t *keys, KmPtr w, int
     flush_hist(sh, w.hist + (long long)b * 256 * w.T, w.T, t);
 }
 
-// exclusive scan along the tiles of each (payload, digit) row of the digit-major
-// counts, in place; the row total goes to dtot[payload][digit].  One warp per row,
-// lanes strided over the tiles (coalesced), rounds chained by a carry.
-constexpr int SCW = 8;  // rows (warps) per CTA
+// exclusive scan down each digit column of a payload's tile-major counts, in place; the
+// column total goes to dtot[payload][digit].  One CTA per (payload, 32 digits): lane =
+// digit (rows of 32 digits are 128-byte coalesced), warp w owns a contiguous range of
+// tiles; warp totals are combined in a fixed order.
+constexpr int SCW = 8;  // warps per CTA
 __global__ void __launch_bounds__(SCW * 32) km_scan(KmPtr w) {
+    __shared__ uint32_t tot[SCW][32];
     const int b = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int d = blockIdx.x * SCW + warp;
-    uint32_t *h = w.hist + ((long long)b * 256 + d) * w.T;
-    uint32_t carry = 0;
-    for (int t0 = 0; t0 < w.T; t0 += 128) {
-        uint32_t c[4];
+    const int d = blockIdx.x * 32 + lane;
+    const int T = w.T, per = (T + SCW - 1) / SCW;
+    const int t0 = warp * per, t1 = min(T, t0 + per);
+    uint32_t *h = w.hist + (long long)b * T * 256 + d;
+    uint32_t sum = 0;
+    for (int t = t0; t < t1; t++) sum += h[(long long)t * 256];
+    tot[warp][lane] = sum;
+    __syncthreads();
+    uint32_t run = 0, all = 0;
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const int t = t0 + 32 * u + lane;
-            c[u] = t < w.T ? h[t] : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            uint32_t inc = c[u];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += y;
-            }
-            const int t = t0 + 32 * u + lane;
-            if (t < w.T) h[t] = carry + inc - c[u];
-            carry += __shfl_sync(0xffffffffu, inc, 31);
-        }
+    for (int q = 0; q < SCW; q++) {
+        if (q < warp) run += tot[q][lane];
+        all += tot[q][lane];
     }
-    if (lane == 0) w.dtot[(long long)b * 256 + d] = carry;
+    for (int t = t0; t < t1; t++) {
+        const uint32_t c = h[(long long)t * 256];
+        h[(long long)t * 256] = run;
+        run += c;
+    }
+    if (warp == 0) w.dtot[(long long)b * 256 + d] = all;
 }
 
 // stable scatter of one tile by the digit: rank = (keys of the digit in earlier warps)
@@ -197,7 +195,7 @@ __global__ void __launch_bounds__(KT, 3) km_scatter(const uint32_t *kin, uint32_
     load_striped(kin, pb + (long long)t * KTILE, k);
     uint32_t base;
     Scan(stmp).ExclusiveSum(w.dtot[(long long)b * 256 + threadIdx.x], base);
-    goff[threadIdx.x] = base + w.hist[((long long)b * 256 + threadIdx.x) * w.T + t];
+    goff[threadIdx.x] = base + w.hist[((long long)b * w.T + t) * 256 + threadIdx.x];
     uint32_t *c = wc + warp * 256;
     for (int i = lane; i < 256; i += 32) c[i] = 0u;
     __syncwarp();
@@ -615,7 +613,7 @@ int kmeans_encode(const float *const *v, KmeansWork &ws, int lloyd, uint8_t *con
     uint32_t *src = ws.keysA, *dst = ws.keysB;
     for (int pass = 0; pass < 4; pass++) {
         if (pass) { km_hist<<<tiles, KT, 0, st>>>(src, w, 8 * pass); k++; }
-        km_scan<<<dim3(256 / SCW, P), SCW * 32, 0, st>>>(w);
+        km_scan<<<dim3(256 / 32, P), SCW * 32, 0, st>>>(w);
         km_scatter<<<tiles, KT, 0, st>>>(src, dst, w, 8 * pass);
         k += 2;
         std::swap(src, dst);
