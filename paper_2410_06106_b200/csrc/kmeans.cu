@@ -84,13 +84,19 @@ __device__ __forceinline__ void load_tile(const uint32_t *keys, long long off, u
 // Warp multisplit by ballots: peers = lanes of the warp whose digit equals mine
 // (8 ballots, no match/atomics).  Keys of a tile are warp-striped: warp w, round r,
 // lane l holds key w*256 + r*32 + l, so (w, r, l) is the tile's index order.
+// Per bit: one predicate from the digit, one VOTE, and the lane keeps either the ballot
+// or its complement (two predicated LOP3s) -- four issue slots per bit.
 __device__ __forceinline__ unsigned digit_peers(uint32_t d) {
     unsigned peers = 0xffffffffu;
 #pragma unroll
     for (int b = 0; b < 8; b++) {
-        const bool bit = (d >> b) & 1u;
-        const unsigned bal = __ballot_sync(0xffffffffu, bit);
-        peers &= bit ? bal : ~bal;
+        asm("{\n\t.reg .pred p;\n\t.reg .b32 t, bal;\n\t"
+            "and.b32 t, %1, %2;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 bal, p, 0xffffffff;\n\t"
+            "@!p not.b32 bal, bal;\n\t"
+            "and.b32 %0, %0, bal;\n\t}"
+            : "+r"(peers) : "r"(d), "r"(1u << b));
     }
     return peers;
 }
