@@ -506,7 +506,11 @@ __global__ void __launch_bounds__(KT) km_final(const float *const *vin, KmPtr w,
             // the B ballot words are warp-uniform: lane 0 stores them (no per-lane select)
             uint32_t word[B > 0 ? B : 1];
 #pragma unroll
-            for (int bit = 0; bit < B; bit++) word[bit] = __ballot_sync(0xffffffffu, l & (1 << bit));
+            for (int bit = 0; bit < B; bit++) {  // predicate from the label bit + VOTE (no SHF/ISETP)
+                asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.u32 p, t, 0;\n\t"
+                    "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t}"
+                    : "=r"(word[bit]) : "r"(l), "r"(1u << bit));
+            }
             if (lane == 0 && g0 + u < G) {
 #pragma unroll
                 for (int bit = 0; bit < B; bit++) planes[(g0 + u) * B + bit] = word[bit];
