@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(SCW * 32) km_scan(KmPtr w) {
 __global__ void __launch_bounds__(KT, 3) km_scatter(const uint32_t *kin, uint32_t *kout, KmPtr w, int shift) {
     using Scan = cub::BlockScan<uint32_t, KT>;
     __shared__ typename Scan::TempStorage stmp;
-    __shared__ uint32_t wc[KT / 32 * 256], goff[256], tstart[256], sk[KTILE];
+    __shared__ uint32_t wc[KT / 32 * 256], goff[256], sk[KTILE];
     const int b = blockIdx.y, t = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long pb = (long long)b * w.T * KTILE;
@@ -226,13 +226,17 @@ __global__ void __launch_bounds__(KT, 3) km_scatter(const uint32_t *kin, uint32_
     }
     uint32_t ts;  // first tile-local position of the digit
     Scan(stmp).ExclusiveSum(run, ts);
-    tstart[threadIdx.x] = ts;
+    // fold the tile start into the per-warp bases and out of the global offset, so each
+    // key below needs one shared-memory lookup per phase
+#pragma unroll
+    for (int q = 0; q < KT / 32; q++) wc[q * 256 + threadIdx.x] += ts;
+    goff[threadIdx.x] -= ts;  // destination of tile position i (digit d) = goff[d] + i (mod 2^32)
     __syncthreads();
     // tile-local sort through shared memory, then runs of equal digits leave coalesced
 #pragma unroll
     for (int r = 0; r < KI; r++) {
         const uint32_t d = (k[r] >> shift) & 255u;
-        sk[tstart[d] + c[d] + rank[r]] = k[r];
+        sk[c[d] + rank[r]] = k[r];
     }
     __syncthreads();
 #pragma unroll
@@ -240,7 +244,7 @@ __global__ void __launch_bounds__(KT, 3) km_scatter(const uint32_t *kin, uint32_
         const int i = r * KT + threadIdx.x;
         const uint32_t key = sk[i];
         const uint32_t d = (key >> shift) & 255u;
-        kout[pb + goff[d] + (i - tstart[d])] = key;
+        kout[pb + (uint32_t)(goff[d] + (uint32_t)i)] = key;
     }
 }
 
