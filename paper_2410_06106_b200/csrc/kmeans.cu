@@ -503,7 +503,8 @@ __global__ void __launch_bounds__(KT) km_final(const float *const *vin, KmPtr w,
             const int q = km_bucket(v[u], lo, scale);
             int l = cnt_s[q];
             const int e = cnt_s[q + 1];
-            for (int k = l; k < e; k++) l += v[u] > thr_s[k] ? 1 : 0;
+#pragma unroll 1
+            for (int k = l; k < e; k++) l += v[u] > thr_s[k] ? 1 : 0;  // usually 0 or 1 trips
             const long long i = (g0 + u) * 32 + lane;
             if (labels && i < nv) labels[i] = l;
             if (dec && i < nv) dec[i] = (TO)cen_s[l];
