@@ -31,36 +31,55 @@ DctTables make_tables(int quality) {
 __device__ __forceinline__ int rs10(int v) { return (v + 512) >> 10; }
 __device__ __forceinline__ long long rs(long long v, int k) { return (v + (1LL << (k - 1))) >> k; }
 
-// per-payload min / max (exact in any order); written to the payload header
+// per-payload min / max (exact in any order); written to the payload header.  A few
+// CTAs per payload stream it with 16-byte loads (warp-shuffle block reduction); the last
+// CTA of a payload combines the per-CTA partials with one warp.
+__device__ __forceinline__ void warp_minmax(float &mn, float &mx) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+}
 __global__ void __launch_bounds__(DT) dct_minmax(const float *const *vin, long long nv, float *partial,
                                                  int part_stride, unsigned *counter,
                                                  uint8_t *const *pay, float *mm_work) {
-    __shared__ float smn[DT], smx[DT];
+    __shared__ float smn[DT / 32], smx[DT / 32];
     __shared__ bool last;
     const int b = blockIdx.y;
     const float *vb = vin[b];
     float mn = INFINITY, mx = -INFINITY;
-    for (long long i = (long long)blockIdx.x * DT + threadIdx.x; i < nv; i += (long long)gridDim.x * DT) {
-        const float x = vb[i];
-        mn = fminf(mn, x);
-        mx = fmaxf(mx, x);
-    }
-    smn[threadIdx.x] = mn;
-    smx[threadIdx.x] = mx;
-    __syncthreads();
-    for (int o = DT / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) {
-            smn[threadIdx.x] = fminf(smn[threadIdx.x], smn[threadIdx.x + o]);
-            smx[threadIdx.x] = fmaxf(smx[threadIdx.x], smx[threadIdx.x + o]);
+    const long long stride = (long long)gridDim.x * DT;
+    if ((nv & 3) == 0 && ((uintptr_t)vb & 15) == 0) {
+        const float4 *v4 = reinterpret_cast<const float4 *>(vb);
+        for (long long i = (long long)blockIdx.x * DT + threadIdx.x; i < nv / 4; i += stride) {
+            const float4 x = __ldg(v4 + i);
+            mn = fminf(fminf(mn, x.x), fminf(x.y, fminf(x.z, x.w)));
+            mx = fmaxf(fmaxf(mx, x.x), fmaxf(x.y, fmaxf(x.z, x.w)));
         }
-        __syncthreads();
+    } else {
+        for (long long i = (long long)blockIdx.x * DT + threadIdx.x; i < nv; i += stride) {
+            const float x = vb[i];
+            mn = fminf(mn, x);
+            mx = fmaxf(mx, x);
+        }
+    }
+    warp_minmax(mn, mx);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) { smn[warp] = mn; smx[warp] = mx; }
+    __syncthreads();
+    if (warp == 0) {
+        mn = lane < DT / 32 ? smn[lane] : INFINITY;
+        mx = lane < DT / 32 ? smx[lane] : -INFINITY;
+        warp_minmax(mn, mx);
     }
     float *part = partial + (long long)b * part_stride;
-    if (threadIdx.x == 0) { part[2 * blockIdx.x] = smn[0]; part[2 * blockIdx.x + 1] = smx[0]; }
-    if (last_block_of_group(counter + b, gridDim.x, &last)) {
-        if (threadIdx.x == 0) {
-            float a = INFINITY, c = -INFINITY;
-            for (unsigned k = 0; k < gridDim.x; k++) { a = fminf(a, __ldcg(part + 2 * k)); c = fmaxf(c, __ldcg(part + 2 * k + 1)); }
+    if (threadIdx.x == 0) { part[2 * blockIdx.x] = mn; part[2 * blockIdx.x + 1] = mx; }
+    if (last_block_of_group(counter + b, gridDim.x, &last) && warp == 0) {
+        float a = INFINITY, c = -INFINITY;
+        for (unsigned k = lane; k < gridDim.x; k += 32) { a = fminf(a, __ldcg(part + 2 * k)); c = fmaxf(c, __ldcg(part + 2 * k + 1)); }
+        warp_minmax(a, c);
+        if (lane == 0) {
             mm_work[2 * b] = a;
             mm_work[2 * b + 1] = c;
             float *hdr = reinterpret_cast<float *>(pay[b]);
@@ -192,7 +211,8 @@ long long dct_payload_bytes(long long nv) { return 8 + 2 * nv; }
 
 void DctWork::alloc(int P_, long long nv) {
     P = P_;
-    part_stride = 2 * (int)std::max(1LL, std::min(1024LL, (nv + DT - 1) / DT));
+    // CTAs per payload for the min / max pass: ~16 K elements each, at most 128
+    part_stride = 2 * (int)std::max(1LL, std::min(128LL, (nv + 16383) / 16384));
     TQ_CHECK_CUDA(cudaMalloc(&minmax, sizeof(float) * 2 * std::max(1, P)));
     TQ_CHECK_CUDA(cudaMalloc(&partial, sizeof(float) * part_stride * std::max(1, P)));
     TQ_CHECK_CUDA(cudaMalloc(&counter, sizeof(unsigned) * std::max(1, P)));

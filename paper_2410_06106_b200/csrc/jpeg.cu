@@ -441,7 +441,7 @@ int jpeg_encode(uint8_t *const *pay, JpegWork &w, cudaStream_t st) {
     jpeg_code<<<grid, JT, 0, st>>>(t, w.coef, pay, w.nv, w.R, w.nint, w.len, w.scratch, w.status);
     jpeg_scan<<<w.P, ST, 0, st>>>(w.len, w.off, w.nint, w.nv, pay, w.status, w.enc_bytes);
     jpeg_copy<<<dim3(ceil_div(w.nint, 8), w.P), 256, 0, st>>>(pay, w.scratch, w.len, w.off, w.nint, w.R, w.status);
-    jpeg_raw_copy<<<dim3(std::max(1, std::min(1184, (int)ceil_div(w.nv / 8, 256))), w.P), 256, 0, st>>>(
+    jpeg_raw_copy<<<dim3(std::max(1, std::min(16, (int)ceil_div(w.nv / 8, 256))), w.P), 256, 0, st>>>(
         w.coef, pay, w.nv, w.status);
     TQ_CHECK_CUDA(cudaGetLastError());
     return 4;
@@ -454,7 +454,7 @@ int jpeg_decode(uint8_t *const *pay, JpegWork &w, cudaStream_t st) {
     jpeg_markers<<<w.P, ST, 0, st>>>(pay, w.nint, w.off, w.status);
     jpeg_decode_k<<<dim3(ceil_div(w.nint, JT), w.P), JT, 0, st>>>(t, pay, w.coef, w.nv, w.R, w.nint, w.off,
                                                                    w.status);
-    jpeg_raw_in<<<dim3(std::max(1, std::min(1184, (int)ceil_div(w.nv / 8, 256))), w.P), 256, 0, st>>>(
+    jpeg_raw_in<<<dim3(std::max(1, std::min(16, (int)ceil_div(w.nv / 8, 256))), w.P), 256, 0, st>>>(
         pay, w.coef, w.nv);
     TQ_CHECK_CUDA(cudaGetLastError());
     return 3;
