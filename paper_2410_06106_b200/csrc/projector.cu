@@ -783,7 +783,8 @@ __global__ void __launch_bounds__(RJ * RG) fp_reduce_kernel(const FpRedArgs<T> a
 
 // ------------------------------------------------------------------ backprojector
 template <typename T, int EPI>
-__global__ void __launch_bounds__(BP_THREADS, sizeof(T) == 4 ? 5 : 1) bp_tile_kernel(const BpArgs<T> a) {
+__global__ void __launch_bounds__(BP_THREADS, sizeof(T) == 4 ? ((EPI == EPI_CGQ || EPI == EPI_PLAIN) ? 5 : 4) : 1)
+bp_tile_kernel(const BpArgs<T> a) {
     extern __shared__ __align__(16) unsigned char bp_smem[];
     T *win = reinterpret_cast<T *>(bp_smem);  // [BP_MAXA][BP_WB], bins pre-scaled by 1/m (fp64)
     float2 *win2 = reinterpret_cast<float2 *>(bp_smem);  // fp32: [BP_MAXA][BP_WB] pairs (s'_j, s'_{j+1})
