@@ -321,16 +321,20 @@ def main():
 
     # ---- end to end through the public API with host buffers: per step, H2D of the
     # slice sinogram from pinned memory, one iteration, D2H of a node's image
-    img_host = torch.empty(cfg.N * cfg.N, dtype=torch.float32).pin_memory()
+    # (the image read-out is tq_get_image_async on a copy stream into two pinned buffers, so the
+    # device-to-host transfer of step k overlaps step k + 1; all copies finish inside the region)
+    img_host = [torch.empty(cfg.N * cfg.N, dtype=torch.float32).pin_memory() for _ in range(2)]
+    copy_stream = torch.cuda.Stream()
     my_node = rank  # node `rank` lives on this rank (interleaved map)
     barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
     e2.record(stream)
-    for _ in range(args.steps):
+    for k in range(args.steps):
         ctx.set_sinogram(0, sino_host)
         ctx.run(1, stream)
-        ctx.image(0, my_node, host_out=img_host)
+        ctx.image_async(img_host[k & 1], copy_stream, 0, my_node)
+    copy_stream.synchronize()
     e3.record(stream)
     barrier()
     e2e_ms = max_over_ranks(e2.elapsed_time(e3))

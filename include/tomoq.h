@@ -138,6 +138,15 @@ tq_status tq_run(tq_ctx *ctx, int32_t iters, void *stream);
  *             paper rule: the consensus x.  out: N*N floats (host or device). */
 tq_status tq_get_image(tq_ctx *ctx, int32_t slice, int32_t node, float *out, int64_t len,
                        int32_t on_device);
+/* The same image, enqueued instead of waited for: the library snapshots it into one of two
+ * device staging buffers (on its own stream, after the last tq_run) and enqueues the copy to
+ * `out` on `stream` (a CUDA stream of the caller's; NULL = the legacy default stream).  The
+ * call returns at once; `out` (page-locked host or device memory) holds the image once
+ * `stream` has completed the copy, and must stay valid until then.  A third call waits for
+ * the copy of the first before reusing its staging buffer, so at most two are in flight --
+ * the next tq_run can overlap the transfer. */
+tq_status tq_get_image_async(tq_ctx *ctx, int32_t slice, int32_t node, float *out, int64_t len,
+                             int32_t on_device, void *stream);
 
 /* State of one local node as 3*N*N doubles: graph rule [x_i | alpha_i | xhat_i];
  * paper rule [u_m | lambda_m | x].  Import recomputes the next right-hand side. */

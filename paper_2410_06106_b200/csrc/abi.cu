@@ -140,6 +140,15 @@ tq_status tq_get_image(tq_ctx *ctx, int32_t slice, int32_t node, float *out, int
     });
 }
 
+tq_status tq_get_image_async(tq_ctx *ctx, int32_t slice, int32_t node, float *out, int64_t len,
+                             int32_t on_device, void *stream) {
+    if (!ctx) return TQ_EINVAL;
+    return guard(ctx, [&] {
+        TQ_REQUIRE(out != nullptr, "null output");
+        ctx->c.get_image_async(slice, node, out, len, on_device != 0, (cudaStream_t)stream);
+    });
+}
+
 tq_status tq_export_state(tq_ctx *ctx, int32_t slice, int32_t node, double *buf, int64_t len) {
     if (!ctx) return TQ_EINVAL;
     return guard(ctx, [&] {

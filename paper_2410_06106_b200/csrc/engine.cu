@@ -259,6 +259,13 @@ void Ctx::destroy() {
         if (g.second.pairs) cudaFree(g.second.pairs);
     gather_maps.clear();
     if (img_stage) cudaFree(img_stage);
+    for (int b = 0; b < 2; b++) {
+        if (img_done[b]) cudaEventSynchronize(img_done[b]);
+        if (img_async[b]) cudaFree(img_async[b]);
+        if (img_ready[b]) cudaEventDestroy(img_ready[b]);
+        if (img_done[b]) cudaEventDestroy(img_done[b]);
+        img_async[b] = nullptr; img_ready[b] = img_done[b] = nullptr;
+    }
     sino_stage = nullptr; img_stage = nullptr;
     if (comm) nccl().CommDestroy(comm);
     comm = nullptr;
@@ -692,6 +699,8 @@ void Ctx::run(int iters, cudaStream_t user) {
     TQ_CHECK_CUDA(cudaSetDevice(device));
     if (!xready) setup_exchange();
     cudaStream_t s = user ? user : stream;
+    for (int b = 0; b < 2; b++)  // an enqueued tq_get_image_async snapshot reads X first
+        if (img_used[b]) TQ_CHECK_CUDA(cudaStreamWaitEvent(s, img_ready[b], 0));
     if (need_rhs) {
         prepare_rhs(s);
         need_rhs = false;
@@ -762,22 +771,15 @@ void Ctx::run(int iters, cudaStream_t user) {
     }
 }
 
-void Ctx::get_image(int slice, int node, float *out, long long len, bool on_device) {
-    TQ_REQUIRE(len == n, "image length must be N*N");
-    TQ_CHECK_CUDA(cudaSetDevice(device));
-    if (!img_stage) TQ_CHECK_CUDA(cudaMalloc(&img_stage, sizeof(float) * n));
-    float *d = img_stage;
+void Ctx::snapshot_image(int slice, int node, float *d) {
     const int blocks = (int)std::min<long long>(2048, (n + 255) / 256);
     if (node >= 0) {
         const int i = local(slice, node);
         if (i < 0) fail(TQ_EINVAL, "node is not local to this rank");
-        if (prec == 0) d = (float *)in.xrow(in.X, i);  // fp32 state: copied out directly
-        else launch_convert(prec, in.xrow(in.X, i), 0, d, n, stream);
+        launch_convert(prec, in.xrow(in.X, i), 0, d, n, stream);
     } else if (segmented()) {
         TQ_REQUIRE(slice >= 0 && slice < S, "slice out of range");
-        const void *xg = (uint8_t *)XG + (prec ? 8 : 4) * (long long)slice * n;
-        if (prec == 0) d = (float *)xg;
-        else launch_convert(prec, xg, 0, d, n, stream);
+        launch_convert(prec, (uint8_t *)XG + (prec ? 8 : 4) * (long long)slice * n, 0, d, n, stream);
     } else {
         const int i0 = local(slice, 0);
         bool all = i0 >= 0;
@@ -787,8 +789,46 @@ void Ctx::get_image(int slice, int node, float *out, long long len, bool on_devi
         else mean_rows<double><<<blocks, 256, 0, stream>>>((const double *)in.xrow(in.X, i0), M, n, d);
         TQ_CHECK_CUDA(cudaGetLastError());
     }
-    TQ_CHECK_CUDA(cudaMemcpyAsync(out, d, sizeof(float) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream));
+}
+
+void Ctx::get_image(int slice, int node, float *out, long long len, bool on_device) {
+    TQ_REQUIRE(len == n, "image length must be N*N");
+    TQ_CHECK_CUDA(cudaSetDevice(device));
+    const float *src = nullptr;
+    if (prec == 0 && node >= 0) {  // fp32 state: copied out directly
+        const int i = local(slice, node);
+        if (i < 0) fail(TQ_EINVAL, "node is not local to this rank");
+        src = (const float *)in.xrow(in.X, i);
+    } else if (prec == 0 && segmented()) {
+        TQ_REQUIRE(slice >= 0 && slice < S, "slice out of range");
+        src = (const float *)((uint8_t *)XG + 4 * (long long)slice * n);
+    } else {
+        if (!img_stage) TQ_CHECK_CUDA(cudaMalloc(&img_stage, sizeof(float) * n));
+        snapshot_image(slice, node, img_stage);
+        src = img_stage;
+    }
+    TQ_CHECK_CUDA(cudaMemcpyAsync(out, src, sizeof(float) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream));
     TQ_CHECK_CUDA(cudaStreamSynchronize(stream));
+}
+
+void Ctx::get_image_async(int slice, int node, float *out, long long len, bool on_device, cudaStream_t s) {
+    TQ_REQUIRE(len == n, "image length must be N*N");
+    TQ_CHECK_CUDA(cudaSetDevice(device));
+    const int b = img_buf;
+    if (!img_async[b]) {
+        TQ_CHECK_CUDA(cudaMalloc(&img_async[b], sizeof(float) * n));
+        TQ_CHECK_CUDA(cudaEventCreateWithFlags(&img_ready[b], cudaEventDisableTiming));
+        TQ_CHECK_CUDA(cudaEventCreateWithFlags(&img_done[b], cudaEventDisableTiming));
+    }
+    if (img_used[b]) TQ_CHECK_CUDA(cudaStreamWaitEvent(stream, img_done[b], 0));  // its last copy left
+    snapshot_image(slice, node, img_async[b]);
+    TQ_CHECK_CUDA(cudaEventRecord(img_ready[b], stream));
+    TQ_CHECK_CUDA(cudaStreamWaitEvent(s, img_ready[b], 0));
+    TQ_CHECK_CUDA(cudaMemcpyAsync(out, img_async[b], sizeof(float) * n,
+                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    TQ_CHECK_CUDA(cudaEventRecord(img_done[b], s));
+    img_used[b] = true;
+    img_buf ^= 1;
 }
 
 static void to_host_double(int prec, const void *src, double *dst, long long n, cudaStream_t s) {

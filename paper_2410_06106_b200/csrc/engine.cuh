@@ -124,6 +124,7 @@ struct Ctx {
     void set_sinogram(int slice, int node, const float *d, long long len, bool on_device);
     void run(int iters, cudaStream_t user);
     void get_image(int slice, int node, float *out, long long len, bool on_device);
+    void get_image_async(int slice, int node, float *out, long long len, bool on_device, cudaStream_t s);
     void export_state(int slice, int node, double *buf, long long len);
     void import_state(int slice, int node, const double *buf, long long len);
     void export_labels(int slice, int node, int32_t *buf, long long len);
@@ -133,6 +134,12 @@ struct Ctx {
     struct GatherMap { int *pairs; int count; };
     std::map<std::pair<int, int>, GatherMap> gather_maps;  // (slice, node) -> sinogram row pairs
     float *img_stage = nullptr;    // persistent staging of tq_get_image
+    float *img_async[2] = {nullptr, nullptr};  // tq_get_image_async staging (double-buffered)
+    cudaEvent_t img_ready[2] = {nullptr, nullptr}, img_done[2] = {nullptr, nullptr};
+    int img_buf = 0;
+    bool img_used[2] = {false, false};
+    // the snapshot kernel of get_image / get_image_async into d (fp32) on `stream`
+    void snapshot_image(int slice, int node, float *d);
 
    private:
     void invalidate();

@@ -67,6 +67,7 @@ _SIGS = {
     "tq_set_sinogram": [_vp, _i32, _i32, _vp, _i64, _i32],
     "tq_run": [_vp, _i32, _vp],
     "tq_get_image": [_vp, _i32, _i32, _vp, _i64, _i32],
+    "tq_get_image_async": [_vp, _i32, _i32, _vp, _i64, _i32, _vp],
     "tq_export_state": [_vp, _i32, _i32, _vp, _i64],
     "tq_import_state": [_vp, _i32, _i32, _vp, _i64],
     "tq_export_labels": [_vp, _i32, _i32, _vp, _i64],
@@ -227,6 +228,13 @@ class Context:
         a = np.zeros(self.n, np.float32)
         self._c(lib().tq_get_image(self.h, slice_, node, a.ctypes.data, self.n, 0))
         return a.reshape(self.N, self.N)
+
+    def image_async(self, out, stream, slice_=0, node=-1):
+        """Enqueue the image copy into `out` (pinned host or CUDA fp32 tensor, N*N) on the
+        torch CUDA `stream`; it is there once `stream` completes (tq_get_image_async)."""
+        self._c(lib().tq_get_image_async(self.h, slice_, node, out.data_ptr(), self.n, 1 if out.is_cuda else 0,
+                                         _stream(stream)))
+        return out
 
     def export_state(self, slice_, node):
         buf = np.zeros(3 * self.n, np.float64)

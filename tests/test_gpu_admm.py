@@ -316,3 +316,29 @@ def test_siddon_projector_admm_c1(prec, tol):
     o = oracle_case(cfg, inp).run(cfg.iters)
     assert rel(ctx.image(), o.image()) <= tol
     assert rel(ctx.image(), oracle_case(C.C1(), inp).run(cfg.iters).image()) > 10 * tol  # not Joseph
+
+
+def test_image_async_double_buffer():
+    """tq_get_image_async: back-to-back iterations with the previous image still in flight
+    deliver exactly the images the blocking call returns, in order (two staging buffers,
+    the next tq_run waits for the snapshot, the third call for the first copy)."""
+    import torch
+    cfg = c2s()
+    inp = C.make_inputs(cfg)
+    a = gpu_context(cfg, inp)
+    b = gpu_context(cfg, inp)
+    st = torch.cuda.Stream()
+    outs = [torch.empty(cfg.N * cfg.N, dtype=torch.float32).pin_memory() for _ in range(4)]
+    want = []
+    for k in range(4):
+        a.run(1)
+        a.image_async(outs[k], st, 0, 1)
+        b.run(1)
+        want.append(b.image(0, 1).ravel())
+    st.synchronize()
+    for k in range(4):
+        assert np.array_equal(outs[k].numpy(), want[k])
+    dev = torch.empty(cfg.N * cfg.N, dtype=torch.float32, device="cuda")
+    a.image_async(dev, st)  # mean image into device memory
+    st.synchronize()
+    assert np.array_equal(dev.cpu().numpy(), a.image().ravel())
