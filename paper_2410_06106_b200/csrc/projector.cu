@@ -887,19 +887,25 @@ bp_tile_kernel(const BpArgs<T> a) {
             const T tau_t = (T)(s_tau[k] + (double)lx * s_csd[k] - (double)prow * s_snd[k]);
             if constexpr (sizeof(T) == 4) {
                 const uint32_t wb = magic_base(win2 + k * BP_WB, a.magic);  // magic = 0x4B000000 << 3
+                // pixels kx, kx + 1 as one packed pair for the position, floor and fraction
+                // (FFMA2 / FADD2.RM / FADD2 / FFMA2: the scalar form's IEEE operations, two per issue)
+                const float2 cs2 = make_float2(cs, cs), mg2 = make_float2(8388608.0f, 8388608.0f);
+                const float2 nmg2 = make_float2(-8388608.0f, -8388608.0f), m1 = make_float2(-1.0f, -1.0f);
 #pragma unroll
                 for (int ky = 0; ky < 2; ky++) {
                     const float tau_r = fmaf((float)(-4 * ky), sn, tau_t);
+                    const float2 tr2 = make_float2(tau_r, tau_r);
 #pragma unroll
-                    for (int kx = 0; kx < 8; kx++) {
-                        const float tau = fmaf((float)(8 * kx), cs, tau_r);
-                        const float m = __fadd_rd(tau, 8388608.0f);   // 2^23 + floor(tau)
-                        const float2 sv = lds64((__float_as_uint(m) << 3) + wb);
-                        const float u = tau - (m - 8388608.0f);
-                        const float w0 = __saturatef(fmaf(-u, a1, a0));
-                        const float w1 = __saturatef(fmaf(u, a1, a0m));
-                        acc[ky][kx] = fmaf(w0, sv.x, acc[ky][kx]);
-                        acc[ky][kx] = fmaf(w1, sv.y, acc[ky][kx]);
+                    for (int kx = 0; kx < 8; kx += 2) {
+                        const float2 tau = __ffma2_rn(make_float2((float)(8 * kx), (float)(8 * kx + 8)), cs2, tr2);
+                        const float2 m = __fadd2_rd(tau, mg2);   // 2^23 + floor(tau)
+                        const float2 sv0 = lds64((__float_as_uint(m.x) << 3) + wb);
+                        const float2 sv1 = lds64((__float_as_uint(m.y) << 3) + wb);
+                        const float2 u = __ffma2_rn(__fadd2_rn(m, nmg2), m1, tau);  // tau - floor(tau)
+                        acc[ky][kx] = fmaf(__saturatef(fmaf(-u.x, a1, a0)), sv0.x, acc[ky][kx]);
+                        acc[ky][kx] = fmaf(__saturatef(fmaf(u.x, a1, a0m)), sv0.y, acc[ky][kx]);
+                        acc[ky][kx + 1] = fmaf(__saturatef(fmaf(-u.y, a1, a0)), sv1.x, acc[ky][kx + 1]);
+                        acc[ky][kx + 1] = fmaf(__saturatef(fmaf(u.y, a1, a0m)), sv1.y, acc[ky][kx + 1]);
                     }
                 }
             } else {
