@@ -635,17 +635,22 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
                     acc1 = acc2.y;
                 } else {  // pixel a + 1 gets g = sat((u - 1/2) / w + 1/2) of the band's length
                     const float iw = siddon_iw(B), hw = 0.5f - 0.5f * iw;
+                    const float2 B2 = make_float2(B, B), kap2 = make_float2(kap, kap);
+                    const float2 mg2 = make_float2(FP2_MAGIC, FP2_MAGIC), nmg2 = make_float2(-FP2_MAGIC, -FP2_MAGIC);
+                    const float2 m1v = make_float2(-1.0f, -1.0f);
+                    float2 acc2 = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int l = 0; l < FP_TH; l += 2) {
-                        const float kf0 = fmaf((float)l, B, kap), kf1 = fmaf((float)(l + 1), B, kap);
-                        const float m0 = __fadd_rd(kf0, FP2_MAGIC), m1 = __fadd_rd(kf1, FP2_MAGIC);
-                        const float2 q0 = lds64((__float_as_uint(m0) << 3) + sb + l * FP2_PITCH * 8);
-                        const float2 q1 = lds64((__float_as_uint(m1) << 3) + sb + (l + 1) * FP2_PITCH * 8);
-                        const float g0 = __saturatef(fmaf(kf0 - (m0 - FP2_MAGIC), iw, hw));
-                        const float g1 = __saturatef(fmaf(kf1 - (m1 - FP2_MAGIC), iw, hw));
-                        acc0 += fmaf(g0, q0.y, q0.x);
-                        acc1 += fmaf(g1, q1.y, q1.x);
+                    for (int l = 0; l < FP_TH; l += 2) {  // line pairs packed as in the Joseph loop
+                        const float2 kf = __ffma2_rn(make_float2((float)l, (float)(l + 1)), B2, kap2);
+                        const float2 m = __fadd2_rd(kf, mg2);
+                        const float2 q0 = lds64((__float_as_uint(m.x) << 3) + sb + l * FP2_PITCH * 8);
+                        const float2 q1 = lds64((__float_as_uint(m.y) << 3) + sb + (l + 1) * FP2_PITCH * 8);
+                        const float2 u = __ffma2_rn(__fadd2_rn(m, nmg2), m1v, kf);  // kf - floor(kf)
+                        const float g0 = __saturatef(fmaf(u.x, iw, hw)), g1 = __saturatef(fmaf(u.y, iw, hw));
+                        acc2 = __fadd2_rn(acc2, make_float2(fmaf(g0, q0.y, q0.x), fmaf(g1, q1.y, q1.x)));
                     }
+                    acc0 = acc2.x;
+                    acc1 = acc2.y;
                 }
                 if (ok)
                     a.partial[((long long)R[k].row * a.nt_line + lt) * 2 * a.n_det + (ct & 1) * a.n_det + R[k].jlo + w] =
