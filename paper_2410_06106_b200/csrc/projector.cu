@@ -794,7 +794,7 @@ __global__ void __launch_bounds__(RJ * RG) fp_reduce_kernel(const FpRedArgs<T> a
 
 // ------------------------------------------------------------------ backprojector
 template <typename T, int EPI>
-__global__ void __launch_bounds__(BP_THREADS, sizeof(T) == 4 ? ((EPI == EPI_CGQ || EPI == EPI_PLAIN) ? 5 : 4) : 1)
+__global__ void __launch_bounds__(BP_THREADS, sizeof(T) == 4 ? 4 : 1)
 bp_tile_kernel(const BpArgs<T> a) {
     extern __shared__ __align__(16) unsigned char bp_smem[];
     T *win = reinterpret_cast<T *>(bp_smem);  // [BP_MAXA][BP_WB], bins pre-scaled by 1/m (fp64)
@@ -840,10 +840,14 @@ bp_tile_kernel(const BpArgs<T> a) {
         asm volatile("cp.async.commit_group;");
     }
     T acc[2][8];
+    float2 acc2[2][8];  // fp32: per pixel the (lower-tap, upper-tap) partial sums
 #pragma unroll
     for (int ky = 0; ky < 2; ky++)
 #pragma unroll
-        for (int kx = 0; kx < 8; kx++) acc[ky][kx] = 0;
+        for (int kx = 0; kx < 8; kx++) {
+            acc[ky][kx] = 0;
+            acc2[ky][kx] = make_float2(0.f, 0.f);
+        }
 
     for (int k0 = 0; k0 < nang; k0 += BP_MAXA) {
         const int kc = min(BP_MAXA, nang - k0);
@@ -907,10 +911,11 @@ bp_tile_kernel(const BpArgs<T> a) {
                         const float2 sv0 = lds64((__float_as_uint(m.x) << 3) + wb);
                         const float2 sv1 = lds64((__float_as_uint(m.y) << 3) + wb);
                         const float2 u = __ffma2_rn(__fadd2_rn(m, nmg2), m1, tau);  // tau - floor(tau)
-                        acc[ky][kx] = fmaf(__saturatef(fmaf(-u.x, a1, a0)), sv0.x, acc[ky][kx]);
-                        acc[ky][kx] = fmaf(__saturatef(fmaf(u.x, a1, a0m)), sv0.y, acc[ky][kx]);
-                        acc[ky][kx + 1] = fmaf(__saturatef(fmaf(-u.y, a1, a0)), sv1.x, acc[ky][kx + 1]);
-                        acc[ky][kx + 1] = fmaf(__saturatef(fmaf(u.y, a1, a0m)), sv1.y, acc[ky][kx + 1]);
+                        // the two taps of a pixel accumulate into a packed (lower, upper) pair
+                        acc2[ky][kx] = __ffma2_rn(make_float2(__saturatef(fmaf(-u.x, a1, a0)),
+                                                              __saturatef(fmaf(u.x, a1, a0m))), sv0, acc2[ky][kx]);
+                        acc2[ky][kx + 1] = __ffma2_rn(make_float2(__saturatef(fmaf(-u.y, a1, a0)),
+                                                                  __saturatef(fmaf(u.y, a1, a0m))), sv1, acc2[ky][kx + 1]);
                     }
                 }
             } else {
@@ -932,6 +937,12 @@ bp_tile_kernel(const BpArgs<T> a) {
                 }
             }
         }
+    }
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int ky = 0; ky < 2; ky++)
+#pragma unroll
+            for (int kx = 0; kx < 8; kx++) acc[ky][kx] = acc2[ky][kx].x + acc2[ky][kx].y;
     }
     // ---------------- epilogue (fp64 in registers)
     if (pre) {
