@@ -320,9 +320,11 @@ def main():
     iters_per_s = args.steps / (ms / 1e3)
 
     # ---- end to end through the public API with host buffers: per step, H2D of the
-    # slice sinogram from pinned memory, one iteration, D2H of a node's image
-    # (the image read-out is tq_get_image_async on a copy stream into two pinned buffers, so the
-    # device-to-host transfer of step k overlaps step k + 1; all copies finish inside the region)
+    # slice sinogram from pinned memory (tq_set_sinogram), one iteration enqueued without
+    # waiting (tq_run_async), D2H of a node's image (tq_get_image_async on a copy stream into
+    # two pinned buffers), so the host work and the transfers of step k overlap the device
+    # work of steps k - 1 and k + 1; tq_wait (divergence check) and every copy finish inside
+    # the region
     img_host = [torch.empty(cfg.N * cfg.N, dtype=torch.float32).pin_memory() for _ in range(2)]
     copy_stream = torch.cuda.Stream()
     my_node = rank  # node `rank` lives on this rank (interleaved map)
@@ -332,8 +334,9 @@ def main():
     e2.record(stream)
     for k in range(args.steps):
         ctx.set_sinogram(0, sino_host)
-        ctx.run(1, stream)
+        ctx.run_async(1, stream)
         ctx.image_async(img_host[k & 1], copy_stream, 0, my_node)
+    ctx.wait()
     copy_stream.synchronize()
     e3.record(stream)
     barrier()

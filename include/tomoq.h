@@ -124,7 +124,8 @@ tq_status tq_set_quantizer(tq_ctx *ctx, const tq_quant *q);
 /* Sinogram of one slice.  node >= 0: that node's shard ([a_node][n_det], its angles in
  * increasing order); node == -1: the full slice sinogram [n_angles][n_det] and the
  * library keeps the rows of its local nodes.  Ignored for nodes not on this rank.
- * len is in floats; on_device: d is a device pointer. */
+ * len is in floats; on_device: d is a device pointer.  Returns once d has been copied (the
+ * caller may reuse it); the new rows replace the old ones after any enqueued run. */
 tq_status tq_set_sinogram(tq_ctx *ctx, int32_t slice, int32_t node, const float *d,
                           int64_t len, int32_t on_device);
 
@@ -132,6 +133,14 @@ tq_status tq_set_sinogram(tq_ctx *ctx, int32_t slice, int32_t node, const float 
  * context's own stream) and wait for them; returns TQ_EDIVERGED if any node's norm
  * exceeds 1e12 after the last iteration. */
 tq_status tq_run(tq_ctx *ctx, int32_t iters, void *stream);
+/* The same iterations, enqueued and not waited for: returns once they are on `stream`.
+ * tq_set_sinogram, tq_get_image_async and a further tq_run_async may follow at once (they
+ * order themselves after it on the device); every other call first waits for it.  Its
+ * statistics and divergence check (TQ_EDIVERGED) are reported by the first call that waits
+ * -- tq_wait, tq_run, tq_get_image, tq_get_stats, tq_export_state, ... */
+tq_status tq_run_async(tq_ctx *ctx, int32_t iters, void *stream);
+/* Wait for the last enqueued run; TQ_EDIVERGED as tq_run.  TQ_OK at once if none. */
+tq_status tq_wait(tq_ctx *ctx);
 
 /* node >= 0: that node's private iterate (graph) / u_m (paper) -- must be local.
  * node == -1: graph rule: mean over the slice's nodes of x_i (all must be local, R-22);

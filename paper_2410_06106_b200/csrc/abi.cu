@@ -131,6 +131,16 @@ tq_status tq_run(tq_ctx *ctx, int32_t iters, void *stream) {
     return guard(ctx, [&] { ctx->c.run(iters, (cudaStream_t)stream); });
 }
 
+tq_status tq_run_async(tq_ctx *ctx, int32_t iters, void *stream) {
+    if (!ctx) return TQ_EINVAL;
+    return guard(ctx, [&] { ctx->c.run_async(iters, (cudaStream_t)stream); });
+}
+
+tq_status tq_wait(tq_ctx *ctx) {
+    if (!ctx) return TQ_EINVAL;
+    return guard(ctx, [&] { ctx->c.finish(); });
+}
+
 tq_status tq_get_image(tq_ctx *ctx, int32_t slice, int32_t node, float *out, int64_t len,
                        int32_t on_device) {
     if (!ctx) return TQ_EINVAL;
@@ -186,8 +196,10 @@ tq_status tq_launch_component(tq_ctx *ctx, int32_t component, int32_t reps, void
 
 tq_status tq_get_stats(const tq_ctx *ctx, tq_stats *out) {
     if (!ctx || !out) return TQ_EINVAL;
+    tq_ctx *c = const_cast<tq_ctx *>(ctx);  // the handle is never a const object
+    const tq_status r = guard(c, [&] { c->c.finish(); });
     *out = ctx->c.st;
-    return TQ_OK;
+    return r;
 }
 
 const char *tq_last_error(const tq_ctx *ctx) { return ctx ? ctx->c.err.c_str() : g_err.c_str(); }

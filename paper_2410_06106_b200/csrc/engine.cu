@@ -190,8 +190,11 @@ void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int ran
     L = (int)loc.size();
     TQ_CHECK_CUDA(cudaSetDevice(device));
     TQ_CHECK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    TQ_CHECK_CUDA(cudaStreamCreateWithFlags(&up_stream, cudaStreamNonBlocking));
     TQ_CHECK_CUDA(cudaEventCreate(&ev0));
     TQ_CHECK_CUDA(cudaEventCreate(&ev1));
+    for (cudaEvent_t *e : {&run_done, &stage_copied[0], &stage_copied[1], &stage_free[0], &stage_free[1]})
+        TQ_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     TQ_REQUIRE(g.projector == TQ_PROJ_JOSEPH || g.projector == TQ_PROJ_SIDDON, "bad projector");
     geo.init(N, n_ang, n_det, g.projector);
     in.init(prec, geo, angles);
@@ -245,7 +248,11 @@ void Ctx::free_exchange() {
 }
 
 void Ctx::destroy() {
+    if (run_done) cudaEventSynchronize(run_done);
+    pending = false;
+    pend_gathers.clear();
     if (stream) cudaStreamSynchronize(stream);
+    if (up_stream) cudaStreamSynchronize(up_stream);
     free_exchange();
     in.release();
     geo.release();
@@ -254,7 +261,11 @@ void Ctx::destroy() {
     if (CSUM) cudaFree(CSUM);
     ALPHA = XG = nullptr;
     CSUM = nullptr;
-    if (sino_stage) cudaFree(sino_stage);
+    for (int b = 0; b < 2; b++) {
+        if (sino_stage[b]) cudaFree(sino_stage[b]);
+        sino_stage[b] = nullptr;
+        sino_stage_len[b] = 0;
+    }
     for (auto &g : gather_maps)
         if (g.second.pairs) cudaFree(g.second.pairs);
     gather_maps.clear();
@@ -266,16 +277,25 @@ void Ctx::destroy() {
         if (img_done[b]) cudaEventDestroy(img_done[b]);
         img_async[b] = nullptr; img_ready[b] = img_done[b] = nullptr;
     }
-    sino_stage = nullptr; img_stage = nullptr;
+    img_stage = nullptr;
     if (comm) nccl().CommDestroy(comm);
     comm = nullptr;
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    for (cudaEvent_t *e : {&run_done, &stage_copied[0], &stage_copied[1], &stage_free[0], &stage_free[1]}) {
+        if (*e) cudaEventDestroy(*e);
+        *e = nullptr;
+    }
+    if (norm_host) cudaFreeHost(norm_host);
+    norm_host = nullptr;
     if (stream) cudaStreamDestroy(stream);
     stream = nullptr;
+    if (up_stream) cudaStreamDestroy(up_stream);
+    up_stream = nullptr;
 }
 
 void Ctx::set_params(const tq_params &p) {
+    finish();
     TQ_REQUIRE(p.rho > 0.0 && std::isfinite(p.rho), "rho must be > 0");
     TQ_REQUIRE(p.inner == TQ_INNER_GD || p.inner == TQ_INNER_CG, "inner must be GD or CG");
     TQ_REQUIRE(p.e1 >= 0 && p.e1 <= 100000, "e1 out of range");
@@ -303,6 +323,7 @@ void Ctx::set_params(const tq_params &p) {
 }
 
 void Ctx::set_quant(const tq_quant &qq) {
+    finish();
     TQ_REQUIRE(qq.kind >= TQ_Q_NONE && qq.kind <= TQ_Q_ALTERNATE, "bad quantizer kind");
     const bool km = qq.kind == TQ_Q_KMEANS || qq.kind == TQ_Q_ALTERNATE;
     const bool dc = qq.kind == TQ_Q_DCT || qq.kind == TQ_Q_ALTERNATE;
@@ -323,17 +344,32 @@ void Ctx::set_sinogram(int slice, int node, const float *d, long long len, bool 
     TQ_REQUIRE(d != nullptr, "null sinogram");
     const long long rows = node < 0 ? n_ang : (aoff[node + 1] - aoff[node]);
     TQ_REQUIRE(len == rows * n_det, "sinogram length mismatch");
-    // staging copy on the device, then a gather of the rows of every local node
+    // staging copy on the device (upload stream, double-buffered), then a gather of the rows
+    // of every local node, deferred to the stream of the next run (flush_gathers)
     TQ_CHECK_CUDA(cudaSetDevice(device));
-    if (sino_stage_len < len) {
-        if (sino_stage) cudaFree(sino_stage);
-        sino_stage = nullptr;
-        TQ_CHECK_CUDA(cudaMalloc(&sino_stage, sizeof(float) * len));
-        sino_stage_len = len;
+    const int b = stage_buf;
+    for (const PendGather &pg : pend_gathers)  // both buffers queued: place the older gathers now
+        if (pg.buf == b) {
+            flush_gathers(pending ? run_s : stream);
+            break;
+        }
+    if (sino_stage_len[b] < len) {
+        TQ_CHECK_CUDA(cudaStreamSynchronize(up_stream));
+        if (sino_stage[b]) {
+            TQ_CHECK_CUDA(cudaEventSynchronize(stage_free[b]));
+            cudaFree(sino_stage[b]);
+        }
+        sino_stage[b] = nullptr;
+        TQ_CHECK_CUDA(cudaMalloc(&sino_stage[b], sizeof(float) * len));
+        sino_stage_len[b] = len;
     }
-    float *stage = sino_stage;
-    TQ_CHECK_CUDA(cudaMemcpyAsync(stage, d, sizeof(float) * len,
-                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream));
+    // the buffer is free once the last gather that read it ran; the caller's buffer is free
+    // once this copy completed (waited for below)
+    TQ_CHECK_CUDA(cudaStreamWaitEvent(up_stream, stage_free[b], 0));
+    TQ_CHECK_CUDA(cudaMemcpyAsync(sino_stage[b], d, sizeof(float) * len,
+                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, up_stream));
+    TQ_CHECK_CUDA(cudaEventRecord(stage_copied[b], up_stream));
+    stage_buf ^= 1;
     // (source row, destination row) pairs of the local nodes, built once per (slice, node)
     auto it = gather_maps.find({slice, node});
     if (it == gather_maps.end()) {
@@ -356,17 +392,41 @@ void Ctx::set_sinogram(int slice, int node, const float *d, long long len, bool 
     }
     for (int i = 0; i < L; i++)
         if (loc[i].first == slice && (node < 0 || loc[i].second == node)) sino_set[i] = 1;
-    if (it->second.count) {
-        const dim3 grid(ceil_div(n_det, 256), it->second.count);
-        if (prec == 0) gather_rows<float><<<grid, 256, 0, stream>>>(stage, it->second.pairs, (float *)in.D, n_det);
-        else gather_rows<double><<<grid, 256, 0, stream>>>(stage, it->second.pairs, (double *)in.D, n_det);
-        TQ_CHECK_CUDA(cudaGetLastError());
+    pend_gathers.push_back(PendGather{b, it->second.pairs, it->second.count});
+    TQ_CHECK_CUDA(cudaEventSynchronize(stage_copied[b]));
+}
+
+// A stream wait on an event that has already completed is left out: no dependency node in
+// front of the next graph launch.
+static void wait_unless_done(cudaStream_t s, cudaEvent_t e) {
+    const cudaError_t q = cudaEventQuery(e);
+    if (q == cudaSuccess) return;
+    if (q != cudaErrorNotReady) TQ_CHECK_CUDA(q);
+    TQ_CHECK_CUDA(cudaStreamWaitEvent(s, e, 0));
+}
+
+// The deferred sinogram gathers, in call order, on s: behind every run enqueued before them
+// (s is the stream of the last run, or the next run's), ahead of the next.
+void Ctx::flush_gathers(cudaStream_t s) {
+    if (pend_gathers.empty()) return;
+    if (pending && s != run_s) TQ_CHECK_CUDA(cudaStreamWaitEvent(s, run_done, 0));
+    for (const PendGather &pg : pend_gathers) {
+        wait_unless_done(s, stage_copied[pg.buf]);
+        if (pg.count) {
+            const dim3 grid(ceil_div(n_det, 256), pg.count);
+            if (prec == 0) gather_rows<float><<<grid, 256, 0, s>>>(sino_stage[pg.buf], pg.pairs, (float *)in.D, n_det);
+            else gather_rows<double><<<grid, 256, 0, s>>>(sino_stage[pg.buf], pg.pairs, (double *)in.D, n_det);
+            TQ_CHECK_CUDA(cudaGetLastError());
+        }
+        TQ_CHECK_CUDA(cudaEventRecord(stage_free[pg.buf], s));
     }
-    TQ_CHECK_CUDA(cudaStreamSynchronize(stream));
+    pend_gathers.clear();
 }
 
 long long Ctx::launch_component(int component, int reps, cudaStream_t s) {
     TQ_REQUIRE(reps >= 0, "reps must be >= 0");
+    finish();
+    flush_gathers(s ? s : stream);
     if (!have_params) fail(TQ_ESTATE, "tq_set_params must be called first");
     TQ_CHECK_CUDA(cudaSetDevice(device));
     if (!xready) setup_exchange();
@@ -692,15 +752,28 @@ int Ctx::prepare_rhs(cudaStream_t s) {
 }
 
 void Ctx::run(int iters, cudaStream_t user) {
+    enqueue(iters, user);
+    finish();
+}
+
+void Ctx::run_async(int iters, cudaStream_t user) { enqueue(iters, user); }
+
+void Ctx::enqueue(int iters, cudaStream_t user) {
     TQ_REQUIRE(iters >= 0, "iters must be >= 0");
     if (!have_params) fail(TQ_ESTATE, "tq_set_params must be called before tq_run");
     for (int i = 0; i < L; i++)
         if (!sino_set[i]) fail(TQ_ESTATE, "sinogram of a local node was never set");
     TQ_CHECK_CUDA(cudaSetDevice(device));
-    if (!xready) setup_exchange();
+    if (!xready) {
+        finish();  // the exchange state is (re)built: nothing may be in flight
+        setup_exchange();
+    }
     cudaStream_t s = user ? user : stream;
+    if (pending && s != run_s) TQ_CHECK_CUDA(cudaStreamWaitEvent(s, run_done, 0));  // previous run
+    flush_gathers(s);  // a new sinogram: its gather, in-stream
     for (int b = 0; b < 2; b++)  // an enqueued tq_get_image_async snapshot reads X first
-        if (img_used[b]) TQ_CHECK_CUDA(cudaStreamWaitEvent(s, img_ready[b], 0));
+        if (img_used[b] && img_s[b] != s) TQ_CHECK_CUDA(cudaStreamWaitEvent(s, img_ready[b], 0));
+    run_s = s;
     if (need_rhs) {
         prepare_rhs(s);
         need_rhs = false;
@@ -746,16 +819,27 @@ void Ctx::run(int iters, cudaStream_t user) {
     TQ_CHECK_CUDA(cudaEventRecord(ev1, s));
     // CG with E1 >= 1 leaves ||x||^2 in the scalar table (its last step); otherwise compute it
     if (!(iters > 0 && prm.inner == TQ_INNER_CG && prm.e1 >= 1)) in.norm2(s);
-    std::vector<double> sc((size_t)S_NSLOT * std::max(1, L));
-    TQ_CHECK_CUDA(cudaMemcpyAsync(sc.data(), in.scal, sizeof(double) * S_NSLOT * L, cudaMemcpyDeviceToHost, s));
-    TQ_CHECK_CUDA(cudaStreamSynchronize(s));
+    if (!norm_host) TQ_CHECK_CUDA(cudaMallocHost(&norm_host, sizeof(double) * S_NSLOT * std::max(1, L)));
+    if (L) TQ_CHECK_CUDA(cudaMemcpyAsync(norm_host, in.scal, sizeof(double) * S_NSLOT * L, cudaMemcpyDeviceToHost, s));
+    TQ_CHECK_CUDA(cudaEventRecord(run_done, s));
+    st.iters += iters;
+    st.kernel_launches = (long long)iters * per_iter;
+    pending = true;
+    pending_iters = iters;
+}
+
+// The host side of an enqueued run: wait for it, then its statistics and the divergence
+// guard (SPEC "divergence guard"; the norms of its last iteration).
+void Ctx::finish() {
+    if (!pending) return;
+    pending = false;
+    TQ_CHECK_CUDA(cudaEventSynchronize(run_done));
+    const int iters = pending_iters;
     float ms = 0.f;
     TQ_CHECK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
     st.ms_last_run = ms;
-    st.iters += iters;
-    st.kernel_launches = (long long)iters * per_iter;
     for (int i = 0; i < L; i++) {
-        const double nrm = sqrt(sc[(size_t)i * S_NSLOT + S_NORM]);
+        const double nrm = sqrt(norm_host[(size_t)i * S_NSLOT + S_NORM]);
         if (!(nrm <= 1e12)) fail(TQ_EDIVERGED, "node iterate norm exceeded 1e12 (diverged)");
     }
     if (iters > 0 && (jenc.P || jdec.P)) {  // entropy-coded DCT payloads: actual sizes, stream checks
@@ -771,7 +855,7 @@ void Ctx::run(int iters, cudaStream_t user) {
     }
 }
 
-void Ctx::snapshot_image(int slice, int node, float *d) {
+void Ctx::snapshot_image(int slice, int node, float *d, cudaStream_t stream) {
     const int blocks = (int)std::min<long long>(2048, (n + 255) / 256);
     if (node >= 0) {
         const int i = local(slice, node);
@@ -793,6 +877,7 @@ void Ctx::snapshot_image(int slice, int node, float *d) {
 
 void Ctx::get_image(int slice, int node, float *out, long long len, bool on_device) {
     TQ_REQUIRE(len == n, "image length must be N*N");
+    finish();
     TQ_CHECK_CUDA(cudaSetDevice(device));
     const float *src = nullptr;
     if (prec == 0 && node >= 0) {  // fp32 state: copied out directly
@@ -804,7 +889,7 @@ void Ctx::get_image(int slice, int node, float *out, long long len, bool on_devi
         src = (const float *)((uint8_t *)XG + 4 * (long long)slice * n);
     } else {
         if (!img_stage) TQ_CHECK_CUDA(cudaMalloc(&img_stage, sizeof(float) * n));
-        snapshot_image(slice, node, img_stage);
+        snapshot_image(slice, node, img_stage, stream);
         src = img_stage;
     }
     TQ_CHECK_CUDA(cudaMemcpyAsync(out, src, sizeof(float) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream));
@@ -820,9 +905,13 @@ void Ctx::get_image_async(int slice, int node, float *out, long long len, bool o
         TQ_CHECK_CUDA(cudaEventCreateWithFlags(&img_ready[b], cudaEventDisableTiming));
         TQ_CHECK_CUDA(cudaEventCreateWithFlags(&img_done[b], cudaEventDisableTiming));
     }
-    if (img_used[b]) TQ_CHECK_CUDA(cudaStreamWaitEvent(stream, img_done[b], 0));  // its last copy left
-    snapshot_image(slice, node, img_async[b]);
-    TQ_CHECK_CUDA(cudaEventRecord(img_ready[b], stream));
+    // the snapshot goes behind the last enqueued run on its stream (or on the context's own
+    // stream when none is pending), once this buffer's previous copy has left
+    cudaStream_t ss = pending ? run_s : stream;
+    if (img_used[b]) wait_unless_done(ss, img_done[b]);
+    snapshot_image(slice, node, img_async[b], ss);
+    TQ_CHECK_CUDA(cudaEventRecord(img_ready[b], ss));
+    img_s[b] = ss;
     TQ_CHECK_CUDA(cudaStreamWaitEvent(s, img_ready[b], 0));
     TQ_CHECK_CUDA(cudaMemcpyAsync(out, img_async[b], sizeof(float) * n,
                                   on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
@@ -851,6 +940,7 @@ static void from_host_double(int prec, const double *src, void *dst, long long n
 
 void Ctx::export_state(int slice, int node, double *buf, long long len) {
     TQ_REQUIRE(len == 3 * n, "state length must be 3*N*N");
+    finish();
     const int i = local(slice, node);
     TQ_REQUIRE(i >= 0, "node is not local to this rank");
     TQ_CHECK_CUDA(cudaSetDevice(device));
@@ -874,6 +964,7 @@ void Ctx::export_state(int slice, int node, double *buf, long long len) {
 
 void Ctx::import_state(int slice, int node, const double *buf, long long len) {
     TQ_REQUIRE(len == 3 * n, "state length must be 3*N*N");
+    finish();
     const int i = local(slice, node);
     TQ_REQUIRE(i >= 0, "node is not local to this rank");
     TQ_CHECK_CUDA(cudaSetDevice(device));
@@ -895,6 +986,7 @@ void Ctx::import_state(int slice, int node, const double *buf, long long len) {
 }
 
 void Ctx::export_labels(int slice, int node, int32_t *buf, long long len) {
+    finish();
     const int i = local(slice, node);
     TQ_REQUIRE(i >= 0, "node is not local to this rank");
     TQ_REQUIRE(xready && (int)label_row.size() == L && label_row[i] >= 0,

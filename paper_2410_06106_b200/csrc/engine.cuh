@@ -122,15 +122,25 @@ struct Ctx {
     void set_params(const tq_params &p);
     void set_quant(const tq_quant &qq);
     void set_sinogram(int slice, int node, const float *d, long long len, bool on_device);
-    void run(int iters, cudaStream_t user);
+    void run(int iters, cudaStream_t user);        // enqueue + finish
+    void run_async(int iters, cudaStream_t user);  // enqueue only; finish() reports later
+    void finish();  // wait for an enqueued run; its stats and divergence check (may fail)
     void get_image(int slice, int node, float *out, long long len, bool on_device);
     void get_image_async(int slice, int node, float *out, long long len, bool on_device, cudaStream_t s);
     void export_state(int slice, int node, double *buf, long long len);
     void import_state(int slice, int node, const double *buf, long long len);
     void export_labels(int slice, int node, int32_t *buf, long long len);
     long long launch_component(int component, int reps, cudaStream_t s);
-    float *sino_stage = nullptr;   // persistent device staging for tq_set_sinogram
-    long long sino_stage_len = 0;
+    // tq_set_sinogram: two device staging buffers filled on the upload stream; the gathers
+    // into D are deferred to the stream of the next run (flush_gathers), so a new sinogram
+    // costs no cross-stream round trip between two runs
+    float *sino_stage[2] = {nullptr, nullptr};
+    long long sino_stage_len[2] = {0, 0};
+    int stage_buf = 0;
+    cudaEvent_t stage_copied[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
+    struct PendGather { int buf; int *pairs; int count; };
+    std::vector<PendGather> pend_gathers;
+    void flush_gathers(cudaStream_t s);
     struct GatherMap { int *pairs; int count; };
     std::map<std::pair<int, int>, GatherMap> gather_maps;  // (slice, node) -> sinogram row pairs
     float *img_stage = nullptr;    // persistent staging of tq_get_image
@@ -138,8 +148,17 @@ struct Ctx {
     cudaEvent_t img_ready[2] = {nullptr, nullptr}, img_done[2] = {nullptr, nullptr};
     int img_buf = 0;
     bool img_used[2] = {false, false};
+    // asynchronous runs: run_done marks the end of the last enqueued run on its stream run_s
+    // (valid while the run is pending); image snapshots go on that stream behind it
+    cudaEvent_t run_done = nullptr;
+    cudaStream_t up_stream = nullptr;  // tq_set_sinogram's host-to-device copies
+    cudaStream_t run_s = nullptr;
+    cudaStream_t img_s[2] = {nullptr, nullptr};  // stream of each staging buffer's snapshot
+    bool pending = false;
+    double *norm_host = nullptr;   // pinned [L][S_NSLOT] scalar table of the last run
+    int pending_iters = 0;
     // the snapshot kernel of get_image / get_image_async into d (fp32) on `stream`
-    void snapshot_image(int slice, int node, float *d);
+    void snapshot_image(int slice, int node, float *d, cudaStream_t s);
 
    private:
     void invalidate();
@@ -152,6 +171,7 @@ struct Ctx {
     void exchange(cudaStream_t s);
     int phase_b(cudaStream_t s);  // decode + dual / next b'
     int prepare_rhs(cudaStream_t s);
+    void enqueue(int iters, cudaStream_t user);
     void *dev_alloc(size_t bytes);
     int local(int slice, int node) const;
 };

@@ -66,6 +66,8 @@ _SIGS = {
     "tq_set_quantizer": [_vp, C.POINTER(Quant)],
     "tq_set_sinogram": [_vp, _i32, _i32, _vp, _i64, _i32],
     "tq_run": [_vp, _i32, _vp],
+    "tq_run_async": [_vp, _i32, _vp],
+    "tq_wait": [_vp],
     "tq_get_image": [_vp, _i32, _i32, _vp, _i64, _i32],
     "tq_get_image_async": [_vp, _i32, _i32, _vp, _i64, _i32, _vp],
     "tq_export_state": [_vp, _i32, _i32, _vp, _i64],
@@ -215,6 +217,14 @@ class Context:
 
     def run(self, iters, stream=None):
         self._c(lib().tq_run(self.h, iters, _stream(stream) if stream is not None else None))
+
+    def run_async(self, iters, stream=None):
+        """Enqueue `iters` iterations without waiting (tq_run_async); `wait()` (or any
+        call that waits) reports their divergence check."""
+        self._c(lib().tq_run_async(self.h, iters, _stream(stream) if stream is not None else None))
+
+    def wait(self):
+        self._c(lib().tq_wait(self.h))
 
     def image(self, slice_=0, node=-1, out=None, host_out=None):
         """Host numpy image; or into a CUDA tensor `out` / a (pinned) host tensor

@@ -342,3 +342,66 @@ def test_image_async_double_buffer():
     a.image_async(dev, st)  # mean image into device memory
     st.synchronize()
     assert np.array_equal(dev.cpu().numpy(), a.image().ravel())
+
+
+def test_run_async_matches_run():
+    """tq_run_async: iterations enqueued back to back on a user stream, with sinogram changes
+    and image read-outs in between and one tq_wait at the end, give bit for bit the state of
+    the blocking sequence (the gather of a new sinogram waits for the run that reads the old
+    one; the next run waits for the gather)."""
+    import torch
+    cfg = c2s()
+    inp = C.make_inputs(cfg)
+    inp2 = C.make_inputs(C.scaled(C.C2(), 64, 90, iters=50, noise=0.03))
+    assert not np.array_equal(inp.sino[0], inp2.sino[0])
+    a = gpu_context(cfg, inp)
+    b = gpu_context(cfg, inp)
+    st = torch.cuda.Stream()
+    cp = torch.cuda.Stream()
+    outs = [torch.empty(cfg.N * cfg.N, dtype=torch.float32).pin_memory() for _ in range(4)]
+    want = []
+    for k in range(4):
+        sino = (inp if k % 2 == 0 else inp2).sino[0]
+        a.set_sinogram(0, sino)
+        a.run(2)
+        want.append(a.image(0, 2).ravel())
+        b.set_sinogram(0, sino)
+        b.run_async(2, st)
+        b.image_async(outs[k], cp, 0, 2)
+    b.wait()
+    cp.synchronize()
+    for k in range(4):
+        assert np.array_equal(outs[k].numpy(), want[k])
+    assert np.array_equal(b.image(), a.image())
+    assert b.stats()["iters"] == a.stats()["iters"] == 8
+
+
+def test_run_async_divergence_reported_by_wait():
+    cfg = C.C1()
+    cfg.inner, cfg.e1 = C.INNER_GD, 10
+    inp = C.make_inputs(cfg)
+    ctx = gpu_context(cfg, inp, eta1=[1.0] * cfg.nodes)
+    ctx.run_async(20)  # enqueued: no check yet
+    with pytest.raises(tomoq.TomoQError) as e:
+        ctx.wait()
+    assert e.value.code == 5
+    ctx.wait()  # reported once
+
+
+def test_set_sinogram_repeated_before_run():
+    """Three tq_set_sinogram calls without a run in between (both staging buffers in use, so
+    the oldest gather is placed early): the run sees the last one, as a fresh context does."""
+    cfg = c2s()
+    inp = C.make_inputs(cfg)
+    inp2 = C.make_inputs(C.scaled(C.C2(), 64, 90, iters=50, noise=0.03))
+    a = gpu_context(cfg, inp)
+    a.run_async(1)
+    a.set_sinogram(0, inp2.sino[0])
+    a.set_sinogram(0, inp.sino[0])
+    a.set_sinogram(0, inp2.sino[0])
+    a.run(2)
+    b = gpu_context(cfg, inp)
+    b.run(1)
+    b.set_sinogram(0, inp2.sino[0])
+    b.run(2)
+    assert np.array_equal(a.image(), b.image())
