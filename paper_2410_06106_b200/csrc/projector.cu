@@ -527,17 +527,21 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
         const int lt = s_hdr[rb][4], ct = s_hdr[rb][5];
         if (active) {  // ---- raw -> (e, d) pairs
             if (U.O == 0) {
+                // lane-consecutive 8-byte reads and 16-byte stores (two pixels' pairs per store):
+                // every access of a warp is one contiguous run, no bank conflicts
                 for (int l = warp; l < FP_TH; l += FP_THREADS / 32) {
-                    const float4 v = *reinterpret_cast<const float4 *>(raw + l * FP_TW + 4 * lane);
-                    float nx = __shfl_down_sync(0xffffffffu, v.x, 1);
-                    if (lane == 31) nx = 0.f;
-                    const int i0 = H + 4 * lane;
-                    float4 *dst = reinterpret_cast<float4 *>(pt + l * FP2_PITCH + i0);
-                    const float2 p0 = pair(v.x, v.y, i0), p1 = pair(v.y, v.z, i0 + 1),
-                                 p2 = pair(v.z, v.w, i0 + 2), p3 = pair(v.w, nx, i0 + 3);
-                    dst[0] = make_float4(p0.x, p0.y, p1.x, p1.y);
-                    dst[1] = make_float4(p2.x, p2.y, p3.x, p3.y);
-                    if (lane == 0) pt[l * FP2_PITCH + H - 1] = pair(0.f, v.x, H - 1);
+                    const float2 *rr = reinterpret_cast<const float2 *>(raw + l * FP_TW);
+                    const float2 va = rr[lane], vb = rr[lane + 32];  // pixels 2 lane (+1), 64 + 2 lane (+1)
+                    float na = __shfl_down_sync(0xffffffffu, va.x, 1);
+                    float nb = __shfl_down_sync(0xffffffffu, vb.x, 1);
+                    const float v64 = __shfl_sync(0xffffffffu, vb.x, 0);
+                    if (lane == 31) { na = v64; nb = 0.f; }
+                    const int ia = H + 2 * lane, ib = ia + 64;
+                    const float2 p0 = pair(va.x, va.y, ia), p1 = pair(va.y, na, ia + 1);
+                    const float2 p2 = pair(vb.x, vb.y, ib), p3 = pair(vb.y, nb, ib + 1);
+                    *reinterpret_cast<float4 *>(pt + l * FP2_PITCH + ia) = make_float4(p0.x, p0.y, p1.x, p1.y);
+                    *reinterpret_cast<float4 *>(pt + l * FP2_PITCH + ib) = make_float4(p2.x, p2.y, p3.x, p3.y);
+                    if (lane == 0) pt[l * FP2_PITCH + H - 1] = pair(0.f, va.x, H - 1);
                 }
             } else {
                 for (int job = warp; job < (FP_TW / 32) * (FP_TH / 4); job += FP_THREADS / 32) {
