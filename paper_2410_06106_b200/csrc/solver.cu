@@ -146,11 +146,16 @@ int Inner::cg(const DevGeom &g, int e1, cudaStream_t st) {
     for (int it = 0; it < e1; it++) {
         k += project(g, P, false, st);
         k += backproject(g, EPI_CGQ, Q, nullptr, P, st);
-        launch_cg_update_r(prec, R, Q, n, L, scal, partial, part_stride, counter, st);
+        // the last step needs neither r nor beta (the next solve restarts from the residual
+        // backprojection): only x += alpha p
+        if (it + 1 < e1) {
+            launch_cg_update_r(prec, R, Q, n, L, scal, partial, part_stride, counter, st);
+            k++;
+        }
         // x += alpha p (deferred from the r update: this pass reads p anyway), then the next
         // search direction p = r + beta p (the last one is never used)
         launch_cg_update_px(prec, X, P, R, n, L, scal, partial, part_stride, counter, it + 1 < e1, st);
-        k += 2;
+        k++;
     }
     return k;
 }
