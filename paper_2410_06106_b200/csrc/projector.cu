@@ -769,18 +769,23 @@ __global__ void __launch_bounds__(RJ * RG) fp_reduce_kernel(const FpRedArgs<T> a
     const int l0 = g * per, l1 = min(nb, l0 + per);
     T acc = 0;
     if (j < a.n_det) {
-        const T *p = a.partial + (long long)row * nb * 2 * a.n_det + j;
+        const int nd = a.n_det;
+        // 32-bit element offsets from the row's first slot (a row holds nt_line * 2 * n_det
+        // slots): one IMAD.WIDE per load instead of 64-bit multiplies
+        const T *p = a.partial + (long long)row * nb * 2 * nd + j;
         int lt = l0;
         for (; lt + 8 <= l1; lt += 8) {  // 16 loads in flight
             T x[16];
+            const T *q = p + 2 * lt * nd;
+            asm("" : "+l"(q));  // keep q as a base register: one IMAD.WIDE per load below
 #pragma unroll
-            for (int u = 0; u < 16; u++) x[u] = p[(long long)(2 * lt + u) * a.n_det];
+            for (int u = 0; u < 16; u++) x[u] = __ldcg(q + u * nd);
             T s8[8];
 #pragma unroll
             for (int u = 0; u < 8; u++) s8[u] = x[2 * u] + x[2 * u + 1];
             acc += ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
         }
-        for (; lt < l1; lt++) acc += p[(long long)(2 * lt) * a.n_det] + p[(long long)(2 * lt + 1) * a.n_det];
+        for (; lt < l1; lt++) acc += p[2 * lt * nd] + p[(2 * lt + 1) * nd];
     }
     part[g][jj] = acc;
     __syncthreads();
