@@ -84,21 +84,29 @@ __device__ __forceinline__ void load_tile(const uint32_t *keys, long long off, u
 // Warp multisplit by ballots: peers = lanes of the warp whose digit equals mine
 // (8 ballots, no match/atomics).  Keys of a tile are warp-striped: warp w, round r,
 // lane l holds key w*256 + r*32 + l, so (w, r, l) is the tile's index order.
-// Per bit: one predicate from the digit, one VOTE, and the lane keeps either the ballot
-// or its complement (two predicated LOP3s) -- four issue slots per bit.
+// Per bit: one predicate from the digit (R2P), one VOTE, and the lane keeps either the
+// ballot or its complement (a predicated LOP3); the eight words meet in four 3-input ANDs.
+__device__ __forceinline__ unsigned digit_ballot(uint32_t d, uint32_t bit) {
+    unsigned bal;
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+        "and.b32 t, %1, %2;\n\t"
+        "setp.ne.u32 p, t, 0;\n\t"
+        "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+        "@!p not.b32 %0, %0;\n\t}"
+        : "=r"(bal) : "r"(d), "r"(bit));
+    return bal;
+}
+__device__ __forceinline__ unsigned and3(unsigned a, unsigned b, unsigned c) {
+    unsigned r;
+    asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
 __device__ __forceinline__ unsigned digit_peers(uint32_t d) {
-    unsigned peers = 0xffffffffu;
-#pragma unroll
-    for (int b = 0; b < 8; b++) {
-        asm("{\n\t.reg .pred p;\n\t.reg .b32 t, bal;\n\t"
-            "and.b32 t, %1, %2;\n\t"
-            "setp.ne.u32 p, t, 0;\n\t"
-            "vote.sync.ballot.b32 bal, p, 0xffffffff;\n\t"
-            "@!p not.b32 bal, bal;\n\t"
-            "and.b32 %0, %0, bal;\n\t}"
-            : "+r"(peers) : "r"(d), "r"(1u << b));
-    }
-    return peers;
+    // the eight (possibly complemented) ballots combined by three-input ANDs (4 LOP3)
+    const unsigned b0 = digit_ballot(d, 1u), b1 = digit_ballot(d, 2u), b2 = digit_ballot(d, 4u),
+                   b3 = digit_ballot(d, 8u), b4 = digit_ballot(d, 16u), b5 = digit_ballot(d, 32u),
+                   b6 = digit_ballot(d, 64u), b7 = digit_ballot(d, 128u);
+    return and3(and3(and3(b0, b1, b2), b3, b4), and3(b5, b6, b7), 0xffffffffu);
 }
 
 __device__ __forceinline__ void load_striped(const uint32_t *keys, long long off, uint32_t (&k)[KI]) {
@@ -211,9 +219,10 @@ __global__ void __launch_bounds__(KT, 3) km_scatter(const uint32_t *kin, uint32_
         const uint32_t d = (k[r] >> shift) & 255u;
         const unsigned peers = digit_peers(d);
         const uint32_t before = c[d];
-        rank[r] = before + (uint32_t)__popc(peers & lt);
+        const uint32_t lower = (uint32_t)__popc(peers & lt);  // 0 for the lowest peer
+        rank[r] = before + lower;
         __syncwarp();
-        if (lane == __ffs(peers) - 1) c[d] = before + (uint32_t)__popc(peers);
+        if (lower == 0u) c[d] = before + (uint32_t)__popc(peers);
         __syncwarp();
     }
     __syncthreads();

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtomoq.so")
+LIB_PATH = os.environ.get("TQ_LIB_PATH") or os.path.join(HERE, "libtomoq.so")  # override: A/B timing tools only
 HEADER = os.path.join(os.path.dirname(HERE), "include", "tomoq.h")
 
 SPLIT_RR, SPLIT_CONTIG = 0, 1
