@@ -48,7 +48,17 @@ __global__ void __launch_bounds__(CT) graph_dual(const T *const *xh, const int *
             const Q4<T> xv = ld4(own + p);
             Q4<T> av = ld4(al + p), bv;
             double s[4] = {0.0, 0.0, 0.0, 0.0};
-            for (int k = 0; k < deg; k++) {
+            int k = 0;
+            for (; k + 4 <= deg; k += 4) {  // four neighbour quads in flight (fixed summation order)
+                Q4<T> y[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) y[j] = ld4(nb[k + j] + p);
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+#pragma unroll
+                    for (int u = 0; u < 4; u++) s[u] += (double)y[j].v[u];
+            }
+            for (; k < deg; k++) {
                 const Q4<T> y = ld4(nb[k] + p);
 #pragma unroll
                 for (int u = 0; u < 4; u++) s[u] += (double)y.v[u];

@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(KT) km_final(const float *const *vin, KmPtr w,
     const int lane = threadIdx.x & 31;
     const long long warp0 = ((long long)blockIdx.x * KT + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * KT) >> 5;
-    constexpr int U = 4;
+    constexpr int U = 8;
     for (long long g0 = warp0 * U; g0 < G; g0 += nwarps * U) {  // warp-uniform
         float v[U];
 #pragma unroll

@@ -1,6 +1,10 @@
 #!/bin/bash
-# A/B of two library builds on the bench workload (device-timed ms/step), alternating.
-for v in old new old new old new; do
-  TQ_LIB_PATH=ab/libtomoq_$v.so python bench.py --steps 50 --warmup 5 --no-cpu-baseline --no-c5-geometry 2>/dev/null | tail -1 | \
-    python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', round(d['ms_per_step'],4), round(d['e2e']['ms_per_step'],4))"
+# A/B of library builds ab/libtomoq_<name>.so on the bench workload (device-timed ms/step),
+# round-robin, 3 rounds.  Usage: bash tools/ab_bench.sh old new [more names]
+names=${@:-old new}
+for round in 1 2 3; do
+  for v in $names; do
+    TQ_LIB_PATH=ab/libtomoq_$v.so python bench.py --steps 50 --warmup 5 --no-cpu-baseline --no-c5-geometry 2>/dev/null | tail -1 | \
+      python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', round(d['ms_per_step'],4), round(d['e2e']['ms_per_step'],4))"
+  done
 done
