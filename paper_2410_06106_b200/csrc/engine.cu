@@ -193,8 +193,11 @@ void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int ran
     TQ_CHECK_CUDA(cudaStreamCreateWithFlags(&up_stream, cudaStreamNonBlocking));
     TQ_CHECK_CUDA(cudaEventCreate(&ev0));
     TQ_CHECK_CUDA(cudaEventCreate(&ev1));
-    for (cudaEvent_t *e : {&run_done, &stage_copied[0], &stage_copied[1], &stage_free[0], &stage_free[1]})
-        TQ_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    TQ_CHECK_CUDA(cudaEventCreateWithFlags(&run_done, cudaEventDisableTiming));
+    for (int b = 0; b < NSTAGE; b++) {
+        TQ_CHECK_CUDA(cudaEventCreateWithFlags(&stage_copied[b], cudaEventDisableTiming));
+        TQ_CHECK_CUDA(cudaEventCreateWithFlags(&stage_free[b], cudaEventDisableTiming));
+    }
     TQ_REQUIRE(g.projector == TQ_PROJ_JOSEPH || g.projector == TQ_PROJ_SIDDON, "bad projector");
     geo.init(N, n_ang, n_det, g.projector);
     in.init(prec, geo, angles);
@@ -261,7 +264,7 @@ void Ctx::destroy() {
     if (CSUM) cudaFree(CSUM);
     ALPHA = XG = nullptr;
     CSUM = nullptr;
-    for (int b = 0; b < 2; b++) {
+    for (int b = 0; b < NSTAGE; b++) {
         if (sino_stage[b]) cudaFree(sino_stage[b]);
         sino_stage[b] = nullptr;
         sino_stage_len[b] = 0;
@@ -282,9 +285,12 @@ void Ctx::destroy() {
     comm = nullptr;
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    for (cudaEvent_t *e : {&run_done, &stage_copied[0], &stage_copied[1], &stage_free[0], &stage_free[1]}) {
-        if (*e) cudaEventDestroy(*e);
-        *e = nullptr;
+    if (run_done) cudaEventDestroy(run_done);
+    run_done = nullptr;
+    for (int b = 0; b < NSTAGE; b++) {
+        if (stage_copied[b]) cudaEventDestroy(stage_copied[b]);
+        if (stage_free[b]) cudaEventDestroy(stage_free[b]);
+        stage_copied[b] = stage_free[b] = nullptr;
     }
     if (norm_host) cudaFreeHost(norm_host);
     norm_host = nullptr;
@@ -348,7 +354,7 @@ void Ctx::set_sinogram(int slice, int node, const float *d, long long len, bool 
     // of every local node, deferred to the stream of the next run (flush_gathers)
     TQ_CHECK_CUDA(cudaSetDevice(device));
     const int b = stage_buf;
-    for (const PendGather &pg : pend_gathers)  // both buffers queued: place the older gathers now
+    for (const PendGather &pg : pend_gathers)  // this buffer still queued: place the older gathers now
         if (pg.buf == b) {
             flush_gathers(pending ? run_s : stream);
             break;
@@ -369,7 +375,7 @@ void Ctx::set_sinogram(int slice, int node, const float *d, long long len, bool 
     TQ_CHECK_CUDA(cudaMemcpyAsync(sino_stage[b], d, sizeof(float) * len,
                                   on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, up_stream));
     TQ_CHECK_CUDA(cudaEventRecord(stage_copied[b], up_stream));
-    stage_buf ^= 1;
+    stage_buf = (stage_buf + 1) % NSTAGE;
     // (source row, destination row) pairs of the local nodes, built once per (slice, node)
     auto it = gather_maps.find({slice, node});
     if (it == gather_maps.end()) {
@@ -860,7 +866,8 @@ void Ctx::snapshot_image(int slice, int node, float *d, cudaStream_t stream) {
     if (node >= 0) {
         const int i = local(slice, node);
         if (i < 0) fail(TQ_EINVAL, "node is not local to this rank");
-        launch_convert(prec, in.xrow(in.X, i), 0, d, n, stream);
+        if (prec == 0) TQ_CHECK_CUDA(cudaMemcpyAsync(d, in.xrow(in.X, i), sizeof(float) * n, cudaMemcpyDeviceToDevice, stream));
+        else launch_convert(prec, in.xrow(in.X, i), 0, d, n, stream);
     } else if (segmented()) {
         TQ_REQUIRE(slice >= 0 && slice < S, "slice out of range");
         launch_convert(prec, (uint8_t *)XG + (prec ? 8 : 4) * (long long)slice * n, 0, d, n, stream);

@@ -131,13 +131,14 @@ struct Ctx {
     void import_state(int slice, int node, const double *buf, long long len);
     void export_labels(int slice, int node, int32_t *buf, long long len);
     long long launch_component(int component, int reps, cudaStream_t s);
-    // tq_set_sinogram: two device staging buffers filled on the upload stream; the gathers
+    // tq_set_sinogram: NSTAGE device staging buffers filled on the upload stream; the gathers
     // into D are deferred to the stream of the next run (flush_gathers), so a new sinogram
     // costs no cross-stream round trip between two runs
-    float *sino_stage[2] = {nullptr, nullptr};
-    long long sino_stage_len[2] = {0, 0};
+    static constexpr int NSTAGE = 4;  // uploads in flight: the host may run this many calls ahead
+    float *sino_stage[NSTAGE] = {};
+    long long sino_stage_len[NSTAGE] = {};
     int stage_buf = 0;
-    cudaEvent_t stage_copied[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
+    cudaEvent_t stage_copied[NSTAGE] = {}, stage_free[NSTAGE] = {};
     struct PendGather { int buf; int *pairs; int count; };
     std::vector<PendGather> pend_gathers;
     void flush_gathers(cudaStream_t s);
