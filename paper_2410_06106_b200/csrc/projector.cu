@@ -17,6 +17,10 @@ constexpr int BP_TS = 64;       // backprojector pixel tile side
 constexpr int BP_THREADS = 256;
 constexpr int BP_WB = 96;       // staged bins per angle: >= 63(|cos|+|sin|) + 4
 constexpr int BP_MAXA = 32;     // angles per staged batch
+// fp32 epilogues with two prefetched operands (x and b') stage 16 angles per batch, so the
+// CTA stays within a quarter of the SM's shared memory (4 CTAs/SM, as the CG variant)
+template <typename T, int EPI>
+constexpr int bp_maxa() { return (sizeof(T) == 4 && (EPI == 2 || EPI == 3)) ? 16 : BP_MAXA; }
 
 template <typename T>
 __device__ __forceinline__ T floor_split(T x, int &i);
@@ -805,6 +809,7 @@ __global__ void __launch_bounds__(RJ * RG) fp_reduce_kernel(const FpRedArgs<T> a
 template <typename T, int EPI>
 __global__ void __launch_bounds__(BP_THREADS, sizeof(T) == 4 ? 4 : 1)
 bp_tile_kernel(const BpArgs<T> a) {
+    constexpr int BP_MAXA = bp_maxa<T, EPI>();  // angles per staged batch of this variant
     extern __shared__ __align__(16) unsigned char bp_smem[];
     T *win = reinterpret_cast<T *>(bp_smem);  // [BP_MAXA][BP_WB], bins pre-scaled by 1/m (fp64)
     float2 *win2 = reinterpret_cast<float2 *>(bp_smem);  // fp32: [BP_MAXA][BP_WB] pairs (s'_j, s'_{j+1})
@@ -1033,7 +1038,7 @@ int g_fpp_grid = 0;  // persistent grid: SMs x resident CTAs (projector_setup)
 template <typename T, int EPI>
 size_t bp_smem() {
     constexpr int NEP = (EPI == EPI_CGQ) ? 1 : ((EPI == EPI_RESID || EPI == EPI_GD) ? 2 : 0);
-    return sizeof(T) == 4 ? sizeof(float2) * BP_MAXA * BP_WB + NEP * sizeof(float) * BP_TS * BP_TS
+    return sizeof(T) == 4 ? sizeof(float2) * bp_maxa<T, EPI>() * BP_WB + NEP * sizeof(float) * BP_TS * BP_TS
                           : sizeof(T) * BP_MAXA * BP_WB;
 }
 
