@@ -825,8 +825,6 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
     TQ_CHECK_CUDA(cudaEventRecord(ev1, s));
     // CG with E1 >= 1 leaves ||x||^2 in the scalar table (its last step); otherwise compute it
     if (!(iters > 0 && prm.inner == TQ_INNER_CG && prm.e1 >= 1)) in.norm2(s);
-    if (!norm_host) TQ_CHECK_CUDA(cudaMallocHost(&norm_host, sizeof(double) * S_NSLOT * std::max(1, L)));
-    if (L) TQ_CHECK_CUDA(cudaMemcpyAsync(norm_host, in.scal, sizeof(double) * S_NSLOT * L, cudaMemcpyDeviceToHost, s));
     TQ_CHECK_CUDA(cudaEventRecord(run_done, s));
     st.iters += iters;
     st.kernel_launches = (long long)iters * per_iter;
@@ -840,6 +838,9 @@ void Ctx::finish() {
     if (!pending) return;
     pending = false;
     TQ_CHECK_CUDA(cudaEventSynchronize(run_done));
+    // the scalar table of the last enqueued run (nothing else writes it before this call)
+    if (!norm_host) TQ_CHECK_CUDA(cudaMallocHost(&norm_host, sizeof(double) * S_NSLOT * std::max(1, L)));
+    if (L) TQ_CHECK_CUDA(cudaMemcpy(norm_host, in.scal, sizeof(double) * S_NSLOT * L, cudaMemcpyDeviceToHost));
     const int iters = pending_iters;
     float ms = 0.f;
     TQ_CHECK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
