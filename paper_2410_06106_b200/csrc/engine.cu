@@ -226,6 +226,8 @@ void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int ran
 void Ctx::invalidate() {
     for (auto &g : segs) cudaGraphExecDestroy(g.exec);
     segs.clear();
+    if (seg2.exec) cudaGraphExecDestroy(seg2.exec);
+    seg2 = Seg{nullptr, 0, COMM_NONE};
 }
 
 void Ctx::free_exchange() {
@@ -813,10 +815,32 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
         cur.push_back(2);
         capture(cur, COMM_NONE);
     }
+    // one rank without communication steps: a second graph holding MULTI iterations (built
+    // with the first, i.e. during warm-up) cuts the graph-to-graph boundaries of long runs
+    if (segs.size() == 1 && segs[0].comm == COMM_NONE && !seg2.exec) {
+        cudaGraph_t g;
+        TQ_CHECK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        int c = 0;
+        try {
+            for (int rep = 0; rep < MULTI; rep++) c += stage(0, s) + stage(1, s) + stage(2, s);
+        } catch (...) {
+            if (cudaStreamEndCapture(s, &g) == cudaSuccess && g) cudaGraphDestroy(g);
+            (void)cudaGetLastError();
+            throw;
+        }
+        TQ_CHECK_CUDA(cudaStreamEndCapture(s, &g));
+        const cudaError_t e = cudaGraphInstantiate(&seg2.exec, g, 0);
+        cudaGraphDestroy(g);
+        TQ_CHECK_CUDA(e);
+        seg2.launches = c;
+    }
     int per_iter = 0;
     for (auto &g : segs) per_iter += g.launches;
     TQ_CHECK_CUDA(cudaEventRecord(ev0, s));
-    for (int it = 0; it < iters; it++)
+    int it0 = 0;
+    if (seg2.exec)
+        for (; it0 + MULTI <= iters; it0 += MULTI) TQ_CHECK_CUDA(cudaGraphLaunch(seg2.exec, s));
+    for (int it = it0; it < iters; it++)
         for (auto &g : segs) {
             TQ_CHECK_CUDA(cudaGraphLaunch(g.exec, s));
             if (g.comm == COMM_REDUCE) reduce_sums(s);

@@ -112,6 +112,8 @@ struct Ctx {
     enum Comm { COMM_NONE = 0, COMM_REDUCE = 1, COMM_EXCHANGE = 2 };
     struct Seg { cudaGraphExec_t exec; int launches, comm; };
     std::vector<Seg> segs;
+    static constexpr int MULTI = 4;
+    Seg seg2{nullptr, 0, COMM_NONE};  // world == 1: MULTI iterations in one graph
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     tq_stats st{};
     std::string err;
