@@ -115,6 +115,28 @@ def test_local_solve_parity(prec, inner, e1):
     assert rel(got.cpu().numpy(), ref) <= (1e-5 if prec == 0 else 1e-11)
 
 
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("inner,e1", [(tomoq.INNER_CG, 3), (tomoq.INNER_GD, 4)])
+def test_local_solve_many_angles(prec, inner, e1):
+    """45 angles on one node: the backprojector's angle batches (32 per batch for the CG
+    epilogue, 16 for the residual / GD epilogues in fp32) span several staging rounds."""
+    N, n_ang, n_det = 96, 90, 137
+    sel = list(range(1, 90, 2))
+    rng = np.random.default_rng(7)
+    truth = phantom(N, 5)
+    d = as_input(oracle.project(truth, n_ang, n_det, sel) + 0.1 * rng.standard_normal((len(sel), n_det)), prec)
+    bp = as_input(rng.standard_normal(N * N) * 0.5, prec)
+    x0 = as_input(truth + 0.1 * rng.standard_normal((N, N)), prec)
+    c, eta = 1.5, 1.0 / (2 * len(sel) * N + 1.5)
+    if inner == tomoq.INNER_CG:
+        ref = oracle.cg(d, bp, c, e1, x0, n_ang, sel)
+    else:
+        ref = oracle.gd(d, bp, c, eta, e1, x0, n_ang, sel)
+    T = lambda a: torch.tensor(a, dtype=DT[prec], device=DEV)
+    got = tomoq.local_solve(T(d), T(bp.reshape(N, N)), c, e1, T(x0), n_ang, sel, inner=inner, eta=eta)
+    assert rel(got.cpu().numpy(), ref) <= (1e-5 if prec == 0 else 1e-11)
+
+
 # ---------------------------------------------------------------- codecs
 def kmeans_input(n, seed):
     rng = np.random.default_rng(seed)
