@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(FP_THREADS) fp_tile_kernel(const FpArgs<T> a) 
                     acc1 = fma(f, v1 - v0, acc1);
                 }
             }
-            if (w < W) a.partial[((long long)s_row[k] * a.nt_line + lt) * 2 * a.n_det + (ct & 1) * a.n_det + s_jlo[k] + w] = acc0 + acc1;
+            if (w < W) a.partial[((long long)s_row[k] * a.nt_line + lt) * 2 * fp_ps(a.n_det) + (ct & 1) * fp_ps(a.n_det) + s_jlo[k] + w] = acc0 + acc1;
         }
     }
 }
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(FP_THREADS, 4) fp_tile_f32(const FpArgs<float>
                 acc1 += fmaf(kf1, q1.y, q1.x);
             }
             if (g0 + lane < R)
-                a.partial[((long long)s_row[k] * a.nt_line + lt) * 2 * a.n_det + (ct & 1) * a.n_det + s_jlo[k] + w] =
+                a.partial[((long long)s_row[k] * a.nt_line + lt) * 2 * fp_ps(a.n_det) + (ct & 1) * fp_ps(a.n_det) + s_jlo[k] + w] =
                     acc0 + acc1;
         }
     }
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
                     acc1 = acc2.y;
                 }
                 if (ok)
-                    a.partial[((long long)R[k].row * a.nt_line + lt) * 2 * a.n_det + (ct & 1) * a.n_det + R[k].jlo + w] =
+                    a.partial[((long long)R[k].row * a.nt_line + lt) * 2 * fp_ps(a.n_det) + (ct & 1) * fp_ps(a.n_det) + R[k].jlo + w] =
                         acc0 + acc1;
             }
             if (b0 + FPP_MAXA < U.a_end) __syncthreads();  // R / plan reuse by the next batch
@@ -773,8 +773,8 @@ __global__ void __launch_bounds__(RJ * RG) fp_reduce_kernel(const FpRedArgs<T> a
     const int l0 = g * per, l1 = min(nb, l0 + per);
     T acc = 0;
     if (j < a.n_det) {
-        const int nd = a.n_det;
-        // 32-bit element offsets from the row's first slot (a row holds nt_line * 2 * n_det
+        const int nd = fp_ps(a.n_det);  // slot row stride
+        // 32-bit element offsets from the row's first slot (a row holds nt_line * 2 * stride
         // slots): one IMAD.WIDE per load instead of 64-bit multiplies
         const T *p = a.partial + (long long)row * nb * 2 * nd + j;
         int lt = l0;
@@ -803,6 +803,68 @@ __global__ void __launch_bounds__(RJ * RG) fp_reduce_kernel(const FpRedArgs<T> a
     T v = (T)((double)tot * inv_m);
     if (RESID) v = a.d[(long long)row * a.n_det + j] - v;
     a.out[(long long)row * a.out_stride + a.out_off + j] = v;
+}
+
+// fp32: four bins per thread (16-byte slot loads; the slot rows are padded to a multiple of
+// four bins and the padding is never written, so it stays zero), RQ quads x RG band groups
+constexpr int RQ = 32;
+template <bool RESID>
+__global__ void __launch_bounds__(RQ * RG) fp_reduce_f32(const FpRedArgs<float> a) {
+    __shared__ float4 part[RG][RQ];
+    const int row = blockIdx.y;
+    const int q = threadIdx.x % RQ, g = threadIdx.x / RQ;
+    const int j0 = 4 * (blockIdx.x * RQ + q);
+    const int nb = a.nt_line, nd = fp_ps(a.n_det);
+    const int per = (nb + RG - 1) / RG;
+    const int l0 = g * per, l1 = min(nb, l0 + per);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (j0 < a.n_det) {
+        const float4 *p = reinterpret_cast<const float4 *>(a.partial + (long long)row * nb * 2 * nd + j0);
+        const int nq = nd / 4;  // slot row stride in quads
+        int lt = l0;
+        for (; lt + 4 <= l1; lt += 4) {  // 8 quads in flight
+            float4 x[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) x[u] = __ldcg(p + (2 * lt + u) * nq);
+#pragma unroll
+            for (int u = 0; u < 8; u += 2) {
+                acc.x += x[u].x + x[u + 1].x;
+                acc.y += x[u].y + x[u + 1].y;
+                acc.z += x[u].z + x[u + 1].z;
+                acc.w += x[u].w + x[u + 1].w;
+            }
+        }
+        for (; lt < l1; lt++) {
+            const float4 x0 = __ldcg(p + 2 * lt * nq), x1 = __ldcg(p + (2 * lt + 1) * nq);
+            acc.x += x0.x + x1.x;
+            acc.y += x0.y + x1.y;
+            acc.z += x0.z + x1.z;
+            acc.w += x0.w + x1.w;
+        }
+    }
+    part[g][q] = acc;
+    __syncthreads();
+    if (g != 0 || j0 >= a.n_det) return;
+    float4 tot = part[0][q];
+#pragma unroll
+    for (int r = 1; r < RG; r++) {
+        tot.x += part[r][q].x;
+        tot.y += part[r][q].y;
+        tot.z += part[r][q].z;
+        tot.w += part[r][q].w;
+    }
+    const int ang = a.rows[row].angle;
+    const double2 t2 = a.trig[ang];
+    const double inv_m = a.xmaj[ang] ? 1.0 / fabs(t2.y) : 1.0 / fabs(t2.x);
+    const float tv[4] = {tot.x, tot.y, tot.z, tot.w};
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        const int j = j0 + e;
+        if (j >= a.n_det) break;
+        float v = (float)((double)tv[e] * inv_m);
+        if (RESID) v = a.d[(long long)row * a.n_det + j] - v;
+        a.out[(long long)row * a.out_stride + a.out_off + j] = v;
+    }
 }
 
 // ------------------------------------------------------------------ backprojector
@@ -1181,8 +1243,9 @@ void launch_fp_reduce(int prec, bool resid, const void *args, int n_rows, int n_
     const dim3 grid(ceil_div(n_det, RJ), n_rows);
     if (prec == 0) {
         const auto &A = *static_cast<const FpRedArgs<float> *>(args);
-        if (resid) fp_reduce_kernel<float, true><<<grid, RJ * RG, 0, st>>>(A);
-        else fp_reduce_kernel<float, false><<<grid, RJ * RG, 0, st>>>(A);
+        const dim3 gq(ceil_div(n_det, 4 * RQ), n_rows);
+        if (resid) fp_reduce_f32<true><<<gq, RQ * RG, 0, st>>>(A);
+        else fp_reduce_f32<false><<<gq, RQ * RG, 0, st>>>(A);
     } else {
         const auto &A = *static_cast<const FpRedArgs<double> *>(args);
         if (resid) fp_reduce_kernel<double, true><<<grid, RJ * RG, 0, st>>>(A);

@@ -106,6 +106,9 @@ struct FpArgs {
     int siddon;            // 1: Siddon weights (R-26) -- generic tile kernel
 };
 
+// row stride (bins) of the forward partial slots: n_det rounded up to a multiple of 4
+__host__ __device__ inline int fp_ps(int n_det) { return (n_det + 3) & ~3; }
+
 template <typename T>
 struct FpRedArgs {
     const T *partial;      // as FpArgs::partial; slots no tile writes stay zero

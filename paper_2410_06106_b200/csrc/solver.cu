@@ -68,7 +68,7 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
     if (!ol.empty()) TQ_CHECK_CUDA(cudaMemcpy(olist, ol.data(), sizeof(int) * ol.size(), cudaMemcpyHostToDevice));
     TQ_CHECK_CUDA(cudaMemcpy(oofs, of.data(), sizeof(int) * of.size(), cudaMemcpyHostToDevice));
     const size_t nwin = (size_t)n_rows * nt_line * nt_cross;
-    A(&fpart, es * (size_t)n_rows * nt_line * 2 * g.n_det);
+    A(&fpart, es * (size_t)n_rows * nt_line * 2 * fp_ps(g.n_det));
     A((void **)&fwin, sizeof(FpWin) * nwin);
     A((void **)&frg, sizeof(FpRowGeo) * n_rows);
     n_olist = (int)ol.size();
