@@ -605,25 +605,26 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
                 }
                 __syncthreads();
                 for (int k = threadIdx.x; k < nb; k += FP_THREADS)
-                    for (int it = ut.hpre[k]; it < ut.hpre[k + 1]; it++) ut.hk[it] = (unsigned char)k;
+                    for (int it = ut.hpre[k]; it < ut.hpre[k + 1]; it++) ut.hk[it] = fp_hk_pack(k, ut.nh[k], it - ut.hpre[k]);
                 __syncthreads();
             }
-            const int *hpre = ut.hpre;
-            const unsigned char *nhv = ut.nh;
-            const unsigned char *hk = ut.hk;
-            const int Hn = hpre[nb];
+            const unsigned short *hk = ut.hk;
+            const int Hn = ut.hpre[nb];
             const int hl = lane & 15;
             // one warp item = two half-warp items (each nh_k <= 16 rays of one angle)
             for (int h0 = 2 * warp; h0 < Hn; h0 += 2 * (FP_THREADS / 32)) {
                 const int hraw = h0 + (lane >> 4);
                 const int hi = min(hraw, Hn - 1);
-                const int k = hk[hi];
-                const int nh = nhv[k], W = R[k].W;
-                const int w0 = (hi - hpre[k]) * nh + hl;
+                const unsigned pk = hk[hi];
+                const int k = pk & 31, nh = (pk >> 5) & 31, rk = (int)(pk >> 10);
+                const double2 ka = *reinterpret_cast<const double2 *>(&R[k].kap);  // (kap, at)
+                const int4 bj = *reinterpret_cast<const int4 *>(&R[k].B);          // (B, jlo, W, row)
+                const int W = bj.z;
+                const int w0 = rk * nh + hl;
                 const bool ok = hraw < Hn && hl < nh && w0 < W;
-                const int w = min(min(w0, (hi - hpre[k]) * nh + nh - 1), W - 1);  // idle lanes repeat a ray
-                const float kap = (float)(R[k].kap + (double)w * R[k].at);
-                const float B = R[k].B;
+                const int w = min(min(w0, rk * nh + nh - 1), W - 1);  // idle lanes repeat a ray
+                const float kap = (float)(ka.x + (double)w * ka.y);
+                const float B = __int_as_float(bj.x);
                 float acc0 = 0.f, acc1 = 0.f;
                 if (!SID) {
                     // lines l, l + 1 as one packed pair: FFMA2 (positions), FADD2.RM (floors) and
@@ -661,7 +662,7 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
                     acc1 = acc2.y;
                 }
                 if (ok)
-                    a.partial[((long long)R[k].row * a.nt_line + lt) * 2 * fp_ps(a.n_det) + (ct & 1) * fp_ps(a.n_det) + R[k].jlo + w] =
+                    a.partial[((long long)bj.w * a.nt_line + lt) * 2 * fp_ps(a.n_det) + (ct & 1) * fp_ps(a.n_det) + bj.y + w] =
                         acc0 + acc1;
             }
             if (b0 + FPP_MAXA < U.a_end) __syncthreads();  // R / plan reuse by the next batch
@@ -752,7 +753,7 @@ __global__ void fp_unit_kernel(const int *oofs, const FpRec *recs, int n_olist, 
             const int mid = (lo + hi + 1) >> 1;
             if (pre[mid] <= it) lo = mid; else hi = mid - 1;
         }
-        t->hk[it] = (unsigned char)lo;
+        t->hk[it] = fp_hk_pack(lo, nhs[lo], it - pre[lo]);
     }
 }
 

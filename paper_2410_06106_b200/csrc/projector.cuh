@@ -76,15 +76,20 @@ struct FpRec {
 // angle k, nh_k = min(16, floor(15 / at_k) + 1), so the 16 lanes of a half-warp read one
 // line's (e, d) pairs within a window of 16 consecutive 8-byte slots: every LDS.64 of the
 // ray walk is conflict-free (2 wavefronts per warp).  hpre = exclusive prefix of the
-// half-item counts ceil(W_k / nh_k); hk = angle of each half-item.  Bulk-copied with the
-// unit's records.
+// half-item counts ceil(W_k / nh_k); hk = per half-item k | nh_k << 5 | (its index within
+// angle k) << 10, so an item learns its angle, width and first ray from one load.
+// Bulk-copied with the unit's records.
 constexpr int FPP_HMAX = 512;  // >= FPP_MAXA * ceil(FP_WMAX / 11) half-items per batch
 struct FpUnitTab {
     int hpre[FPP_MAXA + 1];
     unsigned char nh[FPP_MAXA];
-    unsigned char hk[FPP_HMAX];
+    unsigned short hk[FPP_HMAX];
     int pad[3];
 };
+__host__ __device__ inline unsigned short fp_hk_pack(int k, int nh, int rank) {
+    return (unsigned short)(k | (nh << 5) | (rank << 10));
+}
+static_assert(FPP_MAXA <= 32 && (FP_WMAX + 10) / 11 <= 64, "half-item packing (5 | 5 | 6 bits)");
 static_assert(sizeof(FpUnitTab) % 16 == 0, "bulk-copy granularity");
 static_assert(FPP_MAXA * ((FP_WMAX + 10) / 11) <= FPP_HMAX, "half-item table too small");
 
