@@ -879,8 +879,10 @@ bp_tile_kernel(const BpArgs<T> a) {
     // fp32: the epilogue operands of the tile, prefetched with cp.async at entry so their
     // latency overlaps the angle loop: ep[0] = vin (p or x), ep[1] = b' (RESID, GD)
     float *ep = reinterpret_cast<float *>(bp_smem + (sizeof(T) == 4 ? sizeof(float2) : sizeof(T)) * BP_MAXA * BP_WB);
-    __shared__ double s_tau[BP_MAXA], s_csd[BP_MAXA], s_snd[BP_MAXA];
-    __shared__ T s_cs[BP_MAXA], s_sn[BP_MAXA], s_im[BP_MAXA], s_a1[BP_MAXA], s_a0[BP_MAXA];
+    // per-angle constants of the angle loop, packed so a thread reads them with three 16-byte loads
+    struct __align__(16) AngC { double tau, csd, snd, pad; T cs, sn, a1, a0; };
+    __shared__ AngC s_ang[BP_MAXA];
+    __shared__ T s_im[BP_MAXA];
     __shared__ int s_jlo[BP_MAXA];
     __shared__ const T *s_src[BP_MAXA];
     __shared__ double red[BP_THREADS / 32 + 1];
@@ -940,23 +942,26 @@ bp_tile_kernel(const BpArgs<T> a) {
             const int jlo = (int)floor(tmin - t0) - 1;  // one bin of margin below
             s_jlo[k] = jlo;
             s_src[k] = a.s + (long long)(row0 + k0 + k) * a.s_stride + a.s_off + jlo;
-            s_tau[k] = tp0 - t0 - (double)jlo;  // tile-relative bin coordinate of pixel (r0, c0)
-            s_csd[k] = cs;
-            s_snd[k] = sn;
-            s_cs[k] = (T)cs;
-            s_sn[k] = (T)sn;
+            AngC ac;
+            ac.tau = tp0 - t0 - (double)jlo;  // tile-relative bin coordinate of pixel (r0, c0)
+            ac.csd = cs;
+            ac.snd = sn;
+            ac.pad = 0.0;
+            ac.cs = (T)cs;
+            ac.sn = (T)sn;
             s_im[k] = (T)(1.0 / m);
             // tap weight sat(a0 - s a1) at bin distance s (times the 1/m pre-scale): Joseph
             // a1 = 1/m, a0 = 1; Siddon (R-26) a1 = 1/(m w), a0 = (1 + 1/w)/2, w = drift per line
             if (a.siddon) {
                 const double w = a.xmaj[ang] ? fabs(cs / sn) : fabs(sn / cs);
                 const double iw = w > 1e-9 ? 1.0 / w : 4194304.0;
-                s_a1[k] = (T)(iw / m);
-                s_a0[k] = (T)(0.5 + 0.5 * iw);
+                ac.a1 = (T)(iw / m);
+                ac.a0 = (T)(0.5 + 0.5 * iw);
             } else {
-                s_a1[k] = (T)(1.0 / m);
-                s_a0[k] = (T)1;
+                ac.a1 = (T)(1.0 / m);
+                ac.a0 = (T)1;
             }
+            s_ang[k] = ac;
         }
         __syncthreads();
         // bins of the window: zero guards / pads stand in for j < 0 and j >= n_det (SPAD)
@@ -969,8 +974,9 @@ bp_tile_kernel(const BpArgs<T> a) {
         }
         __syncthreads();
         for (int k = 0; k < kc; k++) {
-            const T cs = s_cs[k], sn = s_sn[k], a1 = s_a1[k], a0 = s_a0[k], a0m = a0 - a1;
-            const T tau_t = (T)(s_tau[k] + (double)lx * s_csd[k] - (double)prow * s_snd[k]);
+            const AngC ac = s_ang[k];
+            const T cs = ac.cs, sn = ac.sn, a1 = ac.a1, a0 = ac.a0, a0m = a0 - a1;
+            const T tau_t = (T)(ac.tau + (double)lx * ac.csd - (double)prow * ac.snd);
             if constexpr (sizeof(T) == 4) {
                 const uint32_t wb = magic_base(win2 + k * BP_WB, a.magic);  // magic = 0x4B000000 << 3
                 // pixels kx, kx + 1 as one packed pair for the position, floor and fraction
