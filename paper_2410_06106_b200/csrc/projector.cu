@@ -965,12 +965,28 @@ bp_tile_kernel(const BpArgs<T> a) {
         }
         __syncthreads();
         // bins of the window: zero guards / pads stand in for j < 0 and j >= n_det (SPAD)
-        for (int i = threadIdx.x; i < kc * BP_WB; i += BP_THREADS) {
-            const int k = i / BP_WB, w = i - k * BP_WB;
-            const T *p = s_src[k] + w;
-            const T im = s_im[k];
-            if constexpr (sizeof(T) == 4) win2[i] = make_float2(__ldg(p) * im, __ldg(p + 1) * im);
-            else win[i] = __ldg(p) * im;
+        if constexpr (sizeof(T) == 4) {
+            // a warp per angle row: each bin loaded once, its right neighbour by shuffle
+            static_assert(BP_WB == 96, "three bins per lane");
+            for (int k = warp; k < kc; k += BP_THREADS / 32) {
+                const T *src = s_src[k];
+                const T im = s_im[k];
+                const float v0 = __ldg(src + lane), v1 = __ldg(src + lane + 32), v2 = __ldg(src + lane + 64);
+                const float v3 = lane == 0 ? __ldg(src + 96) : 0.f;
+                const float n0 = __shfl_down_sync(0xffffffffu, v0, 1), n1 = __shfl_down_sync(0xffffffffu, v1, 1),
+                            n2 = __shfl_down_sync(0xffffffffu, v2, 1);
+                const float f1 = __shfl_sync(0xffffffffu, v1, 0), f2 = __shfl_sync(0xffffffffu, v2, 0),
+                            f3 = __shfl_sync(0xffffffffu, v3, 0);
+                float2 *row = win2 + k * BP_WB;
+                row[lane] = make_float2(v0 * im, (lane == 31 ? f1 : n0) * im);
+                row[lane + 32] = make_float2(v1 * im, (lane == 31 ? f2 : n1) * im);
+                row[lane + 64] = make_float2(v2 * im, (lane == 31 ? f3 : n2) * im);
+            }
+        } else {
+            for (int i = threadIdx.x; i < kc * BP_WB; i += BP_THREADS) {
+                const int k = i / BP_WB, w = i - k * BP_WB;
+                win[i] = __ldg(s_src[k] + w) * s_im[k];
+            }
         }
         __syncthreads();
         for (int k = 0; k < kc; k++) {
