@@ -932,10 +932,18 @@ bp_tile_kernel(const BpArgs<T> a) {
         const int kc = min(BP_MAXA, nang - k0);
         __syncthreads();
         for (int k = threadIdx.x; k < kc; k += BP_THREADS) {
-            const int ang = a.rows[row0 + k0 + k].angle;
-            const double2 t2 = a.trig[ang];
-            const double cs = t2.x, sn = t2.y;
-            const double m = a.xmaj[ang] ? fabs(sn) : fabs(cs);
+            double cs, sn, m, iw;
+            if (a.rowc) {
+                const double4 rc = a.rowc[row0 + k0 + k];
+                cs = rc.x; sn = rc.y; m = rc.z; iw = rc.w;
+            } else {
+                const int ang = a.rows[row0 + k0 + k].angle;
+                const double2 t2 = a.trig[ang];
+                cs = t2.x; sn = t2.y;
+                m = a.xmaj[ang] ? fabs(sn) : fabs(cs);
+                const double w = a.xmaj[ang] ? fabs(cs / sn) : fabs(sn / cs);
+                iw = w > 1e-9 ? 1.0 / w : 4194304.0;
+            }
             const double tp0 = ((double)c0 - h) * cs + (h - (double)r0) * sn;  // t_p of pixel (r0, c0)
             const double ext = (double)(BP_TS - 1);
             const double tmin = tp0 + fmin(0.0, ext * cs) + fmin(0.0, -ext * sn);
@@ -953,8 +961,6 @@ bp_tile_kernel(const BpArgs<T> a) {
             // tap weight sat(a0 - s a1) at bin distance s (times the 1/m pre-scale): Joseph
             // a1 = 1/m, a0 = 1; Siddon (R-26) a1 = 1/(m w), a0 = (1 + 1/w)/2, w = drift per line
             if (a.siddon) {
-                const double w = a.xmaj[ang] ? fabs(cs / sn) : fabs(sn / cs);
-                const double iw = w > 1e-9 ? 1.0 / w : 4194304.0;
                 ac.a1 = (T)(iw / m);
                 ac.a0 = (T)(0.5 + 0.5 * iw);
             } else {
@@ -1274,6 +1280,24 @@ void launch_fp_reduce(int prec, bool resid, const void *args, int n_rows, int n_
         if (resid) fp_reduce_kernel<double, true><<<grid, RJ * RG, 0, st>>>(A);
         else fp_reduce_kernel<double, false><<<grid, RJ * RG, 0, st>>>(A);
     }
+    TQ_CHECK_CUDA(cudaGetLastError());
+}
+
+__global__ void bp_rowc_kernel(const RayRow *rows, const double2 *trig, const int *xmaj, int n_rows,
+                               double4 *rowc) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_rows) return;
+    const int ang = rows[r].angle;
+    const double cs = trig[ang].x, sn = trig[ang].y;
+    const double m = xmaj[ang] ? fabs(sn) : fabs(cs);
+    const double w = xmaj[ang] ? fabs(cs / sn) : fabs(sn / cs);
+    rowc[r] = make_double4(cs, sn, m, w > 1e-9 ? 1.0 / w : 4194304.0);
+}
+
+void launch_bp_rowc(const RayRow *rows, const double2 *trig, const int *xmaj, int n_rows, double4 *rowc,
+                    cudaStream_t st) {
+    if (n_rows == 0) return;
+    bp_rowc_kernel<<<ceil_div(n_rows, 128), 128, 0, st>>>(rows, trig, xmaj, n_rows, rowc);
     TQ_CHECK_CUDA(cudaGetLastError());
 }
 

@@ -111,6 +111,11 @@ struct FpArgs {
     int siddon;            // 1: Siddon weights (R-26) -- generic tile kernel
 };
 
+// per ray row of a context: (cos, sin, m, 1/w) of its angle for the backprojector (one load
+// instead of the rows -> angle -> trig / xmaj chain); 1/w only for Siddon (R-26)
+void launch_bp_rowc(const RayRow *rows, const double2 *trig, const int *xmaj, int n_rows, double4 *rowc,
+                    cudaStream_t st);
+
 // row stride (bins) of the forward partial slots: n_det rounded up to a multiple of 4
 __host__ __device__ inline int fp_ps(int n_det) { return (n_det + 3) & ~3; }
 
@@ -151,6 +156,7 @@ struct BpArgs {
     int part_stride;
     uint32_t magic;          // = 0x4B000000 << 2 (mod 2^32)
     int siddon;              // 1: Siddon weights (R-26)
+    const double4 *rowc;     // [n_rows] (cos, sin, m, 1/w) per ray row, or null (from rows/trig/xmaj)
 };
 
 constexpr uint32_t kMagicBits4 = 0x2C000000u;  // (0x4B000000 << 2) mod 2^32

@@ -75,6 +75,8 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
     A((void **)&frec, sizeof(FpRec) * (size_t)nt_line * nt_cross * std::max(1, n_olist));
     A((void **)&futab, sizeof(FpUnitTab) * 2 * (size_t)std::max(1, L) * nt_line * nt_cross);
     launch_fp_setup(rows, g.xmaj, g.trig, n_rows, g.N, g.n_det, fwin, frg, olist, n_olist, frec, oofs, L, futab, 0);
+    A((void **)&rowc, sizeof(double4) * std::max(1, n_rows));
+    launch_bp_rowc(rows, g.trig, g.xmaj, n_rows, rowc, 0);
     TQ_CHECK_CUDA(cudaDeviceSynchronize());
     for (void **v : {&X, &R, &P, &Q, &BP}) A(v, es * n * L);
     A(&D, es * (size_t)n_rows * g.n_det);
@@ -91,7 +93,7 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
 
 void Inner::release() {
     for (void *p : {(void *)rows, (void *)row0, (void *)nang, X, R, P, Q, BP, D, S_base, (void *)cnode,
-                    (void *)eta, (void *)scal, (void *)partial, (void *)counter, (void *)olist,
+                    (void *)eta, (void *)scal, (void *)partial, (void *)counter, (void *)rowc, (void *)olist,
                     (void *)oofs, fpart, (void *)fwin, (void *)frg, (void *)frec, (void *)futab})
         if (p) cudaFree(p);
     rows = nullptr; row0 = nang = olist = oofs = nullptr;
@@ -99,6 +101,7 @@ void Inner::release() {
     X = R = P = Q = BP = D = S = S_base = nullptr;
     cnode = eta = scal = partial = nullptr;
     counter = nullptr;
+    rowc = nullptr;
 }
 
 int Inner::project(const DevGeom &g, const void *img, bool resid, cudaStream_t st, void *out,
@@ -126,12 +129,12 @@ int Inner::backproject(const DevGeom &g, int epi, void *out, void *out2, const v
     if (prec == 0) {
         BpArgs<float> a{(const float *)S, sp, 1, row0, nang, rows, g.trig, g.xmaj, g.N, g.n_det, n,
                         (float *)out, (float *)out2, (const float *)vin, (const float *)BP, cnode, eta,
-                        partial, counter, scal, part_stride, kMagicBits4, g.proj};
+                        partial, counter, scal, part_stride, kMagicBits4, g.proj, rowc};
         launch_bp(0, epi, &a, L, g.N, st);
     } else {
         BpArgs<double> a{(const double *)S, sp, 1, row0, nang, rows, g.trig, g.xmaj, g.N, g.n_det, n,
                          (double *)out, (double *)out2, (const double *)vin, (const double *)BP, cnode,
-                         eta, partial, counter, scal, part_stride, kMagicBits4, g.proj};
+                         eta, partial, counter, scal, part_stride, kMagicBits4, g.proj, rowc};
         launch_bp(1, epi, &a, L, g.N, st);
     }
     return 1;

@@ -43,6 +43,7 @@ struct Inner {
     double *scal = nullptr;    // [L][S_NSLOT]
     double *partial = nullptr; // [L][part_stride]
     unsigned *counter = nullptr;
+    double4 *rowc = nullptr;     // [n_rows] backprojector per-row angle constants
     std::vector<RayRow> rows_h;
     std::vector<int> row0_h, nang_h;
     // angle lists per local node (global angle ids, increasing)
