@@ -763,10 +763,18 @@ __global__ void fp_unit_kernel(const int *oofs, const FpRec *recs, int n_olist, 
 // per thread for nt_line <= 8 RG), then the group partials are added in a fixed order in
 // shared memory (deterministic, no atomics).
 constexpr int RJ = 32, RG = 4;  // bins per CTA, band groups
+template <typename T>
+__device__ __forceinline__ double fp_row_m(const FpRedArgs<T> &a, int row) {
+    if (a.rowc) return a.rowc[row].z;
+    const int ang = a.rows[row].angle;
+    const double2 t2 = a.trig[ang];
+    return a.xmaj[ang] ? fabs(t2.y) : fabs(t2.x);
+}
 template <typename T, bool RESID>
 __global__ void __launch_bounds__(RJ * RG) fp_reduce_kernel(const FpRedArgs<T> a) {
     __shared__ T part[RG][RJ];
     const int row = blockIdx.y;
+    const double m_row = fp_row_m(a, row);  // issued first: its latency overlaps the slot loads
     const int jj = threadIdx.x % RJ, g = threadIdx.x / RJ;
     const int j = blockIdx.x * RJ + jj;
     const int nb = a.nt_line;
@@ -798,9 +806,7 @@ __global__ void __launch_bounds__(RJ * RG) fp_reduce_kernel(const FpRedArgs<T> a
     T tot = part[0][jj];
 #pragma unroll
     for (int q = 1; q < RG; q++) tot += part[q][jj];
-    const int ang = a.rows[row].angle;
-    const double2 t2 = a.trig[ang];
-    const double inv_m = a.xmaj[ang] ? 1.0 / fabs(t2.y) : 1.0 / fabs(t2.x);
+    const double inv_m = 1.0 / m_row;
     T v = (T)((double)tot * inv_m);
     if (RESID) v = a.d[(long long)row * a.n_det + j] - v;
     a.out[(long long)row * a.out_stride + a.out_off + j] = v;
@@ -813,6 +819,7 @@ template <bool RESID>
 __global__ void __launch_bounds__(RQ * RG) fp_reduce_f32(const FpRedArgs<float> a) {
     __shared__ float4 part[RG][RQ];
     const int row = blockIdx.y;
+    const double m_row = fp_row_m(a, row);  // issued first: its latency overlaps the slot loads
     const int q = threadIdx.x % RQ, g = threadIdx.x / RQ;
     const int j0 = 4 * (blockIdx.x * RQ + q);
     const int nb = a.nt_line, nd = fp_ps(a.n_det);
@@ -854,9 +861,7 @@ __global__ void __launch_bounds__(RQ * RG) fp_reduce_f32(const FpRedArgs<float> 
         tot.z += part[r][q].z;
         tot.w += part[r][q].w;
     }
-    const int ang = a.rows[row].angle;
-    const double2 t2 = a.trig[ang];
-    const double inv_m = a.xmaj[ang] ? 1.0 / fabs(t2.y) : 1.0 / fabs(t2.x);
+    const double inv_m = 1.0 / m_row;
     const float tv[4] = {tot.x, tot.y, tot.z, tot.w};
 #pragma unroll
     for (int e = 0; e < 4; e++) {

@@ -129,6 +129,7 @@ struct FpRedArgs {
     T *out;                // [n_rows][out_stride] + out_off
     int out_stride, out_off;
     int N, n_det, nt_line;
+    const double4 *rowc;   // [n_rows] as BpArgs::rowc (m in .z), or null
 };
 
 template <typename T>
