@@ -32,14 +32,14 @@ __device__ __forceinline__ void graph_dual_elem(const T *const *nb, int deg, con
 
 // one node per blockIdx.y; 4 elements per thread per step through 16-byte accesses
 template <typename T>
-__global__ void __launch_bounds__(CT) graph_dual(const T *const *xh, const int *own_slot,
-                                                 const int *nbr_off, const int *nbr_slot, T *alpha,
+__global__ void __launch_bounds__(CT) graph_dual(const T *const *own_ptr, const T *const *nbr_ptr,
+                                                 const int *nbr_off, T *alpha,
                                                  T *bprime, long long n, double rho, int update) {
     __shared__ const T *nb[MAXNB];
     const int i = blockIdx.y;
-    const T *own = xh[own_slot[i]];
+    const T *own = own_ptr[i];
     const int k0 = nbr_off[i], deg = nbr_off[i + 1] - k0;
-    for (int k = threadIdx.x; k < deg; k += CT) nb[k] = xh[nbr_slot[k0 + k]];
+    for (int k = threadIdx.x; k < deg; k += CT) nb[k] = nbr_ptr[k0 + k];
     __syncthreads();
     T *al = alpha + (long long)i * n;
     T *bp = bprime + (long long)i * n;
@@ -160,17 +160,17 @@ __global__ void __launch_bounds__(CT) to_float(const T *const *src, float *const
 
 }  // namespace
 
-int launch_graph_dual(int prec, const void *const *xh_tab, const int *own_slot, const int *nbr_off,
-                      const int *nbr_slot, void *alpha, void *bprime, long long n, int L, double rho,
+int launch_graph_dual(int prec, const void *const *own_ptr, const void *const *nbr_ptr, const int *nbr_off,
+                      void *alpha, void *bprime, long long n, int L, double rho,
                       int update_alpha, cudaStream_t st) {
     if (L == 0) return 0;
     if (prec == 0)
-        graph_dual<float><<<grid_dual(n, L), CT, 0, st>>>((const float *const *)xh_tab, own_slot, nbr_off,
-                                                        nbr_slot, (float *)alpha, (float *)bprime, n, rho,
+        graph_dual<float><<<grid_dual(n, L), CT, 0, st>>>((const float *const *)own_ptr, (const float *const *)nbr_ptr,
+                                                        nbr_off, (float *)alpha, (float *)bprime, n, rho,
                                                         update_alpha);
     else
-        graph_dual<double><<<grid_dual(n, L), CT, 0, st>>>((const double *const *)xh_tab, own_slot, nbr_off,
-                                                         nbr_slot, (double *)alpha, (double *)bprime, n,
+        graph_dual<double><<<grid_dual(n, L), CT, 0, st>>>((const double *const *)own_ptr, (const double *const *)nbr_ptr,
+                                                         nbr_off, (double *)alpha, (double *)bprime, n,
                                                          rho, update_alpha);
     TQ_CHECK_CUDA(cudaGetLastError());
     return 1;

@@ -8,8 +8,8 @@ namespace tq {
 // rule=graph (R-7): for local node i with public value xh_i = Q(x_i) and
 // neighbour sum S_i = sum_j xh_j:  alpha_i += rho (deg_i xh_i - S_i);
 // b'_i = -alpha_i + rho (deg_i xh_i + S_i).  update_alpha = 0 only recomputes b'.
-int launch_graph_dual(int prec, const void *const *xh_tab, const int *own_slot, const int *nbr_off,
-                      const int *nbr_slot, void *alpha, void *bprime, long long n, int L, double rho,
+int launch_graph_dual(int prec, const void *const *own_ptr, const void *const *nbr_ptr, const int *nbr_off,
+                      void *alpha, void *bprime, long long n, int L, double rho,
                       int update_alpha, cudaStream_t st);
 
 // rule=paper, Alg. 3 on node i's own segment [lo_i, lo_i + len) of its

@@ -247,6 +247,7 @@ void Ctx::free_exchange() {
     sends.clear(); recvs.clear(); send_buf.clear(); recv_buf.clear(); send_bytes.clear(); recv_bytes.clear();
     label_row.clear();
     fstage = nullptr; labels_buf = nullptr; xh_tab = nullptr; own_slot = nbr_off = nbr_slot = nullptr;
+    own_ptr = nbr_ptr = nullptr;
     xg_tab = nullptr; seg_lo = nullptr; seg_len = nullptr; seg_tab = nullptr;
     cs_slice = cs_first = cs_cnt = node_slice = nullptr;
     xready = false;
@@ -607,6 +608,12 @@ void Ctx::setup_exchange() {
         nbr_off = (int *)upload(off.data(), sizeof(int) * (L + 1));
         if (nb.empty()) nb.push_back(0);
         nbr_slot = (int *)upload(nb.data(), sizeof(int) * nb.size());
+        // the same tables resolved to pointers (the dual kernel's prologue: one load level)
+        std::vector<const void *> ownp(std::max(1, L), nullptr), nbp(nb.size());
+        for (int i = 0; i < L; i++) ownp[i] = xh[own[i]];
+        for (size_t k = 0; k < nb.size(); k++) nbp[k] = xh[nb[k]];
+        own_ptr = (const void **)upload(ownp.data(), sizeof(void *) * ownp.size());
+        nbr_ptr = (const void **)upload(nbp.data(), sizeof(void *) * nbp.size());
     } else {
         std::vector<void *> xg(L);
         std::vector<long long> lo(L), len(L);
@@ -747,7 +754,7 @@ int Ctx::phase_b(cudaStream_t s) {
         }
     }
     if (rule == TQ_RULE_GRAPH)
-        k += launch_graph_dual(prec, xh_tab, own_slot, nbr_off, nbr_slot, ALPHA, in.BP, n, L, prm.rho, 1, s);
+        k += launch_graph_dual(prec, own_ptr, nbr_ptr, nbr_off, ALPHA, in.BP, n, L, prm.rho, 1, s);
     else
         k += launch_paper_dual(prec, in.X, ALPHA, in.BP, (const void *const *)xg_tab, n, L, prm.rho, 1, s);
     return k;
@@ -755,7 +762,7 @@ int Ctx::phase_b(cudaStream_t s) {
 
 int Ctx::prepare_rhs(cudaStream_t s) {
     if (rule == TQ_RULE_GRAPH)
-        return launch_graph_dual(prec, xh_tab, own_slot, nbr_off, nbr_slot, ALPHA, in.BP, n, L, prm.rho, 0, s);
+        return launch_graph_dual(prec, own_ptr, nbr_ptr, nbr_off, ALPHA, in.BP, n, L, prm.rho, 0, s);
     return launch_paper_dual(prec, in.X, ALPHA, in.BP, (const void *const *)xg_tab, n, L, prm.rho, 0, s);
 }
 

@@ -95,6 +95,7 @@ struct Ctx {
     // graph rule dual tables
     const void **xh_tab = nullptr;
     int *own_slot = nullptr, *nbr_off = nullptr, *nbr_slot = nullptr;
+    const void **own_ptr = nullptr, **nbr_ptr = nullptr;  // xh_tab[own_slot[i]], xh_tab[nbr_slot[k]]
     // paper / consensus rule tables
     int *cs_slice = nullptr, *cs_first = nullptr, *cs_cnt = nullptr, *node_slice = nullptr;
     void **xg_tab = nullptr;
