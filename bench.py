@@ -254,6 +254,18 @@ def main():
     ap.add_argument("--no-c5-geometry", action="store_true")
     ap.add_argument("--precision", type=int, default=0)
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N` without a launcher: one rank per GPU under torchrun
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    if env_int("WORLD_SIZE", 1) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_int('WORLD_SIZE', 1)} "
+                         f"(launch one rank per GPU, or drop the launcher and let bench.py spawn them)")
     if args.impl == "reference":
         run_reference(args)
         return

@@ -110,10 +110,21 @@ typedef struct {
 } tq_stats;
 
 /* ---------------------------------------------------------------- context API */
+/* Transport ids for world > 1 (the exchange of P:188 / P:248-252 between ranks).
+ * tq_nccl_unique_id: an NCCL unique id (rank 0 creates it, the caller broadcasts it); one
+ *   process per GPU; payloads move with ncclSend / ncclRecv, the consensus sums with ncclReduce.
+ * tq_loopback_id: an in-process world: the `world` contexts created with it live in THIS
+ *   process (one host thread per rank, calling the same sequence of context calls, as NCCL
+ *   ranks would), on one GPU or several.  Each receiver pulls every planned payload with its
+ *   own cudaMemcpyAsync from the sender's buffer; the consensus segment sums are a fixed-order
+ *   (rank 0, 1, ...) kernel at the segment owner.  A rank that does not reach a rendezvous
+ *   within TQ_LOOPBACK_TIMEOUT_S seconds (default 120) makes every rank fail with TQ_ENCCL.
+ *   Results equal the world == 1 run bit for bit (graph and paper rules). */
 tq_status tq_nccl_unique_id(uint8_t id[128]);
+tq_status tq_loopback_id(uint8_t id[128]);
 
-/* One context per process/rank, owning every (slice, node) mapped to this rank.
- * nccl_id: from rank 0's tq_nccl_unique_id (broadcast by the caller), NULL if world == 1.
+/* One context per rank, owning every (slice, node) mapped to this rank.
+ * nccl_id: a transport id (above) from rank 0, the same on every rank; NULL if world == 1.
  * device: CUDA device ordinal to use. */
 tq_status tq_create(const tq_geometry *geom, const tq_graph *graph, int32_t n_slices,
                     int32_t rank, int32_t world, const uint8_t *nccl_id, int32_t precision,
@@ -124,10 +135,17 @@ tq_status tq_set_quantizer(tq_ctx *ctx, const tq_quant *q);
 /* Sinogram of one slice.  node >= 0: that node's shard ([a_node][n_det], its angles in
  * increasing order); node == -1: the full slice sinogram [n_angles][n_det] and the
  * library keeps the rows of its local nodes.  Ignored for nodes not on this rank.
- * len is in floats; on_device: d is a device pointer.  Returns once d has been copied (the
- * caller may reuse it); the new rows replace the old ones after any enqueued run. */
+ * len is in floats; on_device: d is a device pointer, which must hold its final values when
+ * the call is made (no write to it still pending on any stream -- use tq_set_sinogram_stream
+ * for a buffer written asynchronously).  Returns once d has been copied (the caller may reuse
+ * it); the new rows replace the old ones after any enqueued run. */
 tq_status tq_set_sinogram(tq_ctx *ctx, int32_t slice, int32_t node, const float *d,
                           int64_t len, int32_t on_device);
+/* The same for a device buffer d written on the caller's `stream` (NULL = legacy default
+ * stream): the library's copy of d is ordered after everything already enqueued on `stream`
+ * (an event recorded there).  Returns once d has been copied. */
+tq_status tq_set_sinogram_stream(tq_ctx *ctx, int32_t slice, int32_t node, const float *d,
+                                 int64_t len, void *stream);
 
 /* Enqueue `iters` ADMM iterations (Alg. 4) on `stream` (NULL = the
  * context's own stream) and wait for them; returns TQ_EDIVERGED if any node's norm

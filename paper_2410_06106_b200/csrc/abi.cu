@@ -83,6 +83,13 @@ tq_status tq_nccl_unique_id(uint8_t id[128]) {
     });
 }
 
+tq_status tq_loopback_id(uint8_t id[128]) {
+    return guard(nullptr, [&] {
+        TQ_REQUIRE(id != nullptr, "null id");
+        new_loopback_id(id);
+    });
+}
+
 tq_status tq_create(const tq_geometry *geom, const tq_graph *graph, int32_t n_slices, int32_t rank,
                     int32_t world, const uint8_t *nccl_id, int32_t precision, int32_t device,
                     tq_ctx **out) {
@@ -124,6 +131,12 @@ tq_status tq_set_sinogram(tq_ctx *ctx, int32_t slice, int32_t node, const float 
                           int32_t on_device) {
     if (!ctx) return TQ_EINVAL;
     return guard(ctx, [&] { ctx->c.set_sinogram(slice, node, d, len, on_device != 0); });
+}
+
+tq_status tq_set_sinogram_stream(tq_ctx *ctx, int32_t slice, int32_t node, const float *d, int64_t len,
+                                 void *stream) {
+    if (!ctx) return TQ_EINVAL;
+    return guard(ctx, [&] { ctx->c.set_sinogram(slice, node, d, len, true, (cudaStream_t)stream, true); });
 }
 
 tq_status tq_run(tq_ctx *ctx, int32_t iters, void *stream) {

@@ -1,5 +1,4 @@
 // engine.cu -- see engine.cuh.
-#include <dlfcn.h>
 #include <math.h>
 
 #include <algorithm>
@@ -11,44 +10,6 @@
 namespace tq {
 
 [[noreturn]] void fail(tq_status code, const std::string &msg) { throw Error{code, msg}; }
-
-// ---------------------------------------------------------------- NCCL (dlopen'd)
-NcclApi &nccl() {
-    static NcclApi api;
-    static bool tried = false;
-    if (!api.h && !tried) {
-        tried = true;
-        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-        if (h) {
-            bool ok = true;
-            auto sym = [&](const char *name) {
-                void *p = dlsym(h, name);
-                if (!p) ok = false;
-                return p;
-            };
-            api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
-            api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
-            api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
-            api.Send = (decltype(api.Send))sym("ncclSend");
-            api.Recv = (decltype(api.Recv))sym("ncclRecv");
-            api.Reduce = (decltype(api.Reduce))sym("ncclReduce");
-            api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
-            api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
-            api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
-            if (ok) api.h = h;
-        }
-    }
-    if (!api.h) fail(TQ_ENCCL, "libnccl.so.2 could not be loaded");
-    return api;
-}
-
-#define TQ_CHECK_NCCL(call)                                                                       \
-    do {                                                                                          \
-        ncclResult_t _r = (call);                                                                 \
-        if (_r != ncclSuccess)                                                                    \
-            ::tq::fail(TQ_ENCCL, std::string(#call) + ": " + ::tq::nccl().GetErrorString(_r));    \
-    } while (0)
 
 // ---------------------------------------------------------------- exchange plan
 // graph rule: a node's payload goes to every rank owning one of its neighbours
@@ -194,6 +155,8 @@ void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int ran
     TQ_CHECK_CUDA(cudaEventCreate(&ev0));
     TQ_CHECK_CUDA(cudaEventCreate(&ev1));
     TQ_CHECK_CUDA(cudaEventCreateWithFlags(&run_done, cudaEventDisableTiming));
+    TQ_CHECK_CUDA(cudaEventCreateWithFlags(&gathers_done, cudaEventDisableTiming));
+    TQ_CHECK_CUDA(cudaEventCreateWithFlags(&src_ready, cudaEventDisableTiming));
     for (int b = 0; b < NSTAGE; b++) {
         TQ_CHECK_CUDA(cudaEventCreateWithFlags(&stage_copied[b], cudaEventDisableTiming));
         TQ_CHECK_CUDA(cudaEventCreateWithFlags(&stage_free[b], cudaEventDisableTiming));
@@ -212,12 +175,7 @@ void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int ran
         TQ_CHECK_CUDA(cudaMalloc(&CSUM, sizeof(double) * n * S));
         TQ_CHECK_CUDA(cudaMemset(CSUM, 0, sizeof(double) * n * S));
     }
-    if (world > 1) {
-        TQ_REQUIRE(nccl_id != nullptr, "world > 1 needs an NCCL unique id");
-        ncclUniqueId id;
-        memcpy(&id, nccl_id, sizeof(id));
-        TQ_CHECK_NCCL(nccl().CommInitRank(&comm, world, id, rank));
-    }
+    if (world > 1) tr = make_transport(nccl_id, rank, world, device);
     sino_set.assign(L, 0);
     st.local_nodes = L;
     st.world = world;
@@ -244,7 +202,7 @@ void Ctx::free_exchange() {
     pay_of.clear();
     for (auto &b : enc) b = Batch();
     for (auto &b : dec) b = Batch();
-    sends.clear(); recvs.clear(); send_buf.clear(); recv_buf.clear(); send_bytes.clear(); recv_bytes.clear();
+    sends.clear(); recvs.clear(); sum_segs.clear();
     label_row.clear();
     fstage = nullptr; labels_buf = nullptr; xh_tab = nullptr; own_slot = nbr_off = nbr_slot = nullptr;
     own_ptr = nbr_ptr = nullptr;
@@ -284,12 +242,15 @@ void Ctx::destroy() {
         img_async[b] = nullptr; img_ready[b] = img_done[b] = nullptr;
     }
     img_stage = nullptr;
-    if (comm) nccl().CommDestroy(comm);
-    comm = nullptr;
+    tr.reset();
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (run_done) cudaEventDestroy(run_done);
     run_done = nullptr;
+    if (gathers_done) cudaEventDestroy(gathers_done);
+    gathers_done = nullptr;
+    if (src_ready) cudaEventDestroy(src_ready);
+    src_ready = nullptr;
     for (int b = 0; b < NSTAGE; b++) {
         if (stage_copied[b]) cudaEventDestroy(stage_copied[b]);
         if (stage_free[b]) cudaEventDestroy(stage_free[b]);
@@ -327,6 +288,9 @@ void Ctx::set_params(const tq_params &p) {
         TQ_CHECK_CUDA(cudaMemcpy(in.cnode, c.data(), sizeof(double) * L, cudaMemcpyHostToDevice));
         TQ_CHECK_CUDA(cudaMemcpy(in.eta, eta.data(), sizeof(double) * L, cudaMemcpyHostToDevice));
     }
+    // a change of rho (or of c_i) after iterations ran: b' of the current state is rebuilt with
+    // the new values before the next iteration (as tq_import_state does)
+    if (have_params) need_rhs = true;
     have_params = true;
     invalidate();
 }
@@ -347,7 +311,8 @@ void Ctx::set_quant(const tq_quant &qq) {
     q = qq;
 }
 
-void Ctx::set_sinogram(int slice, int node, const float *d, long long len, bool on_device) {
+void Ctx::set_sinogram(int slice, int node, const float *d, long long len, bool on_device, cudaStream_t src_s,
+                       bool has_src_s) {
     TQ_REQUIRE(slice >= 0 && slice < S, "slice out of range");
     TQ_REQUIRE(node >= -1 && node < M, "node out of range");
     TQ_REQUIRE(d != nullptr, "null sinogram");
@@ -375,6 +340,10 @@ void Ctx::set_sinogram(int slice, int node, const float *d, long long len, bool 
     // the buffer is free once the last gather that read it ran; the caller's buffer is free
     // once this copy completed (waited for below)
     TQ_CHECK_CUDA(cudaStreamWaitEvent(up_stream, stage_free[b], 0));
+    if (has_src_s) {  // the caller's device buffer is read after the work already on its stream
+        TQ_CHECK_CUDA(cudaEventRecord(src_ready, src_s));
+        TQ_CHECK_CUDA(cudaStreamWaitEvent(up_stream, src_ready, 0));
+    }
     TQ_CHECK_CUDA(cudaMemcpyAsync(sino_stage[b], d, sizeof(float) * len,
                                   on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, up_stream));
     TQ_CHECK_CUDA(cudaEventRecord(stage_copied[b], up_stream));
@@ -430,12 +399,22 @@ void Ctx::flush_gathers(cudaStream_t s) {
         TQ_CHECK_CUDA(cudaEventRecord(stage_free[pg.buf], s));
     }
     pend_gathers.clear();
+    // a run or component launched later on another stream orders itself after these gathers
+    TQ_CHECK_CUDA(cudaEventRecord(gathers_done, s));
+    gathers_s = s;
+    gathers_live = true;
+}
+
+// the gathers placed by flush_gathers on another stream than s complete before s reads D
+void Ctx::order_after_gathers(cudaStream_t s) {
+    if (gathers_live && gathers_s != s) wait_unless_done(s, gathers_done);
 }
 
 long long Ctx::launch_component(int component, int reps, cudaStream_t s) {
     TQ_REQUIRE(reps >= 0, "reps must be >= 0");
     finish();
     flush_gathers(s ? s : stream);
+    order_after_gathers(s ? s : stream);
     if (!have_params) fail(TQ_ESTATE, "tq_set_params must be called first");
     TQ_CHECK_CUDA(cudaSetDevice(device));
     if (!xready) setup_exchange();
@@ -648,15 +627,11 @@ void Ctx::setup_exchange() {
     for (int s : slices_here) {
         for (auto &x : sp) {
             const int k = pay_of.at({s, x.first});
-            sends.push_back({s, x.first, x.second});
-            send_buf.push_back(pays[k].buf);
-            send_bytes.push_back(pbytes[k]);
+            sends.push_back(XferDesc{s, x.first, x.second, pays[k].buf, pbytes[k]});
         }
         for (auto &x : rp) {
             const int k = pay_of.at({s, x.first});
-            recvs.push_back({s, x.first, x.second});
-            recv_buf.push_back(pays[k].buf);
-            recv_bytes.push_back(pbytes[k]);
+            recvs.push_back(XferDesc{s, x.first, x.second, pays[k].buf, pbytes[k]});
         }
     }
     // ---- logical bytes (what the method sends, independent of placement)
@@ -683,9 +658,14 @@ void Ctx::setup_exchange() {
     }
     st.payload_bytes_logical = logical;
     st.nccl_bytes_sent = 0;
-    for (auto b : send_bytes) st.nccl_bytes_sent += b;
+    for (auto &x : sends) st.nccl_bytes_sent += x.bytes;
     st.nccl_bytes_recv = 0;
-    for (auto b : recv_bytes) st.nccl_bytes_recv += b;
+    for (auto &x : recvs) st.nccl_bytes_recv += x.bytes;
+    if (rule == TQ_RULE_CONSENSUS)
+        for (int t = 0; t < S; t++)
+            for (int m = 0; m < M; m++)
+                sum_segs.push_back(SumSeg{(long long)t * n + (long long)row_off[m] * N,
+                                          (long long)(row_off[m + 1] - row_off[m]) * N, node_rank[m]});
     xready = true;
 }
 
@@ -719,27 +699,15 @@ int Ctx::stage(int id, cudaStream_t s) {
 // consensus rule, world > 1: segment m of every slice's partial sum is summed onto the
 // rank owning node m (one grouped ncclReduce per (slice, segment) -- a reduce-scatter in
 // the paper's segment layout), which then forms x[m] locally.
-void Ctx::reduce_sums(cudaStream_t s) {
-    NcclApi &api = nccl();
-    TQ_CHECK_NCCL(api.GroupStart());
-    for (int t = 0; t < S; t++)
-        for (int m = 0; m < M; m++) {
-            double *p = CSUM + (long long)t * n + (long long)row_off[m] * N;
-            const size_t cnt = (size_t)(row_off[m + 1] - row_off[m]) * N;
-            TQ_CHECK_NCCL(api.Reduce(p, p, cnt, ncclFloat64, ncclSum, node_rank[m], comm, s));
-        }
-    TQ_CHECK_NCCL(api.GroupEnd());
-}
+void Ctx::reduce_sums(cudaStream_t s) { tr->reduce_sum(s, CSUM, sum_segs); }
 
 void Ctx::exchange(cudaStream_t s) {
-    if (world == 1 || (sends.empty() && recvs.empty())) return;
-    NcclApi &api = nccl();
-    TQ_CHECK_NCCL(api.GroupStart());
-    for (size_t i = 0; i < sends.size(); i++)
-        TQ_CHECK_NCCL(api.Send(send_buf[i], (size_t)send_bytes[i], ncclUint8, sends[i].peer, comm, s));
-    for (size_t i = 0; i < recvs.size(); i++)
-        TQ_CHECK_NCCL(api.Recv(recv_buf[i], (size_t)recv_bytes[i], ncclUint8, recvs[i].peer, comm, s));
-    TQ_CHECK_NCCL(api.GroupEnd());
+    if (!has_exchange()) return;
+    tr->exchange(s, sends, recvs);
+}
+
+bool Ctx::has_exchange() const {
+    return world > 1 && (tr->collective_exchange() || !(sends.empty() && recvs.empty()));
 }
 
 int Ctx::phase_b(cudaStream_t s) {
@@ -786,6 +754,7 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
     cudaStream_t s = user ? user : stream;
     if (pending && s != run_s) TQ_CHECK_CUDA(cudaStreamWaitEvent(s, run_done, 0));  // previous run
     flush_gathers(s);  // a new sinogram: its gather, in-stream
+    order_after_gathers(s);  // gathers flushed earlier onto another stream (set_sinogram reuse)
     for (int b = 0; b < 2; b++)  // an enqueued tq_get_image_async snapshot reads X first
         if (img_used[b] && img_s[b] != s) TQ_CHECK_CUDA(cudaStreamWaitEvent(s, img_ready[b], 0));
     run_s = s;
@@ -814,7 +783,7 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
     if (segs.empty()) {
         // stages 0 | reduce | 1 | exchange | 2, merged where no communication separates them
         const bool red = rule == TQ_RULE_CONSENSUS && world > 1;
-        const bool exch = world > 1 && !(sends.empty() && recvs.empty());
+        const bool exch = has_exchange();
         std::vector<int> cur{0};
         if (red) { capture(cur, COMM_REDUCE); cur.clear(); }
         cur.push_back(1);

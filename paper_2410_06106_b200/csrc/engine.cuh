@@ -3,34 +3,17 @@
 // for the three consensus rules, the quantized exchange (NCCL send/recv between ranks,
 // pointers within a rank) and CUDA-graph replay of whole iterations.
 #pragma once
-#include <nccl.h>
-
 #include <map>
+#include <memory>
 
 #include "codecs.cuh"
 #include "consensus.cuh"
 #include "solver.cuh"
+#include "transport.cuh"
 
 namespace tq {
 
-struct NcclApi {
-    void *h = nullptr;
-    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
-    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
-    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*Reduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
-                           cudaStream_t) = nullptr;
-    ncclResult_t (*GroupStart)() = nullptr;
-    ncclResult_t (*GroupEnd)() = nullptr;
-    const char *(*GetErrorString)(ncclResult_t) = nullptr;
-};
-NcclApi &nccl();  // loads libnccl.so.2 on first use (fails with TQ_ENCCL if absent)
 
-struct XferItem {  // one payload crossing ranks in an iteration
-    int slice, node, peer;
-};
 // exchange plan of one rank for one slice-independent graph
 void exchange_plan(int M, const std::vector<int> &edges, const std::vector<int> &node_rank, int rule,
                    int rank, int world, std::vector<std::pair<int, int>> &sends,
@@ -102,11 +85,10 @@ struct Ctx {
     long long *seg_lo = nullptr, *seg_len = nullptr;
     long long seg_max = 0;
     float **seg_tab = nullptr;
-    // NCCL
-    ncclComm_t comm = nullptr;
-    std::vector<XferItem> sends, recvs;
-    std::vector<uint8_t *> send_buf, recv_buf;
-    std::vector<long long> send_bytes, recv_bytes;
+    // communication between ranks (world > 1): NCCL or the in-process loopback
+    std::unique_ptr<Transport> tr;
+    std::vector<XferDesc> sends, recvs;       // this rank's plan entries, sorted by (peer, node)
+    std::vector<SumSeg> sum_segs;             // consensus rule: the segment sums and their owners
     // ---- execution
     cudaStream_t stream = nullptr;
     // an iteration = graph segments separated by communication steps (none when world == 1)
@@ -124,7 +106,8 @@ struct Ctx {
     void destroy();
     void set_params(const tq_params &p);
     void set_quant(const tq_quant &qq);
-    void set_sinogram(int slice, int node, const float *d, long long len, bool on_device);
+    void set_sinogram(int slice, int node, const float *d, long long len, bool on_device,
+                      cudaStream_t src_s = nullptr, bool has_src_s = false);
     void run(int iters, cudaStream_t user);        // enqueue + finish
     void run_async(int iters, cudaStream_t user);  // enqueue only; finish() reports later
     void finish();  // wait for an enqueued run; its stats and divergence check (may fail)
@@ -145,6 +128,11 @@ struct Ctx {
     struct PendGather { int buf; int *pairs; int count; };
     std::vector<PendGather> pend_gathers;
     void flush_gathers(cudaStream_t s);
+    cudaEvent_t gathers_done = nullptr;  // end of the last flushed gathers (on gathers_s)
+    cudaStream_t gathers_s = nullptr;
+    bool gathers_live = false;
+    void order_after_gathers(cudaStream_t s);
+    cudaEvent_t src_ready = nullptr;     // tq_set_sinogram_stream: the caller's stream position
     struct GatherMap { int *pairs; int count; };
     std::map<std::pair<int, int>, GatherMap> gather_maps;  // (slice, node) -> sinogram row pairs
     float *img_stage = nullptr;    // persistent staging of tq_get_image
@@ -173,6 +161,7 @@ struct Ctx {
                                         // 2: decode + dual (phase_b)
     void reduce_sums(cudaStream_t s);   // consensus, world > 1: segment sums to their owners
     void exchange(cudaStream_t s);
+    bool has_exchange() const;
     int phase_b(cudaStream_t s);  // decode + dual / next b'
     int prepare_rhs(cudaStream_t s);
     void enqueue(int iters, cudaStream_t user);

@@ -61,10 +61,12 @@ _lib = None
 _vp, _i32, _i64, _d = C.c_void_p, C.c_int32, C.c_int64, C.c_double
 _SIGS = {
     "tq_nccl_unique_id": [_vp],
+    "tq_loopback_id": [_vp],
     "tq_create": [C.POINTER(Geometry), C.POINTER(Graph), _i32, _i32, _i32, _vp, _i32, _i32, C.POINTER(_vp)],
     "tq_set_params": [_vp, C.POINTER(Params)],
     "tq_set_quantizer": [_vp, C.POINTER(Quant)],
     "tq_set_sinogram": [_vp, _i32, _i32, _vp, _i64, _i32],
+    "tq_set_sinogram_stream": [_vp, _i32, _i32, _vp, _i64, _vp],
     "tq_run": [_vp, _i32, _vp],
     "tq_run_async": [_vp, _i32, _vp],
     "tq_wait": [_vp],
@@ -170,6 +172,14 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def loopback_id() -> bytes:
+    """An in-process world id (tq_loopback_id): pass it as `nccl_id` to the `world`
+    contexts of one process (one thread per rank)."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib().tq_loopback_id(buf))
+    return bytes(buf)
+
+
 # --------------------------------------------------------------------- context
 class Context:
     """One rank's ADMM context (tq_create)."""
@@ -207,8 +217,11 @@ class Context:
             import torch
             if isinstance(sino, torch.Tensor):
                 t = sino.detach().contiguous().to(torch.float32)
-                self._c(lib().tq_set_sinogram(self.h, slice_, node, t.data_ptr(), t.numel(),
-                                              1 if t.is_cuda else 0))
+                if t.is_cuda:  # ordered after torch's pending writes to t (its current stream)
+                    self._c(lib().tq_set_sinogram_stream(self.h, slice_, node, t.data_ptr(), t.numel(),
+                                                         _stream(None)))
+                else:
+                    self._c(lib().tq_set_sinogram(self.h, slice_, node, t.data_ptr(), t.numel(), 0))
                 return
         except ImportError:
             pass

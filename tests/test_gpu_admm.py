@@ -405,3 +405,61 @@ def test_set_sinogram_repeated_before_run():
     b.set_sinogram(0, inp2.sino[0])
     b.run(2)
     assert np.array_equal(a.image(), b.image())
+
+
+def test_set_sinogram_many_slices_then_user_stream():
+    """More tq_set_sinogram calls than upload staging buffers (6 slices, 4 buffers: the older
+    gathers are flushed onto the context's stream), then a run on a user stream: the run is
+    ordered after those gathers (gathers_done event) -- same result as a context
+    that runs on its own stream."""
+    import torch
+    cfg = C.scaled(C.C5(slices=6), 64, 96, iters=2)
+    inp = C.make_inputs(cfg, with_truth=False)
+    a = gpu_context(cfg, inp)  # sets 6 slices
+    st = torch.cuda.Stream()
+    a.run(2, st)
+    b = gpu_context(cfg, inp)
+    b.run(2)
+    for s in range(6):
+        assert np.array_equal(a.image(s, 3), b.image(s, 3))
+
+
+def test_set_sinogram_device_tensor_written_async():
+    """A CUDA sinogram still being written on torch's current stream when tq_set_sinogram is
+    called: the binding passes that stream (tq_set_sinogram_stream), so the upload reads the
+    final values."""
+    import torch
+    cfg = c2s()
+    inp = C.make_inputs(cfg)
+    want = gpu_context(cfg, inp)
+    want.run(2)
+    ctx = gpu_context(cfg, inp)
+    src = torch.tensor(inp.sino[0], device="cuda")
+    big = torch.randn(4096, 4096, device="cuda")
+    for _ in range(20):  # keep the current stream busy
+        big = big @ big / 64.0
+    dev = torch.zeros_like(src)
+    dev.copy_(src)  # enqueued behind the matmuls
+    ctx.set_sinogram(0, dev)
+    ctx.run(2)
+    assert np.array_equal(ctx.image(), want.image())
+
+
+def test_set_params_rho_change_rebuilds_rhs():
+    """Changing rho between runs rebuilds b' from the current state with the new rho before
+    the next iteration: equal to a context that imports the same state under the
+    new rho (tq_import_state also rebuilds b')."""
+    cfg = c2s()
+    cfg.quant = C.Q_NONE
+    inp = C.make_inputs(cfg)
+    a = gpu_context(cfg, inp, precision=1)
+    a.run(3)
+    states = [a.export_state(0, m) for m in range(cfg.nodes)]
+    a.set_params(2.0, inner=cfg.inner, e1=cfg.e1)
+    a.run(2)
+    b = gpu_context(cfg, inp, precision=1)
+    b.set_params(2.0, inner=cfg.inner, e1=cfg.e1)
+    for m in range(cfg.nodes):
+        b.import_state(0, m, states[m])
+    b.run(2)
+    assert rel(a.image(), b.image()) <= 1e-13
