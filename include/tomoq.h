@@ -50,6 +50,12 @@ typedef struct {
                             lengths P_ji = |ray j inside pixel i| (SURVEY NEXT-3,
                             R-26: trig exact at 0 and pi/2, a ray on a pixel edge counts half
                             in each of the two pixels) */
+    const double *angles_rad; /* NULL: theta_a = pi a / n_angles ("evenly distributed from
+                            0 to 180 degrees"), major axis by the integer rule above (R-3).
+                            Else n_angles explicit angles in [0, pi) (radians, any order, copied),
+                            ray (theta, t) = {x cos + y sin = t} as P:42; major axis x iff
+                            |sin theta| >= |cos theta| in fp64 (R-3 for explicit lists); Siddon
+                            takes trig exact where theta == 0 or theta == fl64(pi/2) (R-26). */
 } tq_geometry;
 
 enum { TQ_PROJ_JOSEPH = 0, TQ_PROJ_SIDDON = 1 };
@@ -83,6 +89,15 @@ typedef struct {
     const double *eta1;    /* [n_nodes] GD step per node, or NULL => 1/(2 a_i N + c_i) (R-8) */
     int32_t e2;            /* Alg. 3 steps (paper rule) */
     double eta2;           /* Alg. 3 step, 0 < eta2 rho < 2 */
+    double stop_tol;       /* 0: run exactly the requested iterations.  > 0: the stopping
+                              criterion of P:330 ("stopping criterion of 1e-6", R-13): after
+                              every iteration k the relative change
+                                r_k = max ||x^{k+1} - x^k||_2 / ||x^{k+1}||_2   (0/0 := 0)
+                              over the iterates -- graph rule: every node's private x_i; paper /
+                              consensus rule: the consensus x of every slice -- maximised over
+                              ranks; the run stops after the first iteration with r_k <= stop_tol.
+                              Every iteration then synchronises the host (tq_run_async becomes
+                              blocking).  tq_stats.iters_last_run / rel_change_last report it. */
 } tq_params;
 
 typedef struct {
@@ -107,6 +122,16 @@ typedef struct {
     int64_t nccl_bytes_recv;
     int64_t kernel_launches;       /* kernels launched by the last tq_run (all iterations) */
     double ms_last_run;            /* device time of the last tq_run (CUDA events) */
+    int64_t iters_last_run;        /* iterations the last run performed (fewer than requested
+                                      when tq_params.stop_tol stopped it) */
+    double rel_change_last;        /* r_k of the last iteration (stop_tol > 0), else -1 */
+    int32_t phase_valid;           /* 1: phase_ms holds the last run's phases (tq_set_profiling) */
+    int32_t pad_;
+    double phase_ms[4];            /* device ms of the last run, summed over its iterations:
+                                      [0] inner solves (A3: the E1 CG / GD steps of every local
+                                      node; plus Alg. 3 / the consensus partial sums and their
+                                      cross-rank reduction), [1] encode (A5 / A6 quantizers),
+                                      [2] exchange (A7), [3] decode + dual / next b' (A4) */
 } tq_stats;
 
 /* ---------------------------------------------------------------- context API */
@@ -196,6 +221,19 @@ tq_status tq_launch_component(tq_ctx *ctx, int32_t component, int32_t reps, void
                               int64_t *units);
 
 tq_status tq_get_stats(const tq_ctx *ctx, tq_stats *out);
+/* Phase timing (tq_stats.phase_ms): on = 1 makes later runs launch each phase as its own CUDA
+ * graph with timing events in between (slightly slower than the default whole-iteration
+ * graph; off by default).  Waits for an enqueued run. */
+tq_status tq_set_profiling(tq_ctx *ctx, int32_t on);
+/* Bytes one local node (slice, node) sent and received in the last iteration, as the method
+ * moves them (the per-node communication of P:248-252, independent of where nodes are placed):
+ * graph rule: sent = deg_i x its payload, received = the sum of its neighbours' payloads;
+ * paper rule: sent = (M-1) x its segment payload, received = the other M-1 segment payloads
+ * (with TQ_Q_NONE: sent + received = 2 (M-1)/M X, X = the image bytes); consensus rule:
+ * the paper rule's segment traffic plus the fp64 partial sums (8 B per element) of the other
+ * nodes' segments sent to their owners and received from the other M-1 nodes for its own.
+ * Entropy-coded DCT payloads count their coded size (header included).  Waits for a run. */
+tq_status tq_get_node_bytes(tq_ctx *ctx, int32_t slice, int32_t node, int64_t *sent, int64_t *recv);
 const char *tq_last_error(const tq_ctx *ctx);
 const char *tq_last_error_global(void);
 void tq_destroy(tq_ctx *ctx);

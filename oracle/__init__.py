@@ -47,6 +47,10 @@ def lib():
         L = C.CDLL(build())
         L.or_angles.argtypes = [C.c_int, _dp, _dp, _dp, _ip, _dp]
         L.or_project.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _dp, _dp]
+        L.or_project_t.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, _ip, _dp, _dp]
+        L.or_backproject_t.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, _ip, _dp, _dp]
+        L.or_project_siddon_t.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, _ip, _dp, _dp]
+        L.or_backproject_siddon_t.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, _ip, _dp, _dp]
         L.or_backproject.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _dp, _dp]
         L.or_gd.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _dp, _dp, C.c_double,
                             C.c_double, C.c_int, _dp]
@@ -72,7 +76,8 @@ def lib():
         L.or_admm_run.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip, C.c_int, _ip,
                                   C.c_int, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int,
                                   C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, _dp, C.c_int,
-                                  _dp, _dp, _dp, C.c_int, C.c_int]
+                                  _dp, _dp, _dp, C.c_int, C.c_int, C.c_void_p, C.c_double,
+                                  C.POINTER(C.c_int), C.POINTER(C.c_double)]
         L.or_alg3.restype = C.c_double
         L.or_alg3.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int]
         L.or_memory_model.restype = C.c_double
@@ -103,43 +108,56 @@ def angles(n_ang: int):
     return th, cs, sn, xm, m
 
 
-def project(img, n_ang: int, n_det: int, sel=None):
-    """A img for the selected angles (Eq. 2, Joseph discretisation)."""
+def _theta(theta, n_ang):
+    if theta is None:
+        return None, None
+    t = _f64(theta).ravel()
+    assert t.size == n_ang
+    return t.ctypes.data, t
+
+
+def project(img, n_ang: int, n_det: int, sel=None, theta=None):
+    """A img for the selected angles (Eq. 2, Joseph discretisation).
+    theta: explicit angles in radians (None: pi a / n_ang)."""
     img = _f64(img)
     N = img.shape[0]
     sel = _i32(np.arange(n_ang) if sel is None else sel)
     out = np.zeros((len(sel), n_det))
-    lib().or_project(N, n_det, n_ang, len(sel), sel, img, out)
+    tp, _keep = _theta(theta, n_ang)
+    lib().or_project_t(N, n_det, n_ang, tp, len(sel), sel, img, out)
     return out
 
 
-def project_siddon(img, n_ang: int, n_det: int, sel=None):
+def project_siddon(img, n_ang: int, n_det: int, sel=None, theta=None):
     """A img with P_ji = length of ray j inside pixel i (Siddon's
     algorithm, R-26)."""
     img = _f64(img)
     N = img.shape[0]
     sel = _i32(np.arange(n_ang) if sel is None else sel)
     out = np.zeros((len(sel), n_det))
-    lib().or_project_siddon(N, n_det, n_ang, len(sel), sel, img, out)
+    tp, _keep = _theta(theta, n_ang)
+    lib().or_project_siddon_t(N, n_det, n_ang, tp, len(sel), sel, img, out)
     return out
 
 
-def backproject_siddon(sino, N: int, n_ang: int, sel=None):
+def backproject_siddon(sino, N: int, n_ang: int, sel=None, theta=None):
     sino = _f64(sino)
     sel = _i32(np.arange(n_ang) if sel is None else sel)
     n_det = sino.shape[-1]
     out = np.zeros((N, N))
-    lib().or_backproject_siddon(N, n_det, n_ang, len(sel), sel, sino.reshape(len(sel), n_det), out)
+    tp, _keep = _theta(theta, n_ang)
+    lib().or_backproject_siddon_t(N, n_det, n_ang, tp, len(sel), sel, sino.reshape(len(sel), n_det), out)
     return out
 
 
-def backproject(sino, N: int, n_ang: int, sel=None):
+def backproject(sino, N: int, n_ang: int, sel=None, theta=None):
     """A^T sino (the transpose in Alg. 1/2)."""
     sino = _f64(sino)
     sel = _i32(np.arange(n_ang) if sel is None else sel)
     n_det = sino.shape[-1]
     out = np.zeros((N, N))
-    lib().or_backproject(N, n_det, n_ang, len(sel), sel, sino.reshape(len(sel), n_det), out)
+    tp, _keep = _theta(theta, n_ang)
+    lib().or_backproject_t(N, n_det, n_ang, tp, len(sel), sel, sino.reshape(len(sel), n_det), out)
     return out
 
 
@@ -279,9 +297,12 @@ class OracleADMM:
 
     def __init__(self, N, n_det, n_ang, M, edges, sino_full, split_contig, rule=0, inner=1,
                  e1=5, rho=1.0, eta1=None, e2=10, eta2=0.2, qkind=0, K=16, lloyd=10,
-                 quality=50, threads=1, projector=0):
+                 quality=50, threads=1, projector=0, theta=None, stop_tol=0.0):
         self.N, self.n_det, self.n_ang, self.M = N, n_det, n_ang, M
         self.projector = projector  # 0 Joseph (R-1), 1 Siddon (R-26, NEXT-3)
+        self.theta = None if theta is None else _f64(theta).ravel()  # explicit angles (radians)
+        self.stop_tol = float(stop_tol)  # P:330 stopping criterion (R-13); 0 = fixed count
+        self.last_change = -1.0
         if qkind == 2:  # the DCT codec works on whole 8x8 blocks (R-18)
             rows = N // M if rule in (1, 2) else N
             if N % 8 or rows % 8 or (rule in (1, 2) and N % M):
@@ -306,13 +327,17 @@ class OracleADMM:
         self.bytes_per_iter = 0
 
     def run(self, iters: int):
+        done, change = C.c_int(0), C.c_double(-1.0)
         self.bytes_per_iter = lib().or_admm_run(
             self.N, self.n_det, self.n_ang, self.M, self.off, self.idx, self.n_edges, self.edges,
             self.rule, self.inner, self.e1, self.rho,
             None if self.eta1 is None else self.eta1.ctypes.data, self.e2, self.eta2,
             self.qkind, self.K, self.lloyd, self.quality, self.d, iters, self.X, self.L, self.XH,
-            self.threads, self.projector)
-        self.iters += iters
+            self.threads, self.projector, None if self.theta is None else self.theta.ctypes.data,
+            self.stop_tol, C.byref(done), C.byref(change))
+        self.iters += done.value
+        self.last_run_iters = done.value
+        self.last_change = change.value
         return self
 
     def image(self):

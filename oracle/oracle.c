@@ -34,6 +34,18 @@
  * Major axis (R-3): x-major iff 4a >= n_ang and 4a <= 3 n_ang; m_a = |sin| if
  * x-major else |cos|.
  */
+/* The trig of angle a: theta_a = pi a / n_ang with the integer major-axis rule when theta is
+ * NULL, else the explicit list theta[] (radians in [0, pi)) with x-major iff |sin| >= |cos|
+ * (R-3 for explicit lists). */
+static void joseph_trig(int a, int n_ang, const double *theta, double *cs, double *sn, int *xm)
+{
+    double th = theta ? theta[a] : M_PI * (double)a / (double)n_ang;
+    *cs = cos(th);
+    *sn = sin(th);
+    if (theta) *xm = fabs(*sn) >= fabs(*cs);
+    else *xm = (4 * a >= n_ang && 4 * a <= 3 * n_ang);
+}
+
 void or_angles(int n_ang, double *theta, double *cs, double *sn, int *xmajor, double *m)
 {
     for (int a = 0; a < n_ang; a++) {
@@ -53,15 +65,15 @@ void or_angles(int n_ang, double *theta, double *cs, double *sn, int *xmajor, do
  * (the ray length per line).  Taps outside the grid are zero.
  * img: N*N row-major (row 0 = top).  sino: n_sel x n_det, row k = angle sel[k].
  */
-void or_project(int N, int n_det, int n_ang, int n_sel, const int *sel,
-                const double *img, double *sino)
+void or_project_t(int N, int n_det, int n_ang, const double *theta, int n_sel, const int *sel,
+                  const double *img, double *sino)
 {
     double half = 0.5 * (double)(N - 1);
     for (int k = 0; k < n_sel; k++) {
         int a = sel[k];
-        double th = M_PI * (double)a / (double)n_ang;
-        double cs = cos(th), sn = sin(th);
-        int xm = (4 * a >= n_ang && 4 * a <= 3 * n_ang);
+        double cs, sn;
+        int xm;
+        joseph_trig(a, n_ang, theta, &cs, &sn, &xm);
         for (int j = 0; j < n_det; j++) {
             double t = (double)j - 0.5 * (double)(n_det - 1);
             double acc = 0.0;
@@ -102,17 +114,17 @@ void or_project(int N, int n_det, int n_ang, int n_sel, const int *sel,
  * Pixel-driven: every bin within distance 2 of t_p is visited (all but <= 2 weights
  * are zero).
  */
-void or_backproject(int N, int n_det, int n_ang, int n_sel, const int *sel,
-                    const double *sino, double *img)
+void or_backproject_t(int N, int n_det, int n_ang, const double *theta, int n_sel, const int *sel,
+                      const double *sino, double *img)
 {
     double half = 0.5 * (double)(N - 1);
     double t0 = -0.5 * (double)(n_det - 1);
     for (size_t p = 0; p < (size_t)N * N; p++) img[p] = 0.0;
     for (int k = 0; k < n_sel; k++) {
         int a = sel[k];
-        double th = M_PI * (double)a / (double)n_ang;
-        double cs = cos(th), sn = sin(th);
-        int xm = (4 * a >= n_ang && 4 * a <= 3 * n_ang);
+        double cs, sn;
+        int xm;
+        joseph_trig(a, n_ang, theta, &cs, &sn, &xm);
         double m = xm ? fabs(sn) : fabs(cs);
         for (int r = 0; r < N; r++) {
             for (int c = 0; c < N; c++) {
@@ -143,8 +155,14 @@ void or_backproject(int N, int n_det, int n_ang, int n_sel, const int *sel,
  * mean of the two one-sided limits; pixels outside the grid are absent).
  * Ray (theta, t): P(alpha) = t (cos, sin) + alpha (-sin, cos), unit speed.
  */
-static void siddon_trig(int a, int n_ang, double *cs, double *sn)
+static void siddon_trig(int a, int n_ang, const double *theta, double *cs, double *sn)
 {
+    if (theta) { /* explicit list: exact at theta == 0 and theta == fl64(pi/2) */
+        if (theta[a] == 0.0) { *cs = 1.0; *sn = 0.0; return; }
+        if (theta[a] == M_PI / 2) { *cs = 0.0; *sn = 1.0; return; }
+        *cs = cos(theta[a]); *sn = sin(theta[a]);
+        return;
+    }
     if (a == 0) { *cs = 1.0; *sn = 0.0; return; }
     if (2 * a == n_ang) { *cs = 0.0; *sn = 1.0; return; }
     double th = M_PI * (double)a / (double)n_ang;
@@ -204,13 +222,14 @@ static int siddon_ray(int N, double cs, double sn, double t, int *pix, double *l
     return cnt;
 }
 
-void or_project_siddon(int N, int n_det, int n_ang, int n_sel, const int *sel, const double *img, double *sino)
+void or_project_siddon_t(int N, int n_det, int n_ang, const double *theta, int n_sel, const int *sel,
+                         const double *img, double *sino)
 {
     int *pix = malloc(sizeof(int) * (size_t)(4 * N + 8));
     double *len = malloc(sizeof(double) * (size_t)(4 * N + 8)), *al = malloc(sizeof(double) * (size_t)(2 * N + 8));
     for (int k = 0; k < n_sel; k++) {
         double cs, sn;
-        siddon_trig(sel[k], n_ang, &cs, &sn);
+        siddon_trig(sel[k], n_ang, theta, &cs, &sn);
         for (int j = 0; j < n_det; j++) {
             double t = (double)j - 0.5 * (double)(n_det - 1);
             int cnt = siddon_ray(N, cs, sn, t, pix, len, al);
@@ -222,14 +241,15 @@ void or_project_siddon(int N, int n_det, int n_ang, int n_sel, const int *sel, c
     free(pix); free(len); free(al);
 }
 
-void or_backproject_siddon(int N, int n_det, int n_ang, int n_sel, const int *sel, const double *sino, double *img)
+void or_backproject_siddon_t(int N, int n_det, int n_ang, const double *theta, int n_sel, const int *sel,
+                             const double *sino, double *img)
 {
     int *pix = malloc(sizeof(int) * (size_t)(4 * N + 8));
     double *len = malloc(sizeof(double) * (size_t)(4 * N + 8)), *al = malloc(sizeof(double) * (size_t)(2 * N + 8));
     for (size_t p = 0; p < (size_t)N * N; p++) img[p] = 0.0;
     for (int k = 0; k < n_sel; k++) {
         double cs, sn;
-        siddon_trig(sel[k], n_ang, &cs, &sn);
+        siddon_trig(sel[k], n_ang, theta, &cs, &sn);
         for (int j = 0; j < n_det; j++) {
             double t = (double)j - 0.5 * (double)(n_det - 1);
             int cnt = siddon_ray(N, cs, sn, t, pix, len, al);
@@ -239,16 +259,35 @@ void or_backproject_siddon(int N, int n_det, int n_ang, int n_sel, const int *se
     free(pix); free(len); free(al);
 }
 
-/* the projector of a run: 0 Joseph (R-1), 1 Siddon (R-26) */
-static void fwd(int proj, int N, int n_det, int n_ang, int n_sel, const int *sel, const double *img, double *sino)
+void or_project(int N, int n_det, int n_ang, int n_sel, const int *sel, const double *img, double *sino)
 {
-    if (proj == 1) or_project_siddon(N, n_det, n_ang, n_sel, sel, img, sino);
-    else or_project(N, n_det, n_ang, n_sel, sel, img, sino);
+    or_project_t(N, n_det, n_ang, NULL, n_sel, sel, img, sino);
 }
-static void bwd(int proj, int N, int n_det, int n_ang, int n_sel, const int *sel, const double *sino, double *img)
+void or_backproject(int N, int n_det, int n_ang, int n_sel, const int *sel, const double *sino, double *img)
 {
-    if (proj == 1) or_backproject_siddon(N, n_det, n_ang, n_sel, sel, sino, img);
-    else or_backproject(N, n_det, n_ang, n_sel, sel, sino, img);
+    or_backproject_t(N, n_det, n_ang, NULL, n_sel, sel, sino, img);
+}
+void or_project_siddon(int N, int n_det, int n_ang, int n_sel, const int *sel, const double *img, double *sino)
+{
+    or_project_siddon_t(N, n_det, n_ang, NULL, n_sel, sel, img, sino);
+}
+void or_backproject_siddon(int N, int n_det, int n_ang, int n_sel, const int *sel, const double *sino, double *img)
+{
+    or_backproject_siddon_t(N, n_det, n_ang, NULL, n_sel, sel, sino, img);
+}
+
+/* the projector of a run: 0 Joseph (R-1), 1 Siddon (R-26); theta NULL = uniform angles */
+static void fwd(int proj, int N, int n_det, int n_ang, const double *theta, int n_sel, const int *sel,
+                const double *img, double *sino)
+{
+    if (proj == 1) or_project_siddon_t(N, n_det, n_ang, theta, n_sel, sel, img, sino);
+    else or_project_t(N, n_det, n_ang, theta, n_sel, sel, img, sino);
+}
+static void bwd(int proj, int N, int n_det, int n_ang, const double *theta, int n_sel, const int *sel,
+                const double *sino, double *img)
+{
+    if (proj == 1) or_backproject_siddon_t(N, n_det, n_ang, theta, n_sel, sel, sino, img);
+    else or_backproject_t(N, n_det, n_ang, theta, n_sel, sel, sino, img);
 }
 
 /* ------------------------------------------------------------------ vectors */
@@ -268,15 +307,15 @@ static double dot(size_t n, const double *a, const double *b)
 
 /* Alg. 2: E1 gradient steps  Delta = A^T(A u - d) + c u - b', u -= eta Delta,
  * warm-started from the input u (R-9). */
-void or_gd_p(int proj, int N, int n_det, int n_ang, int n_sel, const int *sel, const double *d,
+void or_gd_p(int proj, int N, int n_det, int n_ang, const double *theta, int n_sel, const int *sel, const double *d,
              const double *bprime, double c, double eta, int e1, double *u)
 {
     size_t n = (size_t)N * N, l = (size_t)n_sel * n_det;
     double *s = malloc(l * sizeof(double)), *g = malloc(n * sizeof(double));
     for (int it = 0; it < e1; it++) {
-        fwd(proj, N, n_det, n_ang, n_sel, sel, u, s);
+        fwd(proj, N, n_det, n_ang, theta, n_sel, sel, u, s);
         for (size_t i = 0; i < l; i++) s[i] = s[i] - d[i];
-        bwd(proj, N, n_det, n_ang, n_sel, sel, s, g);
+        bwd(proj, N, n_det, n_ang, theta, n_sel, sel, s, g);
         for (size_t i = 0; i < n; i++) {
             double delta = g[i] + c * u[i] - bprime[i];
             u[i] = u[i] - eta * delta;
@@ -291,21 +330,21 @@ void or_gd_p(int proj, int N, int n_det, int n_ang, int n_sel, const int *sel, c
  *   repeat E1: q = A^T(A p) + c p; alpha = rr/(p.q); x += alpha p; r -= alpha q;
  *              beta = rr'/rr; p = r + beta p.
  * Guards (R-8): alpha = 0 if p.q <= 0; beta = 0 if rr == 0. */
-void or_cg_p(int proj, int N, int n_det, int n_ang, int n_sel, const int *sel, const double *d,
+void or_cg_p(int proj, int N, int n_det, int n_ang, const double *theta, int n_sel, const int *sel, const double *d,
              const double *bprime, double c, int e1, double *x)
 {
     size_t n = (size_t)N * N, l = (size_t)n_sel * n_det;
     double *s = malloc(l * sizeof(double));
     double *r = malloc(n * sizeof(double)), *p = malloc(n * sizeof(double));
     double *q = malloc(n * sizeof(double));
-    fwd(proj, N, n_det, n_ang, n_sel, sel, x, s);
+    fwd(proj, N, n_det, n_ang, theta, n_sel, sel, x, s);
     for (size_t i = 0; i < l; i++) s[i] = d[i] - s[i];
-    bwd(proj, N, n_det, n_ang, n_sel, sel, s, r);
+    bwd(proj, N, n_det, n_ang, theta, n_sel, sel, s, r);
     for (size_t i = 0; i < n; i++) { r[i] = r[i] + bprime[i] - c * x[i]; p[i] = r[i]; }
     double rr = dot(n, r, r);
     for (int it = 0; it < e1; it++) {
-        fwd(proj, N, n_det, n_ang, n_sel, sel, p, s);
-        bwd(proj, N, n_det, n_ang, n_sel, sel, s, q);
+        fwd(proj, N, n_det, n_ang, theta, n_sel, sel, p, s);
+        bwd(proj, N, n_det, n_ang, theta, n_sel, sel, s, q);
         for (size_t i = 0; i < n; i++) q[i] = q[i] + c * p[i];
         double pq = dot(n, p, q);
         double alpha = pq > 0.0 ? rr / pq : 0.0;
@@ -321,12 +360,12 @@ void or_cg_p(int proj, int N, int n_det, int n_ang, int n_sel, const int *sel, c
 void or_gd(int N, int n_det, int n_ang, int n_sel, const int *sel, const double *d,
            const double *bprime, double c, double eta, int e1, double *u)
 {
-    or_gd_p(0, N, n_det, n_ang, n_sel, sel, d, bprime, c, eta, e1, u);
+    or_gd_p(0, N, n_det, n_ang, NULL, n_sel, sel, d, bprime, c, eta, e1, u);
 }
 void or_cg(int N, int n_det, int n_ang, int n_sel, const int *sel, const double *d,
            const double *bprime, double c, int e1, double *x)
 {
-    or_cg_p(0, N, n_det, n_ang, n_sel, sel, d, bprime, c, e1, x);
+    or_cg_p(0, N, n_det, n_ang, NULL, n_sel, sel, d, bprime, c, e1, x);
 }
 
 /* ------------------------------------------------------------------ K-means (Alg. 5)
@@ -847,6 +886,7 @@ typedef struct {
     int e2; double eta2;
     int qkind, K, lloyd, quality;
     int proj;                        /* 0 Joseph (R-1), 1 Siddon (R-26) */
+    const double *theta;             /* explicit angles (radians) or NULL: pi a / n_ang */
 } or_problem;
 
 /* Alg. 3 for one element of the owned segment x[m]:
@@ -875,20 +915,40 @@ static void local_solve(const or_problem *P, int m, const double *dm, const doub
 {
     int na = P->off[m + 1] - P->off[m];
     const int *sel = P->idx + P->off[m];
-    if (P->inner == 1) or_cg_p(P->proj, P->N, P->n_det, P->n_ang, na, sel, dm, bp, c, P->e1, x);
+    if (P->inner == 1) or_cg_p(P->proj, P->N, P->n_det, P->n_ang, P->theta, na, sel, dm, bp, c, P->e1, x);
     else {
         double eta = P->eta1 ? P->eta1[m] : 1.0 / (2.0 * na * P->N + c);
-        or_gd_p(P->proj, P->N, P->n_det, P->n_ang, na, sel, dm, bp, c, eta, P->e1, x);
+        or_gd_p(P->proj, P->N, P->n_det, P->n_ang, P->theta, na, sel, dm, bp, c, eta, P->e1, x);
     }
 }
 
+/* The stopping test of P:330 ("stopping criterion of 1e-6"; R-13): the relative
+ * change ||x^{k+1} - x^k|| / ||x^{k+1}|| of the iterate (0/0 := 0), maximised over the
+ * iterates compared (graph rule: every node's private x_i; paper / consensus: x). */
+static double rel_change(const double *cur, const double *prev, size_t n)
+{
+    double dd = 0.0, xx = 0.0;
+    for (size_t p = 0; p < n; p++) {
+        double e = cur[p] - prev[p];
+        dd += e * e;
+        xx += cur[p] * cur[p];
+    }
+    if (dd == 0.0) return 0.0;
+    return xx > 0.0 ? sqrt(dd / xx) : INFINITY;
+}
+
+/* stop_tol > 0: stop after the first iteration whose relative change is <= stop_tol;
+ * *iters_done (if not NULL) = iterations performed; *last_change = the last test value. */
 long or_admm_run(int N, int n_det, int n_ang, int M, const int32_t *off, const int32_t *idx,
                  int n_edges, const int32_t *edges, int rule, int inner, int e1, double rho,
                  const double *eta1, int e2, double eta2, int qkind, int K, int lloyd, int quality,
-                 const double *d, int iters, double *X, double *L, double *XH, int threads, int proj)
+                 const double *d, int iters, double *X, double *L, double *XH, int threads, int proj,
+                 const double *theta, double stop_tol, int *iters_done, double *last_change)
 {
     or_problem P = {N, n_det, n_ang, M, off, idx, n_edges, edges, rule, inner, e1, rho, eta1,
-                    e2, eta2, qkind, K, lloyd, quality, proj};
+                    e2, eta2, qkind, K, lloyd, quality, proj, theta};
+    int done = 0;
+    double change = -1.0;
     size_t n = (size_t)N * N;
     int *deg = calloc((size_t)M, sizeof(int)), *nb = calloc((size_t)M * M, sizeof(int));
     adjacency(&P, deg, nb);
@@ -904,7 +964,9 @@ long or_admm_run(int N, int n_det, int n_ang, int M, const int32_t *off, const i
 #endif
     if (rule == 0) {
         double *S = malloc((size_t)M * n * sizeof(double));
+        double *XP = stop_tol > 0.0 ? malloc((size_t)M * n * sizeof(double)) : NULL;
         for (int k = 0; k < iters; k++) {
+            if (XP) memcpy(XP, X, (size_t)M * n * sizeof(double));
             /* b'_i from the public values of iteration k */
             for (int i = 0; i < M; i++) {
                 for (size_t p = 0; p < n; p++) {
@@ -931,13 +993,23 @@ long or_admm_run(int N, int n_det, int n_ang, int M, const int32_t *off, const i
             for (int i = 0; i < M; i++)
                 for (size_t p = 0; p < n; p++)
                     L[(size_t)i * n + p] += rho * ((double)deg[i] * XH[(size_t)i * n + p] - S[(size_t)i * n + p]);
+            done = k + 1;
+            if (XP) {
+                change = 0.0;
+                for (int i = 0; i < M; i++)
+                    change = fmax(change, rel_change(X + (size_t)i * n, XP + (size_t)i * n, n));
+                if (change <= stop_tol) break;
+            }
         }
         free(S);
+        free(XP);
     } else {
         int32_t *roff = malloc((size_t)(M + 1) * sizeof(int32_t));
         or_partition_rows(N, M, roff);
         double *XN = malloc(n * sizeof(double));
+        double *XP = stop_tol > 0.0 ? malloc(n * sizeof(double)) : NULL;
         for (int k = 0; k < iters; k++) {
+            if (XP) memcpy(XP, XH, n * sizeof(double));
             for (int m = 0; m < M; m++)
                 for (size_t p = 0; p < n; p++)
                     BP[(size_t)m * n + p] = rho * XH[p] - L[(size_t)m * n + p];
@@ -966,9 +1038,16 @@ long or_admm_run(int N, int n_det, int n_ang, int M, const int32_t *off, const i
             for (int m = 0; m < M; m++)
                 for (size_t p = 0; p < n; p++)
                     L[(size_t)m * n + p] += rho * (X[(size_t)m * n + p] - XH[p]);
+            done = k + 1;
+            if (XP) {
+                change = rel_change(XH, XP, n);
+                if (change <= stop_tol) break;
+            }
         }
-        free(roff); free(XN);
+        free(roff); free(XN); free(XP);
     }
+    if (iters_done) *iters_done = done;
+    if (last_change) *last_change = change;
     free(deg); free(nb); free(doff); free(BP);
     return bytes;
 }

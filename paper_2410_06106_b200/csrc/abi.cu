@@ -40,6 +40,7 @@ void check_geom(const tq_geometry *g) {
     TQ_REQUIRE(g->projector == TQ_PROJ_JOSEPH || g->projector == TQ_PROJ_SIDDON, "bad projector");
     TQ_REQUIRE((long long)g->n_det * g->n_det >= 2LL * g->image_side * g->image_side,
                "n_det must be >= ceil(N sqrt 2)");
+    check_angles(g->angles_rad, g->n_angles);
 }
 
 // device scratch released at scope exit
@@ -215,6 +216,22 @@ tq_status tq_get_stats(const tq_ctx *ctx, tq_stats *out) {
     return r;
 }
 
+tq_status tq_set_profiling(tq_ctx *ctx, int32_t on) {
+    if (!ctx) return TQ_EINVAL;
+    return guard(ctx, [&] { ctx->c.set_profiling(on != 0); });
+}
+
+tq_status tq_get_node_bytes(tq_ctx *ctx, int32_t slice, int32_t node, int64_t *sent, int64_t *recv) {
+    if (!ctx) return TQ_EINVAL;
+    return guard(ctx, [&] {
+        TQ_REQUIRE(sent && recv, "null output");
+        long long s = 0, r = 0;
+        ctx->c.node_bytes(slice, node, s, r);
+        *sent = s;
+        *recv = r;
+    });
+}
+
 const char *tq_last_error(const tq_ctx *ctx) { return ctx ? ctx->c.err.c_str() : g_err.c_str(); }
 const char *tq_last_error_global(void) { return g_err.c_str(); }
 
@@ -269,7 +286,7 @@ tq_status tq_project(const tq_geometry *g, const int32_t *sel, int32_t n_sel, co
         TQ_REQUIRE(img && sino && (precision == 0 || precision == 1), "bad arguments");
         std::vector<int> s = check_sel(g, sel, n_sel);
         DevGeom geo;
-        geo.init(g->image_side, g->n_angles, g->n_det, g->projector);
+        geo.init(g->image_side, g->n_angles, g->n_det, g->projector, g->angles_rad);
         Inner in;
         in.init(precision, geo, {s});
         cudaStream_t st = (cudaStream_t)stream;
@@ -287,7 +304,7 @@ tq_status tq_backproject(const tq_geometry *g, const int32_t *sel, int32_t n_sel
         TQ_REQUIRE(img && sino && (precision == 0 || precision == 1), "bad arguments");
         std::vector<int> s = check_sel(g, sel, n_sel);
         DevGeom geo;
-        geo.init(g->image_side, g->n_angles, g->n_det, g->projector);
+        geo.init(g->image_side, g->n_angles, g->n_det, g->projector, g->angles_rad);
         DevTmp t;
         std::vector<RayRow> rows;
         for (int k = 0; k < n_sel; k++) rows.push_back(RayRow{0, s[k], k, 0});
@@ -333,7 +350,7 @@ tq_status tq_local_solve(const tq_geometry *g, const int32_t *sel, int32_t n_sel
         TQ_REQUIRE(e1 >= 0 && c >= 0.0, "bad e1 / c");
         std::vector<int> s = check_sel(g, sel, n_sel);
         DevGeom geo;
-        geo.init(g->image_side, g->n_angles, g->n_det, g->projector);
+        geo.init(g->image_side, g->n_angles, g->n_det, g->projector, g->angles_rad);
         Inner in;
         in.init(precision, geo, {s});
         cudaStream_t st = (cudaStream_t)stream;

@@ -32,12 +32,14 @@ struct Error {
 
 // ---------------------------------------------------------------- geometry (host)
 // DESIGN.md R-1..R-3: theta_a = pi a / n_ang; x-major iff 4a in [n_ang, 3 n_ang];
-// m_a = |sin| (x-major) or |cos| (y-major).
+// m_a = |sin| (x-major) or |cos| (y-major).  Explicit angle lists: x-major iff |sin| >= |cos|.
 struct AngleHost {
     double cs, sn, m;
     int xmajor;
 };
-std::vector<AngleHost> make_angles(int n_ang);
+std::vector<AngleHost> make_angles(int n_ang, const double *angles_rad = nullptr);
+// explicit angle lists: every angle in [0, pi) (the half turn of P:315; a parallel ray set repeats after pi)
+void check_angles(const double *angles_rad, int n_ang);
 void partition_angles(int n_ang, int M, int split, std::vector<int> &off, std::vector<int> &idx);
 void partition_rows(int N, int M, std::vector<int> &row_off);
 

@@ -162,7 +162,8 @@ void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int ran
         TQ_CHECK_CUDA(cudaEventCreateWithFlags(&stage_free[b], cudaEventDisableTiming));
     }
     TQ_REQUIRE(g.projector == TQ_PROJ_JOSEPH || g.projector == TQ_PROJ_SIDDON, "bad projector");
-    geo.init(N, n_ang, n_det, g.projector);
+    check_angles(g.angles_rad, n_ang);
+    geo.init(N, n_ang, n_det, g.projector, g.angles_rad);
     in.init(prec, geo, angles);
     const size_t es = prec ? 8 : 4;
     TQ_CHECK_CUDA(cudaMalloc(&ALPHA, std::max<size_t>(16, es * n * L)));
@@ -184,6 +185,9 @@ void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int ran
 void Ctx::invalidate() {
     for (auto &g : segs) cudaGraphExecDestroy(g.exec);
     segs.clear();
+    for (auto &g : psegs) cudaGraphExecDestroy(g.exec);
+    psegs.clear();
+    free_stop_test();
     if (seg2.exec) cudaGraphExecDestroy(seg2.exec);
     seg2 = Seg{nullptr, 0, COMM_NONE};
 }
@@ -245,6 +249,8 @@ void Ctx::destroy() {
     tr.reset();
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    for (cudaEvent_t e : pev) cudaEventDestroy(e);
+    pev.clear();
     if (run_done) cudaEventDestroy(run_done);
     run_done = nullptr;
     if (gathers_done) cudaEventDestroy(gathers_done);
@@ -269,6 +275,7 @@ void Ctx::set_params(const tq_params &p) {
     TQ_REQUIRE(p.rho > 0.0 && std::isfinite(p.rho), "rho must be > 0");
     TQ_REQUIRE(p.inner == TQ_INNER_GD || p.inner == TQ_INNER_CG, "inner must be GD or CG");
     TQ_REQUIRE(p.e1 >= 0 && p.e1 <= 100000, "e1 out of range");
+    TQ_REQUIRE(p.stop_tol >= 0.0 && std::isfinite(p.stop_tol), "stop_tol must be finite and >= 0");
     if (rule == TQ_RULE_PAPER) {
         TQ_REQUIRE(p.e2 >= 0, "e2 must be >= 0");
         TQ_REQUIRE(p.eta2 * p.rho > 0.0 && p.eta2 * p.rho < 2.0, "need 0 < eta2 rho < 2 (Alg. 3 contraction)");
@@ -669,6 +676,43 @@ void Ctx::setup_exchange() {
     xready = true;
 }
 
+// Bytes node (slice, node) sent / received per iteration as the method moves them
+// (tq_get_node_bytes).  Entropy-coded DCT payloads: the coded sizes in their headers.
+void Ctx::node_bytes(int slice, int node, long long &sent, long long &recv) {
+    finish();
+    const int i = local(slice, node);
+    TQ_REQUIRE(i >= 0, "node is not local to this rank");
+    TQ_CHECK_CUDA(cudaSetDevice(device));
+    if (!xready) setup_exchange();
+    const size_t es = prec ? 8 : 4;
+    const bool seg = segmented();
+    auto seglen = [&](int m) { return (long long)(row_off[m + 1] - row_off[m]) * N; };
+    auto pay_bytes = [&](int m) -> long long {
+        const int kd = kind_of_slice(slice);
+        if (kd == TQ_Q_NONE) return (long long)es * (seg ? seglen(m) : n);
+        if (kd == TQ_Q_KMEANS) return kmeans_payload_bytes(q.k, payload_len);
+        if (q.jpeg_restart <= 0) return dct_payload_bytes(payload_len);
+        const Pay &p = pays[pay_of.at({slice, m})];  // [mn][mx][u32 bytes | raw bit 31][u32 blocks]
+        uint32_t w = 0;
+        TQ_CHECK_CUDA(cudaMemcpy(&w, p.buf + 8, sizeof w, cudaMemcpyDeviceToHost));
+        return 16 + ((w & 0x80000000u) ? 2 * payload_len : (long long)w);
+    };
+    sent = recv = 0;
+    if (!seg) {
+        const long long own = pay_bytes(node);
+        sent = own * (long long)adj[node].size();
+        for (int j : adj[node]) recv += pay_bytes(j);
+    } else {
+        sent = pay_bytes(node) * (M - 1);
+        for (int m = 0; m < M; m++)
+            if (m != node) recv += pay_bytes(m);
+        if (rule == TQ_RULE_CONSENSUS) {  // fp64 partial sums of the other segments / of its own
+            sent += 8LL * (n - seglen(node));
+            recv += 8LL * (M - 1) * seglen(node);
+        }
+    }
+}
+
 int Ctx::stage(int id, cudaStream_t s) {
     if (id == 2) return phase_b(s);
     int k = 0;
@@ -762,7 +806,7 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
         prepare_rhs(s);
         need_rhs = false;
     }
-    auto capture = [&](const std::vector<int> &ids, int comm_after) {
+    auto capture = [&](std::vector<Seg> &into, const std::vector<int> &ids, int comm_after) {
         cudaGraph_t g;
         TQ_CHECK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         int c = 0;
@@ -778,22 +822,28 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
         const cudaError_t e = cudaGraphInstantiate(&sg.exec, g, 0);
         cudaGraphDestroy(g);
         TQ_CHECK_CUDA(e);
-        segs.push_back(sg);
+        into.push_back(sg);
     };
+    const bool red = rule == TQ_RULE_CONSENSUS && world > 1;
+    const bool exch = has_exchange();
     if (segs.empty()) {
         // stages 0 | reduce | 1 | exchange | 2, merged where no communication separates them
-        const bool red = rule == TQ_RULE_CONSENSUS && world > 1;
-        const bool exch = has_exchange();
         std::vector<int> cur{0};
-        if (red) { capture(cur, COMM_REDUCE); cur.clear(); }
+        if (red) { capture(segs, cur, COMM_REDUCE); cur.clear(); }
         cur.push_back(1);
-        if (exch) { capture(cur, COMM_EXCHANGE); cur.clear(); }
+        if (exch) { capture(segs, cur, COMM_EXCHANGE); cur.clear(); }
         cur.push_back(2);
-        capture(cur, COMM_NONE);
+        capture(segs, cur, COMM_NONE);
     }
+    if (profiling && psegs.empty()) {  // one graph per phase, timing events in between
+        capture(psegs, {0}, red ? COMM_REDUCE : COMM_NONE);
+        capture(psegs, {1}, exch ? COMM_EXCHANGE : COMM_NONE);
+        capture(psegs, {2}, COMM_NONE);
+    }
+    const bool stop = prm.stop_tol > 0.0;
     // one rank without communication steps: a second graph holding MULTI iterations (built
     // with the first, i.e. during warm-up) cuts the graph-to-graph boundaries of long runs
-    if (segs.size() == 1 && segs[0].comm == COMM_NONE && !seg2.exec) {
+    if (!stop && !profiling && segs.size() == 1 && segs[0].comm == COMM_NONE && !seg2.exec) {
         cudaGraph_t g;
         TQ_CHECK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         int c = 0;
@@ -812,24 +862,117 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
     }
     int per_iter = 0;
     for (auto &g : segs) per_iter += g.launches;
+    if (profiling && (int)pev.size() < 5 * iters) {
+        const size_t old = pev.size();
+        pev.resize(5 * (size_t)iters);
+        for (size_t k = old; k < pev.size(); k++) TQ_CHECK_CUDA(cudaEventCreate(&pev[k]));
+    }
+    if (stop) setup_stop_test(s);
+    auto comm_step = [&](int comm) {
+        if (comm == COMM_REDUCE) reduce_sums(s);
+        else if (comm == COMM_EXCHANGE) exchange(s);
+    };
     TQ_CHECK_CUDA(cudaEventRecord(ev0, s));
-    int it0 = 0;
-    if (seg2.exec)
+    int it0 = 0, done = 0;
+    st.rel_change_last = -1.0;
+    if (seg2.exec && !stop && !profiling)
         for (; it0 + MULTI <= iters; it0 += MULTI) TQ_CHECK_CUDA(cudaGraphLaunch(seg2.exec, s));
-    for (int it = it0; it < iters; it++)
-        for (auto &g : segs) {
-            TQ_CHECK_CUDA(cudaGraphLaunch(g.exec, s));
-            if (g.comm == COMM_REDUCE) reduce_sums(s);
-            else if (g.comm == COMM_EXCHANGE) exchange(s);
+    done = it0;
+    for (int it = it0; it < iters; it++) {
+        if (profiling) {
+            cudaEvent_t *e = &pev[5 * (size_t)it];
+            TQ_CHECK_CUDA(cudaEventRecord(e[0], s));
+            TQ_CHECK_CUDA(cudaGraphLaunch(psegs[0].exec, s));
+            comm_step(psegs[0].comm);
+            TQ_CHECK_CUDA(cudaEventRecord(e[1], s));
+            TQ_CHECK_CUDA(cudaGraphLaunch(psegs[1].exec, s));
+            TQ_CHECK_CUDA(cudaEventRecord(e[2], s));
+            comm_step(psegs[1].comm);
+            TQ_CHECK_CUDA(cudaEventRecord(e[3], s));
+            TQ_CHECK_CUDA(cudaGraphLaunch(psegs[2].exec, s));
+            TQ_CHECK_CUDA(cudaEventRecord(e[4], s));
+        } else {
+            for (auto &g : segs) {
+                TQ_CHECK_CUDA(cudaGraphLaunch(g.exec, s));
+                comm_step(g.comm);
+            }
         }
+        done = it + 1;
+        if (stop) {
+            double r = stop_test(s);
+            if (world > 1) r = tr->allreduce_max(r, s);
+            st.rel_change_last = r;
+            if (r <= prm.stop_tol) break;
+        }
+    }
     TQ_CHECK_CUDA(cudaEventRecord(ev1, s));
     // CG with E1 >= 1 leaves ||x||^2 in the scalar table (its last step); otherwise compute it
-    if (!(iters > 0 && prm.inner == TQ_INNER_CG && prm.e1 >= 1)) in.norm2(s);
+    if (!(done > 0 && prm.inner == TQ_INNER_CG && prm.e1 >= 1)) in.norm2(s);
     TQ_CHECK_CUDA(cudaEventRecord(run_done, s));
-    st.iters += iters;
-    st.kernel_launches = (long long)iters * per_iter;
+    st.iters += done;
+    st.iters_last_run = done;
+    st.kernel_launches = (long long)done * per_iter + (stop ? done : 0);
+    st.phase_valid = 0;
     pending = true;
-    pending_iters = iters;
+    pending_iters = done;
+    prof_iters = profiling ? done : 0;
+}
+
+// tq_params.stop_tol: the iterates whose relative change is tested (graph rule: every local
+// node's private x_i; paper / consensus rules: the consensus x of every slice held here),
+// snapshotted at the start of each run
+void Ctx::setup_stop_test(cudaStream_t s) {
+    const bool seg = segmented();
+    const int V = seg ? S : L;
+    if (chg_V != V) {
+        const size_t es = prec ? 8 : 4;
+        auto A = [&](void **p, size_t bytes) {
+            TQ_CHECK_CUDA(cudaMalloc(p, std::max<size_t>(bytes, 16)));
+            TQ_CHECK_CUDA(cudaMemset(*p, 0, std::max<size_t>(bytes, 16)));
+            chg_owned.push_back(*p);
+        };
+        A(&XPREV, es * n * std::max(1, V));
+        A((void **)&chg_out, sizeof(double) * 2 * std::max(1, V));
+        A((void **)&chg_part, sizeof(double) * 2 * (size_t)vec_blocks(n) * std::max(1, V));
+        A((void **)&chg_cnt, sizeof(unsigned) * std::max(1, V));
+        std::vector<const void *> tab(std::max(1, V), nullptr);
+        for (int v = 0; v < V; v++) tab[v] = seg ? (const void *)((const uint8_t *)XG + es * n * v) : in.xrow(in.X, v);
+        A((void **)&chg_tab, sizeof(void *) * tab.size());
+        TQ_CHECK_CUDA(cudaMemcpy(chg_tab, tab.data(), sizeof(void *) * tab.size(), cudaMemcpyHostToDevice));
+        TQ_CHECK_CUDA(cudaMallocHost(&chg_host, sizeof(double) * 2 * std::max(1, V)));
+        chg_V = V;
+    }
+    const size_t es = prec ? 8 : 4;
+    if (seg) TQ_CHECK_CUDA(cudaMemcpyAsync(XPREV, XG, es * n * V, cudaMemcpyDeviceToDevice, s));
+    else if (V) TQ_CHECK_CUDA(cudaMemcpyAsync(XPREV, in.X, es * n * V, cudaMemcpyDeviceToDevice, s));
+}
+
+// r_k = max over the tested iterates of ||x^{k+1} - x^k|| / ||x^{k+1}|| (0/0 := 0); blocking
+double Ctx::stop_test(cudaStream_t s) {
+    launch_rel_change(prec, chg_tab, XPREV, n, chg_V, chg_out, chg_part, vec_blocks(n), chg_cnt, s);
+    if (chg_V) TQ_CHECK_CUDA(cudaMemcpyAsync(chg_host, chg_out, sizeof(double) * 2 * chg_V, cudaMemcpyDeviceToHost, s));
+    TQ_CHECK_CUDA(cudaStreamSynchronize(s));
+    double r = 0.0;
+    for (int v = 0; v < chg_V; v++) {
+        const double dd = chg_host[2 * v], xx = chg_host[2 * v + 1];
+        const double q = dd == 0.0 ? 0.0 : (xx > 0.0 ? sqrt(dd / xx) : INFINITY);
+        r = std::max(r, q);
+    }
+    return r;
+}
+
+void Ctx::free_stop_test() {
+    for (void *p : chg_owned) cudaFree(p);
+    chg_owned.clear();
+    if (chg_host) cudaFreeHost(chg_host);
+    chg_host = nullptr;
+    XPREV = nullptr; chg_out = chg_part = nullptr; chg_cnt = nullptr; chg_tab = nullptr;
+    chg_V = -1;
+}
+
+void Ctx::set_profiling(bool on) {
+    finish();
+    profiling = on;
 }
 
 // The host side of an enqueued run: wait for it, then its statistics and the divergence
@@ -845,6 +988,18 @@ void Ctx::finish() {
     float ms = 0.f;
     TQ_CHECK_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
     st.ms_last_run = ms;
+    if (prof_iters > 0) {  // per-phase device time of the profiled run
+        double ph[4] = {0, 0, 0, 0};
+        for (int it = 0; it < prof_iters; it++)
+            for (int k = 0; k < 4; k++) {
+                float t = 0.f;
+                TQ_CHECK_CUDA(cudaEventElapsedTime(&t, pev[5 * (size_t)it + k], pev[5 * (size_t)it + k + 1]));
+                ph[k] += t;
+            }
+        for (int k = 0; k < 4; k++) st.phase_ms[k] = ph[k];
+        st.phase_valid = 1;
+        prof_iters = 0;
+    }
     for (int i = 0; i < L; i++) {
         const double nrm = sqrt(norm_host[(size_t)i * S_NSLOT + S_NORM]);
         if (!(nrm <= 1e12)) fail(TQ_EDIVERGED, "node iterate norm exceeded 1e12 (diverged)");

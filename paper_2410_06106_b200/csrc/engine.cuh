@@ -97,6 +97,23 @@ struct Ctx {
     std::vector<Seg> segs;
     static constexpr int MULTI = 4;
     Seg seg2{nullptr, 0, COMM_NONE};  // world == 1: MULTI iterations in one graph
+    // tq_set_profiling: one graph per phase (inner | encode | decode + dual), events between
+    bool profiling = false;
+    std::vector<Seg> psegs;
+    std::vector<cudaEvent_t> pev;    // 5 per iteration of the profiled run
+    int prof_iters = 0;
+    void set_profiling(bool on);
+    // tq_params.stop_tol: previous iterates and the fp64 sums of the relative change
+    void *XPREV = nullptr;
+    double *chg_out = nullptr, *chg_part = nullptr, *chg_host = nullptr;
+    unsigned *chg_cnt = nullptr;
+    const void **chg_tab = nullptr;
+    int chg_V = -1;
+    std::vector<void *> chg_owned;
+    void setup_stop_test(cudaStream_t s);
+    double stop_test(cudaStream_t s);
+    void free_stop_test();
+    void node_bytes(int slice, int node, long long &sent, long long &recv);
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     tq_stats st{};
     std::string err;

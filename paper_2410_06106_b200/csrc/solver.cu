@@ -5,16 +5,18 @@
 
 namespace tq {
 
-void DevGeom::init(int N_, int n_ang_, int n_det_, int proj_) {
+void DevGeom::init(int N_, int n_ang_, int n_det_, int proj_, const double *angles_rad) {
     projector_setup();
     N = N_; n_ang = n_ang_; n_det = n_det_; proj = proj_;
     n = (long long)N * N;
-    std::vector<AngleHost> a = make_angles(n_ang);
+    std::vector<AngleHost> a = make_angles(n_ang, angles_rad);
     std::vector<double2> t(n_ang);
     std::vector<int> xm(n_ang);
     for (int i = 0; i < n_ang; i++) {
         t[i] = make_double2(a[i].cs, a[i].sn);
-        if (proj == 1 && 2 * i == n_ang) t[i] = make_double2(0.0, 1.0);  // R-26: exact trig at pi/2
+        // R-26: exact trig at pi/2 (uniform angles: 2a = n_ang; explicit: theta == fl64(pi/2))
+        const bool half_pi = angles_rad ? angles_rad[i] == M_PI / 2 : 2 * i == n_ang;
+        if (proj == 1 && half_pi) t[i] = make_double2(0.0, 1.0);
         xm[i] = a[i].xmajor;
     }
     TQ_CHECK_CUDA(cudaMalloc(&trig, sizeof(double2) * n_ang));
@@ -179,16 +181,23 @@ int Inner::norm2(cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------- host geometry
-std::vector<AngleHost> make_angles(int n_ang) {
+std::vector<AngleHost> make_angles(int n_ang, const double *angles_rad) {
     std::vector<AngleHost> a(n_ang);
     for (int i = 0; i < n_ang; i++) {
-        const double th = M_PI * (double)i / (double)n_ang;
+        const double th = angles_rad ? angles_rad[i] : M_PI * (double)i / (double)n_ang;
         a[i].cs = cos(th);
         a[i].sn = sin(th);
-        a[i].xmajor = (4 * i >= n_ang && 4 * i <= 3 * n_ang) ? 1 : 0;
+        if (angles_rad) a[i].xmajor = fabs(a[i].sn) >= fabs(a[i].cs) ? 1 : 0;  // R-3, explicit lists
+        else a[i].xmajor = (4 * i >= n_ang && 4 * i <= 3 * n_ang) ? 1 : 0;
         a[i].m = a[i].xmajor ? fabs(a[i].sn) : fabs(a[i].cs);
     }
     return a;
+}
+
+void check_angles(const double *angles_rad, int n_ang) {
+    if (!angles_rad) return;
+    for (int i = 0; i < n_ang; i++)
+        TQ_REQUIRE(angles_rad[i] >= 0.0 && angles_rad[i] < M_PI, "angles_rad: every angle must lie in [0, pi)");
 }
 
 void partition_angles(int n_ang, int M, int split, std::vector<int> &off, std::vector<int> &idx) {

@@ -16,7 +16,7 @@ struct DevGeom {
     double2 *trig = nullptr;  // [n_ang]
     int *xmaj = nullptr;      // [n_ang]
     std::vector<int> xmaj_h;
-    void init(int N, int n_ang, int n_det, int proj = 0);
+    void init(int N, int n_ang, int n_det, int proj = 0, const double *angles_rad = nullptr);
     void release();
 };
 

@@ -145,6 +145,48 @@ __global__ void __launch_bounds__(VT) norm2_kernel(const T *__restrict__ x, long
     }
 }
 
+// stop test of tq_params.stop_tol: for vector v, out[2v] = ||cur_v - prev_v||^2 and
+// out[2v+1] = ||cur_v||^2 (fixed-order fp64 sums), then prev_v = cur_v
+template <typename T>
+__global__ void __launch_bounds__(VT) rel_change_kernel(const void *const *cur_tab, T *__restrict__ prev,
+                                                        long long n, double *out, double *partial,
+                                                        int part_stride, unsigned *counter) {
+    __shared__ double red[VT / 32 + 1];
+    __shared__ bool last;
+    const int v = blockIdx.y;
+    const T *__restrict__ cur = (const T *)cur_tab[v];
+    T *__restrict__ pv = prev + (long long)v * n;
+    double dd = 0.0, xx = 0.0;
+    vec_loop(n,
+        [&](long long i) {
+            const Q4<T> c = ld4(cur + i), p = ld4(pv + i);
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const double d = (double)c.v[u] - (double)p.v[u];
+                dd += d * d;
+                xx += (double)c.v[u] * (double)c.v[u];
+            }
+            st4(pv + i, c);
+        },
+        [&](long long i) {
+            const double c = (double)cur[i], d = c - (double)pv[i];
+            dd += d * d;
+            xx += c * c;
+            pv[i] = cur[i];
+        });
+    const double bd = block_sum<VT>(dd, red);
+    const double bx = block_sum<VT>(xx, red);
+    double *part = partial + (long long)v * part_stride * 2;
+    if (threadIdx.x == 0) { part[2 * blockIdx.x] = bd; part[2 * blockIdx.x + 1] = bx; }
+    if (last_block_of_group(counter + v, gridDim.x, &last)) {
+        double sd = 0.0, sx = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += VT) { sd += __ldcg(part + 2 * b); sx += __ldcg(part + 2 * b + 1); }
+        sd = block_sum<VT>(sd, red);
+        sx = block_sum<VT>(sx, red);
+        if (threadIdx.x == 0) { out[2 * v] = sd; out[2 * v + 1] = sx; }
+    }
+}
+
 template <typename A, typename B>
 __global__ void convert_kernel(const A *src, B *dst, long long n) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -182,6 +224,17 @@ void launch_norm2(int prec, const void *x, long long n, int L, double *scal, dou
         norm2_kernel<float><<<grid, VT, 0, st>>>((const float *)x, n, scal, partial, part_stride, counter);
     else
         norm2_kernel<double><<<grid, VT, 0, st>>>((const double *)x, n, scal, partial, part_stride, counter);
+    TQ_CHECK_CUDA(cudaGetLastError());
+}
+
+void launch_rel_change(int prec, const void *const *cur_tab, void *prev, long long n, int V, double *out,
+                       double *partial, int part_stride, unsigned *counter, cudaStream_t st) {
+    if (V == 0) return;
+    dim3 grid(vec_blocks(n), V);
+    if (prec == 0)
+        rel_change_kernel<float><<<grid, VT, 0, st>>>(cur_tab, (float *)prev, n, out, partial, part_stride, counter);
+    else
+        rel_change_kernel<double><<<grid, VT, 0, st>>>(cur_tab, (double *)prev, n, out, partial, part_stride, counter);
     TQ_CHECK_CUDA(cudaGetLastError());
 }
 

@@ -21,5 +21,9 @@ void launch_norm2(int prec, const void *x, long long n, int L, double *scal, dou
 void launch_convert(int src_prec, const void *src, int dst_prec, void *dst, long long n,
                     cudaStream_t st);
 int vec_blocks(long long n);
+// tq_params.stop_tol: out[2v] = ||cur_tab[v] - prev_v||^2, out[2v+1] = ||cur_tab[v]||^2 (fp64,
+// fixed order), then prev_v = cur_tab[v]; prev [V][n]; partial [V][2 part_stride]; counter [V]
+void launch_rel_change(int prec, const void *const *cur_tab, void *prev, long long n, int V, double *out,
+                       double *partial, int part_stride, unsigned *counter, cudaStream_t st);
 
 }  // namespace tq

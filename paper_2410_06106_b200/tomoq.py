@@ -32,7 +32,17 @@ class TomoQError(RuntimeError):
 
 class Geometry(C.Structure):
     _fields_ = [("image_side", C.c_int32), ("n_angles", C.c_int32), ("n_det", C.c_int32),
-                ("projector", C.c_int32)]
+                ("projector", C.c_int32), ("angles_rad", C.POINTER(C.c_double))]
+
+
+def _geom(N, n_angles, n_det, projector, angles):
+    """Geometry + the array it points to (kept alive by the caller)."""
+    if angles is None:
+        return Geometry(N, n_angles, n_det, projector, None), None
+    a = np.ascontiguousarray(angles, np.float64)
+    if a.size != n_angles:
+        raise ValueError("angles: n_angles values expected")
+    return Geometry(N, n_angles, n_det, projector, a.ctypes.data_as(C.POINTER(C.c_double))), a
 
 
 class Graph(C.Structure):
@@ -42,7 +52,8 @@ class Graph(C.Structure):
 
 class Params(C.Structure):
     _fields_ = [("rho", C.c_double), ("inner", C.c_int32), ("e1", C.c_int32),
-                ("eta1", C.POINTER(C.c_double)), ("e2", C.c_int32), ("eta2", C.c_double)]
+                ("eta1", C.POINTER(C.c_double)), ("e2", C.c_int32), ("eta2", C.c_double),
+                ("stop_tol", C.c_double)]
 
 
 class Quant(C.Structure):
@@ -54,7 +65,8 @@ class Stats(C.Structure):
     _fields_ = [("iters", C.c_int64), ("local_nodes", C.c_int32), ("world", C.c_int32),
                 ("payload_bytes_logical", C.c_int64), ("nccl_bytes_sent", C.c_int64),
                 ("nccl_bytes_recv", C.c_int64), ("kernel_launches", C.c_int64),
-                ("ms_last_run", C.c_double)]
+                ("ms_last_run", C.c_double), ("iters_last_run", C.c_int64), ("rel_change_last", C.c_double),
+                ("phase_valid", C.c_int32), ("pad_", C.c_int32), ("phase_ms", C.c_double * 4)]
 
 
 _lib = None
@@ -76,6 +88,8 @@ _SIGS = {
     "tq_import_state": [_vp, _i32, _i32, _vp, _i64],
     "tq_export_labels": [_vp, _i32, _i32, _vp, _i64],
     "tq_get_stats": [_vp, C.POINTER(Stats)],
+    "tq_set_profiling": [_vp, _i32],
+    "tq_get_node_bytes": [_vp, _i32, _i32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
     "tq_launch_component": [_vp, _i32, _i32, _vp, C.POINTER(C.c_int64)],
     "tq_partition_angles": [_i32, _i32, _i32, _vp, _vp],
     "tq_exchange_plan": [C.POINTER(Graph), _i32, _i32, _vp, _i32, _vp, _vp, _i32, _vp],
@@ -186,10 +200,10 @@ class Context:
 
     def __init__(self, N, n_angles, n_det, n_nodes, edges, split=SPLIT_RR, rule=RULE_GRAPH,
                  n_slices=1, rank=0, world=1, nccl_id: bytes | None = None, precision=0,
-                 device=0, node_rank=None, projector=PROJ_JOSEPH):
+                 device=0, node_rank=None, projector=PROJ_JOSEPH, angles=None):
         self.N, self.n = N, N * N
         self.precision = precision
-        geom = Geometry(N, n_angles, n_det, projector)
+        geom, _keep_angles = _geom(N, n_angles, n_det, projector, angles)
         g, self._keep = _graph(n_nodes, edges, split, rule, node_rank)
         h = C.c_void_p()
         idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id else None
@@ -201,10 +215,10 @@ class Context:
     def _c(self, code):
         _check(code, self.h)
 
-    def set_params(self, rho, inner=INNER_CG, e1=5, eta1=None, e2=10, eta2=0.2):
+    def set_params(self, rho, inner=INNER_CG, e1=5, eta1=None, e2=10, eta2=0.2, stop_tol=0.0):
         self._eta1 = None if eta1 is None else np.ascontiguousarray(eta1, np.float64)
         p = Params(rho, inner, e1, self._eta1.ctypes.data_as(C.POINTER(C.c_double)) if eta1 is not None else None,
-                   e2, eta2)
+                   e2, eta2, stop_tol)
         self._c(lib().tq_set_params(self.h, C.byref(p)))
 
     def set_quantizer(self, kind, k=16, lloyd=10, quality=50, keep_labels=False, jpeg_restart=0):
@@ -284,7 +298,18 @@ class Context:
     def stats(self) -> dict:
         s = Stats()
         self._c(lib().tq_get_stats(self.h, C.byref(s)))
-        return {f: getattr(s, f) for f, _ in Stats._fields_}
+        out = {f: getattr(s, f) for f, _ in Stats._fields_ if f != "pad_"}
+        out["phase_ms"] = list(s.phase_ms)
+        return out
+
+    def set_profiling(self, on=True):
+        self._c(lib().tq_set_profiling(self.h, int(bool(on))))
+
+    def node_bytes(self, slice_, node):
+        """(sent, received) bytes of a local node in the last iteration (tq_get_node_bytes)."""
+        a, b = C.c_int64(), C.c_int64()
+        self._c(lib().tq_get_node_bytes(self.h, slice_, node, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def close(self):
         if getattr(self, "h", None):
@@ -308,23 +333,23 @@ def _prec(t):
     raise TypeError("float32 or float64 tensors only")
 
 
-def project(img, n_angles, n_det, sel=None, stream=None, projector=PROJ_JOSEPH):
+def project(img, n_angles, n_det, sel=None, stream=None, projector=PROJ_JOSEPH, angles=None):
     """A img for the selected angles; img: CUDA tensor N x N (fp32/fp64)."""
     import torch
     N = img.shape[-1]
     sel = _i32arr(np.arange(n_angles) if sel is None else sel)
     out = torch.empty((len(sel), n_det), dtype=img.dtype, device=img.device)
-    g = Geometry(N, n_angles, n_det, projector)
+    g, _keep = _geom(N, n_angles, n_det, projector, angles)
     _check(lib().tq_project(C.byref(g), sel.ctypes.data, len(sel), img.contiguous().data_ptr(),
                             out.data_ptr(), _prec(img), _stream(stream)))
     return out
 
 
-def backproject(sino, N, n_angles, sel=None, stream=None, projector=PROJ_JOSEPH):
+def backproject(sino, N, n_angles, sel=None, stream=None, projector=PROJ_JOSEPH, angles=None):
     import torch
     sel = _i32arr(np.arange(n_angles) if sel is None else sel)
     out = torch.empty((N, N), dtype=sino.dtype, device=sino.device)
-    g = Geometry(N, n_angles, sino.shape[-1], projector)
+    g, _keep = _geom(N, n_angles, sino.shape[-1], projector, angles)
     _check(lib().tq_backproject(C.byref(g), sel.ctypes.data, len(sel), sino.contiguous().data_ptr(),
                                 out.data_ptr(), _prec(sino), _stream(stream)))
     return out
@@ -335,7 +360,7 @@ def local_solve(d, bprime, c, e1, x0, n_angles, sel, inner=INNER_CG, eta=0.0, st
     x = x0.clone().contiguous()
     N = x.shape[-1]
     sel = _i32arr(sel)
-    g = Geometry(N, n_angles, d.shape[-1], projector)
+    g, _keep = _geom(N, n_angles, d.shape[-1], projector, None)
     _check(lib().tq_local_solve(C.byref(g), sel.ctypes.data, len(sel), d.contiguous().data_ptr(),
                                 bprime.contiguous().data_ptr(), float(c), inner, e1, float(eta),
                                 x.data_ptr(), _prec(x), _stream(stream)))

@@ -15,10 +15,11 @@ def slice_kind(cfg, s):
     return cfg.quant
 
 
-def gpu_context(cfg, inp, precision=0, keep_labels=False, eta1=None):
+def gpu_context(cfg, inp, precision=0, keep_labels=False, eta1=None, angles=None, stop_tol=0.0):
     ctx = tomoq.Context(cfg.N, cfg.n_angles, cfg.n_det, cfg.nodes, inp.edges, split=cfg.split,
-                        rule=cfg.rule, n_slices=len(inp.sino), precision=precision, projector=cfg.projector)
-    ctx.set_params(cfg.rho, inner=cfg.inner, e1=cfg.e1, eta1=eta1, e2=cfg.e2, eta2=cfg.eta2)
+                        rule=cfg.rule, n_slices=len(inp.sino), precision=precision, projector=cfg.projector,
+                        angles=angles)
+    ctx.set_params(cfg.rho, inner=cfg.inner, e1=cfg.e1, eta1=eta1, e2=cfg.e2, eta2=cfg.eta2, stop_tol=stop_tol)
     ctx.set_quantizer(cfg.quant, k=cfg.k, lloyd=cfg.lloyd, quality=cfg.quality, keep_labels=keep_labels,
                       jpeg_restart=cfg.jpeg_restart)
     for s, d in enumerate(inp.sino):
@@ -26,12 +27,13 @@ def gpu_context(cfg, inp, precision=0, keep_labels=False, eta1=None):
     return ctx
 
 
-def oracle_case(cfg, inp, s=0, threads=8, eta1=None):
+def oracle_case(cfg, inp, s=0, threads=8, eta1=None, theta=None, stop_tol=0.0):
     return oracle.OracleADMM(cfg.N, cfg.n_det, cfg.n_angles, cfg.nodes, inp.edges,
                              inp.sino[s].astype(np.float64), cfg.split == C.SPLIT_CONTIG,
                              rule=cfg.rule, inner=cfg.inner, e1=cfg.e1, rho=cfg.rho, eta1=eta1,
                              e2=cfg.e2, eta2=cfg.eta2, qkind=QKIND[slice_kind(cfg, s)], K=cfg.k,
-                             lloyd=cfg.lloyd, quality=cfg.quality, threads=threads, projector=cfg.projector)
+                             lloyd=cfg.lloyd, quality=cfg.quality, threads=threads, projector=cfg.projector,
+                             theta=theta, stop_tol=stop_tol)
 
 
 def export_all(ctx, cfg, s=0):

@@ -4,17 +4,18 @@ import math
 import numpy as np
 
 
-def dense_joseph(N, n_ang, n_det, sel=None):
+def dense_joseph(N, n_ang, n_det, sel=None, theta=None):
     """Brute-force Joseph system matrix from the geometry: walk each ray's
     major-axis pixel lines and give each pixel its linear-interpolation weight
-    times the per-line ray length 1/m (rows: selected angles x bins)."""
+    times the per-line ray length 1/m (rows: selected angles x bins).  theta: an
+    explicit angle list (radians; major axis x iff |sin| >= |cos|, R-3)."""
     sel = list(range(n_ang)) if sel is None else list(sel)
     A = np.zeros((len(sel) * n_det, N * N))
     half = (N - 1) / 2.0
     for k, a in enumerate(sel):
-        th = math.pi * a / n_ang
+        th = math.pi * a / n_ang if theta is None else float(theta[a])
         c, s = math.cos(th), math.sin(th)
-        xmaj = 4 * a >= n_ang and 4 * a <= 3 * n_ang
+        xmaj = (4 * a >= n_ang and 4 * a <= 3 * n_ang) if theta is None else abs(s) >= abs(c)
         cols = np.arange(N)
         for j in range(n_det):
             t = j - (n_det - 1) / 2.0
@@ -50,19 +51,22 @@ def clip_length(px0, px1, py0, py1, x0, y0, dx, dy):
     return max(0.0, hi - lo)
 
 
-def dense_siddon(N, n_ang, n_det):
+def dense_siddon(N, n_ang, n_det, theta=None):
     """Exact intersection-length matrix by clipping every ray against every pixel square
     (no Siddon crossing lists); a ray lying on the edge shared by two pixels is counted
-    half in each (R-26), trig exact at 0 and pi/2."""
+    half in each (R-26), trig exact at 0 and pi/2 (explicit lists: theta == 0,
+    theta == fl64(pi/2))."""
     h = N / 2.0
     A = np.zeros((n_ang * n_det, N * N))
     for a in range(n_ang):
-        if a == 0:
+        th = math.pi * a / n_ang if theta is None else float(theta[a])
+        zero = a == 0 if theta is None else th == 0.0
+        half_pi = 2 * a == n_ang if theta is None else th == math.pi / 2
+        if zero:
             cs, sn = 1.0, 0.0
-        elif 2 * a == n_ang:
+        elif half_pi:
             cs, sn = 0.0, 1.0
         else:
-            th = math.pi * a / n_ang
             cs, sn = math.cos(th), math.sin(th)
         for j in range(n_det):
             t = j - 0.5 * (n_det - 1)

@@ -262,3 +262,68 @@ def test_siddon_adjoint_and_admm_runs():
                           projector=1).run(3000)
     ls = np.linalg.lstsq(A, sino.ravel(), rcond=None)[0]
     assert np.linalg.norm(o.image().ravel() - ls) <= 1e-4 * np.linalg.norm(ls)
+
+
+# ---------------------------------------------------------------- explicit angle lists
+def explicit_angles(n, seed):
+    """Seeded irregular angles in [0, pi) including the special ones (0, pi/4, pi/2, 3pi/4)."""
+    rng = np.random.default_rng(seed)
+    t = np.concatenate([[0.0, math.pi / 4, math.pi / 2, 3 * math.pi / 4], rng.uniform(0, math.pi, n - 4)])
+    return t
+
+
+@pytest.mark.parametrize("N,n_det,seed", [(8, 13, 1), (9, 15, 2)])
+def test_explicit_angles_equal_bruteforce_dense(N, n_det, seed):
+    """tq_geometry.angles_rad / the oracle's theta list: the brute-force Joseph matrix built
+    from the same explicit angles (major axis |sin| >= |cos|, R-3), forward and transpose."""
+    from tests.helpers import dense_joseph
+    theta = explicit_angles(10, seed)
+    A = dense_joseph(N, len(theta), n_det, theta=theta)
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((N, N))
+    y = rng.standard_normal((len(theta), n_det))
+    np.testing.assert_allclose(oracle.project(x, len(theta), n_det, theta=theta).ravel(), A @ x.ravel(),
+                               rtol=0, atol=1e-12)
+    np.testing.assert_allclose(oracle.backproject(y, N, len(theta), theta=theta).ravel(), A.T @ y.ravel(),
+                               rtol=0, atol=1e-12)
+
+
+def test_explicit_uniform_list_equals_uniform_angles():
+    """An explicit list equal to pi a / n (no angle on the 45-degree tie) gives the uniform run."""
+    N, n_ang, n_det = 32, 90, 47
+    x = np.random.default_rng(3).standard_normal((N, N))
+    theta = math.pi * np.arange(n_ang) / n_ang
+    np.testing.assert_array_equal(oracle.project(x, n_ang, n_det, theta=theta), oracle.project(x, n_ang, n_det))
+
+
+def test_explicit_angles_analytic_ellipse():
+    """Irregular angles: a 4x4-supersampled rotated ellipse vs its closed-form line integrals
+    (Eq. 1) at those angles, with the bound of test_analytic_chord_lengths."""
+    N, n_det = 256, 363
+    e = synth.Ellipses(np.array([-12.5]), np.array([20.25]), np.array([70.0]),
+                       np.array([35.0]), np.array([0.6]), np.array([0.8]))
+    img = synth.rasterize(e, N)
+    theta = explicit_angles(24, 7)
+    ref = synth.ellipse_sinogram(e, theta, n_det)
+    got = oracle.project(img, len(theta), n_det, theta=theta)
+    assert np.sqrt(np.mean((got - ref) ** 2)) <= 0.005 * ref.max()
+    assert np.max(np.abs(got - ref)) <= 0.08 * ref.max()
+
+
+def test_explicit_angles_adjoint_and_siddon_dense():
+    """Explicit angles: the fp64 adjoint identity (north_star, 1e-10) and Siddon's matrix
+    against the per-pixel clip of every ray (axis rays on pixel edges half-split)."""
+    from tests.helpers import dense_siddon
+    theta = explicit_angles(8, 5)
+    N, n_det = 8, 13
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((N, N))
+    y = rng.standard_normal((len(theta), n_det))
+    lhs = float(np.sum(oracle.project(x, len(theta), n_det, theta=theta) * y))
+    rhs = float(np.sum(x * oracle.backproject(y, N, len(theta), theta=theta)))
+    assert abs(lhs - rhs) <= 1e-10 * abs(lhs)
+    A = dense_siddon(N, len(theta), n_det, theta=theta)
+    np.testing.assert_allclose(oracle.project_siddon(x, len(theta), n_det, theta=theta).ravel(), A @ x.ravel(),
+                               rtol=0, atol=1e-12)
+    np.testing.assert_allclose(oracle.backproject_siddon(y, N, len(theta), theta=theta).ravel(),
+                               A.T @ y.ravel(), rtol=0, atol=1e-12)

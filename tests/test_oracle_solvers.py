@@ -286,3 +286,98 @@ def test_paper_rule_identity_bytes_match_comm_model():
     assert o.bytes_per_iter == (M - 1) * X
     per_node_sent = o.bytes_per_iter / M
     assert per_node_sent * 2 == oracle.comm_model(M, X)
+
+
+def dense_graph_rule(A_blocks, d_blocks, edges, M, N, rho, iters, K, lloyd, private_rhs=False):
+    """Decentralized consensus ADMM over the graph (R-7) written out densely with
+    the K-means quantizer on every exchanged iterate: the local problem solved
+    exactly (dense solve), b'_i from the PUBLIC values xhat (R-11), alpha_i updated from the
+    public values of node i and its neighbours."""
+    n = N * N
+    nb = [[] for _ in range(M)]
+    for i, j in edges:
+        nb[i].append(j)
+        nb[j].append(i)
+    x = np.zeros((M, n)); alpha = np.zeros((M, n)); xh = np.zeros((M, n))
+    for _ in range(iters):
+        for i in range(M):
+            deg = len(nb[i])
+            S = sum(xh[j] for j in nb[i])
+            if private_rhs:  # the plausible mistake: the private iterates instead of xhat
+                S = sum(x[j] for j in nb[i])
+                bp = -alpha[i] + rho * (deg * x[i] + S)
+            else:
+                bp = -alpha[i] + rho * (deg * xh[i] + S)
+            Ai = A_blocks[i]
+            x[i] = np.linalg.solve(Ai.T @ Ai + 2 * rho * deg * np.eye(n), Ai.T @ d_blocks[i] + bp)
+        for i in range(M):  # Q = Alg. 5 on the fp32 wire format (pinned in test_oracle_codecs)
+            cen, lab = oracle.kmeans_encode(x[i].astype(np.float32), K, lloyd)
+            xh[i] = oracle.kmeans_decode(cen, lab).astype(np.float64)
+        for i in range(M):
+            alpha[i] += rho * (len(nb[i]) * xh[i] - sum(xh[j] for j in nb[i]))
+    return x, alpha, xh
+
+
+def test_graph_rule_with_quantizer_steps_match_dense():
+    """The graph rule with K-means (K = 8) step by step against its dense transcription: pins
+    that b' and the dual use the quantized public values xhat, not the private x."""
+    N, n_ang, n_det, M = 16, 24, 23, 4
+    d = small_problem(N, n_ang, n_det)
+    off, idx = oracle.partition_angles(n_ang, M, False)
+    Ab = [dense_joseph(N, n_ang, n_det, idx[off[m]:off[m + 1]]) for m in range(M)]
+    db = [d[idx[off[m]:off[m + 1]]].ravel() for m in range(M)]
+    edges = synth.ring(M)
+    x, alpha, xh = dense_graph_rule(Ab, db, edges, M, N, 0.5, 3, 8, 10)
+    o = oracle.OracleADMM(N, n_det, n_ang, M, edges, d, False, rule=0, inner=1, e1=600, rho=0.5,
+                          qkind=1, K=8, lloyd=10)
+    o.run(3)
+    assert rel(o.X, x) <= 1e-9 and rel(o.L, alpha) <= 1e-9
+    assert np.array_equal(o.XH, xh)
+    # b' from the private x instead of xhat (a plausible bug) gives a clearly different run
+    x_bad, _, _ = dense_graph_rule(Ab, db, edges, M, N, 0.5, 3, 8, 10, private_rhs=True)
+    assert rel(o.X, x_bad) > 1e-4
+
+
+@pytest.mark.parametrize("rule", [0, 1, 2])
+def test_stop_tol_first_iteration_below_tolerance(rule):
+    """tq_params.stop_tol ("stopping criterion", R-13): the run stops after the first
+    iteration k whose relative change ||x^{k+1} - x^k|| / ||x^{k+1}|| (max over the iterates:
+    graph rule every node's x_i, paper / consensus rule x) is <= tol -- found here by running
+    one iteration at a time and measuring the change with numpy."""
+    N, n_ang, n_det = 16, 24, 23
+    d = small_problem(N, n_ang, n_det)
+    kw = dict(rule=rule, inner=1, e1=5, rho=1.0, e2=10, eta2=0.2)
+    M = 4
+    if rule == 1:  # the literal paper rule stalls for M > 1 (SURVEY E2); M = 1 converges (prox point)
+        M, kw["rho"], kw["eta2"] = 1, 0.1, 2.0
+    edges = synth.ring(M) if M > 1 else []
+    step = oracle.OracleADMM(N, n_det, n_ang, M, edges, d, False, **kw)
+    tol = 2e-3
+    k_stop = None
+    for k in range(1, 300):
+        prev = (step.X if rule == 0 else step.XH).copy()
+        step.run(1)
+        cur = step.X if rule == 0 else step.XH
+        r = max(np.linalg.norm(cur[i] - prev[i]) / np.linalg.norm(cur[i]) for i in range(len(cur)))
+        if r <= tol:
+            k_stop = k
+            break
+    assert k_stop is not None and k_stop > 2
+    o = oracle.OracleADMM(N, n_det, n_ang, M, edges, d, False, stop_tol=tol, **kw)
+    o.run(300)
+    assert o.last_run_iters == k_stop and o.iters == k_stop
+    assert o.last_change <= tol
+    assert np.array_equal(o.X, step.X) and np.array_equal(o.XH, step.XH)
+    # stop_tol = 0: the requested count
+    o0 = oracle.OracleADMM(N, n_det, n_ang, M, edges, d, False, **kw)
+    o0.run(7)
+    assert o0.last_run_iters == 7
+
+
+def test_stop_tol_zero_data_stops_after_one_iteration():
+    """Zero data: x stays 0, the change 0/0 counts as 0, so the run stops after iteration 1."""
+    N, n_ang, n_det = 16, 12, 23
+    o = oracle.OracleADMM(N, n_det, n_ang, 2, synth.ring(2), np.zeros((n_ang, n_det)), True,
+                          rule=0, inner=1, e1=3, rho=1.0, stop_tol=1e-6)
+    o.run(50)
+    assert o.last_run_iters == 1 and o.last_change == 0.0
