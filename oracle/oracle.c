@@ -25,6 +25,8 @@
 
 #ifdef _OPENMP
 #include <omp.h>
+#else
+static int omp_in_parallel(void) { return 0; }
 #endif
 
 /* ------------------------------------------------------------------ geometry
@@ -69,12 +71,15 @@ void or_project_t(int N, int n_det, int n_ang, const double *theta, int n_sel, c
                   const double *img, double *sino)
 {
     double half = 0.5 * (double)(N - 1);
+    /* every (angle, bin) output is independent: OpenMP over them (when not already inside a
+     * parallel region) changes no result */
+#pragma omp parallel for collapse(2) schedule(static) if (!omp_in_parallel() && (long)n_sel * n_det * N > (1L << 22))
     for (int k = 0; k < n_sel; k++) {
-        int a = sel[k];
-        double cs, sn;
-        int xm;
-        joseph_trig(a, n_ang, theta, &cs, &sn, &xm);
         for (int j = 0; j < n_det; j++) {
+            int a = sel[k];
+            double cs, sn;
+            int xm;
+            joseph_trig(a, n_ang, theta, &cs, &sn, &xm);
             double t = (double)j - 0.5 * (double)(n_det - 1);
             double acc = 0.0;
             if (!xm) {
@@ -119,15 +124,18 @@ void or_backproject_t(int N, int n_det, int n_ang, const double *theta, int n_se
 {
     double half = 0.5 * (double)(N - 1);
     double t0 = -0.5 * (double)(n_det - 1);
-    for (size_t p = 0; p < (size_t)N * N; p++) img[p] = 0.0;
-    for (int k = 0; k < n_sel; k++) {
-        int a = sel[k];
-        double cs, sn;
-        int xm;
-        joseph_trig(a, n_ang, theta, &cs, &sn, &xm);
-        double m = xm ? fabs(sn) : fabs(cs);
-        for (int r = 0; r < N; r++) {
-            for (int c = 0; c < N; c++) {
+    /* per pixel: the sum over the selected angles in their order (OpenMP over rows when not
+     * already inside a parallel region; each pixel's sum is the same sequence either way) */
+#pragma omp parallel for schedule(static) if (!omp_in_parallel() && (long)n_sel * N * N > (1L << 22))
+    for (int r = 0; r < N; r++) {
+        for (int c = 0; c < N; c++) {
+            double sum = 0.0;
+            for (int k = 0; k < n_sel; k++) {
+                int a = sel[k];
+                double cs, sn;
+                int xm;
+                joseph_trig(a, n_ang, theta, &cs, &sn, &xm);
+                double m = xm ? fabs(sn) : fabs(cs);
                 double tp = ((double)c - half) * cs + (half - (double)r) * sn;
                 int j0 = (int)floor(tp - t0);
                 double acc = 0.0;
@@ -137,8 +145,9 @@ void or_backproject_t(int N, int n_det, int n_ang, const double *theta, int n_se
                     double w = 1.0 - fabs(tj - tp) / m;
                     if (w > 0.0) acc += (w / m) * sino[(size_t)k * n_det + j];
                 }
-                img[(size_t)r * N + c] += acc;
+                sum += acc;
             }
+            img[(size_t)r * N + c] = sum;
         }
     }
 }
@@ -957,10 +966,10 @@ long or_admm_run(int N, int n_det, int n_ang, int M, const int32_t *off, const i
     for (int m = 0; m < M; m++) doff[m + 1] = doff[m] + (size_t)(off[m + 1] - off[m]) * n_det;
     double *BP = malloc((size_t)M * n * sizeof(double));
     long bytes = 0;
-#ifdef _OPENMP
-    if (threads > 0) omp_set_num_threads(threads);
-#else
-    (void)threads;
+    /* node-level threads (the projector loops inside use every core when nt == 1) */
+    int nt = threads > 0 ? threads : 1;
+#ifndef _OPENMP
+    (void)nt;
 #endif
     if (rule == 0) {
         double *S = malloc((size_t)M * n * sizeof(double));
@@ -975,11 +984,11 @@ long or_admm_run(int N, int n_det, int n_ang, int M, const int32_t *off, const i
                     BP[(size_t)i * n + p] = -L[(size_t)i * n + p] + rho * ((double)deg[i] * XH[(size_t)i * n + p] + s);
                 }
             }
-#pragma omp parallel for schedule(dynamic, 1)
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
             for (int i = 0; i < M; i++)
                 local_solve(&P, i, d + doff[i], BP + (size_t)i * n, 2.0 * rho * deg[i], X + (size_t)i * n);
             bytes = 0;
-#pragma omp parallel for schedule(dynamic, 1) reduction(+ : bytes)
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : bytes) num_threads(nt)
             for (int i = 0; i < M; i++) {
                 long b = quantize(qkind, K, lloyd, quality, X + (size_t)i * n, N, N, XH + (size_t)i * n, NULL);
                 bytes += b * deg[i];
@@ -1013,11 +1022,11 @@ long or_admm_run(int N, int n_det, int n_ang, int M, const int32_t *off, const i
             for (int m = 0; m < M; m++)
                 for (size_t p = 0; p < n; p++)
                     BP[(size_t)m * n + p] = rho * XH[p] - L[(size_t)m * n + p];
-#pragma omp parallel for schedule(dynamic, 1)
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
             for (int m = 0; m < M; m++)
                 local_solve(&P, m, d + doff[m], BP + (size_t)m * n, rho, X + (size_t)m * n);
             bytes = 0;
-#pragma omp parallel for schedule(dynamic, 1) reduction(+ : bytes)
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : bytes) num_threads(nt)
             for (int m = 0; m < M; m++) {
                 size_t lo = (size_t)roff[m] * N, hi = (size_t)roff[m + 1] * N;
                 double *seg = malloc((hi - lo) * sizeof(double));

@@ -137,40 +137,58 @@ def test_consensus_rule_lockstep_full_size():
     assert rel(dl, want) <= 1e-3
 
 
-def lockstep(cfg, inp, prec=0, steps=3, warm=2, label_nodes=None):
-    """GPU runs `warm` iterations, then for each step: the oracle advances one
-    iteration from the exported GPU state; compare the pre-quantization iterates."""
+# Lockstep bounds (re-tightened from the observed errors of
+# profiles/r2_lockstep_errors.json: per node and step the relative L2 error of the next
+# pre-quantization iterate is typically ~5e-7 (fp64 epilogues, fp32 storage), with isolated
+# spikes up to 1.3e-4 on ill-conditioned CG steps): the median over nodes and steps must stay
+# <= 1e-5 and the worst <= 1e-3 -- a naive-fp32 CG epilogue (2e-3) fails both.
+LOCK_MEDIAN, LOCK_MAX = 1e-5, 1e-3
+
+
+def lockstep(cfg, inp, prec=0, steps=3, warm=2, label_nodes=None, slices=(0,), threads=8):
+    """GPU runs `warm` iterations, then for each step: the oracle advances one iteration from
+    the exported GPU state of each slice in `slices`; compare the pre-quantization iterates.
+    Returns (median, worst) relative L2 error over nodes and steps."""
+    from tests.cases import slice_kind
     ctx = gpu_context(cfg, inp, precision=prec, keep_labels=True)
     ctx.run(warm)
-    worst = 0.0
+    errs = []
     for _ in range(steps):
-        X, L, XH = export_all(ctx, cfg)
-        o = oracle_case(cfg, inp)
-        o.X, o.L, o.XH = X.copy(), L.copy(), XH.copy()
-        o.run(1)
+        states = {s: export_all(ctx, cfg, s) for s in slices}
         ctx.run(1)
-        Xg, _, _ = export_all(ctx, cfg)
-        for m in range(cfg.nodes):
-            worst = max(worst, rel(Xg[m], o.X[m]))
-        if cfg.quant == C.Q_KMEANS:
-            for m in (label_nodes or range(cfg.nodes)):
-                lab = ctx.labels(0, m, cfg.N * cfg.N)
-                _, lr = oracle.kmeans_encode(Xg[m].astype(np.float32), cfg.k, cfg.lloyd)
-                assert np.mean(lab == lr) >= 0.9999
-        if cfg.quant == C.Q_DCT:
-            for m in range(cfg.nodes):
-                st = ctx.export_state(0, m)
-                cr, mr = oracle.dct_encode(Xg[m].astype(np.float32).reshape(cfg.N, cfg.N), cfg.quality)
-                dec = oracle.dct_decode(cr, mr, cfg.N, cfg.N, cfg.quality)
-                assert np.array_equal(st[2].astype(np.float32), dec.ravel())
-    return worst
+        for s in slices:
+            X, L, XH = states[s]
+            o = oracle_case(cfg, inp, s, threads=threads)
+            o.X, o.L, o.XH = X.copy(), L.copy(), XH.copy()
+            o.run(1)
+            Xg, _, _ = export_all(ctx, cfg, s)
+            errs += [rel(Xg[m], o.X[m]) for m in range(cfg.nodes)]
+            kind = slice_kind(cfg, s)
+            if kind == C.Q_KMEANS:
+                for m in (label_nodes or range(cfg.nodes)):
+                    lab = ctx.labels(s, m, cfg.N * cfg.N)
+                    _, lr = oracle.kmeans_encode(Xg[m].astype(np.float32), cfg.k, cfg.lloyd)
+                    assert np.mean(lab == lr) >= 0.9999
+            if kind == C.Q_DCT:
+                for m in (label_nodes or range(cfg.nodes)):
+                    st = ctx.export_state(s, m)
+                    cr, mr = oracle.dct_encode(Xg[m].astype(np.float32).reshape(cfg.N, cfg.N), cfg.quality)
+                    dec = oracle.dct_decode(cr, mr, cfg.N, cfg.N, cfg.quality)
+                    assert np.array_equal(st[2].astype(np.float32), dec.ravel())
+    ctx.close()
+    return float(np.median(errs)), max(errs)
+
+
+def assert_lockstep(res):
+    med, worst = res
+    assert med <= LOCK_MEDIAN and worst <= LOCK_MAX, res
 
 
 @pytest.mark.parametrize("make", [c2s, c3s])
 def test_lockstep_fp32_quantized(make):
     cfg = make()
     inp = C.make_inputs(cfg)
-    assert lockstep(cfg, inp) <= 1e-3
+    assert_lockstep(lockstep(cfg, inp))
 
 
 def test_lockstep_full_size_bench_config():
@@ -178,7 +196,7 @@ def test_lockstep_full_size_bench_config():
     one full-size lockstep iteration of every node."""
     cfg = C.C4(1)
     inp = C.make_inputs(cfg, with_truth=False)
-    assert lockstep(cfg, inp, steps=1, warm=1, label_nodes=[0, 5]) <= 1e-3
+    assert_lockstep(lockstep(cfg, inp, steps=1, warm=1, label_nodes=[0, 5]))
 
 
 @pytest.mark.parametrize("make", [C.C2, C.C3])
@@ -187,7 +205,48 @@ def test_lockstep_full_size_configs(make):
     stated sizes: one lockstep iteration of every node after one free iteration."""
     cfg = make()
     inp = C.make_inputs(cfg, with_truth=False)
-    assert lockstep(cfg, inp, steps=1, warm=1) <= 1e-3
+    assert_lockstep(lockstep(cfg, inp, steps=1, warm=1))
+
+
+def test_lockstep_config5_stated_size():
+    """Config 5 at its stated size: two 2048^2 slices (1500 angles, 2897 bins, 8 nodes of
+    187-188 angles on a complete graph), slice 0 K-means K=32 and slice 1 DCT q75 (R-20):
+    after one free iteration the oracle advances one iteration of every node of both slices
+    from the exported GPU state (~75 G voxel-updates per slice, OpenMP over pixel rows); the
+    next pre-quantization iterates match, the K-means labels of two nodes agree on >= 99.99%
+    and the DCT decode of two nodes is bit-exact (the paper's 2048^2 size)."""
+    cfg = C.C5(slices=2)
+    inp = C.make_inputs(cfg, with_truth=False)
+    assert_lockstep(lockstep(cfg, inp, steps=1, warm=1, label_nodes=[0, 5], slices=(0, 1), threads=1))
+
+
+@pytest.mark.parametrize("make,iters", [(C.C2, 50), (C.C3, 20)])
+def test_fp64_stated_configs_track_the_oracle(make, iters):
+    """fp64 verification mode on configs 2 (50 iterations, as stated) and 3 (20 of its 100) at
+    their stated sizes.  (1) Per iteration the GPU's fp64 iteration equals
+    the oracle's: lockstep relative L2 <= 1e-10 (summation order only).  (2) Free-running, the
+    ADMM map at rho = 1 with 5-step CG amplifies perturbations by roughly 2x per iteration, so
+    after 20-50 iterations fp64 rounding differences have grown to ~1e-2 -- a property of the
+    iteration, not of the implementation: the oracle run against itself from a state
+    perturbed by 1e-13 (relative) after the first iteration diverges by the same amount, and
+    the GPU's distance to the oracle must stay within 10x of that."""
+    cfg = make()
+    inp = C.make_inputs(cfg, with_truth=False)
+    med, worst = lockstep(cfg, inp, prec=1, steps=2, warm=1, threads=16)
+    assert worst <= 1e-10, (med, worst)
+    ctx = gpu_context(cfg, inp, precision=1)
+    ctx.run(iters)
+    X = np.stack([ctx.export_state(0, m)[0] for m in range(cfg.nodes)])
+    ctx.close()
+    o = oracle_case(cfg, inp, threads=16).run(iters)
+    op = oracle_case(cfg, inp, threads=16).run(1)
+    rng = np.random.default_rng(7)
+    op.X *= 1.0 + 1e-13 * rng.standard_normal(op.X.shape)
+    op.run(iters - 1)
+    d_gpu, d_self = rel(X, o.X), rel(op.X, o.X)
+    print(f"{cfg.name}: fp64 lockstep median {med:.2e} worst {worst:.2e}; after {iters} iterations "
+          f"GPU-oracle {d_gpu:.2e}, oracle-vs-perturbed-oracle {d_self:.2e}")
+    assert d_gpu <= 10 * max(d_self, 1e-9)
 
 
 def test_graph_rule_dual_sum_invariant_full_size():
