@@ -95,6 +95,52 @@ def vu_per_iter(cfg):
     return 2 * apps * cfg.N * cfg.N * cfg.n_angles * cfg.slices
 
 
+def sm_count():
+    import torch
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
+def host_info():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"host_cores": os.cpu_count(), "host_model": model}
+
+
+def c5_iteration(tomoq, torch, stream, slices=4, iters=3):
+    """Config 5 whole ADMM iterations at G = 1 on `slices` of its 32 slices (2048^2, 1500
+    angles, 8 nodes per slice on a complete graph, CG5, even slices K-means 32 / odd slices DCT
+    q75): ms per iteration and G VU/s, CUDA events over `iters` iterations after one warm-up."""
+    from paper_2410_06106_b200 import configs as C
+    cfg = C.C5(slices=slices)
+    inp = C.make_inputs(cfg, with_truth=False)
+    ctx = tomoq.Context(cfg.N, cfg.n_angles, cfg.n_det, cfg.nodes, inp.edges, split=cfg.split, rule=cfg.rule,
+                        n_slices=slices)
+    ctx.set_params(cfg.rho, inner=cfg.inner, e1=cfg.e1)
+    ctx.set_quantizer(cfg.quant, k=cfg.k, lloyd=cfg.lloyd, quality=cfg.quality)
+    for s_, d in enumerate(inp.sino):
+        ctx.set_sinogram(s_, d)
+    ctx.run(1, stream)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    ctx.run(iters, stream)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / iters
+    ctx.close()
+    vu = vu_per_iter(cfg)
+    return {"workload": f"C5 at G = 1: {slices} of its 32 slices (2048^2, 1500 angles, 8 nodes per slice, "
+                        f"K-means 32 / DCT q75 by slice), {iters} timed iterations",
+            "ms_per_iter": ms, "gvu_s": vu / (ms / 1e3) / 1e9,
+            "ms_per_iter_32_slices_extrapolated": ms * 32 / slices}
+
+
 def projector_c5_geometry(tomoq, torch, stream, reps=5):
     """Forward projector and CG backprojector on one C5 slice's geometry: 2048^2 image,
     1500 angles, 8 nodes of 187-188 angles on one GPU (random sinogram: timing only)."""
@@ -108,7 +154,7 @@ def projector_c5_geometry(tomoq, torch, stream, reps=5):
     sino = torch.rand(cfg.n_angles, cfg.n_det, device="cuda")
     ctx.set_sinogram(0, sino)
     out = {"workload": "C5 slice geometry: N=2048, 1500 angles, 2897 bins, 8 nodes x 187-188 angles"}
-    peak = LSU_VU_PER_CLK_SM * 148 * peaks()["sm_max_mhz"] * 1e6 / 1e9
+    peak = LSU_VU_PER_CLK_SM * sm_count() * peaks()["sm_max_mhz"] * 1e6 / 1e9
     for comp, name in ((0, "fp"), (1, "bp_cgq")):
         ctx.launch_component(comp, 2, stream)
         torch.cuda.synchronize()
@@ -131,7 +177,7 @@ def projector_siddon_c4(tomoq, torch, stream, reps=10):
     cfg = C.C4(1)
     inp = C.make_inputs(cfg, with_truth=False)
     out = {"workload": "C4_G1 geometry with the Siddon projector"}
-    peak = LSU_VU_PER_CLK_SM * 148 * peaks()["sm_max_mhz"] * 1e6 / 1e9
+    peak = LSU_VU_PER_CLK_SM * sm_count() * peaks()["sm_max_mhz"] * 1e6 / 1e9
     for proj, name in ((tomoq.PROJ_SIDDON, "siddon"), (tomoq.PROJ_JOSEPH, "joseph")):
         ctx = tomoq.Context(cfg.N, cfg.n_angles, cfg.n_det, cfg.nodes, inp.edges, split=cfg.split, rule=cfg.rule,
                             projector=proj)
@@ -191,8 +237,8 @@ def dct_entropy_c3(tomoq, torch, stream, reps=10, restart=4):
 
 def cpu_baseline(cfg_g1, iters=2):
     """The fp64 oracle as it stands, on the host cores, on a bounded sample: `iters`
-    ADMM iterations of the per-GPU share of the workload (config 4 at G = 1)."""
-    import oracle
+    ADMM iterations of the per-GPU share of the workload (config 4 at G = 1), OpenMP over
+    the nodes and, nested, over the projector's pixel rows / outputs on the spare cores."""
     from paper_2410_06106_b200 import configs as C
     from tests.cases import oracle_case
     inp = C.make_inputs(cfg_g1, with_truth=False)
@@ -201,9 +247,10 @@ def cpu_baseline(cfg_g1, iters=2):
     t0 = time.perf_counter()
     o.run(iters)
     dt = time.perf_counter() - t0
-    return {"value": vu_per_iter(cfg_g1) * iters / dt / 1e9, "unit": UNIT, "cores": threads,
+    return {"value": vu_per_iter(cfg_g1) * iters / dt / 1e9, "unit": UNIT, "cores": os.cpu_count(),
             "kind": "oracle", "sample": f"{iters} ADMM iterations of {cfg_g1.name} (8 nodes, 1024^2, "
-                                        f"K-means 64), OpenMP over nodes", "seconds": round(dt, 2)}
+                                        f"K-means 64), OpenMP over the {threads} nodes and nested over pixel rows",
+            "seconds": round(dt, 2), **host_info()}
 
 
 def bench_config(cfg, world):
@@ -232,14 +279,16 @@ def run_reference(args):
     dt = time.perf_counter() - t0
     value = vu_per_iter(cfg) * args.steps / dt / 1e9
     sample = (f"each step = 1 ADMM iteration of {cfg.name} (the per-GPU share of C4_G{world}: 8 nodes, "
-              f"1024^2, 90 angles, CG5, K-means 64) on the fp64 CPU oracle, OpenMP over nodes")
+              f"1024^2, 90 angles, CG5, K-means 64) on the fp64 CPU oracle, OpenMP over the nodes and "
+              f"nested over pixel rows")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / max(1, args.steps),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": bench_config(C.C4(world), world),
         "admm_iters_per_s": args.steps / dt,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": sample,
+                         **host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -381,7 +430,8 @@ def main():
     names = {0: "forward projector A p (fp_persist_f32 tile pass + fp_reduce)",
              1: "backprojector A^T s + c p with fused p.q (bp_tile_kernel<float,CGQ>)"}
     achieved = comp_units[dom] / (comp_ms[dom] / 1e3) / 1e9
-    peak_vu = LSU_VU_PER_CLK_SM * 148 * pk["sm_max_mhz"] * 1e6 / 1e9
+    n_sm = sm_count()
+    peak_vu = LSU_VU_PER_CLK_SM * n_sm * pk["sm_max_mhz"] * 1e6 / 1e9
     n_local = st["local_nodes"]
     compulsory = 4.0 * n_local * cfg.N ** 2 + 8.0 * (comp_units[dom] / cfg.N ** 2) * cfg.n_det
     traffic = None
@@ -391,10 +441,11 @@ def main():
     except Exception:
         pass
     roofline = {
-        "bound": "alu", "kernel": names[dom], "achieved": achieved, "peak": peak_vu, "unit": "GVU/s",
+        "bound": "smem", "kernel": names[dom], "achieved": achieved, "peak": peak_vu, "unit": "GVU/s",
         "frac": achieved / peak_vu, "traffic": traffic,
-        "peak_basis": f"shared-memory data path: 2 x 4-byte taps per VU at 128 B/clk/SM = {LSU_VU_PER_CLK_SM} "
-                      f"VU/clk/SM x 148 SMs x {pk['sm_max_mhz']} MHz (sm_max_mhz {pk['src']}); DESIGN.md section 6",
+        "peak_basis": f"shared-memory data path (l1tex shared wavefronts, measured 0.977/clk/SM in "
+                      f"profiles/r1_smem_roofline.txt): 2 x 4-byte taps per VU at 128 B/clk/SM = {LSU_VU_PER_CLK_SM} "
+                      f"VU/clk/SM x {n_sm} SMs x {pk['sm_max_mhz']} MHz (sm_max_mhz {pk['src']}); DESIGN.md section 6",
         "hbm_compulsory_gbs": compulsory / (comp_ms[dom] / 1e3) / 1e9, "hbm_peak_gbs": pk["hbm_gbs"],
         "share_of_step": share[dom],
         "components_ms": {"fp": comp_ms[0], "bp_cgq": comp_ms[1]},
@@ -408,6 +459,13 @@ def main():
             c5_geom = projector_c5_geometry(tomoq, torch, stream, reps=5)
         except Exception as exc:  # report, never fail the bench line
             c5_geom = {"error": str(exc)[:200]}
+    # ---- config 5 whole iterations at G = 1 (a slice subset; context, not the headline)
+    c5_iter = None
+    if rank == 0 and world == 1 and not args.no_c5_geometry:
+        try:
+            c5_iter = c5_iteration(tomoq, torch, stream)
+        except Exception as exc:
+            c5_iter = {"error": str(exc)[:200]}
     # ---- NEXT-3: the Siddon projector on the bench geometry (context, not the headline)
     siddon_c4 = None
     if rank == 0 and not args.no_c5_geometry:
@@ -438,6 +496,7 @@ def main():
             "vu_per_step": vu_it,
             "roofline": roofline,
             "projector_c5_geometry": c5_geom,
+            "c5_iteration": c5_iter,
             "dct_entropy_c3": jpeg_c3,
             "projector_siddon_c4": siddon_c4,
             "cpu_baseline": cpu,

@@ -221,6 +221,12 @@ tq_status tq_launch_component(tq_ctx *ctx, int32_t component, int32_t reps, void
                               int64_t *units);
 
 tq_status tq_get_stats(const tq_ctx *ctx, tq_stats *out);
+/* Debug aid (no compute-sanitizer on the GPU pool): with TQ_GUARD=1 in the environment of the
+ * process, every device allocation of the library carries 256-byte guard bands (checked after
+ * every run: TQ_ECUDA on an out-of-bounds write) and starts poisoned with 0xff bytes, so reads
+ * of never-written memory change results.  This call checks every live allocation's guards now
+ * (TQ_OK when TQ_GUARD is unset). */
+tq_status tq_debug_guard_check(void);
 /* Phase timing (tq_stats.phase_ms): on = 1 makes later runs launch each phase as its own CUDA
  * graph with timing events in between (slightly slower than the default whole-iteration
  * graph; off by default).  Waits for an enqueued run. */

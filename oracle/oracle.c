@@ -25,8 +25,15 @@
 
 #ifdef _OPENMP
 #include <omp.h>
+/* threads for a loop over independent outputs: the cores the enclosing team leaves free
+ * (nested inside the node-level loop of or_admm_run, all cores outside it) */
+static int spare_threads(void)
+{
+    int t = omp_get_num_procs() / omp_get_num_threads();
+    return t > 1 ? t : 1;
+}
 #else
-static int omp_in_parallel(void) { return 0; }
+static int spare_threads(void) { return 1; }
 #endif
 
 /* ------------------------------------------------------------------ geometry
@@ -72,8 +79,8 @@ void or_project_t(int N, int n_det, int n_ang, const double *theta, int n_sel, c
 {
     double half = 0.5 * (double)(N - 1);
     /* every (angle, bin) output is independent: OpenMP over them (when not already inside a
-     * parallel region) changes no result */
-#pragma omp parallel for collapse(2) schedule(static) if (!omp_in_parallel() && (long)n_sel * n_det * N > (1L << 22))
+     * parallel region: the spare cores) changes no result */
+#pragma omp parallel for collapse(2) schedule(static) num_threads(spare_threads()) if ((long)n_sel * n_det * N > (1L << 22))
     for (int k = 0; k < n_sel; k++) {
         for (int j = 0; j < n_det; j++) {
             int a = sel[k];
@@ -126,7 +133,7 @@ void or_backproject_t(int N, int n_det, int n_ang, const double *theta, int n_se
     double t0 = -0.5 * (double)(n_det - 1);
     /* per pixel: the sum over the selected angles in their order (OpenMP over rows when not
      * already inside a parallel region; each pixel's sum is the same sequence either way) */
-#pragma omp parallel for schedule(static) if (!omp_in_parallel() && (long)n_sel * N * N > (1L << 22))
+#pragma omp parallel for schedule(static) num_threads(spare_threads()) if ((long)n_sel * N * N > (1L << 22))
     for (int r = 0; r < N; r++) {
         for (int c = 0; c < N; c++) {
             double sum = 0.0;
@@ -966,8 +973,11 @@ long or_admm_run(int N, int n_det, int n_ang, int M, const int32_t *off, const i
     for (int m = 0; m < M; m++) doff[m + 1] = doff[m] + (size_t)(off[m + 1] - off[m]) * n_det;
     double *BP = malloc((size_t)M * n * sizeof(double));
     long bytes = 0;
-    /* node-level threads (the projector loops inside use every core when nt == 1) */
+    /* node-level threads; the projector loops inside use the cores they leave free */
     int nt = threads > 0 ? threads : 1;
+#ifdef _OPENMP
+    omp_set_max_active_levels(2);
+#endif
 #ifndef _OPENMP
     (void)nt;
 #endif

@@ -232,6 +232,13 @@ tq_status tq_get_node_bytes(tq_ctx *ctx, int32_t slice, int32_t node, int64_t *s
     });
 }
 
+tq_status tq_debug_guard_check(void) {
+    return guard(nullptr, [&] {
+        std::string where;
+        if (!guards_intact(where)) fail(TQ_ECUDA, "TQ_GUARD: guard band corrupted: " + where);
+    });
+}
+
 const char *tq_last_error(const tq_ctx *ctx) { return ctx ? ctx->c.err.c_str() : g_err.c_str(); }
 const char *tq_last_error_global(void) { return g_err.c_str(); }
 

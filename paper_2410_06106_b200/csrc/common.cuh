@@ -30,6 +30,22 @@ struct Error {
         if (!(cond)) ::tq::fail(TQ_EINVAL, msg);                                         \
     } while (0)
 
+// ---------------------------------------------------------------- guarded allocations
+// Debug aid standing in for compute-sanitizer (closed on the GPU pool): with TQ_GUARD=1 in the
+// environment every device allocation of the library gets 256-byte guard bands filled with a
+// pattern on both sides (checked after every run and at tq_destroy: an out-of-bounds write
+// fails with TQ_ECUDA) and its contents poisoned with 0xff bytes (NaN / -1) instead of left
+// undefined, so a read of memory nobody wrote changes the results (tests compare bitwise
+// against an unguarded run).  Without TQ_GUARD these are plain cudaMalloc / cudaFree.
+cudaError_t guarded_malloc(void **p, size_t bytes);
+cudaError_t guarded_free(void *p);
+bool guards_enabled();
+bool guards_intact(std::string &where);
+#ifndef TQ_NO_GUARD_MACROS
+#define cudaMalloc(p, b) ::tq::guarded_malloc(reinterpret_cast<void **>(p), (b))
+#define cudaFree(p) ::tq::guarded_free((void *)(p))
+#endif
+
 // ---------------------------------------------------------------- geometry (host)
 // DESIGN.md R-1..R-3: theta_a = pi a / n_ang; x-major iff 4a in [n_ang, 3 n_ang];
 // m_a = |sin| (x-major) or |cos| (y-major).  Explicit angle lists: x-major iff |sin| >= |cos|.

@@ -981,6 +981,10 @@ void Ctx::finish() {
     if (!pending) return;
     pending = false;
     TQ_CHECK_CUDA(cudaEventSynchronize(run_done));
+    if (guards_enabled()) {  // TQ_GUARD=1: the run wrote nothing outside its allocations
+        std::string where;
+        if (!guards_intact(where)) fail(TQ_ECUDA, "TQ_GUARD: guard band corrupted: " + where);
+    }
     // the scalar table of the last enqueued run (nothing else writes it before this call)
     if (!norm_host) TQ_CHECK_CUDA(cudaMallocHost(&norm_host, sizeof(double) * S_NSLOT * std::max(1, L)));
     if (L) TQ_CHECK_CUDA(cudaMemcpy(norm_host, in.scal, sizeof(double) * S_NSLOT * L, cudaMemcpyDeviceToHost));

@@ -89,6 +89,7 @@ _SIGS = {
     "tq_export_labels": [_vp, _i32, _i32, _vp, _i64],
     "tq_get_stats": [_vp, C.POINTER(Stats)],
     "tq_set_profiling": [_vp, _i32],
+    "tq_debug_guard_check": [],
     "tq_get_node_bytes": [_vp, _i32, _i32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
     "tq_launch_component": [_vp, _i32, _i32, _vp, C.POINTER(C.c_int64)],
     "tq_partition_angles": [_i32, _i32, _i32, _vp, _vp],
@@ -184,6 +185,11 @@ def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(lib().tq_nccl_unique_id(buf))
     return bytes(buf)
+
+
+def debug_guard_check():
+    """tq_debug_guard_check: raises if a guard band (TQ_GUARD=1) was overwritten."""
+    _check(lib().tq_debug_guard_check())
 
 
 def loopback_id() -> bytes:
