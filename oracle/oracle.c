@@ -973,10 +973,11 @@ long or_admm_run(int N, int n_det, int n_ang, int M, const int32_t *off, const i
     for (int m = 0; m < M; m++) doff[m + 1] = doff[m] + (size_t)(off[m + 1] - off[m]) * n_det;
     double *BP = malloc((size_t)M * n * sizeof(double));
     long bytes = 0;
-    /* node-level threads; the projector loops inside use the cores they leave free */
+    /* node-level threads; with one node thread the projector loops use every core (nesting
+     * under several node threads measured slower than node-level threads alone) */
     int nt = threads > 0 ? threads : 1;
 #ifdef _OPENMP
-    omp_set_max_active_levels(2);
+    omp_set_max_active_levels(nt > 1 ? 1 : 2);
 #endif
 #ifndef _OPENMP
     (void)nt;
