@@ -248,7 +248,7 @@ def cpu_baseline(cfg_g1, iters=2):
     t0 = time.perf_counter()
     o.run(iters)
     dt = time.perf_counter() - t0
-    return {"value": vu_per_iter(cfg_g1) * iters / dt / 1e9, "unit": UNIT, "cores": os.cpu_count(),
+    return {"value": vu_per_iter(cfg_g1) * iters / dt / 1e9, "unit": UNIT, "cores": threads,
             "kind": "oracle", "sample": f"{iters} ADMM iterations of {cfg_g1.name} (8 nodes, 1024^2, "
                                         f"K-means 64), OpenMP over the {threads} nodes",
             "seconds": round(dt, 2), **host_info()}
@@ -287,7 +287,7 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": bench_config(C.C4(world), world),
         "admm_iters_per_s": args.steps / dt,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": sample,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
                          **host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
