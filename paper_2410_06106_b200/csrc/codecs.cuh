@@ -4,7 +4,7 @@
 // iterates, received payloads and segments of the consensus image.
 //
 // K-means (Alg. 5; exact rules DESIGN.md R-16): LSD radix sort of the
-// payload keys, quantile init as exact order statistics, E_q Lloyd steps as upper
+// payload keys on their top 24 bits (low byte resolved per query), quantile init as exact order statistics, E_q Lloyd steps as upper
 // bounds + fixed-point prefix sums on the sorted keys (exact, deterministic), final
 // assignment, labels packed as ceil(log2 K) bit-planes per 32-element group.
 // Payload: [K fp32 centres][ceil(nv/32) * B uint32 planes, group-major].

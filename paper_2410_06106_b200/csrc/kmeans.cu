@@ -1,17 +1,20 @@
 // kmeans.cu -- K-means quantizer (Alg. 5), exact rules DESIGN.md R-16.
 //
-// Sort-based exact Lloyd.  Each payload's values are mapped to order-preserving
-// 32-bit keys and sorted by an LSD radix sort (4 passes of 8-bit digits: per-tile
-// digit histograms stored tile-major, one exclusive scan per payload over
-// (digit, tile) = the global output offsets, stable match-based tile ranking +
-// scatter).  On the sorted keys:
-//   * the quantile init c_k = v_(floor((2k+1) n / 2K)) is a direct read (exact order
-//     statistic);
+// Sort-based exact Lloyd.  Each payload's values are mapped to order-preserving 32-bit
+// keys and ordered by an LSD radix sort on the key bytes 1..3 (3 passes of 8-bit digits:
+// per-tile digit histograms stored tile-major, one exclusive scan per payload over
+// (digit, tile) = the global output offsets, stable ballot-multisplit tile ranking +
+// scatter).  The keys end up ordered by their top 24 bits -- a "group" = one sign, exponent
+// and top 15 mantissa bits, i.e. values within 2^-15 relative -- with the low byte unordered
+// inside a group; the fourth pass is not needed because every query below resolves the one
+// group it touches.  On the group-sorted keys:
+//   * the quantile init c_k = v_(floor((2k+1) n / 2K)) is an exact order statistic: the
+//     rank falls in the group of the key at that position; the keys of smaller groups are
+//     counted and the group's low bytes histogrammed by one warp;
 //   * a Lloyd step needs, for each threshold b_k, C_k = #{v <= b_k} and
-//     S_k = sum_{v <= b_k} fix(v): C_k is an upper bound in the sorted keys (binary
-//     search over the super-chunk heads held in shared memory, then one warp counts
-//     inside one super-chunk read from global memory),
-//     S_k = (exclusive prefix at the super-chunk start) + the in-chunk part.
+//     S_k = sum_{v <= b_k} fix(v): the super-chunk heads (shared memory) bound the keys of
+//     b_k's group to a few super-chunks, which one warp reads, counting and summing the keys
+//     <= b_k; everything before them is below b_k (exclusive prefix of fix at their start).
 //     Cluster k = (b_{k-1}, b_k], i.e. label(v) = #{k : v > b_k}, ties to the lower
 //     cluster -- the same decision the oracle takes per element.
 // fix(v) = round(v 2^F) as int64 with F chosen from max|v| and n so no sum overflows:
@@ -140,7 +143,8 @@ __device__ __forceinline__ void flush_hist(const uint32_t *sh, uint32_t *hp, int
     hp[(long long)t * 256 + threadIdx.x] = sh[threadIdx.x];  // KT == 256 digits
 }
 
-// keys of the raw payload (padding keys sort last) + digit-0 histogram
+// keys of the raw payload (padding keys sort last) + the histogram of the first sorted digit
+// (bits 8..15: the low byte is never sorted, see kmeans_encode)
 __global__ void __launch_bounds__(KT) km_keys(const float *const *vin, KmPtr w) {
     __shared__ uint32_t sh[256], wc[KT / 32 * 256];
     const int b = blockIdx.y, t = blockIdx.x;
@@ -149,10 +153,10 @@ __global__ void __launch_bounds__(KT) km_keys(const float *const *vin, KmPtr w) 
     uint32_t k[KI];
 #pragma unroll
     for (int r = 0; r < KI; r++) k[r] = (i0 + r * 32 < w.nv) ? f2key(v[i0 + r * 32]) : 0xffffffffu;
-    uint32_t *o = w.keysA + (long long)b * w.T * KTILE + i0;
+    uint32_t *o = w.keysB + (long long)b * w.T * KTILE + i0;
 #pragma unroll
     for (int r = 0; r < KI; r++) o[r * 32] = k[r];
-    tile_hist(k, 0, wc, sh);
+    tile_hist(k, 8, wc, sh);
     flush_hist(sh, w.hist + (long long)b * 256 * w.T, w.T, t);
 }
 
@@ -314,6 +318,23 @@ __global__ void __launch_bounds__(KT) km_csum(KmPtr w, int sh) {
 // CTA's shared memory (DSMEM, double-buffered by iteration parity), one cluster barrier
 // per iteration, and every CTA recomputes the centres from the same integers (identical
 // results).  Rank 0 writes the centres, thresholds and the final-assignment table.
+// last index i of h[0..NS) with p(h[i]) (p monotone: true, then false), -1 if none: a
+// warp-parallel search over strides 256, 8, 1 (NS <= 8192)
+template <typename Pred>
+__device__ __forceinline__ int warp_last(const uint32_t *h, int NS, Pred &&p) {
+    const int lane = threadIdx.x & 31;
+    const int i1 = lane * 256;
+    const unsigned m1 = __ballot_sync(0xffffffffu, i1 < NS && p(h[i1]));
+    if (!m1) return -1;
+    const int b1 = (31 - __clz(m1)) * 256;
+    const int i2 = b1 + lane * 8;
+    const unsigned m2 = __ballot_sync(0xffffffffu, i2 < NS && p(h[i2]));
+    const int b2 = b1 + (31 - __clz(m2)) * 8;
+    const int i3 = b2 + lane;
+    const unsigned m3 = __ballot_sync(0xffffffffu, lane < 8 && i3 < NS && p(h[i3]));
+    return b2 + (31 - __clz(m3));
+}
+
 constexpr int LCL = 8;    // CTAs per payload (portable cluster size)
 constexpr int LCT = 256;  // threads per CTA: LCL * 8 warps >= 64 thresholds
 __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPtr w, int iters, int sh) {
@@ -330,6 +351,7 @@ __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPt
     uint32_t *shead = reinterpret_cast<uint32_t *>(spre + NS);        // [NS] first key of each super-chunk
     __shared__ float cen[256], thr[256];
     __shared__ long long Cs[2][256], Ss[2][256], total_s;
+    __shared__ uint32_t lhist[LCT / 32 * 256];  // per-warp low-byte histograms (quantile init)
     const int rank = (int)cluster.block_rank();
     const int b = blockIdx.x / LCL, K = w.K;
     const long long nv = w.nv, nch = (long long)T * CPT;
@@ -378,11 +400,67 @@ __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPt
             }
         }
     }
-    // quantile init: c_k = v_(floor((2k+1) nv / 2K))
-    for (int k = threadIdx.x; k < K; k += LCT) cen[k] = key2f(sorted[((long long)(2 * k + 1) * nv) / (2LL * K)]);
-    cluster.sync();  // every CTA of the cluster started (DSMEM targets exist) and staged
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int per_lane = S / 32;
+    cluster.sync();  // every CTA of the cluster started (DSMEM targets exist) and staged
+    // The keys are ordered by group (top 24 bits), unordered inside a group.  Keys of the
+    // super-chunks [c_lo, c_hi] cover group g entirely: c_hi = the last super-chunk whose head
+    // is in a group <= g, c_lo = the last one whose head is in a group < g (0 if none); every
+    // key before c_lo's start is in a smaller group, every key after c_hi's end in a larger one.
+    auto group_range = [&](uint32_t g, long long &beg, long long &end) -> bool {
+        const int c_hi = warp_last(shead, NS, [&](uint32_t h) { return (h >> 8) <= g; });
+        if (c_hi < 0) return false;  // every key is in a larger group
+        const int c_lo = max(0, warp_last(shead, NS, [&](uint32_t h) { return (h >> 8) < g; }));
+        beg = (long long)c_lo * S;
+        end = min(nv, (long long)(c_hi + 1) * S);
+        return true;
+    };
+    // quantile init: c_k = v_(floor((2k+1) nv / 2K)), the exact order statistic: rank r falls in
+    // the group of the key at position r; keys of smaller groups are counted and the low bytes of
+    // the group's keys histogrammed (one warp per k), then the byte holding the rank; c_k goes to
+    // every CTA's shared memory
+    uint32_t *wh = lhist + warp * 256;
+    for (int k = rank + LCL * warp; k < K; k += LCL * (LCT / 32)) {
+        const long long r = ((long long)(2 * k + 1) * nv) / (2LL * K);
+        const uint32_t g = sorted[r] >> 8;
+        long long beg = 0, end = 0;
+        group_range(g, beg, end);  // non-empty: position r is in group g
+        for (int d = lane; d < 256; d += 32) wh[d] = 0u;
+        __syncwarp();
+        int below = 0;
+        for (long long i = beg + lane; i < end; i += 32) {
+            const uint32_t e = sorted[i];
+            if ((e >> 8) < g) below++;
+            else if ((e >> 8) == g) atomicAdd(&wh[e & 255u], 1u);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+        __syncwarp();
+        const uint32_t rr = (uint32_t)(r - beg - below);  // rank inside the group
+        uint32_t c8[8], s8 = 0;
+#pragma unroll
+        for (int u = 0; u < 8; u++) { c8[u] = wh[lane * 8 + u]; s8 += c8[u]; }
+        uint32_t inc = s8;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const unsigned own = __ballot_sync(0xffffffffu, rr >= inc - s8 && rr < inc);
+        const int L = __ffs(own) - 1;
+        uint32_t dsel = 0;
+        if (lane == L) {
+            uint32_t e = inc - s8;
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                if (rr < e + c8[u]) { dsel = lane * 8 + u; break; }
+                e += c8[u];
+            }
+        }
+        dsel = __shfl_sync(0xffffffffu, dsel, L);
+        if (lane < LCL) *cluster.map_shared_rank(&cen[k], lane) = key2f((g << 8) | dsel);
+        __syncwarp();
+    }
+    cluster.sync();  // the initial centres delivered everywhere
     for (int it = 0; it < iters; it++) {
         const int buf = it & 1;
         for (int k = threadIdx.x; k + 1 < K; k += LCT) thr[k] = (float)(((double)cen[k] + (double)cen[k + 1]) * 0.5);
@@ -390,32 +468,23 @@ __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPt
         const int kk = rank + LCL * warp;  // this warp's threshold (at most one: K <= 256 < LCL * 8 * 4)
         for (int k0 = kk; k0 + 1 < K; k0 += LCL * (LCT / 32)) {
             const uint32_t kb = f2key(thr[k0]);
-            // last super-chunk whose head key <= kb: warp-parallel search over strides 256, 8, 1
-            int c = -1;
-            const int i1 = lane * 256;
-            const unsigned m1 = __ballot_sync(0xffffffffu, i1 < NS && shead[i1] <= kb);
-            if (m1) {
-                const int b1 = (31 - __clz(m1)) * 256;
-                const int i2 = b1 + lane * 8;
-                const unsigned m2 = __ballot_sync(0xffffffffu, i2 < NS && shead[i2] <= kb);
-                const int b2 = b1 + (31 - __clz(m2)) * 8;
-                const int i3 = b2 + lane;
-                const unsigned m3 = __ballot_sync(0xffffffffu, lane < 8 && i3 < NS && shead[i3] <= kb);
-                c = b2 + (31 - __clz(m3));
-            }
+            long long beg = 0, end = 0;
+            const bool any = group_range(kb >> 8, beg, end);  // keys before beg < kb < keys after end
             int cnt = 0;
             long long sm = 0;
-            if (c >= 0) {
-                for (int u0 = 0; u0 < per_lane; u0 += 4) {
+            if (any) {
+                long long i = beg + lane;
+                for (; i + 96 < end; i += 128) {  // four loads of a lane in flight
                     uint32_t e[4];
 #pragma unroll
-                    for (int u = 0; u < 4; u++) e[u] = sorted[(long long)c * S + 32 * (u0 + u) + lane];
+                    for (int u = 0; u < 4; u++) e[u] = sorted[i + 32 * u];
 #pragma unroll
                     for (int u = 0; u < 4; u++)
-                        if (e[u] <= kb && (long long)c * S + 32 * (u0 + u) + lane < nv) {
-                            cnt++;
-                            sm += __double2ll_rn((double)key2f(e[u]) * scale);
-                        }
+                        if (e[u] <= kb) { cnt++; sm += __double2ll_rn((double)key2f(e[u]) * scale); }
+                }
+                for (; i < end; i += 32) {
+                    const uint32_t e = sorted[i];
+                    if (e <= kb) { cnt++; sm += __double2ll_rn((double)key2f(e) * scale); }
                 }
             }
 #pragma unroll
@@ -423,7 +492,8 @@ __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPt
                 cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
                 sm += __shfl_xor_sync(0xffffffffu, sm, o);
             }
-            const long long cv = c >= 0 ? (long long)c * S + cnt : 0;
+            const int c = any ? (int)(beg / S) : -1;
+            const long long cv = c >= 0 ? beg + cnt : 0;
             const long long sv = c >= 0 ? spre[c] + sm : 0;
             if (lane < LCL) {  // lane r stores into CTA r's shared memory
                 *cluster.map_shared_rank(&Cs[buf][k0], lane) = cv;
@@ -632,17 +702,20 @@ int kmeans_encode(const float *const *v, KmeansWork &ws, int lloyd, uint8_t *con
     const int P = ws.P;
     if (P == 0) return 0;
     const dim3 tiles(ws.T, P);
+    // LSD passes on the key bytes 1, 2, 3 only: the keys end up ordered by their top 24 bits
+    // ("groups": same sign, exponent and top 15 mantissa bits), the low byte unordered inside a
+    // group -- km_lloyd resolves the groups it needs (one pass of 4 saved)
     km_keys<<<tiles, KT, 0, st>>>(v, w);
     int k = 1;
-    uint32_t *src = ws.keysA, *dst = ws.keysB;
-    for (int pass = 0; pass < 4; pass++) {
-        if (pass) { km_hist<<<tiles, KT, 0, st>>>(src, w, 8 * pass); k++; }
+    uint32_t *src = ws.keysB, *dst = ws.keysA;
+    for (int pass = 1; pass < 4; pass++) {
+        if (pass > 1) { km_hist<<<tiles, KT, 0, st>>>(src, w, 8 * pass); k++; }
         km_scan<<<dim3(256 / 32, P), SCW * 32, 0, st>>>(w);
         km_scatter<<<tiles, KT, 0, st>>>(src, dst, w, 8 * pass);
         k += 2;
         std::swap(src, dst);
     }
-    // four passes: A -> B -> A -> B -> A, sorted keys in keysA
+    // three passes: B -> A -> B -> A, group-sorted keys in keysA
     km_csum<<<tiles, KT, 0, st>>>(w, lloyd_shift(ws.T));
     km_lloyd<<<LCL * P, LCT, lloyd_smem(ws.T), st>>>(w, lloyd, lloyd_shift(ws.T));
     long long want = std::max(1LL, (148LL * 8 + P - 1) / P);
