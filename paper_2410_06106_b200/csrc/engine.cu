@@ -826,6 +826,12 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
     };
     const bool red = rule == TQ_RULE_CONSENSUS && world > 1;
     const bool exch = has_exchange();
+    const bool stop = prm.stop_tol > 0.0;
+    if (stop) setup_stop_test(s);  // allocations before any capture of this call
+    // ranks sharing a process (loopback) capture between two host fences: a thread's device
+    // allocation or graph instantiation must not overlap another rank's capture
+    const bool capturing = segs.empty() || (profiling && psegs.empty());
+    if (capturing && world > 1) tr->host_fence();
     if (segs.empty()) {
         // stages 0 | reduce | 1 | exchange | 2, merged where no communication separates them
         std::vector<int> cur{0};
@@ -840,7 +846,7 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
         capture(psegs, {1}, exch ? COMM_EXCHANGE : COMM_NONE);
         capture(psegs, {2}, COMM_NONE);
     }
-    const bool stop = prm.stop_tol > 0.0;
+    if (capturing && world > 1) tr->host_fence();
     // one rank without communication steps: a second graph holding MULTI iterations (built
     // with the first, i.e. during warm-up) cuts the graph-to-graph boundaries of long runs
     if (!stop && !profiling && segs.size() == 1 && segs[0].comm == COMM_NONE && !seg2.exec) {
@@ -867,7 +873,6 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
         pev.resize(5 * (size_t)iters);
         for (size_t k = old; k < pev.size(); k++) TQ_CHECK_CUDA(cudaEventCreate(&pev[k]));
     }
-    if (stop) setup_stop_test(s);
     auto comm_step = [&](int comm) {
         if (comm == COMM_REDUCE) reduce_sums(s);
         else if (comm == COMM_EXCHANGE) exchange(s);

@@ -280,6 +280,8 @@ struct LoopTransport : Transport {
         wait_peers_done(s);  // partial sums stay until every owner has read them
     }
 
+    void host_fence() override { W->barrier(); }
+
     double allreduce_max(double v, cudaStream_t s) override {
         (void)s;
         W->slot[rank].hv = v;

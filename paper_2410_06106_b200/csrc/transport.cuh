@@ -67,6 +67,9 @@ struct Transport {
     virtual void reduce_sum(cudaStream_t s, double *base, const std::vector<SumSeg> &segs) = 0;
     // blocking: maximum of a host scalar over ranks (the stop test of tq_params.stop_tol)
     virtual double allreduce_max(double v, cudaStream_t s) = 0;
+    // host rendezvous of the ranks of one process (loopback): no rank allocates device memory
+    // or instantiates graphs while another rank's thread is capturing one; no-op for NCCL
+    virtual void host_fence() {}
 };
 
 // id: an NCCL unique id (from tq_nccl_unique_id) or a loopback world id (tq_loopback_id)
