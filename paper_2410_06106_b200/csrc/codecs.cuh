@@ -68,12 +68,14 @@ struct JpegWork {
     int P = 0, R = 0, nint = 0;
     long long nv = 0;
     int16_t *coef = nullptr;        // [P][nv] coefficients (encode input / decode output)
-    long long *len = nullptr;       // [P][nint] interval bytes (encode)
-    long long *off = nullptr;       // [P][nint] interval offsets (encode) / starts (decode)
+    long long *len = nullptr;       // [P][nint] interval bytes after stuffing, marker included (encode)
+    long long *ulen = nullptr;      // [P][nint] interval bytes before stuffing (encode)
+    long long *csum = nullptr;      // [P][coder CTAs] stuffed bytes per coder CTA (encode)
+    long long *off = nullptr;       // [P][nint] interval starts (decode)
     unsigned *status = nullptr;     // [P][2]: header word, flags (1 category, 16 slot overflow -> raw;
                                     // decode: 2 markers, 4 code, 8 overrun)
     long long *enc_bytes = nullptr; // [P] payload bytes of the last encode (header included)
-    uint8_t *scratch = nullptr;     // [P][nint][128 R + 16] per-interval coder output (encode)
+    uint8_t *scratch = nullptr;     // [P][nint][128 R + 16] per-interval stream before stuffing (encode)
     void alloc(int P, long long nv, int R);
     void release();
 };

@@ -221,6 +221,35 @@ def test_jpeg_entropy_bit_exact(rows, cols, q, restart):
     assert np.array_equal(dec.cpu().numpy(), coef_r)
 
 
+@pytest.mark.parametrize("restart", [1, 3, 64, 128, 129, 200])
+def test_jpeg_entropy_dense_blocks_and_stuffing(restart):
+    """Dense blocks (every AC coefficient non-zero, categories 1..7 -- up to ~950 coded
+    bits per block, so long intervals cycle the warp coder's bit ring many times) mixed
+    with sparse and all-zero blocks and values chosen so 0xFF bytes (stuffed 0x00) are
+    frequent; byte-identical to the oracle's sequential coder, decoded back exactly."""
+    rng = np.random.default_rng(restart)
+    nb = 300
+    c = np.zeros((nb, 64), np.int16)
+    kind = rng.integers(0, 4, size=nb)
+    for b in range(nb):
+        if kind[b] == 0:    # dense, random categories
+            mag = rng.integers(1, 128, size=64)
+            c[b] = mag * rng.choice([-1, 1], size=64)
+        elif kind[b] == 1:  # all ones: long runs of 1-bits (0xFF bytes) in the codes
+            c[b] = -1
+        elif kind[b] == 2:  # sparse with long zero runs (ZRL)
+            idx = rng.choice(64, size=3, replace=False)
+            c[b, idx] = rng.integers(-300, 300, size=3)
+    c[:, 0] = rng.integers(-1000, 1000, size=nb)
+    flat = c.ravel()
+    ref = oracle.jpeg_encode(flat, restart)
+    assert ref.count(b"\xff\x00") > 10
+    got = tomoq.jpeg_encode(torch.tensor(flat, device=DEV), restart).cpu().numpy().tobytes()
+    assert got == ref
+    back = tomoq.jpeg_decode(torch.tensor(np.frombuffer(ref, np.uint8).copy(), device=DEV), nb, restart)
+    assert np.array_equal(back.cpu().numpy(), flat)
+
+
 def test_jpeg_entropy_extremes_and_errors():
     zz = oracle.jpeg_zigzag()
     rng = np.random.default_rng(7)
