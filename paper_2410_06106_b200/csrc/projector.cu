@@ -685,7 +685,7 @@ __global__ void fp_setup_kernel(const RayRow *rows, const int *xmaj, const doubl
     const double2 t2 = trig[ang];
     const LineGeo G = line_geo(t2.x, t2.y, O, N);
     const double c0 = 0.5 * (double)(n_det - 1);
-    if (blockIdx.x == 0 && threadIdx.x == 0) rgeo[row] = FpRowGeo{G.at, G.B};
+    if (blockIdx.x == 0 && threadIdx.x == 0) rgeo[row] = FpRowGeo{G.at, G.B, G.a0};
     for (int tile = blockIdx.x * blockDim.x + threadIdx.x; tile < ntiles; tile += gridDim.x * blockDim.x) {
         const int lt = tile / nt_cross, ct = tile % nt_cross;
         const int L0 = lt * FP_TH, X0 = ct * FP_TW;
@@ -813,7 +813,34 @@ __global__ void __launch_bounds__(RJ * RG) fp_reduce_kernel(const FpRedArgs<T> a
 }
 
 // fp32: four bins per thread (16-byte slot loads; the slot rows are padded to a multiple of
-// four bins and the padding is never written, so it stays zero), RQ quads x RG band groups
+// four bins and the padding is never written, so it stays zero), RQ quads x RG band groups.
+// With the row geometry (a.rgeo) a quad reads only the parity slots of the cross tiles its
+// rays can cross in each band: the rays' cross coordinate over the band's lines, widened
+// by a margin that covers the windows' padding (fp_setup_kernel), selects the cross tiles;
+// the other slots are never written, i.e. zero, and are skipped (the sum is unchanged).
+struct FpNeed {  // fp32 row geometry of one quad for fp_band_need
+    float ca, cb, B, M;
+    int N, nt_cross;
+};
+__device__ __forceinline__ unsigned fp_band_need(const FpNeed &n, int lt) {
+    const int L0 = lt * FP_TH, L1 = min(L0 + FP_TH, n.N) - 1;
+    const float bA = (float)L0 * n.B, bB = (float)L1 * n.B;
+    const float cmin = n.ca + fminf(bA, bB) - n.M, cmax = n.cb + fmaxf(bA, bB) + n.M;
+    const int lo = max(0, __float2int_rd(cmin * (1.0f / FP_TW)));
+    const int hi = min(n.nt_cross - 1, __float2int_rd(cmax * (1.0f / FP_TW)));
+    // bit 0: the even-parity slot, bit 1: the odd one
+    return lo < hi ? 3u : (lo == hi ? 1u << (lo & 1) : 0u);
+}
+// 16-byte L2 load issued under a predicate (zeros otherwise): a run of these stays one
+// batch of independent loads instead of a branch per load
+__device__ __forceinline__ float4 ldcg_if(const float4 *p, unsigned c) {
+    float4 v;
+    asm(
+        "{\n .reg .pred q;\n setp.ne.u32 q, %5, 0;\n mov.b32 %0, 0;\n mov.b32 %1, 0;\n mov.b32 %2, 0;\n mov.b32 %3, 0;\n"
+        " @q ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];\n}"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "r"(c));
+    return v;
+}
 constexpr int RQ = 32;
 template <bool RESID>
 __global__ void __launch_bounds__(RQ * RG) fp_reduce_f32(const FpRedArgs<float> a) {
@@ -829,11 +856,29 @@ __global__ void __launch_bounds__(RQ * RG) fp_reduce_f32(const FpRedArgs<float> 
     if (j0 < a.n_det) {
         const float4 *p = reinterpret_cast<const float4 *>(a.partial + (long long)row * nb * 2 * nd + j0);
         const int nq = nd / 4;  // slot row stride in quads
+        // cross coordinate range of the quad's rays before the line term (a.rgeo: see above);
+        // fp32 is ample: |error| << the margin M of the windows' padding
+        FpNeed nn{-1e30f, 1e30f, 0.f, 0.f, a.N, a.nt_cross};
+        if (a.rgeo) {
+            const FpRowGeo G = a.rgeo[row];
+            const double c0 = 0.5 * (double)(a.n_det - 1);
+            const double u0 = ((double)j0 - c0) * G.at, u1 = ((double)(j0 + 3) - c0) * G.at;
+            nn.ca = (float)(G.a0 + fmin(u0, u1));
+            nn.cb = (float)(G.a0 + fmax(u0, u1));
+            nn.B = (float)G.B;
+            nn.M = (float)(8.0 + 3.0 * fabs(G.at));
+        }
         int lt = l0;
-        for (; lt + 4 <= l1; lt += 4) {  // 8 quads in flight
+        for (; lt + 4 <= l1; lt += 4) {  // up to 8 quads in flight
+            unsigned nm[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) nm[u] = a.rgeo ? fp_band_need(nn, lt + u) : 3u;
             float4 x[8];
 #pragma unroll
-            for (int u = 0; u < 8; u++) x[u] = __ldcg(p + (2 * lt + u) * nq);
+            for (int u = 0; u < 4; u++) {
+                x[2 * u] = ldcg_if(p + (2 * (lt + u)) * nq, nm[u] & 1u);
+                x[2 * u + 1] = ldcg_if(p + (2 * (lt + u) + 1) * nq, nm[u] & 2u);
+            }
 #pragma unroll
             for (int u = 0; u < 8; u += 2) {
                 acc.x += x[u].x + x[u + 1].x;
@@ -843,7 +888,8 @@ __global__ void __launch_bounds__(RQ * RG) fp_reduce_f32(const FpRedArgs<float> 
             }
         }
         for (; lt < l1; lt++) {
-            const float4 x0 = __ldcg(p + 2 * lt * nq), x1 = __ldcg(p + (2 * lt + 1) * nq);
+            const unsigned nm = a.rgeo ? fp_band_need(nn, lt) : 3u;
+            const float4 x0 = ldcg_if(p + 2 * lt * nq, nm & 1u), x1 = ldcg_if(p + (2 * lt + 1) * nq, nm & 2u);
             acc.x += x0.x + x1.x;
             acc.y += x0.y + x1.y;
             acc.z += x0.z + x1.z;

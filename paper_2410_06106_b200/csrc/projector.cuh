@@ -57,8 +57,8 @@ struct FpWin {
     double kap;
     int jlo, W;
 };
-struct FpRowGeo {   // per ray row: cross step per bin and per line
-    double at, B;
+struct FpRowGeo {   // per ray row: cross step per bin and per line, cross coordinate of bin c0 on line 0
+    double at, B, a0;
 };
 
 // The same, per (tile, position in the orientation-grouped row list `olist`), laid out
@@ -130,6 +130,8 @@ struct FpRedArgs {
     int out_stride, out_off;
     int N, n_det, nt_line;
     const double4 *rowc;   // [n_rows] as BpArgs::rowc (m in .z), or null
+    const FpRowGeo *rgeo;  // [n_rows] (fp32): skip the slots no tile of the row writes; null: read all
+    int nt_cross;
 };
 
 template <typename T>

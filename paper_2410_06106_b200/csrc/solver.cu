@@ -114,14 +114,14 @@ int Inner::project(const DevGeom &g, const void *img, bool resid, cudaStream_t s
                         nt_line, nt_cross, kMagicBits4, frec, n_olist, L, futab, g.proj};
         launch_fp(0, &a, L, st);
         FpRedArgs<float> r{(const float *)fpart, rows, g.trig, g.xmaj, (const float *)D, (float *)out,
-                           out_stride, out_off, g.N, g.n_det, nt_line, rowc};
+                           out_stride, out_off, g.N, g.n_det, nt_line, rowc, frg, nt_cross};
         launch_fp_reduce(0, resid, &r, n_rows, g.n_det, st);
     } else {
         FpArgs<double> a{(const double *)img, n, g.N, g.n_det, olist, oofs, fwin, frg, (double *)fpart,
                          nt_line, nt_cross, kMagicBits4, frec, n_olist, L, futab, g.proj};
         launch_fp(1, &a, L, st);
         FpRedArgs<double> r{(const double *)fpart, rows, g.trig, g.xmaj, (const double *)D,
-                            (double *)out, out_stride, out_off, g.N, g.n_det, nt_line, rowc};
+                            (double *)out, out_stride, out_off, g.N, g.n_det, nt_line, rowc, nullptr, nt_cross};
         launch_fp_reduce(1, resid, &r, n_rows, g.n_det, st);
     }
     return 3;
