@@ -336,6 +336,7 @@ __device__ __forceinline__ int warp_last(const uint32_t *h, int NS, Pred &&p) {
 }
 
 constexpr int LCL = 8;    // CTAs per payload (portable cluster size)
+constexpr int LQ = 16;    // keys per lane in flight in the group scans
 constexpr int LCT = 256;  // threads per CTA: LCL * 8 warps >= 64 thresholds
 __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPtr w, int iters, int sh) {
     namespace cg = cooperative_groups;
@@ -427,10 +428,16 @@ __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPt
         for (int d = lane; d < 256; d += 32) wh[d] = 0u;
         __syncwarp();
         int below = 0;
-        for (long long i = beg + lane; i < end; i += 32) {
-            const uint32_t e = sorted[i];
-            if ((e >> 8) < g) below++;
-            else if ((e >> 8) == g) atomicAdd(&wh[e & 255u], 1u);
+        for (long long i0 = beg + lane; i0 < end; i0 += 32 * LQ) {
+            uint32_t e[LQ];
+#pragma unroll
+            for (int u = 0; u < LQ; u++) e[u] = i0 + 32 * u < end ? __ldg(sorted + i0 + 32 * u) : 0xffffffffu;
+#pragma unroll
+            for (int u = 0; u < LQ; u++) {
+                if (i0 + 32 * u >= end) continue;
+                if ((e[u] >> 8) < g) below++;
+                else if ((e[u] >> 8) == g) atomicAdd(&wh[e[u] & 255u], 1u);
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
@@ -472,19 +479,14 @@ __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPt
             const bool any = group_range(kb >> 8, beg, end);  // keys before beg < kb < keys after end
             int cnt = 0;
             long long sm = 0;
-            if (any) {
-                long long i = beg + lane;
-                for (; i + 96 < end; i += 128) {  // four loads of a lane in flight
-                    uint32_t e[4];
+            if (any) {  // rounds of LQ loads per lane in flight (one L2 round trip per 32 LQ keys)
+                for (long long i0 = beg + lane; i0 < end; i0 += 32 * LQ) {
+                    uint32_t e[LQ];
 #pragma unroll
-                    for (int u = 0; u < 4; u++) e[u] = sorted[i + 32 * u];
+                    for (int u = 0; u < LQ; u++) e[u] = i0 + 32 * u < end ? __ldg(sorted + i0 + 32 * u) : 0u;
 #pragma unroll
-                    for (int u = 0; u < 4; u++)
-                        if (e[u] <= kb) { cnt++; sm += __double2ll_rn((double)key2f(e[u]) * scale); }
-                }
-                for (; i < end; i += 32) {
-                    const uint32_t e = sorted[i];
-                    if (e <= kb) { cnt++; sm += __double2ll_rn((double)key2f(e) * scale); }
+                    for (int u = 0; u < LQ; u++)
+                        if (i0 + 32 * u < end && e[u] <= kb) { cnt++; sm += __double2ll_rn((double)key2f(e[u]) * scale); }
                 }
             }
 #pragma unroll
