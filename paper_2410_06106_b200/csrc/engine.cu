@@ -5,9 +5,21 @@
 #include <cstring>
 #include <set>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "engine.cuh"
 
 namespace tq {
+
+// NVTX ranges (header-only NVTX v3; free when no tool is attached): host phases of the API
+// and, around each graph launch, the ADMM phase its kernels belong to, so `ncu --nvtx
+// --nvtx-include "tq:encode/"` (or a timeline tool) selects one phase's kernels
+struct Nvtx {
+    explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx &) = delete;
+    Nvtx &operator=(const Nvtx &) = delete;
+};
 
 [[noreturn]] void fail(tq_status code, const std::string &msg) { throw Error{code, msg}; }
 
@@ -320,6 +332,7 @@ void Ctx::set_quant(const tq_quant &qq) {
 
 void Ctx::set_sinogram(int slice, int node, const float *d, long long len, bool on_device, cudaStream_t src_s,
                        bool has_src_s) {
+    Nvtx nv("tq:set_sinogram");
     TQ_REQUIRE(slice >= 0 && slice < S, "slice out of range");
     TQ_REQUIRE(node >= -1 && node < M, "node out of range");
     TQ_REQUIRE(d != nullptr, "null sinogram");
@@ -786,6 +799,7 @@ void Ctx::run(int iters, cudaStream_t user) {
 void Ctx::run_async(int iters, cudaStream_t user) { enqueue(iters, user); }
 
 void Ctx::enqueue(int iters, cudaStream_t user) {
+    Nvtx nv("tq:run");
     TQ_REQUIRE(iters >= 0, "iters must be >= 0");
     if (!have_params) fail(TQ_ESTATE, "tq_set_params must be called before tq_run");
     for (int i = 0; i < L; i++)
@@ -807,6 +821,7 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
         need_rhs = false;
     }
     auto capture = [&](std::vector<Seg> &into, const std::vector<int> &ids, int comm_after) {
+        Nvtx nc("tq:capture");
         cudaGraph_t g;
         TQ_CHECK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         int c = 0;
@@ -874,27 +889,33 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
         for (size_t k = old; k < pev.size(); k++) TQ_CHECK_CUDA(cudaEventCreate(&pev[k]));
     }
     auto comm_step = [&](int comm) {
-        if (comm == COMM_REDUCE) reduce_sums(s);
-        else if (comm == COMM_EXCHANGE) exchange(s);
+        if (comm == COMM_REDUCE) { Nvtx nc("tq:reduce"); reduce_sums(s); }
+        else if (comm == COMM_EXCHANGE) { Nvtx nc("tq:exchange"); exchange(s); }
     };
+    // phase of the stage graphs (psegs / a segment starting at stage 0, 1 or 2)
+    static const char *const kPhase[3] = {"tq:inner_solve", "tq:encode", "tq:decode_dual"};
     TQ_CHECK_CUDA(cudaEventRecord(ev0, s));
     int it0 = 0, done = 0;
     st.rel_change_last = -1.0;
     if (seg2.exec && !stop && !profiling)
-        for (; it0 + MULTI <= iters; it0 += MULTI) TQ_CHECK_CUDA(cudaGraphLaunch(seg2.exec, s));
+        for (; it0 + MULTI <= iters; it0 += MULTI) {
+            Nvtx ni("tq:iterations");
+            TQ_CHECK_CUDA(cudaGraphLaunch(seg2.exec, s));
+        }
     done = it0;
     for (int it = it0; it < iters; it++) {
+        Nvtx ni("tq:iteration");
         if (profiling) {
             cudaEvent_t *e = &pev[5 * (size_t)it];
             TQ_CHECK_CUDA(cudaEventRecord(e[0], s));
-            TQ_CHECK_CUDA(cudaGraphLaunch(psegs[0].exec, s));
+            { Nvtx np(kPhase[0]); TQ_CHECK_CUDA(cudaGraphLaunch(psegs[0].exec, s)); }
             comm_step(psegs[0].comm);
             TQ_CHECK_CUDA(cudaEventRecord(e[1], s));
-            TQ_CHECK_CUDA(cudaGraphLaunch(psegs[1].exec, s));
+            { Nvtx np(kPhase[1]); TQ_CHECK_CUDA(cudaGraphLaunch(psegs[1].exec, s)); }
             TQ_CHECK_CUDA(cudaEventRecord(e[2], s));
             comm_step(psegs[1].comm);
             TQ_CHECK_CUDA(cudaEventRecord(e[3], s));
-            TQ_CHECK_CUDA(cudaGraphLaunch(psegs[2].exec, s));
+            { Nvtx np(kPhase[2]); TQ_CHECK_CUDA(cudaGraphLaunch(psegs[2].exec, s)); }
             TQ_CHECK_CUDA(cudaEventRecord(e[4], s));
         } else {
             for (auto &g : segs) {
@@ -984,6 +1005,7 @@ void Ctx::set_profiling(bool on) {
 // guard (SPEC "divergence guard"; the norms of its last iteration).
 void Ctx::finish() {
     if (!pending) return;
+    Nvtx nv("tq:wait");
     pending = false;
     TQ_CHECK_CUDA(cudaEventSynchronize(run_done));
     if (guards_enabled()) {  // TQ_GUARD=1: the run wrote nothing outside its allocations
@@ -1048,6 +1070,7 @@ void Ctx::snapshot_image(int slice, int node, float *d, cudaStream_t stream) {
 }
 
 void Ctx::get_image(int slice, int node, float *out, long long len, bool on_device) {
+    Nvtx nv("tq:get_image");
     TQ_REQUIRE(len == n, "image length must be N*N");
     finish();
     TQ_CHECK_CUDA(cudaSetDevice(device));
@@ -1069,6 +1092,7 @@ void Ctx::get_image(int slice, int node, float *out, long long len, bool on_devi
 }
 
 void Ctx::get_image_async(int slice, int node, float *out, long long len, bool on_device, cudaStream_t s) {
+    Nvtx nv("tq:get_image_async");
     TQ_REQUIRE(len == n, "image length must be N*N");
     TQ_CHECK_CUDA(cudaSetDevice(device));
     const int b = img_buf;
