@@ -89,10 +89,20 @@ class ClockSampler:
 
 
 def vu_per_iter(cfg):
-    """voxel-updates per ADMM iteration over all nodes: (E1+1) A/A^T pairs (CG), each
-    N^2 x (angles of the node) VU; summed over nodes = N^2 x n_angles."""
+    """voxel-updates per ADMM iteration over all nodes, counted algorithmically (the same
+    count for both arms and every round): the standard CG formulation's (E1+1) A/A^T pairs
+    (residual + E1 steps), each N^2 x (angles of the node) VU; summed over nodes = N^2 x
+    n_angles.  The CUDA path executes one backprojection fewer per
+    solve (the last step's r update is never used): see projector_applications."""
     apps = (cfg.e1 + 1) if cfg.inner == 1 else cfg.e1
     return 2 * apps * cfg.N * cfg.N * cfg.n_angles * cfg.slices
+
+
+def projector_applications(cfg):
+    """(algorithmic, executed) projector applications (A or A^T) per ADMM iteration."""
+    if cfg.inner == 1:
+        return 2 * (cfg.e1 + 1), 2 * cfg.e1 + 1
+    return 2 * cfg.e1, 2 * cfg.e1
 
 
 def sm_count():
@@ -424,11 +434,11 @@ def main():
         b.record(stream)
         torch.cuda.synchronize()
         comp_ms[comp] = a.elapsed_time(b) / reps
-    apps = cfg.e1 + 1
-    share = {c: comp_ms[c] * apps / (ms / args.steps) for c in comp_ms}
+    apps = {0: cfg.e1 + 1, 1: cfg.e1}  # forward launches / backprojections (E1 - 1 CG + 1 residual) per iteration
+    share = {c: comp_ms[c] * apps[c] / (ms / args.steps) for c in comp_ms}
     dom = max(comp_ms, key=lambda c: comp_ms[c])
     names = {0: "forward projector A p (fp_persist_f32 tile pass + fp_reduce)",
-             1: "backprojector A^T s + c p with fused p.q (bp_tile_kernel<float,CGQ>)"}
+             1: "backprojector A^T s + c p with the fused CG residual update r -= alpha q (bp_tile_kernel<float,CGR>)"}
     achieved = comp_units[dom] / (comp_ms[dom] / 1e3) / 1e9
     n_sm = sm_count()
     peak_vu = LSU_VU_PER_CLK_SM * n_sm * pk["sm_max_mhz"] * 1e6 / 1e9
@@ -494,6 +504,8 @@ def main():
             "config": bench_config(cfg, world),
             "admm_iters_per_s": iters_per_s,
             "vu_per_step": vu_it,
+            "projector_applications": dict(zip(("algorithmic", "executed"), projector_applications(cfg)),
+                                           vu_basis="vu_per_step counts the algorithmic applications"),
             "roofline": roofline,
             "projector_c5_geometry": c5_geom,
             "c5_iteration": c5_iter,

@@ -442,7 +442,7 @@ long long Ctx::launch_component(int component, int reps, cudaStream_t s) {
     for (int i = 0; i < L; i++) vu += (long long)in.nang_h[i] * n;
     switch (component) {
         case 0: for (int r = 0; r < reps; r++) in.project(geo, in.P, false, s); return vu;
-        case 1: for (int r = 0; r < reps; r++) in.backproject(geo, EPI_CGQ, in.Q, nullptr, in.P, s); return vu;
+        case 1: for (int r = 0; r < reps; r++) in.backproject(geo, EPI_CGR, in.Q, nullptr, in.P, s, in.R); return vu;
         case 2: for (int r = 0; r < reps; r++) in.project(geo, in.X, true, s); return vu;
         case 3:
         case 4: {

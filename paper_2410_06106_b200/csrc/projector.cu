@@ -20,7 +20,7 @@ constexpr int BP_MAXA = 32;     // angles per staged batch
 // fp32 epilogues with two prefetched operands (x and b') stage 16 angles per batch, so the
 // CTA stays within a quarter of the SM's shared memory (4 CTAs/SM, as the CG variant)
 template <typename T, int EPI>
-constexpr int bp_maxa() { return (sizeof(T) == 4 && (EPI == 2 || EPI == 3)) ? 16 : BP_MAXA; }
+constexpr int bp_maxa() { return (sizeof(T) == 4 && (EPI == 2 || EPI == 3 || EPI == 4)) ? 16 : BP_MAXA; }
 
 template <typename T>
 __device__ __forceinline__ T floor_split(T x, int &i);
@@ -770,6 +770,29 @@ __device__ __forceinline__ double fp_row_m(const FpRedArgs<T> &a, int row) {
     const double2 t2 = a.trig[ang];
     return a.xmaj[ang] ? fabs(t2.y) : fabs(t2.x);
 }
+// CG step: this CTA's sum of squared outputs into the node's partials; the node's last CTA
+// adds them in index order and sets p.q = ||A p||^2 + c ||p||^2 and alpha = rr / p.q
+// (R-8).  Called by every thread of the CTA.
+template <typename T, int NT>
+__device__ __forceinline__ void fp_cg_finish(const FpRedArgs<T> &a, int row, double ss, double *red, bool *last) {
+    const double bs = block_sum<NT>(ss, red);
+    const RayRow rr = a.rows[row];
+    double *part = a.cpart + (long long)rr.node * a.part_stride;
+    if (threadIdx.x == 0) part[(long long)rr.k * gridDim.x + blockIdx.x] = bs;
+    const unsigned nb = (unsigned)a.node_nang[rr.node] * gridDim.x;
+    if (last_block_of_group(a.counter + rr.node, nb, last)) {
+        double s = 0.0;
+        for (unsigned b = threadIdx.x; b < nb; b += NT) s += __ldcg(part + b);
+        s = block_sum<NT>(s, red);
+        if (threadIdx.x == 0) {
+            double *sc = a.scal + (long long)rr.node * S_NSLOT;
+            const double pq = s + a.cnode[rr.node] * sc[S_PP];
+            sc[S_PQ] = pq;
+            sc[S_ALPHA] = pq > 0.0 ? sc[S_RR] / pq : 0.0;
+        }
+    }
+}
+
 template <typename T, bool RESID>
 __global__ void __launch_bounds__(RJ * RG) fp_reduce_kernel(const FpRedArgs<T> a) {
     __shared__ T part[RG][RJ];
@@ -802,14 +825,22 @@ __global__ void __launch_bounds__(RJ * RG) fp_reduce_kernel(const FpRedArgs<T> a
     }
     part[g][jj] = acc;
     __syncthreads();
-    if (g != 0 || j >= a.n_det) return;
-    T tot = part[0][jj];
+    double ss = 0.0;
+    if (g == 0 && j < a.n_det) {
+        T tot = part[0][jj];
 #pragma unroll
-    for (int q = 1; q < RG; q++) tot += part[q][jj];
-    const double inv_m = 1.0 / m_row;
-    T v = (T)((double)tot * inv_m);
-    if (RESID) v = a.d[(long long)row * a.n_det + j] - v;
-    a.out[(long long)row * a.out_stride + a.out_off + j] = v;
+        for (int q = 1; q < RG; q++) tot += part[q][jj];
+        const double inv_m = 1.0 / m_row;
+        T v = (T)((double)tot * inv_m);
+        if (RESID) v = a.d[(long long)row * a.n_det + j] - v;
+        a.out[(long long)row * a.out_stride + a.out_off + j] = v;
+        ss = (double)v * (double)v;
+    }
+    if (!RESID && a.cg) {
+        __shared__ double red[RJ * RG / 32 + 1];
+        __shared__ bool last;
+        fp_cg_finish<T, RJ * RG>(a, row, ss, red, &last);
+    }
 }
 
 // fp32: four bins per thread (16-byte slot loads; the slot rows are padded to a multiple of
@@ -898,24 +929,32 @@ __global__ void __launch_bounds__(RQ * RG) fp_reduce_f32(const FpRedArgs<float> 
     }
     part[g][q] = acc;
     __syncthreads();
-    if (g != 0 || j0 >= a.n_det) return;
-    float4 tot = part[0][q];
+    double ss = 0.0;
+    if (g == 0 && j0 < a.n_det) {
+        float4 tot = part[0][q];
 #pragma unroll
-    for (int r = 1; r < RG; r++) {
-        tot.x += part[r][q].x;
-        tot.y += part[r][q].y;
-        tot.z += part[r][q].z;
-        tot.w += part[r][q].w;
+        for (int r = 1; r < RG; r++) {
+            tot.x += part[r][q].x;
+            tot.y += part[r][q].y;
+            tot.z += part[r][q].z;
+            tot.w += part[r][q].w;
+        }
+        const double inv_m = 1.0 / m_row;
+        const float tv[4] = {tot.x, tot.y, tot.z, tot.w};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const int j = j0 + e;
+            if (j >= a.n_det) break;
+            float v = (float)((double)tv[e] * inv_m);
+            if (RESID) v = a.d[(long long)row * a.n_det + j] - v;
+            a.out[(long long)row * a.out_stride + a.out_off + j] = v;
+            ss += (double)v * (double)v;
+        }
     }
-    const double inv_m = 1.0 / m_row;
-    const float tv[4] = {tot.x, tot.y, tot.z, tot.w};
-#pragma unroll
-    for (int e = 0; e < 4; e++) {
-        const int j = j0 + e;
-        if (j >= a.n_det) break;
-        float v = (float)((double)tv[e] * inv_m);
-        if (RESID) v = a.d[(long long)row * a.n_det + j] - v;
-        a.out[(long long)row * a.out_stride + a.out_off + j] = v;
+    if (!RESID && a.cg) {
+        __shared__ double red[RQ * RG / 32 + 1];
+        __shared__ bool last;
+        fp_cg_finish<float, RQ * RG>(a, row, ss, red, &last);
     }
 }
 
@@ -928,7 +967,7 @@ bp_tile_kernel(const BpArgs<T> a) {
     T *win = reinterpret_cast<T *>(bp_smem);  // [BP_MAXA][BP_WB], bins pre-scaled by 1/m (fp64)
     float2 *win2 = reinterpret_cast<float2 *>(bp_smem);  // fp32: [BP_MAXA][BP_WB] pairs (s'_j, s'_{j+1})
     // fp32: the epilogue operands of the tile, prefetched with cp.async at entry so their
-    // latency overlaps the angle loop: ep[0] = vin (p or x), ep[1] = b' (RESID, GD)
+    // latency overlaps the angle loop: ep[0] = vin (p or x), ep[1] = b' (RESID, GD) or r (CGR)
     float *ep = reinterpret_cast<float *>(bp_smem + (sizeof(T) == 4 ? sizeof(float2) : sizeof(T)) * BP_MAXA * BP_WB);
     // per-angle constants of the angle loop, packed so a thread reads them with three 16-byte loads
     struct __align__(16) AngC { double tau, csd, snd, pad; T cs, sn, a1, a0; };
@@ -946,7 +985,7 @@ bp_tile_kernel(const BpArgs<T> a) {
     const int lx = lane & 7, prow = 8 * warp + (lane >> 3);  // pixel (prow + 4 ky, 8 kx + lx)
     const double h = 0.5 * (double)(N - 1), t0 = -0.5 * (double)(a.n_det - 1);
     const int nang = a.node_nang[node], row0 = a.node_row0[node];
-    constexpr int NEP = (EPI == EPI_CGQ) ? 1 : ((EPI == EPI_RESID || EPI == EPI_GD) ? 2 : 0);
+    constexpr int NEP = (EPI == EPI_CGQ) ? 1 : ((EPI == EPI_RESID || EPI == EPI_GD || EPI == EPI_CGR) ? 2 : 0);
     const bool pre = sizeof(T) == 4 && NEP > 0 && (N & 3) == 0;
     if (pre) {
         const long long nb0 = (long long)node * a.n;
@@ -1105,7 +1144,8 @@ bp_tile_kernel(const BpArgs<T> a) {
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();
     }
-    const double c = (EPI == EPI_CGQ || EPI == EPI_RESID || EPI == EPI_GD) ? a.cnode[node] : 0.0;
+    const double c = (EPI == EPI_CGQ || EPI == EPI_RESID || EPI == EPI_GD || EPI == EPI_CGR) ? a.cnode[node] : 0.0;
+    const double alpha = EPI == EPI_CGR ? a.scal[(long long)node * S_NSLOT + S_ALPHA] : 0.0;
     const float cf = (float)c;
     double dot = 0.0;
     float dotf = 0.f;
@@ -1133,6 +1173,18 @@ bp_tile_kernel(const BpArgs<T> a) {
                     a.out[p] = q;
                     dot += pv * (double)q;
                 }
+            } else if (EPI == EPI_CGR) {  // q as in CGQ, then the CG residual update r -= alpha q
+                T q;
+                if constexpr (sizeof(T) == 4) {
+                    const float pv = pre ? ep[sp] : (float)a.vin[p];
+                    q = fmaf(cf, pv, acc[ky][kx]);
+                } else {
+                    q = (T)(g + c * (double)a.vin[p]);
+                }
+                const double rv = pre ? (double)ep[BP_TS * BP_TS + sp] : (double)a.bprime[p];
+                const T rn = (T)(rv - alpha * (double)q);
+                a.out[p] = rn;
+                dot += (double)rn * (double)rn;
             } else if (EPI == EPI_RESID) {
                 const double xv = pre ? (double)ep[sp] : (double)a.vin[p];
                 const double bv = pre ? (double)ep[BP_TS * BP_TS + sp] : (double)a.bprime[p];
@@ -1146,7 +1198,7 @@ bp_tile_kernel(const BpArgs<T> a) {
                 a.out[p] = (T)(xv - a.eta[node] * (c * xv - bv - g));
             }
         }
-    if (EPI == EPI_CGQ || EPI == EPI_RESID) {
+    if (EPI == EPI_CGQ || EPI == EPI_RESID || EPI == EPI_CGR) {
         const double bs = block_sum<BP_THREADS>(dot + (double)dotf, red);
         double *part = a.partial + (long long)node * a.part_stride;
         if (threadIdx.x == 0) part[blockIdx.x] = bs;
@@ -1159,8 +1211,14 @@ bp_tile_kernel(const BpArgs<T> a) {
                 if (EPI == EPI_CGQ) {
                     sc[S_PQ] = s;
                     sc[S_ALPHA] = s > 0.0 ? sc[S_RR] / s : 0.0;
-                } else {
+                } else if (EPI == EPI_CGR) {  // as cg_update_r: beta = rr_new / rr
+                    const double rr = sc[S_RR];
+                    sc[S_RRNEW] = s;
+                    sc[S_BETA] = rr > 0.0 ? s / rr : 0.0;
                     sc[S_RR] = s;
+                } else {  // RESID: r0 and p0 = r0
+                    sc[S_RR] = s;
+                    sc[S_PP] = s;
                 }
             }
         }
@@ -1179,7 +1237,7 @@ size_t fpp_smem() { return 1024 + sizeof(float2) * FP_TH * FP2_PITCH + sizeof(fl
 int g_fpp_grid = 0;  // persistent grid: SMs x resident CTAs (projector_setup)
 template <typename T, int EPI>
 size_t bp_smem() {
-    constexpr int NEP = (EPI == EPI_CGQ) ? 1 : ((EPI == EPI_RESID || EPI == EPI_GD) ? 2 : 0);
+    constexpr int NEP = (EPI == EPI_CGQ) ? 1 : ((EPI == EPI_RESID || EPI == EPI_GD || EPI == EPI_CGR) ? 2 : 0);
     return sizeof(T) == 4 ? sizeof(float2) * bp_maxa<T, EPI>() * BP_WB + NEP * sizeof(float) * BP_TS * BP_TS
                           : sizeof(T) * BP_MAXA * BP_WB;
 }
@@ -1205,6 +1263,7 @@ void set_all_smem() {
     set_smem(bp_tile_kernel<T, EPI_CGQ>, bp_smem<T, EPI_CGQ>());
     set_smem(bp_tile_kernel<T, EPI_RESID>, bp_smem<T, EPI_RESID>());
     set_smem(bp_tile_kernel<T, EPI_GD>, bp_smem<T, EPI_GD>());
+    set_smem(bp_tile_kernel<T, EPI_CGR>, bp_smem<T, EPI_CGR>());
 }
 
 // TMA descriptors of the [L][N][N] fp32 images: a 128 x 32 (cols x rows) box for the
@@ -1276,6 +1335,7 @@ void bp_dispatch(int epi, const BpArgs<T> &A0, dim3 grid, cudaStream_t st) {
         case EPI_PLAIN: bp_tile_kernel<T, EPI_PLAIN><<<grid, BP_THREADS, bp_smem<T, EPI_PLAIN>(), st>>>(A); break;
         case EPI_CGQ: bp_tile_kernel<T, EPI_CGQ><<<grid, BP_THREADS, bp_smem<T, EPI_CGQ>(), st>>>(A); break;
         case EPI_RESID: bp_tile_kernel<T, EPI_RESID><<<grid, BP_THREADS, bp_smem<T, EPI_RESID>(), st>>>(A); break;
+        case EPI_CGR: bp_tile_kernel<T, EPI_CGR><<<grid, BP_THREADS, bp_smem<T, EPI_CGR>(), st>>>(A); break;
         default: bp_tile_kernel<T, EPI_GD><<<grid, BP_THREADS, bp_smem<T, EPI_GD>(), st>>>(A); break;
     }
 }

@@ -34,12 +34,12 @@
 
 namespace tq {
 
-enum BpEpi { EPI_PLAIN = 0, EPI_CGQ = 1, EPI_RESID = 2, EPI_GD = 3 };
+enum BpEpi { EPI_PLAIN = 0, EPI_CGQ = 1, EPI_RESID = 2, EPI_GD = 3, EPI_CGR = 4 };
 // zero elements before and after a backprojector input (rows with zero guard bins at 0 and
 // n_det + 1): the 96-bin windows are staged without bounds checks; slots outside
 // [-1, n_det] only feed pixels outside the image
 constexpr int SPAD = 256;
-enum ScalSlot { S_RR = 0, S_PQ = 1, S_ALPHA = 2, S_RRNEW = 3, S_BETA = 4, S_NORM = 5, S_NSLOT = 8 };
+enum ScalSlot { S_RR = 0, S_PQ = 1, S_ALPHA = 2, S_RRNEW = 3, S_BETA = 4, S_NORM = 5, S_PP = 6, S_NSLOT = 8 };
 
 // forward tile geometry
 constexpr int FP_TH = 32;                 // lines (major-axis steps) per tile
@@ -132,6 +132,14 @@ struct FpRedArgs {
     const double4 *rowc;   // [n_rows] as BpArgs::rowc (m in .z), or null
     const FpRowGeo *rgeo;  // [n_rows] (fp32): skip the slots no tile of the row writes; null: read all
     int nt_cross;
+    // CG step (cg != 0, not RESID): per node ||A p||^2 of the outputs, then in the node's last
+    // block alpha = rr / (||A p||^2 + c ||p||^2) into scal (p.q of the CG step, R-8)
+    int cg;
+    const int *node_nang;  // [L]
+    const double *cnode;   // [L]
+    double *scal, *cpart;  // [L][S_NSLOT], [L][part_stride]
+    unsigned *counter;
+    int part_stride;
 };
 
 template <typename T>
@@ -147,10 +155,10 @@ struct BpArgs {
     int N, n_det;
     long long n;
     // epilogue operands (node-major [L][n])
-    T *out;                  // PLAIN: g; CGQ: q; RESID: r; GD: x (in place)
+    T *out;                  // PLAIN: g; CGQ: q; RESID: r; GD: x (in place); CGR: r - alpha q
     T *out2;                 // RESID: p (= r)
-    const T *vin;            // CGQ: p; RESID/GD: x
-    const T *bprime;         // RESID/GD
+    const T *vin;            // CGQ/CGR: p; RESID/GD: x
+    const T *bprime;         // RESID/GD: b'; CGR: r
     const double *cnode;     // [L] c_i
     const double *eta;       // [L] GD step
     double *partial;         // [L][part_stride]

@@ -53,7 +53,11 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
     nt_line = ceil_div(g.N, FP_TH);
     nt_cross = ceil_div(g.N, FP_TW);
     sp = g.n_det + 2;
-    part_stride = std::max(bp_tiles(g.N), vec_blocks(n));
+    int max_nang = 0;
+    for (int c : nang_h) max_nang = std::max(max_nang, c);
+    // partials per node: backprojector tiles, vector blocks, or the forward reduction's CTAs
+    // (angles x bin blocks of >= 32 bins) of a CG step
+    part_stride = std::max({bp_tiles(g.N), vec_blocks(n), max_nang * ceil_div(g.n_det, 32), 1});
     const size_t es = esize();
     auto A = [&](void **p, size_t bytes) {
         TQ_CHECK_CUDA(cudaMalloc(p, std::max<size_t>(bytes, 16)));
@@ -107,35 +111,39 @@ void Inner::release() {
 }
 
 int Inner::project(const DevGeom &g, const void *img, bool resid, cudaStream_t st, void *out,
-                   int out_stride, int out_off) {
+                   int out_stride, int out_off, bool cg) {
     if (!out) { out = S; out_stride = sp; out_off = 1; }
     if (prec == 0) {
         FpArgs<float> a{(const float *)img, n, g.N, g.n_det, olist, oofs, fwin, frg, (float *)fpart,
                         nt_line, nt_cross, kMagicBits4, frec, n_olist, L, futab, g.proj};
         launch_fp(0, &a, L, st);
         FpRedArgs<float> r{(const float *)fpart, rows, g.trig, g.xmaj, (const float *)D, (float *)out,
-                           out_stride, out_off, g.N, g.n_det, nt_line, rowc, frg, nt_cross};
+                           out_stride, out_off, g.N, g.n_det, nt_line, rowc, frg, nt_cross,
+                           cg ? 1 : 0, nang, cnode, scal, partial, counter, part_stride};
         launch_fp_reduce(0, resid, &r, n_rows, g.n_det, st);
     } else {
         FpArgs<double> a{(const double *)img, n, g.N, g.n_det, olist, oofs, fwin, frg, (double *)fpart,
                          nt_line, nt_cross, kMagicBits4, frec, n_olist, L, futab, g.proj};
         launch_fp(1, &a, L, st);
         FpRedArgs<double> r{(const double *)fpart, rows, g.trig, g.xmaj, (const double *)D,
-                            (double *)out, out_stride, out_off, g.N, g.n_det, nt_line, rowc, nullptr, nt_cross};
+                            (double *)out, out_stride, out_off, g.N, g.n_det, nt_line, rowc, nullptr, nt_cross,
+                            cg ? 1 : 0, nang, cnode, scal, partial, counter, part_stride};
         launch_fp_reduce(1, resid, &r, n_rows, g.n_det, st);
     }
     return 3;
 }
 
-int Inner::backproject(const DevGeom &g, int epi, void *out, void *out2, const void *vin, cudaStream_t st) {
+int Inner::backproject(const DevGeom &g, int epi, void *out, void *out2, const void *vin, cudaStream_t st,
+                       const void *rin) {
+    const void *b2 = epi == EPI_CGR ? rin : BP;  // second epilogue operand: b' (RESID, GD) or r (CGR)
     if (prec == 0) {
         BpArgs<float> a{(const float *)S, sp, 1, row0, nang, rows, g.trig, g.xmaj, g.N, g.n_det, n,
-                        (float *)out, (float *)out2, (const float *)vin, (const float *)BP, cnode, eta,
+                        (float *)out, (float *)out2, (const float *)vin, (const float *)b2, cnode, eta,
                         partial, counter, scal, part_stride, kMagicBits4, g.proj, rowc};
         launch_bp(0, epi, &a, L, g.N, st);
     } else {
         BpArgs<double> a{(const double *)S, sp, 1, row0, nang, rows, g.trig, g.xmaj, g.N, g.n_det, n,
-                         (double *)out, (double *)out2, (const double *)vin, (const double *)BP, cnode,
+                         (double *)out, (double *)out2, (const double *)vin, (const double *)b2, cnode,
                          eta, partial, counter, scal, part_stride, kMagicBits4, g.proj, rowc};
         launch_bp(1, epi, &a, L, g.N, st);
     }
@@ -143,22 +151,20 @@ int Inner::backproject(const DevGeom &g, int epi, void *out, void *out2, const v
 }
 
 // CG on (A^T A + c I) x = A^T d + b' from the warm start X (R-8):
-// r0 = A^T(d - A x) + b' - c x (sinogram-space residual), then E1 steps.
+// r0 = A^T(d - A x) + b' - c x (sinogram-space residual), p0 = r0, then E1 steps of
+//   s = A p;  alpha = rr / p.q with p.q = ||s||^2 + c ||p||^2   (forward reduction)
+//   r -= alpha (A^T s + c p);  beta = rr_new / rr              (backprojector epilogue)
+//   x += alpha p;  p = r + beta p;  ||p||^2                     (vector pass)
+// -- p.q = p.(A^T A p + c p) written through A p, so q is never stored and the residual
+// update rides on the backprojection; the last step needs neither r nor beta (the next
+// solve restarts from the residual backprojection), so it has no backprojection at all.
 int Inner::cg(const DevGeom &g, int e1, cudaStream_t st) {
     int k = 0;
     k += project(g, X, true, st);
     k += backproject(g, EPI_RESID, R, P, X, st);
     for (int it = 0; it < e1; it++) {
-        k += project(g, P, false, st);
-        k += backproject(g, EPI_CGQ, Q, nullptr, P, st);
-        // the last step needs neither r nor beta (the next solve restarts from the residual
-        // backprojection): only x += alpha p
-        if (it + 1 < e1) {
-            launch_cg_update_r(prec, R, Q, n, L, scal, partial, part_stride, counter, st);
-            k++;
-        }
-        // x += alpha p (deferred from the r update: this pass reads p anyway), then the next
-        // search direction p = r + beta p (the last one is never used)
+        k += project(g, P, false, st, nullptr, 0, 0, true);
+        if (it + 1 < e1) k += backproject(g, EPI_CGR, R, nullptr, P, st, R);
         launch_cg_update_px(prec, X, P, R, n, L, scal, partial, part_stride, counter, it + 1 < e1, st);
         k++;
     }

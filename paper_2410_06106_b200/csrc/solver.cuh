@@ -55,10 +55,13 @@ struct Inner {
     int cg(const DevGeom &g, int e1, cudaStream_t st);
     int gd(const DevGeom &g, int e1, cudaStream_t st);
     int norm2(cudaStream_t st);
-    // S = (D -) A img (2 tile launches + 1 reduction); out/out_stride/out_off override S
+    // S = (D -) A img (2 tile launches + 1 reduction); out/out_stride/out_off override S;
+    // cg: the reduction also sets alpha of a CG step from ||S||^2 (see cg())
     int project(const DevGeom &g, const void *img, bool resid, cudaStream_t st, void *out = nullptr,
-                int out_stride = 0, int out_off = 0);
-    int backproject(const DevGeom &g, int epi, void *out, void *out2, const void *vin, cudaStream_t st);
+                int out_stride = 0, int out_off = 0, bool cg = false);
+    // rin: the residual r read by EPI_CGR (out may alias it)
+    int backproject(const DevGeom &g, int epi, void *out, void *out2, const void *vin, cudaStream_t st,
+                    const void *rin = nullptr);
 };
 
 }  // namespace tq

@@ -72,8 +72,10 @@ __global__ void __launch_bounds__(VT) cg_update_r(T *__restrict__ r, const T *__
     }
 }
 
-// WITH_P = false (the last CG step of an inner solve): no new direction; instead the
-// final ||x||^2 per node goes to scal[S_NORM] (the divergence check of tq_run).
+// WITH_P = true: also the new direction p = r + beta p and its ||p||^2 (scal[S_PP], for the
+// next step's p.q = ||A p||^2 + c ||p||^2).  WITH_P = false (the last CG step of an inner
+// solve): no new direction; the final ||x||^2 per node goes to scal[S_NORM] (the divergence
+// check of tq_run).
 template <typename T, bool WITH_P>
 __global__ void __launch_bounds__(VT) cg_update_px(T *__restrict__ x, T *__restrict__ p, const T *__restrict__ r,
                                                    long long n, double *scal, double *partial, int part_stride,
@@ -94,8 +96,12 @@ __global__ void __launch_bounds__(VT) cg_update_px(T *__restrict__ x, T *__restr
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 xv.v[u] = (T)((double)xv.v[u] + alpha * (double)pv.v[u]);
-                if (WITH_P) pv.v[u] = (T)((double)rv.v[u] + beta * (double)pv.v[u]);
-                else nrm += (double)xv.v[u] * (double)xv.v[u];
+                if (WITH_P) {
+                    pv.v[u] = (T)((double)rv.v[u] + beta * (double)pv.v[u]);
+                    nrm += (double)pv.v[u] * (double)pv.v[u];
+                } else {
+                    nrm += (double)xv.v[u] * (double)xv.v[u];
+                }
             }
             st4(x + i, xv);
             if (WITH_P) st4(p + i, pv);
@@ -104,10 +110,14 @@ __global__ void __launch_bounds__(VT) cg_update_px(T *__restrict__ x, T *__restr
             const T pv = p[i];
             const T xv = (T)((double)x[i] + alpha * (double)pv);
             x[i] = xv;
-            if (WITH_P) p[i] = (T)((double)r[i] + beta * (double)pv);
-            else nrm += (double)xv * (double)xv;
+            if (WITH_P) {
+                const T pn = (T)((double)r[i] + beta * (double)pv);
+                p[i] = pn;
+                nrm += (double)pn * (double)pn;
+            } else {
+                nrm += (double)xv * (double)xv;
+            }
         });
-    if (WITH_P) return;
     const double bs = block_sum<VT>(nrm, red);
     double *part = partial + (long long)node * part_stride;
     if (threadIdx.x == 0) part[blockIdx.x] = bs;
@@ -115,7 +125,7 @@ __global__ void __launch_bounds__(VT) cg_update_px(T *__restrict__ x, T *__restr
         double s = 0.0;
         for (int b = threadIdx.x; b < (int)gridDim.x; b += VT) s += __ldcg(part + b);
         s = block_sum<VT>(s, red);
-        if (threadIdx.x == 0) scal[(long long)node * S_NSLOT + S_NORM] = s;
+        if (threadIdx.x == 0) scal[(long long)node * S_NSLOT + (WITH_P ? S_PP : S_NORM)] = s;
     }
 }
 
