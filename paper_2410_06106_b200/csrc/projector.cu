@@ -770,26 +770,13 @@ __device__ __forceinline__ double fp_row_m(const FpRedArgs<T> &a, int row) {
     const double2 t2 = a.trig[ang];
     return a.xmaj[ang] ? fabs(t2.y) : fabs(t2.x);
 }
-// CG step: this CTA's sum of squared outputs into the node's partials; the node's last CTA
-// adds them in index order and sets p.q = ||A p||^2 + c ||p||^2 and alpha = rr / p.q
-// (R-8).  Called by every thread of the CTA.
+// CG step: this CTA's sum of squared outputs into cgs (see FpRedArgs::cg); all threads call it
 template <typename T, int NT>
-__device__ __forceinline__ void fp_cg_finish(const FpRedArgs<T> &a, int row, double ss, double *red, bool *last) {
+__device__ __forceinline__ void fp_cg_partial(const FpRedArgs<T> &a, int row, double ss, double *red) {
     const double bs = block_sum<NT>(ss, red);
-    const RayRow rr = a.rows[row];
-    double *part = a.cpart + (long long)rr.node * a.part_stride;
-    if (threadIdx.x == 0) part[(long long)rr.k * gridDim.x + blockIdx.x] = bs;
-    const unsigned nb = (unsigned)a.node_nang[rr.node] * gridDim.x;
-    if (last_block_of_group(a.counter + rr.node, nb, last)) {
-        double s = 0.0;
-        for (unsigned b = threadIdx.x; b < nb; b += NT) s += __ldcg(part + b);
-        s = block_sum<NT>(s, red);
-        if (threadIdx.x == 0) {
-            double *sc = a.scal + (long long)rr.node * S_NSLOT;
-            const double pq = s + a.cnode[rr.node] * sc[S_PP];
-            sc[S_PQ] = pq;
-            sc[S_ALPHA] = pq > 0.0 ? sc[S_RR] / pq : 0.0;
-        }
+    if (threadIdx.x == 0) {
+        const RayRow rr = a.rows[row];
+        a.cgs[(long long)rr.node * a.part_stride + (long long)rr.k * gridDim.x + blockIdx.x] = bs;
     }
 }
 
@@ -838,8 +825,7 @@ __global__ void __launch_bounds__(RJ * RG) fp_reduce_kernel(const FpRedArgs<T> a
     }
     if (!RESID && a.cg) {
         __shared__ double red[RJ * RG / 32 + 1];
-        __shared__ bool last;
-        fp_cg_finish<T, RJ * RG>(a, row, ss, red, &last);
+        fp_cg_partial<T, RJ * RG>(a, row, ss, red);
     }
 }
 
@@ -953,8 +939,7 @@ __global__ void __launch_bounds__(RQ * RG) fp_reduce_f32(const FpRedArgs<float> 
     }
     if (!RESID && a.cg) {
         __shared__ double red[RQ * RG / 32 + 1];
-        __shared__ bool last;
-        fp_cg_finish<float, RQ * RG>(a, row, ss, red, &last);
+        fp_cg_partial<float, RQ * RG>(a, row, ss, red);
     }
 }
 
@@ -1145,7 +1130,7 @@ bp_tile_kernel(const BpArgs<T> a) {
         __syncthreads();
     }
     const double c = (EPI == EPI_CGQ || EPI == EPI_RESID || EPI == EPI_GD || EPI == EPI_CGR) ? a.cnode[node] : 0.0;
-    const double alpha = EPI == EPI_CGR ? a.scal[(long long)node * S_NSLOT + S_ALPHA] : 0.0;
+    const double alpha = EPI == EPI_CGR ? a.scal[(long long)node * S_NSLOT + S_ALPHA] : 0.0;  // launch_cg_alpha
     const float cf = (float)c;
     double dot = 0.0;
     float dotf = 0.f;
@@ -1211,7 +1196,7 @@ bp_tile_kernel(const BpArgs<T> a) {
                 if (EPI == EPI_CGQ) {
                     sc[S_PQ] = s;
                     sc[S_ALPHA] = s > 0.0 ? sc[S_RR] / s : 0.0;
-                } else if (EPI == EPI_CGR) {  // as cg_update_r: beta = rr_new / rr
+                } else if (EPI == EPI_CGR) {  // beta = rr_new / rr
                     const double rr = sc[S_RR];
                     sc[S_RRNEW] = s;
                     sc[S_BETA] = rr > 0.0 ? s / rr : 0.0;
@@ -1377,6 +1362,8 @@ void launch_fp_setup(const RayRow *rows, const int *xmaj, const double2 *trig, i
         TQ_CHECK_CUDA(cudaGetLastError());
     }
 }
+
+int fp_reduce_blocks(int prec, int n_det) { return prec == 0 ? ceil_div(n_det, 4 * RQ) : ceil_div(n_det, RJ); }
 
 void launch_fp_reduce(int prec, bool resid, const void *args, int n_rows, int n_det, cudaStream_t st) {
     if (n_rows == 0) return;

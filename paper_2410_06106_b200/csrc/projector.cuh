@@ -132,13 +132,10 @@ struct FpRedArgs {
     const double4 *rowc;   // [n_rows] as BpArgs::rowc (m in .z), or null
     const FpRowGeo *rgeo;  // [n_rows] (fp32): skip the slots no tile of the row writes; null: read all
     int nt_cross;
-    // CG step (cg != 0, not RESID): per node ||A p||^2 of the outputs, then in the node's last
-    // block alpha = rr / (||A p||^2 + c ||p||^2) into scal (p.q of the CG step, R-8)
+    // CG step (cg != 0, not RESID): each CTA's sum of squared outputs into cgs[node][k *
+    // gridDim.x + blockIdx.x] (k = the row's angle within its node): ||A p||^2 for cg_alpha
     int cg;
-    const int *node_nang;  // [L]
-    const double *cnode;   // [L]
-    double *scal, *cpart;  // [L][S_NSLOT], [L][part_stride]
-    unsigned *counter;
+    double *cgs;           // [L][part_stride]
     int part_stride;
 };
 
@@ -181,6 +178,7 @@ void launch_fp_setup(const RayRow *rows, const int *xmaj, const double2 *trig, i
                      FpWin *wins, FpRowGeo *rgeo, const int *olist, int n_olist, FpRec *recs, const int *oofs, int L,
                      FpUnitTab *utab, cudaStream_t st);
 void launch_fp_reduce(int prec, bool resid, const void *args, int n_rows, int n_det, cudaStream_t st);
+int fp_reduce_blocks(int prec, int n_det);  // CTAs per row of launch_fp_reduce
 void launch_bp(int prec, int epi, const void *args, int L, int N, cudaStream_t st);
 
 }  // namespace tq

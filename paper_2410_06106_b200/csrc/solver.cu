@@ -94,18 +94,20 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
     A((void **)&eta, sizeof(double) * L);
     A((void **)&scal, sizeof(double) * S_NSLOT * L);
     A((void **)&partial, sizeof(double) * (size_t)part_stride * L);
+    A((void **)&cgs, sizeof(double) * (size_t)part_stride * L);
+    A((void **)&cgp, sizeof(double) * (size_t)part_stride * L);
     A((void **)&counter, sizeof(unsigned) * L);
 }
 
 void Inner::release() {
     for (void *p : {(void *)rows, (void *)row0, (void *)nang, X, R, P, Q, BP, D, S_base, (void *)cnode,
-                    (void *)eta, (void *)scal, (void *)partial, (void *)counter, (void *)rowc, (void *)olist,
+                    (void *)eta, (void *)scal, (void *)partial, (void *)cgs, (void *)cgp, (void *)counter, (void *)rowc, (void *)olist,
                     (void *)oofs, fpart, (void *)fwin, (void *)frg, (void *)frec, (void *)futab})
         if (p) cudaFree(p);
     rows = nullptr; row0 = nang = olist = oofs = nullptr;
     fpart = nullptr; fwin = nullptr; frg = nullptr; frec = nullptr; futab = nullptr;
     X = R = P = Q = BP = D = S = S_base = nullptr;
-    cnode = eta = scal = partial = nullptr;
+    cnode = eta = scal = partial = cgs = cgp = nullptr;
     counter = nullptr;
     rowc = nullptr;
 }
@@ -119,7 +121,7 @@ int Inner::project(const DevGeom &g, const void *img, bool resid, cudaStream_t s
         launch_fp(0, &a, L, st);
         FpRedArgs<float> r{(const float *)fpart, rows, g.trig, g.xmaj, (const float *)D, (float *)out,
                            out_stride, out_off, g.N, g.n_det, nt_line, rowc, frg, nt_cross,
-                           cg ? 1 : 0, nang, cnode, scal, partial, counter, part_stride};
+                           cg ? 1 : 0, cgs, part_stride};
         launch_fp_reduce(0, resid, &r, n_rows, g.n_det, st);
     } else {
         FpArgs<double> a{(const double *)img, n, g.N, g.n_det, olist, oofs, fwin, frg, (double *)fpart,
@@ -127,7 +129,7 @@ int Inner::project(const DevGeom &g, const void *img, bool resid, cudaStream_t s
         launch_fp(1, &a, L, st);
         FpRedArgs<double> r{(const double *)fpart, rows, g.trig, g.xmaj, (const double *)D,
                             (double *)out, out_stride, out_off, g.N, g.n_det, nt_line, rowc, nullptr, nt_cross,
-                            cg ? 1 : 0, nang, cnode, scal, partial, counter, part_stride};
+                            cg ? 1 : 0, cgs, part_stride};
         launch_fp_reduce(1, resid, &r, n_rows, g.n_det, st);
     }
     return 3;
@@ -163,9 +165,14 @@ int Inner::cg(const DevGeom &g, int e1, cudaStream_t st) {
     k += project(g, X, true, st);
     k += backproject(g, EPI_RESID, R, P, X, st);
     for (int it = 0; it < e1; it++) {
+        // ||p||^2 of this step's direction: scal[S_PP] for p0 = r0, then the previous vector
+        // pass's per-CTA partials
+        const int npp = it == 0 ? 0 : vec_blocks(n);
         k += project(g, P, false, st, nullptr, 0, 0, true);
+        launch_cg_alpha(L, scal, cgs, fp_reduce_blocks(prec, g.n_det), nang, cgp, npp, cnode, part_stride, st);
+        k++;
         if (it + 1 < e1) k += backproject(g, EPI_CGR, R, nullptr, P, st, R);
-        launch_cg_update_px(prec, X, P, R, n, L, scal, partial, part_stride, counter, it + 1 < e1, st);
+        launch_cg_update_px(prec, X, P, R, n, L, scal, partial, part_stride, counter, it + 1 < e1, cgp, st);
         k++;
     }
     return k;

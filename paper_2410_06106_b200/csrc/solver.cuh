@@ -42,6 +42,7 @@ struct Inner {
     double *cnode = nullptr, *eta = nullptr;  // [L]
     double *scal = nullptr;    // [L][S_NSLOT]
     double *partial = nullptr; // [L][part_stride]
+    double *cgs = nullptr, *cgp = nullptr;  // [L][part_stride] CG step: ||A p||^2 / ||p||^2 partials (cg_alpha)
     unsigned *counter = nullptr;
     double4 *rowc = nullptr;     // [n_rows] backprojector per-row angle constants
     std::vector<RayRow> rows_h;

@@ -29,63 +29,21 @@ __device__ __forceinline__ void vec_loop(long long n, F4 &&body4, F1 &&body1) {
     }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(VT) cg_update_r(T *__restrict__ r, const T *__restrict__ q, long long n,
-                                                  double *scal, double *partial, int part_stride, unsigned *counter) {
+// x += alpha p (alpha from launch_cg_alpha).  WITH_P = true: the new direction p = r + beta p
+// and each CTA's ||p||^2 into pp_out for the next step's alpha (read after this kernel: no
+// last-block pass).  WITH_P = false (the last CG step of an inner solve): no new direction;
+// the final ||x||^2 per node goes to scal[S_NORM] (the divergence check of tq_run).
+template <typename T, bool WITH_P>
+__global__ void __launch_bounds__(VT) cg_update_px(T *__restrict__ x, T *__restrict__ p, const T *__restrict__ r,
+                                                   long long n, double *scal, double *partial, int part_stride,
+                                                   unsigned *counter, double *pp_out) {
     __shared__ double red[VT / 32 + 1];
     __shared__ bool last;
     const int node = blockIdx.y;
     const long long base = (long long)node * n;
     double *sc = scal + (long long)node * S_NSLOT;
     const double alpha = sc[S_ALPHA];
-    r += base; q += base;
-    double dot = 0.0;
-    vec_loop(n,
-        [&](long long i) {
-            Q4<T> rv = ld4(r + i);
-            const Q4<T> qv = ld4(q + i);
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                rv.v[u] = (T)((double)rv.v[u] - alpha * (double)qv.v[u]);
-                dot += (double)rv.v[u] * (double)rv.v[u];
-            }
-            st4(r + i, rv);
-        },
-        [&](long long i) {
-            const T rv = (T)((double)r[i] - alpha * (double)q[i]);
-            r[i] = rv;
-            dot += (double)rv * (double)rv;
-        });
-    const double bs = block_sum<VT>(dot, red);
-    double *part = partial + (long long)node * part_stride;
-    if (threadIdx.x == 0) part[blockIdx.x] = bs;
-    if (last_block_of_group(counter + node, gridDim.x, &last)) {
-        double s = 0.0;
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += VT) s += __ldcg(part + b);
-        s = block_sum<VT>(s, red);
-        if (threadIdx.x == 0) {
-            const double rr = sc[S_RR];
-            sc[S_RRNEW] = s;
-            sc[S_BETA] = rr > 0.0 ? s / rr : 0.0;
-            sc[S_RR] = s;
-        }
-    }
-}
-
-// WITH_P = true: also the new direction p = r + beta p and its ||p||^2 (scal[S_PP], for the
-// next step's p.q = ||A p||^2 + c ||p||^2).  WITH_P = false (the last CG step of an inner
-// solve): no new direction; the final ||x||^2 per node goes to scal[S_NORM] (the divergence
-// check of tq_run).
-template <typename T, bool WITH_P>
-__global__ void __launch_bounds__(VT) cg_update_px(T *__restrict__ x, T *__restrict__ p, const T *__restrict__ r,
-                                                   long long n, double *scal, double *partial, int part_stride,
-                                                   unsigned *counter) {
-    __shared__ double red[VT / 32 + 1];
-    __shared__ bool last;
-    const int node = blockIdx.y;
-    const long long base = (long long)node * n;
-    const double alpha = scal[(long long)node * S_NSLOT + S_ALPHA];
-    const double beta = scal[(long long)node * S_NSLOT + S_BETA];
+    const double beta = sc[S_BETA];
     x += base; p += base; r += base;
     double nrm = 0.0;
     vec_loop(n,
@@ -119,13 +77,17 @@ __global__ void __launch_bounds__(VT) cg_update_px(T *__restrict__ x, T *__restr
             }
         });
     const double bs = block_sum<VT>(nrm, red);
+    if (WITH_P) {  // read by the next step's cg_alpha (kernel order; no last-block pass)
+        if (threadIdx.x == 0) pp_out[(long long)node * part_stride + blockIdx.x] = bs;
+        return;
+    }
     double *part = partial + (long long)node * part_stride;
     if (threadIdx.x == 0) part[blockIdx.x] = bs;
     if (last_block_of_group(counter + node, gridDim.x, &last)) {
         double s = 0.0;
         for (int b = threadIdx.x; b < (int)gridDim.x; b += VT) s += __ldcg(part + b);
         s = block_sum<VT>(s, red);
-        if (threadIdx.x == 0) scal[(long long)node * S_NSLOT + (WITH_P ? S_PP : S_NORM)] = s;
+        if (threadIdx.x == 0) sc[S_NORM] = s;
     }
 }
 
@@ -204,25 +166,42 @@ __global__ void convert_kernel(const A *src, B *dst, long long n) {
         dst[i] = (B)src[i];
 }
 
-void launch_cg_update_r(int prec, void *r, const void *q, long long n, int L, double *scal, double *partial,
-                        int part_stride, unsigned *counter, cudaStream_t st) {
-    dim3 grid(vec_blocks(n), L);
-    if (prec == 0)
-        cg_update_r<float><<<grid, VT, 0, st>>>((float *)r, (const float *)q, n, scal, partial, part_stride, counter);
-    else
-        cg_update_r<double><<<grid, VT, 0, st>>>((double *)r, (const double *)q, n, scal, partial, part_stride, counter);
+__global__ void __launch_bounds__(VT) cg_alpha_kernel(double *scal, const double *cgs, int nfs_pa, const int *nang,
+                                                      const double *cgp, int npp, const double *cnode, int part_stride) {
+    __shared__ double red[VT / 32 + 1];
+    const int node = blockIdx.x;
+    const double *fs = cgs + (long long)node * part_stride, *ps = cgp + (long long)node * part_stride;
+    const int nfs = nfs_pa * nang[node];
+    double s1 = 0.0, s2 = 0.0;
+    for (int i = threadIdx.x; i < nfs; i += VT) s1 += fs[i];
+    for (int i = threadIdx.x; i < npp; i += VT) s2 += ps[i];
+    s1 = block_sum<VT>(s1, red);
+    s2 = block_sum<VT>(s2, red);
+    if (threadIdx.x == 0) {
+        double *sc = scal + (long long)node * S_NSLOT;
+        const double pq = s1 + cnode[node] * (npp > 0 ? s2 : sc[S_PP]);
+        sc[S_PQ] = pq;
+        sc[S_ALPHA] = pq > 0.0 ? sc[S_RR] / pq : 0.0;
+    }
+}
+
+void launch_cg_alpha(int L, double *scal, const double *cgs, int nfs_pa, const int *nang, const double *cgp,
+                     int npp, const double *cnode, int part_stride, cudaStream_t st) {
+    if (L == 0) return;
+    cg_alpha_kernel<<<L, VT, 0, st>>>(scal, cgs, nfs_pa, nang, cgp, npp, cnode, part_stride);
     TQ_CHECK_CUDA(cudaGetLastError());
 }
 
 void launch_cg_update_px(int prec, void *x, void *p, const void *r, long long n, int L, double *scal,
-                         double *partial, int part_stride, unsigned *counter, bool with_p, cudaStream_t st) {
+                         double *partial, int part_stride, unsigned *counter, bool with_p, double *pp_out,
+                         cudaStream_t st) {
     dim3 grid(vec_blocks(n), L);
     if (prec == 0) {
-        if (with_p) cg_update_px<float, true><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal, partial, part_stride, counter);
-        else cg_update_px<float, false><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal, partial, part_stride, counter);
+        if (with_p) cg_update_px<float, true><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal, partial, part_stride, counter, pp_out);
+        else cg_update_px<float, false><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal, partial, part_stride, counter, pp_out);
     } else {
-        if (with_p) cg_update_px<double, true><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal, partial, part_stride, counter);
-        else cg_update_px<double, false><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal, partial, part_stride, counter);
+        if (with_p) cg_update_px<double, true><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal, partial, part_stride, counter, pp_out);
+        else cg_update_px<double, false><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal, partial, part_stride, counter, pp_out);
     }
     TQ_CHECK_CUDA(cudaGetLastError());
 }

@@ -6,14 +6,17 @@
 
 namespace tq {
 
-// r -= alpha q; rr_new = r.r (per node, deterministic); last block: beta = rr_new / rr,
-// rr = rr_new.  (The matching x += alpha p is deferred to launch_cg_update_px, which reads
-// p anyway: one pass over x, p fewer per CG step, identical arithmetic.)
-void launch_cg_update_r(int prec, void *r, const void *q, long long n, int L, double *scal, double *partial,
-                        int part_stride, unsigned *counter, cudaStream_t st);
-// x += alpha p, then (with_p) p = r + beta p, else scal[node][S_NORM] = ||x||^2 (last CG step)
+// alpha = rr / p.q of a CG step with p.q = ||A p||^2 + c ||p||^2 (R-8), one CTA per
+// node: the forward reduction's per-CTA partials of ||A p||^2 (nfs_pa per angle of the node,
+// cgs) and the previous vector pass's per-CTA partials of ||p||^2 (npp of them in cgp; npp = 0:
+// scal[S_PP], p0 = r0), each summed in a fixed order -> scal[S_PQ], scal[S_ALPHA]
+void launch_cg_alpha(int L, double *scal, const double *cgs, int nfs_pa, const int *nang, const double *cgp,
+                     int npp, const double *cnode, int part_stride, cudaStream_t st);
+// x += alpha p, then (with_p) p = r + beta p and each CTA's ||p||^2 into pp_out[node][block],
+// else scal[node][S_NORM] = ||x||^2 (last CG step)
 void launch_cg_update_px(int prec, void *x, void *p, const void *r, long long n, int L, double *scal,
-                         double *partial, int part_stride, unsigned *counter, bool with_p, cudaStream_t st);
+                         double *partial, int part_stride, unsigned *counter, bool with_p, double *pp_out,
+                         cudaStream_t st);
 // scal[node][S_NORM] = ||x_node||^2
 void launch_norm2(int prec, const void *x, long long n, int L, double *scal, double *partial,
                   int part_stride, unsigned *counter, cudaStream_t st);
