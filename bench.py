@@ -98,10 +98,15 @@ def vu_per_iter(cfg):
     return 2 * apps * cfg.N * cfg.N * cfg.n_angles * cfg.slices
 
 
+AX_MAXAGE = 16  # the engine's refresh period of the kept A x (TQ_AX_MAXAGE)
+
+
 def projector_applications(cfg):
-    """(algorithmic, executed) projector applications (A or A^T) per ADMM iteration."""
+    """(algorithmic, executed) projector applications (A or A^T) per ADMM iteration.  CG on the
+    graph rule executes E1 forward projections (the residual's A x is kept, one refresh per
+    AX_MAXAGE iterations) and E1 backprojections (residual + E1 - 1 steps)."""
     if cfg.inner == 1:
-        return 2 * (cfg.e1 + 1), 2 * cfg.e1 + 1
+        return 2 * (cfg.e1 + 1), 2 * cfg.e1 + 1.0 / AX_MAXAGE
     return 2 * cfg.e1, 2 * cfg.e1
 
 
@@ -434,7 +439,7 @@ def main():
         b.record(stream)
         torch.cuda.synchronize()
         comp_ms[comp] = a.elapsed_time(b) / reps
-    apps = {0: cfg.e1 + 1, 1: cfg.e1}  # forward launches / backprojections (E1 - 1 CG + 1 residual) per iteration
+    apps = {0: cfg.e1, 1: cfg.e1}  # forward projections (A x kept) / backprojections (E1 - 1 CG + 1 residual) per iteration
     share = {c: comp_ms[c] * apps[c] / (ms / args.steps) for c in comp_ms}
     dom = max(comp_ms, key=lambda c: comp_ms[c])
     names = {0: "forward projector A p (fp_persist_f32 tile pass + fp_reduce)",

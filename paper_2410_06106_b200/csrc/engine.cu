@@ -2,6 +2,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 
@@ -107,6 +108,7 @@ void *Ctx::dev_alloc(size_t bytes) {
 void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int rank_, int world_,
                  const uint8_t *nccl_id, int precision, int device_) {
     N = g.image_side; n_ang = g.n_angles; n_det = g.n_det;
+    if (const char *e = getenv("TQ_AX_MAXAGE")) ax_maxage = std::max(0, atoi(e));
     TQ_REQUIRE(N >= 8 && N % 8 == 0, "image_side must be a positive multiple of 8");
     TQ_REQUIRE(N <= 16384, "image_side too large");
     TQ_REQUIRE(n_ang >= 1, "n_angles must be >= 1");
@@ -284,6 +286,7 @@ void Ctx::destroy() {
 
 void Ctx::set_params(const tq_params &p) {
     finish();
+    ax_valid = false;  // e.g. GD steps may have moved x without the kept A x
     TQ_REQUIRE(p.rho > 0.0 && std::isfinite(p.rho), "rho must be > 0");
     TQ_REQUIRE(p.inner == TQ_INNER_GD || p.inner == TQ_INNER_CG, "inner must be GD or CG");
     TQ_REQUIRE(p.e1 >= 0 && p.e1 <= 100000, "e1 out of range");
@@ -726,11 +729,26 @@ void Ctx::node_bytes(int slice, int node, long long &sent, long long &recv) {
     }
 }
 
+bool Ctx::use_ax() const { return ax_maxage > 0 && prm.inner == TQ_INNER_CG && rule == TQ_RULE_GRAPH; }
+
+// before graph launches covering `iters` iterations: refresh the kept A x (outside the graphs)
+// when it is stale or would age past ax_maxage iterations (its fp rounding then stays at the
+// level of a few direct projections)
+void Ctx::ax_before(int iters, cudaStream_t s) {
+    if (!use_ax() || iters <= 0) return;
+    if (!ax_valid || ax_age + iters > std::max(ax_maxage, MULTI)) {
+        in.project(geo, in.X, false, s, in.AX, n_det, 0);
+        ax_valid = true;
+        ax_age = 0;
+    }
+    ax_age += iters;
+}
+
 int Ctx::stage(int id, cudaStream_t s) {
     if (id == 2) return phase_b(s);
     int k = 0;
     if (id == 0) {
-        k += prm.inner == TQ_INNER_CG ? in.cg(geo, prm.e1, s) : in.gd(geo, prm.e1, s);
+        k += prm.inner == TQ_INNER_CG ? in.cg(geo, prm.e1, s, use_ax() ? AX_CACHED : AX_OFF) : in.gd(geo, prm.e1, s);
         if (rule == TQ_RULE_PAPER)
             k += launch_paper_alg3(prec, in.X, ALPHA, xg_tab, seg_lo, seg_len, seg_max, seg_tab, n, L,
                                    prm.rho, prm.eta2, prm.e2, s);
@@ -900,11 +918,13 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
     if (seg2.exec && !stop && !profiling)
         for (; it0 + MULTI <= iters; it0 += MULTI) {
             Nvtx ni("tq:iterations");
+            ax_before(MULTI, s);
             TQ_CHECK_CUDA(cudaGraphLaunch(seg2.exec, s));
         }
     done = it0;
     for (int it = it0; it < iters; it++) {
         Nvtx ni("tq:iteration");
+        ax_before(1, s);
         if (profiling) {
             cudaEvent_t *e = &pev[5 * (size_t)it];
             TQ_CHECK_CUDA(cudaEventRecord(e[0], s));
@@ -1167,6 +1187,7 @@ void Ctx::import_state(int slice, int node, const double *buf, long long len) {
     if (!xready) setup_exchange();
     const size_t es = prec ? 8 : 4;
     from_host_double(prec, buf, in.xrow(in.X, i), n, stream);
+    ax_valid = false;  // x changed outside a solve
     from_host_double(prec, buf + n, (uint8_t *)ALPHA + es * n * i, n, stream);
     if (segmented()) {
         from_host_double(prec, buf + 2 * n, (uint8_t *)XG + es * n * slice, n, stream);

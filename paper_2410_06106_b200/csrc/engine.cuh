@@ -42,6 +42,13 @@ struct Ctx {
     tq_quant q{TQ_Q_NONE, 16, 10, 50, 0, 0};
     std::vector<char> sino_set;
     bool need_rhs = false;      // recompute b' from the state before the next iteration
+    // sinogram-space A x kept across CG solves (graph rule: x changes only in the solve, by
+    // x += alpha p, so A x += alpha A p); recomputed when stale or every AX_MAXAGE iterations
+    bool ax_valid = false;
+    int ax_age = 0;
+    int ax_maxage = 16;         // TQ_AX_MAXAGE (0: no kept A x, the residual projection every solve)
+    bool use_ax() const;
+    void ax_before(int iters, cudaStream_t s);
     // ---- quantizer / exchange state (rebuilt by setup_exchange)
     bool xready = false;
     int kind_of_slice(int s) const;

@@ -86,6 +86,7 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
     TQ_CHECK_CUDA(cudaDeviceSynchronize());
     for (void **v : {&X, &R, &P, &Q, &BP}) A(v, es * n * L);
     A(&D, es * (size_t)n_rows * g.n_det);
+    A(&AX, es * (size_t)n_rows * g.n_det);
     // S rows carry a zero guard bin at 0 and n_det + 1; SPAD zero elements before and after the
     // whole array let the backprojector stage its fixed 96-bin windows without bounds checks
     A(&S_base, es * ((size_t)n_rows * sp + 2 * SPAD));
@@ -100,13 +101,13 @@ void Inner::init(int prec_, const DevGeom &g, const std::vector<std::vector<int>
 }
 
 void Inner::release() {
-    for (void *p : {(void *)rows, (void *)row0, (void *)nang, X, R, P, Q, BP, D, S_base, (void *)cnode,
+    for (void *p : {(void *)rows, (void *)row0, (void *)nang, X, R, P, Q, BP, D, AX, S_base, (void *)cnode,
                     (void *)eta, (void *)scal, (void *)partial, (void *)cgs, (void *)cgp, (void *)counter, (void *)rowc, (void *)olist,
                     (void *)oofs, fpart, (void *)fwin, (void *)frg, (void *)frec, (void *)futab})
         if (p) cudaFree(p);
     rows = nullptr; row0 = nang = olist = oofs = nullptr;
     fpart = nullptr; fwin = nullptr; frg = nullptr; frec = nullptr; futab = nullptr;
-    X = R = P = Q = BP = D = S = S_base = nullptr;
+    X = R = P = Q = BP = D = AX = S = S_base = nullptr;
     cnode = eta = scal = partial = cgs = cgp = nullptr;
     counter = nullptr;
     rowc = nullptr;
@@ -160,9 +161,15 @@ int Inner::backproject(const DevGeom &g, int epi, void *out, void *out2, const v
 // -- p.q = p.(A^T A p + c p) written through A p, so q is never stored and the residual
 // update rides on the backprojection; the last step needs neither r nor beta (the next
 // solve restarts from the residual backprojection), so it has no backprojection at all.
-int Inner::cg(const DevGeom &g, int e1, cudaStream_t st) {
+int Inner::cg(const DevGeom &g, int e1, cudaStream_t st, int ax) {
     int k = 0;
-    k += project(g, X, true, st);
+    if (ax == AX_OFF) {
+        k += project(g, X, true, st);
+    } else {
+        if (ax == AX_REFRESH) k += project(g, X, false, st, AX, g.n_det, 0);
+        launch_resid_from_ax(prec, D, AX, S, n_rows, g.n_det, sp, st);
+        k++;
+    }
     k += backproject(g, EPI_RESID, R, P, X, st);
     for (int it = 0; it < e1; it++) {
         // ||p||^2 of this step's direction: scal[S_PP] for p0 = r0, then the previous vector
@@ -172,7 +179,8 @@ int Inner::cg(const DevGeom &g, int e1, cudaStream_t st) {
         launch_cg_alpha(L, scal, cgs, fp_reduce_blocks(prec, g.n_det), nang, cgp, npp, cnode, part_stride, st);
         k++;
         if (it + 1 < e1) k += backproject(g, EPI_CGR, R, nullptr, P, st, R);
-        launch_cg_update_px(prec, X, P, R, n, L, scal, partial, part_stride, counter, it + 1 < e1, cgp, st);
+        const AxUpdate au{ax == AX_OFF ? nullptr : AX, S, row0, nang, g.n_det, sp};
+        launch_cg_update_px(prec, X, P, R, n, L, scal, partial, part_stride, counter, it + 1 < e1, cgp, au, st);
         k++;
     }
     return k;

@@ -20,6 +20,8 @@ struct DevGeom {
     void release();
 };
 
+enum AxMode { AX_OFF = 0, AX_REFRESH = 1, AX_CACHED = 2 };
+
 struct Inner {
     int prec = 0, L = 0, n_rows = 0, sp = 0, part_stride = 0;
     long long n = 0;
@@ -37,6 +39,7 @@ struct Inner {
     int nt_line = 0, nt_cross = 0;
     void *X = nullptr, *R = nullptr, *P = nullptr, *Q = nullptr, *BP = nullptr;  // [L][n]
     void *D = nullptr;         // [n_rows][n_det]
+    void *AX = nullptr;        // [n_rows][n_det] A x of the current X (CG, ax mode != AX_OFF)
     void *S = nullptr;         // [n_rows][sp], guard column at 0 and n_det+1 (inside S_base)
     void *S_base = nullptr;    // S with SPAD zero elements before and after
     double *cnode = nullptr, *eta = nullptr;  // [L]
@@ -53,7 +56,9 @@ struct Inner {
     size_t esize() const { return prec ? 8 : 4; }
     void *xrow(void *base, int i) const { return (char *)base + esize() * n * i; }
     // launches; return the number of kernels launched
-    int cg(const DevGeom &g, int e1, cudaStream_t st);
+    // ax: AX_OFF = residual projection of X every solve; AX_REFRESH = project X into AX first;
+    // AX_CACHED = residual d - AX (AX = A x maintained by the CG steps: A x += alpha A p)
+    int cg(const DevGeom &g, int e1, cudaStream_t st, int ax = 0);
     int gd(const DevGeom &g, int e1, cudaStream_t st);
     int norm2(cudaStream_t st);
     // S = (D -) A img (2 tile launches + 1 reduction); out/out_stride/out_off override S;

@@ -36,7 +36,7 @@ __device__ __forceinline__ void vec_loop(long long n, F4 &&body4, F1 &&body1) {
 template <typename T, bool WITH_P>
 __global__ void __launch_bounds__(VT) cg_update_px(T *__restrict__ x, T *__restrict__ p, const T *__restrict__ r,
                                                    long long n, double *scal, double *partial, int part_stride,
-                                                   unsigned *counter, double *pp_out) {
+                                                   unsigned *counter, double *pp_out, const AxUpdate au) {
     __shared__ double red[VT / 32 + 1];
     __shared__ bool last;
     const int node = blockIdx.y;
@@ -44,6 +44,16 @@ __global__ void __launch_bounds__(VT) cg_update_px(T *__restrict__ x, T *__restr
     double *sc = scal + (long long)node * S_NSLOT;
     const double alpha = sc[S_ALPHA];
     const double beta = sc[S_BETA];
+    if (au.ax) {  // A x += alpha A p over the node's sinogram rows (x += alpha p below)
+        const long long ne = (long long)au.nang[node] * au.n_det, r0 = au.row0[node];
+        T *axp = reinterpret_cast<T *>(au.ax);
+        const T *sp_ = reinterpret_cast<const T *>(au.s);
+        for (long long e = (long long)blockIdx.x * VT + threadIdx.x; e < ne; e += (long long)gridDim.x * VT) {
+            const long long row = r0 + e / au.n_det, j = e % au.n_det;
+            const long long ia = row * au.n_det + j;
+            axp[ia] = (T)((double)axp[ia] + alpha * (double)sp_[row * au.sp + 1 + j]);
+        }
+    }
     x += base; p += base; r += base;
     double nrm = 0.0;
     vec_loop(n,
@@ -185,6 +195,26 @@ __global__ void __launch_bounds__(VT) cg_alpha_kernel(double *scal, const double
     }
 }
 
+template <typename T>
+__global__ void resid_from_ax_kernel(const T *__restrict__ d, const T *__restrict__ ax, T *__restrict__ s, int n_rows,
+                                     int n_det, int sp) {
+    const long long ne = (long long)n_rows * n_det;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (long long)gridDim.x * blockDim.x) {
+        const long long row = e / n_det, j = e % n_det;
+        s[row * sp + 1 + j] = d[e] - ax[e];
+    }
+}
+
+void launch_resid_from_ax(int prec, const void *d, const void *ax, void *s, int n_rows, int n_det, int sp,
+                          cudaStream_t st) {
+    const long long ne = (long long)n_rows * n_det;
+    if (ne == 0) return;
+    const int blocks = (int)std::min<long long>(1184, (ne + 255) / 256);
+    if (prec == 0) resid_from_ax_kernel<float><<<blocks, 256, 0, st>>>((const float *)d, (const float *)ax, (float *)s, n_rows, n_det, sp);
+    else resid_from_ax_kernel<double><<<blocks, 256, 0, st>>>((const double *)d, (const double *)ax, (double *)s, n_rows, n_det, sp);
+    TQ_CHECK_CUDA(cudaGetLastError());
+}
+
 void launch_cg_alpha(int L, double *scal, const double *cgs, int nfs_pa, const int *nang, const double *cgp,
                      int npp, const double *cnode, int part_stride, cudaStream_t st) {
     if (L == 0) return;
@@ -194,14 +224,14 @@ void launch_cg_alpha(int L, double *scal, const double *cgs, int nfs_pa, const i
 
 void launch_cg_update_px(int prec, void *x, void *p, const void *r, long long n, int L, double *scal,
                          double *partial, int part_stride, unsigned *counter, bool with_p, double *pp_out,
-                         cudaStream_t st) {
+                         const AxUpdate &au, cudaStream_t st) {
     dim3 grid(vec_blocks(n), L);
     if (prec == 0) {
-        if (with_p) cg_update_px<float, true><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal, partial, part_stride, counter, pp_out);
-        else cg_update_px<float, false><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal, partial, part_stride, counter, pp_out);
+        if (with_p) cg_update_px<float, true><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal, partial, part_stride, counter, pp_out, au);
+        else cg_update_px<float, false><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal, partial, part_stride, counter, pp_out, au);
     } else {
-        if (with_p) cg_update_px<double, true><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal, partial, part_stride, counter, pp_out);
-        else cg_update_px<double, false><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal, partial, part_stride, counter, pp_out);
+        if (with_p) cg_update_px<double, true><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal, partial, part_stride, counter, pp_out, au);
+        else cg_update_px<double, false><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal, partial, part_stride, counter, pp_out, au);
     }
     TQ_CHECK_CUDA(cudaGetLastError());
 }

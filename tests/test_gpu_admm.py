@@ -294,6 +294,33 @@ def test_deterministic_bitwise():
     assert np.array_equal(a.image(), b.image())
 
 
+def _x_after(cfg, inp, prec, iters):
+    ctx = gpu_context(cfg, inp, precision=prec)
+    ctx.run(iters)
+    x = np.stack([ctx.export_state(0, m)[0] for m in range(cfg.nodes)])
+    ctx.close()
+    return x
+
+
+@pytest.mark.parametrize("make,iters,prec,tol", [(C.C1, 40, 0, 1e-4), (C.C1, 40, 1, 1e-12),
+                                                 (lambda: C.C4(1), 3, 1, 1e-10)])
+def test_kept_ax_matches_residual_projection(monkeypatch, make, iters, prec, tol):
+    """The CG residual's A x kept across solves (A x += alpha A p, refreshed every 16
+    iterations; R-8) against the residual projection of x every solve
+    (TQ_AX_MAXAGE=0): config 1 for 40 iterations (two refresh cycles and a partial one) in
+    fp32 and fp64, and the bench config C4_G1 (unquantized) for 3 fp64 iterations.  (Configs
+    2-5 amplify any rounding difference along their trajectories -- fp64 C2 unquantized:
+    2e-15 after 3 iterations, 2e-11 after 17, 2e-6 after 40, the same for any change of
+    summation order -- so they are compared early.)"""
+    cfg = make()
+    cfg.quant = C.Q_NONE if cfg.cid == 4 else cfg.quant
+    inp = C.make_inputs(cfg, with_truth=False)
+    xa = _x_after(cfg, inp, prec, iters)
+    monkeypatch.setenv("TQ_AX_MAXAGE", "0")
+    xb = _x_after(cfg, inp, prec, iters)
+    assert rel(xa, xb) <= tol
+
+
 def test_state_roundtrip_and_resume():
     cfg = c2s()
     inp = C.make_inputs(cfg)
