@@ -170,7 +170,7 @@ def projector_c5_geometry(tomoq, torch, stream, reps=5):
     ctx.set_sinogram(0, sino)
     out = {"workload": "C5 slice geometry: N=2048, 1500 angles, 2897 bins, 8 nodes x 187-188 angles"}
     peak = LSU_VU_PER_CLK_SM * sm_count() * peaks()["sm_max_mhz"] * 1e6 / 1e9
-    for comp, name in ((0, "fp"), (1, "bp_cgq")):
+    for comp, name in ((0, "fp"), (1, "bp_cgr")):
         ctx.launch_component(comp, 2, stream)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -201,7 +201,7 @@ def projector_siddon_c4(tomoq, torch, stream, reps=10):
         ctx.set_sinogram(0, torch.tensor(inp.sino[0], device="cuda"))
         ctx.run(1)
         res = {}
-        for comp, cname in ((0, "fp"), (1, "bp_cgq")):
+        for comp, cname in ((0, "fp"), (1, "bp_cgr")):
             ctx.launch_component(comp, 2, stream)
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -463,7 +463,7 @@ def main():
                       f"VU/clk/SM x {n_sm} SMs x {pk['sm_max_mhz']} MHz (sm_max_mhz {pk['src']}); DESIGN.md section 6",
         "hbm_compulsory_gbs": compulsory / (comp_ms[dom] / 1e3) / 1e9, "hbm_peak_gbs": pk["hbm_gbs"],
         "share_of_step": share[dom],
-        "components_ms": {"fp": comp_ms[0], "bp_cgq": comp_ms[1]},
+        "components_ms": {"fp": comp_ms[0], "bp_cgr": comp_ms[1]},
     }
 
     # ---- the same projector kernels on config 5's node geometry (2048^2, 188 angles per node):

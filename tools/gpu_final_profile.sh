@@ -12,7 +12,7 @@ timeout 900 ncu --set full --clock-control none --import-source on --kernel-name
   -k regex:"fp_persist_f32" -s 20 -c 1 -f -o gpurun_out/${TAG}_fp_full $CMD > gpurun_out/${TAG}_ncu_fp.log 2>&1
 echo "ncu fp exit $?"
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k regex:"bp_tile_kernel<float, \\(int\\)1>" -s 20 -c 1 -f -o gpurun_out/${TAG}_bp_full $CMD > gpurun_out/${TAG}_ncu_bp.log 2>&1
+  -k regex:"bp_tile_kernel<float, \\(int\\)4>" -s 20 -c 1 -f -o gpurun_out/${TAG}_bp_full $CMD > gpurun_out/${TAG}_ncu_bp.log 2>&1
 echo "ncu bp exit $?"
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k regex:"fp_reduce_f32" -s 20 -c 1 -f -o gpurun_out/${TAG}_fpred_full $CMD > gpurun_out/${TAG}_ncu_fpred.log 2>&1
