@@ -59,6 +59,24 @@ def test_fp64_free_running_every_config(make):
         assert rel(ctx.image(s), o.image()) <= 1e-6  # observed ~1e-9: fp64 vs fp64
 
 
+@pytest.mark.parametrize("e1", [1, 2, 3])
+def test_fp64_free_running_cg_step_counts(e1):
+    """The CG path's step bookkeeping (no backprojection in the last step, alpha from the
+    forward projection, the kept A x across solves, R-8) at other E1: config 1, fp64, 40
+    iterations (two A x refresh cycles and a partial one) against the oracle.  (Single
+    solves of many CG steps are themselves sensitive to rounding order: 12 steps on the
+    local-solve test problem differ by 6e-9 in fp64 between any two summation orders.)"""
+    cfg = C.C1()
+    cfg.e1, cfg.iters = e1, 40
+    inp = C.make_inputs(cfg)
+    ctx = gpu_context(cfg, inp, precision=1)
+    ctx.run(cfg.iters)
+    o = oracle_case(cfg, inp).run(cfg.iters)
+    X = np.stack([ctx.export_state(0, m)[0] for m in range(cfg.nodes)])  # fp64 (image() is fp32)
+    ctx.close()
+    assert rel(X, np.stack(o.X)) <= 1e-10  # observed 4e-15 ... 2e-12
+
+
 @pytest.mark.parametrize("prec,tol", [(0, 1e-3), (1, 1e-6)])
 def test_paper_rule_c1(prec, tol):
     cfg = C.C1()

@@ -96,7 +96,8 @@ def test_projector_full_size_sampled(N, n_ang, n_det, sel):
 
 
 @pytest.mark.parametrize("prec", [0, 1])
-@pytest.mark.parametrize("inner,e1", [(tomoq.INNER_CG, 5), (tomoq.INNER_GD, 10), (tomoq.INNER_CG, 0)])
+@pytest.mark.parametrize("inner,e1", [(tomoq.INNER_CG, 5), (tomoq.INNER_GD, 10), (tomoq.INNER_CG, 0),
+                                     (tomoq.INNER_CG, 1), (tomoq.INNER_CG, 2)])
 def test_local_solve_parity(prec, inner, e1):
     N, n_ang, n_det = 128, 90, 183
     sel = list(range(2, 90, 8))
