@@ -221,6 +221,11 @@ tq_status tq_launch_component(tq_ctx *ctx, int32_t component, int32_t reps, void
                               int64_t *units);
 
 tq_status tq_get_stats(const tq_ctx *ctx, tq_stats *out);
+/* Environment knob read by tq_create: TQ_AX_MAXAGE (default 16) -- the graph-rule CG keeps the
+ * residual's A x in sinogram space across inner solves (A x += alpha A p; R-8) and
+ * recomputes it by a forward projection when stale and at least every TQ_AX_MAXAGE iterations;
+ * 0 projects x in every solve (the oracle's order of operations). */
+
 /* Debug aid (no compute-sanitizer on the GPU pool): with TQ_GUARD=1 in the environment of the
  * process, every device allocation of the library carries 256-byte guard bands (checked after
  * every run: TQ_ECUDA on an out-of-bounds write) and starts poisoned with 0xff bytes, so reads
