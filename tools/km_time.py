@@ -1,6 +1,6 @@
 """Time the K-means encode component (tq_launch_component 3) of the C4_G1 context alone."""
 import sys
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 import torch
 from paper_2410_06106_b200 import configs as C, tomoq
 cfg = C.C4(1)
