@@ -158,4 +158,26 @@ constexpr int TQ_MAX_DEGREE = 64;  // graph rule: neighbours per node (tq_create
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// Programmatic dependent launch (sm_90+): the hot-loop kernels are launched with the
+// programmatic-serialization attribute so a kernel's launch overlaps the end of the one
+// before it on the stream; each such kernel calls pdl_wait() before it touches memory the
+// previous kernel wrote (griddepcontrol.wait returns once that grid has completed and its
+// writes are visible; a no-op for a normal launch).  TQ_PDL=0 launches them normally.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KP, typename... A>
+inline void launch_pdl(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    TQ_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k, static_cast<KP>(args)...));
+}
+
 }  // namespace tq

@@ -35,6 +35,7 @@ template <typename T>
 __global__ void __launch_bounds__(CT) graph_dual(const T *const *own_ptr, const T *const *nbr_ptr,
                                                  const int *nbr_off, T *alpha,
                                                  T *bprime, long long n, double rho, int update) {
+    pdl_wait();
     __shared__ const T *nb[MAXNB];
     const int i = blockIdx.y;
     const T *own = own_ptr[i];
@@ -165,9 +166,8 @@ int launch_graph_dual(int prec, const void *const *own_ptr, const void *const *n
                       int update_alpha, cudaStream_t st) {
     if (L == 0) return 0;
     if (prec == 0)
-        graph_dual<float><<<grid_dual(n, L), CT, 0, st>>>((const float *const *)own_ptr, (const float *const *)nbr_ptr,
-                                                        nbr_off, (float *)alpha, (float *)bprime, n, rho,
-                                                        update_alpha);
+        launch_pdl(graph_dual<float>, grid_dual(n, L), CT, 0, st, (const float *const *)own_ptr,
+                   (const float *const *)nbr_ptr, nbr_off, (float *)alpha, (float *)bprime, n, rho, update_alpha);
     else
         graph_dual<double><<<grid_dual(n, L), CT, 0, st>>>((const double *const *)own_ptr, (const double *const *)nbr_ptr,
                                                          nbr_off, (double *)alpha, (double *)bprime, n,

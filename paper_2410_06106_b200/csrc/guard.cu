@@ -74,4 +74,13 @@ bool guards_intact(std::string &where) {
     return true;
 }
 
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("TQ_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 }  // namespace tq

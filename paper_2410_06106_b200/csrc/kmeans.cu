@@ -146,6 +146,7 @@ __device__ __forceinline__ void flush_hist(const uint32_t *sh, uint32_t *hp, int
 // keys of the raw payload (padding keys sort last) + the histogram of the first sorted digit
 // (bits 8..15: the low byte is never sorted, see kmeans_encode)
 __global__ void __launch_bounds__(KT) km_keys(const float *const *vin, KmPtr w) {
+    pdl_wait();
     __shared__ uint32_t sh[256], wc[KT / 32 * 256];
     const int b = blockIdx.y, t = blockIdx.x;
     const float *v = vin[b];
@@ -161,6 +162,7 @@ __global__ void __launch_bounds__(KT) km_keys(const float *const *vin, KmPtr w) 
 }
 
 __global__ void __launch_bounds__(KT) km_hist(const uint32_t *keys, KmPtr w, int shift) {
+    pdl_wait();
     __shared__ uint32_t sh[256], wc[KT / 32 * 256];
     const int b = blockIdx.y, t = blockIdx.x;
     uint32_t k[KI];
@@ -175,6 +177,7 @@ __global__ void __launch_bounds__(KT) km_hist(const uint32_t *keys, KmPtr w, int
 // tiles; warp totals are combined in a fixed order.
 constexpr int SCW = 8;  // warps per CTA
 __global__ void __launch_bounds__(SCW * 32) km_scan(KmPtr w) {
+    pdl_wait();
     __shared__ uint32_t tot[SCW][32];
     const int b = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int d = blockIdx.x * 32 + lane;
@@ -203,6 +206,7 @@ __global__ void __launch_bounds__(SCW * 32) km_scan(KmPtr w) {
 // + (in earlier rounds of my warp) + (in lower lanes of my round); destination =
 // offset(digit, tile) + rank.
 __global__ void __launch_bounds__(KT, 3) km_scatter(const uint32_t *kin, uint32_t *kout, KmPtr w, int shift) {
+    pdl_wait();
     using Scan = cub::BlockScan<uint32_t, KT>;
     __shared__ typename Scan::TempStorage stmp;
     __shared__ uint32_t wc[KT / 32 * 256], goff[256], sk[KTILE];
@@ -274,6 +278,7 @@ __device__ __forceinline__ int fixed_exp(const uint32_t *sorted, long long nv) {
 // chunk (128 keys) sums of fix(v) over the sorted keys: csum[chunk] = exclusive prefix of
 // the chunk sums within its tile, cpre[tile] = the tile's total
 __global__ void __launch_bounds__(KT) km_csum(KmPtr w, int sh) {
+    pdl_wait();
     __shared__ long long ch[CPT];
     const int b = blockIdx.y, t = blockIdx.x;
     const uint32_t *sorted = w.keysA + (long long)b * w.T * KTILE;
@@ -549,6 +554,7 @@ __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPt
 template <int B, typename TO>
 __global__ void __launch_bounds__(KT) km_final(const float *const *vin, KmPtr w, uint8_t *const *pay,
                                                int32_t *const *labels_tab, TO *const *dec_out) {
+    pdl_wait();
     __shared__ float thr_s[256], cen_s[256];
     __shared__ int cnt_s[LUT_NB + 1];
     const int b = blockIdx.y;
@@ -707,26 +713,26 @@ int kmeans_encode(const float *const *v, KmeansWork &ws, int lloyd, uint8_t *con
     // LSD passes on the key bytes 1, 2, 3 only: the keys end up ordered by their top 24 bits
     // ("groups": same sign, exponent and top 15 mantissa bits), the low byte unordered inside a
     // group -- km_lloyd resolves the groups it needs (one pass of 4 saved)
-    km_keys<<<tiles, KT, 0, st>>>(v, w);
+    launch_pdl(km_keys, tiles, KT, 0, st, v, w);
     int k = 1;
     uint32_t *src = ws.keysB, *dst = ws.keysA;
     for (int pass = 1; pass < 4; pass++) {
-        if (pass > 1) { km_hist<<<tiles, KT, 0, st>>>(src, w, 8 * pass); k++; }
-        km_scan<<<dim3(256 / 32, P), SCW * 32, 0, st>>>(w);
-        km_scatter<<<tiles, KT, 0, st>>>(src, dst, w, 8 * pass);
+        if (pass > 1) { launch_pdl(km_hist, tiles, KT, 0, st, (const uint32_t *)src, w, 8 * pass); k++; }
+        launch_pdl(km_scan, dim3(256 / 32, P), SCW * 32, 0, st, w);
+        launch_pdl(km_scatter, tiles, KT, 0, st, (const uint32_t *)src, dst, w, 8 * pass);
         k += 2;
         std::swap(src, dst);
     }
     // three passes: B -> A -> B -> A, group-sorted keys in keysA
-    km_csum<<<tiles, KT, 0, st>>>(w, lloyd_shift(ws.T));
+    launch_pdl(km_csum, tiles, KT, 0, st, w, lloyd_shift(ws.T));
     km_lloyd<<<LCL * P, LCT, lloyd_smem(ws.T), st>>>(w, lloyd, lloyd_shift(ws.T));
     long long want = std::max(1LL, (148LL * 8 + P - 1) / P);
     long long need = (ws.nv + KT * 16 - 1) / (KT * 16);
     const dim3 grid((unsigned)std::max(1LL, std::min(want, need)), P);
     with_bits(ws.B, [&](auto Bc) {
         constexpr int BB = decltype(Bc)::value;
-        if (prec == 1) km_final<BB, double><<<grid, KT, 0, st>>>(v, w, pay, labels, (double *const *)dec_out);
-        else km_final<BB, float><<<grid, KT, 0, st>>>(v, w, pay, labels, (float *const *)dec_out);
+        if (prec == 1) launch_pdl(km_final<BB, double>, grid, KT, 0, st, v, w, pay, labels, (double *const *)dec_out);
+        else launch_pdl(km_final<BB, float>, grid, KT, 0, st, v, w, pay, labels, (float *const *)dec_out);
     });
     TQ_CHECK_CUDA(cudaGetLastError());
     return k + 3;

@@ -486,6 +486,7 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    pdl_wait();  // the images come from the previous kernel
     // thread 0: decodes unit u into s_hdr[rb] and issues the TMA of its raw tile + bulk
     // copies of its first window records and item plan (units without angles of their
     // orientation load only the tile and are skipped); every thread learns whether a load
@@ -861,6 +862,7 @@ __device__ __forceinline__ float4 ldcg_if(const float4 *p, unsigned c) {
 constexpr int RQ = 32;
 template <bool RESID>
 __global__ void __launch_bounds__(RQ * RG) fp_reduce_f32(const FpRedArgs<float> a) {
+    pdl_wait();
     __shared__ float4 part[RG][RQ];
     const int row = blockIdx.y;
     const double m_row = fp_row_m(a, row);  // issued first: its latency overlaps the slot loads
@@ -947,6 +949,7 @@ __global__ void __launch_bounds__(RQ * RG) fp_reduce_f32(const FpRedArgs<float> 
 template <typename T, int EPI>
 __global__ void __launch_bounds__(BP_THREADS, sizeof(T) == 4 ? 4 : 1)
 bp_tile_kernel(const BpArgs<T> a) {
+    pdl_wait();
     constexpr int BP_MAXA = bp_maxa<T, EPI>();  // angles per staged batch of this variant
     extern __shared__ __align__(16) unsigned char bp_smem[];
     T *win = reinterpret_cast<T *>(bp_smem);  // [BP_MAXA][BP_WB], bins pre-scaled by 1/m (fp64)
@@ -1300,8 +1303,8 @@ void fp_dispatch(const FpArgs<T> &A, int L, cudaStream_t st) {
             const int nunits = 2 * L * A.nt_line * A.nt_cross;
             CUtensorMap tr, tc;
             make_image_maps(A.img, A.N, L, &tr, &tc);
-            if (A.siddon) fp_persist_f32<true><<<std::min(nunits, g_fpp_grid), FP_THREADS, fpp_smem(), st>>>(B, nunits, tr, tc);
-            else fp_persist_f32<false><<<std::min(nunits, g_fpp_grid), FP_THREADS, fpp_smem(), st>>>(B, nunits, tr, tc);
+            if (A.siddon) launch_pdl(fp_persist_f32<true>, std::min(nunits, g_fpp_grid), FP_THREADS, fpp_smem(), st, B, nunits, tr, tc);
+            else launch_pdl(fp_persist_f32<false>, std::min(nunits, g_fpp_grid), FP_THREADS, fpp_smem(), st, B, nunits, tr, tc);
         } else {
             fp_tile_f32<0><<<grid, FP_THREADS, fp2_smem(), st>>>(B);
             fp_tile_f32<1><<<grid, FP_THREADS, fp2_smem(), st>>>(B);
@@ -1317,11 +1320,11 @@ void bp_dispatch(int epi, const BpArgs<T> &A0, dim3 grid, cudaStream_t st) {
     BpArgs<T> A = A0;
     A.magic = 0x4B000000u << 3;  // fp32 pair windows (wraps mod 2^32)
     switch (epi) {
-        case EPI_PLAIN: bp_tile_kernel<T, EPI_PLAIN><<<grid, BP_THREADS, bp_smem<T, EPI_PLAIN>(), st>>>(A); break;
-        case EPI_CGQ: bp_tile_kernel<T, EPI_CGQ><<<grid, BP_THREADS, bp_smem<T, EPI_CGQ>(), st>>>(A); break;
-        case EPI_RESID: bp_tile_kernel<T, EPI_RESID><<<grid, BP_THREADS, bp_smem<T, EPI_RESID>(), st>>>(A); break;
-        case EPI_CGR: bp_tile_kernel<T, EPI_CGR><<<grid, BP_THREADS, bp_smem<T, EPI_CGR>(), st>>>(A); break;
-        default: bp_tile_kernel<T, EPI_GD><<<grid, BP_THREADS, bp_smem<T, EPI_GD>(), st>>>(A); break;
+        case EPI_PLAIN: launch_pdl(bp_tile_kernel<T, EPI_PLAIN>, grid, BP_THREADS, bp_smem<T, EPI_PLAIN>(), st, A); break;
+        case EPI_CGQ: launch_pdl(bp_tile_kernel<T, EPI_CGQ>, grid, BP_THREADS, bp_smem<T, EPI_CGQ>(), st, A); break;
+        case EPI_RESID: launch_pdl(bp_tile_kernel<T, EPI_RESID>, grid, BP_THREADS, bp_smem<T, EPI_RESID>(), st, A); break;
+        case EPI_CGR: launch_pdl(bp_tile_kernel<T, EPI_CGR>, grid, BP_THREADS, bp_smem<T, EPI_CGR>(), st, A); break;
+        default: launch_pdl(bp_tile_kernel<T, EPI_GD>, grid, BP_THREADS, bp_smem<T, EPI_GD>(), st, A); break;
     }
 }
 
@@ -1371,8 +1374,8 @@ void launch_fp_reduce(int prec, bool resid, const void *args, int n_rows, int n_
     if (prec == 0) {
         const auto &A = *static_cast<const FpRedArgs<float> *>(args);
         const dim3 gq(ceil_div(n_det, 4 * RQ), n_rows);
-        if (resid) fp_reduce_f32<true><<<gq, RQ * RG, 0, st>>>(A);
-        else fp_reduce_f32<false><<<gq, RQ * RG, 0, st>>>(A);
+        if (resid) launch_pdl(fp_reduce_f32<true>, gq, RQ * RG, 0, st, A);
+        else launch_pdl(fp_reduce_f32<false>, gq, RQ * RG, 0, st, A);
     } else {
         const auto &A = *static_cast<const FpRedArgs<double> *>(args);
         if (resid) fp_reduce_kernel<double, true><<<grid, RJ * RG, 0, st>>>(A);

@@ -37,6 +37,7 @@ template <typename T, bool WITH_P>
 __global__ void __launch_bounds__(VT) cg_update_px(T *__restrict__ x, T *__restrict__ p, const T *__restrict__ r,
                                                    long long n, double *scal, double *partial, int part_stride,
                                                    unsigned *counter, double *pp_out, const AxUpdate au) {
+    pdl_wait();
     __shared__ double red[VT / 32 + 1];
     __shared__ bool last;
     const int node = blockIdx.y;
@@ -178,6 +179,7 @@ __global__ void convert_kernel(const A *src, B *dst, long long n) {
 
 __global__ void __launch_bounds__(VT) cg_alpha_kernel(double *scal, const double *cgs, int nfs_pa, const int *nang,
                                                       const double *cgp, int npp, const double *cnode, int part_stride) {
+    pdl_wait();
     __shared__ double red[VT / 32 + 1];
     const int node = blockIdx.x;
     const double *fs = cgs + (long long)node * part_stride, *ps = cgp + (long long)node * part_stride;
@@ -198,6 +200,7 @@ __global__ void __launch_bounds__(VT) cg_alpha_kernel(double *scal, const double
 template <typename T>
 __global__ void resid_from_ax_kernel(const T *__restrict__ d, const T *__restrict__ ax, T *__restrict__ s, int n_rows,
                                      int n_det, int sp) {
+    pdl_wait();
     const long long ne = (long long)n_rows * n_det;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (long long)gridDim.x * blockDim.x) {
         const long long row = e / n_det, j = e % n_det;
@@ -210,15 +213,15 @@ void launch_resid_from_ax(int prec, const void *d, const void *ax, void *s, int 
     const long long ne = (long long)n_rows * n_det;
     if (ne == 0) return;
     const int blocks = (int)std::min<long long>(1184, (ne + 255) / 256);
-    if (prec == 0) resid_from_ax_kernel<float><<<blocks, 256, 0, st>>>((const float *)d, (const float *)ax, (float *)s, n_rows, n_det, sp);
-    else resid_from_ax_kernel<double><<<blocks, 256, 0, st>>>((const double *)d, (const double *)ax, (double *)s, n_rows, n_det, sp);
+    if (prec == 0) launch_pdl(resid_from_ax_kernel<float>, blocks, 256, 0, st, (const float *)d, (const float *)ax, (float *)s, n_rows, n_det, sp);
+    else launch_pdl(resid_from_ax_kernel<double>, blocks, 256, 0, st, (const double *)d, (const double *)ax, (double *)s, n_rows, n_det, sp);
     TQ_CHECK_CUDA(cudaGetLastError());
 }
 
 void launch_cg_alpha(int L, double *scal, const double *cgs, int nfs_pa, const int *nang, const double *cgp,
                      int npp, const double *cnode, int part_stride, cudaStream_t st) {
     if (L == 0) return;
-    cg_alpha_kernel<<<L, VT, 0, st>>>(scal, cgs, nfs_pa, nang, cgp, npp, cnode, part_stride);
+    launch_pdl(cg_alpha_kernel, L, VT, 0, st, scal, cgs, nfs_pa, nang, cgp, npp, cnode, part_stride);
     TQ_CHECK_CUDA(cudaGetLastError());
 }
 
@@ -227,11 +230,11 @@ void launch_cg_update_px(int prec, void *x, void *p, const void *r, long long n,
                          const AxUpdate &au, cudaStream_t st) {
     dim3 grid(vec_blocks(n), L);
     if (prec == 0) {
-        if (with_p) cg_update_px<float, true><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal, partial, part_stride, counter, pp_out, au);
-        else cg_update_px<float, false><<<grid, VT, 0, st>>>((float *)x, (float *)p, (const float *)r, n, scal, partial, part_stride, counter, pp_out, au);
+        if (with_p) launch_pdl(cg_update_px<float, true>, grid, VT, 0, st, (float *)x, (float *)p, (const float *)r, n, scal, partial, part_stride, counter, pp_out, au);
+        else launch_pdl(cg_update_px<float, false>, grid, VT, 0, st, (float *)x, (float *)p, (const float *)r, n, scal, partial, part_stride, counter, pp_out, au);
     } else {
-        if (with_p) cg_update_px<double, true><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal, partial, part_stride, counter, pp_out, au);
-        else cg_update_px<double, false><<<grid, VT, 0, st>>>((double *)x, (double *)p, (const double *)r, n, scal, partial, part_stride, counter, pp_out, au);
+        if (with_p) launch_pdl(cg_update_px<double, true>, grid, VT, 0, st, (double *)x, (double *)p, (const double *)r, n, scal, partial, part_stride, counter, pp_out, au);
+        else launch_pdl(cg_update_px<double, false>, grid, VT, 0, st, (double *)x, (double *)p, (const double *)r, n, scal, partial, part_stride, counter, pp_out, au);
     }
     TQ_CHECK_CUDA(cudaGetLastError());
 }
