@@ -204,7 +204,12 @@ __global__ void __launch_bounds__(SCW * 32) km_scan(KmPtr w) {
 
 // stable scatter of one tile by the digit: rank = (keys of the digit in earlier warps)
 // + (in earlier rounds of my warp) + (in lower lanes of my round); destination =
-// offset(digit, tile) + rank.
+// offset(digit, tile) + rank.  STABLE = false (the first LSD pass, whose input order is
+// arbitrary anyway): the in-warp rank is a shared-memory atomic on the warp's digit counter
+// instead of the ballot multisplit.  The order of equal keys inside a 24-bit group is never
+// observed (every Lloyd quantity is a count or an integer sum over whole groups, R-16), so
+// the results stay bitwise deterministic.
+template <bool STABLE>
 __global__ void __launch_bounds__(KT, 3) km_scatter(const uint32_t *kin, uint32_t *kout, KmPtr w, int shift) {
     pdl_wait();
     using Scan = cub::BlockScan<uint32_t, KT>;
@@ -222,16 +227,21 @@ __global__ void __launch_bounds__(KT, 3) km_scatter(const uint32_t *kin, uint32_
     for (int i = lane; i < 256; i += 32) c[i] = 0u;
     __syncwarp();
     const unsigned lt = (1u << lane) - 1u;
+    if (STABLE) {
 #pragma unroll
-    for (int r = 0; r < KI; r++) {
-        const uint32_t d = (k[r] >> shift) & 255u;
-        const unsigned peers = digit_peers(d);
-        const uint32_t before = c[d];
-        const uint32_t lower = (uint32_t)__popc(peers & lt);  // 0 for the lowest peer
-        rank[r] = before + lower;
-        __syncwarp();
-        if (lower == 0u) c[d] = before + (uint32_t)__popc(peers);
-        __syncwarp();
+        for (int r = 0; r < KI; r++) {
+            const uint32_t d = (k[r] >> shift) & 255u;
+            const unsigned peers = digit_peers(d);
+            const uint32_t before = c[d];
+            const uint32_t lower = (uint32_t)__popc(peers & lt);  // 0 for the lowest peer
+            rank[r] = before + lower;
+            __syncwarp();
+            if (lower == 0u) c[d] = before + (uint32_t)__popc(peers);
+            __syncwarp();
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < KI; r++) rank[r] = atomicAdd(&c[(k[r] >> shift) & 255u], 1u);
     }
     __syncthreads();
     uint32_t run = 0;  // exclusive prefix over warps, per digit (thread = digit), in place
@@ -719,7 +729,8 @@ int kmeans_encode(const float *const *v, KmeansWork &ws, int lloyd, uint8_t *con
     for (int pass = 1; pass < 4; pass++) {
         if (pass > 1) { launch_pdl(km_hist, tiles, KT, 0, st, (const uint32_t *)src, w, 8 * pass); k++; }
         launch_pdl(km_scan, dim3(256 / 32, P), SCW * 32, 0, st, w);
-        launch_pdl(km_scatter, tiles, KT, 0, st, (const uint32_t *)src, dst, w, 8 * pass);
+        if (pass == 1) launch_pdl(km_scatter<false>, tiles, KT, 0, st, (const uint32_t *)src, dst, w, 8 * pass);
+        else launch_pdl(km_scatter<true>, tiles, KT, 0, st, (const uint32_t *)src, dst, w, 8 * pass);
         k += 2;
         std::swap(src, dst);
     }
