@@ -92,15 +92,30 @@ def test_graph_rule_c2_bitwise(world):
         assert s["world"] == world and s["nccl_bytes_sent"] > 0 and s["nccl_bytes_recv"] > 0
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_graph_rule_bench_config_bitwise(world):
     """The bench workload C4_G1 (1024^2, 8 nodes on a random 4-regular graph, K-means 64)
-    split over 2 / 4 ranks equals the one-rank run bit for bit."""
+    split over 2 / 4 / 8 ranks (8: one node per rank, the layout of an 8-GPU run) equals the
+    one-rank run bit for bit."""
     cfg = C.C4(1)
     inp = C.make_inputs(cfg, with_truth=False)
     iters = 2
     ref = reference_images(cfg, inp, iters)[0]
     ctxs, nr = run_world(cfg, inp, world, iters)
+    got = node_images(ctxs, nr, cfg)
+    close_all(ctxs)
+    assert np.array_equal(got, ref)
+
+
+def test_graph_rule_kept_ax_refresh_cadence_bitwise():
+    """20 iterations (past the kept A x's refresh at iteration 16, R-8): one rank runs them as
+    four-iteration graphs, two ranks one iteration per graph between exchanges -- the refresh
+    points coincide and the runs stay bitwise equal."""
+    cfg = C.C2()
+    inp = C.make_inputs(cfg, with_truth=False)
+    iters = 20
+    ref = reference_images(cfg, inp, iters)[0]
+    ctxs, nr = run_world(cfg, inp, 2, iters)
     got = node_images(ctxs, nr, cfg)
     close_all(ctxs)
     assert np.array_equal(got, ref)
