@@ -319,6 +319,17 @@ def test_siddon_axis_rays_exact_half_split():
         assert np.max(np.abs(got - ref)) <= (2e-5 if prec == 0 else 1e-12) * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("n,K", [(1 << 20, 64), (2048 * 2048, 32)])
+def test_kmeans_encode_bitwise_repeatable(n, K):
+    """The first radix pass ranks keys with shared-memory atomics, so the order of equal keys
+    inside a sort group differs from call to call; every output (centres, bit-planes, labels)
+    must not: repeated encodes of the same payload are bitwise equal (R-16)."""
+    v = torch.tensor(kmeans_input(n, 11 + K), device=DEV)
+    outs = [tomoq.kmeans_encode(v, K, 10) for _ in range(3)]
+    for cen, planes, lab in outs[1:]:
+        assert torch.equal(cen, outs[0][0]) and torch.equal(planes, outs[0][1]) and torch.equal(lab, outs[0][2])
+
+
 def test_kmeans_ties_and_extreme_ranges():
     """Values equal to a threshold go to the lower cluster on both sides (R-16); the final
     assignment's bucket map stays exact when the payload range overflows fp32 (max - min =
