@@ -36,6 +36,49 @@ def test_cg_matches_dense_solve():
     assert rel(x, x_ref) <= 1e-10
 
 
+@pytest.mark.parametrize("e1", [1, 2, 5])
+def test_cg_restructured_as_on_the_gpu_equals_oracle_cg(e1):
+    """DESIGN.md R-8: the CUDA path runs CG with p.q formed as ||A p||^2 + c ||p||^2 from the
+    forward projection, r -= alpha q fused into the backprojection, no backprojection in the
+    last step, and the residual's A x kept across solves (A x += alpha A p).  Written out here
+    with the oracle's projector on a dense problem, two consecutive solves (the second from
+    the first's x with a new b', through the kept A x) equal the oracle's CG to fp64 rounding."""
+    N, n_ang, n_det = 16, 24, 23
+    sel = list(range(2, n_ang, 3))
+    rng = np.random.default_rng(3 + e1)
+    d = rng.standard_normal((len(sel), n_det))
+    c = 1.3
+    A = lambda v: oracle.project(v.reshape(N, N), n_ang, n_det, sel)
+    At = lambda y: oracle.backproject(y, N, n_ang, sel).reshape(-1)
+
+    def solve(x, bp, ax):
+        r = At(d - ax) + bp - c * x
+        p, rr = r.copy(), r @ r
+        pp = rr
+        for it in range(e1):
+            s = A(p)
+            alpha = rr / (np.sum(s * s) + c * pp)
+            if it + 1 < e1:
+                r = r - alpha * (At(s) + c * p)
+                rr_new = r @ r
+                beta = rr_new / rr
+                rr = rr_new
+            x = x + alpha * p
+            ax = ax + alpha * s
+            if it + 1 < e1:
+                p = r + beta * p
+                pp = p @ p
+        return x, ax
+
+    x = rng.standard_normal(N * N)
+    bp1, bp2 = rng.standard_normal(N * N), rng.standard_normal(N * N)
+    x1, ax1 = solve(x, bp1, A(x))
+    x2, _ = solve(x1, bp2, ax1)
+    o1 = oracle.cg(d, bp1, c, e1, x.reshape(N, N), n_ang, sel)
+    o2 = oracle.cg(d, bp2, c, e1, o1, n_ang, sel)
+    assert rel(x1, o1) <= 1e-12 and rel(x2, o2) <= 1e-12
+
+
 def test_cg_one_step_is_exact_line_search():
     """One CG step from x0 is steepest descent with exact line search on the quadratic."""
     N, n_ang, n_det = 12, 10, 17
