@@ -888,18 +888,19 @@ __global__ void __launch_bounds__(RQ * RG) fp_reduce_f32(const FpRedArgs<float> 
             nn.M = (float)(8.0 + 3.0 * fabs(G.at));
         }
         int lt = l0;
-        for (; lt + 4 <= l1; lt += 4) {  // up to 8 quads in flight
-            unsigned nm[4];
+        constexpr int FB = 8;  // bands per batch: up to 16 quads in flight (the sums keep band order)
+        for (; lt + FB <= l1; lt += FB) {
+            unsigned nm[FB];
 #pragma unroll
-            for (int u = 0; u < 4; u++) nm[u] = a.rgeo ? fp_band_need(nn, lt + u) : 3u;
-            float4 x[8];
+            for (int u = 0; u < FB; u++) nm[u] = a.rgeo ? fp_band_need(nn, lt + u) : 3u;
+            float4 x[2 * FB];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < FB; u++) {
                 x[2 * u] = ldcg_if(p + (2 * (lt + u)) * nq, nm[u] & 1u);
                 x[2 * u + 1] = ldcg_if(p + (2 * (lt + u) + 1) * nq, nm[u] & 2u);
             }
 #pragma unroll
-            for (int u = 0; u < 8; u += 2) {
+            for (int u = 0; u < 2 * FB; u += 2) {
                 acc.x += x[u].x + x[u + 1].x;
                 acc.y += x[u].y + x[u + 1].y;
                 acc.z += x[u].z + x[u + 1].z;
