@@ -232,6 +232,19 @@ tq_status tq_get_stats(const tq_ctx *ctx, tq_stats *out);
  * of never-written memory change results.  This call checks every live allocation's guards now
  * (TQ_OK when TQ_GUARD is unset). */
 tq_status tq_debug_guard_check(void);
+/* Transport self-check (the A7 exchange layer alone): creates the transport of
+ * `id` (tq_nccl_unique_id or tq_loopback_id) for (rank, world) on `device`, and `rounds` times
+ * runs each of its operations on a synthetic plan: every rank sends `bytes` bytes to every rank
+ * INCLUDING ITSELF (so NCCL's grouped ncclSend / ncclRecv, ncclReduce and ncclAllReduce all run
+ * even at world == 1, e.g. on a one-GPU box, where NCCL refuses two ranks per device), then the
+ * ranks' `n_doubles`-element fp64 buffers are summed onto segment owners (segment g of `world`,
+ * owner g, as the consensus rule's reduce), then the maximum of the rank ids is taken.  Every
+ * received byte and owned sum is compared with its exact host value.  Called by every rank of
+ * the world (loopback: one host thread per rank of this process).  Blocking; allocates and
+ * frees its own buffers.  TQ_OK when everything matched; TQ_ENCCL (message in
+ * tq_last_error_global) on a mismatch or a transport error; TQ_EINVAL on bad arguments. */
+tq_status tq_debug_transport_check(const uint8_t id[128], int32_t rank, int32_t world, int32_t device,
+                                   int64_t bytes, int64_t n_doubles, int32_t rounds);
 /* Phase timing (tq_stats.phase_ms): on = 1 makes later runs launch each phase as its own CUDA
  * graph with timing events in between (slightly slower than the default whole-iteration
  * graph; off by default).  Waits for an enqueued run. */

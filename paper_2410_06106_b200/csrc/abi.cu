@@ -239,6 +239,14 @@ tq_status tq_debug_guard_check(void) {
     });
 }
 
+tq_status tq_debug_transport_check(const uint8_t id[128], int32_t rank, int32_t world, int32_t device,
+                                   int64_t bytes, int64_t n_doubles, int32_t rounds) {
+    return guard(nullptr, [&] {
+        TQ_REQUIRE(id != nullptr, "null transport id");
+        transport_check(id, rank, world, device, bytes, n_doubles, rounds);
+    });
+}
+
 const char *tq_last_error(const tq_ctx *ctx) { return ctx ? ctx->c.err.c_str() : g_err.c_str(); }
 const char *tq_last_error_global(void) { return g_err.c_str(); }
 

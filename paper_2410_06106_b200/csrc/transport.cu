@@ -311,4 +311,91 @@ std::unique_ptr<Transport> make_transport(const uint8_t id[128], int rank, int w
     return std::unique_ptr<Transport>(new NcclTransport(id, rank, world, device));
 }
 
+
+// ---------------------------------------------------------------- transport self-check
+// Every operation of the Transport interface on a synthetic plan (tq_debug_transport_check):
+// each rank sends `bytes` bytes to every rank including itself (a self send / receive is an
+// ordinary NCCL point-to-point pair), then sums `n_doubles` doubles over the ranks onto
+// segment owners (segment g of `world`, owner g), then takes the maximum of the rank ids.
+// Byte k sent from rank a to rank b is pattern(a, b, k); element i of rank a's sum buffer is
+// a + 1 + i / 2, so every expected value is exact and known on the host.
+namespace {
+inline uint8_t xcheck_byte(int a, int b, long long k) {
+    return (uint8_t)(a * 37 + b * 11 + k * 7 + (k >> 8));
+}
+}  // namespace
+
+void transport_check(const uint8_t id[128], int rank, int world, int device, long long bytes, long long n_doubles,
+                     int rounds) {
+    TQ_REQUIRE(world >= 1 && rank >= 0 && rank < world, "bad rank/world");
+    TQ_REQUIRE(bytes >= 1 && n_doubles >= 1 && rounds >= 1, "bytes, n_doubles and rounds must be >= 1");
+    TQ_CHECK_CUDA(cudaSetDevice(device));
+    std::unique_ptr<Transport> tr = make_transport(id, rank, world, device);
+    cudaStream_t s = nullptr;
+    TQ_CHECK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    uint8_t *sbuf = nullptr, *rbuf = nullptr;
+    double *sum = nullptr;
+    std::string bad;
+    try {
+        TQ_CHECK_CUDA(cudaMalloc(&sbuf, (size_t)bytes * world));
+        TQ_CHECK_CUDA(cudaMalloc(&rbuf, (size_t)bytes * world));
+        TQ_CHECK_CUDA(cudaMalloc(&sum, sizeof(double) * (size_t)n_doubles));
+        std::vector<uint8_t> hs((size_t)bytes * world), hr((size_t)bytes * world);
+        for (int q = 0; q < world; q++)
+            for (long long k = 0; k < bytes; k++) hs[(size_t)q * bytes + k] = xcheck_byte(rank, q, k);
+        std::vector<double> hsum((size_t)n_doubles);
+        // segment g = [g * per, ...) owned by rank g (the last one takes the remainder)
+        std::vector<SumSeg> segs;
+        const long long per = n_doubles / world;
+        for (int g = 0; g < world; g++) {
+            const long long off = g * per, cnt = g + 1 < world ? per : n_doubles - off;
+            if (cnt > 0) segs.push_back({off, cnt, g});
+        }
+        std::vector<XferDesc> sends, recvs;  // sorted by (peer, node) as the engine's plan
+        for (int q = 0; q < world; q++) {
+            sends.push_back({0, rank, q, sbuf + (size_t)q * bytes, bytes});
+            recvs.push_back({0, q, q, rbuf + (size_t)q * bytes, bytes});
+        }
+        for (int round = 0; round < rounds && bad.empty(); round++) {
+            for (long long i = 0; i < n_doubles; i++) hsum[(size_t)i] = rank + 1 + 0.5 * (double)i + round;
+            TQ_CHECK_CUDA(cudaMemcpyAsync(sbuf, hs.data(), hs.size(), cudaMemcpyHostToDevice, s));
+            TQ_CHECK_CUDA(cudaMemsetAsync(rbuf, 0, hr.size(), s));
+            TQ_CHECK_CUDA(cudaMemcpyAsync(sum, hsum.data(), sizeof(double) * hsum.size(), cudaMemcpyHostToDevice, s));
+            tr->exchange(s, sends, recvs);
+            tr->reduce_sum(s, sum, segs);
+            TQ_CHECK_CUDA(cudaMemcpyAsync(hr.data(), rbuf, hr.size(), cudaMemcpyDeviceToHost, s));
+            TQ_CHECK_CUDA(cudaMemcpyAsync(hsum.data(), sum, sizeof(double) * hsum.size(), cudaMemcpyDeviceToHost, s));
+            TQ_CHECK_CUDA(cudaStreamSynchronize(s));
+            const double mx = tr->allreduce_max((double)rank + round, s);
+            for (int q = 0; q < world && bad.empty(); q++)
+                for (long long k = 0; k < bytes; k++)
+                    if (hr[(size_t)q * bytes + k] != xcheck_byte(q, rank, k)) {
+                        bad = "exchange: byte " + std::to_string(k) + " from rank " + std::to_string(q) + " differs";
+                        break;
+                    }
+            const double rs = 0.5 * world * (world + 1) + (double)world * round;  // sum of (a + 1 + round)
+            for (const SumSeg &g : segs) {
+                if (g.root != rank || !bad.empty()) continue;
+                for (long long i = g.off; i < g.off + g.count; i++)
+                    if (hsum[(size_t)i] != rs + 0.5 * (double)world * (double)i) {
+                        bad = "reduce_sum: element " + std::to_string(i) + " differs";
+                        break;
+                    }
+            }
+            if (bad.empty() && mx != (double)(world - 1 + round)) bad = "allreduce_max differs";
+        }
+    } catch (...) {
+        if (sbuf) cudaFree(sbuf);
+        if (rbuf) cudaFree(rbuf);
+        if (sum) cudaFree(sum);
+        cudaStreamDestroy(s);
+        throw;
+    }
+    cudaFree(sbuf);
+    cudaFree(rbuf);
+    cudaFree(sum);
+    cudaStreamDestroy(s);
+    if (!bad.empty()) fail(TQ_ENCCL, std::string(tr->name()) + " transport check failed: " + bad);
+}
+
 }  // namespace tq

@@ -76,5 +76,9 @@ struct Transport {
 std::unique_ptr<Transport> make_transport(const uint8_t id[128], int rank, int world, int device);
 bool is_loopback_id(const uint8_t id[128]);
 void new_loopback_id(uint8_t id[128]);
+// tq_debug_transport_check (include/tomoq.h): every Transport operation on a synthetic plan,
+// results compared with their exact host values; throws TQ_ENCCL on a mismatch
+void transport_check(const uint8_t id[128], int rank, int world, int device, long long bytes, long long n_doubles,
+                     int rounds);
 
 }  // namespace tq

@@ -90,6 +90,7 @@ _SIGS = {
     "tq_get_stats": [_vp, C.POINTER(Stats)],
     "tq_set_profiling": [_vp, _i32],
     "tq_debug_guard_check": [],
+    "tq_debug_transport_check": [_vp, _i32, _i32, _i32, _i64, _i64, _i32],
     "tq_get_node_bytes": [_vp, _i32, _i32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
     "tq_launch_component": [_vp, _i32, _i32, _vp, C.POINTER(C.c_int64)],
     "tq_partition_angles": [_i32, _i32, _i32, _vp, _vp],
@@ -190,6 +191,14 @@ def nccl_unique_id() -> bytes:
 def debug_guard_check():
     """tq_debug_guard_check: raises if a guard band (TQ_GUARD=1) was overwritten."""
     _check(lib().tq_debug_guard_check())
+
+
+def debug_transport_check(tid: bytes, rank: int, world: int, device: int = 0, nbytes: int = 1 << 20,
+                          n_doubles: int = 1 << 16, rounds: int = 2):
+    """tq_debug_transport_check: every operation of the transport `tid` (NCCL or loopback id)
+    on a synthetic plan, results compared with exact host values; raises on a mismatch."""
+    buf = (C.c_uint8 * 128).from_buffer_copy(tid)
+    _check(lib().tq_debug_transport_check(buf, rank, world, device, nbytes, n_doubles, rounds))
 
 
 def loopback_id() -> bytes:
