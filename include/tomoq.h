@@ -126,7 +126,8 @@ typedef struct {
                                       when tq_params.stop_tol stopped it) */
     double rel_change_last;        /* r_k of the last iteration (stop_tol > 0), else -1 */
     int32_t phase_valid;           /* 1: phase_ms holds the last run's phases (tq_set_profiling) */
-    int32_t pad_;
+    int32_t node_groups;           /* concurrent node groups of the last run's iteration graph (1, or 2:
+                                      TQ_GROUPS, DESIGN.md 6.1 "two node groups") */
     double phase_ms[4];            /* device ms of the last run, summed over its iterations:
                                       [0] inner solves (A3: the E1 CG / GD steps of every local
                                       node; plus Alg. 3 / the consensus partial sums and their

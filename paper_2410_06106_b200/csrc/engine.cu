@@ -166,6 +166,9 @@ void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int ran
     TQ_CHECK_CUDA(cudaSetDevice(device));
     TQ_CHECK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     TQ_CHECK_CUDA(cudaStreamCreateWithFlags(&up_stream, cudaStreamNonBlocking));
+    TQ_CHECK_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    TQ_CHECK_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    TQ_CHECK_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     TQ_CHECK_CUDA(cudaEventCreate(&ev0));
     TQ_CHECK_CUDA(cudaEventCreate(&ev1));
     TQ_CHECK_CUDA(cudaEventCreateWithFlags(&run_done, cudaEventDisableTiming));
@@ -211,6 +214,9 @@ void Ctx::free_exchange() {
     for (void *p : owned) cudaFree(p);
     owned.clear();
     kmw.release();
+    kmw_g[0].release();
+    kmw_g[1].release();
+    ngroups = 1;
     dctw.release();
     jenc.release();
     jdec.release();
@@ -282,6 +288,11 @@ void Ctx::destroy() {
     stream = nullptr;
     if (up_stream) cudaStreamDestroy(up_stream);
     up_stream = nullptr;
+    if (s2) cudaStreamDestroy(s2);
+    s2 = nullptr;
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    ev_fork = ev_join = nullptr;
 }
 
 void Ctx::set_params(const tq_params &p) {
@@ -597,6 +608,27 @@ void Ctx::setup_exchange() {
             D.out = (void **)upload(out.data(), sizeof(void *) * D.P);
         }
     }
+    // ---- node groups (TQ_GROUPS, default 2; 1 = one launch sequence over all nodes): the graph
+    // rule's fp32 path whose only encode batch is K-means over exactly the local nodes, in order
+    {
+        const char *env = getenv("TQ_GROUPS");
+        const int want = env ? atoi(env) : 2;
+        bool ok = want >= 2 && L >= 2 && prec == 0 && rule == TQ_RULE_GRAPH && geo.N % 4 == 0 && enc[2].P == 0;
+        if (ok && enc[1].P) {
+            ok = enc[1].P == L && !enc[1].need_conv;
+            for (int b = 0; ok && b < enc[1].P; b++) {
+                const Pay &p = pays[enc[1].members[b]];
+                ok = local(p.slice, p.node) == b;
+            }
+        }
+        if (ok) {
+            ngroups = 2;
+            grp_n0[0] = 0; grp_cnt[0] = L / 2;
+            grp_n0[1] = L / 2; grp_cnt[1] = L - L / 2;
+            if (enc[1].P)
+                for (int g = 0; g < 2; g++) kmw_g[g].alloc(grp_cnt[g], q.k, payload_len);
+        }
+    }
     // ---- consensus tables
     if (!paper) {
         xh_tab = (const void **)upload(xh.data(), sizeof(void *) * xh.size());
@@ -744,6 +776,42 @@ void Ctx::ax_before(int iters, cudaStream_t s) {
     ax_age += iters;
 }
 
+bool Ctx::grouped() const {
+    return ngroups == 2 && rule == TQ_RULE_GRAPH && prm.inner == TQ_INNER_CG && prec == 0;
+}
+
+int Ctx::stage01_grouped(cudaStream_t s) {
+    TQ_CHECK_CUDA(cudaEventRecord(ev_fork, s));
+    TQ_CHECK_CUDA(cudaStreamWaitEvent(s2, ev_fork, 0));
+    int k = 0;
+    for (int g = 0; g < 2; g++) {
+        cudaStream_t sg = g ? s2 : s;
+        k += in.cg(geo, prm.e1, sg, use_ax() ? AX_CACHED : AX_OFF, grp_n0[g], grp_cnt[g]);
+        Batch &E = enc[TQ_Q_KMEANS];
+        if (E.P) {
+            const int b0 = grp_n0[g];
+            k += kmeans_encode(E.vin + b0, kmw_g[g], q.lloyd_iters, E.pay + b0, E.labels ? E.labels + b0 : nullptr,
+                               sg, E.dec_out ? E.dec_out + b0 : nullptr, prec);
+        }
+    }
+    TQ_CHECK_CUDA(cudaEventRecord(ev_join, s2));
+    TQ_CHECK_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+    return k;
+}
+
+int Ctx::stages(const std::vector<int> &ids, cudaStream_t s) {
+    int c = 0;
+    for (size_t i = 0; i < ids.size(); i++) {
+        if (ids[i] == 0 && i + 1 < ids.size() && ids[i + 1] == 1 && grouped()) {
+            c += stage01_grouped(s);
+            i++;
+        } else {
+            c += stage(ids[i], s);
+        }
+    }
+    return c;
+}
+
 int Ctx::stage(int id, cudaStream_t s) {
     if (id == 2) return phase_b(s);
     int k = 0;
@@ -844,7 +912,7 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
         TQ_CHECK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         int c = 0;
         try {
-            for (int id : ids) c += stage(id, s);
+            c += stages(ids, s);
         } catch (...) {
             if (cudaStreamEndCapture(s, &g) == cudaSuccess && g) cudaGraphDestroy(g);
             (void)cudaGetLastError();  // do not leave the capture failure as the sticky last error
@@ -887,7 +955,7 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
         TQ_CHECK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         int c = 0;
         try {
-            for (int rep = 0; rep < MULTI; rep++) c += stage(0, s) + stage(1, s) + stage(2, s);
+            for (int rep = 0; rep < MULTI; rep++) c += stages({0, 1, 2}, s);
         } catch (...) {
             if (cudaStreamEndCapture(s, &g) == cudaSuccess && g) cudaGraphDestroy(g);
             (void)cudaGetLastError();
@@ -959,6 +1027,7 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
     st.iters_last_run = done;
     st.kernel_launches = (long long)done * per_iter + (stop ? done : 0);
     st.phase_valid = 0;
+    st.node_groups = (!profiling && grouped()) ? 2 : 1;
     pending = true;
     pending_iters = done;
     prof_iters = profiling ? done : 0;

@@ -495,6 +495,8 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
         if (u >= nunits) return false;
         if (threadIdx.x == 0) {
             const FpUnit U = fp_unit(a, u, ntiles);
+            // unit tables are laid out over all L_all nodes: (O, node0 + node, tile)
+            const long long ug = ((long long)U.O * a.L_all + a.node0 + U.node) * ntiles + U.tile;
             const int lt = U.tile / a.nt_cross, ct = U.tile % a.nt_cross;
             s_hdr[rb][0] = U.O; s_hdr[rb][1] = U.tile; s_hdr[rb][2] = U.a_begin; s_hdr[rb][3] = U.a_end;
             s_hdr[rb][4] = lt; s_hdr[rb][5] = ct;
@@ -507,7 +509,7 @@ __global__ void __launch_bounds__(FP_THREADS, 3) fp_persist_f32(const FpArgs<flo
             if (nb > 0) {
                 bulk_load(rec_s + (uint32_t)(rb * FPP_MAXA * sizeof(FpRec)), a.recs + (long long)U.tile * a.n_olist + U.a_begin,
                           nb * (unsigned)sizeof(FpRec), bar_s);
-                bulk_load((uint32_t)__cvta_generic_to_shared(utb + rb), a.utab + u, (unsigned)sizeof(FpUnitTab), bar_s);
+                bulk_load((uint32_t)__cvta_generic_to_shared(utb + rb), a.utab + ug, (unsigned)sizeof(FpUnitTab), bar_s);
             }
         }
         return true;
@@ -784,7 +786,7 @@ __device__ __forceinline__ void fp_cg_partial(const FpRedArgs<T> &a, int row, do
 template <typename T, bool RESID>
 __global__ void __launch_bounds__(RJ * RG) fp_reduce_kernel(const FpRedArgs<T> a) {
     __shared__ T part[RG][RJ];
-    const int row = blockIdx.y;
+    const int row = blockIdx.y + a.row_base;
     const double m_row = fp_row_m(a, row);  // issued first: its latency overlaps the slot loads
     const int jj = threadIdx.x % RJ, g = threadIdx.x / RJ;
     const int j = blockIdx.x * RJ + jj;
@@ -864,7 +866,7 @@ template <bool RESID>
 __global__ void __launch_bounds__(RQ * RG) fp_reduce_f32(const FpRedArgs<float> a) {
     pdl_wait();
     __shared__ float4 part[RG][RQ];
-    const int row = blockIdx.y;
+    const int row = blockIdx.y + a.row_base;
     const double m_row = fp_row_m(a, row);  // issued first: its latency overlaps the slot loads
     const int q = threadIdx.x % RQ, g = threadIdx.x / RQ;
     const int j0 = 4 * (blockIdx.x * RQ + q);

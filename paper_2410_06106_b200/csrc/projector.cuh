@@ -107,8 +107,11 @@ struct FpArgs {
     uint32_t magic;        // = 0x4B000000 << 2 (mod 2^32), see projector.cu magic_base
     const FpRec *recs;     // [ntiles][n_olist] (fp32 persistent kernel)
     int n_olist, L;
-    const FpUnitTab *utab; // [2 * L * ntiles] (fp32 persistent kernel)
+    const FpUnitTab *utab; // [2 * L_all * ntiles] (fp32 persistent kernel)
     int siddon;            // 1: Siddon weights (R-26) -- generic tile kernel
+    // node group (persistent fp32 kernel): the launch covers nodes [node0, node0 + L) of the
+    // L_all nodes the unit tables were built for; img and oofs point at node0's entries
+    int node0, L_all;
 };
 
 // per ray row of a context: (cos, sin, m, 1/w) of its angle for the backprojector (one load
@@ -137,6 +140,7 @@ struct FpRedArgs {
     int cg;
     double *cgs;           // [L][part_stride]
     int part_stride;
+    int row_base;          // the launch reduces rows [row_base, row_base + gridDim.y) (a node group)
 };
 
 template <typename T>

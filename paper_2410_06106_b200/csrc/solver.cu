@@ -114,41 +114,55 @@ void Inner::release() {
 }
 
 int Inner::project(const DevGeom &g, const void *img, bool resid, cudaStream_t st, void *out,
-                   int out_stride, int out_off, bool cg) {
+                   int out_stride, int out_off, bool cg, int n0, int cnt) {
     if (!out) { out = S; out_stride = sp; out_off = 1; }
+    if (cnt < 0) cnt = L - n0;
+    const bool grp = n0 != 0 || cnt != L;
+    // a node group [n0, n0 + cnt): its images, unit groups and (contiguous) ray rows
+    const int rb = n0 < L ? row0_h[n0] : n_rows, nr = (n0 + cnt < L ? row0_h[n0 + cnt] : n_rows) - rb;
     if (prec == 0) {
-        FpArgs<float> a{(const float *)img, n, g.N, g.n_det, olist, oofs, fwin, frg, (float *)fpart,
-                        nt_line, nt_cross, kMagicBits4, frec, n_olist, L, futab, g.proj};
-        launch_fp(0, &a, L, st);
+        TQ_REQUIRE(!grp || (g.N % 4 == 0 && frec), "node groups need the persistent fp32 forward kernel");
+        FpArgs<float> a{(const float *)img + n * n0, n, g.N, g.n_det, olist, oofs + 2 * n0, fwin, frg, (float *)fpart,
+                        nt_line, nt_cross, kMagicBits4, frec, n_olist, cnt, futab, g.proj, n0, L};
+        launch_fp(0, &a, cnt, st);
         FpRedArgs<float> r{(const float *)fpart, rows, g.trig, g.xmaj, (const float *)D, (float *)out,
                            out_stride, out_off, g.N, g.n_det, nt_line, rowc, frg, nt_cross,
-                           cg ? 1 : 0, cgs, part_stride};
-        launch_fp_reduce(0, resid, &r, n_rows, g.n_det, st);
+                           cg ? 1 : 0, cgs, part_stride, rb};
+        launch_fp_reduce(0, resid, &r, nr, g.n_det, st);
     } else {
+        TQ_REQUIRE(!grp, "node groups are fp32 only");
         FpArgs<double> a{(const double *)img, n, g.N, g.n_det, olist, oofs, fwin, frg, (double *)fpart,
-                         nt_line, nt_cross, kMagicBits4, frec, n_olist, L, futab, g.proj};
+                         nt_line, nt_cross, kMagicBits4, frec, n_olist, L, futab, g.proj, 0, L};
         launch_fp(1, &a, L, st);
         FpRedArgs<double> r{(const double *)fpart, rows, g.trig, g.xmaj, (const double *)D,
                             (double *)out, out_stride, out_off, g.N, g.n_det, nt_line, rowc, nullptr, nt_cross,
-                            cg ? 1 : 0, cgs, part_stride};
+                            cg ? 1 : 0, cgs, part_stride, 0};
         launch_fp_reduce(1, resid, &r, n_rows, g.n_det, st);
     }
     return 3;
 }
 
 int Inner::backproject(const DevGeom &g, int epi, void *out, void *out2, const void *vin, cudaStream_t st,
-                       const void *rin) {
+                       const void *rin, int n0, int cnt) {
     const void *b2 = epi == EPI_CGR ? rin : BP;  // second epilogue operand: b' (RESID, GD) or r (CGR)
+    if (cnt < 0) cnt = L - n0;
+    // a node group: every node-indexed table and node-major vector starts at node n0 (the
+    // sinogram rows are addressed through the absolute node_row0 values)
+    const long long o = n * n0;
     if (prec == 0) {
-        BpArgs<float> a{(const float *)S, sp, 1, row0, nang, rows, g.trig, g.xmaj, g.N, g.n_det, n,
-                        (float *)out, (float *)out2, (const float *)vin, (const float *)b2, cnode, eta,
-                        partial, counter, scal, part_stride, kMagicBits4, g.proj, rowc};
-        launch_bp(0, epi, &a, L, g.N, st);
+        auto f = [o](const void *p) { return p ? (float *)p + o : nullptr; };
+        BpArgs<float> a{(const float *)S, sp, 1, row0 + n0, nang + n0, rows, g.trig, g.xmaj, g.N, g.n_det, n,
+                        f(out), f(out2), f(vin), f(b2), cnode + n0, eta + n0,
+                        partial + (long long)part_stride * n0, counter + n0, scal + (long long)S_NSLOT * n0,
+                        part_stride, kMagicBits4, g.proj, rowc};
+        launch_bp(0, epi, &a, cnt, g.N, st);
     } else {
-        BpArgs<double> a{(const double *)S, sp, 1, row0, nang, rows, g.trig, g.xmaj, g.N, g.n_det, n,
-                         (double *)out, (double *)out2, (const double *)vin, (const double *)b2, cnode,
-                         eta, partial, counter, scal, part_stride, kMagicBits4, g.proj, rowc};
-        launch_bp(1, epi, &a, L, g.N, st);
+        auto f = [o](const void *p) { return p ? (double *)p + o : nullptr; };
+        BpArgs<double> a{(const double *)S, sp, 1, row0 + n0, nang + n0, rows, g.trig, g.xmaj, g.N, g.n_det, n,
+                         f(out), f(out2), f(vin), f(b2), cnode + n0, eta + n0,
+                         partial + (long long)part_stride * n0, counter + n0, scal + (long long)S_NSLOT * n0,
+                         part_stride, kMagicBits4, g.proj, rowc};
+        launch_bp(1, epi, &a, cnt, g.N, st);
     }
     return 1;
 }
@@ -161,26 +175,34 @@ int Inner::backproject(const DevGeom &g, int epi, void *out, void *out2, const v
 // -- p.q = p.(A^T A p + c p) written through A p, so q is never stored and the residual
 // update rides on the backprojection; the last step needs neither r nor beta (the next
 // solve restarts from the residual backprojection), so it has no backprojection at all.
-int Inner::cg(const DevGeom &g, int e1, cudaStream_t st, int ax) {
+int Inner::cg(const DevGeom &g, int e1, cudaStream_t st, int ax, int n0, int cnt) {
+    if (cnt < 0) cnt = L - n0;
+    const int rb = n0 < L ? row0_h[n0] : n_rows, nr = (n0 + cnt < L ? row0_h[n0 + cnt] : n_rows) - rb;
+    const size_t es = esize();
+    auto V = [&](void *base) { return (void *)((char *)base + es * n * n0); };  // node n0's vector
+    const long long ps0 = (long long)part_stride * n0;
     int k = 0;
     if (ax == AX_OFF) {
-        k += project(g, X, true, st);
+        k += project(g, X, true, st, nullptr, 0, 0, false, n0, cnt);
     } else {
-        if (ax == AX_REFRESH) k += project(g, X, false, st, AX, g.n_det, 0);
-        launch_resid_from_ax(prec, D, AX, S, n_rows, g.n_det, sp, st);
+        if (ax == AX_REFRESH) k += project(g, X, false, st, AX, g.n_det, 0, false, n0, cnt);
+        launch_resid_from_ax(prec, (char *)D + es * (size_t)rb * g.n_det, (char *)AX + es * (size_t)rb * g.n_det,
+                             (char *)S + es * (size_t)rb * sp, nr, g.n_det, sp, st);
         k++;
     }
-    k += backproject(g, EPI_RESID, R, P, X, st);
+    k += backproject(g, EPI_RESID, R, P, X, st, nullptr, n0, cnt);
     for (int it = 0; it < e1; it++) {
         // ||p||^2 of this step's direction: scal[S_PP] for p0 = r0, then the previous vector
         // pass's per-CTA partials
         const int npp = it == 0 ? 0 : vec_blocks(n);
-        k += project(g, P, false, st, nullptr, 0, 0, true);
-        launch_cg_alpha(L, scal, cgs, fp_reduce_blocks(prec, g.n_det), nang, cgp, npp, cnode, part_stride, st);
+        k += project(g, P, false, st, nullptr, 0, 0, true, n0, cnt);
+        launch_cg_alpha(cnt, scal + (long long)S_NSLOT * n0, cgs + ps0, fp_reduce_blocks(prec, g.n_det), nang + n0,
+                        cgp + ps0, npp, cnode + n0, part_stride, st);
         k++;
-        if (it + 1 < e1) k += backproject(g, EPI_CGR, R, nullptr, P, st, R);
-        const AxUpdate au{ax == AX_OFF ? nullptr : AX, S, row0, nang, g.n_det, sp};
-        launch_cg_update_px(prec, X, P, R, n, L, scal, partial, part_stride, counter, it + 1 < e1, cgp, au, st);
+        if (it + 1 < e1) k += backproject(g, EPI_CGR, R, nullptr, P, st, R, n0, cnt);
+        const AxUpdate au{ax == AX_OFF ? nullptr : AX, S, row0 + n0, nang + n0, g.n_det, sp};
+        launch_cg_update_px(prec, V(X), V(P), V(R), n, cnt, scal + (long long)S_NSLOT * n0, partial + ps0,
+                            part_stride, counter + n0, it + 1 < e1, cgp + ps0, au, st);
         k++;
     }
     return k;

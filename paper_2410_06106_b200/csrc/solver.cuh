@@ -58,16 +58,18 @@ struct Inner {
     // launches; return the number of kernels launched
     // ax: AX_OFF = residual projection of X every solve; AX_REFRESH = project X into AX first;
     // AX_CACHED = residual d - AX (AX = A x maintained by the CG steps: A x += alpha A p)
-    int cg(const DevGeom &g, int e1, cudaStream_t st, int ax = 0);
+    // n0, cnt: only the node group [n0, n0 + cnt) (cnt < 0: to the last node); every launch of a
+    // group touches only that group's vectors, tables and ray rows (fp32, persistent forward kernel)
+    int cg(const DevGeom &g, int e1, cudaStream_t st, int ax = 0, int n0 = 0, int cnt = -1);
     int gd(const DevGeom &g, int e1, cudaStream_t st);
     int norm2(cudaStream_t st);
     // S = (D -) A img (2 tile launches + 1 reduction); out/out_stride/out_off override S;
     // cg: the reduction also sets alpha of a CG step from ||S||^2 (see cg())
     int project(const DevGeom &g, const void *img, bool resid, cudaStream_t st, void *out = nullptr,
-                int out_stride = 0, int out_off = 0, bool cg = false);
+                int out_stride = 0, int out_off = 0, bool cg = false, int n0 = 0, int cnt = -1);
     // rin: the residual r read by EPI_CGR (out may alias it)
     int backproject(const DevGeom &g, int epi, void *out, void *out2, const void *vin, cudaStream_t st,
-                    const void *rin = nullptr);
+                    const void *rin = nullptr, int n0 = 0, int cnt = -1);
 };
 
 }  // namespace tq

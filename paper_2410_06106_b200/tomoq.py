@@ -66,7 +66,7 @@ class Stats(C.Structure):
                 ("payload_bytes_logical", C.c_int64), ("nccl_bytes_sent", C.c_int64),
                 ("nccl_bytes_recv", C.c_int64), ("kernel_launches", C.c_int64),
                 ("ms_last_run", C.c_double), ("iters_last_run", C.c_int64), ("rel_change_last", C.c_double),
-                ("phase_valid", C.c_int32), ("pad_", C.c_int32), ("phase_ms", C.c_double * 4)]
+                ("phase_valid", C.c_int32), ("node_groups", C.c_int32), ("phase_ms", C.c_double * 4)]
 
 
 _lib = None
@@ -313,7 +313,7 @@ class Context:
     def stats(self) -> dict:
         s = Stats()
         self._c(lib().tq_get_stats(self.h, C.byref(s)))
-        out = {f: getattr(s, f) for f, _ in Stats._fields_ if f != "pad_"}
+        out = {f: getattr(s, f) for f, _ in Stats._fields_}
         out["phase_ms"] = list(s.phase_ms)
         return out
 

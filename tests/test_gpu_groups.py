@@ -1,0 +1,68 @@
+"""Node groups (DESIGN.md 6.1 "two node groups"): the graph rule's fp32 CG + K-means stages run
+as two concurrent launch chains over nodes [0, L/2) and [L/2, L).  Every kernel's result for a
+node depends only on that node's inputs and per-node fixed-order reductions, so the grouped
+iteration must equal the single-chain one (TQ_GROUPS=1) bit for bit: x_i, alpha_i, the decoded
+x_hat_i and the K-means labels of every node (Alg. 4)."""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+from paper_2410_06106_b200 import configs as C
+from tests.cases import export_all, gpu_context
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(cfg, inp, iters, groups, monkeypatch, keep_labels=False):
+    monkeypatch.setenv("TQ_GROUPS", str(groups))
+    ctx = gpu_context(cfg, inp, keep_labels=keep_labels)
+    ctx.run(iters)
+    st = ctx.stats()
+    X, Lm, XH = export_all(ctx, cfg)
+    labels = [ctx.labels(0, m, cfg.N * cfg.N) for m in range(cfg.nodes)] if keep_labels else None
+    ctx.close()
+    return st, X, Lm, XH, labels
+
+
+def _same(a, b):
+    for u, v in zip(a[1:4], b[1:4]):
+        np.testing.assert_array_equal(u, v)
+
+
+@pytest.mark.parametrize("name,cfg,iters", [
+    ("C1 unquantized, 4 nodes", C.C1(), 6),
+    ("C2 K-means 16, 8 nodes", C.C2(), 4),
+    ("C2 on 7 nodes (groups 3 + 4)", replace(C.C2(), nodes=7, graph="ring"), 4),
+    ("C4_G1 bench workload", C.C4(1), 3),
+])
+def test_groups_bitwise_equal_to_one_chain(name, cfg, iters, monkeypatch):
+    inp = C.make_inputs(cfg, with_truth=False)
+    one = _run(cfg, inp, iters, 1, monkeypatch)
+    two = _run(cfg, inp, iters, 2, monkeypatch)
+    assert one[0]["node_groups"] == 1 and two[0]["node_groups"] == 2, name
+    _same(one, two)
+
+
+def test_groups_labels_and_kept_ax_refresh(monkeypatch):
+    """K-means labels, and enough iterations to pass the kept A x refresh (TQ_AX_MAXAGE)."""
+    monkeypatch.setenv("TQ_AX_MAXAGE", "3")
+    cfg = C.C2()
+    inp = C.make_inputs(cfg, with_truth=False)
+    one = _run(cfg, inp, 8, 1, monkeypatch, keep_labels=True)
+    two = _run(cfg, inp, 8, 2, monkeypatch, keep_labels=True)
+    assert two[0]["node_groups"] == 2
+    _same(one, two)
+    for a, b in zip(one[4], two[4]):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_groups_not_used_where_not_applicable(monkeypatch):
+    """DCT payloads, fp64 and GD keep the single chain (and say so in tq_stats)."""
+    monkeypatch.setenv("TQ_GROUPS", "2")
+    for cfg, prec in ((C.C3(), 0), (C.C2(), 1), (replace(C.C2(), inner=C.INNER_GD, e1=10), 0)):
+        inp = C.make_inputs(cfg, with_truth=False)
+        ctx = gpu_context(cfg, inp, precision=prec)
+        ctx.run(1)
+        assert ctx.stats()["node_groups"] == 1, (cfg.name, prec, cfg.inner)
+        ctx.close()
