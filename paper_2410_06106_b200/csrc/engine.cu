@@ -166,9 +166,11 @@ void Ctx::create(const tq_geometry &g, const tq_graph &gr, int n_slices, int ran
     TQ_CHECK_CUDA(cudaSetDevice(device));
     TQ_CHECK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     TQ_CHECK_CUDA(cudaStreamCreateWithFlags(&up_stream, cudaStreamNonBlocking));
-    TQ_CHECK_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
     TQ_CHECK_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    TQ_CHECK_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    for (int g = 1; g < MAXG; g++) {
+        TQ_CHECK_CUDA(cudaStreamCreateWithFlags(&sg[g], cudaStreamNonBlocking));
+        TQ_CHECK_CUDA(cudaEventCreateWithFlags(&ev_join[g], cudaEventDisableTiming));
+    }
     TQ_CHECK_CUDA(cudaEventCreate(&ev0));
     TQ_CHECK_CUDA(cudaEventCreate(&ev1));
     TQ_CHECK_CUDA(cudaEventCreateWithFlags(&run_done, cudaEventDisableTiming));
@@ -214,8 +216,7 @@ void Ctx::free_exchange() {
     for (void *p : owned) cudaFree(p);
     owned.clear();
     kmw.release();
-    kmw_g[0].release();
-    kmw_g[1].release();
+    for (auto &w : kmw_g) w.release();
     ngroups = 1;
     dctw.release();
     jenc.release();
@@ -288,11 +289,14 @@ void Ctx::destroy() {
     stream = nullptr;
     if (up_stream) cudaStreamDestroy(up_stream);
     up_stream = nullptr;
-    if (s2) cudaStreamDestroy(s2);
-    s2 = nullptr;
+    for (int g = 1; g < MAXG; g++) {
+        if (sg[g]) cudaStreamDestroy(sg[g]);
+        if (ev_join[g]) cudaEventDestroy(ev_join[g]);
+        sg[g] = nullptr;
+        ev_join[g] = nullptr;
+    }
     if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
-    ev_fork = ev_join = nullptr;
+    ev_fork = nullptr;
 }
 
 void Ctx::set_params(const tq_params &p) {
@@ -612,8 +616,8 @@ void Ctx::setup_exchange() {
     // rule's fp32 path whose only encode batch is K-means over exactly the local nodes, in order
     {
         const char *env = getenv("TQ_GROUPS");
-        const int want = env ? atoi(env) : 2;
-        bool ok = want >= 2 && L >= 2 && prec == 0 && rule == TQ_RULE_GRAPH && geo.N % 4 == 0 && enc[2].P == 0;
+        const int want = std::min(std::min(env ? atoi(env) : 2, (int)MAXG), L);
+        bool ok = want >= 2 && prec == 0 && rule == TQ_RULE_GRAPH && geo.N % 4 == 0 && enc[2].P == 0;
         if (ok && enc[1].P) {
             ok = enc[1].P == L && !enc[1].need_conv;
             for (int b = 0; ok && b < enc[1].P; b++) {
@@ -622,11 +626,12 @@ void Ctx::setup_exchange() {
             }
         }
         if (ok) {
-            ngroups = 2;
-            grp_n0[0] = 0; grp_cnt[0] = L / 2;
-            grp_n0[1] = L / 2; grp_cnt[1] = L - L / 2;
-            if (enc[1].P)
-                for (int g = 0; g < 2; g++) kmw_g[g].alloc(grp_cnt[g], q.k, payload_len);
+            ngroups = want;
+            for (int g = 0; g < want; g++) {
+                grp_n0[g] = g * L / want;
+                grp_cnt[g] = (g + 1) * L / want - grp_n0[g];
+                if (enc[1].P) kmw_g[g].alloc(grp_cnt[g], q.k, payload_len);
+            }
         }
     }
     // ---- consensus tables
@@ -777,25 +782,27 @@ void Ctx::ax_before(int iters, cudaStream_t s) {
 }
 
 bool Ctx::grouped() const {
-    return ngroups == 2 && rule == TQ_RULE_GRAPH && prm.inner == TQ_INNER_CG && prec == 0;
+    return ngroups >= 2 && rule == TQ_RULE_GRAPH && prm.inner == TQ_INNER_CG && prec == 0;
 }
 
 int Ctx::stage01_grouped(cudaStream_t s) {
     TQ_CHECK_CUDA(cudaEventRecord(ev_fork, s));
-    TQ_CHECK_CUDA(cudaStreamWaitEvent(s2, ev_fork, 0));
+    for (int g = 1; g < ngroups; g++) TQ_CHECK_CUDA(cudaStreamWaitEvent(sg[g], ev_fork, 0));
     int k = 0;
-    for (int g = 0; g < 2; g++) {
-        cudaStream_t sg = g ? s2 : s;
-        k += in.cg(geo, prm.e1, sg, use_ax() ? AX_CACHED : AX_OFF, grp_n0[g], grp_cnt[g]);
+    for (int g = 0; g < ngroups; g++) {
+        cudaStream_t st = g ? sg[g] : s;
+        k += in.cg(geo, prm.e1, st, use_ax() ? AX_CACHED : AX_OFF, grp_n0[g], grp_cnt[g]);
         Batch &E = enc[TQ_Q_KMEANS];
         if (E.P) {
             const int b0 = grp_n0[g];
             k += kmeans_encode(E.vin + b0, kmw_g[g], q.lloyd_iters, E.pay + b0, E.labels ? E.labels + b0 : nullptr,
-                               sg, E.dec_out ? E.dec_out + b0 : nullptr, prec);
+                               st, E.dec_out ? E.dec_out + b0 : nullptr, prec);
         }
     }
-    TQ_CHECK_CUDA(cudaEventRecord(ev_join, s2));
-    TQ_CHECK_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+    for (int g = 1; g < ngroups; g++) {
+        TQ_CHECK_CUDA(cudaEventRecord(ev_join[g], sg[g]));
+        TQ_CHECK_CUDA(cudaStreamWaitEvent(s, ev_join[g], 0));
+    }
     return k;
 }
 
@@ -1027,7 +1034,7 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
     st.iters_last_run = done;
     st.kernel_launches = (long long)done * per_iter + (stop ? done : 0);
     st.phase_valid = 0;
-    st.node_groups = (!profiling && grouped()) ? 2 : 1;
+    st.node_groups = (!profiling && grouped()) ? ngroups : 1;
     pending = true;
     pending_iters = done;
     prof_iters = profiling ? done : 0;

@@ -183,15 +183,16 @@ struct Ctx {
     bool segmented() const { return rule != TQ_RULE_GRAPH; }
     int stage(int id, cudaStream_t s);  // 0: inner solves (+ Alg. 3 / partial sums), 1: x + encode,
                                         // 2: decode + dual (phase_b)
-    // Node groups (DESIGN.md 6.1 "two node groups"): stages 0 + 1 of the graph rule's fp32 CG path
-    // captured as two independent chains (nodes [0, L/2) on the iteration's stream, [L/2, L) on
-    // s2), joined before the exchange / dual, so one group's kernel tails, CG scalar kernels and
-    // Lloyd steps overlap the other group's work.  Per-node arithmetic is unchanged.
+    // Node groups (DESIGN.md 6.1 "node groups"): stages 0 + 1 of the graph rule's fp32 CG path
+    // captured as G independent chains over contiguous node ranges (group 0 on the iteration's
+    // stream, group g on sg[g]), joined before the exchange / dual, so one group's kernel tails,
+    // CG scalar kernels and Lloyd steps overlap the others' work.  Per-node arithmetic is unchanged.
+    static constexpr int MAXG = 4;
     int ngroups = 1;
-    int grp_n0[2] = {0, 0}, grp_cnt[2] = {0, 0};
-    KmeansWork kmw_g[2];
-    cudaStream_t s2 = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int grp_n0[MAXG] = {}, grp_cnt[MAXG] = {};
+    KmeansWork kmw_g[MAXG];
+    cudaStream_t sg[MAXG] = {};       // sg[0] unused: group 0 runs on the iteration's stream
+    cudaEvent_t ev_fork = nullptr, ev_join[MAXG] = {};
     bool grouped() const;
     int stage01_grouped(cudaStream_t s);
     int stages(const std::vector<int> &ids, cudaStream_t s);  // stage() of each id, 0 + 1 grouped

@@ -1,5 +1,5 @@
-"""Node groups (DESIGN.md 6.1 "two node groups"): the graph rule's fp32 CG + K-means stages run
-as two concurrent launch chains over nodes [0, L/2) and [L/2, L).  Every kernel's result for a
+"""Node groups (DESIGN.md 6.1 "node groups"): the graph rule's fp32 CG + K-means stages run as
+concurrent launch chains over contiguous node ranges (default two: [0, L/2) and [L/2, L)).  Every kernel's result for a
 node depends only on that node's inputs and per-node fixed-order reductions, so the grouped
 iteration must equal the single-chain one (TQ_GROUPS=1) bit for bit: x_i, alpha_i, the decoded
 x_hat_i and the K-means labels of every node (Alg. 4)."""
@@ -42,6 +42,17 @@ def test_groups_bitwise_equal_to_one_chain(name, cfg, iters, monkeypatch):
     two = _run(cfg, inp, iters, 2, monkeypatch)
     assert one[0]["node_groups"] == 1 and two[0]["node_groups"] == 2, name
     _same(one, two)
+
+
+@pytest.mark.parametrize("groups", [3, 4])
+def test_more_groups_bitwise_equal(groups, monkeypatch):
+    """Uneven contiguous ranges: 7 nodes as 2 + 2 + 3 / 1 + 2 + 2 + 2."""
+    cfg = replace(C.C2(), nodes=7, graph="ring")
+    inp = C.make_inputs(cfg, with_truth=False)
+    one = _run(cfg, inp, 3, 1, monkeypatch)
+    many = _run(cfg, inp, 3, groups, monkeypatch)
+    assert many[0]["node_groups"] == groups
+    _same(one, many)
 
 
 def test_groups_labels_and_kept_ax_refresh(monkeypatch):
