@@ -127,8 +127,8 @@ typedef struct {
     double rel_change_last;        /* r_k of the last iteration (stop_tol > 0), else -1 */
     int32_t phase_valid;           /* 1: phase_ms holds the last run's phases (tq_set_profiling) */
     int32_t node_groups;           /* concurrent node groups of the last run's iteration graph: 1, or
-                                      TQ_GROUPS (default 2, at most 4) where they apply (DESIGN.md
-                                      6.1 "node groups") */
+                                      TQ_GROUPS / its default where they apply (see TQ_GROUPS below;
+                                      DESIGN.md 6.1 "node groups") */
     double phase_ms[4];            /* device ms of the last run, summed over its iterations:
                                       [0] inner solves (A3: the E1 CG / GD steps of every local
                                       node; plus Alg. 3 / the consensus partial sums and their
@@ -228,10 +228,10 @@ tq_status tq_get_stats(const tq_ctx *ctx, tq_stats *out);
  * recomputes it by a forward projection when stale and at least every TQ_AX_MAXAGE iterations;
  * 0 projects x in every solve (the oracle's order of operations).
  * Environment knob read when the exchange state is built (first run after tq_create /
- * tq_set_quantizer): TQ_GROUPS (default 2, at most 4; 1 disables) -- with the graph rule, fp32,
- * and K-means payloads of exactly the local nodes (or none), the inner solves and encodes of an
- * iteration run as that many concurrent launch chains over contiguous node ranges, joined before
- * the exchange.  Results are bitwise those of one chain (per-node arithmetic is unchanged);
+ * tq_set_quantizer): TQ_GROUPS (at most 8; 1 disables; default one group per local node, up to
+ * 8, for N >= 512, else 1) -- with the graph rule, fp32, and K-means payloads of exactly the local
+ * nodes (or none), the inner solves and encodes of an iteration run as that many concurrent launch
+ * chains over contiguous node ranges, joined before the exchange.  Results are bitwise those of one chain (per-node arithmetic is unchanged);
  * tq_stats.node_groups reports what the last run used. */
 
 /* Debug aid (no compute-sanitizer on the GPU pool): with TQ_GUARD=1 in the environment of the

@@ -616,7 +616,10 @@ void Ctx::setup_exchange() {
     // rule's fp32 path whose only encode batch is K-means over exactly the local nodes, in order
     {
         const char *env = getenv("TQ_GROUPS");
-        const int want = std::min(std::min(env ? atoi(env) : 2, (int)MAXG), L);
+        // default: one group per node (up to MAXG) for images of 512^2 and more; below that the
+        // kernels are short and the extra launches cost more than the overlap gains (C1, C2)
+        const int dflt = geo.N >= 512 ? (int)MAXG : 1;
+        const int want = std::min(std::min(env ? atoi(env) : dflt, (int)MAXG), L);
         bool ok = want >= 2 && prec == 0 && rule == TQ_RULE_GRAPH && geo.N % 4 == 0 && enc[2].P == 0;
         if (ok && enc[1].P) {
             ok = enc[1].P == L && !enc[1].need_conv;

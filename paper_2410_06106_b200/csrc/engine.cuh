@@ -184,10 +184,11 @@ struct Ctx {
     int stage(int id, cudaStream_t s);  // 0: inner solves (+ Alg. 3 / partial sums), 1: x + encode,
                                         // 2: decode + dual (phase_b)
     // Node groups (DESIGN.md 6.1 "node groups"): stages 0 + 1 of the graph rule's fp32 CG path
-    // captured as G independent chains over contiguous node ranges (group 0 on the iteration's
+    // captured as G independent chains over contiguous node ranges (TQ_GROUPS; by default one per
+    // node, up to MAXG, for N >= 512; group 0 on the iteration's
     // stream, group g on sg[g]), joined before the exchange / dual, so one group's kernel tails,
     // CG scalar kernels and Lloyd steps overlap the others' work.  Per-node arithmetic is unchanged.
-    static constexpr int MAXG = 4;
+    static constexpr int MAXG = 8;
     int ngroups = 1;
     int grp_n0[MAXG] = {}, grp_cnt[MAXG] = {};
     KmeansWork kmw_g[MAXG];

@@ -1,6 +1,8 @@
 // projector.cu -- see projector.cuh.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "projector.cuh"
 
 namespace tq {
@@ -1226,6 +1228,8 @@ size_t fp_smem(int o) { return sizeof(T) * FP_TH * (o == 0 ? FP_PITCH_Y : FP_PIT
 size_t fp2_smem() { return sizeof(float2) * FP_TH * FP2_PITCH; }
 size_t fpp_smem() { return 1024 + sizeof(float2) * FP_TH * FP2_PITCH + sizeof(float) * FPP_RAW + sizeof(FpRec) * 2 * FPP_MAXA + 2 * sizeof(FpUnitTab); }
 int g_fpp_grid = 0;  // persistent grid: SMs x resident CTAs (projector_setup)
+int g_fpp_sms = 0, g_fpp_per = 0;
+bool g_fpp_grid_set = false;  // TQ_FPP_GRID given: every launch uses it
 template <typename T, int EPI>
 size_t bp_smem() {
     constexpr int NEP = (EPI == EPI_CGQ) ? 1 : ((EPI == EPI_RESID || EPI == EPI_GD || EPI == EPI_CGR) ? 2 : 0);
@@ -1249,6 +1253,10 @@ void set_all_smem() {
         TQ_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         TQ_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fp_persist_f32<false>, FP_THREADS, fpp_smem()));
         g_fpp_grid = sms * std::max(1, per);
+        g_fpp_sms = sms;
+        g_fpp_per = std::max(1, per);
+        if (const char *e = getenv("TQ_FPP_GRID"))  // A/B timing knob: persistent grid size
+            if (atoi(e) > 0) { g_fpp_grid = atoi(e); g_fpp_grid_set = true; }
     }
     set_smem(bp_tile_kernel<T, EPI_PLAIN>, bp_smem<T, EPI_PLAIN>());
     set_smem(bp_tile_kernel<T, EPI_CGQ>, bp_smem<T, EPI_CGQ>());
@@ -1306,8 +1314,17 @@ void fp_dispatch(const FpArgs<T> &A, int L, cudaStream_t st) {
             const int nunits = 2 * L * A.nt_line * A.nt_cross;
             CUtensorMap tr, tc;
             make_image_maps(A.img, A.N, L, &tr, &tc);
-            if (A.siddon) launch_pdl(fp_persist_f32<true>, std::min(nunits, g_fpp_grid), FP_THREADS, fpp_smem(), st, B, nunits, tr, tc);
-            else launch_pdl(fp_persist_f32<false>, std::min(nunits, g_fpp_grid), FP_THREADS, fpp_smem(), st, B, nunits, tr, tc);
+            // a node group's launch (L < L_all) shares the SMs with the other groups' concurrent
+            // chains: SMs x ceil(2 x resident / groups) CTAs (A.L_all / L groups; measured best at
+            // 2, 4 and 8 groups on C4_G1, DESIGN.md 6.1 "node groups")
+            int grid = g_fpp_grid;
+            if (L < A.L_all && g_fpp_per > 0 && !g_fpp_grid_set) {
+                const int groups = std::max(1, (A.L_all + L - 1) / L);
+                grid = g_fpp_sms * std::max(1, (2 * g_fpp_per + groups - 1) / groups);
+            }
+            grid = std::min(nunits, grid);
+            if (A.siddon) launch_pdl(fp_persist_f32<true>, grid, FP_THREADS, fpp_smem(), st, B, nunits, tr, tc);
+            else launch_pdl(fp_persist_f32<false>, grid, FP_THREADS, fpp_smem(), st, B, nunits, tr, tc);
         } else {
             fp_tile_f32<0><<<grid, FP_THREADS, fp2_smem(), st>>>(B);
             fp_tile_f32<1><<<grid, FP_THREADS, fp2_smem(), st>>>(B);

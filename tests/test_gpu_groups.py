@@ -1,5 +1,5 @@
 """Node groups (DESIGN.md 6.1 "node groups"): the graph rule's fp32 CG + K-means stages run as
-concurrent launch chains over contiguous node ranges (default two: [0, L/2) and [L/2, L)).  Every kernel's result for a
+concurrent launch chains over contiguous node ranges (default for N >= 512: one per node, up to 8).  Every kernel's result for a
 node depends only on that node's inputs and per-node fixed-order reductions, so the grouped
 iteration must equal the single-chain one (TQ_GROUPS=1) bit for bit: x_i, alpha_i, the decoded
 x_hat_i and the K-means labels of every node (Alg. 4)."""
@@ -48,6 +48,27 @@ def test_groups_bitwise_equal_to_one_chain(name, cfg, iters, monkeypatch):
 def test_more_groups_bitwise_equal(groups, monkeypatch):
     """Uneven contiguous ranges: 7 nodes as 2 + 2 + 3 / 1 + 2 + 2 + 2."""
     cfg = replace(C.C2(), nodes=7, graph="ring")
+    inp = C.make_inputs(cfg, with_truth=False)
+    one = _run(cfg, inp, 3, 1, monkeypatch)
+    many = _run(cfg, inp, 3, groups, monkeypatch)
+    assert many[0]["node_groups"] == groups
+    _same(one, many)
+
+
+def test_default_groups(monkeypatch):
+    """Default: one group per node (up to 8) for N >= 512, one chain below."""
+    monkeypatch.delenv("TQ_GROUPS", raising=False)
+    for cfg, want in ((C.C4(1), 8), (C.C2(), 1)):
+        inp = C.make_inputs(cfg, with_truth=False)
+        ctx = gpu_context(cfg, inp)
+        ctx.run(1)
+        assert ctx.stats()["node_groups"] == want, cfg.name
+        ctx.close()
+
+
+@pytest.mark.parametrize("groups", [8])
+def test_one_group_per_node_bitwise_c4(groups, monkeypatch):
+    cfg = C.C4(1)
     inp = C.make_inputs(cfg, with_truth=False)
     one = _run(cfg, inp, 3, 1, monkeypatch)
     many = _run(cfg, inp, 3, groups, monkeypatch)
