@@ -366,7 +366,13 @@ __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPt
     long long *spre = tpre + T + 1;                                   // [NS] prefix at super-chunk starts
     uint32_t *shead = reinterpret_cast<uint32_t *>(spre + NS);        // [NS] first key of each super-chunk
     __shared__ float cen[256], thr[256];
-    __shared__ long long Cs[2][256], Ss[2][256], total_s;
+    // (C_k, S_k) of the step, double-buffered: each threshold's owner warp writes its pair into
+    // every CTA of the cluster with st.async, which also counts its 16 bytes on that CTA's
+    // mbarrier xbar[buf] -- a step's exchange completes on the receiver's barrier, without a
+    // cluster-wide barrier (and its release fence) per Lloyd step
+    __shared__ __align__(16) longlong2 CS[2][256];
+    __shared__ __align__(8) unsigned long long xbar[2];
+    __shared__ long long total_s;
     __shared__ uint32_t lhist[LCT / 32 * 256];  // per-warp low-byte histograms (quantile init)
     const int rank = (int)cluster.block_rank();
     const int b = blockIdx.x / LCL, K = w.K;
@@ -417,7 +423,14 @@ __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPt
         }
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    cluster.sync();  // every CTA of the cluster started (DSMEM targets exist) and staged
+    const uint32_t xbar_s = (uint32_t)__cvta_generic_to_shared(&xbar[0]);
+    const uint32_t cs_s = (uint32_t)__cvta_generic_to_shared(&CS[0][0]);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(xbar_s));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(xbar_s + 8u));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster.sync();  // every CTA of the cluster started (DSMEM targets and barriers exist) and staged
     // The keys are ordered by group (top 24 bits), unordered inside a group.  Keys of the
     // super-chunks [c_lo, c_hi] cover group g entirely: c_hi = the last super-chunk whose head
     // is in a group <= g, c_lo = the last one whose head is in a group < g (0 if none); every
@@ -483,8 +496,12 @@ __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPt
         __syncwarp();
     }
     cluster.sync();  // the initial centres delivered everywhere
+    unsigned xphase = 0u;  // bit b: parity of xbar[b]'s current phase
     for (int it = 0; it < iters; it++) {
         const int buf = it & 1;
+        if (threadIdx.x == 0)  // this step's pairs: one per threshold
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                         ::"r"(xbar_s + 8u * buf), "r"(16u * (unsigned)(K - 1)) : "memory");
         for (int k = threadIdx.x; k + 1 < K; k += LCT) thr[k] = (float)(((double)cen[k] + (double)cen[k + 1]) * 0.5);
         __syncthreads();
         const int kk = rank + LCL * warp;  // this warp's threshold (at most one: K <= 256 < LCL * 8 * 4)
@@ -512,15 +529,26 @@ __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPt
             const int c = any ? (int)(beg / S) : -1;
             const long long cv = c >= 0 ? beg + cnt : 0;
             const long long sv = c >= 0 ? spre[c] + sm : 0;
-            if (lane < LCL) {  // lane r stores into CTA r's shared memory
-                *cluster.map_shared_rank(&Cs[buf][k0], lane) = cv;
-                *cluster.map_shared_rank(&Ss[buf][k0], lane) = sv;
+            if (lane < LCL) {  // lane r stores into CTA r's shared memory and counts on its barrier
+                uint32_t dst, bar;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(cs_s + 16u * (unsigned)(buf * 256 + k0)), "r"(lane));
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(bar) : "r"(xbar_s + 8u * buf), "r"(lane));
+                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.s64 [%0], {%1, %2}, [%3];"
+                             ::"r"(dst), "l"(cv), "l"(sv), "r"(bar) : "memory");
             }
         }
-        cluster.sync();  // all (C_k, S_k) of this iteration delivered everywhere
+        {  // every pair of this step has landed in this CTA's CS[buf]
+            const unsigned par = (xphase >> buf) & 1u;
+            unsigned ok = 0;
+            do {
+                asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+                             " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(xbar_s + 8u * buf), "r"(par) : "memory");
+            } while (!ok);
+            xphase ^= 1u << buf;
+        }
         for (int k = threadIdx.x; k < K; k += LCT) {
-            const long long c1 = k + 1 < K ? Cs[buf][k] : nv, c0 = k ? Cs[buf][k - 1] : 0;
-            const long long s1 = k + 1 < K ? Ss[buf][k] : total_s, s0 = k ? Ss[buf][k - 1] : 0;
+            const long long c1 = k + 1 < K ? CS[buf][k].x : nv, c0 = k ? CS[buf][k - 1].x : 0;
+            const long long s1 = k + 1 < K ? CS[buf][k].y : total_s, s0 = k ? CS[buf][k - 1].y : 0;
             if (c1 > c0) cen[k] = (float)(((double)(s1 - s0) / scale) / (double)(c1 - c0));
         }
         __syncthreads();
