@@ -274,7 +274,8 @@ def bench_config(cfg, world):
     return {"workload": cfg.name, "N": cfg.N, "nodes": cfg.nodes, "nodes_per_gpu": cfg.nodes // world,
             "n_angles": cfg.n_angles, "n_det": cfg.n_det, "graph": "random 4-regular",
             "inner": "CG5", "quantizer": "kmeans K=64 (10 Lloyd)", "rule": "graph",
-            "parallelism": f"nodes interleaved over {world} GPU(s), NCCL send/recv of payloads",
+            "parallelism": f"nodes interleaved over {world} GPU(s), NCCL send/recv of payloads; per GPU the "
+                           f"nodes' inner solves + encodes as concurrent launch chains (node groups, DESIGN.md 6.1)",
             "l2": "no flush: per-GPU working set ~0.25 GB > 126 MB L2"}
 
 
@@ -520,6 +521,7 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(sino_host.numel() * 4),
                     "d2h_bytes_per_step": int(cfg.N * cfg.N * 4), "ms_per_step": max(e2e_ms, e2e_wall) / args.steps},
             "gpu_launches": int(st["kernel_launches"]),
+            "node_groups": int(st["node_groups"]),
             "clocks": clk,
             "payload_bytes_per_step": st["payload_bytes_logical"],
             "nccl_bytes_per_step_rank0": st["nccl_bytes_sent"],
