@@ -217,6 +217,7 @@ void Ctx::free_exchange() {
     owned.clear();
     kmw.release();
     for (auto &w : kmw_g) w.release();
+    for (auto &w : dctw_g) w.release();
     ngroups = 1;
     dctw.release();
     jenc.release();
@@ -612,20 +613,25 @@ void Ctx::setup_exchange() {
             D.out = (void **)upload(out.data(), sizeof(void *) * D.P);
         }
     }
-    // ---- node groups (TQ_GROUPS, default 2; 1 = one launch sequence over all nodes): the graph
-    // rule's fp32 path whose only encode batch is K-means over exactly the local nodes, in order
+    // ---- node groups (TQ_GROUPS; 1 = one launch sequence over all nodes): the graph rule's fp32
+    // path; each encode batch (K-means, plain DCT) must hold local payloads in local-node order,
+    // so a group's payloads are one contiguous subrange of each batch
     {
         const char *env = getenv("TQ_GROUPS");
         // default: one group per node (up to MAXG) for images of 512^2 and more; below that the
         // kernels are short and the extra launches cost more than the overlap gains (C1, C2)
         const int dflt = geo.N >= 512 ? (int)MAXG : 1;
         const int want = std::min(std::min(env ? atoi(env) : dflt, (int)MAXG), L);
-        bool ok = want >= 2 && prec == 0 && rule == TQ_RULE_GRAPH && geo.N % 4 == 0 && enc[2].P == 0;
-        if (ok && enc[1].P) {
-            ok = enc[1].P == L && !enc[1].need_conv;
-            for (int b = 0; ok && b < enc[1].P; b++) {
-                const Pay &p = pays[enc[1].members[b]];
-                ok = local(p.slice, p.node) == b;
+        bool ok = want >= 2 && prec == 0 && rule == TQ_RULE_GRAPH && geo.N % 4 == 0 && q.jpeg_restart == 0;
+        std::vector<int> li_of[3];
+        for (int kd = 1; ok && kd <= 2; kd++) {
+            if (!enc[kd].P) continue;
+            ok = !enc[kd].need_conv;
+            for (int b = 0; ok && b < enc[kd].P; b++) {
+                const Pay &p = pays[enc[kd].members[b]];
+                const int li = local(p.slice, p.node);
+                ok = li >= 0 && (li_of[kd].empty() || li > li_of[kd].back());
+                li_of[kd].push_back(li);
             }
         }
         if (ok) {
@@ -633,7 +639,17 @@ void Ctx::setup_exchange() {
             for (int g = 0; g < want; g++) {
                 grp_n0[g] = g * L / want;
                 grp_cnt[g] = (g + 1) * L / want - grp_n0[g];
-                if (enc[1].P) kmw_g[g].alloc(grp_cnt[g], q.k, payload_len);
+                for (int kd = 1; kd <= 2; kd++) {
+                    int b0 = 0, bc = 0;
+                    for (int li : li_of[kd]) {
+                        if (li < grp_n0[g]) b0++;
+                        else if (li < grp_n0[g] + grp_cnt[g]) bc++;
+                    }
+                    grp_b0[kd][g] = b0;
+                    grp_bc[kd][g] = bc;
+                }
+                if (grp_bc[TQ_Q_KMEANS][g]) kmw_g[g].alloc(grp_bc[TQ_Q_KMEANS][g], q.k, payload_len);
+                if (grp_bc[TQ_Q_DCT][g]) dctw_g[g].alloc(grp_bc[TQ_Q_DCT][g], payload_len);
             }
         }
     }
@@ -795,11 +811,16 @@ int Ctx::stage01_grouped(cudaStream_t s) {
     for (int g = 0; g < ngroups; g++) {
         cudaStream_t st = g ? sg[g] : s;
         k += in.cg(geo, prm.e1, st, use_ax() ? AX_CACHED : AX_OFF, grp_n0[g], grp_cnt[g]);
-        Batch &E = enc[TQ_Q_KMEANS];
-        if (E.P) {
-            const int b0 = grp_n0[g];
+        if (grp_bc[TQ_Q_KMEANS][g]) {
+            Batch &E = enc[TQ_Q_KMEANS];
+            const int b0 = grp_b0[TQ_Q_KMEANS][g];
             k += kmeans_encode(E.vin + b0, kmw_g[g], q.lloyd_iters, E.pay + b0, E.labels ? E.labels + b0 : nullptr,
                                st, E.dec_out ? E.dec_out + b0 : nullptr, prec);
+        }
+        if (grp_bc[TQ_Q_DCT][g]) {
+            Batch &E = enc[TQ_Q_DCT];
+            const int b0 = grp_b0[TQ_Q_DCT][g];
+            k += dct_encode(E.vin + b0, grp_bc[TQ_Q_DCT][g], N, N, q.quality, dctw_g[g], E.pay + b0, st, nullptr);
         }
     }
     for (int g = 1; g < ngroups; g++) {
@@ -933,6 +954,7 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
         const cudaError_t e = cudaGraphInstantiate(&sg.exec, g, 0);
         cudaGraphDestroy(g);
         TQ_CHECK_CUDA(e);
+        TQ_CHECK_CUDA(cudaGraphUpload(sg.exec, s));  // the first launch does not pay the upload
         into.push_back(sg);
     };
     const bool red = rule == TQ_RULE_CONSENSUS && world > 1;
@@ -975,6 +997,7 @@ void Ctx::enqueue(int iters, cudaStream_t user) {
         const cudaError_t e = cudaGraphInstantiate(&seg2.exec, g, 0);
         cudaGraphDestroy(g);
         TQ_CHECK_CUDA(e);
+        TQ_CHECK_CUDA(cudaGraphUpload(seg2.exec, s));
         seg2.launches = c;
     }
     int per_iter = 0;

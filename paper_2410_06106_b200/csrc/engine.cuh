@@ -192,6 +192,8 @@ struct Ctx {
     int ngroups = 1;
     int grp_n0[MAXG] = {}, grp_cnt[MAXG] = {};
     KmeansWork kmw_g[MAXG];
+    DctWork dctw_g[MAXG];
+    int grp_b0[3][MAXG] = {}, grp_bc[3][MAXG] = {};  // [codec kind][group]: the group's subrange of enc[kind]
     cudaStream_t sg[MAXG] = {};       // sg[0] unused: group 0 runs on the iteration's stream
     cudaEvent_t ev_fork = nullptr, ev_join[MAXG] = {};
     bool grouped() const;

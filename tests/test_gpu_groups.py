@@ -89,10 +89,36 @@ def test_groups_labels_and_kept_ax_refresh(monkeypatch):
         np.testing.assert_array_equal(a, b)
 
 
+@pytest.mark.parametrize("name,cfg,groups", [
+    ("C3 DCT q50, 16 nodes torus", C.C3(), 8),
+    ("C3 DCT q50, 16 nodes torus, 3 groups", C.C3(), 3),
+    ("two C2 slices, K-means / DCT alternating", replace(C.C2(), quant=C.Q_ALT, quality=75, slices=2), 4),
+])
+def test_groups_dct_and_alternating_bitwise(name, cfg, groups, monkeypatch):
+    """Plain DCT payloads and slices alternating K-means / DCT (C5's codec mix): each group encodes
+    its contiguous subrange of each codec's batch."""
+    inp = C.make_inputs(cfg, with_truth=False)
+    one = _run_slices(cfg, inp, 3, 1, monkeypatch)
+    many = _run_slices(cfg, inp, 3, groups, monkeypatch)
+    assert one[0]["node_groups"] == 1 and many[0]["node_groups"] == groups, name
+    for a, b in zip(one[1], many[1]):
+        np.testing.assert_array_equal(a, b)
+
+
+def _run_slices(cfg, inp, iters, groups, monkeypatch):
+    monkeypatch.setenv("TQ_GROUPS", str(groups))
+    ctx = gpu_context(cfg, inp)
+    ctx.run(iters)
+    st = ctx.stats()
+    out = [np.concatenate(export_all(ctx, cfg, s)) for s in range(len(inp.sino))]
+    ctx.close()
+    return st, out
+
+
 def test_groups_not_used_where_not_applicable(monkeypatch):
-    """DCT payloads, fp64 and GD keep the single chain (and say so in tq_stats)."""
+    """JPEG entropy-coded DCT payloads, fp64 and GD keep the single chain (tq_stats says so)."""
     monkeypatch.setenv("TQ_GROUPS", "2")
-    for cfg, prec in ((C.C3(), 0), (C.C2(), 1), (replace(C.C2(), inner=C.INNER_GD, e1=10), 0)):
+    for cfg, prec in ((replace(C.C3(), jpeg_restart=4), 0), (C.C2(), 1), (replace(C.C2(), inner=C.INNER_GD, e1=10), 0)):
         inp = C.make_inputs(cfg, with_truth=False)
         ctx = gpu_context(cfg, inp, precision=prec)
         ctx.run(1)
