@@ -359,6 +359,7 @@ __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPt
     using Scan = cub::BlockScan<long long, LCT>;
     __shared__ typename Scan::TempStorage tmp;
     extern __shared__ __align__(16) unsigned char lsm[];
+    pdl_wait();  // the sorted keys, chunk sums and heads come from the previous kernels
     const int T = w.T;
     const int S = KCH << sh;
     const int NS = (int)(((long long)T * KTILE) >> (7 + sh));       // super-chunks (KCH == 2^7)
@@ -764,7 +765,7 @@ int kmeans_encode(const float *const *v, KmeansWork &ws, int lloyd, uint8_t *con
     }
     // three passes: B -> A -> B -> A, group-sorted keys in keysA
     launch_pdl(km_csum, tiles, KT, 0, st, w, lloyd_shift(ws.T));
-    km_lloyd<<<LCL * P, LCT, lloyd_smem(ws.T), st>>>(w, lloyd, lloyd_shift(ws.T));
+    launch_pdl(km_lloyd, LCL * P, LCT, lloyd_smem(ws.T), st, w, lloyd, lloyd_shift(ws.T));
     long long want = std::max(1LL, (148LL * 8 + P - 1) / P);
     long long need = (ws.nv + KT * 16 - 1) / (KT * 16);
     const dim3 grid((unsigned)std::max(1LL, std::min(want, need)), P);
