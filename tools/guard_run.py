@@ -83,6 +83,12 @@ def main(path):
     cfg.inner, cfg.e1 = C.INNER_GD, 3
     run("gd_fp64", cfg, precision=1)
     loopback("loop_c2", C.scaled(C.C2(), 128, 96))
+    # node groups (concurrent chains; the small images need TQ_GROUPS to enable them)
+    for nm, cfg, g in (("c2_groups", C.scaled(C.C2(), 128, 96), "4"), ("c3_groups", C.scaled(C.C3(), 64, 96), "8"),
+                       ("c5_groups", C.scaled(C.C5(slices=2), 64, 96), "4")):
+        os.environ["TQ_GROUPS"] = g
+        run(nm, cfg)
+    os.environ.pop("TQ_GROUPS", None)
     x = torch.rand(64, 64, device="cuda", generator=torch.Generator(device="cuda").manual_seed(3))
     s = tomoq.project(x, 90, 91)
     OUT["stateless_fp"] = s.cpu().numpy()
