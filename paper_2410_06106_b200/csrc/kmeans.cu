@@ -497,7 +497,6 @@ __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPt
         __syncwarp();
     }
     cluster.sync();  // the initial centres delivered everywhere
-    unsigned xphase = 0u;  // bit b: parity of xbar[b]'s current phase
     for (int it = 0; it < iters; it++) {
         const int buf = it & 1;
         if (threadIdx.x == 0)  // this step's pairs: one per threshold
@@ -538,14 +537,13 @@ __global__ void __cluster_dims__(LCL, 1, 1) __launch_bounds__(LCT) km_lloyd(KmPt
                              ::"r"(dst), "l"(cv), "l"(sv), "r"(bar) : "memory");
             }
         }
-        {  // every pair of this step has landed in this CTA's CS[buf]
-            const unsigned par = (xphase >> buf) & 1u;
+        {  // every pair of this step has landed in this CTA's CS[buf] (its (it / 2)-th phase)
+            const unsigned par = (unsigned)(it >> 1) & 1u;
             unsigned ok = 0;
             do {
                 asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
                              " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(xbar_s + 8u * buf), "r"(par) : "memory");
             } while (!ok);
-            xphase ^= 1u << buf;
         }
         for (int k = threadIdx.x; k < K; k += LCT) {
             const long long c1 = k + 1 < K ? CS[buf][k].x : nv, c0 = k ? CS[buf][k - 1].x : 0;
