@@ -229,9 +229,9 @@ tq_status tq_get_stats(const tq_ctx *ctx, tq_stats *out);
  * 0 projects x in every solve (the oracle's order of operations).
  * Environment knob read when the exchange state is built (first run after tq_create /
  * tq_set_quantizer): TQ_GROUPS (at most 8; 1 disables; default one group per local node, up to
- * 8, for N >= 512, else 1) -- with the graph rule, fp32, and K-means / plain DCT payloads (not JPEG
- * entropy-coded ones), the inner solves and encodes of an iteration run as that many concurrent
- * launch chains over contiguous node ranges, joined before the exchange.  Results are bitwise those of one chain (per-node arithmetic is unchanged);
+ * 8, for N >= 512, else 1) -- with the graph rule and fp32, the inner solves and encodes (K-means,
+ * DCT, JPEG-coded DCT) of an iteration run as that many concurrent launch chains over contiguous
+ * node ranges, joined before the exchange.  Results are bitwise those of one chain (per-node arithmetic is unchanged);
  * tq_stats.node_groups reports what the last run used. */
 
 /* Debug aid (no compute-sanitizer on the GPU pool): with TQ_GUARD=1 in the environment of the

@@ -218,6 +218,7 @@ void Ctx::free_exchange() {
     kmw.release();
     for (auto &w : kmw_g) w.release();
     for (auto &w : dctw_g) w.release();
+    for (auto &w : jenc_g) w.release();
     ngroups = 1;
     dctw.release();
     jenc.release();
@@ -622,7 +623,7 @@ void Ctx::setup_exchange() {
         // kernels are short and the extra launches cost more than the overlap gains (C1, C2)
         const int dflt = geo.N >= 512 ? (int)MAXG : 1;
         const int want = std::min(std::min(env ? atoi(env) : dflt, (int)MAXG), L);
-        bool ok = want >= 2 && prec == 0 && rule == TQ_RULE_GRAPH && geo.N % 4 == 0 && q.jpeg_restart == 0;
+        bool ok = want >= 2 && prec == 0 && rule == TQ_RULE_GRAPH && geo.N % 4 == 0;
         std::vector<int> li_of[3];
         for (int kd = 1; ok && kd <= 2; kd++) {
             if (!enc[kd].P) continue;
@@ -649,7 +650,10 @@ void Ctx::setup_exchange() {
                     grp_bc[kd][g] = bc;
                 }
                 if (grp_bc[TQ_Q_KMEANS][g]) kmw_g[g].alloc(grp_bc[TQ_Q_KMEANS][g], q.k, payload_len);
-                if (grp_bc[TQ_Q_DCT][g]) dctw_g[g].alloc(grp_bc[TQ_Q_DCT][g], payload_len);
+                if (grp_bc[TQ_Q_DCT][g]) {
+                    dctw_g[g].alloc(grp_bc[TQ_Q_DCT][g], payload_len);
+                    if (q.jpeg_restart > 0) jenc_g[g].alloc(grp_bc[TQ_Q_DCT][g], payload_len, q.jpeg_restart);
+                }
             }
         }
     }
@@ -820,7 +824,8 @@ int Ctx::stage01_grouped(cudaStream_t s) {
         if (grp_bc[TQ_Q_DCT][g]) {
             Batch &E = enc[TQ_Q_DCT];
             const int b0 = grp_b0[TQ_Q_DCT][g];
-            k += dct_encode(E.vin + b0, grp_bc[TQ_Q_DCT][g], N, N, q.quality, dctw_g[g], E.pay + b0, st, nullptr);
+            k += dct_encode(E.vin + b0, grp_bc[TQ_Q_DCT][g], N, N, q.quality, dctw_g[g], E.pay + b0, st,
+                            q.jpeg_restart > 0 ? &jenc_g[g] : nullptr);
         }
     }
     for (int g = 1; g < ngroups; g++) {
@@ -1160,7 +1165,14 @@ void Ctx::finish() {
     if (iters > 0 && (jenc.P || jdec.P)) {  // entropy-coded DCT payloads: actual sizes, stream checks
         std::vector<long long> eb(std::max(1, jenc.P));
         std::vector<unsigned> sd(2 * std::max(1, jdec.P), 0u);
-        if (jenc.P) TQ_CHECK_CUDA(cudaMemcpy(eb.data(), jenc.enc_bytes, sizeof(long long) * jenc.P, cudaMemcpyDeviceToHost));
+        if (jenc.P && st.node_groups > 1) {  // the last run's coders were the groups' (their subranges)
+            for (int g = 0; g < ngroups; g++)
+                if (jenc_g[g].P)
+                    TQ_CHECK_CUDA(cudaMemcpy(eb.data() + grp_b0[TQ_Q_DCT][g], jenc_g[g].enc_bytes,
+                                             sizeof(long long) * jenc_g[g].P, cudaMemcpyDeviceToHost));
+        } else if (jenc.P) {
+            TQ_CHECK_CUDA(cudaMemcpy(eb.data(), jenc.enc_bytes, sizeof(long long) * jenc.P, cudaMemcpyDeviceToHost));
+        }
         if (jdec.P) TQ_CHECK_CUDA(cudaMemcpy(sd.data(), jdec.status, sizeof(unsigned) * 2 * jdec.P, cudaMemcpyDeviceToHost));
         long long logical = logical_fixed;
         for (int b = 0; b < jenc.P; b++) logical += eb[b] * jmult[b];

@@ -193,6 +193,7 @@ struct Ctx {
     int grp_n0[MAXG] = {}, grp_cnt[MAXG] = {};
     KmeansWork kmw_g[MAXG];
     DctWork dctw_g[MAXG];
+    JpegWork jenc_g[MAXG];            // tq_quant.jpeg_restart > 0: each group's entropy coder
     int grp_b0[3][MAXG] = {}, grp_bc[3][MAXG] = {};  // [codec kind][group]: the group's subrange of enc[kind]
     cudaStream_t sg[MAXG] = {};       // sg[0] unused: group 0 runs on the iteration's stream
     cudaEvent_t ev_fork = nullptr, ev_join[MAXG] = {};

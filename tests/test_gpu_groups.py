@@ -93,6 +93,8 @@ def test_groups_labels_and_kept_ax_refresh(monkeypatch):
     ("C3 DCT q50, 16 nodes torus", C.C3(), 8),
     ("C3 DCT q50, 16 nodes torus, 3 groups", C.C3(), 3),
     ("two C2 slices, K-means / DCT alternating", replace(C.C2(), quant=C.Q_ALT, quality=75, slices=2), 4),
+    ("C3 JPEG entropy-coded DCT, restart 4", replace(C.C3(), jpeg_restart=4), 8),
+    ("C3 JPEG entropy-coded DCT, restart 1, 3 groups", replace(C.C3(), jpeg_restart=1), 3),
 ])
 def test_groups_dct_and_alternating_bitwise(name, cfg, groups, monkeypatch):
     """Plain DCT payloads and slices alternating K-means / DCT (C5's codec mix): each group encodes
@@ -101,6 +103,8 @@ def test_groups_dct_and_alternating_bitwise(name, cfg, groups, monkeypatch):
     one = _run_slices(cfg, inp, 3, 1, monkeypatch)
     many = _run_slices(cfg, inp, 3, groups, monkeypatch)
     assert one[0]["node_groups"] == 1 and many[0]["node_groups"] == groups, name
+    # the coded payload sizes (JPEG: gathered from the groups' coders) are the same bytes
+    assert one[0]["payload_bytes_logical"] == many[0]["payload_bytes_logical"], name
     for a, b in zip(one[1], many[1]):
         np.testing.assert_array_equal(a, b)
 
@@ -116,9 +120,9 @@ def _run_slices(cfg, inp, iters, groups, monkeypatch):
 
 
 def test_groups_not_used_where_not_applicable(monkeypatch):
-    """JPEG entropy-coded DCT payloads, fp64 and GD keep the single chain (tq_stats says so)."""
+    """fp64 and GD keep the single chain (tq_stats says so)."""
     monkeypatch.setenv("TQ_GROUPS", "2")
-    for cfg, prec in ((replace(C.C3(), jpeg_restart=4), 0), (C.C2(), 1), (replace(C.C2(), inner=C.INNER_GD, e1=10), 0)):
+    for cfg, prec in ((C.C2(), 1), (replace(C.C2(), inner=C.INNER_GD, e1=10), 0)):
         inp = C.make_inputs(cfg, with_truth=False)
         ctx = gpu_context(cfg, inp, precision=prec)
         ctx.run(1)
