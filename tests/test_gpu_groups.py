@@ -76,6 +76,18 @@ def test_one_group_per_node_bitwise_c4(groups, monkeypatch):
     _same(one, many)
 
 
+def test_groups_residual_projection_every_solve(monkeypatch):
+    """TQ_AX_MAXAGE=0: each group's solve starts from the forward-projected residual d - A x
+    (the group's rows of the band reduction with the data term) instead of the kept A x."""
+    monkeypatch.setenv("TQ_AX_MAXAGE", "0")
+    cfg = C.C2()
+    inp = C.make_inputs(cfg, with_truth=False)
+    one = _run(cfg, inp, 4, 1, monkeypatch)
+    many = _run(cfg, inp, 4, 4, monkeypatch)
+    assert many[0]["node_groups"] == 4
+    _same(one, many)
+
+
 def test_groups_labels_and_kept_ax_refresh(monkeypatch):
     """K-means labels, and enough iterations to pass the kept A x refresh (TQ_AX_MAXAGE)."""
     monkeypatch.setenv("TQ_AX_MAXAGE", "3")
