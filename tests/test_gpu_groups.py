@@ -35,6 +35,7 @@ def _same(a, b):
     ("C2 K-means 16, 8 nodes", C.C2(), 4),
     ("C2 on 7 nodes (groups 3 + 4)", replace(C.C2(), nodes=7, graph="ring"), 4),
     ("C4_G1 bench workload", C.C4(1), 3),
+    ("C2 with the Siddon projector (R-26)", replace(C.C2(), projector=1), 4),
 ])
 def test_groups_bitwise_equal_to_one_chain(name, cfg, iters, monkeypatch):
     inp = C.make_inputs(cfg, with_truth=False)
