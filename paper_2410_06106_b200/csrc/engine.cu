@@ -615,8 +615,8 @@ void Ctx::setup_exchange() {
         }
     }
     // ---- node groups (TQ_GROUPS; 1 = one launch sequence over all nodes): the graph rule's fp32
-    // path; each encode batch (K-means, plain DCT) must hold local payloads in local-node order,
-    // so a group's payloads are one contiguous subrange of each batch
+    // path; each encode batch (K-means, DCT with or without JPEG coding) must hold local payloads
+    // in local-node order, so a group's payloads are one contiguous subrange of each batch
     {
         const char *env = getenv("TQ_GROUPS");
         // default: one group per node (up to MAXG) for images of 512^2 and more; below that the
